@@ -1,0 +1,78 @@
+"""Pins of the oracle's seeded input generator (readings R-14, R-15, R-16)."""
+import math
+import os
+
+import numpy as np
+import pytest
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def test_splitmix64_published_values(ora):
+    with open(os.path.join(GOLDEN, "splitmix64.txt")) as f:
+        for line in f:
+            if line.startswith("#") or not line.strip():
+                continue
+            z, want = (int(t, 16) for t in line.split())
+            assert ora.sm64(z) == want
+
+
+def test_uniform_and_gauss_statistics(ora):
+    u = np.array([ora.uniform(9, 4, k) for k in range(20000)])
+    assert u.min() >= 0.0 and u.max() < 1.0
+    assert abs(u.mean() - 0.5) < 0.01 and abs(u.var() - 1 / 12) < 0.003
+    z = np.array([ora.gauss(9, 5, k) for k in range(20000)])
+    assert abs(z.mean()) < 0.03 and abs(z.std() - 1) < 0.03
+    # streams differ, draws are reproducible
+    assert ora.uniform(9, 4, 3) == ora.uniform(9, 4, 3)
+    assert ora.uniform(9, 4, 3) != ora.uniform(9, 5, 3)
+
+
+def test_film_recipe(ora):
+    """cfg1 (BASELINE configs[0]): phi = [y<16] + U(+-0.01); c = 0.5 + U(+-0.05); rho = rho_in above."""
+    pr = ora.preset(1)
+    c, phi, rho = ora.initial_fields(pr["ic"], 64, 64, 0)
+    solid = (np.arange(64)[:, None] < 16) * np.ones((1, 64))
+    assert np.max(np.abs(phi - solid)) <= 0.01
+    assert np.max(np.abs(c - 0.5)) <= 0.05
+    assert np.array_equal(rho, 1.0 - solid)
+    assert abs((c - 0.5).mean()) < 2e-3
+
+
+def test_rough_recipe(ora):
+    """cfg2 (configs[1]): substrate height 32, roughness amplitude 2, wavelength 32; c ~ N(0.5, 0.05^2)."""
+    pr = ora.preset(2)
+    c, phi, rho = ora.initial_fields(pr["ic"], 256, 256, 0)
+    i = np.arange(256)[None, :]; j = np.arange(256)[:, None]
+    H = 32 + 2 * np.sin(2 * np.pi * i / 32)
+    want = 0.5 * (1 - np.tanh((j - H) / math.sqrt(2.0)))
+    np.testing.assert_allclose(phi, want, atol=1e-15)
+    np.testing.assert_allclose(rho, 1 - phi, atol=1e-15)
+    assert abs(c.mean() - 0.5) < 1e-3 and abs(c.std() - 0.05) < 1e-3
+
+
+def test_columns_recipe(ora):
+    """cfg5 (configs[4]): 64 columns of random width, c alternating 0.2 / 0.8, tanh film at ny/2."""
+    ic = ora.preset(5)["ic"]
+    nx, ny = 1024, 16
+    ic.height = ny / 2
+    c, phi, rho = ora.initial_fields(ic, nx, ny, 0)
+    row = c[0]
+    assert np.all(c == row[None, :])
+    runs = 1 + np.count_nonzero(np.diff(row))
+    assert runs == 64
+    assert row[0] == 0.2 and set(np.unique(row)) == {0.2, 0.8}
+    starts = np.flatnonzero(np.diff(row)) + 1
+    assert np.all(np.diff(row[np.r_[0, starts]]) != 0)
+
+
+def test_member_rates(ora):
+    """cfg3 (configs[2]): per-member rates uniform in [0.5, 2] x nominal v0 = 0.5; theta = 90 deg."""
+    ic = ora.preset(3)["ic"]
+    v = np.array([ora.member_velocity(ic, m) for m in range(64)])
+    assert np.all(np.abs(v[:, 0]) < 1e-15)
+    sp = -v[:, 1]
+    assert sp.min() >= 0.25 and sp.max() <= 1.0 and sp.std() > 0.1
+    assert len(set(sp)) == 64
+    ic1 = ora.preset(1)["ic"]
+    assert ora.member_velocity(ic1, 0)[1] == -0.5
