@@ -1,0 +1,313 @@
+"""Benchmark of the B200-native PVD phase-field midpoint step (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 3|4|1|2|5] [--impl ours|reference]
+
+Default workload (N=1 and per rank under torchrun): BASELINE.json configs[2], the ensemble of 64
+independent 512 x 512 fp64 members, weak-scaled (64 members per GPU, member ids keyed by rank, no
+collective on the step path; R-20).  A "step" is one explicit-midpoint time step of every member:
+stage-1 and stage-2 fused kernels, plus the diagnostics / blow-up check every check_every = 100
+steps and at the end of the timed call (rows a1-a6 of SURVEY 8(a)).  --config 4 runs the y-slab
+decomposition of configs[3] (4096 x 4096*N, NCCL halo exchange per stage).
+
+Rank 0 prints one JSON line.  The oracle (oracle/, test infrastructure) is only executed in the
+cpu_baseline leg and under --impl reference.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "cell-updates/sec and achieved HBM GB/s (fraction of B200 peak) at 1/2/4/8 GPUs"
+UNIT = "cell-updates/s"
+# Algorithmic HBM bytes per cell and launch of the stage kernel: stage 1 reads
+# u^n (3 fields) and writes u* (3 fields); stage 2 reads u* and u^n (6) and writes u^{n+1} (3).
+VALUES_STAGE1, VALUES_STAGE2 = 6, 9
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def _traffic(config_key):
+    """Per-launch dram bytes of the stage kernel from the committed ncu --set full capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            d = json.load(f)
+        return d.get(config_key)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """Samples SM clocks and throttle reasons via NVML during the timed region."""
+
+    def __init__(self, device_index):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self._nv = None
+
+    def _run(self):
+        nv = self._nv
+        names = {
+            getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8): "hw_slowdown",
+            getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40): "hw_thermal_slowdown",
+            getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20): "sw_thermal_slowdown",
+            getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4): "sw_power_cap",
+            getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80): "hw_power_brake",
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                for bit, name in names.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.02)
+
+    def __enter__(self):
+        if self._nv:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+def _cpu_baseline(seconds=12.0):
+    """The oracle as it stands, single thread, on a bounded sample of configs[2]: member 0
+    (512 x 512 fp64), as many explicit-midpoint steps as fit in ~`seconds`."""
+    from oracle import oracle as ora
+    pr = ora.preset(3)
+    m = ora.member_model(pr, 0)
+    u = ora.initial_fields(pr["ic"], 512, 512, 0)
+    steps, t0 = 0, time.perf_counter()
+    while time.perf_counter() - t0 < seconds:
+        u = ora.step(m, *u, 5)
+        steps += 5
+    el = time.perf_counter() - t0
+    return {"value": 512 * 512 * steps / el, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"configs[2] member 0 (512x512 fp64), {steps} midpoint steps, single thread, {el:.1f} s"}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def run_reference(args):
+    """--impl reference: the oracle (the reference arm of this tier) on the host cores."""
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return 0
+    from oracle import oracle as ora
+    pr = ora.preset(3)
+    m = ora.member_model(pr, 0)
+    u = ora.initial_fields(pr["ic"], 512, 512, 0)
+    for _ in range(args.warmup):
+        u = ora.step(m, *u, 1)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        u = ora.step(m, *u, 1)
+    el = time.perf_counter() - t0
+    v = 512 * 512 * args.steps / el
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": "configs[2] (64 x 512^2 fp64 ensemble); oracle sample: member 0 per step"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": f"configs[2] member 0, 512x512 fp64, {args.steps} steps, single thread"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    from paper_2312_05410_b200 import pf
+
+    ws, rank, local = _dist()
+    if args.gpus != ws and ws > 1:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={ws}")
+    torch.cuda.set_device(local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    cfg = args.config
+    p = pf.pf_default_params(cfg).replace(device=local)
+    if cfg == 3:
+        p = p.replace(member_offset=rank * p.n_members)        # weak: 64 members per GPU
+        mode = "single"
+        workload = f"configs[2]: {p.n_members} x {p.nx}x{p.ny} fp64 ensemble per GPU (weak, {p.n_members * ws} members total)"
+    elif cfg == 4 or cfg == 5:
+        p = p.replace(ny=p.ny * ws) if cfg == 4 else p          # cfg4 weak: 4096 x 4096 per GPU
+        if ws > 1:
+            uid = pf.pf_nccl_unique_id() if rank == 0 else bytes(128)
+            t = torch.tensor(list(uid), dtype=torch.uint8, device="cuda")
+            dist.broadcast(t, 0)
+            mode = ("slab", rank, ws, bytes(t.cpu().tolist()))
+        else:
+            mode = "single"
+        workload = (f"configs[{cfg - 1}]: {p.nx}x{p.ny} {'fp64' if p.precision == 0 else 'fp32'}"
+                    f" y-slab decomposed over {ws} GPU(s)")
+    else:
+        mode = "single"
+        workload = f"configs[{cfg - 1}]: {p.n_members} x {p.nx}x{p.ny}"
+    sim = pf.Simulation(p, mode)
+    ctx = sim.ctx
+    stream = torch.cuda.ExternalStream(pf.pf_stream(ctx), device=torch.device("cuda", local))
+    cells_local = p.n_members * sim.ny_local * p.nx
+    esz = 8 if p.precision == pf.PF_F64 else 4
+
+    # warm-up (untimed)
+    sim.step(args.warmup)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- timed region: K steps through pf_step, stage kernels bracketed by CUDA events ----
+    l0 = pf.pf_launch_count(ctx)
+    pf.pf_profile(ctx, True)
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        sim.step(args.steps)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ms = ev0.elapsed_time(ev1)
+    prof = pf.pf_profile_read(ctx)
+    pf.pf_profile(ctx, False)
+    launches = pf.pf_launch_count(ctx) - l0
+    ms_max = ms
+    if dist is not None:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_max = float(t.item())
+    value = cells_local * ws * args.steps / (ms_max * 1e-3)
+
+    # roofline of the dominant kernel (stage_kernel), algorithmic bytes per launch
+    n1, n2 = prof[1], prof[3]
+    stage_ms = prof[0] + prof[2]
+    nslab_launch = max(1.0, (n1 + n2))
+    alg_bytes = cells_local * esz * (VALUES_STAGE1 * n1 + VALUES_STAGE2 * n2)
+    achieved = alg_bytes / (stage_ms * 1e-3) / 1e9 if stage_ms > 0 else None
+    peak, peak_src = _peaks()
+    key = f"cfg{cfg}_n{ws}"
+    tr = _traffic(key)
+
+    # ---- e2e: the public API with HOST buffers (pinned), copies inside the timed region ----
+    hc = torch.empty((p.n_members, sim.ny_local, p.nx), dtype=torch.float64, pin_memory=True)
+    hp = torch.empty_like(hc).pin_memory()
+    hr = torch.empty_like(hc).pin_memory()
+    pf.pf_get_fields(ctx, -1, hc, hp, hr)
+    e2e_steps = args.steps
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    pf.pf_set_fields(ctx, -1, hc, hp, hr)
+    sim.step(e2e_steps)
+    pf.pf_get_fields(ctx, -1, hc, hp, hr)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ms_e2e = e0.elapsed_time(e1)
+    if dist is not None:
+        t = torch.tensor([ms_e2e], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_e2e = float(t.item())
+    host_bytes = 3 * cells_local * 8
+    e2e = {"value": cells_local * ws * e2e_steps / (ms_e2e * 1e-3), "unit": UNIT,
+           "h2d_bytes_per_step": host_bytes / e2e_steps, "d2h_bytes_per_step": host_bytes / e2e_steps,
+           "note": f"pf_set_fields(all members, pinned fp64) + pf_step({e2e_steps}) + pf_get_fields(all), "
+                   "copies amortised over the steps of one call"}
+
+    line = None
+    if rank == 0:
+        alg_per_cell_step = esz * (VALUES_STAGE1 + VALUES_STAGE2)
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64" if p.precision == pf.PF_F64 else "f32",
+            "data": "synthetic (seeded BASELINE.json configs recipe, DESIGN.md 5)",
+            "config": {"workload": workload, "nx": p.nx, "ny": p.ny, "members_per_gpu": p.n_members,
+                       "check_every": p.check_every,
+                       "l2": f"inputs larger than L2: state {2 * cells_local * 3 * esz / 2**20:.0f} MiB per GPU"},
+            "hbm_gbs_effective": value * alg_per_cell_step / ws / 1e9,
+            "hbm_frac_effective": value * alg_per_cell_step / ws / 1e9 / peak,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": (achieved / peak) if achieved else None, "traffic": tr,
+                         "kernel": "stage_kernel (both midpoint stages)",
+                         "algorithmic_bytes_per_launch": alg_bytes / nslab_launch,
+                         "avg_launch_ms": stage_ms / nslab_launch, "peak_source": peak_src},
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        if not args.no_cpu_baseline:
+            line["cpu_baseline"] = _cpu_baseline()
+        print(json.dumps(line), flush=True)
+    sim.close()
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--config", type=int, default=3, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        raise SystemExit("--warmup must be >= 3")
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

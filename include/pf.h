@@ -1,0 +1,194 @@
+/*
+ * pf.h -- C ABI of libpf, the B200-native PVD phase-field DNS time step.
+ *
+ * The library advances the coupled (c, phi, rho) phase-field model of physical vapour
+ * deposition of arXiv 2312.05410 (section 4.1) with second-order
+ * central differences and the explicit midpoint method (section 4.2 "Dataset":
+ * "second-order-central-difference stencils for all spatial derivatives and an explicit
+ * midpoint method for time integration").  The discrete model, readings R-1..R-20 and the
+ * data layout are in DESIGN.md sections 2, 3 and 6.
+ *
+ * Conventions (all calls):
+ *  - Every call returns a pf_status; no C++ exception crosses this ABI.  On failure
+ *    pf_last_error(ctx) (or pf_last_error(NULL) for pf_create*) holds a message valid
+ *    until the next call on that ctx / thread.
+ *  - Host buffers are owned by the caller, row-major, index (m*ny_local + j)*nx + i,
+ *    j = 0 the bottom (substrate) row, unpadded, local rows only in slab mode.
+ *    NULL means "skip this field".  Pinned host memory is used as is (faster copies).
+ *  - The ctx owns all device memory, streams, CUDA graphs and the NCCL communicator
+ *    and releases them in pf_free.  Calls on one ctx must be serialised (SPEC S:270
+ *    "one writer"); distinct ctxs are independent.
+ *  - Torch (or any other caller) only supplies the process group used to broadcast the
+ *    NCCL unique id; no compute happens outside this library.
+ */
+#ifndef PF_H
+#define PF_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PF_ABI_VERSION 1u
+
+typedef struct pf_ctx pf_ctx; /* opaque */
+
+typedef enum {
+    PF_OK = 0,
+    PF_ERR_ARG = 1,          /* invalid argument / parameter                         */
+    PF_ERR_UNSTABLE_DT = 2,  /* dt violates the stability bound R-18 */
+    PF_ERR_NOMEM = 3,        /* device or host allocation failed                     */
+    PF_ERR_CUDA = 4,         /* CUDA runtime error (message names it)                */
+    PF_ERR_NCCL = 5,         /* NCCL error (slab mode)                               */
+    PF_ERR_BLOWUP = 6,       /* non-finite value detected ("blow-up")     */
+    PF_ERR_STATE = 7,        /* call not allowed in the current state                */
+    PF_ERR_ABI = 8           /* pf_params.abi_version != PF_ABI_VERSION              */
+} pf_status;
+
+typedef enum { PF_F64 = 0, PF_F32 = 1 } pf_precision;
+
+/* Initial-condition recipes (reading R-14 of BASELINE.json configs[0..4]). */
+typedef enum {
+    PF_IC_FILM = 0,            /* phi = [j < ic_height] + U(+-noise_phi); c = ic_c0 + noise  */
+    PF_IC_ROUGH_SUBSTRATE = 1, /* phi = 1/2(1 - tanh((j - H_i)/delta)), H_i = H + amp sin(2 pi i/lambda) */
+    PF_IC_COLUMNS = 2,         /* tanh film at ic_height; ic_ncols columns, c = ic_c_lo / ic_c_hi */
+    PF_IC_NONE = 3             /* all fields zero; caller uses pf_set_fields             */
+} pf_ic;
+
+/* Every physical / numerical parameter of the model (SPEC S:158-161 SolverConfig, the symbols
+ * of P:302-343).  Readings: R-2..R-4 free energy, R-6 mobility, R-7 M_phi, R-9 vapour,
+ * R-10 velocity, R-13 values, R-15 per-member rates. */
+typedef struct {
+    uint32_t abi_version;            /* must be PF_ABI_VERSION                               */
+    int32_t nx, ny;                  /* GLOBAL grid; x periodic, y no-flux; nx, ny >= 8 */
+    int32_t n_members;               /* members held by this ctx (ensemble, grid.z)          */
+    int32_t member_offset;           /* global id of local member 0: keys seeds and rates    */
+    int32_t precision;               /* pf_precision: storage and arithmetic type            */
+    double dx, dt;                   /* grid spacing, time step                              */
+    double kappa_c, kappa_phi;       /* gradient-energy coefficients (R-2)                   */
+    double W_c, W_phi;               /* well heights (R-2)                                   */
+    double M_A_bulk, M_B_bulk, M_A_surf, M_B_surf, sigma_surf; /* P:312-324 (R-6)            */
+    double M_phi;                    /* interface mobility (R-7)                             */
+    double D_rho, rho_in;            /* vapour diffusivity and top reservoir density (R-9, R-12) */
+    double v0, theta_deg;            /* deposition speed and angle: v = v0_m (cos, -sin) (R-10) */
+    double rate_lo, rate_hi;         /* v0_m = v0 (lo + (hi-lo) U(seed, 8m+3, 0)) (R-15)     */
+    int32_t ic;                      /* pf_ic                                                */
+    int32_t ic_ncols;                /* PF_IC_COLUMNS: number of columns                    */
+    double ic_height, ic_amp, ic_wavelength;
+    double ic_c0, ic_c_lo, ic_c_hi;
+    double noise_c, noise_phi;       /* noise amplitudes (uniform +-a, or Gaussian std for c) */
+    int32_t noise_c_gaussian;        /* 1: c = c0 + noise_c N(0,1) (Box-Muller, R-16)        */
+    int32_t check_every;             /* blow-up / diagnostics check period in steps (>= 1)   */
+    uint64_t seed;                   /* counter-RNG seed (R-16)                              */
+    int32_t device;                  /* CUDA device ordinal                                  */
+    int32_t graph_steps;             /* steps per captured CUDA graph (0 = no graphs)        */
+} pf_params;
+
+/* Fill *out with the preset of BASELINE.json configs[cfg-1] (cfg = 1..5; R-13, R-14).
+ * Errors: PF_ERR_ARG for an unknown cfg or out == NULL. */
+pf_status pf_default_params(int32_t cfg, pf_params *out);
+
+/* sizeof(pf_params) as compiled into the library (lets bindings verify their struct mirror). */
+uint32_t pf_params_size(void);
+
+/* Host-only: the seeded initial fields of GLOBAL member `member` (row a0 of SURVEY 8(a);
+ * recipes R-14, RNG R-16) for global rows [y0, y0+rows), written row-major (row, x) as fp64
+ * into caller-owned buffers of rows*nx doubles.  This is exactly what pf_create uploads
+ * (before rounding to fp32 for PF_F32).  Needs no GPU.  Errors: PF_ERR_ARG. */
+pf_status pf_initial_fields(const pf_params *p, int64_t member, int32_t y0, int32_t rows,
+                            double *c, double *phi, double *rho);
+
+/* Host-only: velocity (v_x, v_y) = v0_m (cos theta, -sin theta) of GLOBAL member `member`
+ * (R-10, R-15) and the stability limit of R-18 for p.  Need no GPU.  Errors: PF_ERR_ARG. */
+pf_status pf_member_velocity(const pf_params *p, int64_t member, double *v_x, double *v_y);
+pf_status pf_dt_limit(const pf_params *p, double *dt_max);
+
+/* Create a single-GPU context holding p->n_members independent members of the full
+ * nx x ny grid, generate their seeded initial conditions on the host (a0, R-14..R-16) and
+ * upload them.  Validates p (nx, ny >= 8, dx, dt > 0, ...) and the stability bound R-18.
+ * Errors: PF_ERR_ABI, PF_ERR_ARG, PF_ERR_UNSTABLE_DT, PF_ERR_NOMEM, PF_ERR_CUDA.
+ * On error *out is NULL and pf_last_error(NULL) explains. */
+pf_status pf_create(const pf_params *p, pf_ctx **out);
+
+/* 128-byte NCCL unique id for pf_create_slab (call on rank 0, broadcast the bytes).
+ * Errors: PF_ERR_NCCL. */
+pf_status pf_nccl_unique_id(uint8_t out[128]);
+
+/* Create rank `rank` of an nranks-way y-slab decomposition of the global grid:
+ * rank r owns global rows [r ny/nranks, (r+1) ny/nranks) (ny % nranks == 0, ny/nranks >= 2);
+ * the 2-row halo of c, phi, rho is exchanged with ranks r-1 / r+1 after every midpoint stage
+ * over NCCL (P:348 stages; BASELINE configs[3] "2-cell halo exchanged per stage").
+ * `uid` comes from pf_nccl_unique_id on rank 0.  Errors: as pf_create plus PF_ERR_NCCL. */
+pf_status pf_create_slab(const pf_params *p, int32_t rank, int32_t nranks,
+                         const uint8_t uid[128], pf_ctx **out);
+
+/* Single-process multi-slab context ("loopback"): nslabs y-slabs of every member on ONE
+ * device, with the halo exchange done by device-to-device copies.  Same arithmetic and
+ * exchange schedule as pf_create_slab, used to test the decomposition without NCCL.
+ * Host buffers for get/set still cover the FULL grid.  Errors: as pf_create. */
+pf_status pf_create_loopback(const pf_params *p, int32_t nslabs, pf_ctx **out);
+
+/* Advance every member by n >= 0 explicit midpoint steps: per step, stage 1
+ * u* = u^n + dt/2 R(u^n) and stage 2 u^{n+1} = u^n + dt R(u*), each one fused kernel pass.
+ * Every check_every steps and at the end, the non-finite count is checked:
+ * PF_ERR_BLOWUP names the field and step window; the state is left as computed and
+ * further pf_step calls fail with PF_ERR_STATE until pf_set_fields.  Synchronous.
+ * Errors: PF_ERR_ARG (n < 0), PF_ERR_STATE, PF_ERR_BLOWUP, PF_ERR_CUDA, PF_ERR_NCCL. */
+pf_status pf_step(pf_ctx *ctx, int64_t n);
+
+/* Copy member `member` (0..n_members-1, or -1 = all members, stacked) to host buffers of
+ * ny_local*nx doubles each (times n_members for -1).  fp32 fields are widened to double.
+ * Errors: PF_ERR_ARG, PF_ERR_CUDA. */
+pf_status pf_get_fields(pf_ctx *ctx, int32_t member, double *c, double *phi, double *rho);
+
+/* Inverse of pf_get_fields: overwrite the member's state from host buffers (fp32 fields are
+ * rounded to nearest).  Clears a blow-up state.  Fields passed as NULL are left unchanged.
+ * In slab mode the halo rows are refreshed by an exchange before returning (collective:
+ * every rank must call it).  Errors: PF_ERR_ARG, PF_ERR_CUDA, PF_ERR_NCCL. */
+pf_status pf_set_fields(pf_ctx *ctx, int32_t member, const double *c, const double *phi,
+                        const double *rho);
+
+/* Diagnostics of member `member` (north_star "Reductions"), accumulated in fp64 in a fixed
+ * order (deterministic for a fixed launch shape and nranks):
+ *   out[0] = dx^2 sum c (mass of c), out[1] = dx^2 sum phi, out[2] = dx^2 sum rho,
+ *   out[3] = E_h, out[4] = number of cells with a non-finite field.
+ * Slab mode: global values (per-rank partials all-gathered and summed in rank order;
+ * collective).  Errors: PF_ERR_ARG, PF_ERR_CUDA, PF_ERR_NCCL. */
+pf_status pf_diagnostics(pf_ctx *ctx, int32_t member, double out[5]);
+
+/* Steps taken, simulated time, first global row and number of rows held by this ctx.
+ * Any pointer may be NULL.  Errors: PF_ERR_ARG. */
+pf_status pf_info(pf_ctx *ctx, int64_t *steps, double *t, int32_t *y0, int32_t *ny_local);
+
+/* Override the step counter and time (used when resuming from saved fields).
+ * Errors: PF_ERR_ARG. */
+pf_status pf_set_time(pf_ctx *ctx, int64_t steps, double t);
+
+/* Kernel launches issued by this ctx since creation (stage + diagnostics + exchange kernels);
+ * used by the benchmark to report its launch count.  Errors: PF_ERR_ARG. */
+pf_status pf_launch_count(pf_ctx *ctx, int64_t *launches);
+
+/* Stage-kernel profiling (bench.py's roofline): while enabled (enable != 0), every stage
+ * launch of pf_step is bracketed by CUDA events on the ctx's stream and CUDA graphs are not
+ * used; enabling resets the record.  pf_profile_read returns out[0] = total ms of stage-1
+ * launches, out[1] = their count, out[2] = total ms of stage-2 launches, out[3] = count,
+ * out[4] = total ms of diagnostics launches (pairs), out[5] = their count.
+ * Errors: PF_ERR_ARG, PF_ERR_CUDA. */
+pf_status pf_profile(pf_ctx *ctx, int32_t enable);
+pf_status pf_profile_read(pf_ctx *ctx, double out[6]);
+
+/* The cudaStream_t (as void*) every kernel and copy of this ctx is issued on, so a caller can
+ * time the ctx's work with CUDA events recorded on the same stream.  Errors: PF_ERR_ARG. */
+pf_status pf_stream(pf_ctx *ctx, void **stream);
+
+/* Last error message of ctx (ctx == NULL: the calling thread's last create error). */
+const char *pf_last_error(const pf_ctx *ctx);
+
+/* Release everything the ctx owns.  NULL-safe.  Slab mode: collective (NCCL teardown). */
+void pf_free(pf_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PF_H */

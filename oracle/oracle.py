@@ -175,6 +175,7 @@ def lib():
             "orc_uniform": (dbl, [u64, u64, u64]), "orc_gauss": (dbl, [u64, u64, u64]),
             "orc_member_velocity": (None, [pI, i64, C.POINTER(dbl), C.POINTER(dbl)]),
             "orc_initial_fields": (C.c_int, [pI, C.c_int, C.c_int, i64, _D, _D, _D]),
+            "orc_initial_fields_rows": (C.c_int, [pI, C.c_int, i64, C.c_int, C.c_int, _D, _D, _D]),
             "orc_dt_max": (dbl, [pM, dbl]),
         }
         for name, (res, args) in sig.items():
@@ -286,6 +287,15 @@ def member_velocity(ic: IC, member: int):
 def initial_fields(ic: IC, nx: int, ny: int, member: int = 0):
     c = np.empty((ny, nx)); phi = np.empty((ny, nx)); rho = np.empty((ny, nx))
     rc = lib().orc_initial_fields(C.byref(ic._c()), nx, ny, int(member), c, phi, rho)
+    if rc != 0:
+        raise ValueError("bad IC recipe")
+    return c, phi, rho
+
+
+def initial_fields_rows(ic: IC, nx: int, member: int, y0: int, rows: int):
+    """Global rows [y0, y0+rows) of the member's initial fields (same values as the full grid)."""
+    c = np.empty((rows, nx)); phi = np.empty((rows, nx)); rho = np.empty((rows, nx))
+    rc = lib().orc_initial_fields_rows(C.byref(ic._c()), nx, int(member), int(y0), int(rows), c, phi, rho)
     if rc != 0:
         raise ValueError("bad IC recipe")
     return c, phi, rho

@@ -423,9 +423,10 @@ static int cmp_i64(const void *a, const void *b)
     return (x > y) - (x < y);
 }
 
-/* Fill the global fields of member m (row-major j*nx+i, j = 0 bottom). */
-int orc_initial_fields(const orc_ic *ic, int nx, int ny, int64_t member,
-                       double *c, double *phi, double *rho)
+/* Fill global rows [y0, y0+rows) of member m (row-major (j-y0)*nx+i, j = 0 bottom);
+ * every value depends only on (i, j, nx, member), not on the window. */
+int orc_initial_fields_rows(const orc_ic *ic, int nx, int64_t member, int y0, int rows,
+                            double *c, double *phi, double *rho)
 {
     uint64_t sc = (uint64_t)member * 8u + 0u, sp = (uint64_t)member * 8u + 1u;
     uint64_t scut = (uint64_t)member * 8u + 2u;
@@ -446,19 +447,20 @@ int orc_initial_fields(const orc_ic *ic, int nx, int ny, int64_t member,
         }
         qsort(cuts, (size_t)ncut, sizeof(int64_t), cmp_i64);
     }
-    for (int j = 0; j < ny; ++j)
+    for (int j = y0; j < y0 + rows; ++j)
         for (int i = 0; i < nx; ++i) {
-            size_t k = (size_t)j * nx + i;
+            size_t k = (size_t)j * nx + i;         /* global counter index      */
+            size_t o = (size_t)(j - y0) * nx + i;  /* position in the window    */
             double p, cc;
             if (ic->kind == 0) {
                 double solid = (double)j < ic->height ? 1.0 : 0.0;
                 double u = orc_uniform(ic->seed, sp, k);
                 p = solid + ic->noise_phi * (2.0 * u - 1.0);
-                rho[k] = ic->rho_in * (1.0 - solid);
+                rho[o] = ic->rho_in * (1.0 - solid);
             } else {
                 double Hi = ic->height + ic->amp * sin(2.0 * M_PI * (double)i / ic->wavelength);
                 p = 0.5 * (1.0 - tanh(((double)j - Hi) / delta));
-                rho[k] = ic->rho_in * (1.0 - p);
+                rho[o] = ic->rho_in * (1.0 - p);
             }
             if (ic->kind == 2) {
                 int q = 0;
@@ -470,11 +472,18 @@ int orc_initial_fields(const orc_ic *ic, int nx, int ny, int64_t member,
                 double u = orc_uniform(ic->seed, sc, k);
                 cc = ic->c0 + ic->noise_c * (2.0 * u - 1.0);
             }
-            phi[k] = p;
-            c[k] = cc;
+            phi[o] = p;
+            c[o] = cc;
         }
     free(cuts);
     return 0;
+}
+
+/* Whole grid of member m. */
+int orc_initial_fields(const orc_ic *ic, int nx, int ny, int64_t member,
+                       double *c, double *phi, double *rho)
+{
+    return orc_initial_fields_rows(ic, nx, member, 0, ny, c, phi, rho);
 }
 
 /* Largest stable dt per R-18 (80% of the explicit-midpoint limit of the

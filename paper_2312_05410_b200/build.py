@@ -1,0 +1,94 @@
+"""Build libpf.so in-tree: nvcc for the sm_100a kernels, g++ for the host runtime.
+
+    python -m paper_2312_05410_b200.build [--force] [--verbose]
+
+The shared library lands next to this file (paper_2312_05410_b200/libpf.so) so that it travels
+with the repository snapshot to the GPU box.
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+import sysconfig
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
+BUILD = os.path.join(HERE, "_build")
+LIB = os.path.join(HERE, "libpf.so")
+CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def _nccl_dirs():
+    cands = []
+    try:
+        import nvidia.nccl  # type: ignore
+        base = list(nvidia.nccl.__path__)[0]
+        cands.append((os.path.join(base, "include"), os.path.join(base, "lib")))
+    except Exception:
+        pass
+    sp = sysconfig.get_paths().get("purelib", "")
+    cands.append((os.path.join(sp, "nvidia", "nccl", "include"), os.path.join(sp, "nvidia", "nccl", "lib")))
+    cands.append(("/usr/include", "/usr/lib/x86_64-linux-gnu"))
+    for inc, lib in cands:
+        if os.path.exists(os.path.join(inc, "nccl.h")) and (
+                os.path.exists(os.path.join(lib, "libnccl.so.2")) or os.path.exists(os.path.join(lib, "libnccl.so"))):
+            return inc, lib
+    raise RuntimeError("nccl.h / libnccl.so.2 not found")
+
+
+def _run(cmd, verbose):
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if verbose or r.returncode:
+        sys.stdout.write(r.stdout)
+        sys.stderr.write(r.stderr)
+    if r.returncode:
+        raise RuntimeError(f"build failed: {' '.join(cmd)}")
+    return r
+
+
+def sources():
+    return sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC)
+                  if f.endswith((".cu", ".cpp", ".h", ".cuh"))) + [os.path.join(ROOT, "include", "pf.h")]
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    srcs = sources()
+    if not force and os.path.exists(LIB):
+        t = os.path.getmtime(LIB)
+        if all(os.path.getmtime(s) <= t for s in srcs):
+            return LIB
+    os.makedirs(BUILD, exist_ok=True)
+    inc_nccl, lib_nccl = _nccl_dirs()
+    incs = ["-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", os.path.join(CUDA, "include"),
+            "-I", inc_nccl]
+    objs = []
+    for f in sorted(os.listdir(CSRC)):
+        src = os.path.join(CSRC, f)
+        if f.endswith(".cu"):
+            obj = os.path.join(BUILD, f[:-3] + ".o")
+            _run([os.path.join(CUDA, "bin", "nvcc"), *ARCH, "-O3", "-lineinfo", "-std=c++17",
+                  "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr",
+                  *incs, "-c", src, "-o", obj], verbose)
+            objs.append(obj)
+        elif f.endswith(".cpp"):
+            obj = os.path.join(BUILD, f[:-4] + ".o")
+            # -ffp-contract=off: the initial fields must be bitwise reproducible (R-16)
+            _run(["g++", "-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-fno-fast-math",
+                  "-Wall", *incs, "-c", src, "-o", obj], verbose)
+            objs.append(obj)
+    nccl_so = "libnccl.so.2" if os.path.exists(os.path.join(lib_nccl, "libnccl.so.2")) else "libnccl.so"
+    tmp = LIB + ".tmp"
+    _run([os.path.join(CUDA, "bin", "nvcc"), *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs,
+          "-L", lib_nccl, f"-l:{nccl_so}", "-Xlinker", f"-rpath,{lib_nccl}"], verbose)
+    os.replace(tmp, LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose="--verbose" in sys.argv)
+    print(LIB)

@@ -1,0 +1,919 @@
+// pf_host.cpp -- host runtime of libpf: the C ABI of include/pf.h.
+//
+// Responsibilities:
+//   * parameter presets and validation, including the stability bound (R-18);
+//   * seeded initial conditions on the host (row a0; readings R-14..R-16), this library's own
+//     implementation of the counter-based generator (the oracle has a separate one);
+//   * device buffers in the padded layout of DESIGN.md 6, the stepping loop (two fused stage
+//     kernels per explicit-midpoint step), CUDA-graph replay for launch-bound grids;
+//   * halo exchange between y-slabs: NCCL p2p between ranks, or device copies in loopback mode;
+//   * diagnostics / blow-up checks, get / set of fields, error reporting.
+// Compiled with -ffp-contract=off so the initial fields are bitwise reproducible (R-16).
+#include "pf.h"
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "pf_internal.h"
+
+#ifndef M_PI
+#define M_PI 3.14159265358979323846
+#endif
+
+namespace {
+
+thread_local std::string g_create_error;
+
+std::string fmt(const char *f, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, f);
+    vsnprintf(buf, sizeof buf, f, ap);
+    va_end(ap);
+    return buf;
+}
+
+// ---------------------------------------------------------------------------------------
+// Counter-based generator (reading R-16): key = mix(seed ^ stream * C), draw(k) = mix(key + k).
+class CounterRng {
+public:
+    CounterRng(uint64_t seed, uint64_t stream) : key_(mix(seed ^ (stream * 0xD1B54A32D192ED03ull))) {}
+    uint64_t bits(uint64_t k) const { return mix(key_ + k); }
+    double unif(uint64_t k) const { return (double)(bits(k) >> 11) * 0x1.0p-53; }
+    double normal(uint64_t idx) const {   // Box-Muller, cosine branch
+        const double u1 = unif(2 * idx), u2 = unif(2 * idx + 1);
+        return std::sqrt(-2.0 * std::log(1.0 - u1)) * std::cos(2.0 * M_PI * u2);
+    }
+
+private:
+    static uint64_t mix(uint64_t z) {   // SplitMix64 output function of z + gamma
+        z += 0x9E3779B97F4A7C15ull;
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        return z ^ (z >> 31);
+    }
+    uint64_t key_;
+};
+
+enum Stream : uint64_t { kStreamC = 0, kStreamPhi = 1, kStreamCuts = 2, kStreamRate = 3 };
+
+// Velocity of global member gm (R-10, R-15).
+void member_velocity(const pf_params &p, int64_t gm, double &vx, double &vy) {
+    const CounterRng rng(p.seed, (uint64_t)gm * 8u + kStreamRate);
+    const double mult = p.rate_lo + (p.rate_hi - p.rate_lo) * rng.unif(0);
+    const double v0m = p.v0 * mult;
+    const double th = p.theta_deg * (M_PI / 180.0);
+    vx = v0m * std::cos(th);
+    vy = -(v0m * std::sin(th));
+}
+
+// Column boundaries of the columnar recipe: ncols-1 distinct sorted cuts in [1, nx-1] (R-14).
+std::vector<int64_t> column_cuts(const pf_params &p, int64_t gm) {
+    const CounterRng rng(p.seed, (uint64_t)gm * 8u + kStreamCuts);
+    std::vector<int64_t> cuts;
+    const int want = p.ic_ncols - 1;
+    for (uint64_t k = 0; (int)cuts.size() < want; ++k) {
+        const int64_t cut = 1 + (int64_t)std::floor(rng.unif(k) * (double)(p.nx - 1));
+        if (std::find(cuts.begin(), cuts.end(), cut) == cuts.end()) cuts.push_back(cut);
+    }
+    std::sort(cuts.begin(), cuts.end());
+    return cuts;
+}
+
+// Initial fields of global member gm, global rows [y0, y0+rows), written row-major (row, i)
+// into c/phi/rho (row a0 of SURVEY 8(a)).
+void fill_initial(const pf_params &p, int64_t gm, int y0, int rows, double *c, double *phi,
+                  double *rho) {
+    const int nx = p.nx;
+    const CounterRng rc(p.seed, (uint64_t)gm * 8u + kStreamC);
+    const CounterRng rp(p.seed, (uint64_t)gm * 8u + kStreamPhi);
+    const double delta = std::sqrt(2.0 * p.kappa_phi / p.W_phi);
+    std::vector<int64_t> cuts;
+    if (p.ic == PF_IC_COLUMNS) cuts = column_cuts(p, gm);
+    std::vector<double> Hx(nx);
+    for (int i = 0; i < nx; ++i) Hx[i] = p.ic_height + p.ic_amp * std::sin(2.0 * M_PI * (double)i / p.ic_wavelength);
+    std::vector<double> ccol;
+    if (p.ic == PF_IC_COLUMNS) {
+        ccol.resize(nx);
+        size_t q = 0;
+        for (int i = 0; i < nx; ++i) {
+            while (q < cuts.size() && (int64_t)i >= cuts[q]) ++q;
+            ccol[i] = (q % 2 == 0) ? p.ic_c_lo : p.ic_c_hi;
+        }
+    }
+    for (int r = 0; r < rows; ++r) {
+        const int j = y0 + r;
+        for (int i = 0; i < nx; ++i) {
+            const uint64_t k = (uint64_t)j * (uint64_t)nx + (uint64_t)i;   // global cell index
+            const size_t o = (size_t)r * nx + i;
+            if (p.ic == PF_IC_NONE) {
+                c[o] = phi[o] = rho[o] = 0.0;
+                continue;
+            }
+            if (p.ic == PF_IC_FILM) {
+                const double solid = (double)j < p.ic_height ? 1.0 : 0.0;
+                phi[o] = solid + p.noise_phi * (2.0 * rp.unif(k) - 1.0);
+                rho[o] = p.rho_in * (1.0 - solid);
+            } else {
+                const double ph = 0.5 * (1.0 - std::tanh(((double)j - Hx[i]) / delta));
+                phi[o] = ph;
+                rho[o] = p.rho_in * (1.0 - ph);
+            }
+            if (p.ic == PF_IC_COLUMNS)
+                c[o] = ccol[i];
+            else if (p.noise_c_gaussian)
+                c[o] = p.ic_c0 + p.noise_c * rc.normal(k);
+            else
+                c[o] = p.ic_c0 + p.noise_c * (2.0 * rc.unif(k) - 1.0);
+        }
+    }
+}
+
+// Stability bound R-18.
+double dt_limit(const pf_params &p) {
+    const double Mc = std::max(std::max(std::fabs(p.M_A_bulk), std::fabs(p.M_B_bulk)),
+                               std::max(std::fabs(p.M_A_surf), std::fabs(p.M_B_surf)));
+    const double dx2 = p.dx * p.dx, dx4 = dx2 * dx2;
+    const double a = Mc * (64.0 * p.kappa_c / dx4 + 16.0 * p.W_c / dx2);
+    const double b = p.M_phi * (64.0 * p.kappa_phi / dx4 + 16.0 * p.W_phi / dx2);
+    const double d = 8.0 * p.D_rho / dx2;
+    return 1.6 / std::max(a, std::max(b, d));
+}
+
+pf::Coef make_coef(const pf_params &p) {
+    pf::Coef K;
+    const double dx2 = p.dx * p.dx;
+    K.inv_dx2 = 1.0 / dx2;
+    K.half_inv_dx2 = 0.5 / dx2;
+    K.inv_2dx = 1.0 / (2.0 * p.dx);
+    K.kc_dx2 = p.kappa_c / dx2;
+    K.kp_dx2 = p.kappa_phi / dx2;
+    K.W_c = p.W_c;
+    K.W2c = 2.0 * p.W_c;
+    K.W2p = 2.0 * p.W_phi;
+    K.MBb = p.M_B_bulk;
+    K.dMb = p.M_A_bulk - p.M_B_bulk;
+    K.MBs = p.M_B_surf;
+    K.dMs = p.M_A_surf - p.M_B_surf;
+    K.inv_sigma = 1.0 / p.sigma_surf;
+    K.Mp_dx2 = p.M_phi / dx2;
+    K.Dr_dx2 = p.D_rho / dx2;
+    K.rho_in = p.rho_in;
+    K.dx2 = dx2;
+    K.half_kc = 0.5 * p.kappa_c;
+    K.half_kp = 0.5 * p.kappa_phi;
+    K.W_p = p.W_phi;
+    return K;
+}
+
+struct Slab {
+    pf::Layout L{};
+    void *U = nullptr;    // state u^n (also receives u^{n+1}: stage 2 updates in place)
+    void *Us = nullptr;   // midpoint stage state u*
+    double *partials = nullptr;
+    double *diag = nullptr;   // members * kDiag
+};
+
+enum Mode { kSingle = 0, kLoopback = 1, kNccl = 2 };
+
+}  // namespace
+
+struct pf_ctx {
+    pf_params p{};
+    int mode = kSingle;
+    int rank = 0, nranks = 1;
+    size_t esz = 8;
+    std::vector<Slab> slabs;
+    int ny_host = 0;       // rows covered by the host buffers of get/set
+    int y_host0 = 0;       // first global row of the host buffers
+    cudaStream_t stream = nullptr;
+    ncclComm_t comm = nullptr;
+    void *vel = nullptr;   // [members][2] in the storage precision
+    double *h_diag = nullptr;
+    double *staging = nullptr;
+    size_t staging_n = 0;
+    pf::Coef K{};
+    int64_t steps = 0;
+    double t = 0.0;
+    bool blown = false;
+    std::string err;
+    int64_t launches = 0;
+    // CUDA graph of graph_steps steps
+    cudaGraphExec_t gexec = nullptr;
+    int gsteps = 0;
+    // profiling
+    bool prof = false;
+    std::vector<cudaEvent_t> ev_pool;
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_rec;
+};
+
+namespace {
+
+pf_status set_err(pf_ctx *c, pf_status s, const std::string &m) {
+    if (c) c->err = m;
+    else g_create_error = m;
+    return s;
+}
+
+#define CK(ctx, call)                                                                           \
+    do {                                                                                        \
+        cudaError_t e_ = (call);                                                                \
+        if (e_ != cudaSuccess)                                                                  \
+            return set_err(ctx, PF_ERR_CUDA, fmt("%s failed: %s (%s:%d)", #call,                \
+                                                 cudaGetErrorString(e_), __FILE__, __LINE__));  \
+    } while (0)
+
+#define NK(ctx, call)                                                                           \
+    do {                                                                                        \
+        ncclResult_t r_ = (call);                                                               \
+        if (r_ != ncclSuccess)                                                                  \
+            return set_err(ctx, PF_ERR_NCCL, fmt("%s failed: %s (%s:%d)", #call,                \
+                                                 ncclGetErrorString(r_), __FILE__, __LINE__));  \
+    } while (0)
+
+pf_status validate(const pf_params *p, std::string &why) {
+    if (!p) { why = "params is NULL"; return PF_ERR_ARG; }
+    if (p->abi_version != PF_ABI_VERSION) {
+        why = fmt("abi_version %u != %u", p->abi_version, PF_ABI_VERSION);
+        return PF_ERR_ABI;
+    }
+    if (p->nx < 8 || p->ny < 8) { why = fmt("grid %dx%d: nx, ny must be >= 8 (S:152)", p->nx, p->ny); return PF_ERR_ARG; }
+    if ((int64_t)p->nx * p->ny > (int64_t)1 << 31) { why = "grid larger than 2^31 cells"; return PF_ERR_ARG; }
+    if (p->n_members < 1) { why = "n_members must be >= 1"; return PF_ERR_ARG; }
+    if (p->member_offset < 0) { why = "member_offset must be >= 0"; return PF_ERR_ARG; }
+    if (p->precision != PF_F64 && p->precision != PF_F32) { why = "precision must be PF_F64 or PF_F32"; return PF_ERR_ARG; }
+    if (!(p->dx > 0) || !(p->dt > 0) || !std::isfinite(p->dx) || !std::isfinite(p->dt)) { why = "dx and dt must be finite and > 0"; return PF_ERR_ARG; }
+    if (!(p->sigma_surf > 0)) { why = "sigma_surf must be > 0"; return PF_ERR_ARG; }
+    if (p->kappa_c < 0 || p->kappa_phi < 0 || p->M_phi < 0 || p->D_rho < 0) { why = "kappa, M_phi, D_rho must be >= 0"; return PF_ERR_ARG; }
+    if (p->M_A_bulk < 0 || p->M_B_bulk < 0 || p->M_A_surf < 0 || p->M_B_surf < 0) { why = "mobilities must be >= 0"; return PF_ERR_ARG; }
+    if (p->check_every < 1) { why = "check_every must be >= 1"; return PF_ERR_ARG; }
+    if (p->graph_steps < 0) { why = "graph_steps must be >= 0"; return PF_ERR_ARG; }
+    if (p->ic < PF_IC_FILM || p->ic > PF_IC_NONE) { why = "unknown ic"; return PF_ERR_ARG; }
+    if ((p->ic == PF_IC_ROUGH_SUBSTRATE || p->ic == PF_IC_COLUMNS) && !(p->W_phi > 0)) { why = "tanh recipes need W_phi > 0"; return PF_ERR_ARG; }
+    if (p->ic == PF_IC_ROUGH_SUBSTRATE && !(p->ic_wavelength != 0)) { why = "ic_wavelength must be != 0"; return PF_ERR_ARG; }
+    if (p->ic == PF_IC_COLUMNS && (p->ic_ncols < 1 || p->ic_ncols > p->nx)) { why = "ic_ncols must be in [1, nx]"; return PF_ERR_ARG; }
+    const double lim = dt_limit(*p);
+    if (p->dt > lim) {
+        why = fmt("dt = %g exceeds the stability bound %g (R-18)", p->dt, lim);
+        return PF_ERR_UNSTABLE_DT;
+    }
+    return PF_OK;
+}
+
+void destroy(pf_ctx *c) {
+    if (!c) return;
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    if (c->gexec) cudaGraphExecDestroy(c->gexec);
+    for (auto &s : c->slabs) {
+        cudaFree(s.U);
+        cudaFree(s.Us);
+        cudaFree(s.partials);
+        cudaFree(s.diag);
+    }
+    cudaFree(c->vel);
+    cudaFree(c->staging);
+    if (c->h_diag) cudaFreeHost(c->h_diag);
+    for (auto e : c->ev_pool) cudaEventDestroy(e);
+    for (auto &r : c->ev_rec) {
+        cudaEventDestroy(r.second.first);
+        cudaEventDestroy(r.second.second);
+    }
+    if (c->comm) ncclCommDestroy(c->comm);
+    if (c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+// ---------------------------------------------------------------------------------------
+// halo exchange of one state buffer (which = 0: U, 1: Us)
+
+void *buf_of(Slab &s, int which) { return which == 0 ? s.U : s.Us; }
+
+pf_status exchange(pf_ctx *c, int which) {
+    if (c->mode == kSingle) return PF_OK;
+    const size_t rowb = (size_t)c->p.nx * c->esz;
+    if (c->mode == kLoopback) {
+        const int P = (int)c->slabs.size();
+        for (int s = 0; s < P; ++s) {
+            Slab &me = c->slabs[s];
+            const size_t pitch = (size_t)me.L.fstride * c->esz;
+            char *mine = (char *)buf_of(me, which);
+            if (s > 0) {    // rows -2, -1  <-  slab s-1 rows ny_loc-2, ny_loc-1
+                Slab &lo = c->slabs[s - 1];
+                const char *src = (const char *)buf_of(lo, which) + (size_t)(lo.L.ny_loc) * rowb;
+                CK(c, cudaMemcpy2DAsync(mine, pitch, src, pitch, 2 * rowb, (size_t)3 * me.L.members,
+                                        cudaMemcpyDeviceToDevice, c->stream));
+            }
+            if (s < P - 1) {    // rows ny_loc, ny_loc+1  <-  slab s+1 rows 0, 1
+                Slab &hi = c->slabs[s + 1];
+                const char *src = (const char *)buf_of(hi, which) + 2 * rowb;
+                CK(c, cudaMemcpy2DAsync(mine + (size_t)(me.L.ny_loc + 2) * rowb, pitch, src, pitch,
+                                        2 * rowb, (size_t)3 * me.L.members, cudaMemcpyDeviceToDevice,
+                                        c->stream));
+            }
+        }
+        return PF_OK;
+    }
+    // NCCL: rank r exchanges 2 rows of every field of every member with r-1 and r+1.
+    Slab &me = c->slabs[0];
+    const ncclDataType_t dt = c->p.precision == PF_F64 ? ncclFloat64 : ncclFloat32;
+    const size_t cnt = 2 * (size_t)c->p.nx;
+    char *base = (char *)buf_of(me, which);
+    NK(c, ncclGroupStart());
+    for (int m = 0; m < me.L.members; ++m)
+        for (int f = 0; f < 3; ++f) {
+            char *fb = base + ((size_t)m * me.L.mstride + (size_t)f * me.L.fstride) * c->esz;
+            if (c->rank > 0) {
+                NK(c, ncclSend(fb + 2 * rowb, cnt, dt, c->rank - 1, c->comm, c->stream));
+                NK(c, ncclRecv(fb, cnt, dt, c->rank - 1, c->comm, c->stream));
+            }
+            if (c->rank < c->nranks - 1) {
+                NK(c, ncclSend(fb + (size_t)me.L.ny_loc * rowb, cnt, dt, c->rank + 1, c->comm, c->stream));
+                NK(c, ncclRecv(fb + (size_t)(me.L.ny_loc + 2) * rowb, cnt, dt, c->rank + 1, c->comm,
+                               c->stream));
+            }
+        }
+    NK(c, ncclGroupEnd());
+    return PF_OK;
+}
+
+cudaEvent_t take_event(pf_ctx *c) {
+    if (!c->ev_pool.empty()) {
+        cudaEvent_t e = c->ev_pool.back();
+        c->ev_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+// One explicit-midpoint step for every slab: stage 1, exchange, stage 2, exchange.
+pf_status one_step(pf_ctx *c, bool capture) {
+    const bool prof = c->prof && !capture;
+    for (int stage = 1; stage <= 2; ++stage) {
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        if (prof) {
+            e0 = take_event(c);
+            e1 = take_event(c);
+            CK(c, cudaEventRecord(e0, c->stream));
+        }
+        for (auto &s : c->slabs) {
+            const void *in = stage == 1 ? s.U : s.Us;
+            void *out = stage == 1 ? s.Us : s.U;
+            const double coef = stage == 1 ? 0.5 * c->p.dt : c->p.dt;
+            CK(c, pf::launch_stage(c->p.precision, s.L, c->K, in, s.U, out, c->vel, coef, c->stream));
+            if (!capture) c->launches += pf::kStageLaunches;
+        }
+        if (prof) {
+            CK(c, cudaEventRecord(e1, c->stream));
+            c->ev_rec.push_back({stage, {e0, e1}});
+        }
+        pf_status st = exchange(c, stage == 1 ? 1 : 0);
+        if (st != PF_OK) return st;
+    }
+    return PF_OK;
+}
+
+pf_status ensure_graph(pf_ctx *c) {
+    if (c->gexec || c->p.graph_steps <= 0 || c->mode == kNccl) return PF_OK;
+    cudaGraph_t g = nullptr;
+    CK(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    pf_status st = PF_OK;
+    for (int i = 0; i < c->p.graph_steps && st == PF_OK; ++i) st = one_step(c, true);
+    cudaError_t e = cudaStreamEndCapture(c->stream, &g);
+    if (st != PF_OK) {
+        if (g) cudaGraphDestroy(g);
+        return st;
+    }
+    if (e != cudaSuccess) return set_err(c, PF_ERR_CUDA, fmt("graph capture failed: %s", cudaGetErrorString(e)));
+    e = cudaGraphInstantiate(&c->gexec, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return set_err(c, PF_ERR_CUDA, fmt("graph instantiate failed: %s", cudaGetErrorString(e)));
+    c->gsteps = c->p.graph_steps;
+    return PF_OK;
+}
+
+// Launch the diagnostics of every slab (device results in slab.diag).
+pf_status run_diag(pf_ctx *c) {
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (c->prof) {
+        e0 = take_event(c);
+        e1 = take_event(c);
+        CK(c, cudaEventRecord(e0, c->stream));
+    }
+    for (auto &s : c->slabs) {
+        CK(c, pf::launch_diag(c->p.precision, s.L, c->K, s.U, s.partials, s.diag, c->stream));
+        c->launches += pf::kDiagLaunches;
+    }
+    if (c->prof) {
+        CK(c, cudaEventRecord(e1, c->stream));
+        c->ev_rec.push_back({3, {e0, e1}});
+    }
+    return PF_OK;
+}
+
+// Gather the kDiag record of every member summed over slabs (slab order) / ranks (rank order)
+// into host array out[members * kDiag].
+pf_status gather_diag(pf_ctx *c, std::vector<double> &out) {
+    const int M = c->p.n_members;
+    const size_t n = (size_t)M * pf::kDiag;
+    out.assign(n, 0.0);
+    pf_status st = run_diag(c);
+    if (st != PF_OK) return st;
+    if (c->mode == kNccl) {
+        double *dall = nullptr;
+        CK(c, cudaMallocAsync((void **)&dall, n * c->nranks * sizeof(double), c->stream));
+        NK(c, ncclAllGather(c->slabs[0].diag, dall, n, ncclFloat64, c->comm, c->stream));
+        std::vector<double> h(n * c->nranks);
+        CK(c, cudaMemcpyAsync(h.data(), dall, h.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        CK(c, cudaFreeAsync(dall, c->stream));
+        CK(c, cudaStreamSynchronize(c->stream));
+        for (int r = 0; r < c->nranks; ++r)
+            for (size_t k = 0; k < n; ++k) out[k] += h[r * n + k];
+        return PF_OK;
+    }
+    for (size_t s = 0; s < c->slabs.size(); ++s)
+        CK(c, cudaMemcpyAsync(c->h_diag + s * n, c->slabs[s].diag, n * sizeof(double),
+                              cudaMemcpyDeviceToHost, c->stream));
+    CK(c, cudaStreamSynchronize(c->stream));
+    for (size_t s = 0; s < c->slabs.size(); ++s)
+        for (size_t k = 0; k < n; ++k) out[k] += c->h_diag[s * n + k];
+    return PF_OK;
+}
+
+pf_status check_blowup(pf_ctx *c, int64_t from, int64_t to) {
+    std::vector<double> d;
+    pf_status st = gather_diag(c, d);
+    if (st != PF_OK) return st;
+    double nf[3] = {0, 0, 0};
+    int worst = -1;
+    for (int m = 0; m < c->p.n_members; ++m) {
+        for (int f = 0; f < 3; ++f) nf[f] += d[(size_t)m * pf::kDiag + 5 + f];
+        if (worst < 0 && d[(size_t)m * pf::kDiag + 4] > 0) worst = m;
+    }
+    if (nf[0] + nf[1] + nf[2] > 0) {
+        c->blown = true;
+        std::string fields;
+        const char *names[3] = {"c", "phi", "rho"};
+        for (int f = 0; f < 3; ++f)
+            if (nf[f] > 0) fields += fmt("%s%s (%.0f cells)", fields.empty() ? "" : ", ", names[f], nf[f]);
+        return set_err(c, PF_ERR_BLOWUP,
+                       fmt("blow-up: non-finite %s in steps (%lld, %lld], first member %d", fields.c_str(),
+                           (long long)from, (long long)to, worst + c->p.member_offset));
+    }
+    return PF_OK;
+}
+
+pf_status create_common(const pf_params *p, int mode, int rank, int nranks, const uint8_t *uid,
+                        pf_ctx **out) {
+    if (!out) return set_err(nullptr, PF_ERR_ARG, "out is NULL");
+    *out = nullptr;
+    std::string why;
+    pf_status st = validate(p, why);
+    if (st != PF_OK) return set_err(nullptr, st, why);
+    if (nranks < 1 || rank < 0 || rank >= nranks) return set_err(nullptr, PF_ERR_ARG, "bad rank / nranks");
+    if (p->ny % nranks != 0 || p->ny / nranks < 2)
+        return set_err(nullptr, PF_ERR_ARG, fmt("ny = %d must be a multiple of %d with >= 2 rows per slab", p->ny, nranks));
+    pf_ctx *c = new pf_ctx();
+    c->p = *p;
+    c->mode = mode;
+    c->rank = rank;
+    c->nranks = nranks;
+    c->esz = p->precision == PF_F64 ? 8 : 4;
+    c->K = make_coef(*p);
+    auto fail = [&](pf_status s) {
+        g_create_error = c->err;
+        destroy(c);
+        return s;
+    };
+    cudaError_t e = cudaSetDevice(p->device);
+    if (e != cudaSuccess) {
+        c->err = fmt("cudaSetDevice(%d): %s", p->device, cudaGetErrorString(e));
+        return fail(PF_ERR_CUDA);
+    }
+    e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        c->err = fmt("cudaStreamCreate: %s", cudaGetErrorString(e));
+        return fail(PF_ERR_CUDA);
+    }
+    // slabs
+    const int nsl = mode == kLoopback ? nranks : 1;
+    const int rows = p->ny / nranks;
+    for (int s = 0; s < nsl; ++s) {
+        Slab sl;
+        sl.L.nx = p->nx;
+        sl.L.ny = p->ny;
+        sl.L.ny_loc = rows;
+        sl.L.y0 = (mode == kLoopback ? s : rank) * rows;
+        sl.L.members = p->n_members;
+        sl.L.fstride = (int64_t)(rows + 4) * p->nx;
+        sl.L.mstride = 3 * sl.L.fstride;
+        const size_t bytes = (size_t)sl.L.mstride * p->n_members * c->esz;
+        c->slabs.push_back(sl);
+        Slab &S = c->slabs.back();
+        if (cudaMalloc(&S.U, bytes) != cudaSuccess || cudaMalloc(&S.Us, bytes) != cudaSuccess) {
+            cudaGetLastError();
+            c->err = fmt("cudaMalloc of 2 x %zu bytes failed", bytes);
+            return fail(PF_ERR_NOMEM);
+        }
+        cudaMemsetAsync(S.U, 0, bytes, c->stream);
+        cudaMemsetAsync(S.Us, 0, bytes, c->stream);
+        const size_t pb = (size_t)p->n_members * pf::diag_blocks(S.L) * pf::kDiag * sizeof(double);
+        if (cudaMalloc((void **)&S.partials, pb) != cudaSuccess ||
+            cudaMalloc((void **)&S.diag, (size_t)p->n_members * pf::kDiag * sizeof(double)) != cudaSuccess) {
+            cudaGetLastError();
+            c->err = "cudaMalloc of diagnostics scratch failed";
+            return fail(PF_ERR_NOMEM);
+        }
+    }
+    c->ny_host = mode == kNccl ? rows : p->ny;
+    c->y_host0 = mode == kNccl ? rank * rows : 0;
+    if (cudaMallocHost((void **)&c->h_diag, nsl * (size_t)p->n_members * pf::kDiag * sizeof(double)) != cudaSuccess) {
+        cudaGetLastError();
+        c->err = "cudaMallocHost failed";
+        return fail(PF_ERR_NOMEM);
+    }
+    // velocities (R-10, R-15)
+    {
+        std::vector<double> v(2 * (size_t)p->n_members);
+        for (int m = 0; m < p->n_members; ++m) member_velocity(*p, (int64_t)p->member_offset + m, v[2 * m], v[2 * m + 1]);
+        std::vector<float> vf(v.begin(), v.end());
+        if (cudaMalloc(&c->vel, v.size() * c->esz) != cudaSuccess) {
+            cudaGetLastError();
+            c->err = "cudaMalloc failed";
+            return fail(PF_ERR_NOMEM);
+        }
+        e = cudaMemcpy(c->vel, c->esz == 8 ? (const void *)v.data() : (const void *)vf.data(),
+                       v.size() * c->esz, cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) {
+            c->err = fmt("cudaMemcpy: %s", cudaGetErrorString(e));
+            return fail(PF_ERR_CUDA);
+        }
+    }
+    if (mode == kNccl) {
+        ncclUniqueId id;
+        std::memcpy(&id, uid, sizeof id);
+        ncclResult_t r = ncclCommInitRank(&c->comm, nranks, id, rank);
+        if (r != ncclSuccess) {
+            c->err = fmt("ncclCommInitRank: %s", ncclGetErrorString(r));
+            return fail(PF_ERR_NCCL);
+        }
+    }
+    // initial conditions, generated on the host per member and slab (row a0)
+    for (auto &S : c->slabs) {
+        const size_t n = (size_t)S.L.ny_loc * p->nx;
+        std::vector<double> hc(n), hp(n), hr(n);
+        for (int m = 0; m < p->n_members; ++m) {
+            fill_initial(*p, (int64_t)p->member_offset + m, S.L.y0, S.L.ny_loc, hc.data(), hp.data(), hr.data());
+            const double *src[3] = {hc.data(), hp.data(), hr.data()};
+            for (int f = 0; f < 3; ++f) {
+                char *dst = (char *)S.U + ((size_t)m * S.L.mstride + (size_t)f * S.L.fstride + 2 * (size_t)p->nx) * c->esz;
+                if (c->esz == 8) {
+                    e = cudaMemcpy(dst, src[f], n * 8, cudaMemcpyHostToDevice);
+                } else {
+                    std::vector<float> tmp(src[f], src[f] + n);
+                    e = cudaMemcpy(dst, tmp.data(), n * 4, cudaMemcpyHostToDevice);
+                }
+                if (e != cudaSuccess) {
+                    c->err = fmt("cudaMemcpy: %s", cudaGetErrorString(e));
+                    return fail(PF_ERR_CUDA);
+                }
+            }
+        }
+    }
+    st = exchange(c, 0);
+    if (st != PF_OK) return fail(st);
+    e = cudaStreamSynchronize(c->stream);
+    if (e != cudaSuccess) {
+        c->err = fmt("create: %s", cudaGetErrorString(e));
+        return fail(PF_ERR_CUDA);
+    }
+    *out = c;
+    return PF_OK;
+}
+
+pf_status check_member(pf_ctx *c, int32_t member, int &m0, int &nm) {
+    if (member == -1) {
+        m0 = 0;
+        nm = c->p.n_members;
+        return PF_OK;
+    }
+    if (member < 0 || member >= c->p.n_members) return set_err(c, PF_ERR_ARG, fmt("member %d out of range", member));
+    m0 = member;
+    nm = 1;
+    return PF_OK;
+}
+
+pf_status ensure_staging(pf_ctx *c, size_t n) {
+    if (c->staging_n >= n) return PF_OK;
+    cudaFree(c->staging);
+    c->staging = nullptr;
+    c->staging_n = 0;
+    if (cudaMalloc((void **)&c->staging, n * sizeof(double)) != cudaSuccess) {
+        cudaGetLastError();
+        return set_err(c, PF_ERR_NOMEM, "cudaMalloc of staging buffer failed");
+    }
+    c->staging_n = n;
+    return PF_OK;
+}
+
+}  // namespace
+
+// =========================================================================================
+extern "C" {
+
+pf_status pf_default_params(int32_t cfg, pf_params *o) {
+    if (!o) return set_err(nullptr, PF_ERR_ARG, "out is NULL");
+    if (cfg < 1 || cfg > 5) return set_err(nullptr, PF_ERR_ARG, fmt("no preset %d (1..5)", cfg));
+    pf_params p;
+    std::memset(&p, 0, sizeof p);
+    p.abi_version = PF_ABI_VERSION;
+    p.n_members = 1;
+    p.precision = PF_F64;
+    p.dx = 1.0;
+    p.dt = 1e-3;
+    p.kappa_c = p.kappa_phi = 1.0;
+    p.W_c = p.W_phi = 1.0;
+    p.sigma_surf = 0.5;
+    p.M_phi = 1.0;
+    p.D_rho = 1.0;
+    p.rho_in = 1.0;
+    p.v0 = 0.5;
+    p.theta_deg = 90.0;
+    p.rate_lo = p.rate_hi = 1.0;
+    p.ic_wavelength = 32.0;
+    p.ic_c0 = 0.5;
+    p.ic_c_lo = 0.2;
+    p.ic_c_hi = 0.8;
+    p.check_every = 100;
+    p.seed = (uint64_t)cfg;
+    p.graph_steps = 0;
+    if (cfg == 1) {             // configs[0]: 64^2 film, all mobilities 1
+        p.nx = p.ny = 64;
+        p.M_A_bulk = p.M_B_bulk = p.M_A_surf = p.M_B_surf = 1.0;
+        p.ic = PF_IC_FILM;
+        p.ic_height = 16.0;
+        p.noise_c = 0.05;
+        p.noise_phi = 0.01;
+        p.graph_steps = 50;
+    } else {                    // configs[1..4]: M_c / M_phi = 10
+        p.M_A_bulk = p.M_B_bulk = p.M_A_surf = p.M_B_surf = 10.0;
+        p.ic = PF_IC_ROUGH_SUBSTRATE;
+        p.ic_height = 32.0;
+        p.ic_amp = 2.0;
+        p.noise_c = 0.05;
+        p.noise_c_gaussian = 1;
+        if (cfg == 2) {
+            p.nx = p.ny = 256;
+            p.graph_steps = 50;
+        } else if (cfg == 3) {
+            p.nx = p.ny = 512;
+            p.n_members = 64;
+            p.rate_lo = 0.5;
+            p.rate_hi = 2.0;
+        } else if (cfg == 4) {
+            p.nx = p.ny = 4096;
+            p.ic_height = 512.0;
+        } else {
+            p.nx = p.ny = 8192;
+            p.precision = PF_F32;
+            p.ic = PF_IC_COLUMNS;
+            p.ic_height = 4096.0;
+            p.ic_amp = 0.0;
+            p.ic_ncols = 64;
+            p.noise_c = 0.0;
+            p.noise_c_gaussian = 0;
+        }
+    }
+    *o = p;
+    return PF_OK;
+}
+
+uint32_t pf_params_size(void) { return (uint32_t)sizeof(pf_params); }
+
+pf_status pf_initial_fields(const pf_params *p, int64_t member, int32_t y0, int32_t rows,
+                            double *fc, double *fp, double *fr) {
+    if (!p || !fc || !fp || !fr) return set_err(nullptr, PF_ERR_ARG, "NULL argument");
+    if (p->nx < 1 || y0 < 0 || rows < 0 || member < 0) return set_err(nullptr, PF_ERR_ARG, "bad extent");
+    if (p->ic == PF_IC_COLUMNS && (p->ic_ncols < 1 || p->ic_ncols > p->nx))
+        return set_err(nullptr, PF_ERR_ARG, "ic_ncols must be in [1, nx]");
+    fill_initial(*p, member, y0, rows, fc, fp, fr);
+    return PF_OK;
+}
+
+pf_status pf_member_velocity(const pf_params *p, int64_t member, double *vx, double *vy) {
+    if (!p || !vx || !vy || member < 0) return set_err(nullptr, PF_ERR_ARG, "bad argument");
+    member_velocity(*p, member, *vx, *vy);
+    return PF_OK;
+}
+
+pf_status pf_dt_limit(const pf_params *p, double *dt_max) {
+    if (!p || !dt_max) return set_err(nullptr, PF_ERR_ARG, "NULL argument");
+    *dt_max = dt_limit(*p);
+    return PF_OK;
+}
+
+pf_status pf_create(const pf_params *p, pf_ctx **out) { return create_common(p, kSingle, 0, 1, nullptr, out); }
+
+pf_status pf_create_loopback(const pf_params *p, int32_t nslabs, pf_ctx **out) {
+    if (nslabs < 1) return set_err(nullptr, PF_ERR_ARG, "nslabs must be >= 1");
+    return create_common(p, nslabs == 1 ? kSingle : kLoopback, 0, nslabs, nullptr, out);
+}
+
+pf_status pf_nccl_unique_id(uint8_t out[128]) {
+    if (!out) return set_err(nullptr, PF_ERR_ARG, "out is NULL");
+    ncclUniqueId id;
+    ncclResult_t r = ncclGetUniqueId(&id);
+    if (r != ncclSuccess) return set_err(nullptr, PF_ERR_NCCL, fmt("ncclGetUniqueId: %s", ncclGetErrorString(r)));
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    std::memcpy(out, &id, 128);
+    return PF_OK;
+}
+
+pf_status pf_create_slab(const pf_params *p, int32_t rank, int32_t nranks, const uint8_t uid[128],
+                         pf_ctx **out) {
+    if (!uid) return set_err(nullptr, PF_ERR_ARG, "uid is NULL");
+    return create_common(p, nranks == 1 ? kSingle : kNccl, rank, nranks, uid, out);
+}
+
+pf_status pf_step(pf_ctx *c, int64_t n) {
+    if (!c) return set_err(nullptr, PF_ERR_ARG, "ctx is NULL");
+    if (n < 0) return set_err(c, PF_ERR_ARG, "n must be >= 0");
+    if (c->blown) return set_err(c, PF_ERR_STATE, "state blew up; call pf_set_fields first");
+    cudaSetDevice(c->p.device);
+    const int64_t ce = c->p.check_every;
+    int64_t left = n;
+    while (left > 0) {
+        int64_t chunk = ce - (c->steps % ce);
+        if (chunk > left) chunk = left;
+        int64_t done = 0;
+        const bool use_graph = c->p.graph_steps > 0 && !c->prof && c->mode != kNccl;
+        if (use_graph && chunk >= c->p.graph_steps) {
+            pf_status st = ensure_graph(c);
+            if (st != PF_OK) return st;
+            while (chunk - done >= c->gsteps) {
+                CK(c, cudaGraphLaunch(c->gexec, c->stream));
+                c->launches += (int64_t)c->gsteps * 2 * (int64_t)c->slabs.size() * pf::kStageLaunches;
+                done += c->gsteps;
+            }
+        }
+        for (; done < chunk; ++done) {
+            pf_status st = one_step(c, false);
+            if (st != PF_OK) return st;
+        }
+        const int64_t from = c->steps;
+        c->steps += chunk;
+        c->t += (double)chunk * c->p.dt;
+        left -= chunk;
+        if (c->steps % ce == 0 || left == 0) {
+            pf_status st = check_blowup(c, from, c->steps);
+            if (st != PF_OK) return st;
+        }
+    }
+    CK(c, cudaStreamSynchronize(c->stream));
+    return PF_OK;
+}
+
+pf_status pf_get_fields(pf_ctx *c, int32_t member, double *fc, double *fp, double *fr) {
+    if (!c) return set_err(nullptr, PF_ERR_ARG, "ctx is NULL");
+    int m0, nm;
+    pf_status st = check_member(c, member, m0, nm);
+    if (st != PF_OK) return st;
+    cudaSetDevice(c->p.device);
+    double *dst[3] = {fc, fp, fr};
+    const size_t hrow = (size_t)c->p.nx * sizeof(double);
+    const size_t hmem = (size_t)c->ny_host * hrow;   // host bytes per member
+    for (auto &S : c->slabs) {
+        const size_t nloc = (size_t)S.L.ny_loc * c->p.nx;
+        for (int f = 0; f < 3; ++f) {
+            if (!dst[f]) continue;
+            char *h = (char *)dst[f] + (size_t)(S.L.y0 - c->y_host0) * hrow;
+            if (c->esz == 8) {
+                const char *d = (const char *)S.U + ((size_t)m0 * S.L.mstride + (size_t)f * S.L.fstride + 2 * (size_t)c->p.nx) * 8;
+                CK(c, cudaMemcpy2DAsync(h, hmem, d, (size_t)S.L.mstride * 8, nloc * 8, nm, cudaMemcpyDeviceToHost, c->stream));
+            } else {
+                st = ensure_staging(c, nloc * nm);
+                if (st != PF_OK) return st;
+                CK(c, pf::launch_pack_f64(c->p.precision, S.L, f, m0, nm, S.U, c->staging, c->stream));
+                c->launches += 1;
+                CK(c, cudaMemcpy2DAsync(h, hmem, c->staging, nloc * 8, nloc * 8, nm, cudaMemcpyDeviceToHost, c->stream));
+            }
+        }
+    }
+    CK(c, cudaStreamSynchronize(c->stream));
+    return PF_OK;
+}
+
+pf_status pf_set_fields(pf_ctx *c, int32_t member, const double *fc, const double *fp, const double *fr) {
+    if (!c) return set_err(nullptr, PF_ERR_ARG, "ctx is NULL");
+    int m0, nm;
+    pf_status st = check_member(c, member, m0, nm);
+    if (st != PF_OK) return st;
+    cudaSetDevice(c->p.device);
+    const double *src[3] = {fc, fp, fr};
+    const size_t hrow = (size_t)c->p.nx * sizeof(double);
+    const size_t hmem = (size_t)c->ny_host * hrow;
+    for (auto &S : c->slabs) {
+        const size_t nloc = (size_t)S.L.ny_loc * c->p.nx;
+        for (int f = 0; f < 3; ++f) {
+            if (!src[f]) continue;
+            const char *h = (const char *)src[f] + (size_t)(S.L.y0 - c->y_host0) * hrow;
+            if (c->esz == 8) {
+                char *d = (char *)S.U + ((size_t)m0 * S.L.mstride + (size_t)f * S.L.fstride + 2 * (size_t)c->p.nx) * 8;
+                CK(c, cudaMemcpy2DAsync(d, (size_t)S.L.mstride * 8, h, hmem, nloc * 8, nm, cudaMemcpyHostToDevice, c->stream));
+            } else {
+                st = ensure_staging(c, nloc * nm);
+                if (st != PF_OK) return st;
+                CK(c, cudaMemcpy2DAsync(c->staging, nloc * 8, h, hmem, nloc * 8, nm, cudaMemcpyHostToDevice, c->stream));
+                CK(c, pf::launch_unpack_f64(c->p.precision, S.L, f, m0, nm, c->staging, S.U, c->stream));
+                c->launches += 1;
+            }
+        }
+    }
+    st = exchange(c, 0);
+    if (st != PF_OK) return st;
+    CK(c, cudaStreamSynchronize(c->stream));
+    c->blown = false;
+    return PF_OK;
+}
+
+pf_status pf_diagnostics(pf_ctx *c, int32_t member, double out[5]) {
+    if (!c) return set_err(nullptr, PF_ERR_ARG, "ctx is NULL");
+    if (!out) return set_err(c, PF_ERR_ARG, "out is NULL");
+    if (member < 0 || member >= c->p.n_members) return set_err(c, PF_ERR_ARG, fmt("member %d out of range", member));
+    cudaSetDevice(c->p.device);
+    std::vector<double> d;
+    pf_status st = gather_diag(c, d);
+    if (st != PF_OK) return st;
+    for (int k = 0; k < 5; ++k) out[k] = d[(size_t)member * pf::kDiag + k];
+    return PF_OK;
+}
+
+pf_status pf_info(pf_ctx *c, int64_t *steps, double *t, int32_t *y0, int32_t *ny_local) {
+    if (!c) return set_err(nullptr, PF_ERR_ARG, "ctx is NULL");
+    if (steps) *steps = c->steps;
+    if (t) *t = c->t;
+    if (y0) *y0 = c->y_host0;
+    if (ny_local) *ny_local = c->ny_host;
+    return PF_OK;
+}
+
+pf_status pf_set_time(pf_ctx *c, int64_t steps, double t) {
+    if (!c) return set_err(nullptr, PF_ERR_ARG, "ctx is NULL");
+    if (steps < 0) return set_err(c, PF_ERR_ARG, "steps must be >= 0");
+    c->steps = steps;
+    c->t = t;
+    return PF_OK;
+}
+
+pf_status pf_launch_count(pf_ctx *c, int64_t *launches) {
+    if (!c || !launches) return set_err(c, PF_ERR_ARG, "NULL argument");
+    *launches = c->launches;
+    return PF_OK;
+}
+
+pf_status pf_profile(pf_ctx *c, int32_t enable) {
+    if (!c) return set_err(nullptr, PF_ERR_ARG, "ctx is NULL");
+    CK(c, cudaStreamSynchronize(c->stream));
+    for (auto &r : c->ev_rec) {
+        c->ev_pool.push_back(r.second.first);
+        c->ev_pool.push_back(r.second.second);
+    }
+    c->ev_rec.clear();
+    c->prof = enable != 0;
+    return PF_OK;
+}
+
+pf_status pf_profile_read(pf_ctx *c, double out[6]) {
+    if (!c || !out) return set_err(c, PF_ERR_ARG, "NULL argument");
+    CK(c, cudaStreamSynchronize(c->stream));
+    for (int k = 0; k < 6; ++k) out[k] = 0.0;
+    for (auto &r : c->ev_rec) {
+        float ms = 0.f;
+        CK(c, cudaEventElapsedTime(&ms, r.second.first, r.second.second));
+        const int slot = 2 * (r.first - 1);
+        out[slot] += ms;
+        out[slot + 1] += 1.0;
+    }
+    return PF_OK;
+}
+
+pf_status pf_stream(pf_ctx *c, void **stream) {
+    if (!c || !stream) return set_err(c, PF_ERR_ARG, "NULL argument");
+    *stream = (void *)c->stream;
+    return PF_OK;
+}
+
+const char *pf_last_error(const pf_ctx *c) { return c ? c->err.c_str() : g_create_error.c_str(); }
+
+void pf_free(pf_ctx *c) { destroy(c); }
+
+}  // extern "C"

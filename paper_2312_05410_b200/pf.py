@@ -1,0 +1,302 @@
+"""Thin ctypes binding of libpf (include/pf.h): argument marshalling only.
+
+Every step of the hot path runs inside libpf.so (host runtime + sm_100a kernels).  This module
+never computes model arithmetic and has no fallback: if the shared library is missing it raises.
+Function names mirror the C ABI (``pf_create``, ``pf_step``, ...); ``Simulation`` is a small
+convenience wrapper over the same calls.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libpf.so")
+HEADER = os.path.join(os.path.dirname(_HERE), "include", "pf.h")
+
+PF_ABI_VERSION = 1
+PF_OK, PF_ERR_ARG, PF_ERR_UNSTABLE_DT, PF_ERR_NOMEM, PF_ERR_CUDA, PF_ERR_NCCL, PF_ERR_BLOWUP, \
+    PF_ERR_STATE, PF_ERR_ABI = range(9)
+STATUS_NAMES = ["PF_OK", "PF_ERR_ARG", "PF_ERR_UNSTABLE_DT", "PF_ERR_NOMEM", "PF_ERR_CUDA",
+                "PF_ERR_NCCL", "PF_ERR_BLOWUP", "PF_ERR_STATE", "PF_ERR_ABI"]
+PF_F64, PF_F32 = 0, 1
+PF_IC_FILM, PF_IC_ROUGH_SUBSTRATE, PF_IC_COLUMNS, PF_IC_NONE = range(4)
+
+
+class pf_params(C.Structure):
+    _fields_ = [
+        ("abi_version", C.c_uint32), ("nx", C.c_int32), ("ny", C.c_int32),
+        ("n_members", C.c_int32), ("member_offset", C.c_int32), ("precision", C.c_int32),
+        ("dx", C.c_double), ("dt", C.c_double),
+        ("kappa_c", C.c_double), ("kappa_phi", C.c_double), ("W_c", C.c_double), ("W_phi", C.c_double),
+        ("M_A_bulk", C.c_double), ("M_B_bulk", C.c_double), ("M_A_surf", C.c_double),
+        ("M_B_surf", C.c_double), ("sigma_surf", C.c_double), ("M_phi", C.c_double),
+        ("D_rho", C.c_double), ("rho_in", C.c_double), ("v0", C.c_double), ("theta_deg", C.c_double),
+        ("rate_lo", C.c_double), ("rate_hi", C.c_double),
+        ("ic", C.c_int32), ("ic_ncols", C.c_int32),
+        ("ic_height", C.c_double), ("ic_amp", C.c_double), ("ic_wavelength", C.c_double),
+        ("ic_c0", C.c_double), ("ic_c_lo", C.c_double), ("ic_c_hi", C.c_double),
+        ("noise_c", C.c_double), ("noise_phi", C.c_double),
+        ("noise_c_gaussian", C.c_int32), ("check_every", C.c_int32),
+        ("seed", C.c_uint64), ("device", C.c_int32), ("graph_steps", C.c_int32),
+    ]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+    def replace(self, **kw) -> "pf_params":
+        q = pf_params()
+        C.memmove(C.byref(q), C.byref(self), C.sizeof(self))
+        for k, v in kw.items():
+            if not hasattr(q, k):
+                raise AttributeError(k)
+            setattr(q, k, v)
+        return q
+
+
+class PfError(RuntimeError):
+    def __init__(self, status, msg):
+        self.status = status
+        name = STATUS_NAMES[status] if 0 <= status < len(STATUS_NAMES) else str(status)
+        super().__init__(f"{name}: {msg}")
+
+
+_lib = None
+_ctx_p = C.c_void_p
+_D = C.POINTER(C.c_double)
+
+
+def lib():
+    """Load libpf.so (fails loudly if it was not built: there is no CPU fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built: run `python -m paper_2312_05410_b200.build`")
+        L = C.CDLL(LIB_PATH)
+        P = C.POINTER(pf_params)
+        i32, i64 = C.c_int32, C.c_int64
+        sig = {
+            "pf_params_size": (C.c_uint32, []),
+            "pf_default_params": (C.c_int, [i32, P]),
+            "pf_initial_fields": (C.c_int, [P, i64, i32, i32, _D, _D, _D]),
+            "pf_member_velocity": (C.c_int, [P, i64, _D, _D]),
+            "pf_dt_limit": (C.c_int, [P, _D]),
+            "pf_create": (C.c_int, [P, C.POINTER(_ctx_p)]),
+            "pf_nccl_unique_id": (C.c_int, [C.c_char_p]),
+            "pf_create_slab": (C.c_int, [P, i32, i32, C.c_char_p, C.POINTER(_ctx_p)]),
+            "pf_create_loopback": (C.c_int, [P, i32, C.POINTER(_ctx_p)]),
+            "pf_step": (C.c_int, [_ctx_p, i64]),
+            "pf_get_fields": (C.c_int, [_ctx_p, i32, _D, _D, _D]),
+            "pf_set_fields": (C.c_int, [_ctx_p, i32, _D, _D, _D]),
+            "pf_diagnostics": (C.c_int, [_ctx_p, i32, _D]),
+            "pf_info": (C.c_int, [_ctx_p, C.POINTER(i64), _D, C.POINTER(i32), C.POINTER(i32)]),
+            "pf_set_time": (C.c_int, [_ctx_p, i64, C.c_double]),
+            "pf_launch_count": (C.c_int, [_ctx_p, C.POINTER(i64)]),
+            "pf_profile": (C.c_int, [_ctx_p, i32]),
+            "pf_profile_read": (C.c_int, [_ctx_p, _D]),
+            "pf_stream": (C.c_int, [_ctx_p, C.POINTER(C.c_void_p)]),
+            "pf_last_error": (C.c_char_p, [_ctx_p]),
+            "pf_free": (None, [_ctx_p]),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        if L.pf_params_size() != C.sizeof(pf_params):
+            raise ImportError(f"pf_params size mismatch: lib {L.pf_params_size()} vs binding {C.sizeof(pf_params)}")
+        _lib = L
+    return _lib
+
+
+def _check(st, ctx=None):
+    if st != PF_OK:
+        msg = lib().pf_last_error(ctx)
+        raise PfError(st, msg.decode() if msg else "")
+
+
+def _dptr(a):
+    if a is None:
+        return None
+    if not (isinstance(a, np.ndarray) and a.dtype == np.float64 and a.flags.c_contiguous):
+        raise TypeError("expected a C-contiguous float64 numpy array")
+    return a.ctypes.data_as(_D)
+
+
+def _hptr(a):
+    """Host pointer of a numpy array or of a pinned CPU torch tensor (float64, contiguous)."""
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        return _dptr(a)
+    # torch tensor (pinned host memory for the e2e bench)
+    if getattr(a, "device", None) is not None and str(a.device) != "cpu":
+        raise TypeError("host buffers only")
+    if str(a.dtype) != "torch.float64" or not a.is_contiguous():
+        raise TypeError("expected a contiguous float64 tensor")
+    return C.cast(C.c_void_p(a.data_ptr()), _D)
+
+
+# ------------------------------------------------------------------ ABI-named functions
+def pf_default_params(cfg: int) -> pf_params:
+    p = pf_params()
+    _check(lib().pf_default_params(cfg, C.byref(p)))
+    return p
+
+
+def pf_initial_fields(p: pf_params, member: int, y0: int, rows: int):
+    c = np.empty((rows, p.nx)); phi = np.empty_like(c); rho = np.empty_like(c)
+    _check(lib().pf_initial_fields(C.byref(p), member, y0, rows, _dptr(c), _dptr(phi), _dptr(rho)))
+    return c, phi, rho
+
+
+def pf_member_velocity(p: pf_params, member: int):
+    vx, vy = C.c_double(), C.c_double()
+    _check(lib().pf_member_velocity(C.byref(p), member, C.byref(vx), C.byref(vy)))
+    return vx.value, vy.value
+
+
+def pf_dt_limit(p: pf_params) -> float:
+    d = C.c_double()
+    _check(lib().pf_dt_limit(C.byref(p), C.byref(d)))
+    return d.value
+
+
+def pf_create(p: pf_params):
+    ctx = _ctx_p()
+    _check(lib().pf_create(C.byref(p), C.byref(ctx)))
+    return ctx
+
+
+def pf_create_loopback(p: pf_params, nslabs: int):
+    ctx = _ctx_p()
+    _check(lib().pf_create_loopback(C.byref(p), nslabs, C.byref(ctx)))
+    return ctx
+
+
+def pf_nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(lib().pf_nccl_unique_id(buf))
+    return buf.raw
+
+
+def pf_create_slab(p: pf_params, rank: int, nranks: int, uid: bytes):
+    if len(uid) != 128:
+        raise ValueError("uid must be 128 bytes")
+    ctx = _ctx_p()
+    _check(lib().pf_create_slab(C.byref(p), rank, nranks, uid, C.byref(ctx)))
+    return ctx
+
+
+def pf_step(ctx, n: int):
+    _check(lib().pf_step(ctx, int(n)), ctx)
+
+
+def pf_get_fields(ctx, member, c, phi, rho):
+    _check(lib().pf_get_fields(ctx, member, _hptr(c), _hptr(phi), _hptr(rho)), ctx)
+
+
+def pf_set_fields(ctx, member, c, phi, rho):
+    _check(lib().pf_set_fields(ctx, member, _hptr(c), _hptr(phi), _hptr(rho)), ctx)
+
+
+def pf_diagnostics(ctx, member: int) -> np.ndarray:
+    out = np.zeros(5)
+    _check(lib().pf_diagnostics(ctx, member, _dptr(out)), ctx)
+    return out
+
+
+def pf_info(ctx):
+    s, t, y0, ny = C.c_int64(), C.c_double(), C.c_int32(), C.c_int32()
+    _check(lib().pf_info(ctx, C.byref(s), C.byref(t), C.byref(y0), C.byref(ny)), ctx)
+    return s.value, t.value, y0.value, ny.value
+
+
+def pf_set_time(ctx, steps: int, t: float):
+    _check(lib().pf_set_time(ctx, steps, t), ctx)
+
+
+def pf_launch_count(ctx) -> int:
+    n = C.c_int64()
+    _check(lib().pf_launch_count(ctx, C.byref(n)), ctx)
+    return n.value
+
+
+def pf_profile(ctx, enable: bool):
+    _check(lib().pf_profile(ctx, 1 if enable else 0), ctx)
+
+
+def pf_profile_read(ctx) -> np.ndarray:
+    out = np.zeros(6)
+    _check(lib().pf_profile_read(ctx, _dptr(out)), ctx)
+    return out
+
+
+def pf_stream(ctx) -> int:
+    """cudaStream_t of the ctx as an integer handle (for torch.cuda.ExternalStream)."""
+    s = C.c_void_p()
+    _check(lib().pf_stream(ctx, C.byref(s)), ctx)
+    return s.value or 0
+
+
+def pf_free(ctx):
+    if ctx:
+        lib().pf_free(ctx)
+
+
+# ------------------------------------------------------------------ convenience wrapper
+class Simulation:
+    """Owns one pf_ctx.  mode: 'single' | ('loopback', nslabs) | ('slab', rank, nranks, uid)."""
+
+    def __init__(self, params: pf_params, mode="single"):
+        self.params = params
+        if mode == "single":
+            self.ctx = pf_create(params)
+        elif mode[0] == "loopback":
+            self.ctx = pf_create_loopback(params, mode[1])
+        elif mode[0] == "slab":
+            self.ctx = pf_create_slab(params, mode[1], mode[2], mode[3])
+        else:
+            raise ValueError(mode)
+        _, _, self.y0, self.ny_local = pf_info(self.ctx)
+
+    @property
+    def members(self):
+        return self.params.n_members
+
+    def step(self, n: int):
+        pf_step(self.ctx, n)
+
+    def fields(self, member: int = 0):
+        shape = (self.ny_local, self.params.nx) if member >= 0 else (self.members, self.ny_local, self.params.nx)
+        c = np.empty(shape); phi = np.empty(shape); rho = np.empty(shape)
+        pf_get_fields(self.ctx, member, c, phi, rho)
+        return c, phi, rho
+
+    def set_fields(self, member, c=None, phi=None, rho=None):
+        f = lambda a: None if a is None else np.ascontiguousarray(a, dtype=np.float64)
+        pf_set_fields(self.ctx, member, f(c), f(phi), f(rho))
+
+    def diagnostics(self, member: int = 0):
+        return pf_diagnostics(self.ctx, member)
+
+    def info(self):
+        return pf_info(self.ctx)
+
+    def close(self):
+        if self.ctx:
+            pf_free(self.ctx)
+            self.ctx = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

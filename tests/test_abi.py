@@ -1,0 +1,121 @@
+"""CPU tests of the C-ABI boundary: the library loads, exports every symbol of include/pf.h,
+its host-side pieces (presets, initial conditions, velocities, dt bound, validation) agree with
+the oracle's independent implementation bit for bit, and errors come back as status codes."""
+import ctypes as C
+import re
+from dataclasses import asdict
+
+import numpy as np
+import pytest
+
+from paper_2312_05410_b200 import pf
+
+
+@pytest.fixture(scope="module")
+def L():
+    from paper_2312_05410_b200 import build
+    build.build()
+    return pf.lib()
+
+
+def _declared():
+    src = open(pf.HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(pf_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_exports_every_declared_symbol(L):
+    names = _declared()
+    assert "pf_create" in names and "pf_step" in names and "pf_get_fields" in names and "pf_free" in names
+    for n in names:
+        assert hasattr(L, n), n
+
+
+def test_struct_size(L):
+    assert L.pf_params_size() == C.sizeof(pf.pf_params)
+
+
+def _oracle_view(p):
+    """Map library params onto the oracle's Model/IC field names (names only, no arithmetic)."""
+    return dict(nx=p.nx, ny=p.ny, dx=p.dx, dt=p.dt, kappa_c=p.kappa_c, kappa_phi=p.kappa_phi,
+                W_c=p.W_c, W_phi=p.W_phi, MA_bulk=p.M_A_bulk, MB_bulk=p.M_B_bulk,
+                MA_surf=p.M_A_surf, MB_surf=p.M_B_surf, sigma_surf=p.sigma_surf, M_phi=p.M_phi,
+                D_rho=p.D_rho, rho_in=p.rho_in)
+
+
+def _ic_view(p):
+    kinds = {pf.PF_IC_FILM: "film", pf.PF_IC_ROUGH_SUBSTRATE: "rough", pf.PF_IC_COLUMNS: "columns"}
+    return dict(kind=kinds[p.ic], height=p.ic_height, amp=p.ic_amp, wavelength=p.ic_wavelength,
+                ncols=p.ic_ncols, c0=p.ic_c0, c_lo=p.ic_c_lo, c_hi=p.ic_c_hi, noise_c=p.noise_c,
+                noise_phi=p.noise_phi, noise_c_gaussian=bool(p.noise_c_gaussian),
+                kappa_phi=p.kappa_phi, W_phi=p.W_phi, rho_in=p.rho_in, v0=p.v0,
+                theta_deg=p.theta_deg, rate_lo=p.rate_lo, rate_hi=p.rate_hi, seed=p.seed)
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
+def test_presets_match_oracle(L, ora, cfg):
+    p = pf.pf_default_params(cfg)
+    pr = ora.preset(cfg)
+    mo = asdict(pr["model"]); mo.pop("v_x"); mo.pop("v_y")
+    assert _oracle_view(p) == mo
+    ic = asdict(pr["ic"])
+    got = _ic_view(p)
+    if pr["ic"].kind != "columns":
+        ic.pop("ncols"); got.pop("ncols")
+    assert got == ic
+    assert p.n_members == pr["members"]
+    assert p.precision == (pf.PF_F64 if pr["precision"] == "f64" else pf.PF_F32)
+
+
+def _ora_ic(ora, p):
+    d = _ic_view(p)
+    return ora.IC(**d)
+
+
+@pytest.mark.parametrize("cfg,nx,ny,member", [(1, 64, 64, 0), (2, 256, 64, 0), (3, 96, 48, 37),
+                                               (4, 128, 40, 0), (5, 1024, 24, 0)])
+def test_initial_fields_bitwise_equal_oracle(L, ora, cfg, nx, ny, member):
+    """Row a0: the library's IC generator and the oracle's (independent code, same spec R-16)."""
+    p = pf.pf_default_params(cfg)
+    p.nx, p.ny = nx, ny
+    if cfg == 5:
+        p.ic_height = ny / 2
+    oc, op, orr = ora.initial_fields(_ora_ic(ora, p), nx, ny, member)
+    c, phi, rho = pf.pf_initial_fields(p, member, 0, ny)
+    assert np.array_equal(c, oc) and np.array_equal(phi, op) and np.array_equal(rho, orr)
+    # any row window (slab mode generates only its rows)
+    c2, p2, r2 = pf.pf_initial_fields(p, member, ny // 3, ny // 2)
+    sl = slice(ny // 3, ny // 3 + ny // 2)
+    assert np.array_equal(c2, oc[sl]) and np.array_equal(p2, op[sl]) and np.array_equal(r2, orr[sl])
+
+
+def test_member_velocity_bitwise(L, ora):
+    p = pf.pf_default_params(3)
+    ic = _ora_ic(ora, p)
+    for m in (0, 1, 17, 63, 1000):
+        assert pf.pf_member_velocity(p, m) == ora.member_velocity(ic, m)
+
+
+def test_dt_limit(L, ora):
+    for cfg, mc in ((1, 1.0), (2, 10.0), (5, 10.0)):
+        p = pf.pf_default_params(cfg)
+        m = ora.Model(**_oracle_view(p))
+        assert pf.pf_dt_limit(p) == pytest.approx(ora.dt_max(m, mc), rel=1e-15)
+
+
+def test_create_validation_errors(L):
+    p = pf.pf_default_params(1)
+    with pytest.raises(pf.PfError) as e:
+        pf.pf_create(p.replace(dt=0.05))
+    assert e.value.status == pf.PF_ERR_UNSTABLE_DT and "R-18" in str(e.value)
+    with pytest.raises(pf.PfError) as e:
+        pf.pf_create(p.replace(nx=4))
+    assert e.value.status == pf.PF_ERR_ARG
+    with pytest.raises(pf.PfError) as e:
+        pf.pf_create(p.replace(abi_version=99))
+    assert e.value.status == pf.PF_ERR_ABI
+    with pytest.raises(pf.PfError) as e:
+        pf.pf_create_loopback(p.replace(ny=64), 5)
+    assert e.value.status == pf.PF_ERR_ARG
+    with pytest.raises(pf.PfError):
+        pf.pf_default_params(9)

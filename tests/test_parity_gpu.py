@@ -1,0 +1,104 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on identical seeded
+inputs (BASELINE.json tolerances: fp64 normwise <= 1e-12 after 1 step, <= 1e-8 after 1000 steps on
+configs[0]; diagnostics within 1e-12 relative; fp32 configs[4] <= 1e-4 after 100 steps)."""
+import numpy as np
+import pytest
+
+from paper_2312_05410_b200 import pf
+from tests import inputs
+from tests._maps import oracle_member, normwise
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    pf.lib()
+
+
+def _sim(p, mode="single"):
+    return pf.Simulation(p, mode)
+
+
+def test_cfg1_initial_fields_bitwise(ora):
+    p = pf.pf_default_params(1)
+    m, ic = oracle_member(ora, p, 0)
+    with _sim(p) as s:
+        got = s.fields(0)
+    want = ora.initial_fields(ic, 64, 64, 0)
+    for g, w in zip(got, want):
+        assert np.array_equal(g, w)
+
+
+def test_cfg1_one_step_and_1000_steps(ora):
+    """configs[0]: <= 1e-12 after 1 step, <= 1e-8 after 1000 steps (north_star Tolerances)."""
+    p = pf.pf_default_params(1)
+    m, ic = oracle_member(ora, p, 0)
+    u0 = ora.initial_fields(ic, 64, 64, 0)
+    with _sim(p) as s:
+        s.step(1)
+        e1 = normwise(s.fields(0), ora.step(m, *u0, 1))
+        assert e1 <= 1e-12, e1
+        s.step(999)
+        ref = ora.step(m, *u0, 1000)
+        got = s.fields(0)
+        e = normwise(got, ref)
+        assert e <= 1e-8, e
+        d = s.diagnostics(0)
+        dref = ora.diagnostics(m, *ref)
+        for k in range(4):
+            assert abs(d[k] - dref[k]) <= 1e-12 * abs(dref[k]), (k, d[k], dref[k])
+        assert d[4] == 0
+        steps, t, y0, ny = s.info()
+        assert steps == 1000 and abs(t - 1.0) < 1e-12 and y0 == 0 and ny == 64
+
+
+@pytest.mark.parametrize("nx,ny,members", [(72, 40, 3), (100, 37, 2), (8, 8, 1), (33, 65, 2), (130, 18, 1)])
+def test_ragged_grids_random_inputs(ora, nx, ny, members):
+    """Ragged tails in x and y (not multiples of the 32 x 16 tile), minimum grid 8 x 8, several
+    members with different rates, oblique deposition and unequal mobilities; inputs set through
+    pf_set_fields from the shared seeded generator."""
+    p = pf.pf_default_params(1).replace(nx=nx, ny=ny, n_members=members, theta_deg=63.0,
+                                       M_A_bulk=1.5, M_B_bulk=0.5, M_A_surf=2.0, M_B_surf=0.8,
+                                       rate_lo=0.5, rate_hi=2.0, rho_in=0.9, graph_steps=0, seed=11)
+    with _sim(p) as s:
+        u = [inputs.random_state(nx, ny, 100 + k, phi_kind="smooth") for k in range(members)]
+        for k in range(members):
+            s.set_fields(k, *u[k])
+        s.step(1)
+        for k in range(members):
+            m, _ = oracle_member(ora, p, k)
+            e = normwise(s.fields(k), ora.step(m, *u[k], 1))
+            assert e <= 1e-12, (k, e)
+        s.step(49)
+        for k in range(members):
+            m, _ = oracle_member(ora, p, k)
+            ref = ora.step(m, *u[k], 50)
+            e = normwise(s.fields(k), ref)
+            assert e <= 1e-10, (k, e)
+            d = s.diagnostics(k)
+            dref = ora.diagnostics(m, *ref)
+            for q in range(4):
+                assert abs(d[q] - dref[q]) <= 1e-12 * abs(dref[q]) + 1e-300, (k, q, d[q], dref[q])
+
+
+def test_cfg2_1000_steps(ora):
+    p = pf.pf_default_params(2)
+    m, ic = oracle_member(ora, p, 0)
+    u0 = ora.initial_fields(ic, 256, 256, 0)
+    with _sim(p) as s:
+        s.step(1000)
+        e = normwise(s.fields(0), ora.step(m, *u0, 1000))
+    assert e <= 1e-8, e
+
+
+def test_uniform_state_fixed_point_bitwise():
+    p = pf.pf_default_params(1).replace(ic=pf.PF_IC_NONE, nx=40, ny=24, theta_deg=70.0)
+    with _sim(p) as s:
+        c = np.full((24, 40), 0.37); phi = np.full((24, 40), 0.81); rho = np.full((24, 40), p.rho_in)
+        s.set_fields(0, c, phi, rho)
+        s.step(7)
+        g = s.fields(0)
+    assert np.array_equal(g[0], c) and np.array_equal(g[1], phi) and np.array_equal(g[2], rho)
