@@ -14,6 +14,7 @@ namespace pf {
 struct Layout {
     int nx, ny, ny_loc, y0;      // global grid, owned rows, first owned global row
     int members;
+    int path;                    // stage kernel: 0 auto (streaming when eligible), 1 tile, 2 streaming
     int64_t fstride;             // elements per field  = (ny_loc + 4) * nx
     int64_t mstride;             // elements per member = 3 * fstride
 };

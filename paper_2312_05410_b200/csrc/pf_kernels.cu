@@ -13,6 +13,7 @@
 #include <cmath>
 #include <cstdint>
 
+#include "pf_cell.cuh"
 #include "pf_internal.h"
 
 namespace pf {
@@ -21,19 +22,6 @@ namespace {
 constexpr int BX = 32;   // tile width  (one warp across x)
 constexpr int BY = 16;   // tile height
 constexpr int NT = 256;  // threads per block (32 x 8)
-
-template <typename real>
-struct KC {                    // coefficients in the compute precision
-    real half_inv_dx2, inv_2dx, kc_dx2, kp_dx2, W_c, W2c, W2p;
-    real MBb, dMb, MBs, dMs, inv_sigma, Mp_dx2, Dr_dx2, rho_in, coef;
-};
-
-template <typename real>
-__device__ __forceinline__ real dexp(real x);
-template <>
-__device__ __forceinline__ double dexp<double>(double x) { return exp(x); }
-template <>
-__device__ __forceinline__ float dexp<float>(float x) { return expf(x); }
 
 // Local storage row (relative to owned row 0) holding the c/phi value of local row ly,
 // after the global mirror rule (R-12).  Clamped so that rows no output depends on stay
@@ -51,32 +39,6 @@ __device__ __forceinline__ int row_cphi(int ly, const Layout &L) {
 __device__ __forceinline__ int wrap_x(int gx, int nx) {
     gx += nx;               // gx >= -2 and nx >= 8
     return gx % nx;
-}
-
-// Cell-centre constitutive pass (a2): mu_c, mu_phi and M_c of one cell from its value and
-// its 4 neighbours.  Sum orders are fixed (the same code for every cell).
-template <typename real>
-__device__ __forceinline__ void constitutive(const KC<real> &k, real c, real p, real cl, real cr,
-                                             real cd, real cu, real pl, real pr, real pd, real pu,
-                                             real &mu_c, real &mu_p, real &M) {
-    const real lc = ((cl + cr) + (cd + cu)) - real(4) * c;   // dx^2 L(c)
-    const real lp = ((pl + pr) + (pd + pu)) - real(4) * p;   // dx^2 L(phi)
-    const real omc = real(1) - c;
-    const real c1 = c * omc;                                 // c(1-c)
-    // mu_c = 2 W_c c(1-c)(1-2c) phi - kappa_c L(c)                        (R-2, R-4)
-    mu_c = k.W2c * c1 * (real(1) - real(2) * c) * p - k.kc_dx2 * lc;
-    // mu_phi = W_c c^2(1-c)^2 + 2 W_phi phi(1-phi)(1-2phi) - kappa_phi L(phi)   (R-3)
-    mu_p = k.W_c * (c1 * c1) + k.W2p * (p * (real(1) - p)) * (real(1) - real(2) * p) - k.kp_dx2 * lp;
-    // mobility (R-5, R-6)
-    real ch = c < real(0) ? real(0) : c;
-    ch = ch > real(1) ? real(1) : ch;
-    const real h = ch * ch * (real(3) - real(2) * ch);
-    const real pp = p * p * (real(3) - real(2) * p);         // 1/4 (2-phit)(1+phit)^2
-    const real q = (real(2) * p - real(1)) * k.inv_sigma;
-    const real e = dexp<real>(-(q * q));
-    const real mb = pp * (k.MBb + h * k.dMb);
-    const real ms = k.MBs + h * k.dMs;
-    M = mb + e * (ms - mb);
 }
 
 template <typename real>
@@ -156,32 +118,18 @@ __global__ void __launch_bounds__(NT) stage_kernel(Layout L, KC<real> k, const r
         const int ly = ty0 + q;
         if (gx >= nx || ly >= L.ny_loc) continue;
         const int y = q + 1, x = lx + 1;                    // ring coordinates
-        // R_c: conservative divergence of the face fluxes (M_a + M_b)/2 (mu_b - mu_a)/dx^2
-        const real M0 = sM[y][x], m0 = smc[y][x];
-        const real fe = (M0 + sM[y][x + 1]) * (smc[y][x + 1] - m0);
-        const real fw = (sM[y][x - 1] + M0) * (m0 - smc[y][x - 1]);
-        const real fn = (M0 + sM[y + 1][x]) * (smc[y + 1][x] - m0);
-        const real fs = (sM[y - 1][x] + M0) * (m0 - smc[y - 1][x]);
-        const real Rc = ((fe - fw) + (fn - fs)) * k.half_inv_dx2;
-        // R_phi = M_phi L(mu_phi) + S
-        const real lmp = ((smp[y][x - 1] + smp[y][x + 1]) + (smp[y - 1][x] + smp[y + 1][x])) -
-                         real(4) * smp[y][x];
-        const real r0 = sr[y][x];
         const int cy = q + 2, cx = lx + 2;                   // c/phi tile coordinates
-        const real S = r0 * ((vx * (sp[cy][cx + 1] - sp[cy][cx - 1]) +
-                              vy * (sp[cy + 1][cx] - sp[cy - 1][cx])) * k.inv_2dx);
-        const real Rp = k.Mp_dx2 * lmp + S;
-        // R_rho = D_rho L(rho) - v . G(rho) - S
-        const real rl = sr[y][x - 1], rr = sr[y][x + 1], rd = sr[y - 1][x], ru = sr[y + 1][x];
-        const real lr = ((rl + rr) + (rd + ru)) - real(4) * r0;
-        const real adv = (vx * (rr - rl) + vy * (ru - rd)) * k.inv_2dx;
-        const real Rr = (k.Dr_dx2 * lr - adv) - S;
-
         const int64_t o = m * L.mstride + row0 + (int64_t)ly * nx + gx;
-        const real bc = base[o], bp = base[o + L.fstride], br = base[o + 2 * L.fstride];
-        out[o] = bc + k.coef * Rc;
-        out[o + L.fstride] = bp + k.coef * Rp;
-        out[o + 2 * L.fstride] = br + k.coef * Rr;
+        real oc, op, orr;
+        cell_update<real>(k, vx, vy, sM[y][x], sM[y][x - 1], sM[y][x + 1], sM[y - 1][x], sM[y + 1][x],
+                          smc[y][x], smc[y][x - 1], smc[y][x + 1], smc[y - 1][x], smc[y + 1][x],
+                          smp[y][x], smp[y][x - 1], smp[y][x + 1], smp[y - 1][x], smp[y + 1][x],
+                          sp[cy][cx - 1], sp[cy][cx + 1], sp[cy - 1][cx], sp[cy + 1][cx],
+                          sr[y][x], sr[y][x - 1], sr[y][x + 1], sr[y - 1][x], sr[y + 1][x],
+                          base[o], base[o + L.fstride], base[o + 2 * L.fstride], oc, op, orr);
+        out[o] = oc;
+        out[o + L.fstride] = op;
+        out[o + 2 * L.fstride] = orr;
     }
 }
 
@@ -293,6 +241,210 @@ __global__ void unpack_kernel(Layout L, int field, int member0, int nmem, const 
     }
 }
 
+
+// ----------------------------------------------------------------------------------------
+// Streaming stage kernel (the performance path).
+//
+// A persistent grid (one resident wave) walks the work in y.  The work is the concatenation of
+// all (member, x-strip) columns of W cells, each ny_loc rows tall; block b owns the contiguous
+// row range [R b / B, R (b+1) / B) of that concatenation, so every block gets the same number of
+// rows (+-1) and only pays the halo prologue at its 1-2 segment starts.
+//
+// Rows arrive through a TMA bulk-copy ring (cp.async.bulk global -> shared, completion on an
+// mbarrier per slot, S slots, issued S-3 rows ahead by thread 0).  Load k of a segment carries
+// c/phi row k (+-HL halo columns, x wrap by separate copies), rho row k-1 and, for stage 2, the
+// base row k-2.  Each thread owns one column: it keeps a sliding register window of its own
+// column and takes x-neighbours from shared memory.  Per row: mu/M of row k-1 (own column plus
+// two halo columns) -> smem, one __syncthreads, then the update of row k-2 and its coalesced
+// store.  The arithmetic per cell is pf_cell.cuh's, the same as the tile kernel's.
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+template <typename real, int W, int S>
+struct StreamCfg {
+    static constexpr int HL = 16 / (int)sizeof(real);   // halo columns loaded (one 16 B chunk)
+    static constexpr int RW = W + 2 * HL;               // smem row width incl. halo
+    static constexpr int SLOT = 3 * RW + 3 * W;         // c, phi, rho rows + base c, phi, rho
+    static constexpr int MUW = W + 2;                   // mu / M rows with 1 halo column
+    static constexpr size_t bytes =
+        (size_t)S * SLOT * sizeof(real) + (size_t)9 * MUW * sizeof(real) + (size_t)S * 8;
+};
+
+template <typename real, int W, int S>
+__global__ void __launch_bounds__(W) stream_kernel(Layout L, KC<real> k, const real *__restrict__ in,
+                                                   const real *__restrict__ base, real *out,
+                                                   const real *__restrict__ vel, int has_base) {
+    using Cfg = StreamCfg<real, W, S>;
+    constexpr int HL = Cfg::HL, RW = Cfg::RW, SLOT = Cfg::SLOT, MUW = Cfg::MUW;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    real *slots = reinterpret_cast<real *>(smem_raw);
+    real *mus = slots + S * SLOT;                                  // [3 rows][mu_c, mu_phi, M][MUW]
+    uint64_t *bars = reinterpret_cast<uint64_t *>(mus + 9 * MUW);
+
+    const int t = threadIdx.x;
+    if (t == 0) {
+        for (int q = 0; q < S; ++q) mbar_init(&bars[q], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    const int nx = L.nx, nyl = L.ny_loc;
+    const int strips = (nx + W - 1) / W;
+    const int64_t R = (int64_t)L.members * strips * nyl;
+    const int64_t lo = R * blockIdx.x / gridDim.x, hi = R * (blockIdx.x + 1) / gridDim.x;
+    uint32_t seq = 0;   // loads consumed before the current segment (identical in all threads)
+
+    for (int64_t pos = lo; pos < hi;) {
+        const int64_t col = pos / nyl;
+        const int ya = (int)(pos - col * nyl);
+        const int yb = (int)min((int64_t)nyl, (int64_t)ya + (hi - pos));
+        pos += yb - ya;
+        const int m = (int)(col / strips), sidx = (int)(col - (int64_t)m * strips);
+        const int x0 = sidx * W, Wp = min(W, nx - x0);
+        const int n = yb - ya + 4;                           // loads k = ya-2 .. yb+1
+        const real *fin = in + m * L.mstride + 2 * (int64_t)nx;
+        const real *fba = base + m * L.mstride + 2 * (int64_t)nx;
+        real *fout = out + m * L.mstride + 2 * (int64_t)nx;
+        const real vx = vel[2 * m], vy = vel[2 * m + 1];
+
+        // producer: load i of this segment into slot (seq + i) % S
+        auto issue = [&](int i) {
+            const int kk = ya - 2 + i;
+            const uint32_t g = seq + (uint32_t)i;
+            uint64_t *bar = &bars[g % S];
+            real *sl = slots + (g % S) * SLOT;
+            const int rc = row_cphi(kk, L);                   // c/phi source row (mirror rule)
+            int grho = L.y0 + kk - 1;
+            const bool rho_res = grho >= L.ny;                // reservoir row: no copy (rho_in)
+            if (grho < 0) grho = -1 - grho;
+            const int rr = grho - L.y0;
+            const bool wb = has_base && (kk - 2 >= ya) && (kk - 2 < yb);
+            const uint32_t rowb = (uint32_t)((Wp + 2 * HL) * sizeof(real));
+            const uint32_t bb = (uint32_t)(Wp * sizeof(real));
+            mbar_expect_tx(bar, (rho_res ? 2u : 3u) * rowb + (wb ? 3u * bb : 0u));
+            const bool wrapl = (x0 == 0), wrapr = (x0 + Wp == nx);
+            for (int f = 0; f < 3; ++f) {
+                if (f == 2 && rho_res) continue;
+                const real *row = fin + f * L.fstride + (int64_t)(f == 2 ? rr : rc) * nx;
+                real *d = sl + f * RW;
+                if (!wrapl && !wrapr) {
+                    bulk_g2s(d, row + x0 - HL, rowb, bar);
+                } else {
+                    bulk_g2s(d, row + (wrapl ? nx - HL : x0 - HL), HL * sizeof(real), bar);
+                    bulk_g2s(d + HL, row + x0, bb, bar);
+                    bulk_g2s(d + HL + Wp, row + (wrapr ? 0 : x0 + Wp), HL * sizeof(real), bar);
+                }
+            }
+            if (wb)
+                for (int f = 0; f < 3; ++f)
+                    bulk_g2s(sl + 3 * RW + f * W, fba + f * L.fstride + (int64_t)(kk - 2) * nx + x0, bb, bar);
+        };
+        if (t == 0)
+            for (int i = 0; i < min(S, n); ++i) issue(i);
+
+        // own-column sliding windows
+        real c_m2 = 0, c_m1 = 0, c_0 = 0;                 // c rows k-2, k-1, k
+        real p_m3 = 0, p_m2 = 0, p_m1 = 0, p_0 = 0;       // phi rows k-3 .. k
+        real r_m3 = 0, r_m2 = 0, r_m1 = 0;                // rho rows k-3 .. k-1
+        real a_m3 = 0, a_m2 = 0, a_m1 = 0;                // mu_c rows k-3 .. k-1
+        real b_m3 = 0, b_m2 = 0, b_m1 = 0;                // mu_phi rows k-3 .. k-1
+        real M_m3 = 0, M_m2 = 0, M_m1 = 0;                // M rows k-3 .. k-1
+        const int tc = t < Wp ? t : Wp - 1;               // idle threads shadow the last column
+
+        for (int i = 0; i < n; ++i) {
+            const int kk = ya - 2 + i;
+            const uint32_t g = seq + (uint32_t)i;
+            mbar_wait(&bars[g % S], (g / S) & 1u);
+            const real *s0 = slots + (g % S) * SLOT;                 // load k
+            const real *s1 = slots + ((g + S - 1) % S) * SLOT;       // load k-1
+            const real *s2 = slots + ((g + S - 2) % S) * SLOT;       // load k-2
+            c_m2 = c_m1; c_m1 = c_0; c_0 = s0[HL + tc];
+            p_m3 = p_m2; p_m2 = p_m1; p_m1 = p_0; p_0 = s0[RW + HL + tc];
+            r_m3 = r_m2; r_m2 = r_m1;
+            r_m1 = (L.y0 + kk - 1 >= L.ny) ? k.rho_in : s0[2 * RW + HL + tc];
+            a_m3 = a_m2; a_m2 = a_m1;
+            b_m3 = b_m2; b_m2 = b_m1;
+            M_m3 = M_m2; M_m2 = M_m1;
+            if (i >= 2) {   // mu / M of row k-1 -> smem row (i-1) % 3
+                real *mrow = mus + ((i - 1) % 3) * 3 * MUW;
+                const real *c1 = s1, *p1 = s1 + RW;
+                constitutive<real>(k, c_m1, p_m1, c1[HL + tc - 1], c1[HL + tc + 1], c_m2, c_0, p1[HL + tc - 1],
+                                   p1[HL + tc + 1], p_m2, p_0, a_m1, b_m1, M_m1);
+                if (t < Wp) {
+                    mrow[1 + t] = a_m1;
+                    mrow[MUW + 1 + t] = b_m1;
+                    mrow[2 * MUW + 1 + t] = M_m1;
+                }
+                if (t == 0 || t == Wp - 1) {   // halo columns x0-1 and x0+Wp (all inputs from smem)
+                    const int j = (t == 0) ? HL - 1 : HL + Wp;
+                    real a, b, M;
+                    constitutive<real>(k, c1[j], p1[j], c1[j - 1], c1[j + 1], s2[j], s0[j], p1[j - 1], p1[j + 1],
+                                       s2[RW + j], s0[RW + j], a, b, M);
+                    const int o = (t == 0) ? 0 : 1 + Wp;
+                    mrow[o] = a;
+                    mrow[MUW + o] = b;
+                    mrow[2 * MUW + o] = M;
+                }
+            }
+            __syncthreads();
+            if (t == 0 && i >= 3 && i + S - 3 < n) issue(i + S - 3);
+            if (i >= 4 && t < Wp) {   // update of row k-2
+                const real *mrow = mus + ((i - 2) % 3) * 3 * MUW;   // mu/M row k-2
+                const real *p2 = s2 + RW;                            // phi row k-2
+                const real *r1 = s1 + 2 * RW;                        // rho row k-2
+                const real *bs = s0 + 3 * RW;                        // base row k-2
+                real bc, bp, br;
+                if (has_base) {
+                    bc = bs[t]; bp = bs[W + t]; br = bs[2 * W + t];
+                } else {
+                    bc = c_m2; bp = p_m2; br = r_m2;   // stage 1: base = input
+                }
+                real oc, op, orr;
+                cell_update<real>(k, vx, vy, M_m2, mrow[2 * MUW + t], mrow[2 * MUW + t + 2], M_m3, M_m1,
+                                  a_m2, mrow[t], mrow[t + 2], a_m3, a_m1,
+                                  b_m2, mrow[MUW + t], mrow[MUW + t + 2], b_m3, b_m1,
+                                  p2[HL + t - 1], p2[HL + t + 1], p_m3, p_m1,
+                                  r_m2, r1[HL + t - 1], r1[HL + t + 1], r_m3, r_m1,
+                                  bc, bp, br, oc, op, orr);
+                real *o = fout + (int64_t)(kk - 2) * nx + x0 + t;
+                o[0] = oc;
+                o[L.fstride] = op;
+                o[2 * L.fstride] = orr;
+            }
+        }
+        seq += (uint32_t)n;
+        __syncthreads();   // every slot is free before the next segment's prologue
+    }
+}
+
 template <typename real>
 KC<real> make_kc(const Coef &K, double coef) {
     KC<real> k;
@@ -317,8 +469,54 @@ KC<real> make_kc(const Coef &K, double coef) {
 
 }  // namespace
 
+template <typename real, int W, int S>
+cudaError_t launch_stream_t(const Layout &L, const KC<real> &k, const real *in, const real *base,
+                            real *out, const real *vel, int has_base, cudaStream_t s) {
+    using Cfg = StreamCfg<real, W, S>;
+    static int occ = -1, nsm = 0;
+    if (occ < 0) {
+        cudaError_t e = cudaFuncSetAttribute(stream_kernel<real, W, S>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::bytes);
+        if (e != cudaSuccess) return e;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stream_kernel<real, W, S>, W, Cfg::bytes);
+        if (e != cudaSuccess) return e;
+        if (occ < 1) occ = 1;
+    }
+    const int strips = (L.nx + W - 1) / W;
+    const int64_t R = (int64_t)L.members * strips * L.ny_loc;
+    int64_t B = (int64_t)occ * nsm;
+    const int64_t minrows = 16;
+    if (B > (R + minrows - 1) / minrows) B = (R + minrows - 1) / minrows;
+    if (B < 1) B = 1;
+    stream_kernel<real, W, S><<<(unsigned)B, W, Cfg::bytes, s>>>(L, k, in, base, out, vel, has_base);
+    return cudaGetLastError();
+}
+
+bool stream_eligible(const Layout &L) { return L.nx % 4 == 0 && L.nx >= 64; }
+
+template <typename real, int S>
+cudaError_t launch_stream(const Layout &L, const KC<real> &k, const real *in, const real *base, real *out,
+                          const real *vel, int has_base, cudaStream_t s) {
+    if (L.nx >= 256) return launch_stream_t<real, 256, S>(L, k, in, base, out, vel, has_base, s);
+    if (L.nx >= 128) return launch_stream_t<real, 128, S>(L, k, in, base, out, vel, has_base, s);
+    return launch_stream_t<real, 64, S>(L, k, in, base, out, vel, has_base, s);
+}
+
 cudaError_t launch_stage(int precision, const Layout &L, const Coef &K, const void *in,
                          const void *base, void *out, const void *vel, double coef, cudaStream_t s) {
+    const bool has_base = base != in;
+    const bool stream = L.path != 1 && stream_eligible(L);
+    if (stream) {
+        if (precision == 0)
+            return launch_stream<double, 6>(L, make_kc<double>(K, coef), (const double *)in,
+                                            (const double *)base, (double *)out, (const double *)vel,
+                                            has_base, s);
+        return launch_stream<float, 8>(L, make_kc<float>(K, coef), (const float *)in, (const float *)base,
+                                       (float *)out, (const float *)vel, has_base, s);
+    }
     dim3 grid((L.nx + BX - 1) / BX, (L.ny_loc + BY - 1) / BY, L.members);
     if (precision == 0)
         stage_kernel<double><<<grid, NT, 0, s>>>(L, make_kc<double>(K, coef), (const double *)in,

@@ -41,6 +41,7 @@ class pf_params(C.Structure):
         ("noise_c", C.c_double), ("noise_phi", C.c_double),
         ("noise_c_gaussian", C.c_int32), ("check_every", C.c_int32),
         ("seed", C.c_uint64), ("device", C.c_int32), ("graph_steps", C.c_int32),
+        ("kernel_path", C.c_int32),
     ]
 
     def as_dict(self):

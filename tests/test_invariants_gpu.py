@@ -1,0 +1,143 @@
+"""GPU-only invariants of the CUDA path (bitwise): kernel paths agree, x-translation equivariance,
+ensemble member == single run, run-to-run determinism, resume == straight run, loopback y-slabs ==
+single domain, CUDA graphs == direct launches; blow-up detection."""
+import numpy as np
+import pytest
+
+from paper_2312_05410_b200 import pf
+from tests import inputs
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    pf.lib()
+
+
+def _base(nx=96, ny=48, **kw):
+    p = pf.pf_default_params(2).replace(nx=nx, ny=ny, ic_height=ny / 4, graph_steps=0, seed=21,
+                                       theta_deg=71.0, M_A_bulk=12.0, M_B_bulk=6.0, M_A_surf=9.0,
+                                       M_B_surf=3.0)
+    return p.replace(**kw)
+
+
+def _run(p, n, mode="single", init=None):
+    with pf.Simulation(p, mode) as s:
+        if init is not None:
+            for m, u in enumerate(init):
+                s.set_fields(m, *u)
+        s.step(n)
+        return [s.fields(m) for m in range(p.n_members)]
+
+
+def _eq(a, b):
+    return all(np.array_equal(x, y) for x, y in zip(a, b))
+
+
+@pytest.mark.parametrize("nx,ny,members", [(64, 64, 1), (96, 48, 2), (260, 40, 1), (512, 72, 2)])
+def test_tile_and_stream_paths_bitwise(nx, ny, members):
+    p = _base(nx, ny, n_members=members, rate_lo=0.5, rate_hi=2.0)
+    a = _run(p.replace(kernel_path=1), 20)
+    b = _run(p.replace(kernel_path=2), 20)
+    for m in range(members):
+        assert _eq(a[m], b[m]), m
+
+
+@pytest.mark.parametrize("shift", [64, 5, 1])
+def test_x_translation_equivariance(shift):
+    nx, ny = 256, 40
+    p = _base(nx, ny, ic=pf.PF_IC_NONE)
+    u = inputs.random_state(nx, ny, 5, phi_kind="smooth")
+    a = _run(p, 15, init=[u])[0]
+    us = [np.roll(f, shift, axis=1) for f in u]
+    b = _run(p, 15, init=[us])[0]
+    for fa, fb in zip(a, b):
+        assert np.array_equal(np.roll(fa, shift, axis=1), fb)
+
+
+def test_member_equals_single_run():
+    p = _base(128, 40, n_members=4, rate_lo=0.5, rate_hi=2.0)
+    ens = _run(p, 12)
+    for m in (0, 3):
+        single = _run(p.replace(n_members=1, member_offset=m), 12)[0]
+        assert _eq(ens[m], single), m
+
+
+def test_run_to_run_determinism_and_diagnostics():
+    p = _base(192, 64, n_members=2)
+    with pf.Simulation(p) as s1, pf.Simulation(p) as s2:
+        s1.step(30); s2.step(30)
+        for m in range(2):
+            assert _eq(s1.fields(m), s2.fields(m))
+            assert np.array_equal(s1.diagnostics(m), s2.diagnostics(m))
+
+
+def test_resume_equals_straight_run():
+    p = _base(128, 48)
+    straight = _run(p, 40)[0]
+    with pf.Simulation(p) as s:
+        s.step(17)
+        u = s.fields(0)
+        st, t, _, _ = s.info()
+    with pf.Simulation(p.replace(ic=pf.PF_IC_NONE)) as s:
+        s.set_fields(0, *u)
+        pf.pf_set_time(s.ctx, st, t)
+        s.step(23)
+        assert _eq(s.fields(0), straight)
+        assert s.info()[0] == 40
+
+
+@pytest.mark.parametrize("nslabs,path", [(2, 0), (4, 0), (4, 1), (8, 0)])
+def test_loopback_slabs_equal_single_domain(nslabs, path):
+    """The y-slab decomposition (2-row halo exchanged after every stage) is bitwise invisible."""
+    p = _base(128, 64, n_members=2, kernel_path=path)
+    a = _run(p, 25)
+    b = _run(p, 25, mode=("loopback", nslabs))
+    for m in range(2):
+        assert _eq(a[m], b[m]), m
+    with pf.Simulation(p, ("loopback", nslabs)) as s:
+        s.step(3)
+        d = s.diagnostics(1)
+    with pf.Simulation(p) as s:
+        s.step(3)
+        d1 = s.diagnostics(1)
+    np.testing.assert_allclose(d, d1, rtol=1e-12, atol=0)
+
+
+def test_graphs_equal_direct_launches():
+    p = _base(128, 48)
+    a = _run(p.replace(graph_steps=0), 60)[0]
+    b = _run(p.replace(graph_steps=16), 60)[0]
+    assert _eq(a, b)
+
+
+def test_blowup_detected_and_cleared():
+    p = _base(64, 32, check_every=5)
+    with pf.Simulation(p) as s:
+        c, phi, rho = s.fields(0)
+        phi[10, 7] = np.nan
+        s.set_fields(0, c, phi, rho)
+        with pytest.raises(pf.PfError) as e:
+            s.step(12)
+        assert e.value.status == pf.PF_ERR_BLOWUP
+        assert "phi" in str(e.value) and "(0, 5]" in str(e.value)
+        with pytest.raises(pf.PfError) as e:
+            s.step(1)
+        assert e.value.status == pf.PF_ERR_STATE
+        c2, phi2, rho2 = _run(p, 0)[0]
+        s.set_fields(0, c2, phi2, rho2)
+        s.step(3)
+        assert np.all(np.isfinite(s.fields(0)[1]))
+
+
+def test_get_set_roundtrip_all_members():
+    p = _base(128, 32, n_members=3)
+    with pf.Simulation(p) as s:
+        c, phi, rho = s.fields(-1)
+        assert c.shape == (3, 32, 128)
+        s.set_fields(-1, c[::-1].copy(), phi[::-1].copy(), rho[::-1].copy())
+        c2, _, _ = s.fields(-1)
+        assert np.array_equal(c2, c[::-1])
