@@ -72,7 +72,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if f.endswith(".cu"):
             obj = os.path.join(BUILD, f[:-3] + ".o")
             _run([os.path.join(CUDA, "bin", "nvcc"), *ARCH, "-O3", "-lineinfo", "-std=c++17",
-                  "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr",
+                  "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr", "-fmad=false",
                   *incs, "-c", src, "-o", obj], verbose)
             objs.append(obj)
         elif f.endswith(".cpp"):

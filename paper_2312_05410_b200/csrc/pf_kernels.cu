@@ -12,6 +12,7 @@
 // so results are bitwise independent of tiling, x-translation and slab decomposition.
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 
 #include "pf_cell.cuh"
 #include "pf_internal.h"
@@ -295,153 +296,224 @@ struct StreamCfg {
     static constexpr int SLOT = 3 * RW + 3 * W;         // c, phi, rho rows + base c, phi, rho
     static constexpr int MUW = W + 2;                   // mu / M rows with 1 halo column
     static constexpr size_t bytes =
-        (size_t)S * SLOT * sizeof(real) + (size_t)9 * MUW * sizeof(real) + (size_t)S * 8;
+        (size_t)S * SLOT * sizeof(real) + (size_t)9 * MUW * sizeof(real) + (size_t)S * 16;
 };
 
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void named_sync(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// Segment enumeration shared by the producer and the compute warps.
+struct Seg {
+    int m, x0, Wp, ya, yb;
+};
+template <int W>
+__device__ __forceinline__ bool next_seg(const Layout &L, int64_t &pos, int64_t hi, Seg &sg) {
+    if (pos >= hi) return false;
+    const int nyl = L.ny_loc, strips = (L.nx + W - 1) / W;
+    const int64_t col = pos / nyl;
+    sg.ya = (int)(pos - col * nyl);
+    sg.yb = (int)min((int64_t)nyl, (int64_t)sg.ya + (hi - pos));
+    pos += sg.yb - sg.ya;
+    sg.m = (int)(col / strips);
+    const int sidx = (int)(col - (int64_t)sg.m * strips);
+    sg.x0 = sidx * W;
+    sg.Wp = min(W, L.nx - sg.x0);
+    return true;
+}
+
 template <typename real, int W, int S>
-__global__ void __launch_bounds__(W) stream_kernel(Layout L, KC<real> k, const real *__restrict__ in,
-                                                   const real *__restrict__ base, real *out,
-                                                   const real *__restrict__ vel, int has_base) {
+__global__ void __launch_bounds__(W + 64, (W == 256 ? 2 : (W == 128 ? 3 : 5))) stream_kernel(Layout L, KC<real> k, const real *__restrict__ in,
+                                                        const real *__restrict__ base, real *out,
+                                                        const real *__restrict__ vel, int has_base) {
+    // Warp roles.  Threads [0, W): workers, one column each.  Warp W/32 (halo warp): lanes 0/1
+    // compute mu/M of the halo columns x0-1 / x0+Wp.  Warp W/32+1 (producer): lane 0 issues the
+    // TMA bulk copies, gated by per-slot "empty" mbarriers; it never joins the compute barrier.
+    // The row loop is unrolled by 3 (mu ring of 3 rows, compile-time) and computes
+    // unconditionally (only stores are predicated), so the register windows rotate by renaming.
+    // Segments are padded to a multiple of 3 loads with arrive-only (empty) loads.
     using Cfg = StreamCfg<real, W, S>;
     constexpr int HL = Cfg::HL, RW = Cfg::RW, SLOT = Cfg::SLOT, MUW = Cfg::MUW;
+    constexpr int NCW = W / 32 + 1;                 // compute warps (workers + halo warp)
     extern __shared__ __align__(128) unsigned char smem_raw[];
     real *slots = reinterpret_cast<real *>(smem_raw);
     real *mus = slots + S * SLOT;                                  // [3 rows][mu_c, mu_phi, M][MUW]
-    uint64_t *bars = reinterpret_cast<uint64_t *>(mus + 9 * MUW);
+    uint64_t *full = reinterpret_cast<uint64_t *>(mus + 9 * MUW);
+    uint64_t *empty = full + S;
 
     const int t = threadIdx.x;
+    const int warp = t >> 5, lane = t & 31;
     if (t == 0) {
-        for (int q = 0; q < S; ++q) mbar_init(&bars[q], 1);
+        for (int q = 0; q < S; ++q) {
+            mbar_init(&full[q], 1);
+            mbar_init(&empty[q], NCW);
+        }
         fence_mbar_init();
     }
     __syncthreads();
 
-    const int nx = L.nx, nyl = L.ny_loc;
+    const int nx = L.nx;
     const int strips = (nx + W - 1) / W;
-    const int64_t R = (int64_t)L.members * strips * nyl;
+    const int64_t R = (int64_t)L.members * strips * L.ny_loc;
     const int64_t lo = R * blockIdx.x / gridDim.x, hi = R * (blockIdx.x + 1) / gridDim.x;
-    uint32_t seq = 0;   // loads consumed before the current segment (identical in all threads)
 
-    for (int64_t pos = lo; pos < hi;) {
-        const int64_t col = pos / nyl;
-        const int ya = (int)(pos - col * nyl);
-        const int yb = (int)min((int64_t)nyl, (int64_t)ya + (hi - pos));
-        pos += yb - ya;
-        const int m = (int)(col / strips), sidx = (int)(col - (int64_t)m * strips);
-        const int x0 = sidx * W, Wp = min(W, nx - x0);
-        const int n = yb - ya + 4;                           // loads k = ya-2 .. yb+1
-        const real *fin = in + m * L.mstride + 2 * (int64_t)nx;
-        const real *fba = base + m * L.mstride + 2 * (int64_t)nx;
-        real *fout = out + m * L.mstride + 2 * (int64_t)nx;
-        const real vx = vel[2 * m], vy = vel[2 * m + 1];
-
-        // producer: load i of this segment into slot (seq + i) % S
-        auto issue = [&](int i) {
-            const int kk = ya - 2 + i;
-            const uint32_t g = seq + (uint32_t)i;
-            uint64_t *bar = &bars[g % S];
-            real *sl = slots + (g % S) * SLOT;
-            const int rc = row_cphi(kk, L);                   // c/phi source row (mirror rule)
-            int grho = L.y0 + kk - 1;
-            const bool rho_res = grho >= L.ny;                // reservoir row: no copy (rho_in)
-            if (grho < 0) grho = -1 - grho;
-            const int rr = grho - L.y0;
-            const bool wb = has_base && (kk - 2 >= ya) && (kk - 2 < yb);
-            const uint32_t rowb = (uint32_t)((Wp + 2 * HL) * sizeof(real));
-            const uint32_t bb = (uint32_t)(Wp * sizeof(real));
-            mbar_expect_tx(bar, (rho_res ? 2u : 3u) * rowb + (wb ? 3u * bb : 0u));
-            const bool wrapl = (x0 == 0), wrapr = (x0 + Wp == nx);
-            for (int f = 0; f < 3; ++f) {
-                if (f == 2 && rho_res) continue;
-                const real *row = fin + f * L.fstride + (int64_t)(f == 2 ? rr : rc) * nx;
-                real *d = sl + f * RW;
-                if (!wrapl && !wrapr) {
-                    bulk_g2s(d, row + x0 - HL, rowb, bar);
-                } else {
-                    bulk_g2s(d, row + (wrapl ? nx - HL : x0 - HL), HL * sizeof(real), bar);
-                    bulk_g2s(d + HL, row + x0, bb, bar);
-                    bulk_g2s(d + HL + Wp, row + (wrapr ? 0 : x0 + Wp), HL * sizeof(real), bar);
+    if (warp == NCW) {
+        // ------------------------------- producer -------------------------------
+        if (lane != 0) return;
+        uint32_t g = 0;
+        int64_t pos = lo;
+        Seg sg;
+        while (next_seg<W>(L, pos, hi, sg)) {
+            const int n = sg.yb - sg.ya + 4, npad = (n + 2) / 3 * 3;
+            const real *fin = in + sg.m * L.mstride + 2 * (int64_t)nx;
+            const real *fba = base + sg.m * L.mstride + 2 * (int64_t)nx;
+            const bool wrapl = (sg.x0 == 0), wrapr = (sg.x0 + sg.Wp == nx);
+            const uint32_t rowb = (uint32_t)((sg.Wp + 2 * HL) * sizeof(real));
+            const uint32_t bb = (uint32_t)(sg.Wp * sizeof(real));
+            for (int i = 0; i < npad; ++i, ++g) {
+                const int slot = g % S;
+                if (g >= (uint32_t)S) mbar_wait(&empty[slot], ((g / S) - 1) & 1u);
+                if (i >= n) {
+                    mbar_arrive(&full[slot]);          // padding: completes the phase, no data
+                    continue;
                 }
-            }
-            if (wb)
-                for (int f = 0; f < 3; ++f)
-                    bulk_g2s(sl + 3 * RW + f * W, fba + f * L.fstride + (int64_t)(kk - 2) * nx + x0, bb, bar);
-        };
-        if (t == 0)
-            for (int i = 0; i < min(S, n); ++i) issue(i);
-
-        // own-column sliding windows
-        real c_m2 = 0, c_m1 = 0, c_0 = 0;                 // c rows k-2, k-1, k
-        real p_m3 = 0, p_m2 = 0, p_m1 = 0, p_0 = 0;       // phi rows k-3 .. k
-        real r_m3 = 0, r_m2 = 0, r_m1 = 0;                // rho rows k-3 .. k-1
-        real a_m3 = 0, a_m2 = 0, a_m1 = 0;                // mu_c rows k-3 .. k-1
-        real b_m3 = 0, b_m2 = 0, b_m1 = 0;                // mu_phi rows k-3 .. k-1
-        real M_m3 = 0, M_m2 = 0, M_m1 = 0;                // M rows k-3 .. k-1
-        const int tc = t < Wp ? t : Wp - 1;               // idle threads shadow the last column
-
-        for (int i = 0; i < n; ++i) {
-            const int kk = ya - 2 + i;
-            const uint32_t g = seq + (uint32_t)i;
-            mbar_wait(&bars[g % S], (g / S) & 1u);
-            const real *s0 = slots + (g % S) * SLOT;                 // load k
-            const real *s1 = slots + ((g + S - 1) % S) * SLOT;       // load k-1
-            const real *s2 = slots + ((g + S - 2) % S) * SLOT;       // load k-2
-            c_m2 = c_m1; c_m1 = c_0; c_0 = s0[HL + tc];
-            p_m3 = p_m2; p_m2 = p_m1; p_m1 = p_0; p_0 = s0[RW + HL + tc];
-            r_m3 = r_m2; r_m2 = r_m1;
-            r_m1 = (L.y0 + kk - 1 >= L.ny) ? k.rho_in : s0[2 * RW + HL + tc];
-            a_m3 = a_m2; a_m2 = a_m1;
-            b_m3 = b_m2; b_m2 = b_m1;
-            M_m3 = M_m2; M_m2 = M_m1;
-            if (i >= 2) {   // mu / M of row k-1 -> smem row (i-1) % 3
-                real *mrow = mus + ((i - 1) % 3) * 3 * MUW;
-                const real *c1 = s1, *p1 = s1 + RW;
-                constitutive<real>(k, c_m1, p_m1, c1[HL + tc - 1], c1[HL + tc + 1], c_m2, c_0, p1[HL + tc - 1],
-                                   p1[HL + tc + 1], p_m2, p_0, a_m1, b_m1, M_m1);
-                if (t < Wp) {
-                    mrow[1 + t] = a_m1;
-                    mrow[MUW + 1 + t] = b_m1;
-                    mrow[2 * MUW + 1 + t] = M_m1;
+                const int kk = sg.ya - 2 + i;
+                real *sl = slots + slot * SLOT;
+                const int rc = row_cphi(kk, L);                   // c/phi source row (mirror rule)
+                int grho = L.y0 + kk - 1;
+                const bool rho_res = grho >= L.ny;                // reservoir row: rho_in, no copy
+                if (grho < 0) grho = -1 - grho;
+                const int rr = grho - L.y0;
+                const bool wb = has_base && (kk - 2 >= sg.ya) && (kk - 2 < sg.yb);
+                mbar_expect_tx(&full[slot], (rho_res ? 2u : 3u) * rowb + (wb ? 3u * bb : 0u));
+                for (int f = 0; f < 3; ++f) {
+                    if (f == 2 && rho_res) continue;
+                    const real *row = fin + f * L.fstride + (int64_t)(f == 2 ? rr : rc) * nx;
+                    real *d = sl + f * RW;
+                    if (!wrapl && !wrapr) {
+                        bulk_g2s(d, row + sg.x0 - HL, rowb, &full[slot]);
+                    } else {
+                        bulk_g2s(d, row + (wrapl ? nx - HL : sg.x0 - HL), HL * sizeof(real), &full[slot]);
+                        bulk_g2s(d + HL, row + sg.x0, bb, &full[slot]);
+                        bulk_g2s(d + HL + sg.Wp, row + (wrapr ? 0 : sg.x0 + sg.Wp), HL * sizeof(real), &full[slot]);
+                    }
                 }
-                if (t == 0 || t == Wp - 1) {   // halo columns x0-1 and x0+Wp (all inputs from smem)
-                    const int j = (t == 0) ? HL - 1 : HL + Wp;
-                    real a, b, M;
-                    constitutive<real>(k, c1[j], p1[j], c1[j - 1], c1[j + 1], s2[j], s0[j], p1[j - 1], p1[j + 1],
-                                       s2[RW + j], s0[RW + j], a, b, M);
-                    const int o = (t == 0) ? 0 : 1 + Wp;
-                    mrow[o] = a;
-                    mrow[MUW + o] = b;
-                    mrow[2 * MUW + o] = M;
-                }
-            }
-            __syncthreads();
-            if (t == 0 && i >= 3 && i + S - 3 < n) issue(i + S - 3);
-            if (i >= 4 && t < Wp) {   // update of row k-2
-                const real *mrow = mus + ((i - 2) % 3) * 3 * MUW;   // mu/M row k-2
-                const real *p2 = s2 + RW;                            // phi row k-2
-                const real *r1 = s1 + 2 * RW;                        // rho row k-2
-                const real *bs = s0 + 3 * RW;                        // base row k-2
-                real bc, bp, br;
-                if (has_base) {
-                    bc = bs[t]; bp = bs[W + t]; br = bs[2 * W + t];
-                } else {
-                    bc = c_m2; bp = p_m2; br = r_m2;   // stage 1: base = input
-                }
-                real oc, op, orr;
-                cell_update<real>(k, vx, vy, M_m2, mrow[2 * MUW + t], mrow[2 * MUW + t + 2], M_m3, M_m1,
-                                  a_m2, mrow[t], mrow[t + 2], a_m3, a_m1,
-                                  b_m2, mrow[MUW + t], mrow[MUW + t + 2], b_m3, b_m1,
-                                  p2[HL + t - 1], p2[HL + t + 1], p_m3, p_m1,
-                                  r_m2, r1[HL + t - 1], r1[HL + t + 1], r_m3, r_m1,
-                                  bc, bp, br, oc, op, orr);
-                real *o = fout + (int64_t)(kk - 2) * nx + x0 + t;
-                o[0] = oc;
-                o[L.fstride] = op;
-                o[2 * L.fstride] = orr;
+                if (wb)
+                    for (int f = 0; f < 3; ++f)
+                        bulk_g2s(sl + 3 * RW + f * W, fba + f * L.fstride + (int64_t)(kk - 2) * nx + sg.x0, bb,
+                                 &full[slot]);
             }
         }
-        seq += (uint32_t)n;
-        __syncthreads();   // every slot is free before the next segment's prologue
+        return;
+    }
+
+    // --------------------------- compute warps ---------------------------------
+    const bool halo = warp == NCW - 1;
+    int sidx = 0;                           // ring slot of the current load
+    uint32_t par = 0;                       // its full-barrier phase parity
+    int64_t pos = lo;
+    Seg sg;
+    while (next_seg<W>(L, pos, hi, sg)) {
+        const int n = sg.yb - sg.ya + 4, npad = (n + 2) / 3 * 3;
+        const int Wp = sg.Wp;
+        if (halo) {
+            // lanes 0 / 1: mu/M of the halo columns x0-1 / x0+Wp of row k-1
+            const int j = (lane == 0) ? HL - 1 : HL + Wp;
+            const int o = (lane == 0) ? 0 : 1 + Wp;
+            const bool st = lane < 2;
+            for (int i0 = 0; i0 < npad; i0 += 3) {
+#pragma unroll
+                for (int u = 0; u < 3; ++u) {
+                    const int i = i0 + u;
+                    mbar_wait(&full[sidx], par);
+                    const real *s0 = slots + sidx * SLOT;
+                    const real *s1 = slots + (sidx == 0 ? S - 1 : sidx - 1) * SLOT;
+                    const real *s2 = slots + (sidx >= 2 ? sidx - 2 : sidx + S - 2) * SLOT;
+                    real *mrow_w = mus + ((u + 2) % 3) * 3 * MUW;
+                    real a, b, M;
+                    constitutive<real>(k, s1[j], s1[RW + j], s1[j - 1], s1[j + 1], s2[j], s0[j], s1[RW + j - 1],
+                                       s1[RW + j + 1], s2[RW + j], s0[RW + j], a, b, M);
+                    if (st && i >= 2 && i < n) {
+                        mrow_w[o] = a;
+                        mrow_w[MUW + o] = b;
+                        mrow_w[2 * MUW + o] = M;
+                    }
+                    named_sync(1, NCW * 32);
+                    __syncwarp();
+                    if (i >= 2 && lane == 0) mbar_arrive(&empty[sidx >= 2 ? sidx - 2 : sidx + S - 2]);
+                    if (++sidx == S) { sidx = 0; par ^= 1u; }
+                }
+            }
+        } else {
+            const bool active = t < Wp;
+            const int tc = active ? t : 0;
+            real *orow = out + sg.m * L.mstride + 2 * (int64_t)nx + (int64_t)(sg.ya - 4) * nx + sg.x0 + tc;
+            const real vx = vel[2 * sg.m], vy = vel[2 * sg.m + 1];
+            const int rho_res_i = L.ny - L.y0 - sg.ya + 3;   // first load whose rho row is the reservoir
+
+            real c_m2 = 0, c_m1 = 0, c_0 = 0;                 // c rows k-2, k-1, k (own column)
+            real p_m3 = 0, p_m2 = 0, p_m1 = 0, p_0 = 0;       // phi rows k-3 .. k
+            real r_m3 = 0, r_m2 = 0, r_m1 = 0;                // rho rows k-3 .. k-1
+            real a_m3 = 0, a_m2 = 0, a_m1 = 0;                // mu_c rows k-3 .. k-1
+            real b_m3 = 0, b_m2 = 0, b_m1 = 0;                // mu_phi rows k-3 .. k-1
+            real M_m3 = 0, M_m2 = 0, M_m1 = 0;                // M rows k-3 .. k-1
+            for (int i0 = 0; i0 < npad; i0 += 3) {
+#pragma unroll
+                for (int u = 0; u < 3; ++u) {
+                    const int i = i0 + u;
+                    mbar_wait(&full[sidx], par);
+                    const real *s0 = slots + sidx * SLOT;                                   // load k
+                    const real *s1 = slots + (sidx == 0 ? S - 1 : sidx - 1) * SLOT;          // load k-1
+                    const real *s2 = slots + (sidx >= 2 ? sidx - 2 : sidx + S - 2) * SLOT;   // load k-2
+                    real *mrow_w = mus + ((u + 2) % 3) * 3 * MUW;                           // mu row k-1
+                    const real *mrow = mus + ((u + 1) % 3) * 3 * MUW;                       // mu row k-2
+                    c_m2 = c_m1; c_m1 = c_0; c_0 = s0[HL + tc];
+                    p_m3 = p_m2; p_m2 = p_m1; p_m1 = p_0; p_0 = s0[RW + HL + tc];
+                    r_m3 = r_m2; r_m2 = r_m1;
+                    r_m1 = (i >= rho_res_i) ? k.rho_in : s0[2 * RW + HL + tc];
+                    a_m3 = a_m2; a_m2 = a_m1;
+                    b_m3 = b_m2; b_m2 = b_m1;
+                    M_m3 = M_m2; M_m2 = M_m1;
+                    constitutive<real>(k, c_m1, p_m1, s1[HL + tc - 1], s1[HL + tc + 1], c_m2, c_0,
+                                       s1[RW + HL + tc - 1], s1[RW + HL + tc + 1], p_m2, p_0, a_m1, b_m1, M_m1);
+                    if (active && i >= 2 && i < n) {
+                        mrow_w[1 + t] = a_m1;
+                        mrow_w[MUW + 1 + t] = b_m1;
+                        mrow_w[2 * MUW + 1 + t] = M_m1;
+                    }
+                    named_sync(1, NCW * 32);
+                    // update of row k-2 (stage 1: base = input; stage 2: base row from the ring)
+                    const real *bs = s0 + 3 * RW;
+                    const real bc = has_base ? bs[tc] : c_m2;
+                    const real bp = has_base ? bs[W + tc] : p_m2;
+                    const real br = has_base ? bs[2 * W + tc] : r_m2;
+                    real oc, op, orr;
+                    cell_update<real>(k, vx, vy, M_m2, mrow[2 * MUW + tc], mrow[2 * MUW + tc + 2], M_m3, M_m1,
+                                      a_m2, mrow[tc], mrow[tc + 2], a_m3, a_m1,
+                                      b_m2, mrow[MUW + tc], mrow[MUW + tc + 2], b_m3, b_m1,
+                                      s2[RW + HL + tc - 1], s2[RW + HL + tc + 1], p_m3, p_m1,
+                                      r_m2, s1[2 * RW + HL + tc - 1], s1[2 * RW + HL + tc + 1], r_m3, r_m1,
+                                      bc, bp, br, oc, op, orr);
+                    if (active && i >= 4 && i < n) {
+                        real *o = orow + (int64_t)i * nx;
+                        o[0] = oc;
+                        o[L.fstride] = op;
+                        o[2 * L.fstride] = orr;
+                    }
+                    __syncwarp();
+                    if (i >= 2 && lane == 0) mbar_arrive(&empty[sidx >= 2 ? sidx - 2 : sidx + S - 2]);
+                    if (++sidx == S) { sidx = 0; par ^= 1u; }
+                }
+            }
+        }
+        // release the last two loads of the segment
+        if (lane == 0) {
+            mbar_arrive(&empty[sidx >= 2 ? sidx - 2 : sidx + S - 2]);
+            mbar_arrive(&empty[sidx >= 1 ? sidx - 1 : sidx + S - 1]);
+        }
     }
 }
 
@@ -481,7 +553,7 @@ cudaError_t launch_stream_t(const Layout &L, const KC<real> &k, const real *in, 
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stream_kernel<real, W, S>, W, Cfg::bytes);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stream_kernel<real, W, S>, W + 64, Cfg::bytes);
         if (e != cudaSuccess) return e;
         if (occ < 1) occ = 1;
     }
@@ -491,18 +563,32 @@ cudaError_t launch_stream_t(const Layout &L, const KC<real> &k, const real *in, 
     const int64_t minrows = 16;
     if (B > (R + minrows - 1) / minrows) B = (R + minrows - 1) / minrows;
     if (B < 1) B = 1;
-    stream_kernel<real, W, S><<<(unsigned)B, W, Cfg::bytes, s>>>(L, k, in, base, out, vel, has_base);
+    stream_kernel<real, W, S><<<(unsigned)B, W + 64, Cfg::bytes, s>>>(L, k, in, base, out, vel, has_base);
     return cudaGetLastError();
 }
 
 bool stream_eligible(const Layout &L) { return L.nx % 4 == 0 && L.nx >= 64; }
 
-template <typename real, int S>
+// Strip width W and ring depth S: W = 256 (nx >= 256), 128, 64; S = 6 (fp64) / 8 (fp32).
+// PF_STREAM_W / PF_STREAM_S override them (tuning experiments; read once).
+int env_int(const char *name, int dflt) {
+    const char *v = getenv(name);
+    return v ? atoi(v) : dflt;
+}
+
+template <typename real>
 cudaError_t launch_stream(const Layout &L, const KC<real> &k, const real *in, const real *base, real *out,
                           const real *vel, int has_base, cudaStream_t s) {
-    if (L.nx >= 256) return launch_stream_t<real, 256, S>(L, k, in, base, out, vel, has_base, s);
-    if (L.nx >= 128) return launch_stream_t<real, 128, S>(L, k, in, base, out, vel, has_base, s);
-    return launch_stream_t<real, 64, S>(L, k, in, base, out, vel, has_base, s);
+    static const int envW = env_int("PF_STREAM_W", 0), envS = env_int("PF_STREAM_S", 0);
+    int W = L.nx >= 256 ? 256 : (L.nx >= 128 ? 128 : 64);
+    if (envW && envW <= L.nx) W = envW;
+    int S = envS ? envS : 6;
+#define PF_TRY(WW, SS) \
+    if (W == WW && S == SS) return launch_stream_t<real, WW, SS>(L, k, in, base, out, vel, has_base, s);
+    PF_TRY(256, 6) PF_TRY(256, 5) PF_TRY(256, 7) PF_TRY(256, 8) PF_TRY(128, 6) PF_TRY(128, 8)
+    PF_TRY(128, 10) PF_TRY(64, 6) PF_TRY(64, 8) PF_TRY(64, 12)
+#undef PF_TRY
+    return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_stage(int precision, const Layout &L, const Coef &K, const void *in,
@@ -511,10 +597,10 @@ cudaError_t launch_stage(int precision, const Layout &L, const Coef &K, const vo
     const bool stream = L.path != 1 && stream_eligible(L);
     if (stream) {
         if (precision == 0)
-            return launch_stream<double, 6>(L, make_kc<double>(K, coef), (const double *)in,
+            return launch_stream<double>(L, make_kc<double>(K, coef), (const double *)in,
                                             (const double *)base, (double *)out, (const double *)vel,
                                             has_base, s);
-        return launch_stream<float, 8>(L, make_kc<float>(K, coef), (const float *)in, (const float *)base,
+        return launch_stream<float>(L, make_kc<float>(K, coef), (const float *)in, (const float *)base,
                                        (float *)out, (const float *)vel, has_base, s);
     }
     dim3 grid((L.nx + BX - 1) / BX, (L.ny_loc + BY - 1) / BY, L.members);
