@@ -84,7 +84,7 @@ typedef struct {
     int32_t device;                  /* CUDA device ordinal                                  */
     int32_t graph_steps;             /* steps per captured CUDA graph (0 = no graphs)        */
     int32_t kernel_path;             /* stage kernel: 0 auto (streaming TMA kernel when nx % 4 == 0
-                                        and nx >= 64, else tile kernel), 1 tile, 2 streaming   */
+                                        and nx >= 16, else tile kernel), 1 tile, 2 streaming   */
 } pf_params;
 
 /* Fill *out with the preset of BASELINE.json configs[cfg-1] (cfg = 1..5; R-13, R-14).

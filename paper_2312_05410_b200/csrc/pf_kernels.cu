@@ -42,7 +42,7 @@ __device__ __forceinline__ int wrap_x(int gx, int nx) {
     return gx % nx;
 }
 
-template <typename real>
+template <typename real, bool HMIX>
 __global__ void __launch_bounds__(NT) stage_kernel(Layout L, KC<real> k, const real *__restrict__ in,
                                                    const real *__restrict__ base, real *out,
                                                    const real *__restrict__ vel) {
@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(NT) stage_kernel(Layout L, KC<real> k, const r
         ey = ey < 1 ? 1 : (ey > BY + 2 ? BY + 2 : ey);
         const int ex = sx + 1;
         real mc, mp, M;
-        constitutive<real>(k, sc[ey][ex], sp[ey][ex], sc[ey][ex - 1], sc[ey][ex + 1], sc[ey - 1][ex],
+        constitutive<real, HMIX>(k, sc[ey][ex], sp[ey][ex], sc[ey][ex - 1], sc[ey][ex + 1], sc[ey - 1][ex],
                            sc[ey + 1][ex], sp[ey][ex - 1], sp[ey][ex + 1], sp[ey - 1][ex],
                            sp[ey + 1][ex], mc, mp, M);
         smc[sy][sx] = mc;
@@ -122,8 +122,11 @@ __global__ void __launch_bounds__(NT) stage_kernel(Layout L, KC<real> k, const r
         const int cy = q + 2, cx = lx + 2;                   // c/phi tile coordinates
         const int64_t o = m * L.mstride + row0 + (int64_t)ly * nx + gx;
         real oc, op, orr;
-        cell_update<real>(k, vx, vy, sM[y][x], sM[y][x - 1], sM[y][x + 1], sM[y - 1][x], sM[y + 1][x],
-                          smc[y][x], smc[y][x - 1], smc[y][x + 1], smc[y - 1][x], smc[y + 1][x],
+        const real fe = face_flux<real>(sM[y][x], sM[y][x + 1], smc[y][x], smc[y][x + 1]);
+        const real fw = face_flux<real>(sM[y][x - 1], sM[y][x], smc[y][x - 1], smc[y][x]);
+        const real fn = face_flux<real>(sM[y][x], sM[y + 1][x], smc[y][x], smc[y + 1][x]);
+        const real fs = face_flux<real>(sM[y - 1][x], sM[y][x], smc[y - 1][x], smc[y][x]);
+        cell_update<real>(k, vx, vy, fe, fw, fn, fs,
                           smp[y][x], smp[y][x - 1], smp[y][x + 1], smp[y - 1][x], smp[y + 1][x],
                           sp[cy][cx - 1], sp[cy][cx + 1], sp[cy - 1][cx], sp[cy + 1][cx],
                           sr[y][x], sr[y][x - 1], sr[y][x + 1], sr[y - 1][x], sr[y + 1][x],
@@ -289,59 +292,58 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         : "memory");
 }
 
-template <typename real, int W, int S>
+// Streaming kernel configuration: NCW compute warps per block, each producing 30 output columns
+// (it evaluates mu / M on 32 columns: its 30 plus one on each side), so a strip is at most
+// 30 NCW columns wide; S ring slots.
+template <typename real, int NCW, int S>
 struct StreamCfg {
     static constexpr int HL = 16 / (int)sizeof(real);   // halo columns loaded (one 16 B chunk)
-    static constexpr int RW = W + 2 * HL;               // smem row width incl. halo
-    static constexpr int SLOT = 3 * RW + 3 * W;         // c, phi, rho rows + base c, phi, rho
-    static constexpr int MUW = W + 2;                   // mu / M rows with 1 halo column
-    static constexpr size_t bytes =
-        (size_t)S * SLOT * sizeof(real) + (size_t)9 * MUW * sizeof(real) + (size_t)S * 16;
+    static constexpr int WMAX = (30 * NCW + HL - 1) / HL * HL;   // widest strip (16 B multiple)
+    static constexpr int RW = 32 * NCW + 2 * HL;        // smem row width (>= WMAX + 2 HL + 2)
+    static constexpr int SLOT = 3 * RW + 3 * WMAX;      // c, phi, rho rows + base c, phi, rho
+    static constexpr size_t bytes = (size_t)S * SLOT * sizeof(real) + (size_t)S * 16;
 };
 
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void named_sync(int id, int nthreads) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
 // Segment enumeration shared by the producer and the compute warps.
 struct Seg {
     int m, x0, Wp, ya, yb;
 };
-template <int W>
-__device__ __forceinline__ bool next_seg(const Layout &L, int64_t &pos, int64_t hi, Seg &sg) {
+__device__ __forceinline__ bool next_seg(const Layout &L, int Wo, int64_t &pos, int64_t hi, Seg &sg) {
     if (pos >= hi) return false;
-    const int nyl = L.ny_loc, strips = (L.nx + W - 1) / W;
+    const int nyl = L.ny_loc, strips = (L.nx + Wo - 1) / Wo;
     const int64_t col = pos / nyl;
     sg.ya = (int)(pos - col * nyl);
     sg.yb = (int)min((int64_t)nyl, (int64_t)sg.ya + (hi - pos));
     pos += sg.yb - sg.ya;
     sg.m = (int)(col / strips);
     const int sidx = (int)(col - (int64_t)sg.m * strips);
-    sg.x0 = sidx * W;
-    sg.Wp = min(W, L.nx - sg.x0);
+    sg.x0 = sidx * Wo;
+    sg.Wp = min(Wo, L.nx - sg.x0);
     return true;
 }
 
-template <typename real, int W, int S>
-__global__ void __launch_bounds__(W + 64, (W == 256 ? 2 : (W == 128 ? 3 : 5))) stream_kernel(Layout L, KC<real> k, const real *__restrict__ in,
-                                                        const real *__restrict__ base, real *out,
-                                                        const real *__restrict__ vel, int has_base) {
-    // Warp roles.  Threads [0, W): workers, one column each.  Warp W/32 (halo warp): lanes 0/1
-    // compute mu/M of the halo columns x0-1 / x0+Wp.  Warp W/32+1 (producer): lane 0 issues the
-    // TMA bulk copies, gated by per-slot "empty" mbarriers; it never joins the compute barrier.
-    // The row loop is unrolled by 3 (mu ring of 3 rows, compile-time) and computes
-    // unconditionally (only stores are predicated), so the register windows rotate by renaming.
-    // Segments are padded to a multiple of 3 loads with arrive-only (empty) loads.
-    using Cfg = StreamCfg<real, W, S>;
-    constexpr int HL = Cfg::HL, RW = Cfg::RW, SLOT = Cfg::SLOT, MUW = Cfg::MUW;
-    constexpr int NCW = W / 32 + 1;                 // compute warps (workers + halo warp)
+template <typename real, int NCW, int S, bool BASE, bool HMIX>
+__global__ void __launch_bounds__(32 * NCW + 32, (NCW >= 8 ? 2 : 4)) stream_kernel(
+    Layout L, KC<real> k, const real *__restrict__ in, const real *__restrict__ base, real *out,
+    const real *__restrict__ vel, int Wo) {
+    // BASE: stage 2 (the update base u^n is a separate buffer, streamed through the ring);
+    // otherwise stage 1 (base = the stage input).
+    // Warp roles.  Warps [0, NCW): compute.  Warp NCW: producer -- lane 0 issues the TMA bulk
+    // copies of the row ring, gated per slot by an "empty" mbarrier that every compute warp
+    // arrives on once it is done with the slot.  Compute warps never synchronise with each other:
+    // warp w owns output columns x0 + 30w + [0, 30); lane l evaluates mu / M at column
+    // x0 + 30w - 1 + l and passes them to lanes l -+ 1 by warp shuffles.  The row loop is unrolled
+    // by 3 and computes unconditionally (only stores are predicated), so the per-lane sliding
+    // windows rotate by register renaming.
+    using Cfg = StreamCfg<real, NCW, S>;
+    constexpr int HL = Cfg::HL, RW = Cfg::RW, SLOT = Cfg::SLOT, WMAX = Cfg::WMAX;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     real *slots = reinterpret_cast<real *>(smem_raw);
-    real *mus = slots + S * SLOT;                                  // [3 rows][mu_c, mu_phi, M][MUW]
-    uint64_t *full = reinterpret_cast<uint64_t *>(mus + 9 * MUW);
+    uint64_t *full = reinterpret_cast<uint64_t *>(slots + S * SLOT);
     uint64_t *empty = full + S;
 
     const int t = threadIdx.x;
@@ -356,7 +358,7 @@ __global__ void __launch_bounds__(W + 64, (W == 256 ? 2 : (W == 128 ? 3 : 5))) s
     __syncthreads();
 
     const int nx = L.nx;
-    const int strips = (nx + W - 1) / W;
+    const int strips = (nx + Wo - 1) / Wo;
     const int64_t R = (int64_t)L.members * strips * L.ny_loc;
     const int64_t lo = R * blockIdx.x / gridDim.x, hi = R * (blockIdx.x + 1) / gridDim.x;
 
@@ -366,7 +368,7 @@ __global__ void __launch_bounds__(W + 64, (W == 256 ? 2 : (W == 128 ? 3 : 5))) s
         uint32_t g = 0;
         int64_t pos = lo;
         Seg sg;
-        while (next_seg<W>(L, pos, hi, sg)) {
+        while (next_seg(L, Wo, pos, hi, sg)) {
             const int n = sg.yb - sg.ya + 4, npad = (n + 2) / 3 * 3;
             const real *fin = in + sg.m * L.mstride + 2 * (int64_t)nx;
             const real *fba = base + sg.m * L.mstride + 2 * (int64_t)nx;
@@ -387,7 +389,7 @@ __global__ void __launch_bounds__(W + 64, (W == 256 ? 2 : (W == 128 ? 3 : 5))) s
                 const bool rho_res = grho >= L.ny;                // reservoir row: rho_in, no copy
                 if (grho < 0) grho = -1 - grho;
                 const int rr = grho - L.y0;
-                const bool wb = has_base && (kk - 2 >= sg.ya) && (kk - 2 < sg.yb);
+                const bool wb = BASE && (kk - 2 >= sg.ya) && (kk - 2 < sg.yb);
                 mbar_expect_tx(&full[slot], (rho_res ? 2u : 3u) * rowb + (wb ? 3u * bb : 0u));
                 for (int f = 0; f < 3; ++f) {
                     if (f == 2 && rho_res) continue;
@@ -403,7 +405,7 @@ __global__ void __launch_bounds__(W + 64, (W == 256 ? 2 : (W == 128 ? 3 : 5))) s
                 }
                 if (wb)
                     for (int f = 0; f < 3; ++f)
-                        bulk_g2s(sl + 3 * RW + f * W, fba + f * L.fstride + (int64_t)(kk - 2) * nx + sg.x0, bb,
+                        bulk_g2s(sl + 3 * RW + f * WMAX, fba + f * L.fstride + (int64_t)(kk - 2) * nx + sg.x0, bb,
                                  &full[slot]);
             }
         }
@@ -411,108 +413,90 @@ __global__ void __launch_bounds__(W + 64, (W == 256 ? 2 : (W == 128 ? 3 : 5))) s
     }
 
     // --------------------------- compute warps ---------------------------------
-    const bool halo = warp == NCW - 1;
-    int sidx = 0;                           // ring slot of the current load
+    static_assert(S % 3 == 0, "ring depth must be a multiple of 3 (rows are consumed in groups of 3)");
+    const int cx = 30 * warp - 1 + lane;    // strip-relative column of this lane's mu / M
+    const int ci = HL + cx;                 // its smem index
+    const int bi = cx < 0 ? 0 : (cx >= WMAX ? WMAX - 1 : cx);   // base index (in range)
+    int sidx = 0;                           // ring slot of the current load (0 mod 3 at a group start)
     uint32_t par = 0;                       // its full-barrier phase parity
     int64_t pos = lo;
     Seg sg;
-    while (next_seg<W>(L, pos, hi, sg)) {
+    while (next_seg(L, Wo, pos, hi, sg)) {
         const int n = sg.yb - sg.ya + 4, npad = (n + 2) / 3 * 3;
-        const int Wp = sg.Wp;
-        if (halo) {
-            // lanes 0 / 1: mu/M of the halo columns x0-1 / x0+Wp of row k-1
-            const int j = (lane == 0) ? HL - 1 : HL + Wp;
-            const int o = (lane == 0) ? 0 : 1 + Wp;
-            const bool st = lane < 2;
-            for (int i0 = 0; i0 < npad; i0 += 3) {
-#pragma unroll
-                for (int u = 0; u < 3; ++u) {
-                    const int i = i0 + u;
-                    mbar_wait(&full[sidx], par);
-                    const real *s0 = slots + sidx * SLOT;
-                    const real *s1 = slots + (sidx == 0 ? S - 1 : sidx - 1) * SLOT;
-                    const real *s2 = slots + (sidx >= 2 ? sidx - 2 : sidx + S - 2) * SLOT;
-                    real *mrow_w = mus + ((u + 2) % 3) * 3 * MUW;
-                    real a, b, M;
-                    constitutive<real>(k, s1[j], s1[RW + j], s1[j - 1], s1[j + 1], s2[j], s0[j], s1[RW + j - 1],
-                                       s1[RW + j + 1], s2[RW + j], s0[RW + j], a, b, M);
-                    if (st && i >= 2 && i < n) {
-                        mrow_w[o] = a;
-                        mrow_w[MUW + o] = b;
-                        mrow_w[2 * MUW + o] = M;
-                    }
-                    named_sync(1, NCW * 32);
-                    __syncwarp();
-                    if (i >= 2 && lane == 0) mbar_arrive(&empty[sidx >= 2 ? sidx - 2 : sidx + S - 2]);
-                    if (++sidx == S) { sidx = 0; par ^= 1u; }
-                }
-            }
-        } else {
-            const bool active = t < Wp;
-            const int tc = active ? t : 0;
-            real *orow = out + sg.m * L.mstride + 2 * (int64_t)nx + (int64_t)(sg.ya - 4) * nx + sg.x0 + tc;
-            const real vx = vel[2 * sg.m], vy = vel[2 * sg.m + 1];
-            const int rho_res_i = L.ny - L.y0 - sg.ya + 3;   // first load whose rho row is the reservoir
+        const bool store = lane >= 1 && lane <= 30 && cx < sg.Wp;
+        const int64_t fs1 = L.fstride;
+        real *op_ = out + sg.m * L.mstride + 2 * (int64_t)nx + (int64_t)(sg.ya - 4) * nx + sg.x0 + bi;
+        const real vx = vel[2 * sg.m], vy = vel[2 * sg.m + 1];
+        const int rho_res_i = L.ny - L.y0 - sg.ya + 3;   // first load whose rho row is the reservoir
 
-            real c_m2 = 0, c_m1 = 0, c_0 = 0;                 // c rows k-2, k-1, k (own column)
-            real p_m3 = 0, p_m2 = 0, p_m1 = 0, p_0 = 0;       // phi rows k-3 .. k
-            real r_m3 = 0, r_m2 = 0, r_m1 = 0;                // rho rows k-3 .. k-1
-            real a_m3 = 0, a_m2 = 0, a_m1 = 0;                // mu_c rows k-3 .. k-1
-            real b_m3 = 0, b_m2 = 0, b_m1 = 0;                // mu_phi rows k-3 .. k-1
-            real M_m3 = 0, M_m2 = 0, M_m1 = 0;                // M rows k-3 .. k-1
-            for (int i0 = 0; i0 < npad; i0 += 3) {
+        real c_m2 = 0, c_m1 = 0, c_0 = 0;                 // c rows k-2, k-1, k (own column)
+        real p_m3 = 0, p_m2 = 0, p_m1 = 0, p_0 = 0;       // phi rows k-3 .. k
+        real r_m3 = 0, r_m2 = 0, r_m1 = 0;                // rho rows k-3 .. k-1
+        real a_m2 = 0, a_m1 = 0;                          // mu_c rows k-2, k-1
+        real b_m3 = 0, b_m2 = 0, b_m1 = 0;                // mu_phi rows k-3 .. k-1
+        real M_m2 = 0, M_m1 = 0;                          // M rows k-2, k-1
+        real fn_m = 0;                                    // north face flux of row k-3
+        for (int i0 = 0; i0 < npad; i0 += 3) {
+            // ring pointers of this group of 3 loads (slots sidx .. sidx+2) and the 2 before it
+            const real *g0 = slots + sidx * SLOT + ci;
+            const real *gm1 = slots + (sidx == 0 ? S - 1 : sidx - 1) * SLOT + ci;
+            const real *gm2 = slots + (sidx == 0 ? S - 2 : sidx - 2) * SLOT + ci;
+            uint64_t *fb = &full[sidx];
+            uint64_t *eb0 = &empty[sidx == 0 ? S - 2 : sidx - 2];
+            uint64_t *eb1 = &empty[sidx == 0 ? S - 1 : sidx - 1];
 #pragma unroll
-                for (int u = 0; u < 3; ++u) {
-                    const int i = i0 + u;
-                    mbar_wait(&full[sidx], par);
-                    const real *s0 = slots + sidx * SLOT;                                   // load k
-                    const real *s1 = slots + (sidx == 0 ? S - 1 : sidx - 1) * SLOT;          // load k-1
-                    const real *s2 = slots + (sidx >= 2 ? sidx - 2 : sidx + S - 2) * SLOT;   // load k-2
-                    real *mrow_w = mus + ((u + 2) % 3) * 3 * MUW;                           // mu row k-1
-                    const real *mrow = mus + ((u + 1) % 3) * 3 * MUW;                       // mu row k-2
-                    c_m2 = c_m1; c_m1 = c_0; c_0 = s0[HL + tc];
-                    p_m3 = p_m2; p_m2 = p_m1; p_m1 = p_0; p_0 = s0[RW + HL + tc];
-                    r_m3 = r_m2; r_m2 = r_m1;
-                    r_m1 = (i >= rho_res_i) ? k.rho_in : s0[2 * RW + HL + tc];
-                    a_m3 = a_m2; a_m2 = a_m1;
-                    b_m3 = b_m2; b_m2 = b_m1;
-                    M_m3 = M_m2; M_m2 = M_m1;
-                    constitutive<real>(k, c_m1, p_m1, s1[HL + tc - 1], s1[HL + tc + 1], c_m2, c_0,
-                                       s1[RW + HL + tc - 1], s1[RW + HL + tc + 1], p_m2, p_0, a_m1, b_m1, M_m1);
-                    if (active && i >= 2 && i < n) {
-                        mrow_w[1 + t] = a_m1;
-                        mrow_w[MUW + 1 + t] = b_m1;
-                        mrow_w[2 * MUW + 1 + t] = M_m1;
-                    }
-                    named_sync(1, NCW * 32);
-                    // update of row k-2 (stage 1: base = input; stage 2: base row from the ring)
-                    const real *bs = s0 + 3 * RW;
-                    const real bc = has_base ? bs[tc] : c_m2;
-                    const real bp = has_base ? bs[W + tc] : p_m2;
-                    const real br = has_base ? bs[2 * W + tc] : r_m2;
-                    real oc, op, orr;
-                    cell_update<real>(k, vx, vy, M_m2, mrow[2 * MUW + tc], mrow[2 * MUW + tc + 2], M_m3, M_m1,
-                                      a_m2, mrow[tc], mrow[tc + 2], a_m3, a_m1,
-                                      b_m2, mrow[MUW + tc], mrow[MUW + tc + 2], b_m3, b_m1,
-                                      s2[RW + HL + tc - 1], s2[RW + HL + tc + 1], p_m3, p_m1,
-                                      r_m2, s1[2 * RW + HL + tc - 1], s1[2 * RW + HL + tc + 1], r_m3, r_m1,
-                                      bc, bp, br, oc, op, orr);
-                    if (active && i >= 4 && i < n) {
-                        real *o = orow + (int64_t)i * nx;
-                        o[0] = oc;
-                        o[L.fstride] = op;
-                        o[2 * L.fstride] = orr;
-                    }
-                    __syncwarp();
-                    if (i >= 2 && lane == 0) mbar_arrive(&empty[sidx >= 2 ? sidx - 2 : sidx + S - 2]);
-                    if (++sidx == S) { sidx = 0; par ^= 1u; }
+            for (int u = 0; u < 3; ++u) {
+                const int i = i0 + u;
+                const real *s0 = g0 + u * SLOT;                                      // load k
+                const real *s1 = u == 0 ? gm1 : g0 + (u - 1) * SLOT;                 // load k-1
+                const real *s2 = u == 0 ? gm2 : (u == 1 ? gm1 : g0);                 // load k-2
+                mbar_wait(fb + u, par);
+                c_m2 = c_m1; c_m1 = c_0; c_0 = s0[0];
+                p_m3 = p_m2; p_m2 = p_m1; p_m1 = p_0; p_0 = s0[RW];
+                r_m3 = r_m2; r_m2 = r_m1;
+                r_m1 = (i >= rho_res_i) ? k.rho_in : s0[2 * RW];
+                a_m2 = a_m1;
+                b_m3 = b_m2; b_m2 = b_m1;
+                M_m2 = M_m1;
+                // mu / M of row k-1 at this lane's column
+                constitutive<real, HMIX>(k, c_m1, p_m1, s1[-1], s1[1], c_m2, c_0, s1[RW - 1], s1[RW + 1], p_m2, p_0,
+                                         a_m1, b_m1, M_m1);
+                // update of row k-2.  East face flux from this lane's mu / M and lane+1's; the west
+                // flux is lane-1's east flux; the south flux is last row's north flux.
+                const real ar = __shfl_down_sync(0xffffffffu, a_m2, 1);
+                const real Mr = __shfl_down_sync(0xffffffffu, M_m2, 1);
+                const real bl = __shfl_up_sync(0xffffffffu, b_m2, 1), br_ = __shfl_down_sync(0xffffffffu, b_m2, 1);
+                const real fe = face_flux<real>(M_m2, Mr, a_m2, ar);
+                const real fw = __shfl_up_sync(0xffffffffu, fe, 1);
+                const real fn = face_flux<real>(M_m2, M_m1, a_m2, a_m1);
+                const real fs = fn_m;
+                fn_m = fn;
+                real bc = c_m2, bp = p_m2, bq = r_m2;   // stage 1: base = input
+                if (BASE) {                               // stage 2: base row from the ring
+                    const real *bs = s0 - ci + 3 * RW + bi;
+                    bc = bs[0]; bp = bs[WMAX]; bq = bs[2 * WMAX];
                 }
+                real oc, op, orr;
+                cell_update<real>(k, vx, vy, fe, fw, fn, fs, b_m2, bl, br_, b_m3, b_m1,
+                                  s2[RW - 1], s2[RW + 1], p_m3, p_m1,
+                                  r_m2, s1[2 * RW - 1], s1[2 * RW + 1], r_m3, r_m1,
+                                  bc, bp, bq, oc, op, orr);
+                if (store && i >= 4 && i < n) {
+                    op_[0] = oc;
+                    op_[fs1] = op;
+                    op_[2 * fs1] = orr;
+                }
+                op_ += nx;
+                __syncwarp();
+                if (i >= 2 && lane == 0) mbar_arrive(u == 0 ? eb0 : (u == 1 ? eb1 : &empty[sidx]));
             }
+            sidx += 3;
+            if (sidx == S) { sidx = 0; par ^= 1u; }
         }
         // release the last two loads of the segment
         if (lane == 0) {
-            mbar_arrive(&empty[sidx >= 2 ? sidx - 2 : sidx + S - 2]);
-            mbar_arrive(&empty[sidx >= 1 ? sidx - 1 : sidx + S - 1]);
+            mbar_arrive(&empty[sidx == 0 ? S - 2 : sidx - 2]);
+            mbar_arrive(&empty[sidx == 0 ? S - 1 : sidx - 1]);
         }
     }
 }
@@ -522,8 +506,8 @@ KC<real> make_kc(const Coef &K, double coef) {
     KC<real> k;
     k.half_inv_dx2 = (real)K.half_inv_dx2;
     k.inv_2dx = (real)K.inv_2dx;
-    k.kc_dx2 = (real)K.kc_dx2;
-    k.kp_dx2 = (real)K.kp_dx2;
+    k.m_kc_dx2 = (real)(-K.kc_dx2);
+    k.m_kp_dx2 = (real)(-K.kp_dx2);
     k.W_c = (real)K.W_c;
     k.W2c = (real)K.W2c;
     k.W2p = (real)K.W2p;
@@ -531,7 +515,8 @@ KC<real> make_kc(const Coef &K, double coef) {
     k.dMb = (real)K.dMb;
     k.MBs = (real)K.MBs;
     k.dMs = (real)K.dMs;
-    k.inv_sigma = (real)K.inv_sigma;
+    k.two_inv_sigma = (real)(2.0 * K.inv_sigma);
+    k.hmix = (K.dMb != 0.0 || K.dMs != 0.0) ? 1 : 0;
     k.Mp_dx2 = (real)K.Mp_dx2;
     k.Dr_dx2 = (real)K.Dr_dx2;
     k.rho_in = (real)K.rho_in;
@@ -541,52 +526,68 @@ KC<real> make_kc(const Coef &K, double coef) {
 
 }  // namespace
 
-template <typename real, int W, int S>
-cudaError_t launch_stream_t(const Layout &L, const KC<real> &k, const real *in, const real *base,
-                            real *out, const real *vel, int has_base, cudaStream_t s) {
-    using Cfg = StreamCfg<real, W, S>;
-    static int occ = -1, nsm = 0;
-    if (occ < 0) {
-        cudaError_t e = cudaFuncSetAttribute(stream_kernel<real, W, S>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::bytes);
-        if (e != cudaSuccess) return e;
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stream_kernel<real, W, S>, W + 64, Cfg::bytes);
-        if (e != cudaSuccess) return e;
-        if (occ < 1) occ = 1;
-    }
-    const int strips = (L.nx + W - 1) / W;
-    const int64_t R = (int64_t)L.members * strips * L.ny_loc;
-    int64_t B = (int64_t)occ * nsm;
-    const int64_t minrows = 16;
-    if (B > (R + minrows - 1) / minrows) B = (R + minrows - 1) / minrows;
-    if (B < 1) B = 1;
-    stream_kernel<real, W, S><<<(unsigned)B, W + 64, Cfg::bytes, s>>>(L, k, in, base, out, vel, has_base);
-    return cudaGetLastError();
-}
-
-bool stream_eligible(const Layout &L) { return L.nx % 4 == 0 && L.nx >= 64; }
-
-// Strip width W and ring depth S: W = 256 (nx >= 256), 128, 64; S = 6 (fp64) / 8 (fp32).
-// PF_STREAM_W / PF_STREAM_S override them (tuning experiments; read once).
 int env_int(const char *name, int dflt) {
     const char *v = getenv(name);
     return v ? atoi(v) : dflt;
 }
 
+template <typename real, int NCW, int S, bool BASE, bool HMIX>
+cudaError_t launch_stream_b(const Layout &L, const KC<real> &k, const real *in, const real *base,
+                            real *out, const real *vel, int Wo, cudaStream_t s) {
+    using Cfg = StreamCfg<real, NCW, S>;
+    static int occ = -1, nsm = 0;
+    if (occ < 0) {
+        cudaError_t e = cudaFuncSetAttribute(stream_kernel<real, NCW, S, BASE, HMIX>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::bytes);
+        if (e != cudaSuccess) return e;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stream_kernel<real, NCW, S, BASE, HMIX>, 32 * NCW + 32,
+                                                          Cfg::bytes);
+        if (e != cudaSuccess) return e;
+        if (occ < 1) occ = 1;
+    }
+    const int strips = (L.nx + Wo - 1) / Wo;
+    const int64_t R = (int64_t)L.members * strips * L.ny_loc;
+    int64_t B = (int64_t)occ * nsm;
+    const int64_t minrows = 16;
+    if (B > (R + minrows - 1) / minrows) B = (R + minrows - 1) / minrows;
+    if (B < 1) B = 1;
+    stream_kernel<real, NCW, S, BASE, HMIX><<<(unsigned)B, 32 * NCW + 32, Cfg::bytes, s>>>(L, k, in, base, out, vel, Wo);
+    return cudaGetLastError();
+}
+
+template <typename real, int NCW, int S>
+cudaError_t launch_stream_t(const Layout &L, const KC<real> &k, const real *in, const real *base,
+                            real *out, const real *vel, int has_base, int Wo, cudaStream_t s) {
+    if (k.hmix)
+        return has_base ? launch_stream_b<real, NCW, S, true, true>(L, k, in, base, out, vel, Wo, s)
+                        : launch_stream_b<real, NCW, S, false, true>(L, k, in, base, out, vel, Wo, s);
+    return has_base ? launch_stream_b<real, NCW, S, true, false>(L, k, in, base, out, vel, Wo, s)
+                    : launch_stream_b<real, NCW, S, false, false>(L, k, in, base, out, vel, Wo, s);
+}
+
+bool stream_eligible(const Layout &L) { return L.nx % 4 == 0 && L.nx >= 16; }
+
+// Strip output width Wo (multiple of 4, <= 30 NCW) and warps per block NCW: 256 columns on 9
+// compute warps for wide grids, narrower strips on fewer warps for small nx.  PF_STREAM_NCW /
+// PF_STREAM_S / PF_STREAM_WO override (tuning experiments; read once).
 template <typename real>
 cudaError_t launch_stream(const Layout &L, const KC<real> &k, const real *in, const real *base, real *out,
                           const real *vel, int has_base, cudaStream_t s) {
-    static const int envW = env_int("PF_STREAM_W", 0), envS = env_int("PF_STREAM_S", 0);
-    int W = L.nx >= 256 ? 256 : (L.nx >= 128 ? 128 : 64);
-    if (envW && envW <= L.nx) W = envW;
-    int S = envS ? envS : 6;
-#define PF_TRY(WW, SS) \
-    if (W == WW && S == SS) return launch_stream_t<real, WW, SS>(L, k, in, base, out, vel, has_base, s);
-    PF_TRY(256, 6) PF_TRY(256, 5) PF_TRY(256, 7) PF_TRY(256, 8) PF_TRY(128, 6) PF_TRY(128, 8)
-    PF_TRY(128, 10) PF_TRY(64, 6) PF_TRY(64, 8) PF_TRY(64, 12)
+    static const int envN = env_int("PF_STREAM_NCW", 0), envS = env_int("PF_STREAM_S", 0),
+                     envWo = env_int("PF_STREAM_WO", 0);
+    int ncw = L.nx >= 256 ? 9 : (L.nx >= 120 ? 5 : 3);
+    if (envN) ncw = envN;
+    int Wo = ncw == 9 ? 256 : (ncw == 5 ? 128 : 64);
+    Wo = min(Wo, (30 * ncw) / 4 * 4);
+    if (envWo) Wo = envWo;
+    if (Wo > L.nx) Wo = L.nx;
+    const int S = envS ? envS : 6;
+#define PF_TRY(NN, SS) \
+    if (ncw == NN && S == SS) return launch_stream_t<real, NN, SS>(L, k, in, base, out, vel, has_base, Wo, s);
+    PF_TRY(9, 6) PF_TRY(9, 9) PF_TRY(5, 6) PF_TRY(3, 6)
 #undef PF_TRY
     return cudaErrorInvalidValue;
 }
@@ -604,14 +605,23 @@ cudaError_t launch_stage(int precision, const Layout &L, const Coef &K, const vo
                                        (float *)out, (const float *)vel, has_base, s);
     }
     dim3 grid((L.nx + BX - 1) / BX, (L.ny_loc + BY - 1) / BY, L.members);
-    if (precision == 0)
-        stage_kernel<double><<<grid, NT, 0, s>>>(L, make_kc<double>(K, coef), (const double *)in,
-                                                 (const double *)base, (double *)out,
-                                                 (const double *)vel);
-    else
-        stage_kernel<float><<<grid, NT, 0, s>>>(L, make_kc<float>(K, coef), (const float *)in,
-                                                (const float *)base, (float *)out,
-                                                (const float *)vel);
+    if (precision == 0) {
+        const KC<double> kd = make_kc<double>(K, coef);
+        if (kd.hmix)
+            stage_kernel<double, true><<<grid, NT, 0, s>>>(L, kd, (const double *)in, (const double *)base,
+                                                           (double *)out, (const double *)vel);
+        else
+            stage_kernel<double, false><<<grid, NT, 0, s>>>(L, kd, (const double *)in, (const double *)base,
+                                                            (double *)out, (const double *)vel);
+    } else {
+        const KC<float> kf = make_kc<float>(K, coef);
+        if (kf.hmix)
+            stage_kernel<float, true><<<grid, NT, 0, s>>>(L, kf, (const float *)in, (const float *)base,
+                                                          (float *)out, (const float *)vel);
+        else
+            stage_kernel<float, false><<<grid, NT, 0, s>>>(L, kf, (const float *)in, (const float *)base,
+                                                           (float *)out, (const float *)vel);
+    }
     return cudaGetLastError();
 }
 

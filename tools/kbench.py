@@ -19,6 +19,8 @@ def one(args):
                                                   check_every=1000000)
     if args.members:
         p = p.replace(n_members=args.members)
+    if args.nx:
+        p = p.replace(nx=args.nx, ny=args.ny or args.nx)
     with pf.Simulation(p) as s:
         s.step(5)
         pf.pf_profile(s.ctx, True)
@@ -27,7 +29,7 @@ def one(args):
     cells = p.n_members * p.nx * p.ny
     esz = 8 if p.precision == 0 else 4
     ms1, ms2 = pr[0] / pr[1], pr[2] / pr[3]
-    out = {"W": os.environ.get("PF_STREAM_W", "auto"), "S": os.environ.get("PF_STREAM_S", "auto"),
+    out = {"cfg": args.config, "nx": p.nx, "ny": p.ny, "members": p.n_members, "NCW": os.environ.get("PF_STREAM_NCW", "auto"), "Wo": os.environ.get("PF_STREAM_WO", "auto"), "S": os.environ.get("PF_STREAM_S", "auto"),
            "path": args.path, "ms_stage1": ms1, "ms_stage2": ms2,
            "GBs_stage1": cells * 6 * esz / ms1 / 1e6, "GBs_stage2": cells * 9 * esz / ms2 / 1e6,
            "Gcell_steps_per_s": cells / (ms1 + ms2) / 1e6}
@@ -40,18 +42,20 @@ def main():
     ap.add_argument("--path", type=int, default=0)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--members", type=int, default=0)
+    ap.add_argument("--nx", type=int, default=0)
+    ap.add_argument("--ny", type=int, default=0)
     ap.add_argument("--sweep", action="store_true")
     args = ap.parse_args()
     if not args.sweep:
         return one(args)
-    combos = [("tile", None, None)] + [(256, S) for S in (5, 6, 7, 8)] + [(128, S) for S in (6, 8, 10)] + [(64, 6), (64, 12)]
+    combos = [("tile", None, None), (9, 6, 256), (9, 9, 256), (5, 6, 128)]
     for c in combos:
         env = dict(os.environ)
         cmd = [sys.executable, __file__, "--config", str(args.config), "--steps", str(args.steps)]
         if c[0] == "tile":
             cmd += ["--path", "1"]
         else:
-            env["PF_STREAM_W"], env["PF_STREAM_S"] = str(c[0]), str(c[1])
+            env["PF_STREAM_NCW"], env["PF_STREAM_S"], env["PF_STREAM_WO"] = str(c[0]), str(c[1]), str(c[2])
             cmd += ["--path", "2"]
         if args.members:
             cmd += ["--members", str(args.members)]
