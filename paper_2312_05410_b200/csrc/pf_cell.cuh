@@ -24,34 +24,39 @@ __device__ __forceinline__ float sub_(float a, float b) { return __fsub_rn(a, b)
 __device__ __forceinline__ float mul_(float a, float b) { return __fmul_rn(a, b); }
 __device__ __forceinline__ float fma_(float a, float b, float c) { return __fmaf_rn(a, b, c); }
 
-// exp(x) for x <= 0 (the argument here is -(phit/sigma)^2), branch-free.  Cody-Waite reduction
-// x = n ln2 + r, |r| <= ln2/2 (ln2 split as in fdlibm), exp(r) by its Taylor polynomial to
-// degree 13 (truncation < 5e-18 relative), scaling by 2^n on the exponent field.  x is clamped
-// to -708 (results below 1e-307 are irrelevant to M_c).  Coefficients live in the constant
-// bank so the DFMAs read them directly.
-__constant__ double kExpConst[3] = {1.4426950408889634, -6.93147180369123816490e-01,
-                                    -1.90821492927058770002e-10};   // log2 e, -ln2 hi, -ln2 lo
-__constant__ double kExpTaylor[12] = {
-    1.0 / 6227020800.0, 1.0 / 479001600.0, 1.0 / 39916800.0, 1.0 / 3628800.0,
-    1.0 / 362880.0,     1.0 / 40320.0,     1.0 / 5040.0,     1.0 / 720.0,
-    1.0 / 120.0,        1.0 / 24.0,        1.0 / 6.0,        0.5};
+// exp(x) for x <= 0 (the argument here is -(phit/sigma)^2), branch-free, table-driven:
+// x = (64 n + j) ln2/64 + r with |r| <= ln2/128 (ln2 split as in fdlibm so the reduction is exact),
+// exp(x) = 2^n * T[j] * P(r), T[j] = 2^(j/64) (host-computed, copied to shared memory by each
+// block), P the Taylor polynomial of exp to degree 6 (truncation < 3e-20 relative).  x is
+// clamped to -708 (results below 1e-307 are irrelevant to M_c).  Max error ~2 ulp.
+__constant__ double kExp2Tab[64];                        // 2^(j/64), filled by the host
+__constant__ double kExpPoly[4] = {1.0 / 720.0, 1.0 / 120.0, 1.0 / 24.0, 1.0 / 6.0};
 
-__device__ __forceinline__ double exp_neg(double x) {
-    const double kMagic = 6755399441055744.0;   // 1.5 * 2^52
-    x = fmax(x, -708.0);
-    const double kd = fma_(x, kExpConst[0], kMagic);   // round(x log2 e) in the low word
-    const int n = __double2loint(kd);
+__device__ __forceinline__ double exp_neg(double x, const double *tab) {
+    const double kMagic = 6755399441055744.0;                 // 1.5 * 2^52
+    const double k64Log2e = 92.332482616893656;              // 64 / ln 2
+    const double kLn2Hi64 = 6.93147180369123816490e-01 / 64.0, kLn2Lo64 = 1.90821492927058770002e-10 / 64.0;
+    x = x > -708.0 ? x : -708.0;
+    const double kd = fma_(x, k64Log2e, kMagic);            // m = round(64 x / ln 2) in the low word
+    const int m = __double2loint(kd);
     const double nd = sub_(kd, kMagic);
-    double r = fma_(nd, kExpConst[1], x);
-    r = fma_(nd, kExpConst[2], r);
-    double p = kExpTaylor[0];
-#pragma unroll
-    for (int q = 1; q < 12; ++q) p = fma_(p, r, kExpTaylor[q]);
+    double r = fma_(nd, -kLn2Hi64, x);
+    r = fma_(nd, -kLn2Lo64, r);
+    double p = fma_(kExpPoly[0], r, kExpPoly[1]);
+    p = fma_(p, r, kExpPoly[2]);
+    p = fma_(p, r, kExpPoly[3]);
+    p = fma_(p, r, 0.5);
     p = fma_(p, r, 1.0);
     p = fma_(p, r, 1.0);
-    return __hiloint2double(__double2hiint(p) + (n << 20), __double2loint(p));
+    p = mul_(p, tab[m & 63]);
+    return __hiloint2double(__double2hiint(p) + ((m >> 6) << 20), __double2loint(p));
 }
-__device__ __forceinline__ float exp_neg(float x) { return expf(x); }
+__device__ __forceinline__ float exp_neg(float x, const double *) { return expf(x); }
+
+// Block-wide copy of the exp table into shared memory (call before the first exp_neg).
+__device__ __forceinline__ void load_exp_table(double *tab) {
+    for (int j = threadIdx.x; j < 64; j += blockDim.x) tab[j] = kExp2Tab[j];
+}
 
 template <typename real>
 __device__ __forceinline__ real clamp01(real c) {
@@ -65,8 +70,8 @@ __device__ __forceinline__ real clamp01(real c) {
 // (u[-1] = u[0], u[-2] = u[1]) yields bit-identical mu / M to the cell it mirrors, and the
 // boundary-face fluxes vanish exactly.
 template <typename real, bool HMIX>
-__device__ __forceinline__ void constitutive(const KC<real> &k, real c, real p, real cl, real cr,
-                                             real cd, real cu, real pl, real pr, real pd, real pu,
+__device__ __forceinline__ void constitutive(const KC<real> &k, const double *etab, real c, real p, real cl,
+                                             real cr, real cd, real cu, real pl, real pr, real pd, real pu,
                                              real &mu_c, real &mu_p, real &M) {
     const real one = real(1), m2 = real(-2), m4 = real(-4);
     const real lc = fma_(c, m4, add_(add_(cl, cr), add_(cd, cu)));   // dx^2 L(c)
@@ -82,7 +87,7 @@ __device__ __forceinline__ void constitutive(const KC<real> &k, real c, real p, 
     // M_c = M_bulk + e (M_surf_mix - M_bulk)                         (R-5, R-6)
     const real pp = mul_(mul_(p, p), fma_(p, m2, real(3)));           // 1/4 (2 - phit)(1 + phit)^2
     const real q = mul_(sub_(p, real(0.5)), k.two_inv_sigma);          // phit / sigma_surf
-    const real e = exp_neg(mul_(-q, q));
+    const real e = exp_neg(mul_(-q, q), etab);
     real mb, ms;
     if (HMIX) {
         const real ch = clamp01(c);                                   // clamp(c, 0, 1)

@@ -52,6 +52,8 @@ __global__ void __launch_bounds__(NT) stage_kernel(Layout L, KC<real> k, const r
     __shared__ real smc[BY + 2][BX + 2];
     __shared__ real smp[BY + 2][BX + 2];
     __shared__ real sM[BY + 2][BX + 2];
+    __shared__ double etab[64];
+    load_exp_table(etab);
 
     const int m = blockIdx.z;
     const int tx0 = blockIdx.x * BX;
@@ -102,7 +104,7 @@ __global__ void __launch_bounds__(NT) stage_kernel(Layout L, KC<real> k, const r
         ey = ey < 1 ? 1 : (ey > BY + 2 ? BY + 2 : ey);
         const int ex = sx + 1;
         real mc, mp, M;
-        constitutive<real, HMIX>(k, sc[ey][ex], sp[ey][ex], sc[ey][ex - 1], sc[ey][ex + 1], sc[ey - 1][ex],
+        constitutive<real, HMIX>(k, etab, sc[ey][ex], sp[ey][ex], sc[ey][ex - 1], sc[ey][ex + 1], sc[ey - 1][ex],
                            sc[ey + 1][ex], sp[ey][ex - 1], sp[ey][ex + 1], sp[ey - 1][ex],
                            sp[ey + 1][ex], mc, mp, M);
         smc[sy][sx] = mc;
@@ -295,32 +297,64 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
 // Streaming kernel configuration: NCW compute warps per block, each producing 30 output columns
 // (it evaluates mu / M on 32 columns: its 30 plus one on each side), so a strip is at most
 // 30 NCW columns wide; S ring slots.
-template <typename real, int NCW, int S>
+template <typename real, int NCW, int S, bool BASE>
 struct StreamCfg {
     static constexpr int HL = 16 / (int)sizeof(real);   // halo columns loaded (one 16 B chunk)
     static constexpr int WMAX = (30 * NCW + HL - 1) / HL * HL;   // widest strip (16 B multiple)
     static constexpr int RW = 32 * NCW + 2 * HL;        // smem row width (>= WMAX + 2 HL + 2)
-    static constexpr int SLOT = 3 * RW + 3 * WMAX;      // c, phi, rho rows + base c, phi, rho
-    static constexpr size_t bytes = (size_t)S * SLOT * sizeof(real) + (size_t)S * 16;
+    static constexpr int SLOT = 3 * RW + (BASE ? 3 * WMAX : 0);   // c, phi, rho (+ base) rows
+    static constexpr size_t bytes = (size_t)S * SLOT * sizeof(real) + (size_t)S * 16 + 64 * 8;
 };
 
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-// Segment enumeration shared by the producer and the compute warps.
+// Work schedule shared by the producer and the compute warps.  Grouped mode (G > 0): blocks come in
+// groups of `strips`; block b works on strip b % strips of the row range [T g/G, T (g+1)/G) of the
+// concatenated (member, row) space (T = members * ny_loc rows, g = b / strips), so the blocks of a
+// group stream the same rows at the same time and DRAM sees whole contiguous rows.  Ungrouped
+// mode (G == 0): block b owns the row range [R b/B, R (b+1)/B) of the concatenated
+// (member, strip, row) space, R = members * strips * ny_loc.
 struct Seg {
     int m, x0, Wp, ya, yb;
 };
-__device__ __forceinline__ bool next_seg(const Layout &L, int Wo, int64_t &pos, int64_t hi, Seg &sg) {
-    if (pos >= hi) return false;
+struct Sched {
+    int64_t lo, hi;
+    int strip;        // grouped: fixed strip of this block; -1 ungrouped
+};
+__device__ __forceinline__ Sched make_sched(const Layout &L, int Wo, int G) {
+    const int strips = (L.nx + Wo - 1) / Wo;
+    Sched sc;
+    if (G > 0) {
+        const int g = blockIdx.x / strips;
+        sc.strip = blockIdx.x - g * strips;
+        const int64_t T = (int64_t)L.members * L.ny_loc;
+        sc.lo = T * g / G;
+        sc.hi = T * (g + 1) / G;
+    } else {
+        const int64_t R = (int64_t)L.members * strips * L.ny_loc;
+        sc.strip = -1;
+        sc.lo = R * blockIdx.x / gridDim.x;
+        sc.hi = R * (blockIdx.x + 1) / gridDim.x;
+    }
+    return sc;
+}
+__device__ __forceinline__ bool next_seg(const Layout &L, int Wo, const Sched &sc, int64_t &pos, Seg &sg) {
+    if (pos >= sc.hi) return false;
     const int nyl = L.ny_loc, strips = (L.nx + Wo - 1) / Wo;
-    const int64_t col = pos / nyl;
+    const int64_t col = pos / nyl;      // grouped: member; ungrouped: member * strips + strip
     sg.ya = (int)(pos - col * nyl);
-    sg.yb = (int)min((int64_t)nyl, (int64_t)sg.ya + (hi - pos));
+    sg.yb = (int)min((int64_t)nyl, (int64_t)sg.ya + (sc.hi - pos));
     pos += sg.yb - sg.ya;
-    sg.m = (int)(col / strips);
-    const int sidx = (int)(col - (int64_t)sg.m * strips);
+    int sidx;
+    if (sc.strip >= 0) {
+        sg.m = (int)col;
+        sidx = sc.strip;
+    } else {
+        sg.m = (int)(col / strips);
+        sidx = (int)(col - (int64_t)sg.m * strips);
+    }
     sg.x0 = sidx * Wo;
     sg.Wp = min(Wo, L.nx - sg.x0);
     return true;
@@ -329,7 +363,8 @@ __device__ __forceinline__ bool next_seg(const Layout &L, int Wo, int64_t &pos, 
 template <typename real, int NCW, int S, bool BASE, bool HMIX>
 __global__ void __launch_bounds__(32 * NCW + 32, (NCW >= 8 ? 2 : 4)) stream_kernel(
     Layout L, KC<real> k, const real *__restrict__ in, const real *__restrict__ base, real *out,
-    const real *__restrict__ vel, int Wo) {
+    const real *__restrict__ vel, int Wo, int G, int dbg) {
+    // dbg != 0 (PF_STREAM_DBG, experiments only): skip the arithmetic, keep every load and store.
     // BASE: stage 2 (the update base u^n is a separate buffer, streamed through the ring);
     // otherwise stage 1 (base = the stage input).
     // Warp roles.  Warps [0, NCW): compute.  Warp NCW: producer -- lane 0 issues the TMA bulk
@@ -339,12 +374,14 @@ __global__ void __launch_bounds__(32 * NCW + 32, (NCW >= 8 ? 2 : 4)) stream_kern
     // x0 + 30w - 1 + l and passes them to lanes l -+ 1 by warp shuffles.  The row loop is unrolled
     // by 3 and computes unconditionally (only stores are predicated), so the per-lane sliding
     // windows rotate by register renaming.
-    using Cfg = StreamCfg<real, NCW, S>;
+    using Cfg = StreamCfg<real, NCW, S, BASE>;
     constexpr int HL = Cfg::HL, RW = Cfg::RW, SLOT = Cfg::SLOT, WMAX = Cfg::WMAX;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     real *slots = reinterpret_cast<real *>(smem_raw);
     uint64_t *full = reinterpret_cast<uint64_t *>(slots + S * SLOT);
     uint64_t *empty = full + S;
+    double *etab = reinterpret_cast<double *>(empty + S);
+    load_exp_table(etab);
 
     const int t = threadIdx.x;
     const int warp = t >> 5, lane = t & 31;
@@ -358,17 +395,15 @@ __global__ void __launch_bounds__(32 * NCW + 32, (NCW >= 8 ? 2 : 4)) stream_kern
     __syncthreads();
 
     const int nx = L.nx;
-    const int strips = (nx + Wo - 1) / Wo;
-    const int64_t R = (int64_t)L.members * strips * L.ny_loc;
-    const int64_t lo = R * blockIdx.x / gridDim.x, hi = R * (blockIdx.x + 1) / gridDim.x;
+    const Sched sch = make_sched(L, Wo, G);
 
     if (warp == NCW) {
         // ------------------------------- producer -------------------------------
         if (lane != 0) return;
         uint32_t g = 0;
-        int64_t pos = lo;
+        int64_t pos = sch.lo;
         Seg sg;
-        while (next_seg(L, Wo, pos, hi, sg)) {
+        while (next_seg(L, Wo, sch, pos, sg)) {
             const int n = sg.yb - sg.ya + 4, npad = (n + 2) / 3 * 3;
             const real *fin = in + sg.m * L.mstride + 2 * (int64_t)nx;
             const real *fba = base + sg.m * L.mstride + 2 * (int64_t)nx;
@@ -413,15 +448,15 @@ __global__ void __launch_bounds__(32 * NCW + 32, (NCW >= 8 ? 2 : 4)) stream_kern
     }
 
     // --------------------------- compute warps ---------------------------------
-    static_assert(S % 3 == 0, "ring depth must be a multiple of 3 (rows are consumed in groups of 3)");
+    static_assert(S >= 4, "ring depth");
     const int cx = 30 * warp - 1 + lane;    // strip-relative column of this lane's mu / M
     const int ci = HL + cx;                 // its smem index
     const int bi = cx < 0 ? 0 : (cx >= WMAX ? WMAX - 1 : cx);   // base index (in range)
-    int sidx = 0;                           // ring slot of the current load (0 mod 3 at a group start)
+    int sidx = 0;                           // ring slot of the first load of the current group
     uint32_t par = 0;                       // its full-barrier phase parity
-    int64_t pos = lo;
+    int64_t pos = sch.lo;
     Seg sg;
-    while (next_seg(L, Wo, pos, hi, sg)) {
+    while (next_seg(L, Wo, sch, pos, sg)) {
         const int n = sg.yb - sg.ya + 4, npad = (n + 2) / 3 * 3;
         const bool store = lane >= 1 && lane <= 30 && cx < sg.Wp;
         const int64_t fs1 = L.fstride;
@@ -437,20 +472,21 @@ __global__ void __launch_bounds__(32 * NCW + 32, (NCW >= 8 ? 2 : 4)) stream_kern
         real M_m2 = 0, M_m1 = 0;                          // M rows k-2, k-1
         real fn_m = 0;                                    // north face flux of row k-3
         for (int i0 = 0; i0 < npad; i0 += 3) {
-            // ring pointers of this group of 3 loads (slots sidx .. sidx+2) and the 2 before it
-            const real *g0 = slots + sidx * SLOT + ci;
-            const real *gm1 = slots + (sidx == 0 ? S - 1 : sidx - 1) * SLOT + ci;
-            const real *gm2 = slots + (sidx == 0 ? S - 2 : sidx - 2) * SLOT + ci;
-            uint64_t *fb = &full[sidx];
-            uint64_t *eb0 = &empty[sidx == 0 ? S - 2 : sidx - 2];
-            uint64_t *eb1 = &empty[sidx == 0 ? S - 1 : sidx - 1];
+            // ring slots of this group of 3 loads and of the 2 loads before it (wrapping mod S)
+            const int q1 = sidx + 1 >= S ? sidx + 1 - S : sidx + 1;
+            const int q2 = sidx + 2 >= S ? sidx + 2 - S : sidx + 2;
+            const int qm1 = sidx >= 1 ? sidx - 1 : sidx - 1 + S;
+            const int qm2 = sidx >= 2 ? sidx - 2 : sidx - 2 + S;
+            const real *gq[5] = {slots + qm2 * SLOT + ci, slots + qm1 * SLOT + ci, slots + sidx * SLOT + ci,
+                                 slots + q1 * SLOT + ci, slots + q2 * SLOT + ci};
+            const int qs[5] = {qm2, qm1, sidx, q1, q2};
 #pragma unroll
             for (int u = 0; u < 3; ++u) {
                 const int i = i0 + u;
-                const real *s0 = g0 + u * SLOT;                                      // load k
-                const real *s1 = u == 0 ? gm1 : g0 + (u - 1) * SLOT;                 // load k-1
-                const real *s2 = u == 0 ? gm2 : (u == 1 ? gm1 : g0);                 // load k-2
-                mbar_wait(fb + u, par);
+                const real *s0 = gq[u + 2];                                          // load k
+                const real *s1 = gq[u + 1];                                          // load k-1
+                const real *s2 = gq[u];                                              // load k-2
+                mbar_wait(&full[qs[u + 2]], par ^ (uint32_t)(sidx + u >= S));
                 c_m2 = c_m1; c_m1 = c_0; c_0 = s0[0];
                 p_m3 = p_m2; p_m2 = p_m1; p_m1 = p_0; p_0 = s0[RW];
                 r_m3 = r_m2; r_m2 = r_m1;
@@ -458,8 +494,20 @@ __global__ void __launch_bounds__(32 * NCW + 32, (NCW >= 8 ? 2 : 4)) stream_kern
                 a_m2 = a_m1;
                 b_m3 = b_m2; b_m2 = b_m1;
                 M_m2 = M_m1;
+                if (dbg) {
+                    if (store && i >= 4 && i < n) {
+                        const real *bs = s0 - ci + 3 * RW + bi;
+                        op_[0] = c_m2 + (BASE ? bs[0] : 0);
+                        op_[fs1] = p_m2 + (BASE ? bs[WMAX] : 0);
+                        op_[2 * fs1] = r_m2 + (BASE ? bs[2 * WMAX] : 0);
+                    }
+                    op_ += nx;
+                    __syncwarp();
+                    if (i >= 2 && lane == 0) mbar_arrive(&empty[qs[u]]);
+                    continue;
+                }
                 // mu / M of row k-1 at this lane's column
-                constitutive<real, HMIX>(k, c_m1, p_m1, s1[-1], s1[1], c_m2, c_0, s1[RW - 1], s1[RW + 1], p_m2, p_0,
+                constitutive<real, HMIX>(k, etab, c_m1, p_m1, s1[-1], s1[1], c_m2, c_0, s1[RW - 1], s1[RW + 1], p_m2, p_0,
                                          a_m1, b_m1, M_m1);
                 // update of row k-2.  East face flux from this lane's mu / M and lane+1's; the west
                 // flux is lane-1's east flux; the south flux is last row's north flux.
@@ -488,16 +536,17 @@ __global__ void __launch_bounds__(32 * NCW + 32, (NCW >= 8 ? 2 : 4)) stream_kern
                 }
                 op_ += nx;
                 __syncwarp();
-                if (i >= 2 && lane == 0) mbar_arrive(u == 0 ? eb0 : (u == 1 ? eb1 : &empty[sidx]));
+                if (i >= 2 && lane == 0) mbar_arrive(&empty[qs[u]]);   // load i-2 is no longer read
             }
             sidx += 3;
-            if (sidx == S) { sidx = 0; par ^= 1u; }
+            if (sidx >= S) { sidx -= S; par ^= 1u; }
         }
         // release the last two loads of the segment
         if (lane == 0) {
-            mbar_arrive(&empty[sidx == 0 ? S - 2 : sidx - 2]);
-            mbar_arrive(&empty[sidx == 0 ? S - 1 : sidx - 1]);
+            mbar_arrive(&empty[sidx >= 2 ? sidx - 2 : sidx - 2 + S]);
+            mbar_arrive(&empty[sidx >= 1 ? sidx - 1 : sidx - 1 + S]);
         }
+        __syncwarp();
     }
 }
 
@@ -534,7 +583,7 @@ int env_int(const char *name, int dflt) {
 template <typename real, int NCW, int S, bool BASE, bool HMIX>
 cudaError_t launch_stream_b(const Layout &L, const KC<real> &k, const real *in, const real *base,
                             real *out, const real *vel, int Wo, cudaStream_t s) {
-    using Cfg = StreamCfg<real, NCW, S>;
+    using Cfg = StreamCfg<real, NCW, S, BASE>;
     static int occ = -1, nsm = 0;
     if (occ < 0) {
         cudaError_t e = cudaFuncSetAttribute(stream_kernel<real, NCW, S, BASE, HMIX>,
@@ -550,50 +599,66 @@ cudaError_t launch_stream_b(const Layout &L, const KC<real> &k, const real *in, 
     }
     const int strips = (L.nx + Wo - 1) / Wo;
     const int64_t R = (int64_t)L.members * strips * L.ny_loc;
-    int64_t B = (int64_t)occ * nsm;
     const int64_t minrows = 16;
-    if (B > (R + minrows - 1) / minrows) B = (R + minrows - 1) / minrows;
+    int64_t B = (int64_t)occ * nsm;
+    static const int dbg = env_int("PF_STREAM_DBG", 0), nogroup = env_int("PF_STREAM_NOGROUP", 0);
+    // grouped schedule when at least 4 groups of `strips` blocks fit in one resident wave
+    int64_t G = B / strips;
+    const int64_t T = (int64_t)L.members * L.ny_loc;
+    if (G > (T + minrows - 1) / minrows) G = (T + minrows - 1) / minrows;
+    if (G >= 4 && !nogroup) {
+        B = G * strips;
+    } else {
+        G = 0;
+        if (B > (R + minrows - 1) / minrows) B = (R + minrows - 1) / minrows;
+    }
     if (B < 1) B = 1;
-    stream_kernel<real, NCW, S, BASE, HMIX><<<(unsigned)B, 32 * NCW + 32, Cfg::bytes, s>>>(L, k, in, base, out, vel, Wo);
+    stream_kernel<real, NCW, S, BASE, HMIX><<<(unsigned)B, 32 * NCW + 32, Cfg::bytes, s>>>(L, k, in, base, out, vel, Wo, (int)G, dbg);
     return cudaGetLastError();
-}
-
-template <typename real, int NCW, int S>
-cudaError_t launch_stream_t(const Layout &L, const KC<real> &k, const real *in, const real *base,
-                            real *out, const real *vel, int has_base, int Wo, cudaStream_t s) {
-    if (k.hmix)
-        return has_base ? launch_stream_b<real, NCW, S, true, true>(L, k, in, base, out, vel, Wo, s)
-                        : launch_stream_b<real, NCW, S, false, true>(L, k, in, base, out, vel, Wo, s);
-    return has_base ? launch_stream_b<real, NCW, S, true, false>(L, k, in, base, out, vel, Wo, s)
-                    : launch_stream_b<real, NCW, S, false, false>(L, k, in, base, out, vel, Wo, s);
 }
 
 bool stream_eligible(const Layout &L) { return L.nx % 4 == 0 && L.nx >= 16; }
 
 // Strip output width Wo (multiple of 4, <= 30 NCW) and warps per block NCW: 256 columns on 9
-// compute warps for wide grids, narrower strips on fewer warps for small nx.  PF_STREAM_NCW /
-// PF_STREAM_S / PF_STREAM_WO override (tuning experiments; read once).
+// compute warps for wide grids, narrower strips on fewer warps for small nx.  Ring depth: stage 1
+// streams 3 rows per load, stage 2 six, so stage 1 affords a deeper ring in the same shared
+// memory.  PF_STREAM_NCW / PF_STREAM_S1 / PF_STREAM_S2 / PF_STREAM_WO override (experiments).
 template <typename real>
 cudaError_t launch_stream(const Layout &L, const KC<real> &k, const real *in, const real *base, real *out,
                           const real *vel, int has_base, cudaStream_t s) {
-    static const int envN = env_int("PF_STREAM_NCW", 0), envS = env_int("PF_STREAM_S", 0),
-                     envWo = env_int("PF_STREAM_WO", 0);
+    static const int envN = env_int("PF_STREAM_NCW", 0), envS1 = env_int("PF_STREAM_S1", 0),
+                     envS2 = env_int("PF_STREAM_S2", 0), envWo = env_int("PF_STREAM_WO", 0);
     int ncw = L.nx >= 256 ? 9 : (L.nx >= 120 ? 5 : 3);
     if (envN) ncw = envN;
     int Wo = ncw == 9 ? 256 : (ncw == 5 ? 128 : 64);
     Wo = min(Wo, (30 * ncw) / 4 * 4);
     if (envWo) Wo = envWo;
     if (Wo > L.nx) Wo = L.nx;
-    const int S = envS ? envS : 6;
-#define PF_TRY(NN, SS) \
-    if (ncw == NN && S == SS) return launch_stream_t<real, NN, SS>(L, k, in, base, out, vel, has_base, Wo, s);
-    PF_TRY(9, 6) PF_TRY(9, 9) PF_TRY(5, 6) PF_TRY(3, 6)
+    const int S = has_base ? (envS2 ? envS2 : 8) : (envS1 ? envS1 : 12);
+#define PF_TRY(NN, SS, BB)                                                                      \
+    if (ncw == NN && S == SS && has_base == BB)                                                \
+        return k.hmix ? launch_stream_b<real, NN, SS, BB, true>(L, k, in, base, out, vel, Wo, s) \
+                      : launch_stream_b<real, NN, SS, BB, false>(L, k, in, base, out, vel, Wo, s);
+    PF_TRY(9, 8, 1) PF_TRY(9, 6, 1) PF_TRY(9, 7, 1) PF_TRY(9, 12, 0) PF_TRY(9, 6, 0) PF_TRY(9, 9, 0)
+    PF_TRY(9, 15, 0) PF_TRY(5, 8, 1) PF_TRY(5, 12, 0) PF_TRY(3, 8, 1) PF_TRY(3, 12, 0)
 #undef PF_TRY
     return cudaErrorInvalidValue;
 }
 
+cudaError_t upload_exp_table() {
+    static bool done = false;
+    if (done) return cudaSuccess;
+    double t[64];
+    for (int j = 0; j < 64; ++j) t[j] = exp2((double)j / 64.0);
+    cudaError_t e = cudaMemcpyToSymbol(kExp2Tab, t, sizeof t);
+    if (e == cudaSuccess) done = true;
+    return e;
+}
+
 cudaError_t launch_stage(int precision, const Layout &L, const Coef &K, const void *in,
                          const void *base, void *out, const void *vel, double coef, cudaStream_t s) {
+    cudaError_t te = upload_exp_table();
+    if (te != cudaSuccess) return te;
     const bool has_base = base != in;
     const bool stream = L.path != 1 && stream_eligible(L);
     if (stream) {

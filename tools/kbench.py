@@ -29,7 +29,7 @@ def one(args):
     cells = p.n_members * p.nx * p.ny
     esz = 8 if p.precision == 0 else 4
     ms1, ms2 = pr[0] / pr[1], pr[2] / pr[3]
-    out = {"cfg": args.config, "nx": p.nx, "ny": p.ny, "members": p.n_members, "NCW": os.environ.get("PF_STREAM_NCW", "auto"), "Wo": os.environ.get("PF_STREAM_WO", "auto"), "S": os.environ.get("PF_STREAM_S", "auto"),
+    out = {"cfg": args.config, "nx": p.nx, "ny": p.ny, "members": p.n_members,
            "path": args.path, "ms_stage1": ms1, "ms_stage2": ms2,
            "GBs_stage1": cells * 6 * esz / ms1 / 1e6, "GBs_stage2": cells * 9 * esz / ms2 / 1e6,
            "Gcell_steps_per_s": cells / (ms1 + ms2) / 1e6}
@@ -48,17 +48,15 @@ def main():
     args = ap.parse_args()
     if not args.sweep:
         return one(args)
-    combos = [("tile", None, None), (9, 6, 256), (9, 9, 256), (5, 6, 128)]
+    combos = [{"PF_STREAM_S1": "12", "PF_STREAM_S2": "8"}, {"PF_STREAM_S1": "6", "PF_STREAM_S2": "6"},
+              {"PF_STREAM_S1": "9", "PF_STREAM_S2": "7"}, {"PF_STREAM_S1": "15", "PF_STREAM_S2": "8"}]
     for c in combos:
         env = dict(os.environ)
-        cmd = [sys.executable, __file__, "--config", str(args.config), "--steps", str(args.steps)]
-        if c[0] == "tile":
-            cmd += ["--path", "1"]
-        else:
-            env["PF_STREAM_NCW"], env["PF_STREAM_S"], env["PF_STREAM_WO"] = str(c[0]), str(c[1]), str(c[2])
-            cmd += ["--path", "2"]
+        env.update(c)
+        cmd = [sys.executable, __file__, "--config", str(args.config), "--steps", str(args.steps), "--path", "2"]
         if args.members:
             cmd += ["--members", str(args.members)]
+        print(json.dumps(c), flush=True)
         subprocess.run(cmd, env=env)
 
 
