@@ -495,7 +495,10 @@ __global__ void __launch_bounds__(32 * NCW + 32, (NCW >= 8 ? 2 : 4)) stream_kern
                 b_m3 = b_m2; b_m2 = b_m1;
                 M_m2 = M_m1;
                 if (dbg) {
-                    if (store && i >= 4 && i < n) {
+                    if (dbg == 2 && warp < 8 && i >= 4 && i < n) {   // sector-aligned experiment
+                        real *o2 = op_ - bi + 32 * warp + lane;
+                        o2[0] = c_m2; o2[fs1] = p_m2; o2[2 * fs1] = r_m2;
+                    } else if (dbg == 1 && store && i >= 4 && i < n) {
                         const real *bs = s0 - ci + 3 * RW + bi;
                         op_[0] = c_m2 + (BASE ? bs[0] : 0);
                         op_[fs1] = p_m2 + (BASE ? bs[WMAX] : 0);
