@@ -180,6 +180,7 @@ struct Slab {
     void *Us = nullptr;   // midpoint stage state u*
     double *partials = nullptr;
     double *diag = nullptr;   // members * kDiag
+    pf::StreamPlan plan;      // streaming-kernel geometry and TMA tensor maps (plan.ok: in use)
 };
 
 enum Mode { kSingle = 0, kLoopback = 1, kNccl = 2 };
@@ -300,7 +301,7 @@ void *buf_of(Slab &s, int which) { return which == 0 ? s.U : s.Us; }
 
 pf_status exchange(pf_ctx *c, int which) {
     if (c->mode == kSingle) return PF_OK;
-    const size_t rowb = (size_t)c->p.nx * c->esz;
+    const size_t rowb = (size_t)c->slabs[0].L.pitch * c->esz;   // full padded rows (ghost columns too)
     if (c->mode == kLoopback) {
         const int P = (int)c->slabs.size();
         for (int s = 0; s < P; ++s) {
@@ -326,7 +327,7 @@ pf_status exchange(pf_ctx *c, int which) {
     // NCCL: rank r exchanges 2 rows of every field of every member with r-1 and r+1.
     Slab &me = c->slabs[0];
     const ncclDataType_t dt = c->p.precision == PF_F64 ? ncclFloat64 : ncclFloat32;
-    const size_t cnt = 2 * (size_t)c->p.nx;
+    const size_t cnt = 2 * (size_t)me.L.pitch;
     char *base = (char *)buf_of(me, which);
     NK(c, ncclGroupStart());
     for (int m = 0; m < me.L.members; ++m)
@@ -371,7 +372,7 @@ pf_status one_step(pf_ctx *c, bool capture) {
             const void *in = stage == 1 ? s.U : s.Us;
             void *out = stage == 1 ? s.Us : s.U;
             const double coef = stage == 1 ? 0.5 * c->p.dt : c->p.dt;
-            CK(c, pf::launch_stage(c->p.precision, s.L, c->K, in, s.U, out, c->vel, coef, c->stream));
+            CK(c, pf::launch_stage(c->p.precision, s.L, s.plan, c->K, stage, in, s.U, out, c->vel, coef, c->stream));
             if (!capture) c->launches += pf::kStageLaunches;
         }
         if (prof) {
@@ -517,7 +518,9 @@ pf_status create_common(const pf_params *p, int mode, int rank, int nranks, cons
         sl.L.y0 = (mode == kLoopback ? s : rank) * rows;
         sl.L.members = p->n_members;
         sl.L.path = p->kernel_path;
-        sl.L.fstride = (int64_t)(rows + 4) * p->nx;
+        sl.L.gx = (int)(16 / c->esz);
+        sl.L.pitch = p->nx + 2 * sl.L.gx;
+        sl.L.fstride = (int64_t)(rows + 4) * sl.L.pitch;
         sl.L.mstride = 3 * sl.L.fstride;
         const size_t bytes = (size_t)sl.L.mstride * p->n_members * c->esz;
         c->slabs.push_back(sl);
@@ -529,6 +532,11 @@ pf_status create_common(const pf_params *p, int mode, int rank, int nranks, cons
         }
         cudaMemsetAsync(S.U, 0, bytes, c->stream);
         cudaMemsetAsync(S.Us, 0, bytes, c->stream);
+        e = pf::make_stream_plan(p->precision, S.L, S.U, S.Us, S.plan);
+        if (e != cudaSuccess) {
+            c->err = fmt("TMA tensor-map setup failed: %s", cudaGetErrorString(e));
+            return fail(PF_ERR_CUDA);
+        }
         const size_t pb = (size_t)p->n_members * pf::diag_blocks(S.L) * pf::kDiag * sizeof(double);
         if (cudaMalloc((void **)&S.partials, pb) != cudaSuccess ||
             cudaMalloc((void **)&S.diag, (size_t)p->n_members * pf::kDiag * sizeof(double)) != cudaSuccess) {
@@ -578,12 +586,13 @@ pf_status create_common(const pf_params *p, int mode, int rank, int nranks, cons
             fill_initial(*p, (int64_t)p->member_offset + m, S.L.y0, S.L.ny_loc, hc.data(), hp.data(), hr.data());
             const double *src[3] = {hc.data(), hp.data(), hr.data()};
             for (int f = 0; f < 3; ++f) {
-                char *dst = (char *)S.U + ((size_t)m * S.L.mstride + (size_t)f * S.L.fstride + 2 * (size_t)p->nx) * c->esz;
+                char *dst = (char *)S.U + ((size_t)m * S.L.mstride + (size_t)f * S.L.fstride + (size_t)S.L.at(0, 0)) * c->esz;
+                const size_t dp = (size_t)S.L.pitch * c->esz, w = (size_t)p->nx * c->esz;
                 if (c->esz == 8) {
-                    e = cudaMemcpy(dst, src[f], n * 8, cudaMemcpyHostToDevice);
+                    e = cudaMemcpy2D(dst, dp, src[f], w, w, S.L.ny_loc, cudaMemcpyHostToDevice);
                 } else {
                     std::vector<float> tmp(src[f], src[f] + n);
-                    e = cudaMemcpy(dst, tmp.data(), n * 4, cudaMemcpyHostToDevice);
+                    e = cudaMemcpy2D(dst, dp, tmp.data(), w, w, S.L.ny_loc, cudaMemcpyHostToDevice);
                 }
                 if (e != cudaSuccess) {
                     c->err = fmt("cudaMemcpy: %s", cudaGetErrorString(e));
@@ -591,6 +600,15 @@ pf_status create_common(const pf_params *p, int mode, int rank, int nranks, cons
                 }
             }
         }
+    }
+    for (auto &S : c->slabs) {   // ghost frames of both buffers (rho reservoir rows in Us too)
+        e = pf::launch_fill_ghosts(p->precision, S.L, p->rho_in, S.U, c->stream);
+        if (e == cudaSuccess) e = pf::launch_fill_ghosts(p->precision, S.L, p->rho_in, S.Us, c->stream);
+        if (e != cudaSuccess) {
+            c->err = fmt("fill_ghosts: %s", cudaGetErrorString(e));
+            return fail(PF_ERR_CUDA);
+        }
+        c->launches += 2 * pf::kFillLaunches;
     }
     st = exchange(c, 0);
     if (st != PF_OK) return fail(st);
@@ -800,8 +818,12 @@ pf_status pf_get_fields(pf_ctx *c, int32_t member, double *fc, double *fp, doubl
             if (!dst[f]) continue;
             char *h = (char *)dst[f] + (size_t)(S.L.y0 - c->y_host0) * hrow;
             if (c->esz == 8) {
-                const char *d = (const char *)S.U + ((size_t)m0 * S.L.mstride + (size_t)f * S.L.fstride + 2 * (size_t)c->p.nx) * 8;
-                CK(c, cudaMemcpy2DAsync(h, hmem, d, (size_t)S.L.mstride * 8, nloc * 8, nm, cudaMemcpyDeviceToHost, c->stream));
+                for (int mm = 0; mm < nm; ++mm) {
+                    const char *d = (const char *)S.U +
+                                    ((size_t)(m0 + mm) * S.L.mstride + (size_t)f * S.L.fstride + S.L.at(0, 0)) * 8;
+                    CK(c, cudaMemcpy2DAsync(h + mm * hmem, hrow, d, (size_t)S.L.pitch * 8, hrow, S.L.ny_loc,
+                                            cudaMemcpyDeviceToHost, c->stream));
+                }
             } else {
                 st = ensure_staging(c, nloc * nm);
                 if (st != PF_OK) return st;
@@ -830,8 +852,11 @@ pf_status pf_set_fields(pf_ctx *c, int32_t member, const double *fc, const doubl
             if (!src[f]) continue;
             const char *h = (const char *)src[f] + (size_t)(S.L.y0 - c->y_host0) * hrow;
             if (c->esz == 8) {
-                char *d = (char *)S.U + ((size_t)m0 * S.L.mstride + (size_t)f * S.L.fstride + 2 * (size_t)c->p.nx) * 8;
-                CK(c, cudaMemcpy2DAsync(d, (size_t)S.L.mstride * 8, h, hmem, nloc * 8, nm, cudaMemcpyHostToDevice, c->stream));
+                for (int mm = 0; mm < nm; ++mm) {
+                    char *d = (char *)S.U + ((size_t)(m0 + mm) * S.L.mstride + (size_t)f * S.L.fstride + S.L.at(0, 0)) * 8;
+                    CK(c, cudaMemcpy2DAsync(d, (size_t)S.L.pitch * 8, h + mm * hmem, hrow, hrow, S.L.ny_loc,
+                                            cudaMemcpyHostToDevice, c->stream));
+                }
             } else {
                 st = ensure_staging(c, nloc * nm);
                 if (st != PF_OK) return st;
@@ -840,6 +865,8 @@ pf_status pf_set_fields(pf_ctx *c, int32_t member, const double *fc, const doubl
                 c->launches += 1;
             }
         }
+        CK(c, pf::launch_fill_ghosts(c->p.precision, S.L, c->p.rho_in, S.U, c->stream));
+        c->launches += pf::kFillLaunches;
     }
     st = exchange(c, 0);
     if (st != PF_OK) return st;

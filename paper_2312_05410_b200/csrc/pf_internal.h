@@ -2,21 +2,28 @@
 // Not part of the ABI.  See DESIGN.md section 6 for the layout.
 #pragma once
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace pf {
 
 // Device layout of one state buffer:
-//   [member][field = c, phi, rho][row = -2 .. ny_loc+1][x = 0 .. nx-1]
-// Row r of a field lives at storage row r + 2: two ghost rows below and above the owned rows
-// carry the neighbouring slab's rows in slab mode.  x has no ghost columns (periodic wrap is
-// done by index in the kernels).
+//   [member][field = c, phi, rho][row = -2 .. ny_loc+1][x = -gx .. nx+gx-1]
+// Row r of a field lives at storage row r + 2 and column x at storage column x + gx, so the
+// ghost frame is physically present: gx = 16 bytes / sizeof(real) ghost columns on each side
+// hold the periodic copies, two ghost rows below / above hold the y-mirror rows (c, phi), the
+// rho reservoir value rho_in (top) or, at a slab-interior face, the neighbouring slab's rows.
+// The streaming kernel keeps the frame up to date as it writes; fill_ghosts rebuilds it after
+// host writes.  With the frame present, a TMA box needs no wrap or mirror logic.
 struct Layout {
     int nx, ny, ny_loc, y0;      // global grid, owned rows, first owned global row
     int members;
     int path;                    // stage kernel: 0 auto (streaming when eligible), 1 tile, 2 streaming
-    int64_t fstride;             // elements per field  = (ny_loc + 4) * nx
+    int gx;                      // ghost columns per side (16 B / element size)
+    int pitch;                   // elements per storage row = nx + 2 gx
+    int64_t fstride;             // elements per field  = (ny_loc + 4) * pitch
     int64_t mstride;             // elements per member = 3 * fstride
+    __host__ __device__ int64_t at(int r, int x) const { return (int64_t)(r + 2) * pitch + (x + gx); }
 };
 
 // Coefficients of the discrete model, folded on the host once per ctx.
@@ -33,24 +40,41 @@ struct Coef {
     double W_p;                     // W_phi (diagnostics)
 };
 
+// Streaming-kernel plan of one slab (host-built once per ctx): strip geometry and the 3D TMA
+// tensor maps (x, storage row, member*3 + field) of the two state buffers.
+struct StreamPlan {
+    bool ok = false;
+    int ncw = 0, Wo = 0, strips = 0;
+    int box_x = 0;                  // Wo + 2 halo columns (16 B each side)
+    int rows1 = 0, rows2 = 0;       // rows per TMA box: stage 1 / stage 2
+    CUtensorMap mapU1, mapUs1;      // box (box_x, rows1, 3) over U / Us
+    CUtensorMap mapU2, mapUs2;      // box (box_x, rows2, 3) over U / Us
+};
+
 // Number of values in a per-member diagnostics record (internal).
 // [0] sum c, [1] sum phi, [2] sum rho, [3] E_h, [4] cells with any non-finite field,
 // [5] non-finite c, [6] non-finite phi, [7] non-finite rho.
 constexpr int kDiag = 8;
 
-// Launchers (pf_kernels.cu).  All return the cudaError_t of the launch.
-// stage: out = base + coef * R(in)   (base may alias out: each cell reads its own base value
-// before writing it; `in` must not alias `out`).
-cudaError_t launch_stage(int precision, const Layout &L, const Coef &K, const void *in,
-                         const void *base, void *out, const void *vel, double coef,
+// Build the streaming plan (tensor maps) for buffers U, Us of layout L; plan.ok = false when
+// the grid is not eligible or the tile path is forced (then the tile kernel is used).
+cudaError_t make_stream_plan(int precision, const Layout &L, void *U, void *Us, StreamPlan &plan);
+// stage: out = base + coef * R(in).  stage 1: in = U, base = U, out = Us; stage 2: in = Us,
+// base = U, out = U (each cell reads its own base value before writing it).
+cudaError_t launch_stage(int precision, const Layout &L, const StreamPlan &plan, const Coef &K, int stage,
+                         const void *in, const void *base, void *out, const void *vel, double coef,
                          cudaStream_t s);
+// Rebuild the ghost frame of a buffer from its owned cells (periodic columns; mirror rows and
+// the rho reservoir at global y boundaries).  Slab-interior ghost rows are left to the exchange.
+cudaError_t launch_fill_ghosts(int precision, const Layout &L, double rho_in, void *state, cudaStream_t s);
+constexpr int kFillLaunches = 2;
 // diag: per-member kDiag doubles into out[members * kDiag]; `partials` scratch of
 // members * diag_blocks() * kDiag doubles.  The energy's top y-face of the last owned row is
 // included only when the next global row exists (uses the ghost row in slab mode).
 int diag_blocks(const Layout &L);
 cudaError_t launch_diag(int precision, const Layout &L, const Coef &K, const void *state,
                         double *partials, double *out, cudaStream_t s);
-// field <-> contiguous fp64 [members][ny_loc][nx] (for fp32 storage; fp64 uses memcpy).
+// field <-> contiguous fp64 [members][ny_loc][nx].
 cudaError_t launch_pack_f64(int precision, const Layout &L, int field, int member0, int nmem,
                             const void *state, double *dst, cudaStream_t s);
 cudaError_t launch_unpack_f64(int precision, const Layout &L, int field, int member0, int nmem,

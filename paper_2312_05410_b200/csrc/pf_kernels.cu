@@ -1,32 +1,43 @@
 // pf_kernels.cu -- sm_100a kernels of the PVD phase-field midpoint step.
 //
-// stage_kernel: one fused pass per explicit-midpoint stage (section 4.2):
-//   load a tile of c, phi (+2 halo) and rho (+1 halo) into shared memory, applying the ghost
-//   rules (x periodic, y mirror for c/phi, rho mirror below / reservoir above; R-12),
-//   phase 1: h, p, e, M_c, mu_c, mu_phi on the tile + 1-ring (R-2..R-7),
-//   phase 2: conservative flux divergence R_c, M_phi L(mu_phi), source S, vapour R_rho,
-//            and the Euler-form update out = base + coef R (R-11).
-// diag_kernel: fp64 sums, free energy E_h and non-finite counts, fixed-order reductions.
+// stream_kernel (performance path): one fused pass per explicit-midpoint stage (P:348 section
+//   4.2).  Persistent blocks walk x-strips of the grid in y.  A producer warp streams boxes of
+//   R rows x 3 fields (c, phi, rho) of a strip -- plus the stage-2 base rows -- into a shared-
+//   memory ring with 3D TMA tensor copies (cp.async.bulk.tensor, mbarrier completion); compute
+//   warps evaluate mu / M once per cell (row a2) and the flux divergence, source, vapour and
+//   Euler-form update (rows a3-a5), exchanging x-neighbours by warp shuffles, and write the
+//   result together with its ghost-frame copies (row a1).
+// stage_kernel (fallback path, any nx): 2D shared-memory tiles with a 2-cell halo, ghost rules
+//   applied by index.
+// diag_kernel: fp64 sums, free energy E_h and non-finite counts with fixed-order reductions.
 //
-// Every cell's value comes from the same inlined code path (interior, tile ring, slab edge),
-// so results are bitwise independent of tiling, x-translation and slab decomposition.
+// Every cell's value comes from the same arithmetic (pf_cell.cuh) on every path, so results are
+// bitwise independent of the kernel path, tiling, x-translation and slab decomposition.
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
+#include <cudaTypedefs.h>
 
 #include "pf_cell.cuh"
 #include "pf_internal.h"
 
 namespace pf {
+
+int env_int(const char *name, int dflt) {
+    const char *v = getenv(name);
+    return v ? atoi(v) : dflt;
+}
+
 namespace {
 
+// ========================================================================================
+// Tile kernel (fallback)
 constexpr int BX = 32;   // tile width  (one warp across x)
 constexpr int BY = 16;   // tile height
 constexpr int NT = 256;  // threads per block (32 x 8)
 
-// Local storage row (relative to owned row 0) holding the c/phi value of local row ly,
-// after the global mirror rule (R-12).  Clamped so that rows no output depends on stay
-// in bounds.
+// Local row holding the c/phi value of local row ly after the global mirror rule (R-12),
+// clamped so that rows no output depends on stay in bounds.
 __device__ __forceinline__ int row_cphi(int ly, const Layout &L) {
     int g = L.y0 + ly;
     if (g < 0) g = -1 - g;
@@ -59,17 +70,14 @@ __global__ void __launch_bounds__(NT) stage_kernel(Layout L, KC<real> k, const r
     const int tx0 = blockIdx.x * BX;
     const int ty0 = blockIdx.y * BY;
     const int nx = L.nx;
-    const int64_t row0 = 2 * (int64_t)nx;                 // storage offset of owned row 0
-    const real *ic = in + m * L.mstride + row0;
+    const real *ic = in + m * L.mstride;
     const real *ip = ic + L.fstride;
     const real *ir = ip + L.fstride;
 
     // ---- load c, phi with a 2-cell halo (ghost rules applied by index) ----
     for (int t = threadIdx.x; t < (BY + 4) * (BX + 4); t += NT) {
         const int sy = t / (BX + 4), sx = t - sy * (BX + 4);
-        const int gx = wrap_x(tx0 - 2 + sx, nx);
-        const int r = row_cphi(ty0 - 2 + sy, L);
-        const int64_t off = (int64_t)r * nx + gx;
+        const int64_t off = L.at(row_cphi(ty0 - 2 + sy, L), wrap_x(tx0 - 2 + sx, nx));
         sc[sy][sx] = ic[off];
         sp[sy][sx] = ip[off];
     }
@@ -86,27 +94,20 @@ __global__ void __launch_bounds__(NT) stage_kernel(Layout L, KC<real> k, const r
             int r = g - L.y0;
             r = r < -2 ? -2 : r;
             r = r > L.ny_loc + 1 ? L.ny_loc + 1 : r;
-            v = ir[(int64_t)r * nx + gx];
+            v = ir[L.at(r, gx)];
         }
         sr[sy][sx] = v;
     }
     __syncthreads();
 
     // ---- phase 1: mu_c, mu_phi, M on the tile + 1 ring ----
-    // A ring cell outside the global y range takes the values of its mirror cell (computed by
-    // the same code from the same inputs), which makes the boundary face fluxes exactly zero.
     for (int t = threadIdx.x; t < (BY + 2) * (BX + 2); t += NT) {
         const int sy = t / (BX + 2), sx = t - sy * (BX + 2);
-        int g = L.y0 + ty0 - 1 + sy;
-        if (g < 0) g = -1 - g;
-        if (g >= L.ny) g = 2 * L.ny - 1 - g;
-        int ey = g - L.y0 - (ty0 - 2);                       // row in sc/sp
-        ey = ey < 1 ? 1 : (ey > BY + 2 ? BY + 2 : ey);
-        const int ex = sx + 1;
+        const int ey = sy + 1, ex = sx + 1;
         real mc, mp, M;
         constitutive<real, HMIX>(k, etab, sc[ey][ex], sp[ey][ex], sc[ey][ex - 1], sc[ey][ex + 1], sc[ey - 1][ex],
-                           sc[ey + 1][ex], sp[ey][ex - 1], sp[ey][ex + 1], sp[ey - 1][ex],
-                           sp[ey + 1][ex], mc, mp, M);
+                                 sc[ey + 1][ex], sp[ey][ex - 1], sp[ey][ex + 1], sp[ey - 1][ex], sp[ey + 1][ex], mc,
+                                 mp, M);
         smc[sy][sx] = mc;
         smp[sy][sx] = mp;
         sM[sy][sx] = M;
@@ -122,7 +123,7 @@ __global__ void __launch_bounds__(NT) stage_kernel(Layout L, KC<real> k, const r
         if (gx >= nx || ly >= L.ny_loc) continue;
         const int y = q + 1, x = lx + 1;                    // ring coordinates
         const int cy = q + 2, cx = lx + 2;                   // c/phi tile coordinates
-        const int64_t o = m * L.mstride + row0 + (int64_t)ly * nx + gx;
+        const int64_t o = m * L.mstride + L.at(ly, gx);
         real oc, op, orr;
         const real fe = face_flux<real>(sM[y][x], sM[y][x + 1], smc[y][x], smc[y][x + 1]);
         const real fw = face_flux<real>(sM[y][x - 1], sM[y][x], smc[y][x - 1], smc[y][x]);
@@ -139,7 +140,54 @@ __global__ void __launch_bounds__(NT) stage_kernel(Layout L, KC<real> k, const r
     }
 }
 
-// ----------------------------------------------------------------------------------------
+// ========================================================================================
+// Ghost frame (row a1 in memory)
+template <typename real>
+__global__ void ghost_rows_kernel(Layout L, real rho_in, real *st) {
+    // global y boundaries: c, phi mirror (r = -1 - g); rho: bottom mirror, top reservoir
+    const int64_t per = (int64_t)4 * L.nx;   // 2 rows below + 2 rows above
+    const int64_t total = per * 3 * L.members;
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t mf = q / per;
+        const int rem = (int)(q - mf * per);
+        const int slot = rem / L.nx, x = rem - slot * L.nx;
+        const int f = (int)(mf % 3);
+        real *b = st + mf * L.fstride;
+        if (slot < 2) {                           // ghost rows -1, -2 of the bottom slab
+            if (L.y0 != 0) continue;
+            const int r = -1 - slot;
+            b[L.at(r, x)] = b[L.at(-1 - r, x)];
+        } else {                                  // ghost rows ny_loc, ny_loc+1 of the top slab
+            if (L.y0 + L.ny_loc != L.ny) continue;
+            const int r = L.ny_loc + (slot - 2);
+            b[L.at(r, x)] = (f == 2) ? rho_in : b[L.at(2 * L.ny_loc - 1 - r, x)];
+        }
+    }
+}
+
+template <typename real>
+__global__ void ghost_cols_kernel(Layout L, real *st) {
+    // periodic x ghost columns of every storage row (incl. ghost rows -> corners)
+    const int gx = L.gx;
+    const int64_t rows = (int64_t)(L.ny_loc + 4) * 3 * L.members;
+    const int64_t total = rows * 2 * gx;
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = q / (2 * gx);
+        const int j = (int)(q - row * 2 * gx);
+        const int64_t mf = row / (L.ny_loc + 4);
+        const int r = (int)(row - mf * (L.ny_loc + 4)) - 2;
+        real *b = st + mf * L.fstride;
+        if (j < gx) {
+            const int x = -gx + j;                // left ghost <- x + nx
+            b[L.at(r, x)] = b[L.at(r, x + L.nx)];
+        } else {
+            const int x = L.nx + (j - gx);        // right ghost <- x - nx
+            b[L.at(r, x)] = b[L.at(r, x - L.nx)];
+        }
+    }
+}
+
+// ========================================================================================
 // diagnostics
 constexpr int DT = 256;
 
@@ -154,8 +202,7 @@ __global__ void __launch_bounds__(DT) diag_kernel(Layout L, Coef K, const real *
                                                   double *partials) {
     const int m = blockIdx.y;
     const int nx = L.nx;
-    const int64_t row0 = 2 * (int64_t)nx;
-    const real *c = st + m * L.mstride + row0;
+    const real *c = st + m * L.mstride;
     const real *p = c + L.fstride;
     const real *r = p + L.fstride;
     double acc[kDiag];
@@ -164,19 +211,21 @@ __global__ void __launch_bounds__(DT) diag_kernel(Layout L, Coef K, const real *
     const int64_t ncell = (int64_t)L.ny_loc * nx;
     for (int64_t k = (int64_t)blockIdx.x * DT + threadIdx.x; k < ncell; k += (int64_t)gridDim.x * DT) {
         const int ly = (int)(k / nx), i = (int)(k - (int64_t)ly * nx);
-        const double cc = (double)c[k], pp = (double)p[k], rr = (double)r[k];
+        const int64_t o = L.at(ly, i);
+        const double cc = (double)c[o], pp = (double)p[o], rr = (double)r[o];
         const bool fc = isfinite(cc), fp = isfinite(pp), fr = isfinite(rr);
         acc[0] += cc;
         acc[1] += pp;
         acc[2] += rr;
-        const int ir = (i + 1 == nx) ? 0 : i + 1;
-        const double dcx = (double)c[(int64_t)ly * nx + ir] - cc;
-        const double dpx = (double)p[(int64_t)ly * nx + ir] - pp;
+        const int64_t ox = L.at(ly, (i + 1 == nx) ? 0 : i + 1);
+        const double dcx = (double)c[ox] - cc;
+        const double dpx = (double)p[ox] - pp;
         const double omc = 1.0 - cc, omp = 1.0 - pp;
         double e = K.dx2 * (K.W_c * (cc * cc) * (omc * omc) * pp + K.W_p * (pp * pp) * (omp * omp));
         e += K.half_kc * (dcx * dcx) + K.half_kp * (dpx * dpx);
         if (L.y0 + ly < L.ny - 1) {      // y-face above (ghost row at the slab top)
-            const double dcy = (double)c[k + nx] - cc, dpy = (double)p[k + nx] - pp;
+            const int64_t oy = L.at(ly + 1, i);
+            const double dcy = (double)c[oy] - cc, dpy = (double)p[oy] - pp;
             e += K.half_kc * (dcy * dcy) + K.half_kp * (dpy * dpy);
         }
         acc[3] += e;
@@ -232,7 +281,8 @@ __global__ void pack_kernel(Layout L, int field, int member0, int nmem, const re
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < total;
          k += (int64_t)gridDim.x * blockDim.x) {
         const int64_t mm = k / per, rem = k - mm * per;
-        dst[k] = (double)st[(member0 + mm) * L.mstride + field * L.fstride + 2 * (int64_t)L.nx + rem];
+        const int r = (int)(rem / L.nx), x = (int)(rem - (int64_t)r * L.nx);
+        dst[k] = (double)st[(member0 + mm) * L.mstride + field * L.fstride + L.at(r, x)];
     }
 }
 
@@ -243,27 +293,13 @@ __global__ void unpack_kernel(Layout L, int field, int member0, int nmem, const 
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < total;
          k += (int64_t)gridDim.x * blockDim.x) {
         const int64_t mm = k / per, rem = k - mm * per;
-        st[(member0 + mm) * L.mstride + field * L.fstride + 2 * (int64_t)L.nx + rem] = (real)src[k];
+        const int r = (int)(rem / L.nx), x = (int)(rem - (int64_t)r * L.nx);
+        st[(member0 + mm) * L.mstride + field * L.fstride + L.at(r, x)] = (real)src[k];
     }
 }
 
-
-// ----------------------------------------------------------------------------------------
-// Streaming stage kernel (the performance path).
-//
-// A persistent grid (one resident wave) walks the work in y.  The work is the concatenation of
-// all (member, x-strip) columns of W cells, each ny_loc rows tall; block b owns the contiguous
-// row range [R b / B, R (b+1) / B) of that concatenation, so every block gets the same number of
-// rows (+-1) and only pays the halo prologue at its 1-2 segment starts.
-//
-// Rows arrive through a TMA bulk-copy ring (cp.async.bulk global -> shared, completion on an
-// mbarrier per slot, S slots, issued S-3 rows ahead by thread 0).  Load k of a segment carries
-// c/phi row k (+-HL halo columns, x wrap by separate copies), rho row k-1 and, for stage 2, the
-// base row k-2.  Each thread owns one column: it keeps a sliding register window of its own
-// column and takes x-neighbours from shared memory.  Per row: mu/M of row k-1 (own column plus
-// two halo columns) -> smem, one __syncthreads, then the update of row k-2 and its coalesced
-// store.  The arithmetic per cell is pf_cell.cuh's, the same as the tile kernel's.
-
+// ========================================================================================
+// Streaming kernel
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return (uint32_t)__cvta_generic_to_shared(p);
 }
@@ -277,12 +313,8 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                  : "memory");
 }
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     asm volatile(
@@ -293,29 +325,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
-
-// Streaming kernel configuration: NCW compute warps per block, each producing 30 output columns
-// (it evaluates mu / M on 32 columns: its 30 plus one on each side), so a strip is at most
-// 30 NCW columns wide; S ring slots.
-template <typename real, int NCW, int S, bool BASE>
-struct StreamCfg {
-    static constexpr int HL = 16 / (int)sizeof(real);   // halo columns loaded (one 16 B chunk)
-    static constexpr int WMAX = (30 * NCW + HL - 1) / HL * HL;   // widest strip (16 B multiple)
-    static constexpr int RW = 32 * NCW + 2 * HL;        // smem row width (>= WMAX + 2 HL + 2)
-    static constexpr int SLOT = 3 * RW + (BASE ? 3 * WMAX : 0);   // c, phi, rho (+ base) rows
-    static constexpr size_t bytes = (size_t)S * SLOT * sizeof(real) + (size_t)S * 16 + 64 * 8;
-};
-
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+// 3D TMA tile load: box at (x, y, z) of the tensor map -> shared memory, completion on bar.
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, int x, int y, int z, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap *map) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
 
-// Work schedule shared by the producer and the compute warps.  Grouped mode (G > 0): blocks come in
-// groups of `strips`; block b works on strip b % strips of the row range [T g/G, T (g+1)/G) of the
-// concatenated (member, row) space (T = members * ny_loc rows, g = b / strips), so the blocks of a
-// group stream the same rows at the same time and DRAM sees whole contiguous rows.  Ungrouped
-// mode (G == 0): block b owns the row range [R b/B, R (b+1)/B) of the concatenated
-// (member, strip, row) space, R = members * strips * ny_loc.
+// Work schedule shared by the producer and the compute warps.  Grouped mode (G > 0): blocks come
+// in groups of `strips`; block b works on strip b % strips of the row range [T g/G, T (g+1)/G) of
+// the concatenated (member, row) space (T = members * ny_loc rows, g = b / strips), so the blocks
+// of a group stream the same rows at the same time.  Ungrouped mode (G == 0): block b owns the
+// row range [R b/B, R (b+1)/B) of the concatenated (member, strip, row) space.
 struct Seg {
     int m, x0, Wp, ya, yb;
 };
@@ -360,25 +386,65 @@ __device__ __forceinline__ bool next_seg(const Layout &L, int Wo, const Sched &s
     return true;
 }
 
-template <typename real, int NCW, int S, bool BASE, bool HMIX>
-__global__ void __launch_bounds__(32 * NCW + 32, (NCW >= 8 ? 2 : 4)) stream_kernel(
-    Layout L, KC<real> k, const real *__restrict__ in, const real *__restrict__ base, real *out,
-    const real *__restrict__ vel, int Wo, int G, int dbg) {
-    // dbg != 0 (PF_STREAM_DBG, experiments only): skip the arithmetic, keep every load and store.
-    // BASE: stage 2 (the update base u^n is a separate buffer, streamed through the ring);
-    // otherwise stage 1 (base = the stage input).
-    // Warp roles.  Warps [0, NCW): compute.  Warp NCW: producer -- lane 0 issues the TMA bulk
-    // copies of the row ring, gated per slot by an "empty" mbarrier that every compute warp
-    // arrives on once it is done with the slot.  Compute warps never synchronise with each other:
-    // warp w owns output columns x0 + 30w + [0, 30); lane l evaluates mu / M at column
-    // x0 + 30w - 1 + l and passes them to lanes l -+ 1 by warp shuffles.  The row loop is unrolled
-    // by 3 and computes unconditionally (only stores are predicated), so the per-lane sliding
-    // windows rotate by register renaming.
-    using Cfg = StreamCfg<real, NCW, S, BASE>;
-    constexpr int HL = Cfg::HL, RW = Cfg::RW, SLOT = Cfg::SLOT, WMAX = Cfg::WMAX;
+// Shared-memory geometry of the ring (runtime box width bx).
+template <typename real>
+struct Ring {
+    int bx;            // box width in elements (Wo + 2 HL)
+    int in_elems;      // one input box: 3 fields x R rows x bx (rounded to 128 B)
+    int slot_elems;    // input box (+ base box for stage 2)
+    __host__ __device__ static int round128(int elems) {
+        const int b = elems * (int)sizeof(real);
+        return ((b + 127) / 128 * 128) / (int)sizeof(real);
+    }
+    __host__ __device__ Ring(int bx_, int R, bool base) : bx(bx_) {
+        in_elems = round128(3 * R * bx);
+        slot_elems = in_elems * (base ? 2 : 1);
+    }
+};
+
+template <typename real>
+size_t stream_smem_bytes(int bx, int R, int S, bool base) {
+    Ring<real> rg(bx, R, base);
+    return 128 + (size_t)S * rg.slot_elems * sizeof(real) + 64 * sizeof(real) /* read slack */ +
+           (size_t)S * 16 + 64 * 8;
+}
+
+// Store one output value (field f, local row r, column x) and its ghost-frame copies: periodic
+// x ghost columns and, at the global y boundaries, the mirror ghost rows (c, phi; rho at the
+// bottom; rho's top ghost rows hold the reservoir value and are never overwritten).
+template <typename real>
+__device__ __forceinline__ void store_with_ghosts(const Layout &L, real *b, int f, int r, int x, real v) {
+    const int g = L.y0 + r;
+    int rr[2];
+    int nr = 0;
+    rr[nr++] = r;
+    if (g <= 1) rr[nr++] = -1 - r;                                        // y0 == 0 here
+    else if (g >= L.ny - 2 && f != 2) rr[nr++] = 2 * L.ny_loc - 1 - r;    // top slab
+    for (int q = 0; q < nr; ++q) {
+        b[L.at(rr[q], x)] = v;
+        if (x < L.gx) b[L.at(rr[q], x + L.nx)] = v;
+        if (x >= L.nx - L.gx) b[L.at(rr[q], x - L.nx)] = v;
+    }
+}
+
+template <typename real, int NCW, int R, int S, bool BASE, bool HMIX>
+__global__ void __launch_bounds__(32 * NCW + 32, (NCW >= 6 ? 2 : 3)) stream_kernel(
+    Layout L, KC<real> k, const __grid_constant__ CUtensorMap mapIn, const __grid_constant__ CUtensorMap mapBase,
+    real *out, const real *__restrict__ vel, int Wo, int G) {
+    // Warp roles.  Warps [0, NCW): compute.  Warp NCW: producer -- lane 0 issues one TMA box per
+    // ring slot (R rows x 3 fields of the strip with 16 B halo columns on each side, plus the base
+    // box in stage 2), gated per slot by an "empty" mbarrier that every compute warp arrives on
+    // once it no longer reads the slot.  Compute warps never synchronise with each other: warp w
+    // owns output columns x0 + 30w + [0, 30); lane l evaluates mu / M at column x0 + 30w - 1 + l
+    // and passes them to lanes l -+ 1 by warp shuffles.  Rows are consumed R per slot (unrolled),
+    // computing unconditionally (only stores are predicated) so the per-lane sliding windows
+    // rotate by register renaming.
+    constexpr int HL = 16 / (int)sizeof(real);
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    real *slots = reinterpret_cast<real *>(smem_raw);
-    uint64_t *full = reinterpret_cast<uint64_t *>(slots + S * SLOT);
+    const int bx = Wo + 2 * HL;
+    const Ring<real> rg(bx, R, BASE);
+    real *slots = reinterpret_cast<real *>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~(uintptr_t)127);
+    uint64_t *full = reinterpret_cast<uint64_t *>(slots + S * rg.slot_elems + 64);
     uint64_t *empty = full + S;
     double *etab = reinterpret_cast<double *>(empty + S);
     load_exp_table(etab);
@@ -396,73 +462,46 @@ __global__ void __launch_bounds__(32 * NCW + 32, (NCW >= 8 ? 2 : 4)) stream_kern
 
     const int nx = L.nx;
     const Sched sch = make_sched(L, Wo, G);
+    const uint32_t box_bytes = (uint32_t)(3 * R * bx * sizeof(real));
 
     if (warp == NCW) {
         // ------------------------------- producer -------------------------------
         if (lane != 0) return;
+        prefetch_tmap(&mapIn);
+        if (BASE) prefetch_tmap(&mapBase);
         uint32_t g = 0;
         int64_t pos = sch.lo;
         Seg sg;
         while (next_seg(L, Wo, sch, pos, sg)) {
-            const int n = sg.yb - sg.ya + 4, npad = (n + 2) / 3 * 3;
-            const real *fin = in + sg.m * L.mstride + 2 * (int64_t)nx;
-            const real *fba = base + sg.m * L.mstride + 2 * (int64_t)nx;
-            const bool wrapl = (sg.x0 == 0), wrapr = (sg.x0 + sg.Wp == nx);
-            const uint32_t rowb = (uint32_t)((sg.Wp + 2 * HL) * sizeof(real));
-            const uint32_t bb = (uint32_t)(sg.Wp * sizeof(real));
-            for (int i = 0; i < npad; ++i, ++g) {
+            const int n = sg.yb - sg.ya + 4, nsl = (n + R - 1) / R;
+            for (int j = 0; j < nsl; ++j, ++g) {
                 const int slot = g % S;
                 if (g >= (uint32_t)S) mbar_wait(&empty[slot], ((g / S) - 1) & 1u);
-                if (i >= n) {
-                    mbar_arrive(&full[slot]);          // padding: completes the phase, no data
-                    continue;
-                }
-                const int kk = sg.ya - 2 + i;
-                real *sl = slots + slot * SLOT;
-                const int rc = row_cphi(kk, L);                   // c/phi source row (mirror rule)
-                int grho = L.y0 + kk - 1;
-                const bool rho_res = grho >= L.ny;                // reservoir row: rho_in, no copy
-                if (grho < 0) grho = -1 - grho;
-                const int rr = grho - L.y0;
-                const bool wb = BASE && (kk - 2 >= sg.ya) && (kk - 2 < sg.yb);
-                mbar_expect_tx(&full[slot], (rho_res ? 2u : 3u) * rowb + (wb ? 3u * bb : 0u));
-                for (int f = 0; f < 3; ++f) {
-                    if (f == 2 && rho_res) continue;
-                    const real *row = fin + f * L.fstride + (int64_t)(f == 2 ? rr : rc) * nx;
-                    real *d = sl + f * RW;
-                    if (!wrapl && !wrapr) {
-                        bulk_g2s(d, row + sg.x0 - HL, rowb, &full[slot]);
-                    } else {
-                        bulk_g2s(d, row + (wrapl ? nx - HL : sg.x0 - HL), HL * sizeof(real), &full[slot]);
-                        bulk_g2s(d + HL, row + sg.x0, bb, &full[slot]);
-                        bulk_g2s(d + HL + sg.Wp, row + (wrapr ? 0 : sg.x0 + sg.Wp), HL * sizeof(real), &full[slot]);
-                    }
-                }
-                if (wb)
-                    for (int f = 0; f < 3; ++f)
-                        bulk_g2s(sl + 3 * RW + f * WMAX, fba + f * L.fstride + (int64_t)(kk - 2) * nx + sg.x0, bb,
-                                 &full[slot]);
+                real *sl = slots + slot * rg.slot_elems;
+                const int k0 = sg.ya - 2 + j * R;                 // first row of the box
+                mbar_expect_tx(&full[slot], BASE ? 2 * box_bytes : box_bytes);
+                // x: storage column of x0 - HL is x0 (gx == HL); y: storage row of k0 is k0 + 2
+                tma_load_3d(sl, &mapIn, sg.x0, k0 + 2, 3 * sg.m, &full[slot]);
+                if (BASE) tma_load_3d(sl + rg.in_elems, &mapBase, sg.x0, k0, 3 * sg.m, &full[slot]);
             }
         }
         return;
     }
 
     // --------------------------- compute warps ---------------------------------
-    static_assert(S >= 4, "ring depth");
     const int cx = 30 * warp - 1 + lane;    // strip-relative column of this lane's mu / M
-    const int ci = HL + cx;                 // its smem index
-    const int bi = cx < 0 ? 0 : (cx >= WMAX ? WMAX - 1 : cx);   // base index (in range)
-    int sidx = 0;                           // ring slot of the first load of the current group
+    const int ci = HL + cx;                 // its column in a box row
+    const int plane = R * bx;               // elements per field plane of a box
+    int sidx = 0;                           // ring slot of the current box
     uint32_t par = 0;                       // its full-barrier phase parity
     int64_t pos = sch.lo;
     Seg sg;
     while (next_seg(L, Wo, sch, pos, sg)) {
-        const int n = sg.yb - sg.ya + 4, npad = (n + 2) / 3 * 3;
+        const int n = sg.yb - sg.ya + 4, nsl = (n + R - 1) / R;
+        const int x = sg.x0 + cx;           // global column of this lane
         const bool store = lane >= 1 && lane <= 30 && cx < sg.Wp;
-        const int64_t fs1 = L.fstride;
-        real *op_ = out + sg.m * L.mstride + 2 * (int64_t)nx + (int64_t)(sg.ya - 4) * nx + sg.x0 + bi;
+        real *ob = out + sg.m * L.mstride;
         const real vx = vel[2 * sg.m], vy = vel[2 * sg.m + 1];
-        const int rho_res_i = L.ny - L.y0 - sg.ya + 3;   // first load whose rho row is the reservoir
 
         real c_m2 = 0, c_m1 = 0, c_0 = 0;                 // c rows k-2, k-1, k (own column)
         real p_m3 = 0, p_m2 = 0, p_m1 = 0, p_0 = 0;       // phi rows k-3 .. k
@@ -471,47 +510,25 @@ __global__ void __launch_bounds__(32 * NCW + 32, (NCW >= 8 ? 2 : 4)) stream_kern
         real b_m3 = 0, b_m2 = 0, b_m1 = 0;                // mu_phi rows k-3 .. k-1
         real M_m2 = 0, M_m1 = 0;                          // M rows k-2, k-1
         real fn_m = 0;                                    // north face flux of row k-3
-        for (int i0 = 0; i0 < npad; i0 += 3) {
-            // ring slots of this group of 3 loads and of the 2 loads before it (wrapping mod S)
-            const int q1 = sidx + 1 >= S ? sidx + 1 - S : sidx + 1;
-            const int q2 = sidx + 2 >= S ? sidx + 2 - S : sidx + 2;
-            const int qm1 = sidx >= 1 ? sidx - 1 : sidx - 1 + S;
-            const int qm2 = sidx >= 2 ? sidx - 2 : sidx - 2 + S;
-            const real *gq[5] = {slots + qm2 * SLOT + ci, slots + qm1 * SLOT + ci, slots + sidx * SLOT + ci,
-                                 slots + q1 * SLOT + ci, slots + q2 * SLOT + ci};
-            const int qs[5] = {qm2, qm1, sidx, q1, q2};
+        const real *prev = slots + (sidx == 0 ? S - 1 : sidx - 1) * rg.slot_elems + ci;
+        for (int j = 0; j < nsl; ++j) {
+            const real *cur = slots + sidx * rg.slot_elems + ci;
+            mbar_wait(&full[sidx], par);
 #pragma unroll
-            for (int u = 0; u < 3; ++u) {
-                const int i = i0 + u;
-                const real *s0 = gq[u + 2];                                          // load k
-                const real *s1 = gq[u + 1];                                          // load k-1
-                const real *s2 = gq[u];                                              // load k-2
-                mbar_wait(&full[qs[u + 2]], par ^ (uint32_t)(sidx + u >= S));
-                c_m2 = c_m1; c_m1 = c_0; c_0 = s0[0];
-                p_m3 = p_m2; p_m2 = p_m1; p_m1 = p_0; p_0 = s0[RW];
-                r_m3 = r_m2; r_m2 = r_m1;
-                r_m1 = (i >= rho_res_i) ? k.rho_in : s0[2 * RW];
+            for (int u = 0; u < R; ++u) {
+                const int i = j * R + u;                  // row k = ya - 2 + i
+                const real *rk = cur + u * bx;                                             // row k
+                const real *rk1 = u >= 1 ? cur + (u - 1) * bx : prev + (R - 1) * bx;       // row k-1
+                const real *rk2 = u >= 2 ? cur + (u - 2) * bx : prev + (R - 2 + u) * bx;   // row k-2
+                c_m2 = c_m1; c_m1 = c_0; c_0 = rk[0];
+                p_m3 = p_m2; p_m2 = p_m1; p_m1 = p_0; p_0 = rk[plane];
+                r_m3 = r_m2; r_m2 = r_m1; r_m1 = rk1[2 * plane];
                 a_m2 = a_m1;
                 b_m3 = b_m2; b_m2 = b_m1;
                 M_m2 = M_m1;
-                if (dbg) {
-                    if (dbg == 2 && warp < 8 && i >= 4 && i < n) {   // sector-aligned experiment
-                        real *o2 = op_ - bi + 32 * warp + lane;
-                        o2[0] = c_m2; o2[fs1] = p_m2; o2[2 * fs1] = r_m2;
-                    } else if (dbg == 1 && store && i >= 4 && i < n) {
-                        const real *bs = s0 - ci + 3 * RW + bi;
-                        op_[0] = c_m2 + (BASE ? bs[0] : 0);
-                        op_[fs1] = p_m2 + (BASE ? bs[WMAX] : 0);
-                        op_[2 * fs1] = r_m2 + (BASE ? bs[2 * WMAX] : 0);
-                    }
-                    op_ += nx;
-                    __syncwarp();
-                    if (i >= 2 && lane == 0) mbar_arrive(&empty[qs[u]]);
-                    continue;
-                }
                 // mu / M of row k-1 at this lane's column
-                constitutive<real, HMIX>(k, etab, c_m1, p_m1, s1[-1], s1[1], c_m2, c_0, s1[RW - 1], s1[RW + 1], p_m2, p_0,
-                                         a_m1, b_m1, M_m1);
+                constitutive<real, HMIX>(k, etab, c_m1, p_m1, rk1[-1], rk1[1], c_m2, c_0, rk1[plane - 1],
+                                         rk1[plane + 1], p_m2, p_0, a_m1, b_m1, M_m1);
                 // update of row k-2.  East face flux from this lane's mu / M and lane+1's; the west
                 // flux is lane-1's east flux; the south flux is last row's north flux.
                 const real ar = __shfl_down_sync(0xffffffffu, a_m2, 1);
@@ -523,33 +540,38 @@ __global__ void __launch_bounds__(32 * NCW + 32, (NCW >= 8 ? 2 : 4)) stream_kern
                 const real fs = fn_m;
                 fn_m = fn;
                 real bc = c_m2, bp = p_m2, bq = r_m2;   // stage 1: base = input
-                if (BASE) {                               // stage 2: base row from the ring
-                    const real *bs = s0 - ci + 3 * RW + bi;
-                    bc = bs[0]; bp = bs[WMAX]; bq = bs[2 * WMAX];
+                if (BASE) {                               // stage 2: base row k-2 = row u of the base box
+                    const real *bs = cur + rg.in_elems + u * bx;
+                    bc = bs[0]; bp = bs[plane]; bq = bs[2 * plane];
                 }
                 real oc, op, orr;
                 cell_update<real>(k, vx, vy, fe, fw, fn, fs, b_m2, bl, br_, b_m3, b_m1,
-                                  s2[RW - 1], s2[RW + 1], p_m3, p_m1,
-                                  r_m2, s1[2 * RW - 1], s1[2 * RW + 1], r_m3, r_m1,
+                                  rk2[plane - 1], rk2[plane + 1], p_m3, p_m1,
+                                  r_m2, rk2[2 * plane - 1], rk2[2 * plane + 1], r_m3, r_m1,
                                   bc, bp, bq, oc, op, orr);
                 if (store && i >= 4 && i < n) {
-                    op_[0] = oc;
-                    op_[fs1] = op;
-                    op_[2 * fs1] = orr;
+                    const int r = sg.ya - 4 + i;          // local row k-2
+                    const bool edge = (x < L.gx) | (x >= nx - L.gx) | (L.y0 + r <= 1) | (L.y0 + r >= L.ny - 2);
+                    if (!edge) {
+                        const int64_t o = L.at(r, x);
+                        ob[o] = oc;
+                        ob[o + L.fstride] = op;
+                        ob[o + 2 * L.fstride] = orr;
+                    } else {
+                        store_with_ghosts<real>(L, ob, 0, r, x, oc);
+                        store_with_ghosts<real>(L, ob + L.fstride, 1, r, x, op);
+                        store_with_ghosts<real>(L, ob + 2 * L.fstride, 2, r, x, orr);
+                    }
                 }
-                op_ += nx;
-                __syncwarp();
-                if (i >= 2 && lane == 0) mbar_arrive(&empty[qs[u]]);   // load i-2 is no longer read
             }
-            sidx += 3;
-            if (sidx >= S) { sidx -= S; par ^= 1u; }
-        }
-        // release the last two loads of the segment
-        if (lane == 0) {
-            mbar_arrive(&empty[sidx >= 2 ? sidx - 2 : sidx - 2 + S]);
-            mbar_arrive(&empty[sidx >= 1 ? sidx - 1 : sidx - 1 + S]);
+            // the previous box is no longer read (its last row was row k-2 of iteration jR+1)
+            __syncwarp();
+            if (j >= 1 && lane == 0) mbar_arrive(&empty[sidx == 0 ? S - 1 : sidx - 1]);
+            prev = cur;
+            if (++sidx == S) { sidx = 0; par ^= 1u; }
         }
         __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[sidx == 0 ? S - 1 : sidx - 1]);   // the segment's last box
     }
 }
 
@@ -576,76 +598,71 @@ KC<real> make_kc(const Coef &K, double coef) {
     return k;
 }
 
-}  // namespace
+// Rows per box and ring depth: stage 1 R = 4, S = 4 (16 rows in flight); stage 2 R = 2, S = 6.
+constexpr int kR1 = 4, kS1 = 4, kR2 = 2, kS2 = 6;
 
-int env_int(const char *name, int dflt) {
-    const char *v = getenv(name);
-    return v ? atoi(v) : dflt;
-}
-
-template <typename real, int NCW, int S, bool BASE, bool HMIX>
-cudaError_t launch_stream_b(const Layout &L, const KC<real> &k, const real *in, const real *base,
-                            real *out, const real *vel, int Wo, cudaStream_t s) {
-    using Cfg = StreamCfg<real, NCW, S, BASE>;
+template <typename real, int NCW, int R, int S, bool BASE, bool HMIX>
+cudaError_t launch_stream_k(const Layout &L, const StreamPlan &P, const KC<real> &k, int stage, real *out,
+                            const real *vel, cudaStream_t s) {
+    const size_t smem = stream_smem_bytes<real>(P.box_x, R, S, BASE);
     static int occ = -1, nsm = 0;
-    if (occ < 0) {
-        cudaError_t e = cudaFuncSetAttribute(stream_kernel<real, NCW, S, BASE, HMIX>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::bytes);
+    static size_t smem_set = 0;
+    auto kern = stream_kernel<real, NCW, R, S, BASE, HMIX>;
+    if (smem > smem_set) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
+        smem_set = smem;
+        occ = -1;
+    }
+    if (occ < 0) {
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stream_kernel<real, NCW, S, BASE, HMIX>, 32 * NCW + 32,
-                                                          Cfg::bytes);
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * NCW + 32, smem);
         if (e != cudaSuccess) return e;
         if (occ < 1) occ = 1;
     }
-    const int strips = (L.nx + Wo - 1) / Wo;
-    const int64_t R = (int64_t)L.members * strips * L.ny_loc;
+    const int64_t R_ = (int64_t)L.members * P.strips * L.ny_loc;
     const int64_t minrows = 16;
     int64_t B = (int64_t)occ * nsm;
-    static const int dbg = env_int("PF_STREAM_DBG", 0), nogroup = env_int("PF_STREAM_NOGROUP", 0);
+    static const int nogroup = env_int("PF_STREAM_NOGROUP", 0);
     // grouped schedule when at least 4 groups of `strips` blocks fit in one resident wave
-    int64_t G = B / strips;
+    int64_t G = B / P.strips;
     const int64_t T = (int64_t)L.members * L.ny_loc;
     if (G > (T + minrows - 1) / minrows) G = (T + minrows - 1) / minrows;
     if (G >= 4 && !nogroup) {
-        B = G * strips;
+        B = G * P.strips;
     } else {
         G = 0;
-        if (B > (R + minrows - 1) / minrows) B = (R + minrows - 1) / minrows;
+        if (B > (R_ + minrows - 1) / minrows) B = (R_ + minrows - 1) / minrows;
     }
     if (B < 1) B = 1;
-    stream_kernel<real, NCW, S, BASE, HMIX><<<(unsigned)B, 32 * NCW + 32, Cfg::bytes, s>>>(L, k, in, base, out, vel, Wo, (int)G, dbg);
+    const CUtensorMap &mIn = stage == 1 ? (R == kR1 ? P.mapU1 : P.mapU2) : (R == kR1 ? P.mapUs1 : P.mapUs2);
+    const CUtensorMap &mBase = R == kR1 ? P.mapU1 : P.mapU2;
+    kern<<<(unsigned)B, 32 * NCW + 32, smem, s>>>(L, k, mIn, mBase, out, vel, P.Wo, (int)G);
     return cudaGetLastError();
 }
 
-bool stream_eligible(const Layout &L) { return L.nx % 4 == 0 && L.nx >= 16; }
+template <typename real, int NCW>
+cudaError_t launch_stream_n(const Layout &L, const StreamPlan &P, const KC<real> &k, int stage, real *out,
+                            const real *vel, cudaStream_t s) {
+    if (stage == 1)
+        return k.hmix ? launch_stream_k<real, NCW, kR1, kS1, false, true>(L, P, k, stage, out, vel, s)
+                      : launch_stream_k<real, NCW, kR1, kS1, false, false>(L, P, k, stage, out, vel, s);
+    return k.hmix ? launch_stream_k<real, NCW, kR2, kS2, true, true>(L, P, k, stage, out, vel, s)
+                  : launch_stream_k<real, NCW, kR2, kS2, true, false>(L, P, k, stage, out, vel, s);
+}
 
-// Strip output width Wo (multiple of 4, <= 30 NCW) and warps per block NCW: 256 columns on 9
-// compute warps for wide grids, narrower strips on fewer warps for small nx.  Ring depth: stage 1
-// streams 3 rows per load, stage 2 six, so stage 1 affords a deeper ring in the same shared
-// memory.  PF_STREAM_NCW / PF_STREAM_S1 / PF_STREAM_S2 / PF_STREAM_WO override (experiments).
 template <typename real>
-cudaError_t launch_stream(const Layout &L, const KC<real> &k, const real *in, const real *base, real *out,
-                          const real *vel, int has_base, cudaStream_t s) {
-    static const int envN = env_int("PF_STREAM_NCW", 0), envS1 = env_int("PF_STREAM_S1", 0),
-                     envS2 = env_int("PF_STREAM_S2", 0), envWo = env_int("PF_STREAM_WO", 0);
-    int ncw = L.nx >= 256 ? 9 : (L.nx >= 120 ? 5 : 3);
-    if (envN) ncw = envN;
-    int Wo = ncw == 9 ? 256 : (ncw == 5 ? 128 : 64);
-    Wo = min(Wo, (30 * ncw) / 4 * 4);
-    if (envWo) Wo = envWo;
-    if (Wo > L.nx) Wo = L.nx;
-    const int S = has_base ? (envS2 ? envS2 : 8) : (envS1 ? envS1 : 12);
-#define PF_TRY(NN, SS, BB)                                                                      \
-    if (ncw == NN && S == SS && has_base == BB)                                                \
-        return k.hmix ? launch_stream_b<real, NN, SS, BB, true>(L, k, in, base, out, vel, Wo, s) \
-                      : launch_stream_b<real, NN, SS, BB, false>(L, k, in, base, out, vel, Wo, s);
-    PF_TRY(9, 8, 1) PF_TRY(9, 6, 1) PF_TRY(9, 7, 1) PF_TRY(9, 12, 0) PF_TRY(9, 6, 0) PF_TRY(9, 9, 0)
-    PF_TRY(9, 15, 0) PF_TRY(5, 8, 1) PF_TRY(5, 12, 0) PF_TRY(3, 8, 1) PF_TRY(3, 12, 0)
-#undef PF_TRY
-    return cudaErrorInvalidValue;
+cudaError_t launch_stream(const Layout &L, const StreamPlan &P, const KC<real> &k, int stage, real *out,
+                          const real *vel, cudaStream_t s) {
+    switch (P.ncw) {
+        case 2: return launch_stream_n<real, 2>(L, P, k, stage, out, vel, s);
+        case 4: return launch_stream_n<real, 4>(L, P, k, stage, out, vel, s);
+        case 6: return launch_stream_n<real, 6>(L, P, k, stage, out, vel, s);
+        case 8: return launch_stream_n<real, 8>(L, P, k, stage, out, vel, s);
+        default: return cudaErrorInvalidValue;
+    }
 }
 
 cudaError_t upload_exp_table() {
@@ -658,19 +675,74 @@ cudaError_t upload_exp_table() {
     return e;
 }
 
-cudaError_t launch_stage(int precision, const Layout &L, const Coef &K, const void *in,
-                         const void *base, void *out, const void *vel, double coef, cudaStream_t s) {
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void *p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+bool encode_map(CUtensorMap *m, int precision, const Layout &L, void *buf, int box_x, int rows) {
+    auto enc = get_encode();
+    if (!enc) return false;
+    const size_t esz = precision == 0 ? 8 : 4;
+    cuuint64_t dims[3] = {(cuuint64_t)L.pitch, (cuuint64_t)(L.ny_loc + 4), (cuuint64_t)(3 * L.members)};
+    cuuint64_t strides[2] = {(cuuint64_t)L.pitch * esz, (cuuint64_t)L.fstride * esz};
+    cuuint32_t box[3] = {(cuuint32_t)box_x, (cuuint32_t)rows, 3};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = enc(m, precision == 0 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, buf,
+                     dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+bool stream_eligible(const Layout &L) { return L.nx >= 16 && (L.nx * L.gx) % 4 == 0 && L.ny_loc >= 2; }
+
+cudaError_t make_stream_plan(int precision, const Layout &L, void *U, void *Us, StreamPlan &P) {
+    P = StreamPlan();
+    if (L.path == 1 || !stream_eligible(L)) return cudaSuccess;
+    const int gx = L.gx;                         // = HL (16 B of halo columns)
+    // strip width: at most 256 - 2 gx - 12 columns (box <= 256 elements), split nx evenly, a
+    // multiple of gx so boxes and rows stay 16 B aligned; NCW warps of 30 columns each
+    const int maxw = 256 - 2 * gx - 12;
+    int strips = (L.nx + maxw - 1) / maxw;
+    int Wo = (L.nx + strips - 1) / strips;
+    Wo = (Wo + gx - 1) / gx * gx;
+    strips = (L.nx + Wo - 1) / Wo;
+    const int need = (Wo + 29) / 30;
+    int ncw = need <= 2 ? 2 : (need <= 4 ? 4 : (need <= 6 ? 6 : 8));
+    static const int envN = env_int("PF_STREAM_NCW", 0);
+    if (envN) ncw = envN;
+    if (30 * ncw < Wo) return cudaErrorInvalidValue;
+    P.ncw = ncw;
+    P.Wo = Wo;
+    P.strips = strips;
+    P.box_x = Wo + 2 * gx;
+    P.rows1 = kR1;
+    P.rows2 = kR2;
+    if (!encode_map(&P.mapU1, precision, L, U, P.box_x, kR1) || !encode_map(&P.mapUs1, precision, L, Us, P.box_x, kR1) ||
+        !encode_map(&P.mapU2, precision, L, U, P.box_x, kR2) || !encode_map(&P.mapUs2, precision, L, Us, P.box_x, kR2))
+        return cudaErrorInvalidValue;
+    P.ok = true;
+    return cudaSuccess;
+}
+
+cudaError_t launch_stage(int precision, const Layout &L, const StreamPlan &P, const Coef &K, int stage,
+                         const void *in, const void *base, void *out, const void *vel, double coef,
+                         cudaStream_t s) {
     cudaError_t te = upload_exp_table();
     if (te != cudaSuccess) return te;
-    const bool has_base = base != in;
-    const bool stream = L.path != 1 && stream_eligible(L);
-    if (stream) {
+    if (P.ok) {
         if (precision == 0)
-            return launch_stream<double>(L, make_kc<double>(K, coef), (const double *)in,
-                                            (const double *)base, (double *)out, (const double *)vel,
-                                            has_base, s);
-        return launch_stream<float>(L, make_kc<float>(K, coef), (const float *)in, (const float *)base,
-                                       (float *)out, (const float *)vel, has_base, s);
+            return launch_stream<double>(L, P, make_kc<double>(K, coef), stage, (double *)out, (const double *)vel, s);
+        return launch_stream<float>(L, P, make_kc<float>(K, coef), stage, (float *)out, (const float *)vel, s);
     }
     dim3 grid((L.nx + BX - 1) / BX, (L.ny_loc + BY - 1) / BY, L.members);
     if (precision == 0) {
@@ -689,6 +761,21 @@ cudaError_t launch_stage(int precision, const Layout &L, const Coef &K, const vo
         else
             stage_kernel<float, false><<<grid, NT, 0, s>>>(L, kf, (const float *)in, (const float *)base,
                                                            (float *)out, (const float *)vel);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_fill_ghosts(int precision, const Layout &L, double rho_in, void *state, cudaStream_t s) {
+    const int64_t nr = (int64_t)4 * L.nx * 3 * L.members;
+    const int64_t nc = (int64_t)(L.ny_loc + 4) * 3 * L.members * 2 * L.gx;
+    const int b1 = (int)((nr + 255) / 256 > 4096 ? 4096 : (nr + 255) / 256);
+    const int b2 = (int)((nc + 255) / 256 > 4096 ? 4096 : (nc + 255) / 256);
+    if (precision == 0) {
+        ghost_rows_kernel<double><<<b1, 256, 0, s>>>(L, rho_in, (double *)state);
+        ghost_cols_kernel<double><<<b2, 256, 0, s>>>(L, (double *)state);
+    } else {
+        ghost_rows_kernel<float><<<b1, 256, 0, s>>>(L, (float)rho_in, (float *)state);
+        ghost_cols_kernel<float><<<b2, 256, 0, s>>>(L, (float *)state);
     }
     return cudaGetLastError();
 }
