@@ -83,8 +83,9 @@ typedef struct {
     uint64_t seed;                   /* counter-RNG seed (R-16)                              */
     int32_t device;                  /* CUDA device ordinal                                  */
     int32_t graph_steps;             /* steps per captured CUDA graph (0 = no graphs)        */
-    int32_t kernel_path;             /* stage kernel: 0 auto (streaming TMA kernel when nx % 4 == 0
-                                        and nx >= 16, else tile kernel), 1 tile, 2 streaming   */
+    int32_t kernel_path;             /* stage kernel: 0 auto (pair kernel when nx % 4 == 0 and
+                                        nx >= 16, else tile kernel), 1 tile, 2 one-column streaming
+                                        kernel, 3 pair streaming kernel                         */
 } pf_params;
 
 /* Fill *out with the preset of BASELINE.json configs[cfg-1] (cfg = 1..5; R-13, R-14).

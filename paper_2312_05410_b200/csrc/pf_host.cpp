@@ -257,8 +257,8 @@ pf_status validate(const pf_params *p, std::string &why) {
     if (p->M_A_bulk < 0 || p->M_B_bulk < 0 || p->M_A_surf < 0 || p->M_B_surf < 0) { why = "mobilities must be >= 0"; return PF_ERR_ARG; }
     if (p->check_every < 1) { why = "check_every must be >= 1"; return PF_ERR_ARG; }
     if (p->graph_steps < 0) { why = "graph_steps must be >= 0"; return PF_ERR_ARG; }
-    if (p->kernel_path < 0 || p->kernel_path > 2) { why = "kernel_path must be 0, 1 or 2"; return PF_ERR_ARG; }
-    if (p->kernel_path == 2 && !(p->nx % 4 == 0 && p->nx >= 16)) { why = "streaming kernel needs nx % 4 == 0 and nx >= 16"; return PF_ERR_ARG; }
+    if (p->kernel_path < 0 || p->kernel_path > 3) { why = "kernel_path must be 0, 1, 2 or 3"; return PF_ERR_ARG; }
+    if (p->kernel_path >= 2 && !(p->nx % 4 == 0 && p->nx >= 16)) { why = "streaming kernels need nx % 4 == 0 and nx >= 16"; return PF_ERR_ARG; }
     if (p->ic < PF_IC_FILM || p->ic > PF_IC_NONE) { why = "unknown ic"; return PF_ERR_ARG; }
     if ((p->ic == PF_IC_ROUGH_SUBSTRATE || p->ic == PF_IC_COLUMNS) && !(p->W_phi > 0)) { why = "tanh recipes need W_phi > 0"; return PF_ERR_ARG; }
     if (p->ic == PF_IC_ROUGH_SUBSTRATE && !(p->ic_wavelength != 0)) { why = "ic_wavelength must be != 0"; return PF_ERR_ARG; }

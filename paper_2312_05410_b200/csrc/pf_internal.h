@@ -18,7 +18,7 @@ namespace pf {
 struct Layout {
     int nx, ny, ny_loc, y0;      // global grid, owned rows, first owned global row
     int members;
-    int path;                    // stage kernel: 0 auto (streaming when eligible), 1 tile, 2 streaming
+    int path;                    // stage kernel: 0 auto (= 3 when eligible), 1 tile, 2 stream, 3 pair
     int gx;                      // ghost columns per side (16 B / element size)
     int pitch;                   // elements per storage row = nx + 2 gx
     int64_t fstride;             // elements per field  = (ny_loc + 4) * pitch
@@ -44,11 +44,10 @@ struct Coef {
 // tensor maps (x, storage row, member*3 + field) of the two state buffers.
 struct StreamPlan {
     bool ok = false;
+    int kind = 0;                   // 1: stream_kernel (one column per lane), 2: pair_kernel
     int ncw = 0, Wo = 0, strips = 0;
     int box_x = 0;                  // Wo + 2 halo columns (16 B each side)
-    int rows1 = 0, rows2 = 0;       // rows per TMA box: stage 1 / stage 2
-    CUtensorMap mapU1, mapUs1;      // box (box_x, rows1, 3) over U / Us
-    CUtensorMap mapU2, mapUs2;      // box (box_x, rows2, 3) over U / Us
+    CUtensorMap mapU[2], mapUs[2];  // box (box_x, 2 or 4 rows, 3) over U / Us (index: rows == 4)
 };
 
 // Number of values in a per-member diagnostics record (internal).

@@ -427,8 +427,8 @@ __device__ __forceinline__ void store_with_ghosts(const Layout &L, real *b, int 
     }
 }
 
-template <typename real, int NCW, int R, int S, bool BASE, bool HMIX>
-__global__ void __launch_bounds__(32 * NCW + 32, (NCW >= 6 ? 2 : 3)) stream_kernel(
+template <typename real, int NCW, int R, int S, bool BASE, bool HMIX, int MINB>
+__global__ void __launch_bounds__(32 * NCW + 32, MINB) stream_kernel(
     Layout L, KC<real> k, const __grid_constant__ CUtensorMap mapIn, const __grid_constant__ CUtensorMap mapBase,
     real *out, const real *__restrict__ vel, int Wo, int G) {
     // Warp roles.  Warps [0, NCW): compute.  Warp NCW: producer -- lane 0 issues one TMA box per
@@ -443,7 +443,9 @@ __global__ void __launch_bounds__(32 * NCW + 32, (NCW >= 6 ? 2 : 3)) stream_kern
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int bx = Wo + 2 * HL;
     const Ring<real> rg(bx, R, BASE);
-    real *slots = reinterpret_cast<real *>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~(uintptr_t)127);
+    // 128 B-aligned ring base, derived from smem_raw by an offset so that the compiler keeps the
+    // shared address space (LDS, not generic LD) for every ring access.
+    real *slots = reinterpret_cast<real *>(smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u));
     uint64_t *full = reinterpret_cast<uint64_t *>(slots + S * rg.slot_elems + 64);
     uint64_t *empty = full + S;
     double *etab = reinterpret_cast<double *>(empty + S);
@@ -575,6 +577,183 @@ __global__ void __launch_bounds__(32 * NCW + 32, (NCW >= 6 ? 2 : 3)) stream_kern
     }
 }
 
+// ----------------------------------------------------------------------------------------
+// Pair kernel (default performance path).  Same producer / ring / schedule as stream_kernel, but
+// every compute lane owns TWO adjacent columns, so a warp covers 64 columns (60 outputs plus one
+// halo column on each side).  Per row and pair of cells a lane issues 128-bit shared loads, 10
+// shuffles and 128-bit global stores -- half the per-cell shuffle, load, barrier, loop and store
+// instructions of the one-column layout -- and the two columns give the scheduler independent
+// fp64 chains.  The per-cell arithmetic is the same pf_cell.cuh code, so results are bitwise
+// identical to the tile and stream kernels.
+template <typename real> struct Vec2;
+template <> struct Vec2<double> { using T = double2; };
+template <> struct Vec2<float> { using T = float2; };
+
+template <typename real>
+__device__ __forceinline__ typename Vec2<real>::T ld2(const real *p) {
+    return *reinterpret_cast<const typename Vec2<real>::T *>(p);
+}
+template <typename real>
+__device__ __forceinline__ void st2(real *p, real x, real y) {
+    typename Vec2<real>::T v;
+    v.x = x;
+    v.y = y;
+    *reinterpret_cast<typename Vec2<real>::T *>(p) = v;
+}
+
+constexpr int kPairCols = 60;   // output columns per compute warp
+constexpr int kPairHalo = 4;    // box columns left of the strip (and right of it)
+
+template <typename real, int NCW, int R, int S, bool BASE, bool HMIX, int MINB>
+__global__ void __launch_bounds__(32 * NCW + 32, MINB) pair_kernel(
+    Layout L, KC<real> k, const __grid_constant__ CUtensorMap mapIn, const __grid_constant__ CUtensorMap mapBase,
+    real *out, const real *__restrict__ vel, int Wo, int G) {
+    static_assert(R >= 2, "rows k-1, k-2 must lie in the current or the previous box");
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int bx = Wo + 2 * kPairHalo;
+    const Ring<real> rg(bx, R, BASE);
+    unsigned char *base_sm = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
+    real *slots = reinterpret_cast<real *>(base_sm);
+    uint64_t *full = reinterpret_cast<uint64_t *>(base_sm + (size_t)S * rg.slot_elems * sizeof(real));
+    uint64_t *empty = full + S;
+    double *etab = reinterpret_cast<double *>(empty + S);
+    load_exp_table(etab);
+
+    const int t = threadIdx.x;
+    const int warp = t >> 5, lane = t & 31;
+    if (t == 0) {
+        for (int q = 0; q < S; ++q) {
+            mbar_init(&full[q], 1);
+            mbar_init(&empty[q], NCW);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    const int nx = L.nx;
+    const Sched sch = make_sched(L, Wo, G);
+    const uint32_t box_bytes = (uint32_t)(3 * R * bx * sizeof(real));
+
+    if (warp == NCW) {
+        // ------------------------------- producer -------------------------------
+        if (lane != 0) return;
+        prefetch_tmap(&mapIn);
+        if (BASE) prefetch_tmap(&mapBase);
+        uint32_t g = 0;
+        int64_t pos = sch.lo;
+        Seg sg;
+        while (next_seg(L, Wo, sch, pos, sg)) {
+            const int n = sg.yb - sg.ya + 4, nsl = (n + R - 1) / R;
+            const int bxs = sg.x0 - kPairHalo + L.gx;           // storage column of the box origin
+            for (int j = 0; j < nsl; ++j, ++g) {
+                const int slot = g % S;
+                if (g >= (uint32_t)S) mbar_wait(&empty[slot], ((g / S) - 1) & 1u);
+                real *sl = slots + slot * rg.slot_elems;
+                const int k0 = sg.ya - 2 + j * R;                 // first row of the box
+                mbar_expect_tx(&full[slot], BASE ? 2 * box_bytes : box_bytes);
+                tma_load_3d(sl, &mapIn, bxs, k0 + 2, 3 * sg.m, &full[slot]);
+                if (BASE) tma_load_3d(sl + rg.in_elems, &mapBase, bxs, k0, 3 * sg.m, &full[slot]);
+            }
+        }
+        return;
+    }
+
+    // --------------------------- compute warps ---------------------------------
+    // Lane l of warp w owns strip-relative columns cx, cx + 1 with cx = 60 w + 2 l - 2: lanes 1..30
+    // write them, lane 0's right column and lane 31's left column are the flux halo.
+    const int cx = kPairCols * warp + 2 * lane - 2;
+    const int ci = kPairHalo + cx;          // its (even) column in a box row
+    const int plane = R * bx;
+    int sidx = 0;
+    uint32_t par = 0;
+    int64_t pos = sch.lo;
+    Seg sg;
+    while (next_seg(L, Wo, sch, pos, sg)) {
+        const int n = sg.yb - sg.ya + 4, nsl = (n + R - 1) / R;
+        const int x = sg.x0 + cx;
+        const bool store = lane >= 1 && lane <= 30 && cx < sg.Wp;
+        const bool xedge = (x < L.gx) | (x + 1 >= nx - L.gx);
+        real *ob = out + sg.m * L.mstride;
+        const real vx = vel[2 * sg.m], vy = vel[2 * sg.m + 1];
+
+        real A1x = 0, A1y = 0, A2x = 0, A2y = 0;          // mu_c rows k-1, k-2
+        real M1x = 0, M1y = 0, M2x = 0, M2y = 0;          // M rows k-1, k-2
+        real B1x = 0, B1y = 0, B2x = 0, B2y = 0, B3x = 0, B3y = 0;   // mu_phi rows k-1 .. k-3
+        real P3x = 0, P3y = 0, R3x = 0, R3y = 0;          // phi, rho row k-3
+        real Fsx = 0, Fsy = 0;                            // south face fluxes of row k-2
+        const real *prev = slots + (sidx == 0 ? S - 1 : sidx - 1) * rg.slot_elems + ci;
+        for (int j = 0; j < nsl; ++j) {
+            const real *cur = slots + sidx * rg.slot_elems + ci;
+            mbar_wait(&full[sidx], par);
+#pragma unroll
+            for (int u = 0; u < R; ++u) {
+                const int i = j * R + u;                  // row k = ya - 2 + i
+                const real *rk = cur + u * bx;
+                const real *rk1 = u >= 1 ? cur + (u - 1) * bx : prev + (R - 1) * bx;
+                const real *rk2 = u >= 2 ? cur + (u - 2) * bx : prev + (R - 2 + u) * bx;
+                const auto c0 = ld2(rk), c1 = ld2(rk1), c2 = ld2(rk2);
+                const auto p0 = ld2(rk + plane), p1 = ld2(rk1 + plane), p2 = ld2(rk2 + plane);
+                const auto r1 = ld2(rk1 + 2 * plane), r2 = ld2(rk2 + 2 * plane);
+                // rotate the windows: row k-1 of the last iteration is row k-2 now
+                A2x = A1x; A2y = A1y; M2x = M1x; M2y = M1y;
+                B3x = B2x; B3y = B2y; B2x = B1x; B2y = B1y;
+                // a2: mu_c, mu_phi, M of row k-1 at both columns
+                constitutive<real, HMIX>(k, etab, c1.x, p1.x, rk1[-1], c1.y, c2.x, c0.x, rk1[plane - 1], p1.y, p2.x,
+                                         p0.x, A1x, B1x, M1x);
+                constitutive<real, HMIX>(k, etab, c1.y, p1.y, c1.x, rk1[2], c2.y, c0.y, p1.x, rk1[plane + 2], p2.y,
+                                         p0.y, A1y, B1y, M1y);
+                // a3-a5: update of row k-2.  x faces: (a, a+1) in lane, (a+1, next a) by shuffle,
+                // the west face of a is the previous lane's east face of its right column.
+                const real An = __shfl_down_sync(0xffffffffu, A2x, 1);
+                const real Mn = __shfl_down_sync(0xffffffffu, M2x, 1);
+                const real Bn = __shfl_down_sync(0xffffffffu, B2x, 1);
+                const real Bp = __shfl_up_sync(0xffffffffu, B2y, 1);
+                const real fex = face_flux<real>(M2x, M2y, A2x, A2y);
+                const real fey = face_flux<real>(M2y, Mn, A2y, An);
+                const real fwx = __shfl_up_sync(0xffffffffu, fey, 1);
+                const real fnx = face_flux<real>(M2x, M1x, A2x, A1x);
+                const real fny = face_flux<real>(M2y, M1y, A2y, A1y);
+                real bcx = c2.x, bcy = c2.y, bpx = p2.x, bpy = p2.y, brx = r2.x, bry = r2.y;
+                if (BASE) {
+                    const real *bs = cur + rg.in_elems + u * bx;
+                    const auto b0 = ld2(bs), b1 = ld2(bs + plane), b2 = ld2(bs + 2 * plane);
+                    bcx = b0.x; bcy = b0.y; bpx = b1.x; bpy = b1.y; brx = b2.x; bry = b2.y;
+                }
+                real ocx, opx, orx, ocy, opy, ory;
+                cell_update<real>(k, vx, vy, fex, fwx, fnx, Fsx, B2x, Bp, B2y, B3x, B1x, rk2[plane - 1], p2.y, P3x,
+                                  p1.x, r2.x, rk2[2 * plane - 1], r2.y, R3x, r1.x, bcx, bpx, brx, ocx, opx, orx);
+                cell_update<real>(k, vx, vy, fey, fex, fny, Fsy, B2y, B2x, Bn, B3y, B1y, p2.x, rk2[plane + 2], P3y,
+                                  p1.y, r2.y, r2.x, rk2[2 * plane + 2], R3y, r1.y, bcy, bpy, bry, ocy, opy, ory);
+                Fsx = fnx; Fsy = fny;
+                P3x = p2.x; P3y = p2.y; R3x = r2.x; R3y = r2.y;
+                if (store && i >= 4 && i < n) {
+                    const int r = sg.ya - 4 + i;          // local row k-2
+                    const bool edge = xedge | (L.y0 + r <= 1) | (L.y0 + r >= L.ny - 2);
+                    if (!edge) {
+                        real *o = ob + L.at(r, x);
+                        st2(o, ocx, ocy);
+                        st2(o + L.fstride, opx, opy);
+                        st2(o + 2 * L.fstride, orx, ory);
+                    } else {
+                        store_with_ghosts<real>(L, ob, 0, r, x, ocx);
+                        store_with_ghosts<real>(L, ob + L.fstride, 1, r, x, opx);
+                        store_with_ghosts<real>(L, ob + 2 * L.fstride, 2, r, x, orx);
+                        store_with_ghosts<real>(L, ob, 0, r, x + 1, ocy);
+                        store_with_ghosts<real>(L, ob + L.fstride, 1, r, x + 1, opy);
+                        store_with_ghosts<real>(L, ob + 2 * L.fstride, 2, r, x + 1, ory);
+                    }
+                }
+            }
+            __syncwarp();
+            if (j >= 1 && lane == 0) mbar_arrive(&empty[sidx == 0 ? S - 1 : sidx - 1]);
+            prev = cur;
+            if (++sidx == S) { sidx = 0; par ^= 1u; }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[sidx == 0 ? S - 1 : sidx - 1]);
+    }
+}
+
 template <typename real>
 KC<real> make_kc(const Coef &K, double coef) {
     KC<real> k;
@@ -598,16 +777,37 @@ KC<real> make_kc(const Coef &K, double coef) {
     return k;
 }
 
-// Rows per box and ring depth: stage 1 R = 4, S = 4 (16 rows in flight); stage 2 R = 2, S = 6.
-constexpr int kR1 = 4, kS1 = 4, kR2 = 2, kS2 = 6;
+// Ring geometry (rows per TMA box R, ring depth S, resident blocks per SM MINB) per kernel kind
+// and stage.  Stage 1 streams 3 fields per row, stage 2 six (input + base), so stage 2 gets the
+// shallower ring.
+struct RingVariant {
+    int R, S, minb;
+};
+constexpr RingVariant kStream1{4, 4, 2}, kStream2{2, 6, 2};
+// Pair kernel: about 128 registers per thread, so MINB = 16 / (NCW + 1) blocks of NCW + 1 warps
+// fill the register file with 12-16 compute warps per SM; rings of 2-row boxes as deep as the
+// shared memory left to each of the MINB blocks allows (at most 8 boxes).
+template <typename real, int NCW, bool BASE>
+struct PairCfg {
+    static constexpr int minb = 16 / (NCW + 1) > 8 ? 8 : 16 / (NCW + 1);
+    static constexpr int R = 2;
+    static constexpr int bx_max = kPairCols * NCW + 2 * kPairHalo;
+    static constexpr int slot = (3 * R * bx_max * (int)sizeof(real) + 127) / 128 * 128 * (BASE ? 2 : 1);
+    static constexpr int budget = (227 * 1024) / minb - 2048;
+    static constexpr int S = budget / slot > 8 ? 8 : budget / slot;
+    static_assert(S >= 3, "ring too shallow");
+};
 
-template <typename real, int NCW, int R, int S, bool BASE, bool HMIX>
-cudaError_t launch_stream_k(const Layout &L, const StreamPlan &P, const KC<real> &k, int stage, real *out,
-                            const real *vel, cudaStream_t s) {
+enum Kind { kStreamKind = 1, kPairKind = 2 };
+
+template <int KIND, typename real, int NCW, int R, int S, bool BASE, bool HMIX, int MINB>
+cudaError_t launch_ring(const Layout &L, const StreamPlan &P, const KC<real> &k, int stage, real *out,
+                        const real *vel, cudaStream_t s) {
     const size_t smem = stream_smem_bytes<real>(P.box_x, R, S, BASE);
     static int occ = -1, nsm = 0;
     static size_t smem_set = 0;
-    auto kern = stream_kernel<real, NCW, R, S, BASE, HMIX>;
+    auto kern = KIND == kPairKind ? pair_kernel<real, NCW, R, S, BASE, HMIX, MINB>
+                                  : stream_kernel<real, NCW, R, S, BASE, HMIX, MINB>;
     if (smem > smem_set) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
@@ -637,25 +837,50 @@ cudaError_t launch_stream_k(const Layout &L, const StreamPlan &P, const KC<real>
         if (B > (R_ + minrows - 1) / minrows) B = (R_ + minrows - 1) / minrows;
     }
     if (B < 1) B = 1;
-    const CUtensorMap &mIn = stage == 1 ? (R == kR1 ? P.mapU1 : P.mapU2) : (R == kR1 ? P.mapUs1 : P.mapUs2);
-    const CUtensorMap &mBase = R == kR1 ? P.mapU1 : P.mapU2;
-    kern<<<(unsigned)B, 32 * NCW + 32, smem, s>>>(L, k, mIn, mBase, out, vel, P.Wo, (int)G);
+    const int ri = R == 4 ? 1 : 0;
+    const CUtensorMap &mIn = stage == 1 ? P.mapU[ri] : P.mapUs[ri];
+    kern<<<(unsigned)B, 32 * NCW + 32, smem, s>>>(L, k, mIn, P.mapU[ri], out, vel, P.Wo, (int)G);
     return cudaGetLastError();
+}
+
+template <int KIND, typename real, int NCW, bool BASE, int R, int S, int MINB>
+cudaError_t launch_ring_h(const Layout &L, const StreamPlan &P, const KC<real> &k, int stage, real *out,
+                          const real *vel, cudaStream_t s) {
+    return k.hmix ? launch_ring<KIND, real, NCW, R, S, BASE, true, MINB>(L, P, k, stage, out, vel, s)
+                  : launch_ring<KIND, real, NCW, R, S, BASE, false, MINB>(L, P, k, stage, out, vel, s);
 }
 
 template <typename real, int NCW>
 cudaError_t launch_stream_n(const Layout &L, const StreamPlan &P, const KC<real> &k, int stage, real *out,
                             const real *vel, cudaStream_t s) {
     if (stage == 1)
-        return k.hmix ? launch_stream_k<real, NCW, kR1, kS1, false, true>(L, P, k, stage, out, vel, s)
-                      : launch_stream_k<real, NCW, kR1, kS1, false, false>(L, P, k, stage, out, vel, s);
-    return k.hmix ? launch_stream_k<real, NCW, kR2, kS2, true, true>(L, P, k, stage, out, vel, s)
-                  : launch_stream_k<real, NCW, kR2, kS2, true, false>(L, P, k, stage, out, vel, s);
+        return launch_ring_h<kStreamKind, real, NCW, false, kStream1.R, kStream1.S, kStream1.minb>(L, P, k, stage,
+                                                                                                    out, vel, s);
+    return launch_ring_h<kStreamKind, real, NCW, true, kStream2.R, kStream2.S, kStream2.minb>(L, P, k, stage, out,
+                                                                                              vel, s);
+}
+
+template <typename real, int NCW>
+cudaError_t launch_pair_n(const Layout &L, const StreamPlan &P, const KC<real> &k, int stage, real *out,
+                          const real *vel, cudaStream_t s) {
+    using C1 = PairCfg<real, NCW, false>;
+    using C2 = PairCfg<real, NCW, true>;
+    if (stage == 1) return launch_ring_h<kPairKind, real, NCW, false, C1::R, C1::S, C1::minb>(L, P, k, stage, out, vel, s);
+    return launch_ring_h<kPairKind, real, NCW, true, C2::R, C2::S, C2::minb>(L, P, k, stage, out, vel, s);
 }
 
 template <typename real>
 cudaError_t launch_stream(const Layout &L, const StreamPlan &P, const KC<real> &k, int stage, real *out,
                           const real *vel, cudaStream_t s) {
+    if (P.kind == kPairKind) {
+        switch (P.ncw) {
+            case 1: return launch_pair_n<real, 1>(L, P, k, stage, out, vel, s);
+            case 2: return launch_pair_n<real, 2>(L, P, k, stage, out, vel, s);
+            case 3: return launch_pair_n<real, 3>(L, P, k, stage, out, vel, s);
+            case 4: return launch_pair_n<real, 4>(L, P, k, stage, out, vel, s);
+            default: return cudaErrorInvalidValue;
+        }
+    }
     switch (P.ncw) {
         case 2: return launch_stream_n<real, 2>(L, P, k, stage, out, vel, s);
         case 4: return launch_stream_n<real, 4>(L, P, k, stage, out, vel, s);
@@ -709,27 +934,39 @@ cudaError_t make_stream_plan(int precision, const Layout &L, void *U, void *Us, 
     P = StreamPlan();
     if (L.path == 1 || !stream_eligible(L)) return cudaSuccess;
     const int gx = L.gx;                         // = HL (16 B of halo columns)
-    // strip width: at most 256 - 2 gx - 12 columns (box <= 256 elements), split nx evenly, a
-    // multiple of gx so boxes and rows stay 16 B aligned; NCW warps of 30 columns each
-    const int maxw = 256 - 2 * gx - 12;
-    int strips = (L.nx + maxw - 1) / maxw;
-    int Wo = (L.nx + strips - 1) / strips;
-    Wo = (Wo + gx - 1) / gx * gx;
-    strips = (L.nx + Wo - 1) / Wo;
-    const int need = (Wo + 29) / 30;
-    int ncw = need <= 2 ? 2 : (need <= 4 ? 4 : (need <= 6 ? 6 : 8));
-    static const int envN = env_int("PF_STREAM_NCW", 0);
-    if (envN) ncw = envN;
-    if (30 * ncw < Wo) return cudaErrorInvalidValue;
-    P.ncw = ncw;
-    P.Wo = Wo;
-    P.strips = strips;
-    P.box_x = Wo + 2 * gx;
-    P.rows1 = kR1;
-    P.rows2 = kR2;
-    if (!encode_map(&P.mapU1, precision, L, U, P.box_x, kR1) || !encode_map(&P.mapUs1, precision, L, Us, P.box_x, kR1) ||
-        !encode_map(&P.mapU2, precision, L, U, P.box_x, kR2) || !encode_map(&P.mapUs2, precision, L, Us, P.box_x, kR2))
-        return cudaErrorInvalidValue;
+    if (L.path == 3 || L.path == 0) {
+        // pair kernel: strips of Wo <= 240 columns (box Wo + 8 <= 256 elements), Wo a multiple of
+        // 4 (16 B rows for fp32 too), split nx evenly; 60 output columns per compute warp
+        int strips = (L.nx + 239) / 240;
+        int Wo = (L.nx + strips - 1) / strips;
+        Wo = (Wo + 3) / 4 * 4;
+        strips = (L.nx + Wo - 1) / Wo;
+        P.kind = 2;
+        P.ncw = (Wo + kPairCols - 1) / kPairCols;
+        P.Wo = Wo;
+        P.strips = strips;
+        P.box_x = Wo + 2 * kPairHalo;
+    } else {
+        // stream kernel: strip width at most 256 - 2 gx - 12 columns (box <= 256 elements), split
+        // nx evenly, a multiple of gx so boxes and rows stay 16 B aligned; NCW warps of 30 columns
+        const int maxw = 256 - 2 * gx - 12;
+        int strips = (L.nx + maxw - 1) / maxw;
+        int Wo = (L.nx + strips - 1) / strips;
+        Wo = (Wo + gx - 1) / gx * gx;
+        strips = (L.nx + Wo - 1) / Wo;
+        const int need = (Wo + 29) / 30;
+        int ncw = need <= 2 ? 2 : (need <= 4 ? 4 : (need <= 6 ? 6 : 8));
+        if (30 * ncw < Wo) return cudaErrorInvalidValue;
+        P.kind = 1;
+        P.ncw = ncw;
+        P.Wo = Wo;
+        P.strips = strips;
+        P.box_x = Wo + 2 * gx;
+    }
+    for (int ri = 0; ri < 2; ++ri)
+        if (!encode_map(&P.mapU[ri], precision, L, U, P.box_x, ri ? 4 : 2) ||
+            !encode_map(&P.mapUs[ri], precision, L, Us, P.box_x, ri ? 4 : 2))
+            return cudaErrorInvalidValue;
     P.ok = true;
     return cudaSuccess;
 }
