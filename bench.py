@@ -276,7 +276,7 @@ def run_ours(args):
             "hbm_frac_effective": value * alg_per_cell_step / ws / 1e9 / peak,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": tr,
-                         "kernel": "stage_kernel (both midpoint stages)",
+                         "kernel": "pair_kernel (both midpoint stages; stage 1 and stage 2 launches)",
                          "algorithmic_bytes_per_launch": alg_bytes / nslab_launch,
                          "avg_launch_ms": stage_ms / nslab_launch, "peak_source": peak_src},
             "e2e": e2e,

@@ -518,7 +518,7 @@ pf_status create_common(const pf_params *p, int mode, int rank, int nranks, cons
         sl.L.y0 = (mode == kLoopback ? s : rank) * rows;
         sl.L.members = p->n_members;
         sl.L.path = p->kernel_path;
-        sl.L.gx = (int)(16 / c->esz);
+        sl.L.gx = (int)(32 / c->esz);   // 32 B: 128-bit output pairs start on 32 B sectors
         sl.L.pitch = p->nx + 2 * sl.L.gx;
         sl.L.fstride = (int64_t)(rows + 4) * sl.L.pitch;
         sl.L.mstride = 3 * sl.L.fstride;

@@ -482,9 +482,9 @@ __global__ void __launch_bounds__(32 * NCW + 32, MINB) stream_kernel(
                 real *sl = slots + slot * rg.slot_elems;
                 const int k0 = sg.ya - 2 + j * R;                 // first row of the box
                 mbar_expect_tx(&full[slot], BASE ? 2 * box_bytes : box_bytes);
-                // x: storage column of x0 - HL is x0 (gx == HL); y: storage row of k0 is k0 + 2
-                tma_load_3d(sl, &mapIn, sg.x0, k0 + 2, 3 * sg.m, &full[slot]);
-                if (BASE) tma_load_3d(sl + rg.in_elems, &mapBase, sg.x0, k0, 3 * sg.m, &full[slot]);
+                // x: storage column of x0 - HL is x0 - HL + gx; y: storage row of k0 is k0 + 2
+                tma_load_3d(sl, &mapIn, sg.x0 - HL + L.gx, k0 + 2, 3 * sg.m, &full[slot]);
+                if (BASE) tma_load_3d(sl + rg.in_elems, &mapBase, sg.x0 - HL + L.gx, k0, 3 * sg.m, &full[slot]);
             }
         }
         return;
@@ -734,7 +734,7 @@ __global__ void __launch_bounds__(32 * NCW + 32, MINB) pair_kernel(
                         st2(o, ocx, ocy);
                         st2(o + L.fstride, opx, opy);
                         st2(o + 2 * L.fstride, orx, ory);
-                    } else {
+                    } else {      // the value and its ghost-frame copies
                         store_with_ghosts<real>(L, ob, 0, r, x, ocx);
                         store_with_ghosts<real>(L, ob + L.fstride, 1, r, x, opx);
                         store_with_ghosts<real>(L, ob + 2 * L.fstride, 2, r, x, orx);
@@ -789,12 +789,13 @@ constexpr RingVariant kStream1{4, 4, 2}, kStream2{2, 6, 2};
 // shared memory left to each of the MINB blocks allows (at most 8 boxes).
 template <typename real, int NCW, bool BASE>
 struct PairCfg {
-    static constexpr int minb = 16 / (NCW + 1) > 8 ? 8 : 16 / (NCW + 1);
     static constexpr int R = 2;
     static constexpr int bx_max = kPairCols * NCW + 2 * kPairHalo;
     static constexpr int slot = (3 * R * bx_max * (int)sizeof(real) + 127) / 128 * 128 * (BASE ? 2 : 1);
-    static constexpr int budget = (227 * 1024) / minb - 2048;
-    static constexpr int S = budget / slot > 8 ? 8 : budget / slot;
+    static constexpr int ring(int b) { return ((227 * 1024) / b - 2048) / slot; }
+    static constexpr int pick(int b) { return b <= 1 || ring(b) >= 3 ? b : pick(b - 1); }
+    static constexpr int minb = pick(16 / (NCW + 1) > 8 ? 8 : 16 / (NCW + 1));
+    static constexpr int S = ring(minb) > 8 ? 8 : ring(minb);
     static_assert(S >= 3, "ring too shallow");
 };
 
@@ -928,12 +929,12 @@ bool encode_map(CUtensorMap *m, int precision, const Layout &L, void *buf, int b
 
 }  // namespace
 
-bool stream_eligible(const Layout &L) { return L.nx >= 16 && (L.nx * L.gx) % 4 == 0 && L.ny_loc >= 2; }
+bool stream_eligible(const Layout &L) { return L.nx >= 16 && L.nx % 4 == 0 && L.ny_loc >= 2; }
 
 cudaError_t make_stream_plan(int precision, const Layout &L, void *U, void *Us, StreamPlan &P) {
     P = StreamPlan();
     if (L.path == 1 || !stream_eligible(L)) return cudaSuccess;
-    const int gx = L.gx;                         // = HL (16 B of halo columns)
+    const int HL = precision == 0 ? 2 : 4;       // stream-kernel box halo: 16 B of columns
     if (L.path == 3 || L.path == 0) {
         // pair kernel: strips of Wo <= 240 columns (box Wo + 8 <= 256 elements), Wo a multiple of
         // 4 (16 B rows for fp32 too), split nx evenly; 60 output columns per compute warp
@@ -947,12 +948,12 @@ cudaError_t make_stream_plan(int precision, const Layout &L, void *U, void *Us, 
         P.strips = strips;
         P.box_x = Wo + 2 * kPairHalo;
     } else {
-        // stream kernel: strip width at most 256 - 2 gx - 12 columns (box <= 256 elements), split
-        // nx evenly, a multiple of gx so boxes and rows stay 16 B aligned; NCW warps of 30 columns
-        const int maxw = 256 - 2 * gx - 12;
+        // stream kernel: strip width at most 256 - 2 HL - 12 columns (box <= 256 elements), split
+        // nx evenly, a multiple of HL so boxes and rows stay 16 B aligned; NCW warps of 30 columns
+        const int maxw = 256 - 2 * HL - 12;
         int strips = (L.nx + maxw - 1) / maxw;
         int Wo = (L.nx + strips - 1) / strips;
-        Wo = (Wo + gx - 1) / gx * gx;
+        Wo = (Wo + HL - 1) / HL * HL;
         strips = (L.nx + Wo - 1) / Wo;
         const int need = (Wo + 29) / 30;
         int ncw = need <= 2 ? 2 : (need <= 4 ? 4 : (need <= 6 ? 6 : 8));
@@ -961,7 +962,7 @@ cudaError_t make_stream_plan(int precision, const Layout &L, void *U, void *Us, 
         P.ncw = ncw;
         P.Wo = Wo;
         P.strips = strips;
-        P.box_x = Wo + 2 * gx;
+        P.box_x = Wo + 2 * HL;
     }
     for (int ri = 0; ri < 2; ++ri)
         if (!encode_map(&P.mapU[ri], precision, L, U, P.box_x, ri ? 4 : 2) ||
