@@ -1,0 +1,180 @@
+"""GPU parity at BASELINE.json's full sizes, in the launch configuration bench.py times.
+
+The oracle cannot run configs[2..4] to their full horizons in test time (cfg4 alone is ~34 G
+cell-steps at ~2.5 M cell-steps/s), so full-size parity uses two things:
+
+* full-grid comparisons after a few steps (every cell, every member);
+* light-cone windows for longer horizons.  One explicit-midpoint step reads radius 2 per stage
+  (13-point diamond), so a cell after n steps depends only on the initial state
+  within radius 4n.  The oracle runs on a window of the seeded initial state (x-periodic wrap of
+  the window, physical y boundaries where the window reaches them); cells farther than 4n from
+  the window's artificial edges are exactly the full-grid values and are compared to the GPU run
+  of the full grid.
+
+Tolerances are BASELINE.json's (normwise, R-17): fp64 <= 1e-12 after 1 step and <= 1e-8 at the
+horizon; diagnostics within 1e-12 relative; fp32 configs[4] <= 1e-4 after 100 steps.  Oracle calls
+run concurrently in threads (ctypes releases the GIL; each call stays single-threaded)."""
+import os
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+import pytest
+
+from paper_2312_05410_b200 import pf
+from tests._maps import oracle_member, normwise
+
+pytestmark = pytest.mark.gpu
+
+_POOL = ThreadPoolExecutor(max_workers=max(2, min(8, os.cpu_count() or 2)))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    pf.lib()
+
+
+def _window(ora, m, ic, member, nx, ny, i0, j0, W, H, n):
+    """Oracle result of n steps on the window [j0, j0+H) x [i0, i0+W) (x wraps) and its valid mask."""
+    c, p, r = ora.initial_fields_rows(ic, nx, member, j0, H)
+    cols = (np.arange(W) + i0) % nx
+    u = [f[:, cols].copy() for f in (c, p, r)]
+    ref = ora.step(m, *u, n)
+    R = 4 * n
+    lo = 0 if j0 == 0 else R
+    hi = H if j0 + H == ny else H - R
+    xl, xh = (0, W) if W == nx else (R, W - R)
+    assert hi > lo and xh > xl, "window too small for the light cone"
+    return ref, (slice(lo, hi), slice(xl, xh)), cols
+
+
+def _window_err(gpu_fields, j0, H, cols, ref, valid):
+    rows = slice(j0 + valid[0].start, j0 + valid[0].stop)
+    ccols = cols[valid[1]]
+    err = 0.0
+    for g, r in zip(gpu_fields, ref):
+        gw = g[rows][:, ccols]
+        rw = r[valid]
+        err = max(err, float(np.abs(gw - rw).max() / max(np.abs(rw).max(), 1e-300)))
+    return err
+
+
+def test_cfg3_all_members_one_step_and_four_members_400_steps(ora):
+    """configs[2] (64 x 512^2 fp64, per-member rates): every member after 1 step (<= 1e-12, plus
+    mass / energy diagnostics within 1e-12), members 0, 21, 42, 63 after 400 steps (<= 1e-8)."""
+    p = pf.pf_default_params(3)
+    nx, ny, M = p.nx, p.ny, p.n_members
+    with pf.Simulation(p) as s:
+        s.step(1)
+        got = s.fields(-1)
+        diag = [s.diagnostics(k) for k in range(M)]
+        s.step(399)
+        got400 = {k: s.fields(k) for k in (0, 21, 42, 63)}
+
+    def one(k):
+        m, ic = oracle_member(ora, p, k)
+        u0 = ora.initial_fields(ic, nx, ny, k)
+        ref = ora.step(m, *u0, 1)
+        return k, ref, ora.diagnostics(m, *ref)
+
+    for k, ref, dref in _POOL.map(one, range(M)):
+        e = normwise([got[0][k], got[1][k], got[2][k]], ref)
+        assert e <= 1e-12, (k, e)
+        for q in range(4):
+            assert abs(diag[k][q] - dref[q]) <= 1e-12 * abs(dref[q]), (k, q, diag[k][q], dref[q])
+        assert diag[k][4] == 0
+
+    def long(k):
+        m, ic = oracle_member(ora, p, k)
+        return k, ora.step(m, *ora.initial_fields(ic, nx, ny, k), 400)
+
+    for k, ref in _POOL.map(long, (0, 21, 42, 63)):
+        e = normwise(got400[k], ref)
+        assert e <= 1e-8, (k, e)
+
+
+def test_cfg4_full_grid_one_step_and_windows_100_steps(ora):
+    """configs[3] (4096^2 fp64): the full grid after 1 step (<= 1e-12; diagnostics 1e-12) and
+    two light-cone windows after 100 steps (<= 1e-8): one on the substrate boundary (j0 = 0),
+    one across the film interface at y = 512."""
+    p = pf.pf_default_params(4)
+    nx, ny = p.nx, p.ny
+    m, ic = oracle_member(ora, p, 0)
+    wins = [(1000, 0, 1024, 1024), (3000, 100, 1024, 1024)]
+    futs = [_POOL.submit(_window, ora, m, ic, 0, nx, ny, i0, j0, W, H, 100) for i0, j0, W, H in wins]
+    with pf.Simulation(p) as s:
+        s.step(1)
+        g1 = s.fields(0)
+        d1 = s.diagnostics(0)
+        s.step(99)
+        g100 = s.fields(0)
+    u0 = ora.initial_fields(ic, nx, ny, 0)
+    ref1 = ora.step(m, *u0, 1)
+    assert normwise(g1, ref1) <= 1e-12
+    dref = ora.diagnostics(m, *ref1)
+    for q in range(4):
+        assert abs(d1[q] - dref[q]) <= 1e-12 * abs(dref[q]), (q, d1[q], dref[q])
+    for (i0, j0, W, H), f in zip(wins, futs):
+        ref, valid, cols = f.result()
+        e = _window_err(g100, j0, H, cols, ref, valid)
+        assert e <= 1e-8, ((i0, j0), e)
+
+
+def test_cfg5_fp32_windows_100_steps(ora):
+    """configs[4] (8192^2, fp32 storage and arithmetic) against the fp64 oracle after 100 steps,
+    normwise <= 1e-4 on two light-cone windows: across the film interface (y = 4096) straddling
+    column boundaries, and at the substrate boundary."""
+    p = pf.pf_default_params(5)
+    nx, ny = p.nx, p.ny
+    m, ic = oracle_member(ora, p, 0)
+    wins = [(2000, 3584, 1024, 1024), (6000, 0, 1024, 1024)]
+    futs = [_POOL.submit(_window, ora, m, ic, 0, nx, ny, i0, j0, W, H, 100) for i0, j0, W, H in wins]
+    with pf.Simulation(p) as s:
+        s.step(100)
+        g = s.fields(0)
+        d = s.diagnostics(0)
+    assert d[4] == 0
+    for (i0, j0, W, H), f in zip(wins, futs):
+        ref, valid, cols = f.result()
+        e = _window_err(g, j0, H, cols, ref, valid)
+        assert e <= 1e-4, ((i0, j0), e)
+
+
+def test_cfg5_recipe_1024_full_grid_fp32(ora):
+    """The configs[4] recipe at 1024^2 (64 columns, tanh film at ny/2), fp32 vs the fp64 oracle on
+    the whole grid after 100 steps (<= 1e-4) -- the CI-size version of the 8192^2 check."""
+    p = pf.pf_default_params(5).replace(nx=1024, ny=1024, ic_height=512.0)
+    m, ic = oracle_member(ora, p, 0)
+    fut = _POOL.submit(lambda: ora.step(m, *ora.initial_fields(ic, 1024, 1024, 0), 100))
+    with pf.Simulation(p) as s:
+        s.step(100)
+        g = s.fields(0)
+    e = normwise(g, fut.result())
+    assert e <= 1e-4, e
+
+
+@pytest.mark.skipif(os.environ.get("PF_NIGHTLY") != "1", reason="full horizons take ~10 min of oracle time; PF_NIGHTLY=1")
+def test_nightly_full_horizons(ora):
+    """SURVEY 8(c.4) full horizons: configs[1] 10,000 steps and configs[2] members 0, 21, 42, 63
+    after 5,000 steps, <= 1e-8 normwise."""
+    p2 = pf.pf_default_params(2)
+    m2, ic2 = oracle_member(ora, p2, 0)
+    f2 = _POOL.submit(lambda: ora.step(m2, *ora.initial_fields(ic2, 256, 256, 0), 10000))
+    p3 = pf.pf_default_params(3)
+
+    def long(k):
+        m, ic = oracle_member(ora, p3, k)
+        return k, ora.step(m, *ora.initial_fields(ic, 512, 512, k), 5000)
+
+    f3 = [_POOL.submit(long, k) for k in (0, 21, 42, 63)]
+    with pf.Simulation(p2) as s:
+        s.step(10000)
+        g2 = s.fields(0)
+    with pf.Simulation(p3) as s:
+        s.step(5000)
+        g3 = {k: s.fields(k) for k in (0, 21, 42, 63)}
+    assert normwise(g2, f2.result()) <= 1e-8
+    for f in f3:
+        k, ref = f.result()
+        assert normwise(g3[k], ref) <= 1e-8, k
