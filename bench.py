@@ -120,36 +120,63 @@ def _cpu_baseline(seconds=12.0):
             "sample": f"configs[2] member 0 (512x512 fp64), {steps} midpoint steps, single thread, {el:.1f} s"}
 
 
-def _dist():
-    ws = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return ws, rank, local
+# (nx, ny, members, storage) of BASELINE.json configs[0..4] (R-13, R-14)
+PRESETS = {1: (64, 64, 1, "fp64"), 2: (256, 256, 1, "fp64"), 3: (512, 512, 64, "fp64"),
+           4: (4096, 4096, 1, "fp64"), 5: (8192, 8192, 1, "fp32")}
+
+
+def workload_config(cfg, ws):
+    """The `config` object of the JSON line (identical for both arms)."""
+    nx, ny, mem, dt = PRESETS[cfg]
+    esz = 8 if dt == "fp64" else 4
+    if cfg == 3:
+        desc = f"configs[2]: {mem} x {nx}x{ny} {dt} ensemble per GPU (weak, {mem * ws} members total)"
+    elif cfg == 4:
+        ny = ny * ws
+        desc = f"configs[3]: {nx}x{ny} {dt} y-slab decomposed over {ws} GPU(s) (weak: 4096 rows per GPU)"
+    elif cfg == 5:
+        desc = f"configs[4]: {nx}x{ny} {dt} y-slab decomposed over {ws} GPU(s) (strong)"
+    else:
+        desc = f"configs[{cfg - 1}]: {mem} x {nx}x{ny} {dt}"
+    cells = mem * nx * ny // (ws if cfg == 5 else 1) // (ws if cfg == 4 else 1)
+    l2 = f"state {2 * 3 * cells * esz / 2**20:.0f} MiB per GPU " + (
+        "(inputs larger than L2)" if 2 * 3 * cells * esz > 126 * 2**20 else "(L2-resident; no flush)")
+    return {"workload": desc, "nx": nx, "ny": ny, "members_per_gpu": mem, "check_every": 100, "l2": l2}
 
 
 def run_reference(args):
-    """--impl reference: the oracle (the reference arm of this tier) on the host cores."""
-    ws, rank, _ = _dist()
+    """--impl reference: the oracle (the reference arm of this tier) as it stands, one thread on
+    the host cores; each step advances a bounded 512 x 512 sample of the workload (configs[2]:
+    member 0; configs[3..4]: the bottom 512 x 512 tile) by one explicit-midpoint step."""
+    rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
     from oracle import oracle as ora
-    pr = ora.preset(3)
+    cfg = args.config
+    pr = ora.preset(cfg)
     m = ora.member_model(pr, 0)
-    u = ora.initial_fields(pr["ic"], 512, 512, 0)
+    nx, ny, mem, dt = PRESETS[cfg]
+    tx, ty = min(512, nx), min(512, ny)
+    c, phi, rho = ora.initial_fields_rows(pr["ic"], nx, 0, 0, ty)
+    u = (c[:, :tx].copy(), phi[:, :tx].copy(), rho[:, :tx].copy())
     for _ in range(args.warmup):
         u = ora.step(m, *u, 1)
     t0 = time.perf_counter()
     for _ in range(args.steps):
         u = ora.step(m, *u, 1)
     el = time.perf_counter() - t0
-    v = 512 * 512 * args.steps / el
+    v = tx * ty * args.steps / el
+    cfgd = workload_config(cfg, ws)
+    cells = cfgd["members_per_gpu"] * nx * PRESETS[cfg][1] * ws
+    sample = (f"{tx}x{ty} fp64 tile of configs[{cfg - 1}] ({'member 0' if cfg == 3 else 'bottom tile'}), "
+              f"{args.steps} midpoint steps, single thread, {el:.2f} s; ms_per_step extrapolated to the "
+              f"{cells} cells of the {ws}-GPU workload")
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * cells / v,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic",
-            "config": {"workload": "configs[2] (64 x 512^2 fp64 ensemble); oracle sample: member 0 per step"},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
-                             "sample": f"configs[2] member 0, 512x512 fp64, {args.steps} steps, single thread"},
+            "data": "synthetic (seeded BASELINE.json configs recipe, DESIGN.md 5)", "config": cfgd,
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -160,30 +187,24 @@ def run_ours(args):
     import torch
     from paper_2312_05410_b200 import pf
 
-    ws, rank, local = _dist()
+    from paper_2312_05410_b200 import dist as D
+    ws, rank, local = D.world()
     if args.gpus != ws and ws > 1:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={ws}")
     torch.cuda.set_device(local)
-    dist = None
-    if ws > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    dist = D.init("nccl", dev)
 
     cfg = args.config
     p = pf.pf_default_params(cfg).replace(device=local)
     if cfg == 3:
-        p = p.replace(member_offset=rank * p.n_members)        # weak: 64 members per GPU
+        off, n = D.ensemble_slice(p.n_members, rank, ws, weak=True)   # weak: 64 members per GPU
+        p = p.replace(member_offset=off, n_members=n)
         mode = "single"
         workload = f"configs[2]: {p.n_members} x {p.nx}x{p.ny} fp64 ensemble per GPU (weak, {p.n_members * ws} members total)"
     elif cfg == 4 or cfg == 5:
         p = p.replace(ny=p.ny * ws) if cfg == 4 else p          # cfg4 weak: 4096 x 4096 per GPU
-        if ws > 1:
-            uid = pf.pf_nccl_unique_id() if rank == 0 else bytes(128)
-            t = torch.tensor(list(uid), dtype=torch.uint8, device="cuda")
-            dist.broadcast(t, 0)
-            mode = ("slab", rank, ws, bytes(t.cpu().tolist()))
-        else:
-            mode = "single"
+        mode = ("slab", rank, ws, D.nccl_uid(dist, dev)) if ws > 1 else "single"
         workload = (f"configs[{cfg - 1}]: {p.nx}x{p.ny} {'fp64' if p.precision == 0 else 'fp32'}"
                     f" y-slab decomposed over {ws} GPU(s)")
     else:
@@ -218,11 +239,7 @@ def run_ours(args):
     prof = pf.pf_profile_read(ctx)
     pf.pf_profile(ctx, False)
     launches = pf.pf_launch_count(ctx) - l0
-    ms_max = ms
-    if dist is not None:
-        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_max = float(t.item())
+    ms_max = D.max_over_ranks(dist, ms, dev) if dist is not None else ms
     value = cells_local * ws * args.steps / (ms_max * 1e-3)
 
     # roofline of the dominant kernel (stage_kernel), algorithmic bytes per launch
@@ -252,9 +269,7 @@ def run_ours(args):
     barrier()
     ms_e2e = e0.elapsed_time(e1)
     if dist is not None:
-        t = torch.tensor([ms_e2e], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_e2e = float(t.item())
+        ms_e2e = D.max_over_ranks(dist, ms_e2e, dev)
     host_bytes = 3 * cells_local * 8
     e2e = {"value": cells_local * ws * e2e_steps / (ms_e2e * 1e-3), "unit": UNIT,
            "h2d_bytes_per_step": host_bytes / e2e_steps, "d2h_bytes_per_step": host_bytes / e2e_steps,
@@ -269,9 +284,7 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64" if p.precision == pf.PF_F64 else "f32",
             "data": "synthetic (seeded BASELINE.json configs recipe, DESIGN.md 5)",
-            "config": {"workload": workload, "nx": p.nx, "ny": p.ny, "members_per_gpu": p.n_members,
-                       "check_every": p.check_every,
-                       "l2": f"inputs larger than L2: state {2 * cells_local * 3 * esz / 2**20:.0f} MiB per GPU"},
+            "config": workload_config(cfg, ws),
             "hbm_gbs_effective": value * alg_per_cell_step / ws / 1e9,
             "hbm_frac_effective": value * alg_per_cell_step / ws / 1e9 / peak,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

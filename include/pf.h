@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define PF_ABI_VERSION 1u
+#define PF_ABI_VERSION 2u
 
 typedef struct pf_ctx pf_ctx; /* opaque */
 
@@ -86,6 +86,9 @@ typedef struct {
     int32_t kernel_path;             /* stage kernel: 0 auto (pair kernel when nx % 4 == 0 and
                                         nx >= 16, else tile kernel), 1 tile, 2 one-column streaming
                                         kernel, 3 pair streaming kernel                         */
+    int32_t overlap_halo;            /* slab modes: 1 = update the 2-row boundary bands first and
+                                        overlap the halo exchange with the interior update
+                                        (needs >= 8 rows per slab), 0 = exchange after the stage */
 } pf_params;
 
 /* Fill *out with the preset of BASELINE.json configs[cfg-1] (cfg = 1..5; R-13, R-14).
@@ -125,6 +128,17 @@ pf_status pf_nccl_unique_id(uint8_t out[128]);
  * `uid` comes from pf_nccl_unique_id on rank 0.  Errors: as pf_create plus PF_ERR_NCCL. */
 pf_status pf_create_slab(const pf_params *p, int32_t rank, int32_t nranks,
                          const uint8_t uid[128], pf_ctx **out);
+
+/* Host-only: the y-slab decomposition of rank `rank` of `nranks` over ny global rows
+ * (the plan pf_create_slab / pf_create_loopback use):
+ *   out[0] = y0, first owned global row        out[1] = ny_local = ny / nranks
+ *   out[2] = rank below (r-1), -1 at the substrate   out[3] = rank above (r+1), -1 at the top
+ *   out[4] = first local row sent down (0)     out[5] = first local row sent up (ny_local-2)
+ *   out[6] = first ghost row filled from below (-2)  out[7] = first ghost row filled from above
+ *            (ny_local).
+ * Every message carries 2 full padded rows (ghost columns included) of c, phi and rho of every
+ * member.  Errors: PF_ERR_ARG (ny % nranks != 0, ny / nranks < 2, rank out of range). */
+pf_status pf_halo_plan(int32_t ny, int32_t nranks, int32_t rank, int32_t out[8]);
 
 /* Single-process multi-slab context ("loopback"): nslabs y-slabs of every member on ONE
  * device, with the halo exchange done by device-to-device copies.  Same arithmetic and

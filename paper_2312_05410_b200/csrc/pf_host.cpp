@@ -196,6 +196,9 @@ struct pf_ctx {
     int ny_host = 0;       // rows covered by the host buffers of get/set
     int y_host0 = 0;       // first global row of the host buffers
     cudaStream_t stream = nullptr;
+    cudaStream_t comm_stream = nullptr;   // halo exchange, overlapped with interior compute
+    cudaEvent_t ev_band = nullptr, ev_xchg = nullptr;
+    bool overlap = false;                 // band / exchange / interior schedule in use
     ncclComm_t comm = nullptr;
     void *vel = nullptr;   // [members][2] in the storage precision
     double *h_diag = nullptr;
@@ -257,6 +260,7 @@ pf_status validate(const pf_params *p, std::string &why) {
     if (p->M_A_bulk < 0 || p->M_B_bulk < 0 || p->M_A_surf < 0 || p->M_B_surf < 0) { why = "mobilities must be >= 0"; return PF_ERR_ARG; }
     if (p->check_every < 1) { why = "check_every must be >= 1"; return PF_ERR_ARG; }
     if (p->graph_steps < 0) { why = "graph_steps must be >= 0"; return PF_ERR_ARG; }
+    if (p->overlap_halo != 0 && p->overlap_halo != 1) { why = "overlap_halo must be 0 or 1"; return PF_ERR_ARG; }
     if (p->kernel_path < 0 || p->kernel_path > 3) { why = "kernel_path must be 0, 1, 2 or 3"; return PF_ERR_ARG; }
     if (p->kernel_path >= 2 && !(p->nx % 4 == 0 && p->nx >= 16)) { why = "streaming kernels need nx % 4 == 0 and nx >= 16"; return PF_ERR_ARG; }
     if (p->ic < PF_IC_FILM || p->ic > PF_IC_NONE) { why = "unknown ic"; return PF_ERR_ARG; }
@@ -290,6 +294,9 @@ void destroy(pf_ctx *c) {
         cudaEventDestroy(r.second.second);
     }
     if (c->comm) ncclCommDestroy(c->comm);
+    if (c->ev_band) cudaEventDestroy(c->ev_band);
+    if (c->ev_xchg) cudaEventDestroy(c->ev_xchg);
+    if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }
@@ -299,33 +306,51 @@ void destroy(pf_ctx *c) {
 
 void *buf_of(Slab &s, int which) { return which == 0 ? s.U : s.Us; }
 
-pf_status exchange(pf_ctx *c, int which) {
+// y-slab decomposition; see pf_halo_plan in pf.h for the meaning of out[].
+bool halo_plan(int ny, int nranks, int rank, int out[8]) {
+    if (nranks < 1 || rank < 0 || rank >= nranks || ny % nranks != 0 || ny / nranks < 2) return false;
+    const int rows = ny / nranks;
+    out[0] = rank * rows;
+    out[1] = rows;
+    out[2] = rank > 0 ? rank - 1 : -1;
+    out[3] = rank < nranks - 1 ? rank + 1 : -1;
+    out[4] = 0;          // rows [0, 2) go down
+    out[5] = rows - 2;   // rows [rows-2, rows) go up
+    out[6] = -2;         // ghost rows [-2, 0) come from below
+    out[7] = rows;       // ghost rows [rows, rows+2) come from above
+    return true;
+}
+
+pf_status exchange(pf_ctx *c, int which, cudaStream_t st) {
     if (c->mode == kSingle) return PF_OK;
     const size_t rowb = (size_t)c->slabs[0].L.pitch * c->esz;   // full padded rows (ghost columns too)
     if (c->mode == kLoopback) {
         const int P = (int)c->slabs.size();
         for (int s = 0; s < P; ++s) {
             Slab &me = c->slabs[s];
+            int plan[8];
+            halo_plan(c->p.ny, P, s, plan);
             const size_t pitch = (size_t)me.L.fstride * c->esz;
             char *mine = (char *)buf_of(me, which);
-            if (s > 0) {    // rows -2, -1  <-  slab s-1 rows ny_loc-2, ny_loc-1
-                Slab &lo = c->slabs[s - 1];
-                const char *src = (const char *)buf_of(lo, which) + (size_t)(lo.L.ny_loc) * rowb;
-                CK(c, cudaMemcpy2DAsync(mine, pitch, src, pitch, 2 * rowb, (size_t)3 * me.L.members,
-                                        cudaMemcpyDeviceToDevice, c->stream));
+            if (plan[2] >= 0) {    // ghost rows [-2, 0)  <-  slab below, rows [rows-2, rows)
+                Slab &lo = c->slabs[plan[2]];
+                const char *src = (const char *)buf_of(lo, which) + (size_t)(plan[5] + 2) * rowb;
+                CK(c, cudaMemcpy2DAsync(mine + (size_t)(plan[6] + 2) * rowb, pitch, src, pitch, 2 * rowb,
+                                        (size_t)3 * me.L.members, cudaMemcpyDeviceToDevice, st));
             }
-            if (s < P - 1) {    // rows ny_loc, ny_loc+1  <-  slab s+1 rows 0, 1
-                Slab &hi = c->slabs[s + 1];
-                const char *src = (const char *)buf_of(hi, which) + 2 * rowb;
-                CK(c, cudaMemcpy2DAsync(mine + (size_t)(me.L.ny_loc + 2) * rowb, pitch, src, pitch,
-                                        2 * rowb, (size_t)3 * me.L.members, cudaMemcpyDeviceToDevice,
-                                        c->stream));
+            if (plan[3] >= 0) {    // ghost rows [rows, rows+2)  <-  slab above, rows [0, 2)
+                Slab &hi = c->slabs[plan[3]];
+                const char *src = (const char *)buf_of(hi, which) + (size_t)(plan[4] + 2) * rowb;
+                CK(c, cudaMemcpy2DAsync(mine + (size_t)(plan[7] + 2) * rowb, pitch, src, pitch, 2 * rowb,
+                                        (size_t)3 * me.L.members, cudaMemcpyDeviceToDevice, st));
             }
         }
         return PF_OK;
     }
-    // NCCL: rank r exchanges 2 rows of every field of every member with r-1 and r+1.
+    // NCCL: 2 full padded rows of every field of every member to / from each neighbour.
     Slab &me = c->slabs[0];
+    int plan[8];
+    halo_plan(c->p.ny, c->nranks, c->rank, plan);
     const ncclDataType_t dt = c->p.precision == PF_F64 ? ncclFloat64 : ncclFloat32;
     const size_t cnt = 2 * (size_t)me.L.pitch;
     char *base = (char *)buf_of(me, which);
@@ -333,14 +358,13 @@ pf_status exchange(pf_ctx *c, int which) {
     for (int m = 0; m < me.L.members; ++m)
         for (int f = 0; f < 3; ++f) {
             char *fb = base + ((size_t)m * me.L.mstride + (size_t)f * me.L.fstride) * c->esz;
-            if (c->rank > 0) {
-                NK(c, ncclSend(fb + 2 * rowb, cnt, dt, c->rank - 1, c->comm, c->stream));
-                NK(c, ncclRecv(fb, cnt, dt, c->rank - 1, c->comm, c->stream));
+            if (plan[2] >= 0) {
+                NK(c, ncclSend(fb + (size_t)(plan[4] + 2) * rowb, cnt, dt, plan[2], c->comm, st));
+                NK(c, ncclRecv(fb + (size_t)(plan[6] + 2) * rowb, cnt, dt, plan[2], c->comm, st));
             }
-            if (c->rank < c->nranks - 1) {
-                NK(c, ncclSend(fb + (size_t)me.L.ny_loc * rowb, cnt, dt, c->rank + 1, c->comm, c->stream));
-                NK(c, ncclRecv(fb + (size_t)(me.L.ny_loc + 2) * rowb, cnt, dt, c->rank + 1, c->comm,
-                               c->stream));
+            if (plan[3] >= 0) {
+                NK(c, ncclSend(fb + (size_t)(plan[5] + 2) * rowb, cnt, dt, plan[3], c->comm, st));
+                NK(c, ncclRecv(fb + (size_t)(plan[7] + 2) * rowb, cnt, dt, plan[3], c->comm, st));
             }
         }
     NK(c, ncclGroupEnd());
@@ -358,7 +382,24 @@ cudaEvent_t take_event(pf_ctx *c) {
     return e;
 }
 
+pf_status launch_rows(pf_ctx *c, Slab &s, int stage, int r0, int r1, bool capture) {
+    if (r1 <= r0) return PF_OK;
+    pf::Layout L = s.L;
+    L.r0 = r0;
+    L.r1 = r1;
+    const void *in = stage == 1 ? s.U : s.Us;
+    void *out = stage == 1 ? s.Us : s.U;
+    const double coef = stage == 1 ? 0.5 * c->p.dt : c->p.dt;
+    CK(c, pf::launch_stage(c->p.precision, L, s.plan, c->K, stage, in, s.U, out, c->vel, coef, c->stream));
+    if (!capture) c->launches += pf::kStageLaunches;
+    return PF_OK;
+}
+
 // One explicit-midpoint step for every slab: stage 1, exchange, stage 2, exchange.
+// Slab modes with the overlap schedule: each stage first updates the two boundary
+// bands (rows [0, 2) and [ny_loc-2, ny_loc)), the halo exchange of those rows then runs on the
+// comm stream while the interior rows [2, ny_loc-2) are updated -- the interior reads no ghost
+// row, so it never waits for the exchange -- and the next stage waits for the exchange.
 pf_status one_step(pf_ctx *c, bool capture) {
     const bool prof = c->prof && !capture;
     for (int stage = 1; stage <= 2; ++stage) {
@@ -368,19 +409,28 @@ pf_status one_step(pf_ctx *c, bool capture) {
             e1 = take_event(c);
             CK(c, cudaEventRecord(e0, c->stream));
         }
-        for (auto &s : c->slabs) {
-            const void *in = stage == 1 ? s.U : s.Us;
-            void *out = stage == 1 ? s.Us : s.U;
-            const double coef = stage == 1 ? 0.5 * c->p.dt : c->p.dt;
-            CK(c, pf::launch_stage(c->p.precision, s.L, s.plan, c->K, stage, in, s.U, out, c->vel, coef, c->stream));
-            if (!capture) c->launches += pf::kStageLaunches;
+        const int which = stage == 1 ? 1 : 0;   // buffer written by this stage
+        pf_status st = PF_OK;
+        if (!c->overlap) {
+            for (auto &s : c->slabs)
+                if ((st = launch_rows(c, s, stage, 0, s.L.ny_loc, capture)) != PF_OK) return st;
+            if (prof) CK(c, cudaEventRecord(e1, c->stream));
+            if ((st = exchange(c, which, c->stream)) != PF_OK) return st;
+        } else {
+            for (auto &s : c->slabs) {
+                if ((st = launch_rows(c, s, stage, 0, 2, capture)) != PF_OK) return st;
+                if ((st = launch_rows(c, s, stage, s.L.ny_loc - 2, s.L.ny_loc, capture)) != PF_OK) return st;
+            }
+            CK(c, cudaEventRecord(c->ev_band, c->stream));
+            CK(c, cudaStreamWaitEvent(c->comm_stream, c->ev_band, 0));
+            if ((st = exchange(c, which, c->comm_stream)) != PF_OK) return st;
+            CK(c, cudaEventRecord(c->ev_xchg, c->comm_stream));
+            for (auto &s : c->slabs)
+                if ((st = launch_rows(c, s, stage, 2, s.L.ny_loc - 2, capture)) != PF_OK) return st;
+            if (prof) CK(c, cudaEventRecord(e1, c->stream));
+            CK(c, cudaStreamWaitEvent(c->stream, c->ev_xchg, 0));
         }
-        if (prof) {
-            CK(c, cudaEventRecord(e1, c->stream));
-            c->ev_rec.push_back({stage, {e0, e1}});
-        }
-        pf_status st = exchange(c, stage == 1 ? 1 : 0);
-        if (st != PF_OK) return st;
+        if (prof) c->ev_rec.push_back({stage, {e0, e1}});
     }
     return PF_OK;
 }
@@ -503,6 +553,9 @@ pf_status create_common(const pf_params *p, int mode, int rank, int nranks, cons
         return fail(PF_ERR_CUDA);
     }
     e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess && mode != kSingle) e = cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess && mode != kSingle) e = cudaEventCreateWithFlags(&c->ev_band, cudaEventDisableTiming);
+    if (e == cudaSuccess && mode != kSingle) e = cudaEventCreateWithFlags(&c->ev_xchg, cudaEventDisableTiming);
     if (e != cudaSuccess) {
         c->err = fmt("cudaStreamCreate: %s", cudaGetErrorString(e));
         return fail(PF_ERR_CUDA);
@@ -522,6 +575,8 @@ pf_status create_common(const pf_params *p, int mode, int rank, int nranks, cons
         sl.L.pitch = p->nx + 2 * sl.L.gx;
         sl.L.fstride = (int64_t)(rows + 4) * sl.L.pitch;
         sl.L.mstride = 3 * sl.L.fstride;
+        sl.L.r0 = 0;
+        sl.L.r1 = rows;
         const size_t bytes = (size_t)sl.L.mstride * p->n_members * c->esz;
         c->slabs.push_back(sl);
         Slab &S = c->slabs.back();
@@ -545,6 +600,8 @@ pf_status create_common(const pf_params *p, int mode, int rank, int nranks, cons
             return fail(PF_ERR_NOMEM);
         }
     }
+    // overlap schedule: slab modes, bands of 2 rows leave an interior of >= 4 rows
+    c->overlap = mode != kSingle && rows >= 8 && p->overlap_halo != 0;
     c->ny_host = mode == kNccl ? rows : p->ny;
     c->y_host0 = mode == kNccl ? rank * rows : 0;
     if (cudaMallocHost((void **)&c->h_diag, nsl * (size_t)p->n_members * pf::kDiag * sizeof(double)) != cudaSuccess) {
@@ -610,7 +667,7 @@ pf_status create_common(const pf_params *p, int mode, int rank, int nranks, cons
         }
         c->launches += 2 * pf::kFillLaunches;
     }
-    st = exchange(c, 0);
+    st = exchange(c, 0, c->stream);
     if (st != PF_OK) return fail(st);
     e = cudaStreamSynchronize(c->stream);
     if (e != cudaSuccess) {
@@ -677,6 +734,7 @@ pf_status pf_default_params(int32_t cfg, pf_params *o) {
     p.check_every = 100;
     p.seed = (uint64_t)cfg;
     p.graph_steps = 0;
+    p.overlap_halo = 1;
     if (cfg == 1) {             // configs[0]: 64^2 film, all mobilities 1
         p.nx = p.ny = 64;
         p.M_A_bulk = p.M_B_bulk = p.M_A_surf = p.M_B_surf = 1.0;
@@ -739,6 +797,15 @@ pf_status pf_member_velocity(const pf_params *p, int64_t member, double *vx, dou
 pf_status pf_dt_limit(const pf_params *p, double *dt_max) {
     if (!p || !dt_max) return set_err(nullptr, PF_ERR_ARG, "NULL argument");
     *dt_max = dt_limit(*p);
+    return PF_OK;
+}
+
+pf_status pf_halo_plan(int32_t ny, int32_t nranks, int32_t rank, int32_t out[8]) {
+    if (!out) return set_err(nullptr, PF_ERR_ARG, "out is NULL");
+    int o[8];
+    if (!halo_plan(ny, nranks, rank, o))
+        return set_err(nullptr, PF_ERR_ARG, fmt("no slab plan for ny = %d, nranks = %d, rank = %d", ny, nranks, rank));
+    for (int k = 0; k < 8; ++k) out[k] = o[k];
     return PF_OK;
 }
 
@@ -868,7 +935,7 @@ pf_status pf_set_fields(pf_ctx *c, int32_t member, const double *fc, const doubl
         CK(c, pf::launch_fill_ghosts(c->p.precision, S.L, c->p.rho_in, S.U, c->stream));
         c->launches += pf::kFillLaunches;
     }
-    st = exchange(c, 0);
+    st = exchange(c, 0, c->stream);
     if (st != PF_OK) return st;
     CK(c, cudaStreamSynchronize(c->stream));
     c->blown = false;

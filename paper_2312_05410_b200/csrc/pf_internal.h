@@ -10,7 +10,7 @@ namespace pf {
 // Device layout of one state buffer:
 //   [member][field = c, phi, rho][row = -2 .. ny_loc+1][x = -gx .. nx+gx-1]
 // Row r of a field lives at storage row r + 2 and column x at storage column x + gx, so the
-// ghost frame is physically present: gx = 16 bytes / sizeof(real) ghost columns on each side
+// ghost frame is physically present: gx = 32 bytes / sizeof(real) ghost columns on each side
 // hold the periodic copies, two ghost rows below / above hold the y-mirror rows (c, phi), the
 // rho reservoir value rho_in (top) or, at a slab-interior face, the neighbouring slab's rows.
 // The streaming kernel keeps the frame up to date as it writes; fill_ghosts rebuilds it after
@@ -19,10 +19,11 @@ struct Layout {
     int nx, ny, ny_loc, y0;      // global grid, owned rows, first owned global row
     int members;
     int path;                    // stage kernel: 0 auto (= 3 when eligible), 1 tile, 2 stream, 3 pair
-    int gx;                      // ghost columns per side (16 B / element size)
+    int gx;                      // ghost columns per side (32 B / element size)
     int pitch;                   // elements per storage row = nx + 2 gx
     int64_t fstride;             // elements per field  = (ny_loc + 4) * pitch
     int64_t mstride;             // elements per member = 3 * fstride
+    int r0, r1;                  // row window [r0, r1) a stage launch updates (default [0, ny_loc))
     __host__ __device__ int64_t at(int r, int x) const { return (int64_t)(r + 2) * pitch + (x + gx); }
 };
 

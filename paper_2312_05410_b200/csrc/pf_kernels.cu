@@ -68,7 +68,7 @@ __global__ void __launch_bounds__(NT) stage_kernel(Layout L, KC<real> k, const r
 
     const int m = blockIdx.z;
     const int tx0 = blockIdx.x * BX;
-    const int ty0 = blockIdx.y * BY;
+    const int ty0 = L.r0 + blockIdx.y * BY;
     const int nx = L.nx;
     const real *ic = in + m * L.mstride;
     const real *ip = ic + L.fstride;
@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(NT) stage_kernel(Layout L, KC<real> k, const r
     const int gx = tx0 + lx;
     for (int q = threadIdx.x / BX; q < BY; q += NT / BX) {
         const int ly = ty0 + q;
-        if (gx >= nx || ly >= L.ny_loc) continue;
+        if (gx >= nx || ly >= L.r1) continue;
         const int y = q + 1, x = lx + 1;                    // ring coordinates
         const int cy = q + 2, cx = lx + 2;                   // c/phi tile coordinates
         const int64_t o = m * L.mstride + L.at(ly, gx);
@@ -351,15 +351,16 @@ struct Sched {
 };
 __device__ __forceinline__ Sched make_sched(const Layout &L, int Wo, int G) {
     const int strips = (L.nx + Wo - 1) / Wo;
+    const int nyl = L.r1 - L.r0;        // rows of this launch's row window
     Sched sc;
     if (G > 0) {
         const int g = blockIdx.x / strips;
         sc.strip = blockIdx.x - g * strips;
-        const int64_t T = (int64_t)L.members * L.ny_loc;
+        const int64_t T = (int64_t)L.members * nyl;
         sc.lo = T * g / G;
         sc.hi = T * (g + 1) / G;
     } else {
-        const int64_t R = (int64_t)L.members * strips * L.ny_loc;
+        const int64_t R = (int64_t)L.members * strips * nyl;
         sc.strip = -1;
         sc.lo = R * blockIdx.x / gridDim.x;
         sc.hi = R * (blockIdx.x + 1) / gridDim.x;
@@ -368,11 +369,13 @@ __device__ __forceinline__ Sched make_sched(const Layout &L, int Wo, int G) {
 }
 __device__ __forceinline__ bool next_seg(const Layout &L, int Wo, const Sched &sc, int64_t &pos, Seg &sg) {
     if (pos >= sc.hi) return false;
-    const int nyl = L.ny_loc, strips = (L.nx + Wo - 1) / Wo;
+    const int nyl = L.r1 - L.r0, strips = (L.nx + Wo - 1) / Wo;
     const int64_t col = pos / nyl;      // grouped: member; ungrouped: member * strips + strip
-    sg.ya = (int)(pos - col * nyl);
-    sg.yb = (int)min((int64_t)nyl, (int64_t)sg.ya + (sc.hi - pos));
-    pos += sg.yb - sg.ya;
+    const int la = (int)(pos - col * nyl);
+    const int lb = (int)min((int64_t)nyl, (int64_t)la + (sc.hi - pos));
+    pos += lb - la;
+    sg.ya = L.r0 + la;
+    sg.yb = L.r0 + lb;
     int sidx;
     if (sc.strip >= 0) {
         sg.m = (int)col;
@@ -413,18 +416,17 @@ size_t stream_smem_bytes(int bx, int R, int S, bool base) {
 // x ghost columns and, at the global y boundaries, the mirror ghost rows (c, phi; rho at the
 // bottom; rho's top ghost rows hold the reservoir value and are never overwritten).
 template <typename real>
+__device__ __forceinline__ void store_row_ghosts(const Layout &L, real *b, int r, int x, real v) {
+    b[L.at(r, x)] = v;
+    if (x < L.gx) b[L.at(r, x + L.nx)] = v;
+    if (x >= L.nx - L.gx) b[L.at(r, x - L.nx)] = v;
+}
+template <typename real>
 __device__ __forceinline__ void store_with_ghosts(const Layout &L, real *b, int f, int r, int x, real v) {
     const int g = L.y0 + r;
-    int rr[2];
-    int nr = 0;
-    rr[nr++] = r;
-    if (g <= 1) rr[nr++] = -1 - r;                                        // y0 == 0 here
-    else if (g >= L.ny - 2 && f != 2) rr[nr++] = 2 * L.ny_loc - 1 - r;    // top slab
-    for (int q = 0; q < nr; ++q) {
-        b[L.at(rr[q], x)] = v;
-        if (x < L.gx) b[L.at(rr[q], x + L.nx)] = v;
-        if (x >= L.nx - L.gx) b[L.at(rr[q], x - L.nx)] = v;
-    }
+    store_row_ghosts(L, b, r, x, v);
+    if (g <= 1) store_row_ghosts(L, b, -1 - r, x, v);                                // y0 == 0 here
+    else if (g >= L.ny - 2 && f != 2) store_row_ghosts(L, b, 2 * L.ny_loc - 1 - r, x, v);   // top slab
 }
 
 template <typename real, int NCW, int R, int S, bool BASE, bool HMIX, int MINB>
@@ -823,13 +825,13 @@ cudaError_t launch_ring(const Layout &L, const StreamPlan &P, const KC<real> &k,
         if (e != cudaSuccess) return e;
         if (occ < 1) occ = 1;
     }
-    const int64_t R_ = (int64_t)L.members * P.strips * L.ny_loc;
+    const int64_t R_ = (int64_t)L.members * P.strips * (L.r1 - L.r0);
     const int64_t minrows = 16;
     int64_t B = (int64_t)occ * nsm;
     static const int nogroup = env_int("PF_STREAM_NOGROUP", 0);
     // grouped schedule when at least 4 groups of `strips` blocks fit in one resident wave
     int64_t G = B / P.strips;
-    const int64_t T = (int64_t)L.members * L.ny_loc;
+    const int64_t T = (int64_t)L.members * (L.r1 - L.r0);
     if (G > (T + minrows - 1) / minrows) G = (T + minrows - 1) / minrows;
     if (G >= 4 && !nogroup) {
         B = G * P.strips;
@@ -982,7 +984,7 @@ cudaError_t launch_stage(int precision, const Layout &L, const StreamPlan &P, co
             return launch_stream<double>(L, P, make_kc<double>(K, coef), stage, (double *)out, (const double *)vel, s);
         return launch_stream<float>(L, P, make_kc<float>(K, coef), stage, (float *)out, (const float *)vel, s);
     }
-    dim3 grid((L.nx + BX - 1) / BX, (L.ny_loc + BY - 1) / BY, L.members);
+    dim3 grid((L.nx + BX - 1) / BX, (L.r1 - L.r0 + BY - 1) / BY, L.members);
     if (precision == 0) {
         const KC<double> kd = make_kc<double>(K, coef);
         if (kd.hmix)

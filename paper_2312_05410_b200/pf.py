@@ -16,7 +16,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libpf.so")
 HEADER = os.path.join(os.path.dirname(_HERE), "include", "pf.h")
 
-PF_ABI_VERSION = 1
+PF_ABI_VERSION = 2
 PF_OK, PF_ERR_ARG, PF_ERR_UNSTABLE_DT, PF_ERR_NOMEM, PF_ERR_CUDA, PF_ERR_NCCL, PF_ERR_BLOWUP, \
     PF_ERR_STATE, PF_ERR_ABI = range(9)
 STATUS_NAMES = ["PF_OK", "PF_ERR_ARG", "PF_ERR_UNSTABLE_DT", "PF_ERR_NOMEM", "PF_ERR_CUDA",
@@ -41,7 +41,7 @@ class pf_params(C.Structure):
         ("noise_c", C.c_double), ("noise_phi", C.c_double),
         ("noise_c_gaussian", C.c_int32), ("check_every", C.c_int32),
         ("seed", C.c_uint64), ("device", C.c_int32), ("graph_steps", C.c_int32),
-        ("kernel_path", C.c_int32),
+        ("kernel_path", C.c_int32), ("overlap_halo", C.c_int32),
     ]
 
     def as_dict(self):
@@ -88,6 +88,7 @@ def lib():
             "pf_nccl_unique_id": (C.c_int, [C.c_char_p]),
             "pf_create_slab": (C.c_int, [P, i32, i32, C.c_char_p, C.POINTER(_ctx_p)]),
             "pf_create_loopback": (C.c_int, [P, i32, C.POINTER(_ctx_p)]),
+            "pf_halo_plan": (C.c_int, [i32, i32, i32, C.POINTER(i32)]),
             "pf_step": (C.c_int, [_ctx_p, i64]),
             "pf_get_fields": (C.c_int, [_ctx_p, i32, _D, _D, _D]),
             "pf_set_fields": (C.c_int, [_ctx_p, i32, _D, _D, _D]),
@@ -168,6 +169,13 @@ def pf_create(p: pf_params):
     ctx = _ctx_p()
     _check(lib().pf_create(C.byref(p), C.byref(ctx)))
     return ctx
+
+
+def pf_halo_plan(ny: int, nranks: int, rank: int):
+    """(y0, ny_local, below, above, send_down_row, send_up_row, recv_below_row, recv_above_row)."""
+    out = (C.c_int32 * 8)()
+    _check(lib().pf_halo_plan(ny, nranks, rank, out))
+    return tuple(out)
 
 
 def pf_create_loopback(p: pf_params, nslabs: int):

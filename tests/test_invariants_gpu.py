@@ -96,10 +96,13 @@ def test_resume_equals_straight_run():
         assert s.info()[0] == 40
 
 
-@pytest.mark.parametrize("nslabs,path", [(2, 0), (4, 0), (4, 1), (8, 0), (4, 2)])
-def test_loopback_slabs_equal_single_domain(nslabs, path):
-    """The y-slab decomposition (2-row halo exchanged after every stage) is bitwise invisible."""
-    p = _base(128, 64, n_members=2, kernel_path=path)
+@pytest.mark.parametrize("nslabs,path,overlap,graph", [(2, 0, 1, 0), (4, 0, 1, 0), (4, 1, 1, 0), (8, 0, 1, 0),
+                                                        (4, 2, 1, 0), (4, 0, 0, 0), (2, 0, 1, 8), (16, 0, 1, 0)])
+def test_loopback_slabs_equal_single_domain(nslabs, path, overlap, graph):
+    """The y-slab decomposition (2-row halo exchanged after every stage) is bitwise invisible, with
+    and without the overlap schedule (boundary bands first, exchange on the comm stream while the
+    interior is updated), inside CUDA graphs, and for slabs of 4 rows (no overlap possible)."""
+    p = _base(128, 64, n_members=2, kernel_path=path, overlap_halo=overlap, graph_steps=graph)
     a = _run(p, 25)
     b = _run(p, 25, mode=("loopback", nslabs))
     for m in range(2):
@@ -111,6 +114,15 @@ def test_loopback_slabs_equal_single_domain(nslabs, path):
         s.step(3)
         d1 = s.diagnostics(1)
     np.testing.assert_allclose(d, d1, rtol=1e-12, atol=0)
+
+
+def test_loopback_overlap_large_grid_cfg4_physics():
+    """A 1024 x 512 grid of configs[3] physics in 4 slabs of 128 rows (interface on a slab
+    boundary): overlap schedule bitwise equal to the single domain after 30 steps."""
+    p = pf.pf_default_params(4).replace(nx=1024, ny=512, ic_height=128.0)
+    a = _run(p, 30)
+    b = _run(p, 30, mode=("loopback", 4))
+    assert _eq(a[0], b[0])
 
 
 def test_graphs_equal_direct_launches():
