@@ -27,10 +27,10 @@ __device__ __forceinline__ float fma_(float a, float b, float c) { return __fmaf
 // exp(x) for x <= 0 (the argument here is -(phit/sigma)^2), branch-free, table-driven:
 // x = (64 n + j) ln2/64 + r with |r| <= ln2/128 (ln2 split as in fdlibm so the reduction is exact),
 // exp(x) = 2^n * T[j] * P(r), T[j] = 2^(j/64) (host-computed, copied to shared memory by each
-// block), P the Taylor polynomial of exp to degree 6 (truncation < 3e-20 relative).  x is
-// clamped to -708 (results below 1e-307 are irrelevant to M_c).  Max error ~2 ulp.
+// block), P the Taylor polynomial of exp to degree 5 (truncation |r|^6/720 < 4e-17 relative),
+// evaluated in Estrin form (dependency depth 3 instead of 5).  x is clamped to -708 (results below
+// 1e-307 are irrelevant to M_c).  Max error ~2 ulp.
 __constant__ double kExp2Tab[64];                        // 2^(j/64), filled by the host
-__constant__ double kExpPoly[4] = {1.0 / 720.0, 1.0 / 120.0, 1.0 / 24.0, 1.0 / 6.0};
 
 __device__ __forceinline__ double exp_neg(double x, const double *tab) {
     const double kMagic = 6755399441055744.0;                 // 1.5 * 2^52
@@ -42,12 +42,12 @@ __device__ __forceinline__ double exp_neg(double x, const double *tab) {
     const double nd = sub_(kd, kMagic);
     double r = fma_(nd, -kLn2Hi64, x);
     r = fma_(nd, -kLn2Lo64, r);
-    double p = fma_(kExpPoly[0], r, kExpPoly[1]);
-    p = fma_(p, r, kExpPoly[2]);
-    p = fma_(p, r, kExpPoly[3]);
-    p = fma_(p, r, 0.5);
-    p = fma_(p, r, 1.0);
-    p = fma_(p, r, 1.0);
+    // P(r) = (1 + r) + r^2 ((1/2 + r/6) + r^2 (1/24 + r/120))
+    const double r2 = mul_(r, r);
+    const double a = add_(r, 1.0);
+    const double b = fma_(r, 1.0 / 6.0, 0.5);
+    const double c = fma_(r, 1.0 / 120.0, 1.0 / 24.0);
+    double p = fma_(r2, fma_(r2, c, b), a);
     p = mul_(p, tab[m & 63]);
     return __hiloint2double(__double2hiint(p) + ((m >> 6) << 20), __double2loint(p));
 }
