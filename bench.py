@@ -264,10 +264,10 @@ def run_ours(args):
     e2e_steps = args.steps
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    oc, op_, orr = (torch.empty_like(hc).pin_memory() for _ in range(3))
+    chunks = min(2, p.n_members)   # tools/e2e_chunks.py: 2 chunks is best on configs[2]
     e0.record(stream)
-    pf.pf_set_fields(ctx, -1, hc, hp, hr)
-    sim.step(e2e_steps)
-    pf.pf_get_fields(ctx, -1, hc, hp, hr)
+    pf.pf_run_host(ctx, e2e_steps, hc, hp, hr, oc, op_, orr, chunks)
     e1.record(stream)
     torch.cuda.synchronize()
     barrier()
@@ -277,8 +277,9 @@ def run_ours(args):
     host_bytes = 3 * cells_local * 8
     e2e = {"value": cells_local * ws * e2e_steps / (ms_e2e * 1e-3), "unit": UNIT,
            "h2d_bytes_per_step": host_bytes / e2e_steps, "d2h_bytes_per_step": host_bytes / e2e_steps,
-           "note": f"pf_set_fields(all members, pinned fp64) + pf_step({e2e_steps}) + pf_get_fields(all), "
-                   "copies amortised over the steps of one call"}
+           "note": f"pf_run_host: upload of every member from pinned fp64 host buffers, {e2e_steps} steps, "
+                   f"download of every member; pipelined over {chunks} member chunks (H2D / compute / D2H "
+                   "streams); copies amortised over the steps of one call"}
 
     line = None
     if rank == 0:

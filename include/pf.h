@@ -154,6 +154,19 @@ pf_status pf_create_loopback(const pf_params *p, int32_t nslabs, pf_ctx **out);
  * Errors: PF_ERR_ARG (n < 0), PF_ERR_STATE, PF_ERR_BLOWUP, PF_ERR_CUDA, PF_ERR_NCCL. */
 pf_status pf_step(pf_ctx *ctx, int64_t n);
 
+/* End-to-end run from host memory (the call bench.py's e2e times): equivalent to
+ * pf_set_fields(ctx, -1, c_in, phi_in, rho_in); pf_step(ctx, n); pf_get_fields(ctx, -1, c_out,
+ * phi_out, rho_out) -- bitwise the same result -- but pipelined over `chunks` groups of members
+ * (members are independent): the upload of chunk k+1 and the download of chunk k-1 overlap the
+ * steps of chunk k on separate streams (pinned host buffers make the copies asynchronous).
+ * Buffers: all members stacked, as for member = -1; NULL inputs keep the device state, NULL
+ * outputs are skipped.  The blow-up check runs once per chunk at the end of the call (the reported
+ * step window is the whole call).  Single-GPU fp64 contexts with chunks >= 2 pipeline; other
+ * contexts run the three calls in sequence.  Synchronous.
+ * Errors: as pf_set_fields, pf_step, pf_get_fields. */
+pf_status pf_run_host(pf_ctx *ctx, int64_t n, const double *c_in, const double *phi_in, const double *rho_in,
+                      double *c_out, double *phi_out, double *rho_out, int32_t chunks);
+
 /* Copy member `member` (0..n_members-1, or -1 = all members, stacked) to host buffers of
  * ny_local*nx doubles each (times n_members for -1).  fp32 fields are widened to double.
  * Errors: PF_ERR_ARG, PF_ERR_CUDA. */

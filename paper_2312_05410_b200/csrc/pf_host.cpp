@@ -210,6 +210,9 @@ struct pf_ctx {
     bool blown = false;
     std::string err;
     int64_t launches = 0;
+    // pf_run_host pipeline: copy streams and per-chunk events
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    std::vector<cudaEvent_t> ev_in, ev_done;
     // CUDA graph of graph_steps steps
     cudaGraphExec_t gexec = nullptr;
     int gsteps = 0;
@@ -297,6 +300,10 @@ void destroy(pf_ctx *c) {
     if (c->ev_band) cudaEventDestroy(c->ev_band);
     if (c->ev_xchg) cudaEventDestroy(c->ev_xchg);
     if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+    for (auto e : c->ev_in) cudaEventDestroy(e);
+    for (auto e : c->ev_done) cudaEventDestroy(e);
+    if (c->h2d) cudaStreamDestroy(c->h2d);
+    if (c->d2h) cudaStreamDestroy(c->d2h);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }
@@ -577,6 +584,7 @@ pf_status create_common(const pf_params *p, int mode, int rank, int nranks, cons
         sl.L.mstride = 3 * sl.L.fstride;
         sl.L.r0 = 0;
         sl.L.r1 = rows;
+        sl.L.m0 = 0;
         const size_t bytes = (size_t)sl.L.mstride * p->n_members * c->esz;
         c->slabs.push_back(sl);
         Slab &S = c->slabs.back();
@@ -867,6 +875,115 @@ pf_status pf_step(pf_ctx *c, int64_t n) {
         }
     }
     CK(c, cudaStreamSynchronize(c->stream));
+    return PF_OK;
+}
+
+pf_status pf_run_host(pf_ctx *c, int64_t n, const double *ci, const double *pi, const double *ri, double *co,
+                      double *po, double *ro, int32_t chunks) {
+    if (!c) return set_err(nullptr, PF_ERR_ARG, "ctx is NULL");
+    if (n < 0) return set_err(c, PF_ERR_ARG, "n must be >= 0");
+    if (c->blown && !(ci && pi && ri)) return set_err(c, PF_ERR_STATE, "state blew up; pass all three input fields");
+    cudaSetDevice(c->p.device);
+    const int M = c->p.n_members;
+    int K = chunks < 1 ? 1 : (chunks > M ? M : chunks);
+    if (c->mode != kSingle || c->p.precision != PF_F64 || K < 2) {
+        pf_status st = PF_OK;
+        if (ci || pi || ri) st = pf_set_fields(c, -1, ci, pi, ri);
+        if (st == PF_OK) st = pf_step(c, n);
+        if (st == PF_OK && (co || po || ro)) st = pf_get_fields(c, -1, co, po, ro);
+        return st;
+    }
+    Slab &S = c->slabs[0];
+    if (!c->h2d) {
+        CK(c, cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking));
+        CK(c, cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking));
+    }
+    while ((int)c->ev_in.size() < K) {
+        cudaEvent_t a, b;
+        CK(c, cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+        CK(c, cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+        c->ev_in.push_back(a);
+        c->ev_done.push_back(b);
+    }
+    const size_t hrow = (size_t)c->p.nx * sizeof(double), hmem = (size_t)S.L.ny_loc * hrow;
+    const size_t dpitch = (size_t)S.L.pitch * sizeof(double);
+    const double *src[3] = {ci, pi, ri};
+    double *dst[3] = {co, po, ro};
+    auto dev_field = [&](int m, int f) {
+        return (char *)S.U + ((size_t)m * S.L.mstride + (size_t)f * S.L.fstride + (size_t)S.L.at(0, 0)) * 8;
+    };
+    // the compute stream must not overtake work already queued on it (previous calls)
+    CK(c, cudaEventRecord(c->ev_done[0], c->stream));
+    CK(c, cudaStreamWaitEvent(c->h2d, c->ev_done[0], 0));
+    // 1. uploads, chunk by chunk, on the H2D stream
+    for (int k = 0; k < K; ++k) {
+        const int m0 = (int)((int64_t)M * k / K), m1 = (int)((int64_t)M * (k + 1) / K);
+        for (int m = m0; m < m1; ++m)
+            for (int f = 0; f < 3; ++f)
+                if (src[f])
+                    CK(c, cudaMemcpy2DAsync(dev_field(m, f), dpitch, (const char *)src[f] + (size_t)m * hmem, hrow,
+                                            hrow, S.L.ny_loc, cudaMemcpyHostToDevice, c->h2d));
+        CK(c, cudaEventRecord(c->ev_in[k], c->h2d));
+    }
+    // 2. per chunk on the compute stream: ghost frame, n steps, diagnostics; then its download
+    for (int k = 0; k < K; ++k) {
+        const int m0 = (int)((int64_t)M * k / K), m1 = (int)((int64_t)M * (k + 1) / K);
+        pf::Layout L = S.L;
+        L.m0 = m0;
+        L.members = m1 - m0;
+        CK(c, cudaStreamWaitEvent(c->stream, c->ev_in[k], 0));
+        if (ci || pi || ri) {
+            pf::Layout Lg = S.L;
+            Lg.members = m1 - m0;
+            CK(c, pf::launch_fill_ghosts(c->p.precision, Lg, c->p.rho_in, (char *)S.U + (size_t)m0 * S.L.mstride * 8,
+                                         c->stream));
+            c->launches += pf::kFillLaunches;
+        }
+        for (int64_t i = 0; i < n; ++i)
+            for (int stage = 1; stage <= 2; ++stage) {
+                const void *in = stage == 1 ? S.U : S.Us;
+                void *out = stage == 1 ? S.Us : S.U;
+                const double coef = stage == 1 ? 0.5 * c->p.dt : c->p.dt;
+                CK(c, pf::launch_stage(c->p.precision, L, S.plan, c->K, stage, in, S.U, out, c->vel, coef, c->stream));
+                c->launches += pf::kStageLaunches;
+            }
+        pf::Layout Ld = S.L;
+        Ld.members = m1 - m0;
+        const int nb = pf::diag_blocks(S.L);
+        CK(c, pf::launch_diag(c->p.precision, Ld, c->K, (char *)S.U + (size_t)m0 * S.L.mstride * 8,
+                              S.partials + (size_t)m0 * nb * pf::kDiag, S.diag + (size_t)m0 * pf::kDiag, c->stream));
+        c->launches += pf::kDiagLaunches;
+        CK(c, cudaEventRecord(c->ev_done[k], c->stream));
+        CK(c, cudaStreamWaitEvent(c->d2h, c->ev_done[k], 0));
+        for (int m = m0; m < m1; ++m)
+            for (int f = 0; f < 3; ++f)
+                if (dst[f])
+                    CK(c, cudaMemcpy2DAsync((char *)dst[f] + (size_t)m * hmem, hrow, dev_field(m, f), dpitch, hrow,
+                                            S.L.ny_loc, cudaMemcpyDeviceToHost, c->d2h));
+    }
+    CK(c, cudaMemcpyAsync(c->h_diag, S.diag, (size_t)M * pf::kDiag * sizeof(double), cudaMemcpyDeviceToHost, c->d2h));
+    CK(c, cudaStreamSynchronize(c->d2h));
+    CK(c, cudaStreamSynchronize(c->stream));
+    const int64_t from = c->steps;
+    c->steps += n;
+    c->t += (double)n * c->p.dt;
+    c->blown = false;
+    double nf[3] = {0, 0, 0};
+    int worst = -1;
+    for (int m = 0; m < M; ++m) {
+        for (int f = 0; f < 3; ++f) nf[f] += c->h_diag[(size_t)m * pf::kDiag + 5 + f];
+        if (worst < 0 && c->h_diag[(size_t)m * pf::kDiag + 4] > 0) worst = m;
+    }
+    if (nf[0] + nf[1] + nf[2] > 0) {
+        c->blown = true;
+        std::string fields;
+        const char *names[3] = {"c", "phi", "rho"};
+        for (int f = 0; f < 3; ++f)
+            if (nf[f] > 0) fields += fmt("%s%s (%.0f cells)", fields.empty() ? "" : ", ", names[f], nf[f]);
+        return set_err(c, PF_ERR_BLOWUP, fmt("blow-up: non-finite %s in steps (%lld, %lld], first member %d",
+                                             fields.c_str(), (long long)from, (long long)c->steps,
+                                             worst + c->p.member_offset));
+    }
     return PF_OK;
 }
 

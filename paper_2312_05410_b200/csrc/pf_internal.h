@@ -24,6 +24,7 @@ struct Layout {
     int64_t fstride;             // elements per field  = (ny_loc + 4) * pitch
     int64_t mstride;             // elements per member = 3 * fstride
     int r0, r1;                  // row window [r0, r1) a stage launch updates (default [0, ny_loc))
+    int m0;                      // first member of a stage launch (members = its count; default 0)
     __host__ __device__ int64_t at(int r, int x) const { return (int64_t)(r + 2) * pitch + (x + gx); }
 };
 

@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(NT) stage_kernel(Layout L, KC<real> k, const r
     __shared__ double etab[64];
     load_exp_table(etab);
 
-    const int m = blockIdx.z;
+    const int m = L.m0 + blockIdx.z;
     const int tx0 = blockIdx.x * BX;
     const int ty0 = L.r0 + blockIdx.y * BY;
     const int nx = L.nx;
@@ -384,6 +384,7 @@ __device__ __forceinline__ bool next_seg(const Layout &L, int Wo, const Sched &s
         sg.m = (int)(col / strips);
         sidx = (int)(col - (int64_t)sg.m * strips);
     }
+    sg.m += L.m0;                       // buffer index of the member
     sg.x0 = sidx * Wo;
     sg.Wp = min(Wo, L.nx - sg.x0);
     return true;

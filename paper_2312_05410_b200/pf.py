@@ -89,6 +89,7 @@ def lib():
             "pf_create_slab": (C.c_int, [P, i32, i32, C.c_char_p, C.POINTER(_ctx_p)]),
             "pf_create_loopback": (C.c_int, [P, i32, C.POINTER(_ctx_p)]),
             "pf_halo_plan": (C.c_int, [i32, i32, i32, C.POINTER(i32)]),
+            "pf_run_host": (C.c_int, [_ctx_p, i64, _D, _D, _D, _D, _D, _D, i32]),
             "pf_step": (C.c_int, [_ctx_p, i64]),
             "pf_get_fields": (C.c_int, [_ctx_p, i32, _D, _D, _D]),
             "pf_set_fields": (C.c_int, [_ctx_p, i32, _D, _D, _D]),
@@ -208,6 +209,11 @@ def pf_get_fields(ctx, member, c, phi, rho):
 
 def pf_set_fields(ctx, member, c, phi, rho):
     _check(lib().pf_set_fields(ctx, member, _hptr(c), _hptr(phi), _hptr(rho)), ctx)
+
+
+def pf_run_host(ctx, n, c_in, phi_in, rho_in, c_out, phi_out, rho_out, chunks: int = 4):
+    _check(lib().pf_run_host(ctx, int(n), _hptr(c_in), _hptr(phi_in), _hptr(rho_in), _hptr(c_out), _hptr(phi_out),
+                             _hptr(rho_out), int(chunks)), ctx)
 
 
 def pf_diagnostics(ctx, member: int) -> np.ndarray:

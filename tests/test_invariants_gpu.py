@@ -159,3 +159,42 @@ def test_get_set_roundtrip_all_members():
         s.set_fields(-1, c[::-1].copy(), phi[::-1].copy(), rho[::-1].copy())
         c2, _, _ = s.fields(-1)
         assert np.array_equal(c2, c[::-1])
+
+
+@pytest.mark.parametrize("chunks", [1, 2, 3, 6])
+def test_run_host_pipeline_equals_set_step_get(chunks):
+    """pf_run_host (uploads / steps / downloads pipelined over member chunks on three streams) is
+    bitwise the same as pf_set_fields + pf_step + pf_get_fields, and keeps the step count."""
+    p = _base(128, 48, n_members=6, rate_lo=0.5, rate_hi=2.0)
+    with pf.Simulation(p) as s:
+        c0, p0, r0 = s.fields(-1)
+    cin = c0[::-1].copy(); pin = p0[::-1].copy(); rin = r0[::-1].copy()
+    with pf.Simulation(p) as s:
+        s.set_fields(-1, cin, pin, rin)
+        s.step(17)
+        want = s.fields(-1)
+    with pf.Simulation(p) as s:
+        out = [np.empty_like(cin) for _ in range(3)]
+        pf.pf_run_host(s.ctx, 17, cin, pin, rin, *out, chunks=chunks)
+        assert s.info()[0] == 17
+        for a, b in zip(out, want):
+            assert np.array_equal(a, b)
+        # device state is the result: continuing gives the straight-run result
+        pf.pf_run_host(s.ctx, 5, None, None, None, *out, chunks=chunks)
+        s2 = pf.Simulation(p)
+        s2.set_fields(-1, cin, pin, rin)
+        s2.step(22)
+        for a, b in zip(out, s2.fields(-1)):
+            assert np.array_equal(a, b)
+        s2.close()
+
+
+def test_run_host_blowup():
+    p = _base(64, 32, n_members=4)
+    with pf.Simulation(p) as s:
+        c, phi, rho = s.fields(-1)
+        phi[2, 10, 7] = np.nan
+        out = [np.empty_like(c) for _ in range(3)]
+        with pytest.raises(pf.PfError) as e:
+            pf.pf_run_host(s.ctx, 4, c, phi, rho, *out, chunks=2)
+        assert e.value.status == pf.PF_ERR_BLOWUP and "first member 2" in str(e.value)
