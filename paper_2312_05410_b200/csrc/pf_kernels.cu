@@ -790,6 +790,10 @@ constexpr RingVariant kStream1{4, 4, 2}, kStream2{2, 6, 2};
 // Pair kernel: about 128 registers per thread, so MINB = 16 / (NCW + 1) blocks of NCW + 1 warps
 // fill the register file with 12-16 compute warps per SM; rings of 2-row boxes as deep as the
 // shared memory left to each of the MINB blocks allows (at most 8 boxes).
+#ifndef PF_F32_SLOTS
+#define PF_F32_SLOTS 20
+#endif
+constexpr int kF32Slots = PF_F32_SLOTS;
 template <typename real, int NCW, bool BASE>
 struct PairCfg {
     static constexpr int R = 2;
@@ -797,7 +801,8 @@ struct PairCfg {
     static constexpr int slot = (3 * R * bx_max * (int)sizeof(real) + 127) / 128 * 128 * (BASE ? 2 : 1);
     static constexpr int ring(int b) { return ((227 * 1024) / b - 2048) / slot; }
     static constexpr int pick(int b) { return b <= 1 || ring(b) >= 3 ? b : pick(b - 1); }
-    static constexpr int minb = pick(16 / (NCW + 1) > 8 ? 8 : 16 / (NCW + 1));
+    static constexpr int wslots = sizeof(real) == 8 ? 16 : kF32Slots;   // warp slots per SM budget
+    static constexpr int minb = pick(wslots / (NCW + 1) > 8 ? 8 : wslots / (NCW + 1));
     static constexpr int S = ring(minb) > 8 ? 8 : ring(minb);
     static_assert(S >= 3, "ring too shallow");
 };
