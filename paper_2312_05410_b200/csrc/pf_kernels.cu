@@ -799,7 +799,11 @@ struct PairCfg {
     static constexpr int R = 2;
     static constexpr int bx_max = kPairCols * NCW + 2 * kPairHalo;
     static constexpr int slot = (3 * R * bx_max * (int)sizeof(real) + 127) / 128 * 128 * (BASE ? 2 : 1);
-    static constexpr int ring(int b) { return ((227 * 1024) / b - 2048) / slot; }
+    // fp64 stage 1 keeps its ring small (>= 3 boxes) to leave L1 to the output stores: measured
+    // 4-5% faster than filling the shared memory (profiles/r1_kbench.log)
+    static constexpr int smem_kb = (sizeof(real) == 8 && !BASE) ? 150 : 227;
+    static constexpr int ring_raw(int b) { return ((smem_kb * 1024) / b - 2048) / slot; }
+    static constexpr int ring(int b) { return (!BASE && sizeof(real) == 8 && ring_raw(b) < 3) ? 3 : ring_raw(b); }
     static constexpr int pick(int b) { return b <= 1 || ring(b) >= 3 ? b : pick(b - 1); }
     static constexpr int wslots = sizeof(real) == 8 ? 16 : kF32Slots;   // warp slots per SM budget
     static constexpr int minb = pick(wslots / (NCW + 1) > 8 ? 8 : wslots / (NCW + 1));
