@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define PF_ABI_VERSION 2u
+#define PF_ABI_VERSION 3u
 
 typedef struct pf_ctx pf_ctx; /* opaque */
 
@@ -73,6 +73,8 @@ typedef struct {
     double D_rho, rho_in;            /* vapour diffusivity and top reservoir density (R-9, R-12) */
     double v0, theta_deg;            /* deposition speed and angle: v = v0_m (cos, -sin) (R-10) */
     double rate_lo, rate_hi;         /* v0_m = v0 (lo + (hi-lo) U(seed, 8m+3, 0)) (R-15)     */
+    double theta_span;               /* theta_m = theta_deg + theta_span U(seed, 8m+4, 0) degrees
+                                        (0: every member at theta_deg; R-21, P:352 sweeps 50..90) */
     int32_t ic;                      /* pf_ic                                                */
     int32_t ic_ncols;                /* PF_IC_COLUMNS: number of columns                    */
     double ic_height, ic_amp, ic_wavelength;
@@ -166,6 +168,17 @@ pf_status pf_step(pf_ctx *ctx, int64_t n);
  * Errors: as pf_set_fields, pf_step, pf_get_fields. */
 pf_status pf_run_host(pf_ctx *ctx, int64_t n, const double *c_in, const double *phi_in, const double *rho_in,
                       double *c_out, double *phi_out, double *rho_out, int32_t chunks);
+
+/* Trajectory / dataset driver ("50 time snapshots equally spaced
+ * taken over the entire course of the simulation", dataset shape members x (50, 256, 256)):
+ * n_snapshots snapshots of the composite composition field, snapshot 0 = the current state and
+ * snapshot s after s * steps_between further steps (pf_step, with its blow-up checks).  The
+ * composite field is c where phi > 1/2 and 0 in the vapour.  out (caller-owned,
+ * fp64): [member][snapshot][ny_local][nx]; times (optional, NULL to skip): t of each snapshot.
+ * Each snapshot is copied to the host on a separate stream while the next steps run (pinned
+ * host memory makes the copies asynchronous).  Synchronous.
+ * Errors: PF_ERR_ARG, PF_ERR_NOMEM, PF_ERR_STATE, and pf_step's errors. */
+pf_status pf_trajectory(pf_ctx *ctx, int32_t n_snapshots, int64_t steps_between, double *out, double *times);
 
 /* Copy member `member` (0..n_members-1, or -1 = all members, stacked) to host buffers of
  * ny_local*nx doubles each (times n_members for -1).  fp32 fields are widened to double.

@@ -49,7 +49,7 @@ class _IC(C.Structure):
                 ("noise_phi", C.c_double), ("noise_c_gaussian", C.c_int32),
                 ("kappa_phi", C.c_double), ("W_phi", C.c_double), ("rho_in", C.c_double),
                 ("v0", C.c_double), ("theta_deg", C.c_double), ("rate_lo", C.c_double),
-                ("rate_hi", C.c_double), ("seed", C.c_uint64)]
+                ("rate_hi", C.c_double), ("theta_span", C.c_double), ("seed", C.c_uint64)]
 
 
 IC_KINDS = {"film": 0, "rough": 1, "columns": 2}
@@ -105,6 +105,7 @@ class IC:
     theta_deg: float = 90.0
     rate_lo: float = 1.0
     rate_hi: float = 1.0
+    theta_span: float = 0.0
     seed: int = 1
 
     def _c(self) -> _IC:
@@ -299,6 +300,13 @@ def initial_fields_rows(ic: IC, nx: int, member: int, y0: int, rows: int):
     if rc != 0:
         raise ValueError("bad IC recipe")
     return c, phi, rho
+
+
+def composite(c, phi):
+    """Composite composition field of a dataset snapshot ("50 time snapshots"; SPEC S:442:
+    the stored field carries c in the solid and exactly 0 in the vapour): c where phi > 1/2."""
+    c, phi = np.asarray(c, dtype=np.float64), np.asarray(phi, dtype=np.float64)
+    return np.where(phi > 0.5, c, 0.0)
 
 
 def member_model(cfg_or_preset, member: int) -> Model:

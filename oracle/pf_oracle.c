@@ -401,18 +401,24 @@ typedef struct {
     int32_t noise_c_gaussian;
     double kappa_phi, W_phi, rho_in;
     double v0, theta_deg, rate_lo, rate_hi;
+    double theta_span;       /* per-member angle sweep width in degrees (R-21) */
     uint64_t seed;
 } orc_ic;
 
-/* Velocity of global member m (R-10, R-15):
+/* Velocity of global member m (R-10, R-15, R-21):
  *   v0_m = v0 (rate_lo + (rate_hi - rate_lo) U(seed, 8m+3, 0));
- *   v = v0_m (cos theta, -sin theta).                                       */
+ *   theta_m = theta_deg + theta_span U(seed, 8m+4, 0)   (theta_span = 0: theta_deg; the paper
+ *             sweeps the deposition angle over 50..90 degrees);
+ *   v = v0_m (cos theta_m, -sin theta_m).                                   */
 void orc_member_velocity(const orc_ic *ic, int64_t member, double *v_x, double *v_y)
 {
     double u = orc_uniform(ic->seed, (uint64_t)member * 8u + 3u, 0);
     double mult = ic->rate_lo + (ic->rate_hi - ic->rate_lo) * u;
     double v0m = ic->v0 * mult;
-    double th = ic->theta_deg * (M_PI / 180.0);
+    double th_deg = ic->theta_deg;
+    if (ic->theta_span != 0.0)
+        th_deg = ic->theta_deg + ic->theta_span * orc_uniform(ic->seed, (uint64_t)member * 8u + 4u, 0);
+    double th = th_deg * (M_PI / 180.0);
     *v_x = v0m * cos(th);
     *v_y = -(v0m * sin(th));
 }

@@ -63,14 +63,16 @@ private:
     uint64_t key_;
 };
 
-enum Stream : uint64_t { kStreamC = 0, kStreamPhi = 1, kStreamCuts = 2, kStreamRate = 3 };
+enum Stream : uint64_t { kStreamC = 0, kStreamPhi = 1, kStreamCuts = 2, kStreamRate = 3, kStreamAngle = 4 };
 
-// Velocity of global member gm (R-10, R-15).
+// Velocity of global member gm (R-10, R-15, R-21).
 void member_velocity(const pf_params &p, int64_t gm, double &vx, double &vy) {
     const CounterRng rng(p.seed, (uint64_t)gm * 8u + kStreamRate);
     const double mult = p.rate_lo + (p.rate_hi - p.rate_lo) * rng.unif(0);
     const double v0m = p.v0 * mult;
-    const double th = p.theta_deg * (M_PI / 180.0);
+    double th_deg = p.theta_deg;   // per-member angle sweep (R-21)
+    if (p.theta_span != 0.0) th_deg = p.theta_deg + p.theta_span * CounterRng(p.seed, (uint64_t)gm * 8u + kStreamAngle).unif(0);
+    const double th = th_deg * (M_PI / 180.0);
     vx = v0m * std::cos(th);
     vy = -(v0m * std::sin(th));
 }
@@ -213,6 +215,10 @@ struct pf_ctx {
     // pf_run_host pipeline: copy streams and per-chunk events
     cudaStream_t h2d = nullptr, d2h = nullptr;
     std::vector<cudaEvent_t> ev_in, ev_done;
+    // pf_trajectory: two device snapshot buffers, copy-done events
+    double *snap[2] = {nullptr, nullptr};
+    size_t snap_n = 0;
+    cudaEvent_t ev_snap[2] = {nullptr, nullptr}, ev_copied[2] = {nullptr, nullptr};
     // CUDA graph of graph_steps steps
     cudaGraphExec_t gexec = nullptr;
     int gsteps = 0;
@@ -303,6 +309,11 @@ void destroy(pf_ctx *c) {
     for (auto e : c->ev_in) cudaEventDestroy(e);
     for (auto e : c->ev_done) cudaEventDestroy(e);
     if (c->h2d) cudaStreamDestroy(c->h2d);
+    for (int b = 0; b < 2; ++b) {
+        cudaFree(c->snap[b]);
+        if (c->ev_snap[b]) cudaEventDestroy(c->ev_snap[b]);
+        if (c->ev_copied[b]) cudaEventDestroy(c->ev_copied[b]);
+    }
     if (c->d2h) cudaStreamDestroy(c->d2h);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
@@ -984,6 +995,63 @@ pf_status pf_run_host(pf_ctx *c, int64_t n, const double *ci, const double *pi, 
                                              fields.c_str(), (long long)from, (long long)c->steps,
                                              worst + c->p.member_offset));
     }
+    return PF_OK;
+}
+
+pf_status pf_trajectory(pf_ctx *c, int32_t n_snapshots, int64_t steps_between, double *out, double *times) {
+    if (!c) return set_err(nullptr, PF_ERR_ARG, "ctx is NULL");
+    if (n_snapshots < 1 || steps_between < 0 || !out) return set_err(c, PF_ERR_ARG, "bad trajectory arguments");
+    if (c->blown) return set_err(c, PF_ERR_STATE, "state blew up; call pf_set_fields first");
+    cudaSetDevice(c->p.device);
+    const int M = c->p.n_members;
+    const size_t per = (size_t)c->ny_host * c->p.nx;           // doubles per member snapshot
+    const size_t n = per * M;
+    if (c->snap_n < n) {
+        for (int b = 0; b < 2; ++b) {
+            cudaFree(c->snap[b]);
+            c->snap[b] = nullptr;
+        }
+        c->snap_n = 0;
+        for (int b = 0; b < 2; ++b)
+            if (cudaMalloc((void **)&c->snap[b], n * sizeof(double)) != cudaSuccess) {
+                cudaGetLastError();
+                return set_err(c, PF_ERR_NOMEM, "cudaMalloc of snapshot buffers failed");
+            }
+        c->snap_n = n;
+    }
+    if (!c->d2h) {
+        CK(c, cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking));
+        CK(c, cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking));
+    }
+    for (int b = 0; b < 2; ++b)
+        if (!c->ev_snap[b]) {
+            CK(c, cudaEventCreateWithFlags(&c->ev_snap[b], cudaEventDisableTiming));
+            CK(c, cudaEventCreateWithFlags(&c->ev_copied[b], cudaEventDisableTiming));
+        }
+    for (int s = 0; s < n_snapshots; ++s) {
+        if (s > 0) {
+            pf_status st = pf_step(c, steps_between);
+            if (st != PF_OK) {
+                cudaStreamSynchronize(c->d2h);
+                return st;
+            }
+        }
+        const int b = s & 1;
+        if (s >= 2) CK(c, cudaStreamWaitEvent(c->stream, c->ev_copied[b], 0));   // buffer b is free again
+        for (auto &S : c->slabs) {
+            CK(c, pf::launch_composite(c->p.precision, S.L, S.U, c->snap[b], (int64_t)per, S.L.y0 - c->y_host0,
+                                       c->stream));
+            c->launches += 1;
+        }
+        CK(c, cudaEventRecord(c->ev_snap[b], c->stream));
+        CK(c, cudaStreamWaitEvent(c->d2h, c->ev_snap[b], 0));
+        // out[m][s][row][x]: one strided copy for all members
+        CK(c, cudaMemcpy2DAsync(out + (size_t)s * per, (size_t)n_snapshots * per * sizeof(double), c->snap[b],
+                                per * sizeof(double), per * sizeof(double), (size_t)M, cudaMemcpyDeviceToHost, c->d2h));
+        CK(c, cudaEventRecord(c->ev_copied[b], c->d2h));
+        if (times) times[s] = c->t;
+    }
+    CK(c, cudaStreamSynchronize(c->d2h));
     return PF_OK;
 }
 

@@ -75,6 +75,10 @@ constexpr int kFillLaunches = 2;
 int diag_blocks(const Layout &L);
 cudaError_t launch_diag(int precision, const Layout &L, const Coef &K, const void *state,
                         double *partials, double *out, cudaStream_t s);
+// Composite snapshot field (c where phi > 1/2, else 0) of every member of a slab, fp64, into
+// dst[m * dst_mstride + (row0 + r) * nx + x].
+cudaError_t launch_composite(int precision, const Layout &L, const void *state, double *dst, int64_t dst_mstride,
+                             int row0, cudaStream_t s);
 // field <-> contiguous fp64 [members][ny_loc][nx].
 cudaError_t launch_pack_f64(int precision, const Layout &L, int field, int member0, int nmem,
                             const void *state, double *dst, cudaStream_t s);

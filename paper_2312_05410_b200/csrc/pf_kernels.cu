@@ -298,6 +298,22 @@ __global__ void unpack_kernel(Layout L, int field, int member0, int nmem, const 
     }
 }
 
+// Composite composition field of a snapshot (NEXT-1 of SURVEY 8(f)): the
+// dataset stores c where the cell is solid (phi > 1/2) and 0 in the vapour.  fp64 output,
+// dst[m * dst_mstride + (row0 + r) * nx + x] for local rows r of the slab.
+template <typename real>
+__global__ void composite_kernel(Layout L, const real *st, double *dst, int64_t dst_mstride, int row0) {
+    const int64_t per = (int64_t)L.ny_loc * L.nx;
+    const int64_t total = per * L.members;
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t m = q / per, rem = q - m * per;
+        const int r = (int)(rem / L.nx), x = (int)(rem - (int64_t)r * L.nx);
+        const real *b = st + m * L.mstride;
+        const double c = (double)b[L.at(r, x)], ph = (double)b[L.fstride + L.at(r, x)];
+        dst[m * dst_mstride + (int64_t)(row0 + r) * L.nx + x] = ph > 0.5 ? c : 0.0;
+    }
+}
+
 // ========================================================================================
 // Streaming kernel
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -1049,6 +1065,17 @@ cudaError_t launch_diag(int precision, const Layout &L, const Coef &K, const voi
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     diag_final<<<L.members, DT, 0, s>>>(nb, partials, K.dx2, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_composite(int precision, const Layout &L, const void *state, double *dst, int64_t dst_mstride,
+                             int row0, cudaStream_t s) {
+    const int64_t total = (int64_t)L.ny_loc * L.nx * L.members;
+    const int nb = (int)((total + 255) / 256 > 8192 ? 8192 : (total + 255) / 256);
+    if (precision == 0)
+        composite_kernel<double><<<nb, 256, 0, s>>>(L, (const double *)state, dst, dst_mstride, row0);
+    else
+        composite_kernel<float><<<nb, 256, 0, s>>>(L, (const float *)state, dst, dst_mstride, row0);
     return cudaGetLastError();
 }
 

@@ -16,7 +16,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libpf.so")
 HEADER = os.path.join(os.path.dirname(_HERE), "include", "pf.h")
 
-PF_ABI_VERSION = 2
+PF_ABI_VERSION = 3
 PF_OK, PF_ERR_ARG, PF_ERR_UNSTABLE_DT, PF_ERR_NOMEM, PF_ERR_CUDA, PF_ERR_NCCL, PF_ERR_BLOWUP, \
     PF_ERR_STATE, PF_ERR_ABI = range(9)
 STATUS_NAMES = ["PF_OK", "PF_ERR_ARG", "PF_ERR_UNSTABLE_DT", "PF_ERR_NOMEM", "PF_ERR_CUDA",
@@ -34,7 +34,7 @@ class pf_params(C.Structure):
         ("M_A_bulk", C.c_double), ("M_B_bulk", C.c_double), ("M_A_surf", C.c_double),
         ("M_B_surf", C.c_double), ("sigma_surf", C.c_double), ("M_phi", C.c_double),
         ("D_rho", C.c_double), ("rho_in", C.c_double), ("v0", C.c_double), ("theta_deg", C.c_double),
-        ("rate_lo", C.c_double), ("rate_hi", C.c_double),
+        ("rate_lo", C.c_double), ("rate_hi", C.c_double), ("theta_span", C.c_double),
         ("ic", C.c_int32), ("ic_ncols", C.c_int32),
         ("ic_height", C.c_double), ("ic_amp", C.c_double), ("ic_wavelength", C.c_double),
         ("ic_c0", C.c_double), ("ic_c_lo", C.c_double), ("ic_c_hi", C.c_double),
@@ -90,6 +90,7 @@ def lib():
             "pf_create_loopback": (C.c_int, [P, i32, C.POINTER(_ctx_p)]),
             "pf_halo_plan": (C.c_int, [i32, i32, i32, C.POINTER(i32)]),
             "pf_run_host": (C.c_int, [_ctx_p, i64, _D, _D, _D, _D, _D, _D, i32]),
+            "pf_trajectory": (C.c_int, [_ctx_p, i32, i64, _D, _D]),
             "pf_step": (C.c_int, [_ctx_p, i64]),
             "pf_get_fields": (C.c_int, [_ctx_p, i32, _D, _D, _D]),
             "pf_set_fields": (C.c_int, [_ctx_p, i32, _D, _D, _D]),
@@ -214,6 +215,11 @@ def pf_set_fields(ctx, member, c, phi, rho):
 def pf_run_host(ctx, n, c_in, phi_in, rho_in, c_out, phi_out, rho_out, chunks: int = 4):
     _check(lib().pf_run_host(ctx, int(n), _hptr(c_in), _hptr(phi_in), _hptr(rho_in), _hptr(c_out), _hptr(phi_out),
                              _hptr(rho_out), int(chunks)), ctx)
+
+
+def pf_trajectory(ctx, n_snapshots: int, steps_between: int, out, times=None):
+    """out: [members][n_snapshots][ny_local][nx] fp64 (numpy or pinned torch); times: [n_snapshots]."""
+    _check(lib().pf_trajectory(ctx, int(n_snapshots), int(steps_between), _hptr(out), _hptr(times)), ctx)
 
 
 def pf_diagnostics(ctx, member: int) -> np.ndarray:

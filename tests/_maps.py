@@ -16,7 +16,8 @@ def ic_kw(p):
                 ncols=p.ic_ncols, c0=p.ic_c0, c_lo=p.ic_c_lo, c_hi=p.ic_c_hi, noise_c=p.noise_c,
                 noise_phi=p.noise_phi, noise_c_gaussian=bool(p.noise_c_gaussian),
                 kappa_phi=p.kappa_phi, W_phi=p.W_phi, rho_in=p.rho_in, v0=p.v0,
-                theta_deg=p.theta_deg, rate_lo=p.rate_lo, rate_hi=p.rate_hi, seed=p.seed)
+                theta_deg=p.theta_deg, rate_lo=p.rate_lo, rate_hi=p.rate_hi, theta_span=p.theta_span,
+                seed=p.seed)
 
 
 def oracle_member(ora, p, member_global):

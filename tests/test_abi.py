@@ -49,7 +49,8 @@ def _ic_view(p):
                 ncols=p.ic_ncols, c0=p.ic_c0, c_lo=p.ic_c_lo, c_hi=p.ic_c_hi, noise_c=p.noise_c,
                 noise_phi=p.noise_phi, noise_c_gaussian=bool(p.noise_c_gaussian),
                 kappa_phi=p.kappa_phi, W_phi=p.W_phi, rho_in=p.rho_in, v0=p.v0,
-                theta_deg=p.theta_deg, rate_lo=p.rate_lo, rate_hi=p.rate_hi, seed=p.seed)
+                theta_deg=p.theta_deg, rate_lo=p.rate_lo, rate_hi=p.rate_hi, theta_span=p.theta_span,
+                seed=p.seed)
 
 
 @pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
@@ -91,9 +92,10 @@ def test_initial_fields_bitwise_equal_oracle(L, ora, cfg, nx, ny, member):
 
 def test_member_velocity_bitwise(L, ora):
     p = pf.pf_default_params(3)
-    ic = _ora_ic(ora, p)
-    for m in (0, 1, 17, 63, 1000):
-        assert pf.pf_member_velocity(p, m) == ora.member_velocity(ic, m)
+    for q in (p, p.replace(theta_deg=50.0, theta_span=40.0, rate_lo=0.6, rate_hi=2.0)):
+        ic = _ora_ic(ora, q)
+        for m in (0, 1, 17, 63, 1000):
+            assert pf.pf_member_velocity(q, m) == ora.member_velocity(ic, m)
 
 
 def test_dt_limit(L, ora):

@@ -76,3 +76,36 @@ def test_member_rates(ora):
     assert len(set(sp)) == 64
     ic1 = ora.preset(1)["ic"]
     assert ora.member_velocity(ic1, 0)[1] == -0.5
+
+
+def test_member_angle_sweep_pins(ora):
+    """R-21: theta_m = theta_deg + theta_span U(seed, 8m+4, 0).  The velocity direction recovered
+    with atan2 lies in [50, 90) degrees for the paper's sweep, its mean over many members is
+    the interval's midpoint, the speed is the member's rate (R-15), and theta_span = 0 reproduces the
+    fixed-angle velocity bit for bit."""
+    import math
+    ic = ora.IC(kind="rough", v0=0.5, theta_deg=50.0, theta_span=40.0, rate_lo=0.6, rate_hi=2.0, seed=9)
+    angs = []
+    for m in range(2000):
+        vx, vy = ora.member_velocity(ic, m)
+        a = math.degrees(math.atan2(-vy, vx))
+        assert 50.0 - 1e-9 <= a < 90.0 + 1e-9
+        u = ora.uniform(9, 8 * m + 3, 0)
+        assert math.isclose(math.hypot(vx, vy), 0.5 * (0.6 + 1.4 * u), rel_tol=1e-14)
+        angs.append(a)
+    assert abs(sum(angs) / len(angs) - 70.0) < 1.0
+    fixed = ora.IC(kind="rough", v0=0.5, theta_deg=63.0, theta_span=0.0, seed=9)
+    vx, vy = ora.member_velocity(fixed, 5)
+    u = ora.uniform(9, 8 * 5 + 3, 0)
+    th = 63.0 * (math.pi / 180.0)
+    assert vx == 0.5 * (1.0 + 0.0 * u) * math.cos(th) and vy == -(0.5 * (1.0 + 0.0 * u) * math.sin(th))
+
+
+def test_composite_definition(ora):
+    """Composite snapshot field: c in the solid (phi > 1/2), exactly 0 in the vapour; phi = 1/2 is
+    vapour (strict inequality)."""
+    import numpy as np
+    c = np.array([[0.3, 0.7, 0.5], [0.2, 0.9, 0.4]])
+    phi = np.array([[1.0, 0.5000000001, 0.5], [0.0, 0.49, 2.0]])
+    want = np.array([[0.3, 0.7, 0.0], [0.0, 0.0, 0.4]])
+    assert np.array_equal(ora.composite(c, phi), want)
