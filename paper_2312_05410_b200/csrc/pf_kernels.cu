@@ -622,6 +622,10 @@ __device__ __forceinline__ void st2(real *p, real x, real y) {
 
 constexpr int kPairCols = 60;   // output columns per compute warp
 constexpr int kPairHalo = 4;    // box columns left of the strip (and right of it)
+#ifndef PF_SINGLES_SHFL
+#define PF_SINGLES_SHFL 1
+#endif
+constexpr bool kSinglesShfl = PF_SINGLES_SHFL;
 
 template <typename real, int NCW, int R, int S, bool BASE, bool HMIX, int MINB>
 __global__ void __launch_bounds__(32 * NCW + 32, MINB) pair_kernel(
@@ -713,13 +717,29 @@ __global__ void __launch_bounds__(32 * NCW + 32, MINB) pair_kernel(
                 const auto c0 = ld2(rk), c1 = ld2(rk1), c2 = ld2(rk2);
                 const auto p0 = ld2(rk + plane), p1 = ld2(rk1 + plane), p2 = ld2(rk2 + plane);
                 const auto r1 = ld2(rk1 + 2 * plane), r2 = ld2(rk2 + 2 * plane);
+                // x-neighbours one column outside the lane's pair: the adjacent lanes' values
+                // (lane 0's left and lane 31's right column only feed halo results)
+                real cw1, ce1, pw1, pe1, pw2, pe2, rw2, re2;
+                if (kSinglesShfl) {
+                    cw1 = __shfl_up_sync(0xffffffffu, c1.y, 1);
+                    ce1 = __shfl_down_sync(0xffffffffu, c1.x, 1);
+                    pw1 = __shfl_up_sync(0xffffffffu, p1.y, 1);
+                    pe1 = __shfl_down_sync(0xffffffffu, p1.x, 1);
+                    pw2 = __shfl_up_sync(0xffffffffu, p2.y, 1);
+                    pe2 = __shfl_down_sync(0xffffffffu, p2.x, 1);
+                    rw2 = __shfl_up_sync(0xffffffffu, r2.y, 1);
+                    re2 = __shfl_down_sync(0xffffffffu, r2.x, 1);
+                } else {
+                    cw1 = rk1[-1]; ce1 = rk1[2]; pw1 = rk1[plane - 1]; pe1 = rk1[plane + 2];
+                    pw2 = rk2[plane - 1]; pe2 = rk2[plane + 2]; rw2 = rk2[2 * plane - 1]; re2 = rk2[2 * plane + 2];
+                }
                 // rotate the windows: row k-1 of the last iteration is row k-2 now
                 A2x = A1x; A2y = A1y; M2x = M1x; M2y = M1y;
                 B3x = B2x; B3y = B2y; B2x = B1x; B2y = B1y;
                 // a2: mu_c, mu_phi, M of row k-1 at both columns
-                constitutive<real, HMIX>(k, etab, c1.x, p1.x, rk1[-1], c1.y, c2.x, c0.x, rk1[plane - 1], p1.y, p2.x,
+                constitutive<real, HMIX>(k, etab, c1.x, p1.x, cw1, c1.y, c2.x, c0.x, pw1, p1.y, p2.x,
                                          p0.x, A1x, B1x, M1x);
-                constitutive<real, HMIX>(k, etab, c1.y, p1.y, c1.x, rk1[2], c2.y, c0.y, p1.x, rk1[plane + 2], p2.y,
+                constitutive<real, HMIX>(k, etab, c1.y, p1.y, c1.x, ce1, c2.y, c0.y, p1.x, pe1, p2.y,
                                          p0.y, A1y, B1y, M1y);
                 // a3-a5: update of row k-2.  x faces: (a, a+1) in lane, (a+1, next a) by shuffle,
                 // the west face of a is the previous lane's east face of its right column.
@@ -739,10 +759,10 @@ __global__ void __launch_bounds__(32 * NCW + 32, MINB) pair_kernel(
                     bcx = b0.x; bcy = b0.y; bpx = b1.x; bpy = b1.y; brx = b2.x; bry = b2.y;
                 }
                 real ocx, opx, orx, ocy, opy, ory;
-                cell_update<real>(k, vx, vy, fex, fwx, fnx, Fsx, B2x, Bp, B2y, B3x, B1x, rk2[plane - 1], p2.y, P3x,
-                                  p1.x, r2.x, rk2[2 * plane - 1], r2.y, R3x, r1.x, bcx, bpx, brx, ocx, opx, orx);
-                cell_update<real>(k, vx, vy, fey, fex, fny, Fsy, B2y, B2x, Bn, B3y, B1y, p2.x, rk2[plane + 2], P3y,
-                                  p1.y, r2.y, r2.x, rk2[2 * plane + 2], R3y, r1.y, bcy, bpy, bry, ocy, opy, ory);
+                cell_update<real>(k, vx, vy, fex, fwx, fnx, Fsx, B2x, Bp, B2y, B3x, B1x, pw2, p2.y, P3x,
+                                  p1.x, r2.x, rw2, r2.y, R3x, r1.x, bcx, bpx, brx, ocx, opx, orx);
+                cell_update<real>(k, vx, vy, fey, fex, fny, Fsy, B2y, B2x, Bn, B3y, B1y, p2.x, pe2, P3y,
+                                  p1.y, r2.y, r2.x, re2, R3y, r1.y, bcy, bpy, bry, ocy, opy, ory);
                 Fsx = fnx; Fsy = fny;
                 P3x = p2.x; P3y = p2.y; R3x = r2.x; R3y = r2.y;
                 if (store && i >= 4 && i < n) {
