@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define PF_ABI_VERSION 3u
+#define PF_ABI_VERSION 4u
 
 typedef struct pf_ctx pf_ctx; /* opaque */
 
@@ -75,6 +75,9 @@ typedef struct {
     double rate_lo, rate_hi;         /* v0_m = v0 (lo + (hi-lo) U(seed, 8m+3, 0)) (R-15)     */
     double theta_span;               /* theta_m = theta_deg + theta_span U(seed, 8m+4, 0) degrees
                                         (0: every member at theta_deg; R-21, P:352 sweeps 50..90) */
+    double mob_lo, mob_hi;           /* species mobility sweep (R-23, "species mobilities"):
+                                        member m scales M_A (bulk, surf) by a = lo + (hi-lo) U(seed,
+                                        8m+5, 0) and M_B by b (stream 8m+6); 1, 1 = no sweep     */
     int32_t ic;                      /* pf_ic                                                */
     int32_t ic_ncols;                /* PF_IC_COLUMNS: number of columns                    */
     double ic_height, ic_amp, ic_wavelength;
@@ -110,6 +113,9 @@ pf_status pf_initial_fields(const pf_params *p, int64_t member, int32_t y0, int3
 /* Host-only: velocity (v_x, v_y) = v0_m (cos theta, -sin theta) of GLOBAL member `member`
  * (R-10, R-15) and the stability limit of R-18 for p.  Need no GPU.  Errors: PF_ERR_ARG. */
 pf_status pf_member_velocity(const pf_params *p, int64_t member, double *v_x, double *v_y);
+/* Host-only: composition mobilities of GLOBAL member `member` (R-6, R-23):
+ * out = {M_A^bulk, M_B^bulk, M_A^surf, M_B^surf}.  Errors: PF_ERR_ARG. */
+pf_status pf_member_mobility(const pf_params *p, int64_t member, double out[4]);
 pf_status pf_dt_limit(const pf_params *p, double *dt_max);
 
 /* Create a single-GPU context holding p->n_members independent members of the full

@@ -49,7 +49,8 @@ class _IC(C.Structure):
                 ("noise_phi", C.c_double), ("noise_c_gaussian", C.c_int32),
                 ("kappa_phi", C.c_double), ("W_phi", C.c_double), ("rho_in", C.c_double),
                 ("v0", C.c_double), ("theta_deg", C.c_double), ("rate_lo", C.c_double),
-                ("rate_hi", C.c_double), ("theta_span", C.c_double), ("seed", C.c_uint64)]
+                ("rate_hi", C.c_double), ("theta_span", C.c_double), ("mob_lo", C.c_double),
+                ("mob_hi", C.c_double), ("seed", C.c_uint64)]
 
 
 IC_KINDS = {"film": 0, "rough": 1, "columns": 2}
@@ -106,6 +107,8 @@ class IC:
     rate_lo: float = 1.0
     rate_hi: float = 1.0
     theta_span: float = 0.0
+    mob_lo: float = 1.0
+    mob_hi: float = 1.0
     seed: int = 1
 
     def _c(self) -> _IC:
@@ -175,6 +178,7 @@ def lib():
             "orc_sm64": (u64, [u64]), "orc_draw": (u64, [u64, u64, u64]),
             "orc_uniform": (dbl, [u64, u64, u64]), "orc_gauss": (dbl, [u64, u64, u64]),
             "orc_member_velocity": (None, [pI, i64, C.POINTER(dbl), C.POINTER(dbl)]),
+            "orc_member_mobility": (None, [pI, i64, C.POINTER(dbl), C.POINTER(dbl)]),
             "orc_initial_fields": (C.c_int, [pI, C.c_int, C.c_int, i64, _D, _D, _D]),
             "orc_initial_fields_rows": (C.c_int, [pI, C.c_int, i64, C.c_int, C.c_int, _D, _D, _D]),
             "orc_dt_max": (dbl, [pM, dbl]),
@@ -300,6 +304,23 @@ def initial_fields_rows(ic: IC, nx: int, member: int, y0: int, rows: int):
     if rc != 0:
         raise ValueError("bad IC recipe")
     return c, phi, rho
+
+
+def member_mobility(ic: IC, member: int):
+    """(a, b): multipliers of the species-A and species-B mobilities of global member (R-23)."""
+    a, b = C.c_double(), C.c_double()
+    lib().orc_member_mobility(C.byref(ic._c()), int(member), C.byref(a), C.byref(b))
+    return a.value, b.value
+
+
+def member_model_sweep(m: Model, ic: IC, member: int) -> Model:
+    """Copy of Model m with member's velocity (R-10, R-15, R-21) and mobilities (R-23)."""
+    q = Model(**asdict(m))
+    q.v_x, q.v_y = member_velocity(ic, member)
+    a, b = member_mobility(ic, member)
+    q.MA_bulk, q.MA_surf = m.MA_bulk * a, m.MA_surf * a
+    q.MB_bulk, q.MB_surf = m.MB_bulk * b, m.MB_surf * b
+    return q
 
 
 def composite(c, phi):

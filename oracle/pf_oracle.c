@@ -402,6 +402,7 @@ typedef struct {
     double kappa_phi, W_phi, rho_in;
     double v0, theta_deg, rate_lo, rate_hi;
     double theta_span;       /* per-member angle sweep width in degrees (R-21) */
+    double mob_lo, mob_hi;   /* per-member species-mobility multipliers (R-23) */
     uint64_t seed;
 } orc_ic;
 
@@ -421,6 +422,15 @@ void orc_member_velocity(const orc_ic *ic, int64_t member, double *v_x, double *
     double th = th_deg * (M_PI / 180.0);
     *v_x = v0m * cos(th);
     *v_y = -(v0m * sin(th));
+}
+
+/* Species-mobility multipliers of global member m (R-23; P:352 varies "species mobilites (M_A,
+ * M_B)" between trajectories): a scales both mobilities of species A, b both of species B,
+ *   a = mob_lo + (mob_hi - mob_lo) U(seed, 8m+5, 0),  b = mob_lo + (mob_hi - mob_lo) U(seed, 8m+6, 0). */
+void orc_member_mobility(const orc_ic *ic, int64_t member, double *a, double *b)
+{
+    *a = ic->mob_lo + (ic->mob_hi - ic->mob_lo) * orc_uniform(ic->seed, (uint64_t)member * 8u + 5u, 0);
+    *b = ic->mob_lo + (ic->mob_hi - ic->mob_lo) * orc_uniform(ic->seed, (uint64_t)member * 8u + 6u, 0);
 }
 
 static int cmp_i64(const void *a, const void *b)

@@ -6,14 +6,30 @@
 #pragma once
 #include <cstdint>
 
+#include "pf_internal.h"
+
 namespace pf {
 
 template <typename real>
 struct KC {                    // coefficients folded into the compute precision
     real half_inv_dx2, inv_2dx, m_kc_dx2, m_kp_dx2, W_c, W2c, W2p;   // m_ = negated
-    real MBb, dMb, MBs, dMs, two_inv_sigma, Mp_dx2, Dr_dx2, rho_in, coef;
-    int hmix;                  // 0: M_A = M_B for bulk and surface (h(c) drops out exactly)
+    real two_inv_sigma, Mp_dx2, Dr_dx2, rho_in, coef;
+    real MBb, dMb, MBs, dMs;   // mobilities shared by all members (MOB 0, 1)
+    int mob;                   // 0: shared, M_A = M_B (h(c) drops out); 1: shared, M_A != M_B;
+                               // 2: per member (record array, R-23)
 };
+
+// Per-member record (device array, storage precision, kMembStride values per member, pf_internal.h):
+// velocity (R-10, R-15, R-21) and composition mobilities (R-6, R-23).
+template <typename real>
+struct Mob {
+    real MBb, dMb, MBs, dMs;
+};
+template <typename real>
+__device__ __forceinline__ Mob<real> load_mob(const real *memb, int m) {
+    const real *q = memb + (int64_t)m * kMembStride + 2;
+    return Mob<real>{q[0], q[1], q[2], q[3]};
+}
 
 __device__ __forceinline__ double add_(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double sub_(double a, double b) { return __dsub_rn(a, b); }
@@ -69,10 +85,10 @@ __device__ __forceinline__ real clamp01(real c) {
 // The neighbour sums are ((l + r) + (d + u)): symmetric in (d, u), so a mirrored ghost row
 // (u[-1] = u[0], u[-2] = u[1]) yields bit-identical mu / M to the cell it mirrors, and the
 // boundary-face fluxes vanish exactly.
-template <typename real, bool HMIX>
-__device__ __forceinline__ void constitutive(const KC<real> &k, const double *etab, real c, real p, real cl,
-                                             real cr, real cd, real cu, real pl, real pr, real pd, real pu,
-                                             real &mu_c, real &mu_p, real &M) {
+template <typename real, int MOB>
+__device__ __forceinline__ void constitutive(const KC<real> &k, const Mob<real> &mo, const double *etab, real c,
+                                             real p, real cl, real cr, real cd, real cu, real pl, real pr, real pd,
+                                             real pu, real &mu_c, real &mu_p, real &M) {
     const real one = real(1), m2 = real(-2), m4 = real(-4);
     const real lc = fma_(c, m4, add_(add_(cl, cr), add_(cd, cu)));   // dx^2 L(c)
     const real lp = fma_(p, m4, add_(add_(pl, pr), add_(pd, pu)));   // dx^2 L(phi)
@@ -89,11 +105,13 @@ __device__ __forceinline__ void constitutive(const KC<real> &k, const double *et
     const real q = mul_(sub_(p, real(0.5)), k.two_inv_sigma);          // phit / sigma_surf
     const real e = exp_neg(mul_(-q, q), etab);
     real mb, ms;
-    if (HMIX) {
+    if (MOB != 0) {
         const real ch = clamp01(c);                                   // clamp(c, 0, 1)
         const real h = mul_(mul_(ch, ch), fma_(ch, m2, real(3)));     // smoothstep h(c)
-        mb = mul_(pp, fma_(h, k.dMb, k.MBb));
-        ms = fma_(h, k.dMs, k.MBs);
+        const real MBb = MOB == 2 ? mo.MBb : k.MBb, dMb = MOB == 2 ? mo.dMb : k.dMb;
+        const real MBs = MOB == 2 ? mo.MBs : k.MBs, dMs = MOB == 2 ? mo.dMs : k.dMs;
+        mb = mul_(pp, fma_(h, dMb, MBb));
+        ms = fma_(h, dMs, MBs);
     } else {   // M_A = M_B: h (M_A - M_B) + M_B == M_B exactly
         mb = mul_(pp, k.MBb);
         ms = k.MBs;

@@ -63,7 +63,8 @@ private:
     uint64_t key_;
 };
 
-enum Stream : uint64_t { kStreamC = 0, kStreamPhi = 1, kStreamCuts = 2, kStreamRate = 3, kStreamAngle = 4 };
+enum Stream : uint64_t { kStreamC = 0, kStreamPhi = 1, kStreamCuts = 2, kStreamRate = 3, kStreamAngle = 4,
+                         kStreamMobA = 5, kStreamMobB = 6 };
 
 // Velocity of global member gm (R-10, R-15, R-21).
 void member_velocity(const pf_params &p, int64_t gm, double &vx, double &vy) {
@@ -75,6 +76,18 @@ void member_velocity(const pf_params &p, int64_t gm, double &vx, double &vy) {
     const double th = th_deg * (M_PI / 180.0);
     vx = v0m * std::cos(th);
     vy = -(v0m * std::sin(th));
+}
+
+// Composition mobilities of global member gm (R-6, R-23): species A scaled by
+// a = mob_lo + (mob_hi - mob_lo) U(seed, 8gm+5, 0), species B by b (stream 8gm+6).
+// out = {M_A^bulk, M_B^bulk, M_A^surf, M_B^surf}.
+void member_mobility(const pf_params &p, int64_t gm, double out[4]) {
+    const double a = p.mob_lo + (p.mob_hi - p.mob_lo) * CounterRng(p.seed, (uint64_t)gm * 8u + kStreamMobA).unif(0);
+    const double b = p.mob_lo + (p.mob_hi - p.mob_lo) * CounterRng(p.seed, (uint64_t)gm * 8u + kStreamMobB).unif(0);
+    out[0] = p.M_A_bulk * a;
+    out[1] = p.M_B_bulk * b;
+    out[2] = p.M_A_surf * a;
+    out[3] = p.M_B_surf * b;
 }
 
 // Column boundaries of the columnar recipe: ncols-1 distinct sorted cuts in [1, nx-1] (R-14).
@@ -142,7 +155,8 @@ void fill_initial(const pf_params &p, int64_t gm, int y0, int rows, double *c, d
 // Stability bound R-18.
 double dt_limit(const pf_params &p) {
     const double Mc = std::max(std::max(std::fabs(p.M_A_bulk), std::fabs(p.M_B_bulk)),
-                               std::max(std::fabs(p.M_A_surf), std::fabs(p.M_B_surf)));
+                               std::max(std::fabs(p.M_A_surf), std::fabs(p.M_B_surf))) *
+                      std::max(1.0, p.mob_hi);   // largest member multiplier (R-23)
     const double dx2 = p.dx * p.dx, dx4 = dx2 * dx2;
     const double a = Mc * (64.0 * p.kappa_c / dx4 + 16.0 * p.W_c / dx2);
     const double b = p.M_phi * (64.0 * p.kappa_phi / dx4 + 16.0 * p.W_phi / dx2);
@@ -165,6 +179,7 @@ pf::Coef make_coef(const pf_params &p) {
     K.dMb = p.M_A_bulk - p.M_B_bulk;
     K.MBs = p.M_B_surf;
     K.dMs = p.M_A_surf - p.M_B_surf;
+    K.mob = (p.mob_lo != 1.0 || p.mob_hi != 1.0) ? 2 : ((K.dMb != 0.0 || K.dMs != 0.0) ? 1 : 0);
     K.inv_sigma = 1.0 / p.sigma_surf;
     K.Mp_dx2 = p.M_phi / dx2;
     K.Dr_dx2 = p.D_rho / dx2;
@@ -269,6 +284,7 @@ pf_status validate(const pf_params *p, std::string &why) {
     if (p->M_A_bulk < 0 || p->M_B_bulk < 0 || p->M_A_surf < 0 || p->M_B_surf < 0) { why = "mobilities must be >= 0"; return PF_ERR_ARG; }
     if (p->check_every < 1) { why = "check_every must be >= 1"; return PF_ERR_ARG; }
     if (p->graph_steps < 0) { why = "graph_steps must be >= 0"; return PF_ERR_ARG; }
+    if (!(p->mob_lo > 0) || !(p->mob_hi >= p->mob_lo)) { why = "need 0 < mob_lo <= mob_hi"; return PF_ERR_ARG; }
     if (p->overlap_halo != 0 && p->overlap_halo != 1) { why = "overlap_halo must be 0 or 1"; return PF_ERR_ARG; }
     if (p->kernel_path < 0 || p->kernel_path > 3) { why = "kernel_path must be 0, 1, 2 or 3"; return PF_ERR_ARG; }
     if (p->kernel_path >= 2 && !(p->nx % 4 == 0 && p->nx >= 16)) { why = "streaming kernels need nx % 4 == 0 and nx >= 16"; return PF_ERR_ARG; }
@@ -628,10 +644,21 @@ pf_status create_common(const pf_params *p, int mode, int rank, int nranks, cons
         c->err = "cudaMallocHost failed";
         return fail(PF_ERR_NOMEM);
     }
-    // velocities (R-10, R-15)
+    // per-member records: velocity (R-10, R-15, R-21) and mobilities (R-6, R-23), pf_cell.cuh
     {
-        std::vector<double> v(2 * (size_t)p->n_members);
-        for (int m = 0; m < p->n_members; ++m) member_velocity(*p, (int64_t)p->member_offset + m, v[2 * m], v[2 * m + 1]);
+        constexpr int W = pf::kMembStride;
+        std::vector<double> v(W * (size_t)p->n_members);
+        for (int m = 0; m < p->n_members; ++m) {
+            const int64_t gm = (int64_t)p->member_offset + m;
+            double *q = &v[W * (size_t)m];
+            member_velocity(*p, gm, q[0], q[1]);
+            double mob[4];
+            member_mobility(*p, gm, mob);   // M_A^bulk, M_B^bulk, M_A^surf, M_B^surf
+            q[2] = mob[1];
+            q[3] = mob[0] - mob[1];
+            q[4] = mob[3];
+            q[5] = mob[2] - mob[3];
+        }
         std::vector<float> vf(v.begin(), v.end());
         if (cudaMalloc(&c->vel, v.size() * c->esz) != cudaSuccess) {
             cudaGetLastError();
@@ -746,6 +773,7 @@ pf_status pf_default_params(int32_t cfg, pf_params *o) {
     p.v0 = 0.5;
     p.theta_deg = 90.0;
     p.rate_lo = p.rate_hi = 1.0;
+    p.mob_lo = p.mob_hi = 1.0;
     p.ic_wavelength = 32.0;
     p.ic_c0 = 0.5;
     p.ic_c_lo = 0.2;
@@ -810,6 +838,12 @@ pf_status pf_initial_fields(const pf_params *p, int64_t member, int32_t y0, int3
 pf_status pf_member_velocity(const pf_params *p, int64_t member, double *vx, double *vy) {
     if (!p || !vx || !vy || member < 0) return set_err(nullptr, PF_ERR_ARG, "bad argument");
     member_velocity(*p, member, *vx, *vy);
+    return PF_OK;
+}
+
+pf_status pf_member_mobility(const pf_params *p, int64_t member, double out[4]) {
+    if (!p || !out || member < 0) return set_err(nullptr, PF_ERR_ARG, "bad argument");
+    member_mobility(*p, member, out);
     return PF_OK;
 }
 

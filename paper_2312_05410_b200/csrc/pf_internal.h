@@ -33,7 +33,8 @@ struct Coef {
     double inv_dx2, half_inv_dx2, inv_2dx;
     double kc_dx2, kp_dx2;          // kappa_c/dx^2, kappa_phi/dx^2
     double W_c, W2c, W2p;           // W_c, 2 W_c, 2 W_phi
-    double MBb, dMb, MBs, dMs;      // M_B_bulk, M_A_bulk - M_B_bulk, M_B_surf, M_A_surf - M_B_surf
+    double MBb, dMb, MBs, dMs;      // mobilities shared by all members (when mob < 2)
+    int mob;                        // 0 shared with M_A = M_B, 1 shared, 2 per member (R-23)
     double inv_sigma;               // 1/sigma_surf
     double Mp_dx2, Dr_dx2;          // M_phi/dx^2, D_rho/dx^2
     double rho_in;
@@ -52,6 +53,10 @@ struct StreamPlan {
     CUtensorMap mapU[2], mapUs[2];  // box (box_x, 2 or 4 rows, 3) over U / Us (index: rows == 4)
 };
 
+// Per-member record of the `vel` device array: v_x, v_y, M_B^bulk, M_A^bulk - M_B^bulk, M_B^surf,
+// M_A^surf - M_B^surf (storage precision; R-10, R-15, R-21, R-6, R-23).
+constexpr int kMembStride = 6;
+
 // Number of values in a per-member diagnostics record (internal).
 // [0] sum c, [1] sum phi, [2] sum rho, [3] E_h, [4] cells with any non-finite field,
 // [5] non-finite c, [6] non-finite phi, [7] non-finite rho.
@@ -62,6 +67,7 @@ constexpr int kDiag = 8;
 cudaError_t make_stream_plan(int precision, const Layout &L, void *U, void *Us, StreamPlan &plan);
 // stage: out = base + coef * R(in).  stage 1: in = U, base = U, out = Us; stage 2: in = Us,
 // base = U, out = U (each cell reads its own base value before writing it).
+// vel: the per-member record array (kMembStride values per member, pf_cell.cuh).
 cudaError_t launch_stage(int precision, const Layout &L, const StreamPlan &plan, const Coef &K, int stage,
                          const void *in, const void *base, void *out, const void *vel, double coef,
                          cudaStream_t s);

@@ -53,7 +53,7 @@ __device__ __forceinline__ int wrap_x(int gx, int nx) {
     return gx % nx;
 }
 
-template <typename real, bool HMIX>
+template <typename real, int MOB>
 __global__ void __launch_bounds__(NT) stage_kernel(Layout L, KC<real> k, const real *__restrict__ in,
                                                    const real *__restrict__ base, real *out,
                                                    const real *__restrict__ vel) {
@@ -101,11 +101,12 @@ __global__ void __launch_bounds__(NT) stage_kernel(Layout L, KC<real> k, const r
     __syncthreads();
 
     // ---- phase 1: mu_c, mu_phi, M on the tile + 1 ring ----
+    const Mob<real> mo = MOB == 2 ? load_mob(vel, m) : Mob<real>{};
     for (int t = threadIdx.x; t < (BY + 2) * (BX + 2); t += NT) {
         const int sy = t / (BX + 2), sx = t - sy * (BX + 2);
         const int ey = sy + 1, ex = sx + 1;
         real mc, mp, M;
-        constitutive<real, HMIX>(k, etab, sc[ey][ex], sp[ey][ex], sc[ey][ex - 1], sc[ey][ex + 1], sc[ey - 1][ex],
+        constitutive<real, MOB>(k, mo, etab, sc[ey][ex], sp[ey][ex], sc[ey][ex - 1], sc[ey][ex + 1], sc[ey - 1][ex],
                                  sc[ey + 1][ex], sp[ey][ex - 1], sp[ey][ex + 1], sp[ey - 1][ex], sp[ey + 1][ex], mc,
                                  mp, M);
         smc[sy][sx] = mc;
@@ -115,7 +116,7 @@ __global__ void __launch_bounds__(NT) stage_kernel(Layout L, KC<real> k, const r
     __syncthreads();
 
     // ---- phase 2: fluxes, source, vapour, update ----
-    const real vx = vel[2 * m], vy = vel[2 * m + 1];
+    const real vx = vel[kMembStride * m], vy = vel[kMembStride * m + 1];
     const int lx = threadIdx.x & (BX - 1);
     const int gx = tx0 + lx;
     for (int q = threadIdx.x / BX; q < BY; q += NT / BX) {
@@ -446,7 +447,7 @@ __device__ __forceinline__ void store_with_ghosts(const Layout &L, real *b, int 
     else if (g >= L.ny - 2 && f != 2) store_row_ghosts(L, b, 2 * L.ny_loc - 1 - r, x, v);   // top slab
 }
 
-template <typename real, int NCW, int R, int S, bool BASE, bool HMIX, int MINB>
+template <typename real, int NCW, int R, int S, bool BASE, int MOB, int MINB>
 __global__ void __launch_bounds__(32 * NCW + 32, MINB) stream_kernel(
     Layout L, KC<real> k, const __grid_constant__ CUtensorMap mapIn, const __grid_constant__ CUtensorMap mapBase,
     real *out, const real *__restrict__ vel, int Wo, int G) {
@@ -522,7 +523,8 @@ __global__ void __launch_bounds__(32 * NCW + 32, MINB) stream_kernel(
         const int x = sg.x0 + cx;           // global column of this lane
         const bool store = lane >= 1 && lane <= 30 && cx < sg.Wp;
         real *ob = out + sg.m * L.mstride;
-        const real vx = vel[2 * sg.m], vy = vel[2 * sg.m + 1];
+        const real vx = vel[kMembStride * sg.m], vy = vel[kMembStride * sg.m + 1];
+        const Mob<real> mo = MOB == 2 ? load_mob(vel, sg.m) : Mob<real>{};
 
         real c_m2 = 0, c_m1 = 0, c_0 = 0;                 // c rows k-2, k-1, k (own column)
         real p_m3 = 0, p_m2 = 0, p_m1 = 0, p_0 = 0;       // phi rows k-3 .. k
@@ -548,7 +550,7 @@ __global__ void __launch_bounds__(32 * NCW + 32, MINB) stream_kernel(
                 b_m3 = b_m2; b_m2 = b_m1;
                 M_m2 = M_m1;
                 // mu / M of row k-1 at this lane's column
-                constitutive<real, HMIX>(k, etab, c_m1, p_m1, rk1[-1], rk1[1], c_m2, c_0, rk1[plane - 1],
+                constitutive<real, MOB>(k, mo, etab, c_m1, p_m1, rk1[-1], rk1[1], c_m2, c_0, rk1[plane - 1],
                                          rk1[plane + 1], p_m2, p_0, a_m1, b_m1, M_m1);
                 // update of row k-2.  East face flux from this lane's mu / M and lane+1's; the west
                 // flux is lane-1's east flux; the south flux is last row's north flux.
@@ -627,7 +629,7 @@ constexpr int kPairHalo = 4;    // box columns left of the strip (and right of i
 #endif
 constexpr bool kSinglesShfl = PF_SINGLES_SHFL;
 
-template <typename real, int NCW, int R, int S, bool BASE, bool HMIX, int MINB>
+template <typename real, int NCW, int R, int S, bool BASE, int MOB, int MINB>
 __global__ void __launch_bounds__(32 * NCW + 32, MINB) pair_kernel(
     Layout L, KC<real> k, const __grid_constant__ CUtensorMap mapIn, const __grid_constant__ CUtensorMap mapBase,
     real *out, const real *__restrict__ vel, int Wo, int G) {
@@ -697,7 +699,8 @@ __global__ void __launch_bounds__(32 * NCW + 32, MINB) pair_kernel(
         const bool store = lane >= 1 && lane <= 30 && cx < sg.Wp;
         const bool xedge = (x < L.gx) | (x + 1 >= nx - L.gx);
         real *ob = out + sg.m * L.mstride;
-        const real vx = vel[2 * sg.m], vy = vel[2 * sg.m + 1];
+        const real vx = vel[kMembStride * sg.m], vy = vel[kMembStride * sg.m + 1];
+        const Mob<real> mo = MOB == 2 ? load_mob(vel, sg.m) : Mob<real>{};
 
         real A1x = 0, A1y = 0, A2x = 0, A2y = 0;          // mu_c rows k-1, k-2
         real M1x = 0, M1y = 0, M2x = 0, M2y = 0;          // M rows k-1, k-2
@@ -737,9 +740,9 @@ __global__ void __launch_bounds__(32 * NCW + 32, MINB) pair_kernel(
                 A2x = A1x; A2y = A1y; M2x = M1x; M2y = M1y;
                 B3x = B2x; B3y = B2y; B2x = B1x; B2y = B1y;
                 // a2: mu_c, mu_phi, M of row k-1 at both columns
-                constitutive<real, HMIX>(k, etab, c1.x, p1.x, cw1, c1.y, c2.x, c0.x, pw1, p1.y, p2.x,
+                constitutive<real, MOB>(k, mo, etab, c1.x, p1.x, cw1, c1.y, c2.x, c0.x, pw1, p1.y, p2.x,
                                          p0.x, A1x, B1x, M1x);
-                constitutive<real, HMIX>(k, etab, c1.y, p1.y, c1.x, ce1, c2.y, c0.y, p1.x, pe1, p2.y,
+                constitutive<real, MOB>(k, mo, etab, c1.y, p1.y, c1.x, ce1, c2.y, c0.y, p1.x, pe1, p2.y,
                                          p0.y, A1y, B1y, M1y);
                 // a3-a5: update of row k-2.  x faces: (a, a+1) in lane, (a+1, next a) by shuffle,
                 // the west face of a is the previous lane's east face of its right column.
@@ -803,12 +806,12 @@ KC<real> make_kc(const Coef &K, double coef) {
     k.W_c = (real)K.W_c;
     k.W2c = (real)K.W2c;
     k.W2p = (real)K.W2p;
+    k.two_inv_sigma = (real)(2.0 * K.inv_sigma);
     k.MBb = (real)K.MBb;
     k.dMb = (real)K.dMb;
     k.MBs = (real)K.MBs;
     k.dMs = (real)K.dMs;
-    k.two_inv_sigma = (real)(2.0 * K.inv_sigma);
-    k.hmix = (K.dMb != 0.0 || K.dMs != 0.0) ? 1 : 0;
+    k.mob = K.mob;
     k.Mp_dx2 = (real)K.Mp_dx2;
     k.Dr_dx2 = (real)K.Dr_dx2;
     k.rho_in = (real)K.rho_in;
@@ -849,14 +852,14 @@ struct PairCfg {
 
 enum Kind { kStreamKind = 1, kPairKind = 2 };
 
-template <int KIND, typename real, int NCW, int R, int S, bool BASE, bool HMIX, int MINB>
+template <int KIND, typename real, int NCW, int R, int S, bool BASE, int MOB, int MINB>
 cudaError_t launch_ring(const Layout &L, const StreamPlan &P, const KC<real> &k, int stage, real *out,
                         const real *vel, cudaStream_t s) {
     const size_t smem = stream_smem_bytes<real>(P.box_x, R, S, BASE);
     static int occ = -1, nsm = 0;
     static size_t smem_set = 0;
-    auto kern = KIND == kPairKind ? pair_kernel<real, NCW, R, S, BASE, HMIX, MINB>
-                                  : stream_kernel<real, NCW, R, S, BASE, HMIX, MINB>;
+    auto kern = KIND == kPairKind ? pair_kernel<real, NCW, R, S, BASE, MOB, MINB>
+                                  : stream_kernel<real, NCW, R, S, BASE, MOB, MINB>;
     if (smem > smem_set) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
@@ -895,8 +898,11 @@ cudaError_t launch_ring(const Layout &L, const StreamPlan &P, const KC<real> &k,
 template <int KIND, typename real, int NCW, bool BASE, int R, int S, int MINB>
 cudaError_t launch_ring_h(const Layout &L, const StreamPlan &P, const KC<real> &k, int stage, real *out,
                           const real *vel, cudaStream_t s) {
-    return k.hmix ? launch_ring<KIND, real, NCW, R, S, BASE, true, MINB>(L, P, k, stage, out, vel, s)
-                  : launch_ring<KIND, real, NCW, R, S, BASE, false, MINB>(L, P, k, stage, out, vel, s);
+    switch (k.mob) {
+        case 0: return launch_ring<KIND, real, NCW, R, S, BASE, 0, MINB>(L, P, k, stage, out, vel, s);
+        case 1: return launch_ring<KIND, real, NCW, R, S, BASE, 1, MINB>(L, P, k, stage, out, vel, s);
+        default: return launch_ring<KIND, real, NCW, R, S, BASE, 2, MINB>(L, P, k, stage, out, vel, s);
+    }
 }
 
 template <typename real, int NCW>
@@ -1033,20 +1039,12 @@ cudaError_t launch_stage(int precision, const Layout &L, const StreamPlan &P, co
     dim3 grid((L.nx + BX - 1) / BX, (L.r1 - L.r0 + BY - 1) / BY, L.members);
     if (precision == 0) {
         const KC<double> kd = make_kc<double>(K, coef);
-        if (kd.hmix)
-            stage_kernel<double, true><<<grid, NT, 0, s>>>(L, kd, (const double *)in, (const double *)base,
-                                                           (double *)out, (const double *)vel);
-        else
-            stage_kernel<double, false><<<grid, NT, 0, s>>>(L, kd, (const double *)in, (const double *)base,
-                                                            (double *)out, (const double *)vel);
+        auto kern = kd.mob == 0 ? stage_kernel<double, 0> : kd.mob == 1 ? stage_kernel<double, 1> : stage_kernel<double, 2>;
+        kern<<<grid, NT, 0, s>>>(L, kd, (const double *)in, (const double *)base, (double *)out, (const double *)vel);
     } else {
         const KC<float> kf = make_kc<float>(K, coef);
-        if (kf.hmix)
-            stage_kernel<float, true><<<grid, NT, 0, s>>>(L, kf, (const float *)in, (const float *)base,
-                                                          (float *)out, (const float *)vel);
-        else
-            stage_kernel<float, false><<<grid, NT, 0, s>>>(L, kf, (const float *)in, (const float *)base,
-                                                           (float *)out, (const float *)vel);
+        auto kern = kf.mob == 0 ? stage_kernel<float, 0> : kf.mob == 1 ? stage_kernel<float, 1> : stage_kernel<float, 2>;
+        kern<<<grid, NT, 0, s>>>(L, kf, (const float *)in, (const float *)base, (float *)out, (const float *)vel);
     }
     return cudaGetLastError();
 }

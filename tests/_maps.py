@@ -17,14 +17,13 @@ def ic_kw(p):
                 noise_phi=p.noise_phi, noise_c_gaussian=bool(p.noise_c_gaussian),
                 kappa_phi=p.kappa_phi, W_phi=p.W_phi, rho_in=p.rho_in, v0=p.v0,
                 theta_deg=p.theta_deg, rate_lo=p.rate_lo, rate_hi=p.rate_hi, theta_span=p.theta_span,
-                seed=p.seed)
+                mob_lo=p.mob_lo, mob_hi=p.mob_hi, seed=p.seed)
 
 
 def oracle_member(ora, p, member_global):
-    """(Model with the member's velocity, IC) for the oracle."""
+    """(Model with the member's velocity and mobilities, IC) for the oracle."""
     ic = ora.IC(**ic_kw(p))
-    m = ora.Model(**model_kw(p))
-    m.v_x, m.v_y = ora.member_velocity(ic, member_global)
+    m = ora.member_model_sweep(ora.Model(**model_kw(p)), ic, member_global)
     return m, ic
 
 

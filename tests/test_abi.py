@@ -50,7 +50,7 @@ def _ic_view(p):
                 noise_phi=p.noise_phi, noise_c_gaussian=bool(p.noise_c_gaussian),
                 kappa_phi=p.kappa_phi, W_phi=p.W_phi, rho_in=p.rho_in, v0=p.v0,
                 theta_deg=p.theta_deg, rate_lo=p.rate_lo, rate_hi=p.rate_hi, theta_span=p.theta_span,
-                seed=p.seed)
+                mob_lo=p.mob_lo, mob_hi=p.mob_hi, seed=p.seed)
 
 
 @pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
@@ -121,3 +121,16 @@ def test_create_validation_errors(L):
     assert e.value.status == pf.PF_ERR_ARG
     with pytest.raises(pf.PfError):
         pf.pf_default_params(9)
+
+
+def test_member_mobility_bitwise(L, ora):
+    p = pf.pf_default_params(3).replace(mob_lo=0.5, mob_hi=2.0, M_A_bulk=3.0, M_B_bulk=7.0, M_A_surf=5.0,
+                                        M_B_surf=11.0)
+    ic = _ora_ic(ora, p)
+    for m in (0, 5, 63, 999):
+        a, b = ora.member_mobility(ic, m)
+        assert pf.pf_member_mobility(p, m) == (3.0 * a, 7.0 * b, 5.0 * a, 11.0 * b)
+    q = pf.pf_default_params(3)
+    assert pf.pf_member_mobility(q, 12) == (q.M_A_bulk, q.M_B_bulk, q.M_A_surf, q.M_B_surf)
+    # the stability bound accounts for the largest multiplier (R-18, R-23)
+    assert pf.pf_dt_limit(p) == pytest.approx(pf.pf_dt_limit(p.replace(mob_lo=1.0, mob_hi=1.0)) / 2.0, rel=1e-12)

@@ -109,3 +109,20 @@ def test_composite_definition(ora):
     phi = np.array([[1.0, 0.5000000001, 0.5], [0.0, 0.49, 2.0]])
     want = np.array([[0.3, 0.7, 0.0], [0.0, 0.0, 0.4]])
     assert np.array_equal(ora.composite(c, phi), want)
+
+
+def test_member_mobility_sweep_pins(ora):
+    """R-23: species-mobility multipliers a (stream 8m+5) and b (stream 8m+6) are the affine maps
+    of the counter generator's uniforms onto [mob_lo, mob_hi); no sweep gives exactly 1."""
+    ic = ora.IC(kind="rough", mob_lo=0.5, mob_hi=2.0, seed=4)
+    A, B = [], []
+    for m in range(3000):
+        a, b = ora.member_mobility(ic, m)
+        assert a == 0.5 + 1.5 * ora.uniform(4, 8 * m + 5, 0)
+        assert b == 0.5 + 1.5 * ora.uniform(4, 8 * m + 6, 0)
+        assert 0.5 <= a < 2.0 and 0.5 <= b < 2.0
+        A.append(a); B.append(b)
+    import numpy as np
+    assert abs(np.mean(A) - 1.25) < 0.03 and abs(np.mean(B) - 1.25) < 0.03
+    assert abs(np.corrcoef(A, B)[0, 1]) < 0.06
+    assert ora.member_mobility(ora.IC(kind="rough", seed=4), 7) == (1.0, 1.0)

@@ -102,3 +102,23 @@ def test_uniform_state_fixed_point_bitwise():
         s.step(7)
         g = s.fields(0)
     assert np.array_equal(g[0], c) and np.array_equal(g[1], phi) and np.array_equal(g[2], rho)
+
+
+def test_dataset_sweeps_parity(ora):
+    """Per-member deposition rate, angle (R-15, R-21) and species mobilities (R-23) -- the paper's
+    dataset sweep -- on an ensemble: every member against the oracle with its own
+    parameters after 1 step (<= 1e-12) and 60 steps (<= 1e-10)."""
+    p = pf.pf_default_params(2).replace(nx=96, ny=64, ic_height=20.0, n_members=4, member_offset=10,
+                                       theta_deg=50.0, theta_span=40.0, rate_lo=0.6, rate_hi=2.0,
+                                       mob_lo=0.4, mob_hi=1.0, M_A_bulk=10.0, M_B_bulk=4.0, M_A_surf=8.0,
+                                       M_B_surf=2.0, seed=31)
+    with _sim(p) as s:
+        s.step(1)
+        g1 = [s.fields(k) for k in range(4)]
+        s.step(59)
+        g60 = [s.fields(k) for k in range(4)]
+    for k in range(4):
+        m, ic = oracle_member(ora, p, 10 + k)
+        u0 = ora.initial_fields(ic, p.nx, p.ny, 10 + k)
+        assert normwise(g1[k], ora.step(m, *u0, 1)) <= 1e-12, k
+        assert normwise(g60[k], ora.step(m, *u0, 60)) <= 1e-10, k

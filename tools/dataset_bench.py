@@ -1,5 +1,6 @@
 """NEXT-1 measurement: dataset-generation throughput of pf_trajectory on the paper's workload shape
-(256^2 mesh, per-member deposition rate v in [0.3, 1.0] and angle in [50, 90] degrees,
+(256^2 mesh, per-member deposition rate v in [0.3, 1.0], angle in [50, 90] degrees and
+species mobilities (R-23: M_A, M_B scaled by [0.5, 1]),
 50 equally spaced snapshots of the composite field), against plain stepping of the same ensemble.
 
     python tools/dataset_bench.py [--members 64] [--snapshots 50] [--every 20]
@@ -22,7 +23,7 @@ def main():
     ap.add_argument("--every", type=int, default=20)
     a = ap.parse_args()
     p = pf.pf_default_params(2).replace(n_members=a.members, v0=0.5, rate_lo=0.6, rate_hi=2.0, theta_deg=50.0,
-                                       theta_span=40.0, seed=2024)
+                                       theta_span=40.0, mob_lo=0.5, mob_hi=1.0, seed=2024)
     cells = p.n_members * p.nx * p.ny
     steps = (a.snapshots - 1) * a.every
     out = torch.empty((p.n_members, a.snapshots, p.ny, p.nx), dtype=torch.float64).pin_memory()
