@@ -231,6 +231,24 @@ pf_status pf_profile_read(pf_ctx *ctx, double out[6]);
  * time the ctx's work with CUDA events recorded on the same stream.  Errors: PF_ERR_ARG. */
 pf_status pf_stream(pf_ctx *ctx, void **stream);
 
+/* ---- NEXT-2: microstructure statistics of the paper's evaluation
+ * (section 2.3 "spatial autocorrelation S2^(A,A)(r, t)", section 4.5 "Rel. L2";
+ * SPEC S:456-526; readings R-24..R-26).  Context-free; run on the current CUDA device; inputs and
+ * outputs are host buffers of fp64.  Errors are status codes only (PF_ERR_ARG, PF_ERR_NOMEM,
+ * PF_ERR_CUDA; no message).
+ *   Indicator I = [comp >= threshold] of a composite field (vapour c = 0, R-24).
+ *   S2(r) = (1/N) sum_x I(x) I(x + r), periodic, N = nx ny cells, computed as
+ *   IFFT(|FFT(I)|^2) / N^2 with cuFFT; maps are centred: s2[b][ny/2 + dy][nx/2 + dx].
+ *   Radial profile: mean of the centred map over bins round(|r|), bins 0 .. pf_s2_nbins - 1 (R-25). */
+int32_t pf_s2_nbins(int32_t nx, int32_t ny);
+/* comp: [batch][ny][nx] composite fields; s2 (or NULL): [batch][ny][nx]; radial (or NULL):
+ * [batch][nbins] with nbins == pf_s2_nbins(nx, ny). */
+pf_status pf_s2(const double *comp, int32_t nx, int32_t ny, int32_t batch, double threshold, double *s2,
+                double *radial, int32_t nbins);
+/* out[b] = ||S2(true_b) - S2(pred_b)||_2 / ||S2(true_b)||_2 for batch pairs of fields. */
+pf_status pf_s2_rel_l2(const double *comp_true, const double *comp_pred, int32_t nx, int32_t ny, int32_t batch,
+                       double threshold, double *out);
+
 /* Last error message of ctx (ctx == NULL: the calling thread's last create error). */
 const char *pf_last_error(const pf_ctx *ctx);
 

@@ -336,3 +336,66 @@ def member_model(cfg_or_preset, member: int) -> Model:
     m = Model(**asdict(pr["model"]))
     m.v_x, m.v_y = member_velocity(pr["ic"], member)
     return m
+
+
+# --------------------------------------------------------------------------- NEXT-2 statistics
+# Microstructure statistics of the paper's evaluation (section 2.3, P:486-504 section
+# 4.5; SPEC S:456-526 and readings R-24..R-26 of DESIGN.md 12).  numpy, fp64; the FFT is a
+# library primitive used as one step of the stated definition.
+
+def indicator(comp, threshold=0.5):
+    """Phase-A indicator of a composite field (R-24): 1 where c >= threshold (the vapour carries
+    c = 0 in the composite, so it is never phase A), else 0."""
+    return (np.asarray(comp, dtype=np.float64) >= threshold).astype(np.float64)
+
+
+def s2_direct(ind):
+    """S2(r) = (1/N) sum_x I(x) I(x + r), periodic, N = number of cells, by the double sum
+    (brute force, small grids only); returned centered: out[ny//2 + dy, nx//2 + dx]."""
+    I = np.asarray(ind, dtype=np.float64)
+    ny, nx = I.shape
+    out = np.zeros((ny, nx))
+    for dy in range(-(ny // 2), ny - ny // 2):
+        for dx in range(-(nx // 2), nx - nx // 2):
+            acc = 0.0
+            for y in range(ny):
+                for x in range(nx):
+                    acc += I[y, x] * I[(y + dy) % ny, (x + dx) % nx]
+            out[ny // 2 + dy, nx // 2 + dx] = acc / (nx * ny)
+    return out
+
+
+def s2_fft(ind):
+    """Same as s2_direct through the Wiener-Khinchin identity: ifft(|fft(I)|^2) / N, centered."""
+    I = np.asarray(ind, dtype=np.float64)
+    F = np.fft.fft2(I)
+    corr = np.real(np.fft.ifft2(F * np.conj(F))) / I.size
+    return np.fft.fftshift(corr)
+
+
+def radial_bins(ny, nx):
+    """Bin of every entry of a centered map: round(|r|) (R-25, integer-radius bins)."""
+    dy = np.arange(ny)[:, None] - ny // 2
+    dx = np.arange(nx)[None, :] - nx // 2
+    return np.floor(np.sqrt(dx * dx + dy * dy) + 0.5).astype(np.int64)
+
+
+def radial_average(s2):
+    """Mean of the centered map over each integer-radius bin; bins 0 .. max."""
+    b = radial_bins(*s2.shape)
+    n = b.max() + 1
+    sums = np.bincount(b.ravel(), weights=np.asarray(s2, dtype=np.float64).ravel(), minlength=n)
+    cnt = np.bincount(b.ravel(), minlength=n)
+    return sums / cnt
+
+
+def rel_l2(true, pred):
+    """Rel. L2 = ||true - pred||_2 / ||true||_2 (P:501-504)."""
+    t, p = np.asarray(true, dtype=np.float64), np.asarray(pred, dtype=np.float64)
+    return float(np.sqrt(np.sum((t - p) ** 2)) / np.sqrt(np.sum(t ** 2)))
+
+
+def rel_mse(true, pred):
+    """Rel. MSE in the norm-ratio reading (R-26): sum (t - p)^2 / sum t^2."""
+    t, p = np.asarray(true, dtype=np.float64), np.asarray(pred, dtype=np.float64)
+    return float(np.sum((t - p) ** 2) / np.sum(t ** 2))

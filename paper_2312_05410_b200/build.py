@@ -84,7 +84,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     nccl_so = "libnccl.so.2" if os.path.exists(os.path.join(lib_nccl, "libnccl.so.2")) else "libnccl.so"
     tmp = LIB + ".tmp"
     _run([os.path.join(CUDA, "bin", "nvcc"), *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs,
-          "-L", lib_nccl, f"-l:{nccl_so}", "-Xlinker", f"-rpath,{lib_nccl}"], verbose)
+          "-L", lib_nccl, f"-l:{nccl_so}", "-Xlinker", f"-rpath,{lib_nccl}",
+          "-L", os.path.join(CUDA, "lib64"), "-lcufft", "-Xlinker", f"-rpath,{os.path.join(CUDA, 'lib64')}"], verbose)
     os.replace(tmp, LIB)
     return LIB
 

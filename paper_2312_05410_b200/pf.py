@@ -93,6 +93,9 @@ def lib():
             "pf_halo_plan": (C.c_int, [i32, i32, i32, C.POINTER(i32)]),
             "pf_run_host": (C.c_int, [_ctx_p, i64, _D, _D, _D, _D, _D, _D, i32]),
             "pf_trajectory": (C.c_int, [_ctx_p, i32, i64, _D, _D]),
+            "pf_s2_nbins": (i32, [i32, i32]),
+            "pf_s2": (C.c_int, [_D, i32, i32, i32, C.c_double, _D, _D, i32]),
+            "pf_s2_rel_l2": (C.c_int, [_D, _D, i32, i32, i32, C.c_double, _D]),
             "pf_step": (C.c_int, [_ctx_p, i64]),
             "pf_get_fields": (C.c_int, [_ctx_p, i32, _D, _D, _D]),
             "pf_set_fields": (C.c_int, [_ctx_p, i32, _D, _D, _D]),
@@ -229,6 +232,34 @@ def pf_run_host(ctx, n, c_in, phi_in, rho_in, c_out, phi_out, rho_out, chunks: i
 def pf_trajectory(ctx, n_snapshots: int, steps_between: int, out, times=None):
     """out: [members][n_snapshots][ny_local][nx] fp64 (numpy or pinned torch); times: [n_snapshots]."""
     _check(lib().pf_trajectory(ctx, int(n_snapshots), int(steps_between), _hptr(out), _hptr(times)), ctx)
+
+
+def pf_s2(comp, threshold: float = 0.5, maps: bool = True, radial: bool = True):
+    """S2 maps [batch][ny][nx] (centred) and radial profiles [batch][nbins] of composite fields
+    comp [batch][ny][nx] (or [ny][nx]), computed on the GPU (NEXT-2)."""
+    comp = np.ascontiguousarray(comp, dtype=np.float64)
+    single = comp.ndim == 2
+    if single:
+        comp = comp[None]
+    b, ny, nx = comp.shape
+    nb = lib().pf_s2_nbins(nx, ny)
+    s2 = np.empty_like(comp) if maps else None
+    rad = np.empty((b, nb)) if radial else None
+    _check(lib().pf_s2(_dptr(comp), nx, ny, b, float(threshold), _dptr(s2), _dptr(rad), nb))
+    if single:
+        s2 = None if s2 is None else s2[0]
+        rad = None if rad is None else rad[0]
+    return s2, rad
+
+
+def pf_s2_rel_l2(comp_true, comp_pred, threshold: float = 0.5) -> np.ndarray:
+    t = np.ascontiguousarray(comp_true, dtype=np.float64)
+    p_ = np.ascontiguousarray(comp_pred, dtype=np.float64)
+    if t.ndim == 2:
+        t, p_ = t[None], p_[None]
+    out = np.empty(t.shape[0])
+    _check(lib().pf_s2_rel_l2(_dptr(t), _dptr(p_), t.shape[2], t.shape[1], t.shape[0], float(threshold), _dptr(out)))
+    return out
 
 
 def pf_diagnostics(ctx, member: int) -> np.ndarray:
