@@ -340,7 +340,7 @@ def member_model(cfg_or_preset, member: int) -> Model:
 
 # --------------------------------------------------------------------------- NEXT-2 statistics
 # Microstructure statistics of the paper's evaluation (section 2.3, P:486-504 section
-# 4.5; SPEC S:456-526 and readings R-24..R-26 of DESIGN.md 12).  numpy, fp64; the FFT is a
+# 4.5; SPEC S:456-526 and readings R-24..R-26 of DESIGN.md 11).  numpy, fp64; the FFT is a
 # library primitive used as one step of the stated definition.
 
 def indicator(comp, threshold=0.5):

@@ -1,6 +1,6 @@
 // pf_stats.cu -- NEXT-2 of SURVEY 8(f): microstructure statistics of the paper's evaluation
 // (section 2.3, section 4.5; readings R-24..R-26 of
-// DESIGN.md 12), on the GPU:
+// DESIGN.md 11), on the GPU:
 //   indicator I = [composite c >= threshold]                                  (R-24)
 //   S2(r) = (1/N) sum_x I(x) I(x + r) = IFFT(|FFT(I)|^2) / N^2  (cuFFT, unnormalised inverse)
 //   centred map out[ny/2 + dy][nx/2 + dx], radial average over bins round(|r|) (R-25)
