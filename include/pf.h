@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define PF_ABI_VERSION 4u
+#define PF_ABI_VERSION 5u
 
 typedef struct pf_ctx pf_ctx; /* opaque */
 
@@ -78,6 +78,9 @@ typedef struct {
     double mob_lo, mob_hi;           /* species mobility sweep (R-23, "species mobilities"):
                                         member m scales M_A (bulk, surf) by a = lo + (hi-lo) U(seed,
                                         8m+5, 0) and M_B by b (stream 8m+6); 1, 1 = no sweep     */
+    double noise_rho;                /* stochastic inflow (R-27): > 0 replaces the top
+                                        reservoir rho_in by a per-step, per-column draw from
+                                        N(rho_in, noise_rho^2) truncated to [0, 2 rho_in]; 0 = off */
     int32_t ic;                      /* pf_ic                                                */
     int32_t ic_ncols;                /* PF_IC_COLUMNS: number of columns                    */
     double ic_height, ic_amp, ic_wavelength;
@@ -116,6 +119,10 @@ pf_status pf_member_velocity(const pf_params *p, int64_t member, double *v_x, do
 /* Host-only: composition mobilities of GLOBAL member `member` (R-6, R-23):
  * out = {M_A^bulk, M_B^bulk, M_A^surf, M_B^surf}.  Errors: PF_ERR_ARG. */
 pf_status pf_member_mobility(const pf_params *p, int64_t member, double out[4]);
+/* Host-only: the stochastic reservoir row (R-27) of GLOBAL member `member` for global step
+ * `step` (the draw both midpoint stages of that step see): out[nx]; rho_in when noise_rho == 0.
+ * Errors: PF_ERR_ARG. */
+pf_status pf_inflow_row(const pf_params *p, int64_t member, int64_t step, double *out);
 pf_status pf_dt_limit(const pf_params *p, double *dt_max);
 
 /* Create a single-GPU context holding p->n_members independent members of the full

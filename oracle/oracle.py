@@ -179,6 +179,8 @@ def lib():
             "orc_uniform": (dbl, [u64, u64, u64]), "orc_gauss": (dbl, [u64, u64, u64]),
             "orc_member_velocity": (None, [pI, i64, C.POINTER(dbl), C.POINTER(dbl)]),
             "orc_member_mobility": (None, [pI, i64, C.POINTER(dbl), C.POINTER(dbl)]),
+            "orc_inflow": (dbl, [C.c_uint64, i64, i64, C.c_int, C.c_int, dbl, dbl]),
+            "orc_run_inflow": (None, [pM, _D, _D, _D, i64, i64, C.c_uint64, i64, dbl]),
             "orc_initial_fields": (C.c_int, [pI, C.c_int, C.c_int, i64, _D, _D, _D]),
             "orc_initial_fields_rows": (C.c_int, [pI, C.c_int, i64, C.c_int, C.c_int, _D, _D, _D]),
             "orc_dt_max": (dbl, [pM, dbl]),
@@ -255,6 +257,18 @@ def step(m: Model, c, phi, rho, n: int = 1, euler: bool = False):
             lib().orc_step_euler(C.byref(mc), c, phi, rho)
     else:
         lib().orc_run(C.byref(mc), c, phi, rho, int(n))
+    return c, phi, rho
+
+
+def inflow(seed: int, member: int, step: int, nx: int, i: int, rho_in: float, sigma: float) -> float:
+    """Stochastic reservoir value of column i at global step `step` (R-27)."""
+    return lib().orc_inflow(seed, member, step, nx, i, rho_in, sigma)
+
+
+def step_inflow(m: Model, c, phi, rho, n: int, step0: int, seed: int, member: int, sigma: float):
+    """n midpoint steps with the per-step stochastic inflow row (R-27); step0 = global step index."""
+    c, phi, rho = _a(c).copy(), _a(phi).copy(), _a(rho).copy()
+    lib().orc_run_inflow(C.byref(m._c(c.shape)), c, phi, rho, int(n), int(step0), seed, int(member), float(sigma))
     return c, phi, rho
 
 

@@ -49,12 +49,19 @@ enum { ORC_MIRROR = 0, ORC_RESERVOIR = 1 };
  * x wraps modulo nx; y mirrors about the boundary face (u[-1]=u[0],
  * u[-2]=u[1], u[ny]=u[ny-1], u[ny+1]=u[ny-2]); with ORC_RESERVOIR the top ghost
  * row holds the constant `top` (rho reservoir, R-12). */
+static double nb_row(const double *u, int nx, int ny, int i, int j, int rule, double top, const double *toprow);
 static double nb(const double *u, int nx, int ny, int i, int j, int rule, double top)
+{
+    return nb_row(u, nx, ny, i, j, rule, top, NULL);
+}
+/* As nb, with the reservoir row given per column (toprow[i], stochastic inflow R-27) when
+ * toprow != NULL. */
+static double nb_row(const double *u, int nx, int ny, int i, int j, int rule, double top, const double *toprow)
 {
     i = ((i % nx) + nx) % nx;
     if (j < 0) j = -1 - j;
     if (j >= ny) {
-        if (rule == ORC_RESERVOIR) return top;
+        if (rule == ORC_RESERVOIR) return toprow ? toprow[((i % nx) + nx) % nx] : top;
         j = 2 * ny - 1 - j;
     }
     return u[(size_t)j * nx + i];
@@ -106,26 +113,38 @@ double orc_mobility_c(const orc_model *m, double c, double phi)
 /* ------------------------------------------------------------------------- */
 
 /* L(u) = (u_{i+1,j} + u_{i-1,j} + u_{i,j+1} + u_{i,j-1} - 4 u_ij) / dx^2. */
+static void laplacian_row(int nx, int ny, double dx, const double *u, int rule, double top, const double *toprow,
+                          double *out);
 void orc_laplacian(int nx, int ny, double dx, const double *u, int rule, double top, double *out)
+{
+    laplacian_row(nx, ny, dx, u, rule, top, NULL, out);
+}
+static void laplacian_row(int nx, int ny, double dx, const double *u, int rule, double top, const double *toprow,
+                          double *out)
 {
     for (int j = 0; j < ny; ++j)
         for (int i = 0; i < nx; ++i) {
-            double s = nb(u, nx, ny, i + 1, j, rule, top) + nb(u, nx, ny, i - 1, j, rule, top)
-                     + nb(u, nx, ny, i, j + 1, rule, top) + nb(u, nx, ny, i, j - 1, rule, top)
+            double s = nb_row(u, nx, ny, i + 1, j, rule, top, toprow) + nb_row(u, nx, ny, i - 1, j, rule, top, toprow)
+                     + nb_row(u, nx, ny, i, j + 1, rule, top, toprow) + nb_row(u, nx, ny, i, j - 1, rule, top, toprow)
                      - 4.0 * u[(size_t)j * nx + i];
             out[(size_t)j * nx + i] = s / (dx * dx);
         }
 }
 
 /* G(u) = ((u_{i+1,j} - u_{i-1,j}) / (2dx), (u_{i,j+1} - u_{i,j-1}) / (2dx)). */
-void orc_gradient(int nx, int ny, double dx, const double *u, int rule, double top,
-                  double *gx, double *gy)
+static void gradient_row(int nx, int ny, double dx, const double *u, int rule, double top, const double *toprow,
+                         double *gx, double *gy)
 {
     for (int j = 0; j < ny; ++j)
         for (int i = 0; i < nx; ++i) {
-            gx[(size_t)j * nx + i] = (nb(u, nx, ny, i + 1, j, rule, top) - nb(u, nx, ny, i - 1, j, rule, top)) / (2.0 * dx);
-            gy[(size_t)j * nx + i] = (nb(u, nx, ny, i, j + 1, rule, top) - nb(u, nx, ny, i, j - 1, rule, top)) / (2.0 * dx);
+            gx[(size_t)j * nx + i] = (nb_row(u, nx, ny, i + 1, j, rule, top, toprow) - nb_row(u, nx, ny, i - 1, j, rule, top, toprow)) / (2.0 * dx);
+            gy[(size_t)j * nx + i] = (nb_row(u, nx, ny, i, j + 1, rule, top, toprow) - nb_row(u, nx, ny, i, j - 1, rule, top, toprow)) / (2.0 * dx);
         }
+}
+void orc_gradient(int nx, int ny, double dx, const double *u, int rule, double top,
+                  double *gx, double *gy)
+{
+    gradient_row(nx, ny, dx, u, rule, top, NULL, gx, gy);
 }
 
 /* ------------------------------------------------------------------------- */
@@ -180,8 +199,16 @@ void orc_source(const orc_model *m, const double *phi, const double *rho, double
  *   R_phi = M_phi L(mu_phi) + S;
  *   R_rho = D_rho L(rho) - v . G(rho) - S.
  * Any output pointer may be NULL.                                             */
+static void rhs_row(const orc_model *m, const double *c, const double *phi, const double *rho, const double *toprow,
+                    double *Rc, double *Rphi, double *Rrho, double *S_out);
 void orc_rhs(const orc_model *m, const double *c, const double *phi, const double *rho,
              double *Rc, double *Rphi, double *Rrho, double *S_out)
+{
+    rhs_row(m, c, phi, rho, NULL, Rc, Rphi, Rrho, S_out);
+}
+/* The right-hand sides; toprow (or NULL: rho_in everywhere) is the rho reservoir row. */
+static void rhs_row(const orc_model *m, const double *c, const double *phi, const double *rho, const double *toprow,
+                    double *Rc, double *Rphi, double *Rrho, double *S_out)
 {
     int nx = m->nx, ny = m->ny;
     size_t n = (size_t)nx * ny;
@@ -227,8 +254,8 @@ void orc_rhs(const orc_model *m, const double *c, const double *phi, const doubl
     if (Rphi)
         for (size_t k = 0; k < n; ++k) Rphi[k] = m->M_phi * lmu[k] + S[k];
 
-    orc_laplacian(nx, ny, m->dx, rho, ORC_RESERVOIR, m->rho_in, lrho);
-    orc_gradient(nx, ny, m->dx, rho, ORC_RESERVOIR, m->rho_in, grx, gry);
+    laplacian_row(nx, ny, m->dx, rho, ORC_RESERVOIR, m->rho_in, toprow, lrho);
+    gradient_row(nx, ny, m->dx, rho, ORC_RESERVOIR, m->rho_in, toprow, grx, gry);
     if (Rrho)
         for (size_t k = 0; k < n; ++k)
             Rrho[k] = m->D_rho * lrho[k] - (m->v_x * grx[k] + m->v_y * gry[k]) - S[k];
@@ -241,7 +268,12 @@ void orc_rhs(const orc_model *m, const double *c, const double *phi, const doubl
 /* One explicit midpoint step (R-11):
  *   u*      = u^n + (dt/2) R(u^n)
  *   u^{n+1} = u^n + dt R(u*)                                                  */
+static void step_row(const orc_model *m, double *c, double *phi, double *rho, const double *toprow);
 void orc_step(const orc_model *m, double *c, double *phi, double *rho)
+{
+    step_row(m, c, phi, rho, NULL);
+}
+static void step_row(const orc_model *m, double *c, double *phi, double *rho, const double *toprow)
 {
     size_t n = (size_t)m->nx * m->ny;
     double *Rc = (double *)malloc(n * sizeof(double));
@@ -252,13 +284,13 @@ void orc_step(const orc_model *m, double *c, double *phi, double *rho)
     double *rs = (double *)malloc(n * sizeof(double));
     double hdt = 0.5 * m->dt;
 
-    orc_rhs(m, c, phi, rho, Rc, Rp, Rr, NULL);
+    rhs_row(m, c, phi, rho, toprow, Rc, Rp, Rr, NULL);
     for (size_t k = 0; k < n; ++k) {
         cs[k] = c[k] + hdt * Rc[k];
         ps[k] = phi[k] + hdt * Rp[k];
         rs[k] = rho[k] + hdt * Rr[k];
     }
-    orc_rhs(m, cs, ps, rs, Rc, Rp, Rr, NULL);
+    rhs_row(m, cs, ps, rs, toprow, Rc, Rp, Rr, NULL);
     for (size_t k = 0; k < n; ++k) {
         c[k] = c[k] + m->dt * Rc[k];
         phi[k] = phi[k] + m->dt * Rp[k];
@@ -431,6 +463,38 @@ void orc_member_mobility(const orc_ic *ic, int64_t member, double *a, double *b)
 {
     *a = ic->mob_lo + (ic->mob_hi - ic->mob_lo) * orc_uniform(ic->seed, (uint64_t)member * 8u + 5u, 0);
     *b = ic->mob_lo + (ic->mob_hi - ic->mob_lo) * orc_uniform(ic->seed, (uint64_t)member * 8u + 6u, 0);
+}
+
+/* Stochastic inflow (R-27; "top boundary rho = per-column draw from a Gaussian
+ * N(rho_in, noise_sigma) truncated to [0, 2 rho_in], re-drawn each step"; "a random draw
+ * from a truncated Gaussian distribution"): the reservoir value of column i for global step
+ * `step` of global member m.  Attempt a = 0..7 draws z_a by Box-Muller (cosine branch) from the
+ * uniforms at counters 2q, 2q+1, q = (step nx + i) 8 + a, of stream 8m+7; the first
+ * v = rho_in + sigma z_a inside [0, 2 rho_in] is taken; after 8 rejections v = rho_in. */
+double orc_inflow(uint64_t seed, int64_t member, int64_t step, int nx, int i, double rho_in, double sigma)
+{
+    const uint64_t stream = (uint64_t)member * 8u + 7u;
+    for (int a = 0; a < 8; ++a) {
+        uint64_t q = ((uint64_t)step * (uint64_t)nx + (uint64_t)i) * 8u + (uint64_t)a;
+        double u1 = orc_uniform(seed, stream, 2 * q), u2 = orc_uniform(seed, stream, 2 * q + 1);
+        double z = sqrt(-2.0 * log(1.0 - u1)) * cos(2.0 * M_PI * u2);
+        double v = rho_in + sigma * z;
+        if (v >= 0.0 && v <= 2.0 * rho_in) return v;
+    }
+    return rho_in;
+}
+
+/* n midpoint steps with the stochastic inflow row of each step (both stages of a step use the
+ * same row); step0 = global index of the first step. */
+void orc_run_inflow(const orc_model *m, double *c, double *phi, double *rho, int64_t nsteps, int64_t step0,
+                    uint64_t seed, int64_t member, double sigma)
+{
+    double *row = (double *)malloc((size_t)m->nx * sizeof(double));
+    for (int64_t s = 0; s < nsteps; ++s) {
+        for (int i = 0; i < m->nx; ++i) row[i] = orc_inflow(seed, member, step0 + s, m->nx, i, m->rho_in, sigma);
+        step_row(m, c, phi, rho, row);
+    }
+    free(row);
 }
 
 static int cmp_i64(const void *a, const void *b)

@@ -64,7 +64,7 @@ private:
 };
 
 enum Stream : uint64_t { kStreamC = 0, kStreamPhi = 1, kStreamCuts = 2, kStreamRate = 3, kStreamAngle = 4,
-                         kStreamMobA = 5, kStreamMobB = 6 };
+                         kStreamMobA = 5, kStreamMobB = 6, kStreamInflow = 7 };
 
 // Velocity of global member gm (R-10, R-15, R-21).
 void member_velocity(const pf_params &p, int64_t gm, double &vx, double &vy) {
@@ -88,6 +88,19 @@ void member_mobility(const pf_params &p, int64_t gm, double out[4]) {
     out[1] = p.M_B_bulk * b;
     out[2] = p.M_A_surf * a;
     out[3] = p.M_B_surf * b;
+}
+
+// Stochastic inflow value (R-27), this library's host implementation (the kernels have their own).
+double inflow_host(const pf_params &p, int64_t gm, int64_t step, int i) {
+    const CounterRng rng(p.seed, (uint64_t)gm * 8u + kStreamInflow);
+    for (int a = 0; a < 8; ++a) {
+        const uint64_t q = ((uint64_t)step * (uint64_t)p.nx + (uint64_t)i) * 8u + (uint64_t)a;
+        const double u1 = rng.unif(2 * q), u2 = rng.unif(2 * q + 1);
+        const double z = std::sqrt(-2.0 * std::log(1.0 - u1)) * std::cos(2.0 * M_PI * u2);
+        const double v = p.rho_in + p.noise_rho * z;
+        if (v >= 0.0 && v <= 2.0 * p.rho_in) return v;
+    }
+    return p.rho_in;
 }
 
 // Column boundaries of the columnar recipe: ncols-1 distinct sorted cuts in [1, nx-1] (R-14).
@@ -284,6 +297,7 @@ pf_status validate(const pf_params *p, std::string &why) {
     if (p->M_A_bulk < 0 || p->M_B_bulk < 0 || p->M_A_surf < 0 || p->M_B_surf < 0) { why = "mobilities must be >= 0"; return PF_ERR_ARG; }
     if (p->check_every < 1) { why = "check_every must be >= 1"; return PF_ERR_ARG; }
     if (p->graph_steps < 0) { why = "graph_steps must be >= 0"; return PF_ERR_ARG; }
+    if (!(p->noise_rho >= 0) || !std::isfinite(p->noise_rho)) { why = "noise_rho must be finite and >= 0"; return PF_ERR_ARG; }
     if (!(p->mob_lo > 0) || !(p->mob_hi >= p->mob_lo)) { why = "need 0 < mob_lo <= mob_hi"; return PF_ERR_ARG; }
     if (p->overlap_halo != 0 && p->overlap_halo != 1) { why = "overlap_halo must be 0 or 1"; return PF_ERR_ARG; }
     if (p->kernel_path < 0 || p->kernel_path > 3) { why = "kernel_path must be 0, 1, 2 or 3"; return PF_ERR_ARG; }
@@ -434,8 +448,14 @@ pf_status launch_rows(pf_ctx *c, Slab &s, int stage, int r0, int r1, bool captur
 // bands (rows [0, 2) and [ny_loc-2, ny_loc)), the halo exchange of those rows then runs on the
 // comm stream while the interior rows [2, ny_loc-2) are updated -- the interior reads no ghost
 // row, so it never waits for the exchange -- and the next stage waits for the exchange.
-pf_status one_step(pf_ctx *c, bool capture) {
+pf_status one_step(pf_ctx *c, bool capture, int64_t step) {
     const bool prof = c->prof && !capture;
+    if (c->p.noise_rho > 0.0)   // stochastic inflow of this step (R-27); never inside a graph
+        for (auto &s : c->slabs) {
+            CK(c, pf::launch_inflow(c->p.precision, s.L, c->p.rho_in, c->p.noise_rho, c->p.seed, c->p.member_offset,
+                                    step, s.U, s.Us, c->stream));
+            if (!capture) c->launches += 1;
+        }
     for (int stage = 1; stage <= 2; ++stage) {
         cudaEvent_t e0 = nullptr, e1 = nullptr;
         if (prof) {
@@ -474,7 +494,7 @@ pf_status ensure_graph(pf_ctx *c) {
     cudaGraph_t g = nullptr;
     CK(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
     pf_status st = PF_OK;
-    for (int i = 0; i < c->p.graph_steps && st == PF_OK; ++i) st = one_step(c, true);
+    for (int i = 0; i < c->p.graph_steps && st == PF_OK; ++i) st = one_step(c, true, 0);
     cudaError_t e = cudaStreamEndCapture(c->stream, &g);
     if (st != PF_OK) {
         if (g) cudaGraphDestroy(g);
@@ -847,6 +867,12 @@ pf_status pf_member_mobility(const pf_params *p, int64_t member, double out[4]) 
     return PF_OK;
 }
 
+pf_status pf_inflow_row(const pf_params *p, int64_t member, int64_t step, double *out) {
+    if (!p || !out || member < 0 || step < 0 || p->nx < 1) return set_err(nullptr, PF_ERR_ARG, "bad argument");
+    for (int i = 0; i < p->nx; ++i) out[i] = p->noise_rho > 0.0 ? inflow_host(*p, member, step, i) : p->rho_in;
+    return PF_OK;
+}
+
 pf_status pf_dt_limit(const pf_params *p, double *dt_max) {
     if (!p || !dt_max) return set_err(nullptr, PF_ERR_ARG, "NULL argument");
     *dt_max = dt_limit(*p);
@@ -896,7 +922,7 @@ pf_status pf_step(pf_ctx *c, int64_t n) {
         int64_t chunk = ce - (c->steps % ce);
         if (chunk > left) chunk = left;
         int64_t done = 0;
-        const bool use_graph = c->p.graph_steps > 0 && !c->prof && c->mode != kNccl;
+        const bool use_graph = c->p.graph_steps > 0 && !c->prof && c->mode != kNccl && !(c->p.noise_rho > 0.0);
         if (use_graph && chunk >= c->p.graph_steps) {
             pf_status st = ensure_graph(c);
             if (st != PF_OK) return st;
@@ -907,7 +933,7 @@ pf_status pf_step(pf_ctx *c, int64_t n) {
             }
         }
         for (; done < chunk; ++done) {
-            pf_status st = one_step(c, false);
+            pf_status st = one_step(c, false, c->steps + done);
             if (st != PF_OK) return st;
         }
         const int64_t from = c->steps;
@@ -986,6 +1012,11 @@ pf_status pf_run_host(pf_ctx *c, int64_t n, const double *ci, const double *pi, 
         }
         for (int64_t i = 0; i < n; ++i)
             for (int stage = 1; stage <= 2; ++stage) {
+                if (stage == 1 && c->p.noise_rho > 0.0) {
+                    CK(c, pf::launch_inflow(c->p.precision, L, c->p.rho_in, c->p.noise_rho, c->p.seed,
+                                            c->p.member_offset, c->steps + i, S.U, S.Us, c->stream));
+                    c->launches += 1;
+                }
                 const void *in = stage == 1 ? S.U : S.Us;
                 void *out = stage == 1 ? S.Us : S.U;
                 const double coef = stage == 1 ? 0.5 * c->p.dt : c->p.dt;

@@ -81,6 +81,10 @@ constexpr int kFillLaunches = 2;
 int diag_blocks(const Layout &L);
 cudaError_t launch_diag(int precision, const Layout &L, const Coef &K, const void *state,
                         double *partials, double *out, cudaStream_t s);
+// Stochastic inflow (R-27): the step's truncated-Gaussian reservoir rows of rho in U and Us for
+// members [L.m0, L.m0 + L.members) (global ids gmember0 + m); no-op unless this is the top slab.
+cudaError_t launch_inflow(int precision, const Layout &L, double rho_in, double sigma, uint64_t seed,
+                          int64_t gmember0, int64_t step, void *U, void *Us, cudaStream_t s);
 // Composite snapshot field (c where phi > 1/2, else 0) of every member of a slab, fp64, into
 // dst[m * dst_mstride + (row0 + r) * nx + x].
 cudaError_t launch_composite(int precision, const Layout &L, const void *state, double *dst, int64_t dst_mstride,

@@ -315,6 +315,47 @@ __global__ void composite_kernel(Layout L, const real *st, double *dst, int64_t 
     }
 }
 
+// Stochastic inflow (NEXT-3 of SURVEY 8(f); reading R-27): before each step the
+// top slab's rho reservoir rows (ghost rows ny_loc, ny_loc+1 of U and Us, ghost columns included)
+// get the step's truncated-Gaussian draw per column: attempt a = 0..7 takes z by Box-Muller
+// (cosine branch) from counters 2q, 2q+1, q = (step nx + i) 8 + a, of stream 8m+7 of the
+// counter generator (R-16); the first rho_in + sigma z inside [0, 2 rho_in] is used, else rho_in.
+__device__ __forceinline__ uint64_t sm64_dev(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+__device__ double inflow_value(uint64_t seed, int64_t member, int64_t step, int nx, int i, double rho_in,
+                               double sigma) {
+    const uint64_t key = sm64_dev(seed ^ (((uint64_t)member * 8u + 7u) * 0xD1B54A32D192ED03ull));
+    for (int a = 0; a < 8; ++a) {
+        const uint64_t q = ((uint64_t)step * (uint64_t)nx + (uint64_t)i) * 8u + (uint64_t)a;
+        const double u1 = (double)(sm64_dev(key + 2 * q) >> 11) * 0x1.0p-53;
+        const double u2 = (double)(sm64_dev(key + 2 * q + 1) >> 11) * 0x1.0p-53;
+        const double z = sqrt(-2.0 * log(1.0 - u1)) * cos(2.0 * 3.14159265358979323846 * u2);
+        const double v = rho_in + sigma * z;
+        if (v >= 0.0 && v <= 2.0 * rho_in) return v;
+    }
+    return rho_in;
+}
+template <typename real>
+__global__ void inflow_kernel(Layout L, double rho_in, double sigma, uint64_t seed, int64_t gmember0, int64_t step,
+                              real *U, real *Us) {
+    const int64_t total = (int64_t)L.members * L.pitch;
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
+        const int ml = (int)(q / L.pitch), xs = (int)(q - (int64_t)ml * L.pitch);
+        const int m = L.m0 + ml;
+        const int i = ((xs - L.gx) % L.nx + L.nx) % L.nx;
+        const real v = (real)inflow_value(seed, gmember0 + m, step, L.nx, i, rho_in, sigma);
+        const int64_t o = (int64_t)m * L.mstride + 2 * L.fstride + (int64_t)(L.ny_loc + 2) * L.pitch + xs;
+        U[o] = v;
+        U[o + L.pitch] = v;
+        Us[o] = v;
+        Us[o + L.pitch] = v;
+    }
+}
+
 // ========================================================================================
 // Streaming kernel
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -1094,6 +1135,18 @@ cudaError_t launch_composite(int precision, const Layout &L, const void *state, 
         composite_kernel<double><<<nb, 256, 0, s>>>(L, (const double *)state, dst, dst_mstride, row0);
     else
         composite_kernel<float><<<nb, 256, 0, s>>>(L, (const float *)state, dst, dst_mstride, row0);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_inflow(int precision, const Layout &L, double rho_in, double sigma, uint64_t seed,
+                          int64_t gmember0, int64_t step, void *U, void *Us, cudaStream_t s) {
+    if (L.y0 + L.ny_loc != L.ny) return cudaSuccess;   // only the top slab has the reservoir
+    const int64_t total = (int64_t)L.members * L.pitch;
+    const int nb = (int)((total + 255) / 256 > 4096 ? 4096 : (total + 255) / 256);
+    if (precision == 0)
+        inflow_kernel<double><<<nb, 256, 0, s>>>(L, rho_in, sigma, seed, gmember0, step, (double *)U, (double *)Us);
+    else
+        inflow_kernel<float><<<nb, 256, 0, s>>>(L, rho_in, sigma, seed, gmember0, step, (float *)U, (float *)Us);
     return cudaGetLastError();
 }
 

@@ -16,7 +16,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libpf.so")
 HEADER = os.path.join(os.path.dirname(_HERE), "include", "pf.h")
 
-PF_ABI_VERSION = 4
+PF_ABI_VERSION = 5
 PF_OK, PF_ERR_ARG, PF_ERR_UNSTABLE_DT, PF_ERR_NOMEM, PF_ERR_CUDA, PF_ERR_NCCL, PF_ERR_BLOWUP, \
     PF_ERR_STATE, PF_ERR_ABI = range(9)
 STATUS_NAMES = ["PF_OK", "PF_ERR_ARG", "PF_ERR_UNSTABLE_DT", "PF_ERR_NOMEM", "PF_ERR_CUDA",
@@ -35,7 +35,7 @@ class pf_params(C.Structure):
         ("M_B_surf", C.c_double), ("sigma_surf", C.c_double), ("M_phi", C.c_double),
         ("D_rho", C.c_double), ("rho_in", C.c_double), ("v0", C.c_double), ("theta_deg", C.c_double),
         ("rate_lo", C.c_double), ("rate_hi", C.c_double), ("theta_span", C.c_double),
-        ("mob_lo", C.c_double), ("mob_hi", C.c_double),
+        ("mob_lo", C.c_double), ("mob_hi", C.c_double), ("noise_rho", C.c_double),
         ("ic", C.c_int32), ("ic_ncols", C.c_int32),
         ("ic_height", C.c_double), ("ic_amp", C.c_double), ("ic_wavelength", C.c_double),
         ("ic_c0", C.c_double), ("ic_c_lo", C.c_double), ("ic_c_hi", C.c_double),
@@ -86,6 +86,7 @@ def lib():
             "pf_member_velocity": (C.c_int, [P, i64, _D, _D]),
             "pf_dt_limit": (C.c_int, [P, _D]),
             "pf_member_mobility": (C.c_int, [P, i64, _D]),
+            "pf_inflow_row": (C.c_int, [P, i64, i64, _D]),
             "pf_create": (C.c_int, [P, C.POINTER(_ctx_p)]),
             "pf_nccl_unique_id": (C.c_int, [C.c_char_p]),
             "pf_create_slab": (C.c_int, [P, i32, i32, C.c_char_p, C.POINTER(_ctx_p)]),
@@ -171,6 +172,12 @@ def pf_member_mobility(p: pf_params, member: int):
     out = np.zeros(4)
     _check(lib().pf_member_mobility(C.byref(p), int(member), _dptr(out)))
     return tuple(float(x) for x in out)
+
+
+def pf_inflow_row(p: pf_params, member: int, step: int) -> np.ndarray:
+    out = np.zeros(p.nx)
+    _check(lib().pf_inflow_row(C.byref(p), int(member), int(step), _dptr(out)))
+    return out
 
 
 def pf_dt_limit(p: pf_params) -> float:

@@ -134,3 +134,12 @@ def test_member_mobility_bitwise(L, ora):
     assert pf.pf_member_mobility(q, 12) == (q.M_A_bulk, q.M_B_bulk, q.M_A_surf, q.M_B_surf)
     # the stability bound accounts for the largest multiplier (R-18, R-23)
     assert pf.pf_dt_limit(p) == pytest.approx(pf.pf_dt_limit(p.replace(mob_lo=1.0, mob_hi=1.0)) / 2.0, rel=1e-12)
+
+
+def test_inflow_row_bitwise(L, ora):
+    p = pf.pf_default_params(2).replace(nx=40, noise_rho=0.2, rho_in=0.9, seed=8)
+    for m, st in ((0, 0), (3, 17), (63, 100000)):
+        row = pf.pf_inflow_row(p, m, st)
+        want = [ora.inflow(8, m, st, 40, i, 0.9, 0.2) for i in range(40)]
+        assert row.tolist() == want
+    assert np.all(pf.pf_inflow_row(p.replace(noise_rho=0.0), 1, 1) == 0.9)

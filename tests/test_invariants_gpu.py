@@ -198,3 +198,31 @@ def test_run_host_blowup():
         with pytest.raises(pf.PfError) as e:
             pf.pf_run_host(s.ctx, 4, c, phi, rho, *out, chunks=2)
         assert e.value.status == pf.PF_ERR_BLOWUP and "first member 2" in str(e.value)
+
+
+def test_stochastic_inflow_invariants():
+    """With stochastic inflow: member == single run (draws keyed by the global member id), loopback
+    slabs == single domain, pf_run_host == pf_step, and resuming at step n draws step n's row."""
+    p = _base(96, 64, n_members=3, noise_rho=0.25)
+    ens = _run(p, 15)
+    one = _run(p.replace(n_members=1, member_offset=2), 15)[0]
+    assert _eq(ens[2], one)
+    b = _run(p, 15, mode=("loopback", 4))
+    for m in range(3):
+        assert _eq(ens[m], b[m])
+    with pf.Simulation(p) as s:
+        c, phi, rho = s.fields(-1)
+        out = [np.empty_like(c) for _ in range(3)]
+        pf.pf_run_host(s.ctx, 15, c, phi, rho, *out, chunks=3)
+        for m in range(3):
+            assert _eq([out[0][m], out[1][m], out[2][m]], ens[m])
+    with pf.Simulation(p) as s:
+        s.step(6)
+        u = s.fields(-1)
+        st, t, _, _ = s.info()
+    with pf.Simulation(p.replace(ic=pf.PF_IC_NONE)) as s:
+        s.set_fields(-1, *u)
+        pf.pf_set_time(s.ctx, st, t)
+        s.step(9)
+        for m in range(3):
+            assert _eq(s.fields(m), ens[m])

@@ -126,3 +126,24 @@ def test_member_mobility_sweep_pins(ora):
     assert abs(np.mean(A) - 1.25) < 0.03 and abs(np.mean(B) - 1.25) < 0.03
     assert abs(np.corrcoef(A, B)[0, 1]) < 0.06
     assert ora.member_mobility(ora.IC(kind="rough", seed=4), 7) == (1.0, 1.0)
+
+
+def test_stochastic_inflow_pins(ora):
+    """R-27: per-step, per-column truncated Gaussian N(rho_in, sigma^2) on [0, 2 rho_in].
+    sigma = 0 gives rho_in exactly; small sigma gives mean rho_in and standard deviation sigma (the
+    truncation is inactive); large sigma keeps every value inside the bounds; draws differ between
+    steps, columns and members; a zero-noise run equals the deterministic run bit for bit."""
+    import numpy as np
+    assert ora.inflow(3, 2, 10, 64, 5, 0.8, 0.0) == 0.8
+    v = np.array([ora.inflow(3, 2, s, 64, i, 1.0, 0.05) for s in range(100) for i in range(64)])
+    assert abs(v.mean() - 1.0) < 3 * 0.05 / np.sqrt(v.size) * 2 and abs(v.std() - 0.05) < 0.003
+    w = np.array([ora.inflow(3, 2, s, 64, i, 1.0, 2.0) for s in range(50) for i in range(64)])
+    assert w.min() >= 0.0 and w.max() <= 2.0 and abs(w.mean() - 1.0) < 0.05
+    assert ora.inflow(3, 2, 7, 64, 5, 1.0, 0.1) != ora.inflow(3, 2, 8, 64, 5, 1.0, 0.1)
+    assert ora.inflow(3, 2, 7, 64, 5, 1.0, 0.1) != ora.inflow(3, 3, 7, 64, 5, 1.0, 0.1)
+    m = ora.Model(nx=16, ny=12, v_y=-0.5)
+    g = np.random.default_rng(0)
+    u = (0.5 + 0.05 * g.random((12, 16)), g.random((12, 16)), g.random((12, 16)))
+    a = ora.step(m, *u, 5)
+    b = ora.step_inflow(m, *u, 5, 0, 3, 2, 0.0)
+    assert all(np.array_equal(x, y) for x, y in zip(a, b))

@@ -122,3 +122,27 @@ def test_dataset_sweeps_parity(ora):
         u0 = ora.initial_fields(ic, p.nx, p.ny, 10 + k)
         assert normwise(g1[k], ora.step(m, *u0, 1)) <= 1e-12, k
         assert normwise(g60[k], ora.step(m, *u0, 60)) <= 1e-10, k
+
+
+def test_stochastic_inflow_parity(ora):
+    """R-27 stochastic inflow (the kernels draw the truncated-Gaussian reservoir row of every step
+    on the device): each member against the oracle's own generator and step after 1 step
+    (<= 1e-12) and 40 steps (<= 1e-10); c mass unchanged (the inflow only feeds rho)."""
+    p = pf.pf_default_params(2).replace(nx=64, ny=48, ic_height=16.0, n_members=3, member_offset=4,
+                                       noise_rho=0.3, rho_in=1.0, theta_deg=70.0, seed=12, graph_steps=8)
+    with _sim(p) as s:
+        s.step(1)
+        g1 = [s.fields(k) for k in range(3)]
+        s.step(39)
+        g40 = [s.fields(k) for k in range(3)]
+        d = [s.diagnostics(k) for k in range(3)]
+    for k in range(3):
+        m, ic = oracle_member(ora, p, 4 + k)
+        u0 = ora.initial_fields(ic, p.nx, p.ny, 4 + k)
+        r1 = ora.step_inflow(m, *u0, 1, 0, 12, 4 + k, 0.3)
+        r40 = ora.step_inflow(m, *u0, 40, 0, 12, 4 + k, 0.3)
+        assert normwise(g1[k], r1) <= 1e-12, k
+        assert normwise(g40[k], r40) <= 1e-10, k
+        assert abs(d[k][0] - ora.diagnostics(m, *u0)[0]) <= 1e-12 * abs(d[k][0])
+        # the noise is really there: the deterministic run differs
+        assert normwise(g40[k], ora.step(m, *u0, 40)) > 1e-8
