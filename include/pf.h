@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define PF_ABI_VERSION 5u
+#define PF_ABI_VERSION 6u
 
 typedef struct pf_ctx pf_ctx; /* opaque */
 
@@ -81,6 +81,10 @@ typedef struct {
     double noise_rho;                /* stochastic inflow (R-27): > 0 replaces the top
                                         reservoir rho_in by a per-step, per-column draw from
                                         N(rho_in, noise_rho^2) truncated to [0, 2 rho_in]; 0 = off */
+    int32_t fe_model;                /* composition free energy: 0 = W_c c^2 (1-c)^2 phi (R-2);
+                                        1 = regular solution [omega c(1-c) + temp_rs (c ln c +
+                                        (1-c) ln(1-c))] phi (R-28, north_star wording)           */
+    double omega, temp_rs;           /* regular-solution interaction and temperature (R-28)   */
     int32_t ic;                      /* pf_ic                                                */
     int32_t ic_ncols;                /* PF_IC_COLUMNS: number of columns                    */
     double ic_height, ic_amp, ic_wavelength;

@@ -39,7 +39,8 @@ class _Model(C.Structure):
                 ("W_phi", C.c_double), ("MA_bulk", C.c_double), ("MB_bulk", C.c_double),
                 ("MA_surf", C.c_double), ("MB_surf", C.c_double), ("sigma_surf", C.c_double),
                 ("M_phi", C.c_double), ("D_rho", C.c_double), ("rho_in", C.c_double),
-                ("v_x", C.c_double), ("v_y", C.c_double)]
+                ("v_x", C.c_double), ("v_y", C.c_double), ("fe", C.c_int32), ("omega", C.c_double),
+                ("temp", C.c_double)]
 
 
 class _IC(C.Structure):
@@ -77,6 +78,9 @@ class Model:
     rho_in: float = 1.0
     v_x: float = 0.0
     v_y: float = 0.0
+    fe: int = 0            # 0 polynomial composition well (R-2), 1 regular solution (R-28)
+    omega: float = 0.0
+    temp: float = 0.0
 
     def _c(self, shape=None) -> _Model:
         d = {k: getattr(self, k) for k, _ in _Model._fields_}

@@ -40,6 +40,8 @@ typedef struct {
     double M_phi;            /* interface mobility (R-7)                        */
     double D_rho, rho_in;    /* vapour transport (R-9, R-12)         */
     double v_x, v_y;         /* vapour velocity of this member (R-10)           */
+    int32_t fe;              /* composition free energy: 0 polynomial (R-2), 1 regular solution (R-28) */
+    double omega, temp;      /* regular-solution interaction Omega and temperature T (R-28)          */
 } orc_model;
 
 /* Boundary rules for the ghost values (R-12). */
@@ -153,6 +155,23 @@ void orc_gradient(int nx, int ny, double dx, const double *u, int rule, double t
 /*   mu_c   = df/dc   - kappa_c   L(c)                                         */
 /*   mu_phi = df/dphi - kappa_phi L(phi)                                       */
 /* ------------------------------------------------------------------------- */
+/* Regular-solution variant (R-28; north_star "double-well and regular-solution derivatives"):
+ *   g(c) = Omega c~(1-c~) + T (c~ ln c~ + (1-c~) ln(1-c~)),  c~ = min(max(c, eps), 1-eps),
+ *   f = g(c~) phi + W_phi phi^2 (1-phi)^2,
+ *   df/dc = phi (Omega (1 - 2c~) + T (ln c~ - ln(1-c~))),  df/dphi = g(c~) + ...        */
+static const double ORC_FE_EPS = 1e-9;
+static double clampe(double c) { return c < ORC_FE_EPS ? ORC_FE_EPS : (c > 1.0 - ORC_FE_EPS ? 1.0 - ORC_FE_EPS : c); }
+static double g_rs(const orc_model *m, double c)
+{
+    double t = clampe(c);
+    return m->omega * t * (1.0 - t) + m->temp * (t * log(t) + (1.0 - t) * log(1.0 - t));
+}
+static double dg_rs(const orc_model *m, double c)
+{
+    double t = clampe(c);
+    return m->omega * (1.0 - 2.0 * t) + m->temp * (log(t) - log(1.0 - t));
+}
+
 void orc_mu(const orc_model *m, const double *c, const double *phi, double *mu_c, double *mu_phi)
 {
     int nx = m->nx, ny = m->ny;
@@ -163,9 +182,15 @@ void orc_mu(const orc_model *m, const double *c, const double *phi, double *mu_c
     orc_laplacian(nx, ny, m->dx, phi, ORC_MIRROR, 0.0, lp);
     for (size_t k = 0; k < n; ++k) {
         double cc = c[k], pp = phi[k];
-        double dfdc = 2.0 * m->W_c * cc * (1.0 - cc) * (1.0 - 2.0 * cc) * pp;
-        double dfdphi = m->W_c * cc * cc * (1.0 - cc) * (1.0 - cc)
-                      + 2.0 * m->W_phi * pp * (1.0 - pp) * (1.0 - 2.0 * pp);
+        double dfdc, dfdphi;
+        if (m->fe == 1) {
+            dfdc = pp * dg_rs(m, cc);
+            dfdphi = g_rs(m, cc) + 2.0 * m->W_phi * pp * (1.0 - pp) * (1.0 - 2.0 * pp);
+        } else {
+            dfdc = 2.0 * m->W_c * cc * (1.0 - cc) * (1.0 - 2.0 * cc) * pp;
+            dfdphi = m->W_c * cc * cc * (1.0 - cc) * (1.0 - cc)
+                   + 2.0 * m->W_phi * pp * (1.0 - pp) * (1.0 - 2.0 * pp);
+        }
         mu_c[k] = dfdc - m->kappa_c * lc[k];
         mu_phi[k] = dfdphi - m->kappa_phi * lp[k];
     }
@@ -355,8 +380,8 @@ double orc_energy(const orc_model *m, const double *c, const double *phi)
             size_t k = (size_t)j * nx + i;
             size_t kx = (size_t)j * nx + (i + 1) % nx;
             double cc = c[k], pp = phi[k];
-            double f = m->W_c * cc * cc * (1.0 - cc) * (1.0 - cc) * pp
-                     + m->W_phi * pp * pp * (1.0 - pp) * (1.0 - pp);
+            double fc = m->fe == 1 ? g_rs(m, cc) : m->W_c * cc * cc * (1.0 - cc) * (1.0 - cc);
+            double f = fc * pp + m->W_phi * pp * pp * (1.0 - pp) * (1.0 - pp);
             nadd(&E, dx2 * f);
             double dcx = c[kx] - cc, dpx = phi[kx] - pp;
             nadd(&E, 0.5 * m->kappa_c * dcx * dcx + 0.5 * m->kappa_phi * dpx * dpx);
@@ -571,7 +596,8 @@ int orc_initial_fields(const orc_ic *ic, int nx, int ny, int64_t member,
 double orc_dt_max(const orc_model *m, double M_c_max)
 {
     double dx2 = m->dx * m->dx, dx4 = dx2 * dx2;
-    double a = M_c_max * (64.0 * m->kappa_c / dx4 + 16.0 * m->W_c / dx2);
+    double fpp = m->fe == 1 ? 2.0 * fabs(m->omega) + m->temp / (0.05 * 0.95) : 2.0 * m->W_c;   /* R-18, R-28 */
+    double a = M_c_max * (64.0 * m->kappa_c / dx4 + 8.0 * fpp / dx2);
     double b = m->M_phi * (64.0 * m->kappa_phi / dx4 + 16.0 * m->W_phi / dx2);
     double d = 8.0 * m->D_rho / dx2;
     double mx = a;

@@ -15,6 +15,8 @@ struct KC {                    // coefficients folded into the compute precision
     real half_inv_dx2, inv_2dx, m_kc_dx2, m_kp_dx2, W_c, W2c, W2p;   // m_ = negated
     real two_inv_sigma, Mp_dx2, Dr_dx2, rho_in, coef;
     real MBb, dMb, MBs, dMs;   // mobilities shared by all members (MOB 0, 1)
+    real omega, temp;          // regular-solution composition energy (FE 1, R-28)
+    int fe;                    // 0 polynomial composition well (R-2), 1 regular solution (R-28)
     int mob;                   // 0: shared, M_A = M_B (h(c) drops out); 1: shared, M_A != M_B;
                                // 2: per member (record array, R-23)
 };
@@ -85,7 +87,19 @@ __device__ __forceinline__ real clamp01(real c) {
 // The neighbour sums are ((l + r) + (d + u)): symmetric in (d, u), so a mirrored ghost row
 // (u[-1] = u[0], u[-2] = u[1]) yields bit-identical mu / M to the cell it mirrors, and the
 // boundary-face fluxes vanish exactly.
-template <typename real, int MOB>
+// Regular-solution composition energy (R-28): g(c) = Omega c~(1-c~) + T (c~ ln c~ + (1-c~) ln(1-c~)),
+// c~ = min(max(c, 1e-9), 1 - 1e-9); returns g and g' = Omega (1 - 2c~) + T (ln c~ - ln(1-c~)).
+template <typename real>
+__device__ __forceinline__ void regular_solution(const KC<real> &k, real c, real &g, real &dg) {
+    const real eps = real(1e-9), one = real(1);
+    const real t = c < eps ? eps : (c > one - eps ? one - eps : c);
+    const real u = sub_(one, t);
+    const real lt = log(t), lu = log(u);
+    g = fma_(k.omega, mul_(t, u), mul_(k.temp, fma_(t, lt, mul_(u, lu))));
+    dg = fma_(k.omega, fma_(t, real(-2), one), mul_(k.temp, sub_(lt, lu)));
+}
+
+template <typename real, int MOB, int FE = 0>
 __device__ __forceinline__ void constitutive(const KC<real> &k, const Mob<real> &mo, const double *etab, real c,
                                              real p, real cl, real cr, real cd, real cu, real pl, real pr, real pd,
                                              real pu, real &mu_c, real &mu_p, real &M) {
@@ -94,12 +108,19 @@ __device__ __forceinline__ void constitutive(const KC<real> &k, const Mob<real> 
     const real lp = fma_(p, m4, add_(add_(pl, pr), add_(pd, pu)));   // dx^2 L(phi)
     const real c1 = mul_(c, sub_(one, c));                            // c(1-c)
     const real t2c = fma_(c, m2, one);                                // 1-2c
-    // mu_c = 2 W_c c(1-c)(1-2c) phi - kappa_c L(c)                              (R-2, R-4)
-    mu_c = fma_(lc, k.m_kc_dx2, mul_(mul_(mul_(c1, k.W2c), t2c), p));
-    // mu_phi = W_c c^2(1-c)^2 + 2 W_phi phi(1-phi)(1-2phi) - kappa_phi L(phi)    (R-3)
     const real p1 = mul_(p, sub_(one, p));                            // phi(1-phi)
     const real t2p = fma_(p, m2, one);                                // 1-2phi
-    mu_p = fma_(lp, k.m_kp_dx2, fma_(mul_(c1, c1), k.W_c, mul_(mul_(p1, k.W2p), t2p)));
+    if (FE == 1) {   // regular solution (R-28): mu_c = phi g'(c) - kappa_c L(c); mu_phi = g(c) + ...
+        real g, dg;
+        regular_solution(k, c, g, dg);
+        mu_c = fma_(lc, k.m_kc_dx2, mul_(dg, p));
+        mu_p = fma_(lp, k.m_kp_dx2, add_(g, mul_(mul_(p1, k.W2p), t2p)));
+    } else {
+        // mu_c = 2 W_c c(1-c)(1-2c) phi - kappa_c L(c)                          (R-2, R-4)
+        mu_c = fma_(lc, k.m_kc_dx2, mul_(mul_(mul_(c1, k.W2c), t2c), p));
+        // mu_phi = W_c c^2(1-c)^2 + 2 W_phi phi(1-phi)(1-2phi) - kappa_phi L(phi) (R-3)
+        mu_p = fma_(lp, k.m_kp_dx2, fma_(mul_(c1, c1), k.W_c, mul_(mul_(p1, k.W2p), t2p)));
+    }
     // M_c = M_bulk + e (M_surf_mix - M_bulk)                         (R-5, R-6)
     const real pp = mul_(mul_(p, p), fma_(p, m2, real(3)));           // 1/4 (2 - phit)(1 + phit)^2
     const real q = mul_(sub_(p, real(0.5)), k.two_inv_sigma);          // phit / sigma_surf

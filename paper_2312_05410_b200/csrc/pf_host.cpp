@@ -171,7 +171,10 @@ double dt_limit(const pf_params &p) {
                                std::max(std::fabs(p.M_A_surf), std::fabs(p.M_B_surf))) *
                       std::max(1.0, p.mob_hi);   // largest member multiplier (R-23)
     const double dx2 = p.dx * p.dx, dx4 = dx2 * dx2;
-    const double a = Mc * (64.0 * p.kappa_c / dx4 + 16.0 * p.W_c / dx2);
+    // |f''| bound of the composition energy: 2 W_c (polynomial), 2|Omega| + T / (0.01 * 0.99) for
+    // the regular solution on c in [0.05, 0.95] (R-28)
+    const double fpp = p.fe_model == 1 ? 2.0 * std::fabs(p.omega) + p.temp_rs / (0.05 * 0.95) : 2.0 * p.W_c;
+    const double a = Mc * (64.0 * p.kappa_c / dx4 + 8.0 * fpp / dx2);
     const double b = p.M_phi * (64.0 * p.kappa_phi / dx4 + 16.0 * p.W_phi / dx2);
     const double d = 8.0 * p.D_rho / dx2;
     return 1.6 / std::max(a, std::max(b, d));
@@ -201,6 +204,9 @@ pf::Coef make_coef(const pf_params &p) {
     K.half_kc = 0.5 * p.kappa_c;
     K.half_kp = 0.5 * p.kappa_phi;
     K.W_p = p.W_phi;
+    K.fe = p.fe_model;
+    K.omega = p.omega;
+    K.temp = p.temp_rs;
     return K;
 }
 
@@ -297,6 +303,8 @@ pf_status validate(const pf_params *p, std::string &why) {
     if (p->M_A_bulk < 0 || p->M_B_bulk < 0 || p->M_A_surf < 0 || p->M_B_surf < 0) { why = "mobilities must be >= 0"; return PF_ERR_ARG; }
     if (p->check_every < 1) { why = "check_every must be >= 1"; return PF_ERR_ARG; }
     if (p->graph_steps < 0) { why = "graph_steps must be >= 0"; return PF_ERR_ARG; }
+    if (p->fe_model != 0 && p->fe_model != 1) { why = "fe_model must be 0 or 1"; return PF_ERR_ARG; }
+    if (p->fe_model == 1 && !(p->temp_rs >= 0)) { why = "temp_rs must be >= 0"; return PF_ERR_ARG; }
     if (!(p->noise_rho >= 0) || !std::isfinite(p->noise_rho)) { why = "noise_rho must be finite and >= 0"; return PF_ERR_ARG; }
     if (!(p->mob_lo > 0) || !(p->mob_hi >= p->mob_lo)) { why = "need 0 < mob_lo <= mob_hi"; return PF_ERR_ARG; }
     if (p->overlap_halo != 0 && p->overlap_halo != 1) { why = "overlap_halo must be 0 or 1"; return PF_ERR_ARG; }

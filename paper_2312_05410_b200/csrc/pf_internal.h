@@ -41,6 +41,8 @@ struct Coef {
     double dx2;                     // dx^2 (diagnostics)
     double half_kc, half_kp;        // kappa/2 (diagnostics)
     double W_p;                     // W_phi (diagnostics)
+    int fe;                         // composition free energy: 0 polynomial (R-2), 1 regular solution (R-28)
+    double omega, temp;             // regular-solution Omega, T (R-28)
 };
 
 // Streaming-kernel plan of one slab (host-built once per ctx): strip geometry and the 3D TMA

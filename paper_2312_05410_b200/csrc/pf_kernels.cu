@@ -53,7 +53,7 @@ __device__ __forceinline__ int wrap_x(int gx, int nx) {
     return gx % nx;
 }
 
-template <typename real, int MOB>
+template <typename real, int MOB, int FE>
 __global__ void __launch_bounds__(NT) stage_kernel(Layout L, KC<real> k, const real *__restrict__ in,
                                                    const real *__restrict__ base, real *out,
                                                    const real *__restrict__ vel) {
@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(NT) stage_kernel(Layout L, KC<real> k, const r
         const int sy = t / (BX + 2), sx = t - sy * (BX + 2);
         const int ey = sy + 1, ex = sx + 1;
         real mc, mp, M;
-        constitutive<real, MOB>(k, mo, etab, sc[ey][ex], sp[ey][ex], sc[ey][ex - 1], sc[ey][ex + 1], sc[ey - 1][ex],
+        constitutive<real, MOB, FE>(k, mo, etab, sc[ey][ex], sp[ey][ex], sc[ey][ex - 1], sc[ey][ex + 1], sc[ey - 1][ex],
                                  sc[ey + 1][ex], sp[ey][ex - 1], sp[ey][ex + 1], sp[ey - 1][ex], sp[ey + 1][ex], mc,
                                  mp, M);
         smc[sy][sx] = mc;
@@ -222,7 +222,14 @@ __global__ void __launch_bounds__(DT) diag_kernel(Layout L, Coef K, const real *
         const double dcx = (double)c[ox] - cc;
         const double dpx = (double)p[ox] - pp;
         const double omc = 1.0 - cc, omp = 1.0 - pp;
-        double e = K.dx2 * (K.W_c * (cc * cc) * (omc * omc) * pp + K.W_p * (pp * pp) * (omp * omp));
+        double gc;
+        if (K.fe == 1) {   // regular solution (R-28)
+            const double t = cc < 1e-9 ? 1e-9 : (cc > 1.0 - 1e-9 ? 1.0 - 1e-9 : cc), u = 1.0 - t;
+            gc = K.omega * t * u + K.temp * (t * log(t) + u * log(u));
+        } else {
+            gc = K.W_c * (cc * cc) * (omc * omc);
+        }
+        double e = K.dx2 * (gc * pp + K.W_p * (pp * pp) * (omp * omp));
         e += K.half_kc * (dcx * dcx) + K.half_kp * (dpx * dpx);
         if (L.y0 + ly < L.ny - 1) {      // y-face above (ghost row at the slab top)
             const int64_t oy = L.at(ly + 1, i);
@@ -488,7 +495,7 @@ __device__ __forceinline__ void store_with_ghosts(const Layout &L, real *b, int 
     else if (g >= L.ny - 2 && f != 2) store_row_ghosts(L, b, 2 * L.ny_loc - 1 - r, x, v);   // top slab
 }
 
-template <typename real, int NCW, int R, int S, bool BASE, int MOB, int MINB>
+template <typename real, int NCW, int R, int S, bool BASE, int MOB, int FE, int MINB>
 __global__ void __launch_bounds__(32 * NCW + 32, MINB) stream_kernel(
     Layout L, KC<real> k, const __grid_constant__ CUtensorMap mapIn, const __grid_constant__ CUtensorMap mapBase,
     real *out, const real *__restrict__ vel, int Wo, int G) {
@@ -591,7 +598,7 @@ __global__ void __launch_bounds__(32 * NCW + 32, MINB) stream_kernel(
                 b_m3 = b_m2; b_m2 = b_m1;
                 M_m2 = M_m1;
                 // mu / M of row k-1 at this lane's column
-                constitutive<real, MOB>(k, mo, etab, c_m1, p_m1, rk1[-1], rk1[1], c_m2, c_0, rk1[plane - 1],
+                constitutive<real, MOB, FE>(k, mo, etab, c_m1, p_m1, rk1[-1], rk1[1], c_m2, c_0, rk1[plane - 1],
                                          rk1[plane + 1], p_m2, p_0, a_m1, b_m1, M_m1);
                 // update of row k-2.  East face flux from this lane's mu / M and lane+1's; the west
                 // flux is lane-1's east flux; the south flux is last row's north flux.
@@ -670,7 +677,7 @@ constexpr int kPairHalo = 4;    // box columns left of the strip (and right of i
 #endif
 constexpr bool kSinglesShfl = PF_SINGLES_SHFL;
 
-template <typename real, int NCW, int R, int S, bool BASE, int MOB, int MINB>
+template <typename real, int NCW, int R, int S, bool BASE, int MOB, int FE, int MINB>
 __global__ void __launch_bounds__(32 * NCW + 32, MINB) pair_kernel(
     Layout L, KC<real> k, const __grid_constant__ CUtensorMap mapIn, const __grid_constant__ CUtensorMap mapBase,
     real *out, const real *__restrict__ vel, int Wo, int G) {
@@ -781,9 +788,9 @@ __global__ void __launch_bounds__(32 * NCW + 32, MINB) pair_kernel(
                 A2x = A1x; A2y = A1y; M2x = M1x; M2y = M1y;
                 B3x = B2x; B3y = B2y; B2x = B1x; B2y = B1y;
                 // a2: mu_c, mu_phi, M of row k-1 at both columns
-                constitutive<real, MOB>(k, mo, etab, c1.x, p1.x, cw1, c1.y, c2.x, c0.x, pw1, p1.y, p2.x,
+                constitutive<real, MOB, FE>(k, mo, etab, c1.x, p1.x, cw1, c1.y, c2.x, c0.x, pw1, p1.y, p2.x,
                                          p0.x, A1x, B1x, M1x);
-                constitutive<real, MOB>(k, mo, etab, c1.y, p1.y, c1.x, ce1, c2.y, c0.y, p1.x, pe1, p2.y,
+                constitutive<real, MOB, FE>(k, mo, etab, c1.y, p1.y, c1.x, ce1, c2.y, c0.y, p1.x, pe1, p2.y,
                                          p0.y, A1y, B1y, M1y);
                 // a3-a5: update of row k-2.  x faces: (a, a+1) in lane, (a+1, next a) by shuffle,
                 // the west face of a is the previous lane's east face of its right column.
@@ -853,6 +860,9 @@ KC<real> make_kc(const Coef &K, double coef) {
     k.MBs = (real)K.MBs;
     k.dMs = (real)K.dMs;
     k.mob = K.mob;
+    k.fe = K.fe;
+    k.omega = (real)K.omega;
+    k.temp = (real)K.temp;
     k.Mp_dx2 = (real)K.Mp_dx2;
     k.Dr_dx2 = (real)K.Dr_dx2;
     k.rho_in = (real)K.rho_in;
@@ -893,14 +903,14 @@ struct PairCfg {
 
 enum Kind { kStreamKind = 1, kPairKind = 2 };
 
-template <int KIND, typename real, int NCW, int R, int S, bool BASE, int MOB, int MINB>
+template <int KIND, typename real, int NCW, int R, int S, bool BASE, int MOB, int FE, int MINB>
 cudaError_t launch_ring(const Layout &L, const StreamPlan &P, const KC<real> &k, int stage, real *out,
                         const real *vel, cudaStream_t s) {
     const size_t smem = stream_smem_bytes<real>(P.box_x, R, S, BASE);
     static int occ = -1, nsm = 0;
     static size_t smem_set = 0;
-    auto kern = KIND == kPairKind ? pair_kernel<real, NCW, R, S, BASE, MOB, MINB>
-                                  : stream_kernel<real, NCW, R, S, BASE, MOB, MINB>;
+    auto kern = KIND == kPairKind ? pair_kernel<real, NCW, R, S, BASE, MOB, FE, MINB>
+                                  : stream_kernel<real, NCW, R, S, BASE, MOB, FE, MINB>;
     if (smem > smem_set) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
@@ -939,10 +949,17 @@ cudaError_t launch_ring(const Layout &L, const StreamPlan &P, const KC<real> &k,
 template <int KIND, typename real, int NCW, bool BASE, int R, int S, int MINB>
 cudaError_t launch_ring_h(const Layout &L, const StreamPlan &P, const KC<real> &k, int stage, real *out,
                           const real *vel, cudaStream_t s) {
+    if (k.fe == 1) {
+        switch (k.mob) {
+            case 0: return launch_ring<KIND, real, NCW, R, S, BASE, 0, 1, MINB>(L, P, k, stage, out, vel, s);
+            case 1: return launch_ring<KIND, real, NCW, R, S, BASE, 1, 1, MINB>(L, P, k, stage, out, vel, s);
+            default: return launch_ring<KIND, real, NCW, R, S, BASE, 2, 1, MINB>(L, P, k, stage, out, vel, s);
+        }
+    }
     switch (k.mob) {
-        case 0: return launch_ring<KIND, real, NCW, R, S, BASE, 0, MINB>(L, P, k, stage, out, vel, s);
-        case 1: return launch_ring<KIND, real, NCW, R, S, BASE, 1, MINB>(L, P, k, stage, out, vel, s);
-        default: return launch_ring<KIND, real, NCW, R, S, BASE, 2, MINB>(L, P, k, stage, out, vel, s);
+        case 0: return launch_ring<KIND, real, NCW, R, S, BASE, 0, 0, MINB>(L, P, k, stage, out, vel, s);
+        case 1: return launch_ring<KIND, real, NCW, R, S, BASE, 1, 0, MINB>(L, P, k, stage, out, vel, s);
+        default: return launch_ring<KIND, real, NCW, R, S, BASE, 2, 0, MINB>(L, P, k, stage, out, vel, s);
     }
 }
 
@@ -1080,11 +1097,13 @@ cudaError_t launch_stage(int precision, const Layout &L, const StreamPlan &P, co
     dim3 grid((L.nx + BX - 1) / BX, (L.r1 - L.r0 + BY - 1) / BY, L.members);
     if (precision == 0) {
         const KC<double> kd = make_kc<double>(K, coef);
-        auto kern = kd.mob == 0 ? stage_kernel<double, 0> : kd.mob == 1 ? stage_kernel<double, 1> : stage_kernel<double, 2>;
+        auto kern = kd.fe == 1 ? (kd.mob == 0 ? stage_kernel<double, 0, 1> : kd.mob == 1 ? stage_kernel<double, 1, 1> : stage_kernel<double, 2, 1>)
+                               : (kd.mob == 0 ? stage_kernel<double, 0, 0> : kd.mob == 1 ? stage_kernel<double, 1, 0> : stage_kernel<double, 2, 0>);
         kern<<<grid, NT, 0, s>>>(L, kd, (const double *)in, (const double *)base, (double *)out, (const double *)vel);
     } else {
         const KC<float> kf = make_kc<float>(K, coef);
-        auto kern = kf.mob == 0 ? stage_kernel<float, 0> : kf.mob == 1 ? stage_kernel<float, 1> : stage_kernel<float, 2>;
+        auto kern = kf.fe == 1 ? (kf.mob == 0 ? stage_kernel<float, 0, 1> : kf.mob == 1 ? stage_kernel<float, 1, 1> : stage_kernel<float, 2, 1>)
+                               : (kf.mob == 0 ? stage_kernel<float, 0, 0> : kf.mob == 1 ? stage_kernel<float, 1, 0> : stage_kernel<float, 2, 0>);
         kern<<<grid, NT, 0, s>>>(L, kf, (const float *)in, (const float *)base, (float *)out, (const float *)vel);
     }
     return cudaGetLastError();

@@ -16,7 +16,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libpf.so")
 HEADER = os.path.join(os.path.dirname(_HERE), "include", "pf.h")
 
-PF_ABI_VERSION = 5
+PF_ABI_VERSION = 6
 PF_OK, PF_ERR_ARG, PF_ERR_UNSTABLE_DT, PF_ERR_NOMEM, PF_ERR_CUDA, PF_ERR_NCCL, PF_ERR_BLOWUP, \
     PF_ERR_STATE, PF_ERR_ABI = range(9)
 STATUS_NAMES = ["PF_OK", "PF_ERR_ARG", "PF_ERR_UNSTABLE_DT", "PF_ERR_NOMEM", "PF_ERR_CUDA",
@@ -36,6 +36,7 @@ class pf_params(C.Structure):
         ("D_rho", C.c_double), ("rho_in", C.c_double), ("v0", C.c_double), ("theta_deg", C.c_double),
         ("rate_lo", C.c_double), ("rate_hi", C.c_double), ("theta_span", C.c_double),
         ("mob_lo", C.c_double), ("mob_hi", C.c_double), ("noise_rho", C.c_double),
+        ("fe_model", C.c_int32), ("omega", C.c_double), ("temp_rs", C.c_double),
         ("ic", C.c_int32), ("ic_ncols", C.c_int32),
         ("ic_height", C.c_double), ("ic_amp", C.c_double), ("ic_wavelength", C.c_double),
         ("ic_c0", C.c_double), ("ic_c_lo", C.c_double), ("ic_c_hi", C.c_double),

@@ -40,7 +40,7 @@ def _oracle_view(p):
     return dict(nx=p.nx, ny=p.ny, dx=p.dx, dt=p.dt, kappa_c=p.kappa_c, kappa_phi=p.kappa_phi,
                 W_c=p.W_c, W_phi=p.W_phi, MA_bulk=p.M_A_bulk, MB_bulk=p.M_B_bulk,
                 MA_surf=p.M_A_surf, MB_surf=p.M_B_surf, sigma_surf=p.sigma_surf, M_phi=p.M_phi,
-                D_rho=p.D_rho, rho_in=p.rho_in)
+                D_rho=p.D_rho, rho_in=p.rho_in, fe=p.fe_model, omega=p.omega, temp=p.temp_rs)
 
 
 def _ic_view(p):

@@ -440,3 +440,68 @@ def test_stability_bound_values(ora):
     """R-18: dt_max = 1.6 / max(M_c (64 kappa_c/dx^4 + 16 W_c/dx^2), ...): 0.02 (cfg1), 2e-3 (cfg2-5)."""
     assert ora.dt_max(ora.preset(1)["model"], 1.0) == pytest.approx(0.02, rel=1e-15)
     assert ora.dt_max(ora.preset(2)["model"], 10.0) == pytest.approx(2e-3, rel=1e-15)
+
+
+# --------------------------------------------------------------------------- regular solution (R-28)
+def _energy_complex_rs(m, c, phi):
+    """E_h with the regular-solution composition energy (R-28), complex-safe (no clamping: the
+    states stay inside (1e-9, 1 - 1e-9))."""
+    g = m.omega * c * (1 - c) + m.temp * (c * np.log(c) + (1 - c) * np.log(1 - c))
+    f = g * phi + m.W_phi * phi**2 * (1 - phi) ** 2
+    E = m.dx**2 * f.sum()
+    for u, k in ((c, m.kappa_c), (phi, m.kappa_phi)):
+        dxu = np.roll(u, -1, axis=1) - u
+        dyu = u[1:, :] - u[:-1, :]
+        E = E + 0.5 * k * ((dxu**2).sum() + (dyu**2).sum())
+    return E
+
+
+def test_regular_solution_mu_is_variational_derivative(ora):
+    """R-28: mu = (1/dx^2) dE_h/du for the regular-solution energy (complex step)."""
+    nx = ny = 6
+    eps = 1e-30
+    m = _model(ora, dx=0.9, kappa_c=0.6, kappa_phi=1.1, W_phi=0.8, fe=1, omega=2.7, temp=0.4)
+    g = np.random.default_rng(11)
+    c = 0.05 + 0.9 * g.random((ny, nx)); phi = g.random((ny, nx))
+    mu_c, mu_p = ora.mu(m, c, phi)
+    for field_idx, want in ((0, mu_c), (1, mu_p)):
+        got = np.zeros((ny, nx))
+        for j in range(ny):
+            for i in range(nx):
+                cc = c.astype(complex); pp = phi.astype(complex)
+                (cc if field_idx == 0 else pp)[j, i] += 1j * eps
+                got[j, i] = _energy_complex_rs(m, cc, pp).imag / eps / m.dx**2
+        np.testing.assert_allclose(want, got, atol=1e-12, rtol=0)
+    assert ora.energy(m, c, phi) == pytest.approx(_energy_complex_rs(m, c, phi).real, rel=1e-13)
+
+
+@pytest.mark.parametrize("mode,n", [(3, 800), (6, 400), (20, 300)])
+def test_regular_solution_linear_growth(ora, mode, n):
+    """R-28 linearised about c = 1/2 (phi = 1, v0 = 0): g''(1/2) = -2 Omega + 4 T, so
+    sigma = -M lam (g''(1/2) + kappa_c lam) and the midpoint factor G = 1 + sigma dt + (sigma dt)^2/2."""
+    nx, ny, a = 64, 4, 1e-6
+    M, Om, T = 1.0, 2.5, 0.5
+    m = _model(ora, dt=0.01, MA_bulk=M, MB_bulk=M, MA_surf=M, MB_surf=M, v_x=0.0, v_y=0.0, fe=1, omega=Om, temp=T)
+    c = inputs.cos_mode_x(nx, ny, mode, a)
+    phi = np.ones((ny, nx)); rho = np.ones((ny, nx))
+    lam = 4 / m.dx**2 * math.sin(math.pi * mode / nx) ** 2
+    sig = -M * lam * ((-2 * Om + 4 * T) + m.kappa_c * lam)
+    G = 1 + sig * m.dt + (sig * m.dt) ** 2 / 2
+    c1, _, _ = ora.step(m, c, phi, rho, n)
+    want = a * G**n
+    assert abs(_mode_amp_x(c1, mode, 0.5) - want) <= 1e-8 * abs(want)
+
+
+def test_regular_solution_energy_decay(ora):
+    """Pure Cahn-Hilliard with the regular solution (v0 = 0): E_h non-increasing every step, c mass
+    conserved."""
+    m = _model(ora, dt=0.005, v_x=0.0, v_y=0.0, fe=1, omega=2.5, temp=0.5, W_phi=1.0)
+    c, phi, rho = inputs.random_state(24, 20, 4, phi_kind="smooth")
+    E = [ora.energy(m, c, phi)]
+    mass0 = c.sum()
+    for _ in range(60):
+        c, phi, rho = ora.step(m, c, phi, rho, 1)
+        E.append(ora.energy(m, c, phi))
+    assert all(E[k + 1] <= E[k] + 1e-14 * abs(E[k]) for k in range(60))
+    assert E[-1] < E[0]
+    assert abs(c.sum() - mass0) <= 1e-12 * mass0

@@ -146,3 +146,26 @@ def test_stochastic_inflow_parity(ora):
         assert abs(d[k][0] - ora.diagnostics(m, *u0)[0]) <= 1e-12 * abs(d[k][0])
         # the noise is really there: the deterministic run differs
         assert normwise(g40[k], ora.step(m, *u0, 40)) > 1e-8
+
+
+def test_regular_solution_parity(ora):
+    """R-28 regular-solution composition energy on the device (fp64 log): each member against the
+    oracle after 1 step (<= 1e-12) and 80 steps (<= 1e-10); mass and energy diagnostics (the energy
+    uses the same free energy) within 1e-12."""
+    p = pf.pf_default_params(2).replace(nx=80, ny=48, ic_height=16.0, n_members=2, fe_model=1, omega=2.5,
+                                       temp_rs=0.5, theta_deg=75.0, M_A_bulk=6.0, M_B_bulk=3.0, seed=19, dt=4e-4)
+    with _sim(p) as s:
+        s.step(1)
+        g1 = [s.fields(k) for k in range(2)]
+        s.step(79)
+        g80 = [s.fields(k) for k in range(2)]
+        d = [s.diagnostics(k) for k in range(2)]
+    for k in range(2):
+        m, ic = oracle_member(ora, p, k)
+        u0 = ora.initial_fields(ic, p.nx, p.ny, k)
+        assert normwise(g1[k], ora.step(m, *u0, 1)) <= 1e-12, k
+        r80 = ora.step(m, *u0, 80)
+        assert normwise(g80[k], r80) <= 1e-10, k
+        dref = ora.diagnostics(m, *r80)
+        for q in (0, 3):
+            assert abs(d[k][q] - dref[q]) <= 1e-12 * abs(dref[q]), (k, q, d[k][q], dref[q])
