@@ -15,6 +15,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <utility>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -235,6 +236,7 @@ struct pf_ctx {
     cudaStream_t comm_stream = nullptr;   // halo exchange, overlapped with interior compute
     cudaEvent_t ev_band = nullptr, ev_xchg = nullptr;
     bool overlap = false;                 // band / exchange / interior schedule in use
+    bool fused = false;                   // fused-step kernel in use (kernel_path 4)
     ncclComm_t comm = nullptr;
     void *vel = nullptr;   // [members][2] in the storage precision
     double *h_diag = nullptr;
@@ -308,7 +310,7 @@ pf_status validate(const pf_params *p, std::string &why) {
     if (!(p->noise_rho >= 0) || !std::isfinite(p->noise_rho)) { why = "noise_rho must be finite and >= 0"; return PF_ERR_ARG; }
     if (!(p->mob_lo > 0) || !(p->mob_hi >= p->mob_lo)) { why = "need 0 < mob_lo <= mob_hi"; return PF_ERR_ARG; }
     if (p->overlap_halo != 0 && p->overlap_halo != 1) { why = "overlap_halo must be 0 or 1"; return PF_ERR_ARG; }
-    if (p->kernel_path < 0 || p->kernel_path > 3) { why = "kernel_path must be 0, 1, 2 or 3"; return PF_ERR_ARG; }
+    if (p->kernel_path < 0 || p->kernel_path > 4) { why = "kernel_path must be 0 .. 4"; return PF_ERR_ARG; }
     if (p->kernel_path >= 2 && !(p->nx % 4 == 0 && p->nx >= 16)) { why = "streaming kernels need nx % 4 == 0 and nx >= 16"; return PF_ERR_ARG; }
     if (p->ic < PF_IC_FILM || p->ic > PF_IC_NONE) { why = "unknown ic"; return PF_ERR_ARG; }
     if ((p->ic == PF_IC_ROUGH_SUBSTRATE || p->ic == PF_IC_COLUMNS) && !(p->W_phi > 0)) { why = "tanh recipes need W_phi > 0"; return PF_ERR_ARG; }
@@ -464,6 +466,24 @@ pf_status one_step(pf_ctx *c, bool capture, int64_t step) {
                                     step, s.U, s.Us, c->stream));
             if (!capture) c->launches += 1;
         }
+    if (c->fused) {   // one fused pass per step (kernel_path 4, single domain): U -> Us, then swap
+        Slab &S = c->slabs[0];
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        if (prof) {
+            e0 = take_event(c);
+            e1 = take_event(c);
+            CK(c, cudaEventRecord(e0, c->stream));
+        }
+        CK(c, pf::launch_fused(c->p.precision, S.L, S.plan, c->K, S.Us, c->vel, c->p.dt, c->stream));
+        if (!capture) c->launches += 1;
+        std::swap(S.U, S.Us);
+        pf::swap_plan_buffers(S.plan);
+        if (prof) {
+            CK(c, cudaEventRecord(e1, c->stream));
+            c->ev_rec.push_back({1, {e0, e1}});
+        }
+        return PF_OK;
+    }
     for (int stage = 1; stage <= 2; ++stage) {
         cudaEvent_t e0 = nullptr, e1 = nullptr;
         if (prof) {
@@ -665,6 +685,7 @@ pf_status create_common(const pf_params *p, int mode, int rank, int nranks, cons
     }
     // overlap schedule: slab modes, bands of 2 rows leave an interior of >= 4 rows
     c->overlap = mode != kSingle && rows >= 8 && p->overlap_halo != 0;
+    c->fused = mode == kSingle && p->kernel_path == 4 && c->slabs[0].plan.fused;
     c->ny_host = mode == kNccl ? rows : p->ny;
     c->y_host0 = mode == kNccl ? rank * rows : 0;
     if (cudaMallocHost((void **)&c->h_diag, nsl * (size_t)p->n_members * pf::kDiag * sizeof(double)) != cudaSuccess) {
@@ -930,7 +951,8 @@ pf_status pf_step(pf_ctx *c, int64_t n) {
         int64_t chunk = ce - (c->steps % ce);
         if (chunk > left) chunk = left;
         int64_t done = 0;
-        const bool use_graph = c->p.graph_steps > 0 && !c->prof && c->mode != kNccl && !(c->p.noise_rho > 0.0);
+        const bool use_graph = c->p.graph_steps > 0 && !c->prof && c->mode != kNccl && !(c->p.noise_rho > 0.0) &&
+                               !c->fused;   // the fused path swaps buffers on the host each step
         if (use_graph && chunk >= c->p.graph_steps) {
             pf_status st = ensure_graph(c);
             if (st != PF_OK) return st;

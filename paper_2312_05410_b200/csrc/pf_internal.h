@@ -53,7 +53,14 @@ struct StreamPlan {
     int ncw = 0, Wo = 0, strips = 0;
     int box_x = 0;                  // Wo + 2 halo columns (16 B each side)
     CUtensorMap mapU[2], mapUs[2];  // box (box_x, 2 or 4 rows, 3) over U / Us (index: rows == 4)
+    // fused-step kernel (kernel_path 4): one pass per midpoint step, u^n in U -> u^{n+1} in Us,
+    // then the host swaps U and Us (and these maps)
+    bool fused = false;
+    int fncw = 0, fWo = 0, fstrips = 0, fbox = 0;
+    CUtensorMap fmapU, fmapUs;      // box (fbox, 1 row, 3) over U / Us
 };
+// Swap the roles of the two state buffers in a plan (after a fused step).
+void swap_plan_buffers(StreamPlan &P);
 
 // Per-member record of the `vel` device array: v_x, v_y, M_B^bulk, M_A^bulk - M_B^bulk, M_B^surf,
 // M_A^surf - M_B^surf (storage precision; R-10, R-15, R-21, R-6, R-23).
@@ -73,6 +80,9 @@ cudaError_t make_stream_plan(int precision, const Layout &L, void *U, void *Us, 
 cudaError_t launch_stage(int precision, const Layout &L, const StreamPlan &plan, const Coef &K, int stage,
                          const void *in, const void *base, void *out, const void *vel, double coef,
                          cudaStream_t s);
+// Fused step: out (the other buffer) = u^{n+1} of the state in the buffer P.fmapU describes.
+cudaError_t launch_fused(int precision, const Layout &L, const StreamPlan &P, const Coef &K, void *out, const void *vel,
+                         double dt, cudaStream_t s);
 // Rebuild the ghost frame of a buffer from its owned cells (periodic columns; mirror rows and
 // the rho reservoir at global y boundaries).  Slab-interior ghost rows are left to the exchange.
 cudaError_t launch_fill_ghosts(int precision, const Layout &L, double rho_in, void *state, cudaStream_t s);

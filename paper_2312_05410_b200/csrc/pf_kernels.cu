@@ -17,6 +17,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cudaTypedefs.h>
+#include <utility>
 
 #include "pf_cell.cuh"
 #include "pf_internal.h"
@@ -844,6 +845,224 @@ __global__ void __launch_bounds__(32 * NCW + 32, MINB) pair_kernel(
     }
 }
 
+// ----------------------------------------------------------------------------------------
+// Fused-step kernel (SURVEY 7 "B9"): one pass per explicit-midpoint STEP instead of per stage.
+// Reads u^n once (3 fields) and writes u^{n+1} once (48 B per fp64 cell-step instead of 120 B);
+// the midpoint state u* never leaves the SM.  Rows stream through a TMA ring of 1-row boxes; per
+// input row k a compute lane (two columns, as in the pair kernel) evaluates
+//   stage 1: mu, M of u^n at row k-1 and u* at row k-2;
+//   stage 2 (lag 3): mu, M of u* at row k-3 and u^{n+1} at row k-4.
+// u* stays in registers (rows k-2 .. k-5), x-neighbours by warp shuffles.  A warp covers 64
+// columns; its u* is valid on 62, its stage-2 mu on 60, its outputs on the middle 56 (lanes
+// 2..29), so warps overlap by 8 columns (the halo is recomputed, 14%).  The midpoint ghost rows
+// of u* at the global y boundaries are replaced by the identities the two-pass kernels get from
+// the mirrored rows (zero boundary flux, mu_phi(-1) = mu_phi(0), phi*(-1) = phi*(0),
+// rho*(-1) = rho*(0), rho* above the top = the reservoir row), so every cell gets the same bits as
+// with the stage kernels.  Single-domain contexts only (a y-slab would need a 4-row u^n halo).
+constexpr int kFusedCols = 56;   // output columns per compute warp
+constexpr int kFusedHalo = 4;    // box columns left of the strip (and right of it)
+
+template <typename real, int NCW, int S, int MOB, int FE, int MINB>
+__global__ void __launch_bounds__(32 * NCW + 32, MINB) fused_kernel(
+    Layout L, KC<real> k, real coef1, real coef2, const __grid_constant__ CUtensorMap mapIn, real *out,
+    const real *__restrict__ vel, int Wo, int G) {
+    static_assert(S >= 8, "rows k .. k-4 are read from the ring, plus prefetch");
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int bx = Wo + 2 * kFusedHalo;
+    const Ring<real> rg(bx, 1, false);
+    unsigned char *base_sm = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
+    real *slots = reinterpret_cast<real *>(base_sm);
+    uint64_t *full = reinterpret_cast<uint64_t *>(base_sm + (size_t)S * rg.slot_elems * sizeof(real));
+    uint64_t *empty = full + S;
+    double *etab = reinterpret_cast<double *>(empty + S);
+    load_exp_table(etab);
+
+    const int t = threadIdx.x;
+    const int warp = t >> 5, lane = t & 31;
+    if (t == 0) {
+        for (int q = 0; q < S; ++q) {
+            mbar_init(&full[q], 1);
+            mbar_init(&empty[q], NCW);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    const int nx = L.nx;
+    const Sched sch = make_sched(L, Wo, G);
+    const uint32_t box_bytes = (uint32_t)(3 * bx * sizeof(real));
+    constexpr int LEAD = 4, TRAIL = 4;   // input rows before / after the segment's output rows
+
+    if (warp == NCW) {
+        // ------------------------------- producer -------------------------------
+        if (lane != 0) return;
+        prefetch_tmap(&mapIn);
+        uint32_t g = 0;
+        int64_t pos = sch.lo;
+        Seg sg;
+        while (next_seg(L, Wo, sch, pos, sg)) {
+            const int n = sg.yb - sg.ya + LEAD + TRAIL;
+            const int bxs = sg.x0 - kFusedHalo + L.gx;
+            for (int j = 0; j < n; ++j, ++g) {
+                const int slot = g % S;
+                if (g >= (uint32_t)S) mbar_wait(&empty[slot], ((g / S) - 1) & 1u);
+                mbar_expect_tx(&full[slot], box_bytes);
+                // input row sg.ya - LEAD + j (storage row + 2); rows past the frame are zero-filled
+                tma_load_3d(slots + slot * rg.slot_elems, &mapIn, bxs, sg.ya - LEAD + j + 2, 3 * sg.m, &full[slot]);
+            }
+        }
+        return;
+    }
+
+    // --------------------------- compute warps ---------------------------------
+    // lane l of warp w owns strip columns cx, cx + 1, cx = 56 w + 2 l - 4; lanes 2..29 store
+    const int cx = kFusedCols * warp + 2 * lane - 4;
+    const int ci = kFusedHalo + cx;          // its (even) column in a box row
+    const int plane = bx;                    // fields of a 1-row box are bx apart
+    const unsigned FULL = 0xffffffffu;
+    int sidx = 0;
+    uint32_t par = 0;
+    int64_t pos = sch.lo;
+    Seg sg;
+    while (next_seg(L, Wo, sch, pos, sg)) {
+        const int n = sg.yb - sg.ya + LEAD + TRAIL;
+        const int x = sg.x0 + cx;
+        const bool store = lane >= 2 && lane <= 29 && cx < sg.Wp;
+        const bool xedge = (x < L.gx) | (x + 1 >= nx - L.gx);
+        real *ob = out + sg.m * L.mstride;
+        const real vx = vel[kMembStride * sg.m], vy = vel[kMembStride * sg.m + 1];
+        const Mob<real> mo = MOB == 2 ? load_mob(vel, sg.m) : Mob<real>{};
+        // stage 1 windows (rows of u^n's mu / M): as in the pair kernel
+        real A1x = 0, A1y = 0, A2x = 0, A2y = 0, M1x = 0, M1y = 0, M2x = 0, M2y = 0;
+        real B1x = 0, B1y = 0, B2x = 0, B2y = 0, B3x = 0, B3y = 0, P3x = 0, P3y = 0, R3x = 0, R3y = 0;
+        real Fsx = 0, Fsy = 0;
+        // u* rows (pairs): c* k-2..k-4, phi* and rho* k-2..k-5
+        real Cs2x = 0, Cs2y = 0, Cs3x = 0, Cs3y = 0, Cs4x = 0, Cs4y = 0;
+        real Ps2x = 0, Ps2y = 0, Ps3x = 0, Ps3y = 0, Ps4x = 0, Ps4y = 0, Ps5x = 0, Ps5y = 0;
+        real Rs2x = 0, Rs2y = 0, Rs3x = 0, Rs3y = 0, Rs4x = 0, Rs4y = 0, Rs5x = 0, Rs5y = 0;
+        // stage 2 windows (rows of u*'s mu / M): A, M rows k-3, k-4; B rows k-3 .. k-5
+        real D1x = 0, D1y = 0, D2x = 0, D2y = 0, N1x = 0, N1y = 0, N2x = 0, N2y = 0;
+        real E1x = 0, E1y = 0, E2x = 0, E2y = 0, E3x = 0, E3y = 0, Gsx = 0, Gsy = 0;
+        // ring rows k-1 .. k-4 (slot pointers at this lane's column)
+        const real *r1 = nullptr, *r2 = nullptr, *r3 = nullptr, *r4 = nullptr;
+        for (int i = 0; i < n; ++i) {
+            const real *r0 = slots + sidx * rg.slot_elems + ci;     // row k = ya - 4 + i
+            mbar_wait(&full[sidx], par);
+            const int kk = sg.ya - LEAD + i;                          // local row k
+            // ---------------- stage 1: mu1 at k-1, u* at k-2 ----------------
+            if (i >= 2) {
+                const auto c0 = ld2(r0), c1 = ld2(r1), c2 = ld2(r2);
+                const auto p0 = ld2(r0 + plane), p1 = ld2(r1 + plane), p2 = ld2(r2 + plane);
+                const auto q1 = ld2(r1 + 2 * plane), q2 = ld2(r2 + 2 * plane);
+                const real cw1 = __shfl_up_sync(FULL, c1.y, 1), ce1 = __shfl_down_sync(FULL, c1.x, 1);
+                const real pw1 = __shfl_up_sync(FULL, p1.y, 1), pe1 = __shfl_down_sync(FULL, p1.x, 1);
+                const real pw2 = __shfl_up_sync(FULL, p2.y, 1), pe2 = __shfl_down_sync(FULL, p2.x, 1);
+                const real rw2 = __shfl_up_sync(FULL, q2.y, 1), re2 = __shfl_down_sync(FULL, q2.x, 1);
+                A2x = A1x; A2y = A1y; M2x = M1x; M2y = M1y;
+                B3x = B2x; B3y = B2y; B2x = B1x; B2y = B1y;
+                constitutive<real, MOB, FE>(k, mo, etab, c1.x, p1.x, cw1, c1.y, c2.x, c0.x, pw1, p1.y, p2.x, p0.x,
+                                            A1x, B1x, M1x);
+                constitutive<real, MOB, FE>(k, mo, etab, c1.y, p1.y, c1.x, ce1, c2.y, c0.y, p1.x, pe1, p2.y, p0.y,
+                                            A1y, B1y, M1y);
+                const real An = __shfl_down_sync(FULL, A2x, 1), Mn = __shfl_down_sync(FULL, M2x, 1);
+                const real Bn = __shfl_down_sync(FULL, B2x, 1), Bp = __shfl_up_sync(FULL, B2y, 1);
+                const real fex = face_flux<real>(M2x, M2y, A2x, A2y);
+                const real fey = face_flux<real>(M2y, Mn, A2y, An);
+                const real fwx = __shfl_up_sync(FULL, fey, 1);
+                const real fnx = face_flux<real>(M2x, M1x, A2x, A1x);
+                const real fny = face_flux<real>(M2y, M1y, A2y, A1y);
+                // rotate the u* window, then u*(k-2) = u^n(k-2) + dt/2 R(u^n)
+                Cs4x = Cs3x; Cs4y = Cs3y; Cs3x = Cs2x; Cs3y = Cs2y;
+                Ps5x = Ps4x; Ps5y = Ps4y; Ps4x = Ps3x; Ps4y = Ps3y; Ps3x = Ps2x; Ps3y = Ps2y;
+                Rs5x = Rs4x; Rs5y = Rs4y; Rs4x = Rs3x; Rs4y = Rs3y; Rs3x = Rs2x; Rs3y = Rs2y;
+                KC<real> k1 = k;
+                k1.coef = coef1;
+                cell_update<real>(k1, vx, vy, fex, fwx, fnx, Fsx, B2x, Bp, B2y, B3x, B1x, pw2, p2.y, P3x, p1.x, q2.x,
+                                  rw2, q2.y, R3x, q1.x, c2.x, p2.x, q2.x, Cs2x, Ps2x, Rs2x);
+                cell_update<real>(k1, vx, vy, fey, fex, fny, Fsy, B2y, B2x, Bn, B3y, B1y, p2.x, pe2, P3y, p1.y, q2.y,
+                                  q2.x, re2, R3y, q1.y, c2.y, p2.y, q2.y, Cs2y, Ps2y, Rs2y);
+                Fsx = fnx; Fsy = fny;
+                P3x = p2.x; P3y = p2.y; R3x = q2.x; R3y = q2.y;
+            }
+            // ---------------- stage 2: mu2 at k-3, u^{n+1} at k-4 ----------------
+            if (i >= 5) {
+                const int gq = L.y0 + kk - 3, gu = L.y0 + kk - 4;      // global rows
+                // mu2 of u* at row k-3: the ghost neighbours at the y boundaries are mirrors
+                const bool qbot = gq == 0, qtop = gq == L.ny - 1;
+                const real cdx = qbot ? Cs3x : Cs4x, cdy = qbot ? Cs3y : Cs4y;
+                const real cux = qtop ? Cs3x : Cs2x, cuy = qtop ? Cs3y : Cs2y;
+                const real pdx = qbot ? Ps3x : Ps4x, pdy = qbot ? Ps3y : Ps4y;
+                const real pux = qtop ? Ps3x : Ps2x, puy = qtop ? Ps3y : Ps2y;
+                const real cw = __shfl_up_sync(FULL, Cs3y, 1), ce = __shfl_down_sync(FULL, Cs3x, 1);
+                const real pw = __shfl_up_sync(FULL, Ps3y, 1), pe = __shfl_down_sync(FULL, Ps3x, 1);
+                D2x = D1x; D2y = D1y; N2x = N1x; N2y = N1y;
+                E3x = E2x; E3y = E2y; E2x = E1x; E2y = E1y;
+                constitutive<real, MOB, FE>(k, mo, etab, Cs3x, Ps3x, cw, Cs3y, cdx, cux, pw, Ps3y, pdx, pux, D1x, E1x,
+                                            N1x);
+                constitutive<real, MOB, FE>(k, mo, etab, Cs3y, Ps3y, Cs3x, ce, cdy, cuy, Ps3x, pe, pdy, puy, D1y, E1y,
+                                            N1y);
+                // update of row k-4 (u* row k-4 is Cs4/Ps4/Rs4; mu2 rows k-5, k-4, k-3 = E3, E2, E1)
+                const bool ubot = gu == 0, utop = gu == L.ny - 1;
+                const real An = __shfl_down_sync(FULL, D2x, 1), Mn = __shfl_down_sync(FULL, N2x, 1);
+                const real Bn = __shfl_down_sync(FULL, E2x, 1), Bp = __shfl_up_sync(FULL, E2y, 1);
+                const real fex = face_flux<real>(N2x, N2y, D2x, D2y);
+                const real fey = face_flux<real>(N2y, Mn, D2y, An);
+                const real fwx = __shfl_up_sync(FULL, fey, 1);
+                real fnx = face_flux<real>(N2x, N1x, D2x, D1x), fny = face_flux<real>(N2y, N1y, D2y, D1y);
+                if (utop) { fnx = real(0); fny = real(0); }
+                const real fsx = ubot ? real(0) : Gsx, fsy = ubot ? real(0) : Gsy;
+                Gsx = fnx; Gsy = fny;
+                const real qdx = ubot ? E2x : E3x, qdy = ubot ? E2y : E3y;
+                const real qux = utop ? E2x : E1x, quy = utop ? E2y : E1y;
+                const real phdx = ubot ? Ps4x : Ps5x, phdy = ubot ? Ps4y : Ps5y;
+                const real phux = utop ? Ps4x : Ps3x, phuy = utop ? Ps4y : Ps3y;
+                const auto rt = ld2(r3 + 2 * plane);                    // rho ghost row (reservoir) if utop
+                const real rdx = ubot ? Rs4x : Rs5x, rdy = ubot ? Rs4y : Rs5y;
+                const real rux = utop ? rt.x : Rs3x, ruy = utop ? rt.y : Rs3y;
+                const real pw4 = __shfl_up_sync(FULL, Ps4y, 1), pe4 = __shfl_down_sync(FULL, Ps4x, 1);
+                const real rw4 = __shfl_up_sync(FULL, Rs4y, 1), re4 = __shfl_down_sync(FULL, Rs4x, 1);
+                const auto b0 = ld2(r4), b1 = ld2(r4 + plane), b2 = ld2(r4 + 2 * plane);   // u^n row k-4
+                KC<real> k2 = k;
+                k2.coef = coef2;
+                real ocx, opx, orx, ocy, opy, ory;
+                cell_update<real>(k2, vx, vy, fex, fwx, fnx, fsx, E2x, Bp, E2y, qdx, qux, pw4, Ps4y, phdx, phux, Rs4x,
+                                  rw4, Rs4y, rdx, rux, b0.x, b1.x, b2.x, ocx, opx, orx);
+                cell_update<real>(k2, vx, vy, fey, fex, fny, fsy, E2y, E2x, Bn, qdy, quy, Ps4x, pe4, phdy, phuy, Rs4y,
+                                  Rs4x, re4, rdy, ruy, b0.y, b1.y, b2.y, ocy, opy, ory);
+                if (store && i >= LEAD + 4 && kk - 4 < sg.yb) {
+                    const int r = kk - 4;
+                    const bool edge = xedge | (L.y0 + r <= 1) | (L.y0 + r >= L.ny - 2);
+                    if (!edge) {
+                        real *o = ob + L.at(r, x);
+                        st2(o, ocx, ocy);
+                        st2(o + L.fstride, opx, opy);
+                        st2(o + 2 * L.fstride, orx, ory);
+                    } else {
+                        store_with_ghosts<real>(L, ob, 0, r, x, ocx);
+                        store_with_ghosts<real>(L, ob + L.fstride, 1, r, x, opx);
+                        store_with_ghosts<real>(L, ob + 2 * L.fstride, 2, r, x, orx);
+                        store_with_ghosts<real>(L, ob, 0, r, x + 1, ocy);
+                        store_with_ghosts<real>(L, ob + L.fstride, 1, r, x + 1, opy);
+                        store_with_ghosts<real>(L, ob + 2 * L.fstride, 2, r, x + 1, ory);
+                    }
+                }
+            }
+            // the slot of row k-4 is no longer read
+            __syncwarp();
+            if (i >= 4 && lane == 0) {
+                const int s4 = sidx >= 4 ? sidx - 4 : sidx - 4 + S;
+                mbar_arrive(&empty[s4]);
+            }
+            r4 = r3; r3 = r2; r2 = r1; r1 = r0;
+            if (++sidx == S) { sidx = 0; par ^= 1u; }
+        }
+        // release the segment's last 4 rows
+        __syncwarp();
+        if (lane == 0)
+            for (int d = 1; d <= 4 && d <= n; ++d) mbar_arrive(&empty[sidx >= d ? sidx - d : sidx - d + S]);
+    }
+}
+
 template <typename real>
 KC<real> make_kc(const Coef &K, double coef) {
     KC<real> k;
@@ -1003,6 +1222,82 @@ cudaError_t launch_stream(const Layout &L, const StreamPlan &P, const KC<real> &
     }
 }
 
+// Fused-step kernel configuration: ~2 blocks of NCW + 1 warps per SM (its two sets of stage windows
+// need ~2x the registers of the pair kernel); 1-row ring slots, 12 deep (rows k .. k-4 held).
+template <typename real, int NCW>
+struct FusedCfg {
+    static constexpr int minb = 2;
+    static constexpr int S = 12;
+};
+
+template <typename real, int NCW, int MOB, int FE>
+cudaError_t launch_fused_k(const Layout &L, const StreamPlan &P, const KC<real> &k, real c1, real c2, real *out,
+                           const real *vel, cudaStream_t s) {
+    using C = FusedCfg<real, NCW>;
+    const size_t smem = stream_smem_bytes<real>(P.fbox, 1, C::S, false);
+    static int occ = -1, nsm = 0;
+    static size_t smem_set = 0;
+    auto kern = fused_kernel<real, NCW, C::S, MOB, FE, C::minb>;
+    if (smem > smem_set) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        smem_set = smem;
+        occ = -1;
+    }
+    if (occ < 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * NCW + 32, smem);
+        if (e != cudaSuccess) return e;
+        if (occ < 1) occ = 1;
+    }
+    const int64_t T = (int64_t)L.members * (L.r1 - L.r0);
+    const int64_t minrows = 24;
+    int64_t B = (int64_t)occ * nsm;
+    int64_t G = B / P.fstrips;
+    if (G > (T + minrows - 1) / minrows) G = (T + minrows - 1) / minrows;
+    if (G >= 4) {
+        B = G * P.fstrips;
+    } else {
+        G = 0;
+        const int64_t R_ = (int64_t)L.members * P.fstrips * (L.r1 - L.r0);
+        if (B > (R_ + minrows - 1) / minrows) B = (R_ + minrows - 1) / minrows;
+    }
+    if (B < 1) B = 1;
+    kern<<<(unsigned)B, 32 * NCW + 32, smem, s>>>(L, k, c1, c2, P.fmapU, out, vel, P.fWo, (int)G);
+    return cudaGetLastError();
+}
+
+template <typename real, int NCW>
+cudaError_t launch_fused_n(const Layout &L, const StreamPlan &P, const KC<real> &k, real c1, real c2, real *out,
+                           const real *vel, cudaStream_t s) {
+    if (k.fe == 1) {
+        switch (k.mob) {
+            case 0: return launch_fused_k<real, NCW, 0, 1>(L, P, k, c1, c2, out, vel, s);
+            case 1: return launch_fused_k<real, NCW, 1, 1>(L, P, k, c1, c2, out, vel, s);
+            default: return launch_fused_k<real, NCW, 2, 1>(L, P, k, c1, c2, out, vel, s);
+        }
+    }
+    switch (k.mob) {
+        case 0: return launch_fused_k<real, NCW, 0, 0>(L, P, k, c1, c2, out, vel, s);
+        case 1: return launch_fused_k<real, NCW, 1, 0>(L, P, k, c1, c2, out, vel, s);
+        default: return launch_fused_k<real, NCW, 2, 0>(L, P, k, c1, c2, out, vel, s);
+    }
+}
+
+template <typename real>
+cudaError_t launch_fused_t(const Layout &L, const StreamPlan &P, const KC<real> &k, real c1, real c2, real *out,
+                           const real *vel, cudaStream_t s) {
+    switch (P.fncw) {
+        case 1: return launch_fused_n<real, 1>(L, P, k, c1, c2, out, vel, s);
+        case 2: return launch_fused_n<real, 2>(L, P, k, c1, c2, out, vel, s);
+        case 3: return launch_fused_n<real, 3>(L, P, k, c1, c2, out, vel, s);
+        case 4: return launch_fused_n<real, 4>(L, P, k, c1, c2, out, vel, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
 cudaError_t upload_exp_table() {
     static bool done = false;
     if (done) return cudaSuccess;
@@ -1047,7 +1342,7 @@ cudaError_t make_stream_plan(int precision, const Layout &L, void *U, void *Us, 
     P = StreamPlan();
     if (L.path == 1 || !stream_eligible(L)) return cudaSuccess;
     const int HL = precision == 0 ? 2 : 4;       // stream-kernel box halo: 16 B of columns
-    if (L.path == 3 || L.path == 0) {
+    if (L.path == 3 || L.path == 0 || L.path == 4) {
         // pair kernel: strips of Wo <= 240 columns (box Wo + 8 <= 256 elements), Wo a multiple of
         // 4 (16 B rows for fp32 too), split nx evenly; 60 output columns per compute warp
         int strips = (L.nx + 239) / 240;
@@ -1081,7 +1376,40 @@ cudaError_t make_stream_plan(int precision, const Layout &L, void *U, void *Us, 
             !encode_map(&P.mapUs[ri], precision, L, Us, P.box_x, ri ? 4 : 2))
             return cudaErrorInvalidValue;
     P.ok = true;
+    if (L.path == 4) {
+        // fused kernel: strips of 56 NCW columns, NCW for the least idle columns (ties: wider)
+        int best = 1, waste = 1 << 30;
+        for (int ncw = 1; ncw <= 4; ++ncw) {
+            const int w = kFusedCols * ncw, st = (L.nx + w - 1) / w, idle = st * w - L.nx;
+            if (idle <= waste + L.nx / 50) { if (idle < waste) waste = idle; best = ncw; }
+        }
+        static const int force = env_int("PF_FUSED_NCW", 0);
+        if (force >= 1 && force <= 4) best = force;
+        P.fncw = best;
+        P.fWo = kFusedCols * best;
+        P.fstrips = (L.nx + P.fWo - 1) / P.fWo;
+        P.fbox = P.fWo + 2 * kFusedHalo;
+        if (!encode_map(&P.fmapU, precision, L, U, P.fbox, 1) || !encode_map(&P.fmapUs, precision, L, Us, P.fbox, 1))
+            return cudaErrorInvalidValue;
+        P.fused = true;
+    }
     return cudaSuccess;
+}
+
+cudaError_t launch_fused(int precision, const Layout &L, const StreamPlan &P, const Coef &K, void *out, const void *vel,
+                         double dt, cudaStream_t s) {
+    cudaError_t te = upload_exp_table();
+    if (te != cudaSuccess) return te;
+    if (!P.fused) return cudaErrorInvalidValue;
+    if (precision == 0)
+        return launch_fused_t<double>(L, P, make_kc<double>(K, 0.5 * dt), 0.5 * dt, dt, (double *)out, (const double *)vel, s);
+    return launch_fused_t<float>(L, P, make_kc<float>(K, 0.5 * dt), (float)(0.5 * dt), (float)dt, (float *)out,
+                                 (const float *)vel, s);
+}
+
+void swap_plan_buffers(StreamPlan &P) {
+    for (int i = 0; i < 2; ++i) std::swap(P.mapU[i], P.mapUs[i]);
+    std::swap(P.fmapU, P.fmapUs);
 }
 
 cudaError_t launch_stage(int precision, const Layout &L, const StreamPlan &P, const Coef &K, int stage,
