@@ -310,7 +310,7 @@ pf_status validate(const pf_params *p, std::string &why) {
     if (!(p->noise_rho >= 0) || !std::isfinite(p->noise_rho)) { why = "noise_rho must be finite and >= 0"; return PF_ERR_ARG; }
     if (!(p->mob_lo > 0) || !(p->mob_hi >= p->mob_lo)) { why = "need 0 < mob_lo <= mob_hi"; return PF_ERR_ARG; }
     if (p->overlap_halo != 0 && p->overlap_halo != 1) { why = "overlap_halo must be 0 or 1"; return PF_ERR_ARG; }
-    if (p->kernel_path < 0 || p->kernel_path > 4) { why = "kernel_path must be 0 .. 4"; return PF_ERR_ARG; }
+    if (p->kernel_path < 0 || p->kernel_path > 5) { why = "kernel_path must be 0 .. 5"; return PF_ERR_ARG; }
     if (p->kernel_path >= 2 && !(p->nx % 4 == 0 && p->nx >= 16)) { why = "streaming kernels need nx % 4 == 0 and nx >= 16"; return PF_ERR_ARG; }
     if (p->ic < PF_IC_FILM || p->ic > PF_IC_NONE) { why = "unknown ic"; return PF_ERR_ARG; }
     if ((p->ic == PF_IC_ROUGH_SUBSTRATE || p->ic == PF_IC_COLUMNS) && !(p->W_phi > 0)) { why = "tanh recipes need W_phi > 0"; return PF_ERR_ARG; }
@@ -685,7 +685,7 @@ pf_status create_common(const pf_params *p, int mode, int rank, int nranks, cons
     }
     // overlap schedule: slab modes, bands of 2 rows leave an interior of >= 4 rows
     c->overlap = mode != kSingle && rows >= 8 && p->overlap_halo != 0;
-    c->fused = mode == kSingle && p->kernel_path == 4 && c->slabs[0].plan.fused;
+    c->fused = mode == kSingle && (p->kernel_path == 4 || p->kernel_path == 5) && c->slabs[0].plan.fused;
     c->ny_host = mode == kNccl ? rows : p->ny;
     c->y_host0 = mode == kNccl ? rank * rows : 0;
     if (cudaMallocHost((void **)&c->h_diag, nsl * (size_t)p->n_members * pf::kDiag * sizeof(double)) != cudaSuccess) {

@@ -56,6 +56,7 @@ struct StreamPlan {
     // fused-step kernel (kernel_path 4): one pass per midpoint step, u^n in U -> u^{n+1} in Us,
     // then the host swaps U and Us (and these maps)
     bool fused = false;
+    bool ws = false;                // kernel_path 5: the warp-specialised step kernel (fmap*, fWo, ...)
     int fncw = 0, fWo = 0, fstrips = 0, fbox = 0;
     CUtensorMap fmapU, fmapUs;      // box (fbox, 1 row, 3) over U / Us
 };

@@ -1063,6 +1063,263 @@ __global__ void __launch_bounds__(32 * NCW + 32, MINB) fused_kernel(
     }
 }
 
+// ----------------------------------------------------------------------------------------
+// Warp-specialised step kernel (kernel_path 5): one pass per explicit-midpoint STEP through an
+// on-chip pipeline, u^n read once and u^{n+1} written once (48 B per fp64 cell-step):
+//   producer warp --TMA 1-row boxes of u^n--> input ring
+//   NCW stage-1 warps (the pair kernel's arithmetic with coef dt/2): u*(k-2) from input rows
+//       k .. k-2; they write u* and the base u^n of that row (6 planes) into a u* ring in shared
+//       memory, each warp its 60 columns [60 w - 2, 60 w + 58) of the strip
+//   NCW stage-2 warps (the pair kernel's arithmetic with coef dt): u^{n+1}(q-2) from u* rows
+//       q .. q-2 of the u* ring, stored to HBM with the ghost frame.
+// Both stages keep the pair kernel's register footprint (each warp runs one stage), so the SM
+// holds as many compute warps as the two-pass path while HBM traffic drops from 120 to 48 B per
+// cell-step.  At the global y boundaries stage 2 substitutes the identities the two-pass kernels
+// get from u*'s mirrored ghost rows (zero boundary flux, mu_phi(-1) = mu_phi(0), phi*(-1) = phi*(0),
+// rho*(-1) = rho*(0), rho* above the top = the reservoir row), so results are bitwise those of
+// the stage kernels.  Single-domain contexts only.
+template <typename real, int NCW, int SI, int SU, int MOB, int FE, int MINB>
+__global__ void __launch_bounds__(32 * (2 * NCW + 1), MINB) ws_kernel(
+    Layout L, KC<real> k, real coef1, real coef2, const __grid_constant__ CUtensorMap mapIn, real *out,
+    const real *__restrict__ vel, int Wo, int G) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int bx = Wo + 2 * kPairHalo;
+    const int in_el = ((3 * bx * (int)sizeof(real) + 127) / 128 * 128) / (int)sizeof(real);
+    const int us_el = ((6 * bx * (int)sizeof(real) + 127) / 128 * 128) / (int)sizeof(real);
+    unsigned char *base_sm = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
+    real *ring = reinterpret_cast<real *>(base_sm);
+    real *usr = ring + (size_t)SI * in_el;
+    uint64_t *full_in = reinterpret_cast<uint64_t *>(usr + (size_t)SU * us_el + 64);
+    uint64_t *empty_in = full_in + SI;
+    uint64_t *us_full = empty_in + SI;
+    uint64_t *us_empty = us_full + SU;
+    double *etab = reinterpret_cast<double *>(us_empty + SU);
+    load_exp_table(etab);
+
+    const int t = threadIdx.x;
+    const int warp = t >> 5, lane = t & 31;
+    if (t == 0) {
+        for (int q = 0; q < SI; ++q) {
+            mbar_init(&full_in[q], 1);
+            mbar_init(&empty_in[q], NCW);
+        }
+        for (int q = 0; q < SU; ++q) {
+            mbar_init(&us_full[q], NCW);
+            mbar_init(&us_empty[q], NCW);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    const int nx = L.nx;
+    const Sched sch = make_sched(L, Wo, G);
+    const uint32_t box_bytes = (uint32_t)(3 * bx * sizeof(real));
+    constexpr int LEAD = 4, TRAIL = 4;
+    const unsigned FULL = 0xffffffffu;
+
+    if (warp == 2 * NCW) {
+        // ------------------------------- producer -------------------------------
+        if (lane != 0) return;
+        prefetch_tmap(&mapIn);
+        uint32_t g = 0;
+        int64_t pos = sch.lo;
+        Seg sg;
+        while (next_seg(L, Wo, sch, pos, sg)) {
+            const int n = sg.yb - sg.ya + LEAD + TRAIL;
+            const int bxs = sg.x0 - kPairHalo + L.gx;
+            for (int j = 0; j < n; ++j, ++g) {
+                const int slot = g % SI;
+                if (g >= (uint32_t)SI) mbar_wait(&empty_in[slot], ((g / SI) - 1) & 1u);
+                mbar_expect_tx(&full_in[slot], box_bytes);
+                tma_load_3d(ring + slot * in_el, &mapIn, bxs, sg.ya - LEAD + j + 2, 3 * sg.m, &full_in[slot]);
+            }
+        }
+        return;
+    }
+
+    if (warp < NCW) {
+        // --------------------------- stage-1 warps ------------------------------
+        const int cx = kPairCols * warp + 2 * lane - 4;       // strip column of the lane's left column
+        const int ci = kPairHalo + cx;
+        const bool wr = lane >= 1 && lane <= 30;               // writes u* columns [60 w - 2, 60 w + 58)
+        int sidx = 0, uidx = 0;
+        uint32_t par = 0, upar = 0;
+        uint32_t ucount = 0;
+        int64_t pos = sch.lo;
+        Seg sg;
+        while (next_seg(L, Wo, sch, pos, sg)) {
+            const int n = sg.yb - sg.ya + LEAD + TRAIL;
+            const real vx = vel[kMembStride * sg.m], vy = vel[kMembStride * sg.m + 1];
+            const Mob<real> mo = MOB == 2 ? load_mob(vel, sg.m) : Mob<real>{};
+            real A1x = 0, A1y = 0, A2x = 0, A2y = 0, M1x = 0, M1y = 0, M2x = 0, M2y = 0;
+            real B1x = 0, B1y = 0, B2x = 0, B2y = 0, B3x = 0, B3y = 0, P3x = 0, P3y = 0, R3x = 0, R3y = 0;
+            real Fsx = 0, Fsy = 0;
+            const real *r1 = nullptr, *r2 = nullptr;
+            for (int i = 0; i < n; ++i) {
+                const real *r0 = ring + sidx * in_el + ci;
+                mbar_wait(&full_in[sidx], par);
+                if (i >= 2) {
+                    const auto c0 = ld2(r0), c1 = ld2(r1), c2 = ld2(r2);
+                    const auto p0 = ld2(r0 + bx), p1 = ld2(r1 + bx), p2 = ld2(r2 + bx);
+                    const auto q1 = ld2(r1 + 2 * bx), q2 = ld2(r2 + 2 * bx);
+                    const real cw1 = __shfl_up_sync(FULL, c1.y, 1), ce1 = __shfl_down_sync(FULL, c1.x, 1);
+                    const real pw1 = __shfl_up_sync(FULL, p1.y, 1), pe1 = __shfl_down_sync(FULL, p1.x, 1);
+                    const real pw2 = __shfl_up_sync(FULL, p2.y, 1), pe2 = __shfl_down_sync(FULL, p2.x, 1);
+                    const real rw2 = __shfl_up_sync(FULL, q2.y, 1), re2 = __shfl_down_sync(FULL, q2.x, 1);
+                    A2x = A1x; A2y = A1y; M2x = M1x; M2y = M1y;
+                    B3x = B2x; B3y = B2y; B2x = B1x; B2y = B1y;
+                    constitutive<real, MOB, FE>(k, mo, etab, c1.x, p1.x, cw1, c1.y, c2.x, c0.x, pw1, p1.y, p2.x,
+                                                p0.x, A1x, B1x, M1x);
+                    constitutive<real, MOB, FE>(k, mo, etab, c1.y, p1.y, c1.x, ce1, c2.y, c0.y, p1.x, pe1, p2.y,
+                                                p0.y, A1y, B1y, M1y);
+                    const real An = __shfl_down_sync(FULL, A2x, 1), Mn = __shfl_down_sync(FULL, M2x, 1);
+                    const real Bn = __shfl_down_sync(FULL, B2x, 1), Bp = __shfl_up_sync(FULL, B2y, 1);
+                    const real fex = face_flux<real>(M2x, M2y, A2x, A2y);
+                    const real fey = face_flux<real>(M2y, Mn, A2y, An);
+                    const real fwx = __shfl_up_sync(FULL, fey, 1);
+                    const real fnx = face_flux<real>(M2x, M1x, A2x, A1x);
+                    const real fny = face_flux<real>(M2y, M1y, A2y, A1y);
+                    real csx, psx, rsx, csy, psy, rsy;
+                    KC<real> k1 = k;
+                    k1.coef = coef1;
+                    cell_update<real>(k1, vx, vy, fex, fwx, fnx, Fsx, B2x, Bp, B2y, B3x, B1x, pw2, p2.y, P3x, p1.x,
+                                      q2.x, rw2, q2.y, R3x, q1.x, c2.x, p2.x, q2.x, csx, psx, rsx);
+                    cell_update<real>(k1, vx, vy, fey, fex, fny, Fsy, B2y, B2x, Bn, B3y, B1y, p2.x, pe2, P3y, p1.y,
+                                      q2.y, q2.x, re2, R3y, q1.y, c2.y, p2.y, q2.y, csy, psy, rsy);
+                    Fsx = fnx; Fsy = fny;
+                    P3x = p2.x; P3y = p2.y; R3x = q2.x; R3y = q2.y;
+                    if (i >= LEAD) {          // u* row k-2 (and its base u^n row) into the u* ring
+                        if (ucount >= (uint32_t)SU) mbar_wait(&us_empty[uidx], upar ^ 1u);
+                        if (wr) {
+                            real *u = usr + uidx * us_el + ci;
+                            st2(u, csx, csy);
+                            st2(u + bx, psx, psy);
+                            st2(u + 2 * bx, rsx, rsy);
+                            st2(u + 3 * bx, c2.x, c2.y);
+                            st2(u + 4 * bx, p2.x, p2.y);
+                            st2(u + 5 * bx, q2.x, q2.y);
+                        }
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&us_full[uidx]);
+                        ++ucount;
+                        if (++uidx == SU) { uidx = 0; upar ^= 1u; }
+                    }
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&empty_in[sidx >= 2 ? sidx - 2 : sidx - 2 + SI]);   // row k-2 done
+                }
+                r2 = r1; r1 = r0;
+                if (++sidx == SI) { sidx = 0; par ^= 1u; }
+            }
+            __syncwarp();
+            if (lane == 0) {   // rows k-1, k of the segment's last iteration
+                mbar_arrive(&empty_in[sidx >= 1 ? sidx - 1 : sidx - 1 + SI]);
+                mbar_arrive(&empty_in[sidx >= 2 ? sidx - 2 : sidx - 2 + SI]);
+            }
+        }
+        return;
+    }
+
+    // --------------------------- stage-2 warps ---------------------------------
+    const int w2 = warp - NCW;
+    const int cx = kPairCols * w2 + 2 * lane - 2;
+    const int ci = kPairHalo + cx;
+    int uidx = 0;
+    uint32_t upar = 0;
+    int64_t pos = sch.lo;
+    Seg sg;
+    while (next_seg(L, Wo, sch, pos, sg)) {
+        const int n = sg.yb - sg.ya + 4;                 // u* rows ya-2 .. yb+1
+        const int x = sg.x0 + cx;
+        const bool store = lane >= 1 && lane <= 30 && cx < sg.Wp;
+        const bool xedge = (x < L.gx) | (x + 1 >= nx - L.gx);
+        real *ob = out + sg.m * L.mstride;
+        const real vx = vel[kMembStride * sg.m], vy = vel[kMembStride * sg.m + 1];
+        const Mob<real> mo = MOB == 2 ? load_mob(vel, sg.m) : Mob<real>{};
+        real A1x = 0, A1y = 0, A2x = 0, A2y = 0, M1x = 0, M1y = 0, M2x = 0, M2y = 0;
+        real B1x = 0, B1y = 0, B2x = 0, B2y = 0, B3x = 0, B3y = 0, P3x = 0, P3y = 0, R3x = 0, R3y = 0;
+        real Fsx = 0, Fsy = 0;
+        const real *r1 = nullptr, *r2 = nullptr;
+        for (int i = 0; i < n; ++i) {
+            const real *r0 = usr + uidx * us_el + ci;    // u* row q = ya - 2 + i
+            mbar_wait(&us_full[uidx], upar);
+            if (i >= 2) {
+                const int q = sg.ya - 2 + i;
+                const int gq = L.y0 + q - 1, gu = L.y0 + q - 2;   // global rows of mu2 and of the update
+                const bool qbot = gq == 0, qtop = gq == L.ny - 1, ubot = gu == 0, utop = gu == L.ny - 1;
+                const auto c0 = ld2(r0), c1 = ld2(r1), c2 = ld2(r2);
+                const auto p0 = ld2(r0 + bx), p1 = ld2(r1 + bx), p2 = ld2(r2 + bx);
+                const auto q1 = ld2(r1 + 2 * bx), q2 = ld2(r2 + 2 * bx);
+                const real cw1 = __shfl_up_sync(FULL, c1.y, 1), ce1 = __shfl_down_sync(FULL, c1.x, 1);
+                const real pw1 = __shfl_up_sync(FULL, p1.y, 1), pe1 = __shfl_down_sync(FULL, p1.x, 1);
+                const real pw2 = __shfl_up_sync(FULL, p2.y, 1), pe2 = __shfl_down_sync(FULL, p2.x, 1);
+                const real rw2 = __shfl_up_sync(FULL, q2.y, 1), re2 = __shfl_down_sync(FULL, q2.x, 1);
+                // mu2 at row q-1: its down / up neighbour rows are mirrors at the global boundaries
+                const real cdx = qbot ? c1.x : c2.x, cdy = qbot ? c1.y : c2.y, cux = qtop ? c1.x : c0.x,
+                           cuy = qtop ? c1.y : c0.y;
+                const real pdx = qbot ? p1.x : p2.x, pdy = qbot ? p1.y : p2.y, pux = qtop ? p1.x : p0.x,
+                           puy = qtop ? p1.y : p0.y;
+                A2x = A1x; A2y = A1y; M2x = M1x; M2y = M1y;
+                B3x = B2x; B3y = B2y; B2x = B1x; B2y = B1y;
+                constitutive<real, MOB, FE>(k, mo, etab, c1.x, p1.x, cw1, c1.y, cdx, cux, pw1, p1.y, pdx, pux, A1x,
+                                            B1x, M1x);
+                constitutive<real, MOB, FE>(k, mo, etab, c1.y, p1.y, c1.x, ce1, cdy, cuy, p1.x, pe1, pdy, puy, A1y,
+                                            B1y, M1y);
+                const real An = __shfl_down_sync(FULL, A2x, 1), Mn = __shfl_down_sync(FULL, M2x, 1);
+                const real Bn = __shfl_down_sync(FULL, B2x, 1), Bp = __shfl_up_sync(FULL, B2y, 1);
+                const real fex = face_flux<real>(M2x, M2y, A2x, A2y);
+                const real fey = face_flux<real>(M2y, Mn, A2y, An);
+                const real fwx = __shfl_up_sync(FULL, fey, 1);
+                real fnx = face_flux<real>(M2x, M1x, A2x, A1x), fny = face_flux<real>(M2y, M1y, A2y, A1y);
+                if (utop) { fnx = real(0); fny = real(0); }
+                const real fsx = ubot ? real(0) : Fsx, fsy = ubot ? real(0) : Fsy;
+                Fsx = fnx; Fsy = fny;
+                const real qdx = ubot ? B2x : B3x, qdy = ubot ? B2y : B3y;
+                const real qux = utop ? B2x : B1x, quy = utop ? B2y : B1y;
+                const real phdx = ubot ? p2.x : P3x, phdy = ubot ? p2.y : P3y;
+                const real phux = utop ? p2.x : p1.x, phuy = utop ? p2.y : p1.y;
+                const auto rt = ld2(r1 + 5 * bx);            // base rho of row q-1: the reservoir if utop
+                const real rdx = ubot ? q2.x : R3x, rdy = ubot ? q2.y : R3y;
+                const real rux = utop ? rt.x : q1.x, ruy = utop ? rt.y : q1.y;
+                const auto b0 = ld2(r2 + 3 * bx), b1 = ld2(r2 + 4 * bx), b2 = ld2(r2 + 5 * bx);   // u^n row q-2
+                KC<real> k2 = k;
+                k2.coef = coef2;
+                real ocx, opx, orx, ocy, opy, ory;
+                cell_update<real>(k2, vx, vy, fex, fwx, fnx, fsx, B2x, Bp, B2y, qdx, qux, pw2, p2.y, phdx, phux,
+                                  q2.x, rw2, q2.y, rdx, rux, b0.x, b1.x, b2.x, ocx, opx, orx);
+                cell_update<real>(k2, vx, vy, fey, fex, fny, fsy, B2y, B2x, Bn, qdy, quy, p2.x, pe2, phdy, phuy,
+                                  q2.y, q2.x, re2, rdy, ruy, b0.y, b1.y, b2.y, ocy, opy, ory);
+                P3x = p2.x; P3y = p2.y; R3x = q2.x; R3y = q2.y;
+                const int r = q - 2;
+                if (store && r >= sg.ya && r < sg.yb) {
+                    const bool edge = xedge | (L.y0 + r <= 1) | (L.y0 + r >= L.ny - 2);
+                    if (!edge) {
+                        real *o = ob + L.at(r, x);
+                        st2(o, ocx, ocy);
+                        st2(o + L.fstride, opx, opy);
+                        st2(o + 2 * L.fstride, orx, ory);
+                    } else {
+                        store_with_ghosts<real>(L, ob, 0, r, x, ocx);
+                        store_with_ghosts<real>(L, ob + L.fstride, 1, r, x, opx);
+                        store_with_ghosts<real>(L, ob + 2 * L.fstride, 2, r, x, orx);
+                        store_with_ghosts<real>(L, ob, 0, r, x + 1, ocy);
+                        store_with_ghosts<real>(L, ob + L.fstride, 1, r, x + 1, opy);
+                        store_with_ghosts<real>(L, ob + 2 * L.fstride, 2, r, x + 1, ory);
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&us_empty[uidx >= 2 ? uidx - 2 : uidx - 2 + SU]);   // row q-2 done
+            }
+            r2 = r1; r1 = r0;
+            if (++uidx == SU) { uidx = 0; upar ^= 1u; }
+        }
+        __syncwarp();
+        if (lane == 0) {
+            mbar_arrive(&us_empty[uidx >= 1 ? uidx - 1 : uidx - 1 + SU]);
+            mbar_arrive(&us_empty[uidx >= 2 ? uidx - 2 : uidx - 2 + SU]);
+        }
+    }
+}
+
 template <typename real>
 KC<real> make_kc(const Coef &K, double coef) {
     KC<real> k;
@@ -1298,6 +1555,76 @@ cudaError_t launch_fused_t(const Layout &L, const StreamPlan &P, const KC<real> 
     }
 }
 
+// Warp-specialised step kernel: NCW stage-1 + NCW stage-2 warps + 1 producer per block.
+template <typename real, int NCW>
+struct WsCfg {
+    static constexpr int minb = NCW <= 2 ? 3 : 2;
+    static constexpr int SI = 8, SU = 6;
+};
+
+template <typename real>
+size_t ws_smem_bytes(int bx, int SI, int SU) {
+    const size_t in_b = (3 * bx * sizeof(real) + 127) / 128 * 128, us_b = (6 * bx * sizeof(real) + 127) / 128 * 128;
+    return 128 + SI * in_b + SU * us_b + 64 * sizeof(real) + (size_t)(2 * SI + 2 * SU) * 8 + 64 * 8;
+}
+
+template <typename real, int NCW, int MOB, int FE>
+cudaError_t launch_ws_k(const Layout &L, const StreamPlan &P, const KC<real> &k, real c1, real c2, real *out,
+                        const real *vel, cudaStream_t s) {
+    using C = WsCfg<real, NCW>;
+    const size_t smem = ws_smem_bytes<real>(P.fbox, C::SI, C::SU);
+    static int occ = -1, nsm = 0;
+    static size_t smem_set = 0;
+    auto kern = ws_kernel<real, NCW, C::SI, C::SU, MOB, FE, C::minb>;
+    const int threads = 32 * (2 * NCW + 1);
+    if (smem > smem_set) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        smem_set = smem;
+        occ = -1;
+    }
+    if (occ < 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
+        if (e != cudaSuccess) return e;
+        if (occ < 1) occ = 1;
+    }
+    const int64_t T = (int64_t)L.members * (L.r1 - L.r0);
+    const int64_t minrows = 24;
+    int64_t B = (int64_t)occ * nsm;
+    int64_t G = B / P.fstrips;
+    if (G > (T + minrows - 1) / minrows) G = (T + minrows - 1) / minrows;
+    if (G >= 4) {
+        B = G * P.fstrips;
+    } else {
+        G = 0;
+        const int64_t R_ = (int64_t)L.members * P.fstrips * (L.r1 - L.r0);
+        if (B > (R_ + minrows - 1) / minrows) B = (R_ + minrows - 1) / minrows;
+    }
+    if (B < 1) B = 1;
+    kern<<<(unsigned)B, threads, smem, s>>>(L, k, c1, c2, P.fmapU, out, vel, P.fWo, (int)G);
+    return cudaGetLastError();
+}
+
+template <typename real, int NCW>
+cudaError_t launch_ws_n(const Layout &L, const StreamPlan &P, const KC<real> &k, real c1, real c2, real *out,
+                        const real *vel, cudaStream_t s) {
+    if (k.fe == 1) {
+        switch (k.mob) {
+            case 0: return launch_ws_k<real, NCW, 0, 1>(L, P, k, c1, c2, out, vel, s);
+            case 1: return launch_ws_k<real, NCW, 1, 1>(L, P, k, c1, c2, out, vel, s);
+            default: return launch_ws_k<real, NCW, 2, 1>(L, P, k, c1, c2, out, vel, s);
+        }
+    }
+    switch (k.mob) {
+        case 0: return launch_ws_k<real, NCW, 0, 0>(L, P, k, c1, c2, out, vel, s);
+        case 1: return launch_ws_k<real, NCW, 1, 0>(L, P, k, c1, c2, out, vel, s);
+        default: return launch_ws_k<real, NCW, 2, 0>(L, P, k, c1, c2, out, vel, s);
+    }
+}
+
 cudaError_t upload_exp_table() {
     static bool done = false;
     if (done) return cudaSuccess;
@@ -1342,7 +1669,7 @@ cudaError_t make_stream_plan(int precision, const Layout &L, void *U, void *Us, 
     P = StreamPlan();
     if (L.path == 1 || !stream_eligible(L)) return cudaSuccess;
     const int HL = precision == 0 ? 2 : 4;       // stream-kernel box halo: 16 B of columns
-    if (L.path == 3 || L.path == 0 || L.path == 4) {
+    if (L.path == 3 || L.path == 0 || L.path == 4 || L.path == 5) {
         // pair kernel: strips of Wo <= 240 columns (box Wo + 8 <= 256 elements), Wo a multiple of
         // 4 (16 B rows for fp32 too), split nx evenly; 60 output columns per compute warp
         int strips = (L.nx + 239) / 240;
@@ -1376,6 +1703,27 @@ cudaError_t make_stream_plan(int precision, const Layout &L, void *U, void *Us, 
             !encode_map(&P.mapUs[ri], precision, L, Us, P.box_x, ri ? 4 : 2))
             return cudaErrorInvalidValue;
     P.ok = true;
+    if (L.path == 5) {
+        // warp-specialised step kernel: strips of 60 NCW - 4 columns (stage-1 warps cover the strip
+        // plus 2 columns of u* on each side), NCW in {2, 3} for the least idle columns
+        static const int force = env_int("PF_WS_NCW", 0);
+        int best = 3;
+        if (force == 2 || force == 3) {
+            best = force;
+        } else {
+            const int w3 = kPairCols * 3 - 4, w2 = kPairCols * 2 - 4;
+            const int i3 = (L.nx + w3 - 1) / w3 * w3 - L.nx, i2 = (L.nx + w2 - 1) / w2 * w2 - L.nx;
+            best = (i2 + L.nx / 40 < i3) ? 2 : 3;
+        }
+        P.fncw = best;
+        P.fWo = kPairCols * best - 4;
+        P.fstrips = (L.nx + P.fWo - 1) / P.fWo;
+        P.fbox = P.fWo + 2 * kPairHalo;
+        if (!encode_map(&P.fmapU, precision, L, U, P.fbox, 1) || !encode_map(&P.fmapUs, precision, L, Us, P.fbox, 1))
+            return cudaErrorInvalidValue;
+        P.fused = true;
+        P.ws = true;
+    }
     if (L.path == 4) {
         // fused kernel: strips of 56 NCW columns, NCW for the least idle columns (ties: wider)
         int best = 1, waste = 1 << 30;
@@ -1401,6 +1749,16 @@ cudaError_t launch_fused(int precision, const Layout &L, const StreamPlan &P, co
     cudaError_t te = upload_exp_table();
     if (te != cudaSuccess) return te;
     if (!P.fused) return cudaErrorInvalidValue;
+    if (P.ws) {
+        if (precision == 0) {
+            const KC<double> kd = make_kc<double>(K, 0.5 * dt);
+            return P.fncw == 2 ? launch_ws_n<double, 2>(L, P, kd, 0.5 * dt, dt, (double *)out, (const double *)vel, s)
+                               : launch_ws_n<double, 3>(L, P, kd, 0.5 * dt, dt, (double *)out, (const double *)vel, s);
+        }
+        const KC<float> kf = make_kc<float>(K, 0.5 * dt);
+        return P.fncw == 2 ? launch_ws_n<float, 2>(L, P, kf, (float)(0.5 * dt), (float)dt, (float *)out, (const float *)vel, s)
+                           : launch_ws_n<float, 3>(L, P, kf, (float)(0.5 * dt), (float)dt, (float *)out, (const float *)vel, s);
+    }
     if (precision == 0)
         return launch_fused_t<double>(L, P, make_kc<double>(K, 0.5 * dt), 0.5 * dt, dt, (double *)out, (const double *)vel, s);
     return launch_fused_t<float>(L, P, make_kc<float>(K, 0.5 * dt), (float)(0.5 * dt), (float)dt, (float *)out,

@@ -251,3 +251,17 @@ def test_fused_step_kernel_bitwise(nx, ny, members, extra):
     b = _run(p.replace(kernel_path=4), 7)
     for m in range(members):
         assert _eq(a[m], b[m]), m
+
+
+@pytest.mark.parametrize("nx,ny,members,extra", [(128, 40, 2, {}), (512, 72, 2, {}), (96, 64, 3, dict(noise_rho=0.2)),
+                                                  (1000, 24, 1, {}), (200, 48, 2, dict(fe_model=1, omega=2.2,
+                                                                                     temp_rs=0.45, dt=4e-4))])
+def test_warp_specialised_step_kernel_bitwise(nx, ny, members, extra):
+    """The experimental warp-specialised step kernel (kernel_path 5: stage-1 warps hand u* to
+    stage-2 warps through a shared-memory ring, one HBM pass per step) gives the same bits as the
+    two-stage pair kernel."""
+    p = _base(nx, ny, n_members=members, rate_lo=0.5, rate_hi=2.0, **extra)
+    a = _run(p.replace(kernel_path=3), 7)
+    b = _run(p.replace(kernel_path=5), 7)
+    for m in range(members):
+        assert _eq(a[m], b[m]), m
