@@ -14,6 +14,7 @@ template <typename real>
 struct KC {                    // coefficients folded into the compute precision
     real half_inv_dx2, inv_2dx, m_kc_dx2, m_kp_dx2, W_c, W2c, W2p;   // m_ = negated
     real two_inv_sigma, Mp_dx2, Dr_dx2, rho_in, coef;
+    real coefc;                // coef / (2 dx^2): the composition update's factor (R_c folded in)
     real MBb, dMb, MBs, dMs;   // mobilities shared by all members (MOB 0, 1)
     real omega, temp;          // regular-solution composition energy (FE 1, R-28)
     int fe;                    // 0 polynomial composition well (R-2), 1 regular solution (R-28)
@@ -140,6 +141,13 @@ __device__ __forceinline__ void constitutive(const KC<real> &k, const Mob<real> 
     M = fma_(e, sub_(ms, mb), mb);
 }
 
+// The member's velocity divided by 2 dx, the form cell_update takes (central differences G, R-8).
+template <typename real>
+__device__ __forceinline__ void scaled_velocity(const KC<real> &k, const real *vel, int m, real &vx, real &vy) {
+    vx = mul_(vel[(int64_t)m * kMembStride], k.inv_2dx);
+    vy = mul_(vel[(int64_t)m * kMembStride + 1], k.inv_2dx);
+}
+
 // Face flux (M_a + M_b) (mu_b - mu_a) of the face between cells a and b (times 2/dx^2 of the
 // flux F = (M_a + M_b)/2 (mu_b - mu_a)/dx^2).  The same expression is used for a face
 // seen from either of its cells, so the divergence telescopes (exact mass conservation).
@@ -155,6 +163,7 @@ __device__ __forceinline__ real face_flux(real Ma, real Mb, real mua, real mub) 
 //   R_phi = M_phi L(mu_phi) + S                                    (R-7)
 //   R_rho = D_rho L(rho) - v . G(rho) - S                          (R-9)
 //   out   = base + coef R                                          (R-11)
+// vx, vy are the member's velocity divided by 2 dx (folded once per segment, see scaled_velocity).
 template <typename real>
 __device__ __forceinline__ void cell_update(const KC<real> &k, real vx, real vy,
                                             real fe, real fw, real fn, real fs,
@@ -164,14 +173,14 @@ __device__ __forceinline__ void cell_update(const KC<real> &k, real vx, real vy,
                                             real bc, real bp, real br,
                                             real &oc, real &op, real &orr) {
     const real m4 = real(-4);
-    const real Rc = mul_(add_(sub_(fe, fw), sub_(fn, fs)), k.half_inv_dx2);
+    const real Rc2 = add_(sub_(fe, fw), sub_(fn, fs));                      // 2 dx^2 R_c
     const real lq = fma_(q0, m4, add_(add_(ql, qr), add_(qd, qu)));          // dx^2 L(mu_phi)
-    const real S = mul_(r0, mul_(fma_(vx, sub_(pr, pl), mul_(vy, sub_(pu, pd))), k.inv_2dx));
+    const real S = mul_(r0, fma_(vx, sub_(pr, pl), mul_(vy, sub_(pu, pd))));
     const real Rp = fma_(lq, k.Mp_dx2, S);
     const real lr = fma_(r0, m4, add_(add_(rl, rr), add_(rd, ru)));          // dx^2 L(rho)
-    const real adv = mul_(fma_(vx, sub_(rr, rl), mul_(vy, sub_(ru, rd))), k.inv_2dx);
+    const real adv = fma_(vx, sub_(rr, rl), mul_(vy, sub_(ru, rd)));
     const real Rr = sub_(fma_(lr, k.Dr_dx2, -adv), S);
-    oc = fma_(Rc, k.coef, bc);
+    oc = fma_(Rc2, k.coefc, bc);
     op = fma_(Rp, k.coef, bp);
     orr = fma_(Rr, k.coef, br);
 }

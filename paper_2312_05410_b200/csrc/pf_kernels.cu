@@ -117,7 +117,8 @@ __global__ void __launch_bounds__(NT) stage_kernel(Layout L, KC<real> k, const r
     __syncthreads();
 
     // ---- phase 2: fluxes, source, vapour, update ----
-    const real vx = vel[kMembStride * m], vy = vel[kMembStride * m + 1];
+    real vx, vy;
+    scaled_velocity(k, vel, m, vx, vy);
     const int lx = threadIdx.x & (BX - 1);
     const int gx = tx0 + lx;
     for (int q = threadIdx.x / BX; q < BY; q += NT / BX) {
@@ -572,7 +573,8 @@ __global__ void __launch_bounds__(32 * NCW + 32, MINB) stream_kernel(
         const int x = sg.x0 + cx;           // global column of this lane
         const bool store = lane >= 1 && lane <= 30 && cx < sg.Wp;
         real *ob = out + sg.m * L.mstride;
-        const real vx = vel[kMembStride * sg.m], vy = vel[kMembStride * sg.m + 1];
+        real vx, vy;
+        scaled_velocity(k, vel, sg.m, vx, vy);
         const Mob<real> mo = MOB == 2 ? load_mob(vel, sg.m) : Mob<real>{};
 
         real c_m2 = 0, c_m1 = 0, c_0 = 0;                 // c rows k-2, k-1, k (own column)
@@ -748,7 +750,8 @@ __global__ void __launch_bounds__(32 * NCW + 32, MINB) pair_kernel(
         const bool store = lane >= 1 && lane <= 30 && cx < sg.Wp;
         const bool xedge = (x < L.gx) | (x + 1 >= nx - L.gx);
         real *ob = out + sg.m * L.mstride;
-        const real vx = vel[kMembStride * sg.m], vy = vel[kMembStride * sg.m + 1];
+        real vx, vy;
+        scaled_velocity(k, vel, sg.m, vx, vy);
         const Mob<real> mo = MOB == 2 ? load_mob(vel, sg.m) : Mob<real>{};
 
         real A1x = 0, A1y = 0, A2x = 0, A2y = 0;          // mu_c rows k-1, k-2
@@ -864,7 +867,7 @@ constexpr int kFusedHalo = 4;    // box columns left of the strip (and right of 
 
 template <typename real, int NCW, int S, int MOB, int FE, int MINB>
 __global__ void __launch_bounds__(32 * NCW + 32, MINB) fused_kernel(
-    Layout L, KC<real> k, real coef1, real coef2, const __grid_constant__ CUtensorMap mapIn, real *out,
+    Layout L, KC<real> k, KC<real> k2, const __grid_constant__ CUtensorMap mapIn, real *out,
     const real *__restrict__ vel, int Wo, int G) {
     static_assert(S >= 8, "rows k .. k-4 are read from the ring, plus prefetch");
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -930,7 +933,8 @@ __global__ void __launch_bounds__(32 * NCW + 32, MINB) fused_kernel(
         const bool store = lane >= 2 && lane <= 29 && cx < sg.Wp;
         const bool xedge = (x < L.gx) | (x + 1 >= nx - L.gx);
         real *ob = out + sg.m * L.mstride;
-        const real vx = vel[kMembStride * sg.m], vy = vel[kMembStride * sg.m + 1];
+        real vx, vy;
+        scaled_velocity(k, vel, sg.m, vx, vy);
         const Mob<real> mo = MOB == 2 ? load_mob(vel, sg.m) : Mob<real>{};
         // stage 1 windows (rows of u^n's mu / M): as in the pair kernel
         real A1x = 0, A1y = 0, A2x = 0, A2y = 0, M1x = 0, M1y = 0, M2x = 0, M2y = 0;
@@ -975,11 +979,9 @@ __global__ void __launch_bounds__(32 * NCW + 32, MINB) fused_kernel(
                 Cs4x = Cs3x; Cs4y = Cs3y; Cs3x = Cs2x; Cs3y = Cs2y;
                 Ps5x = Ps4x; Ps5y = Ps4y; Ps4x = Ps3x; Ps4y = Ps3y; Ps3x = Ps2x; Ps3y = Ps2y;
                 Rs5x = Rs4x; Rs5y = Rs4y; Rs4x = Rs3x; Rs4y = Rs3y; Rs3x = Rs2x; Rs3y = Rs2y;
-                KC<real> k1 = k;
-                k1.coef = coef1;
-                cell_update<real>(k1, vx, vy, fex, fwx, fnx, Fsx, B2x, Bp, B2y, B3x, B1x, pw2, p2.y, P3x, p1.x, q2.x,
+                cell_update<real>(k, vx, vy, fex, fwx, fnx, Fsx, B2x, Bp, B2y, B3x, B1x, pw2, p2.y, P3x, p1.x, q2.x,
                                   rw2, q2.y, R3x, q1.x, c2.x, p2.x, q2.x, Cs2x, Ps2x, Rs2x);
-                cell_update<real>(k1, vx, vy, fey, fex, fny, Fsy, B2y, B2x, Bn, B3y, B1y, p2.x, pe2, P3y, p1.y, q2.y,
+                cell_update<real>(k, vx, vy, fey, fex, fny, Fsy, B2y, B2x, Bn, B3y, B1y, p2.x, pe2, P3y, p1.y, q2.y,
                                   q2.x, re2, R3y, q1.y, c2.y, p2.y, q2.y, Cs2y, Ps2y, Rs2y);
                 Fsx = fnx; Fsy = fny;
                 P3x = p2.x; P3y = p2.y; R3x = q2.x; R3y = q2.y;
@@ -1022,8 +1024,6 @@ __global__ void __launch_bounds__(32 * NCW + 32, MINB) fused_kernel(
                 const real pw4 = __shfl_up_sync(FULL, Ps4y, 1), pe4 = __shfl_down_sync(FULL, Ps4x, 1);
                 const real rw4 = __shfl_up_sync(FULL, Rs4y, 1), re4 = __shfl_down_sync(FULL, Rs4x, 1);
                 const auto b0 = ld2(r4), b1 = ld2(r4 + plane), b2 = ld2(r4 + 2 * plane);   // u^n row k-4
-                KC<real> k2 = k;
-                k2.coef = coef2;
                 real ocx, opx, orx, ocy, opy, ory;
                 cell_update<real>(k2, vx, vy, fex, fwx, fnx, fsx, E2x, Bp, E2y, qdx, qux, pw4, Ps4y, phdx, phux, Rs4x,
                                   rw4, Rs4y, rdx, rux, b0.x, b1.x, b2.x, ocx, opx, orx);
@@ -1080,7 +1080,7 @@ __global__ void __launch_bounds__(32 * NCW + 32, MINB) fused_kernel(
 // the stage kernels.  Single-domain contexts only.
 template <typename real, int NCW, int SI, int SU, int MOB, int FE, int MINB>
 __global__ void __launch_bounds__(32 * (2 * NCW + 1), MINB) ws_kernel(
-    Layout L, KC<real> k, real coef1, real coef2, const __grid_constant__ CUtensorMap mapIn, real *out,
+    Layout L, KC<real> k, KC<real> k2, const __grid_constant__ CUtensorMap mapIn, real *out,
     const real *__restrict__ vel, int Wo, int G) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int bx = Wo + 2 * kPairHalo;
@@ -1149,7 +1149,8 @@ __global__ void __launch_bounds__(32 * (2 * NCW + 1), MINB) ws_kernel(
         Seg sg;
         while (next_seg(L, Wo, sch, pos, sg)) {
             const int n = sg.yb - sg.ya + LEAD + TRAIL;
-            const real vx = vel[kMembStride * sg.m], vy = vel[kMembStride * sg.m + 1];
+            real vx, vy;
+        scaled_velocity(k, vel, sg.m, vx, vy);
             const Mob<real> mo = MOB == 2 ? load_mob(vel, sg.m) : Mob<real>{};
             real A1x = 0, A1y = 0, A2x = 0, A2y = 0, M1x = 0, M1y = 0, M2x = 0, M2y = 0;
             real B1x = 0, B1y = 0, B2x = 0, B2y = 0, B3x = 0, B3y = 0, P3x = 0, P3y = 0, R3x = 0, R3y = 0;
@@ -1180,11 +1181,9 @@ __global__ void __launch_bounds__(32 * (2 * NCW + 1), MINB) ws_kernel(
                     const real fnx = face_flux<real>(M2x, M1x, A2x, A1x);
                     const real fny = face_flux<real>(M2y, M1y, A2y, A1y);
                     real csx, psx, rsx, csy, psy, rsy;
-                    KC<real> k1 = k;
-                    k1.coef = coef1;
-                    cell_update<real>(k1, vx, vy, fex, fwx, fnx, Fsx, B2x, Bp, B2y, B3x, B1x, pw2, p2.y, P3x, p1.x,
+                    cell_update<real>(k, vx, vy, fex, fwx, fnx, Fsx, B2x, Bp, B2y, B3x, B1x, pw2, p2.y, P3x, p1.x,
                                       q2.x, rw2, q2.y, R3x, q1.x, c2.x, p2.x, q2.x, csx, psx, rsx);
-                    cell_update<real>(k1, vx, vy, fey, fex, fny, Fsy, B2y, B2x, Bn, B3y, B1y, p2.x, pe2, P3y, p1.y,
+                    cell_update<real>(k, vx, vy, fey, fex, fny, Fsy, B2y, B2x, Bn, B3y, B1y, p2.x, pe2, P3y, p1.y,
                                       q2.y, q2.x, re2, R3y, q1.y, c2.y, p2.y, q2.y, csy, psy, rsy);
                     Fsx = fnx; Fsy = fny;
                     P3x = p2.x; P3y = p2.y; R3x = q2.x; R3y = q2.y;
@@ -1233,7 +1232,8 @@ __global__ void __launch_bounds__(32 * (2 * NCW + 1), MINB) ws_kernel(
         const bool store = lane >= 1 && lane <= 30 && cx < sg.Wp;
         const bool xedge = (x < L.gx) | (x + 1 >= nx - L.gx);
         real *ob = out + sg.m * L.mstride;
-        const real vx = vel[kMembStride * sg.m], vy = vel[kMembStride * sg.m + 1];
+        real vx, vy;
+        scaled_velocity(k, vel, sg.m, vx, vy);
         const Mob<real> mo = MOB == 2 ? load_mob(vel, sg.m) : Mob<real>{};
         real A1x = 0, A1y = 0, A2x = 0, A2y = 0, M1x = 0, M1y = 0, M2x = 0, M2y = 0;
         real B1x = 0, B1y = 0, B2x = 0, B2y = 0, B3x = 0, B3y = 0, P3x = 0, P3y = 0, R3x = 0, R3y = 0;
@@ -1281,8 +1281,6 @@ __global__ void __launch_bounds__(32 * (2 * NCW + 1), MINB) ws_kernel(
                 const real rdx = ubot ? q2.x : R3x, rdy = ubot ? q2.y : R3y;
                 const real rux = utop ? rt.x : q1.x, ruy = utop ? rt.y : q1.y;
                 const auto b0 = ld2(r2 + 3 * bx), b1 = ld2(r2 + 4 * bx), b2 = ld2(r2 + 5 * bx);   // u^n row q-2
-                KC<real> k2 = k;
-                k2.coef = coef2;
                 real ocx, opx, orx, ocy, opy, ory;
                 cell_update<real>(k2, vx, vy, fex, fwx, fnx, fsx, B2x, Bp, B2y, qdx, qux, pw2, p2.y, phdx, phux,
                                   q2.x, rw2, q2.y, rdx, rux, b0.x, b1.x, b2.x, ocx, opx, orx);
@@ -1343,6 +1341,7 @@ KC<real> make_kc(const Coef &K, double coef) {
     k.Dr_dx2 = (real)K.Dr_dx2;
     k.rho_in = (real)K.rho_in;
     k.coef = (real)coef;
+    k.coefc = (real)(coef * K.half_inv_dx2);
     return k;
 }
 
@@ -1488,7 +1487,7 @@ struct FusedCfg {
 };
 
 template <typename real, int NCW, int MOB, int FE>
-cudaError_t launch_fused_k(const Layout &L, const StreamPlan &P, const KC<real> &k, real c1, real c2, real *out,
+cudaError_t launch_fused_k(const Layout &L, const StreamPlan &P, const KC<real> &k, const KC<real> &k2, real *out,
                            const real *vel, cudaStream_t s) {
     using C = FusedCfg<real, NCW>;
     const size_t smem = stream_smem_bytes<real>(P.fbox, 1, C::S, false);
@@ -1522,35 +1521,35 @@ cudaError_t launch_fused_k(const Layout &L, const StreamPlan &P, const KC<real> 
         if (B > (R_ + minrows - 1) / minrows) B = (R_ + minrows - 1) / minrows;
     }
     if (B < 1) B = 1;
-    kern<<<(unsigned)B, 32 * NCW + 32, smem, s>>>(L, k, c1, c2, P.fmapU, out, vel, P.fWo, (int)G);
+    kern<<<(unsigned)B, 32 * NCW + 32, smem, s>>>(L, k, k2, P.fmapU, out, vel, P.fWo, (int)G);
     return cudaGetLastError();
 }
 
 template <typename real, int NCW>
-cudaError_t launch_fused_n(const Layout &L, const StreamPlan &P, const KC<real> &k, real c1, real c2, real *out,
+cudaError_t launch_fused_n(const Layout &L, const StreamPlan &P, const KC<real> &k, const KC<real> &k2, real *out,
                            const real *vel, cudaStream_t s) {
     if (k.fe == 1) {
         switch (k.mob) {
-            case 0: return launch_fused_k<real, NCW, 0, 1>(L, P, k, c1, c2, out, vel, s);
-            case 1: return launch_fused_k<real, NCW, 1, 1>(L, P, k, c1, c2, out, vel, s);
-            default: return launch_fused_k<real, NCW, 2, 1>(L, P, k, c1, c2, out, vel, s);
+            case 0: return launch_fused_k<real, NCW, 0, 1>(L, P, k, k2, out, vel, s);
+            case 1: return launch_fused_k<real, NCW, 1, 1>(L, P, k, k2, out, vel, s);
+            default: return launch_fused_k<real, NCW, 2, 1>(L, P, k, k2, out, vel, s);
         }
     }
     switch (k.mob) {
-        case 0: return launch_fused_k<real, NCW, 0, 0>(L, P, k, c1, c2, out, vel, s);
-        case 1: return launch_fused_k<real, NCW, 1, 0>(L, P, k, c1, c2, out, vel, s);
-        default: return launch_fused_k<real, NCW, 2, 0>(L, P, k, c1, c2, out, vel, s);
+        case 0: return launch_fused_k<real, NCW, 0, 0>(L, P, k, k2, out, vel, s);
+        case 1: return launch_fused_k<real, NCW, 1, 0>(L, P, k, k2, out, vel, s);
+        default: return launch_fused_k<real, NCW, 2, 0>(L, P, k, k2, out, vel, s);
     }
 }
 
 template <typename real>
-cudaError_t launch_fused_t(const Layout &L, const StreamPlan &P, const KC<real> &k, real c1, real c2, real *out,
+cudaError_t launch_fused_t(const Layout &L, const StreamPlan &P, const KC<real> &k, const KC<real> &k2, real *out,
                            const real *vel, cudaStream_t s) {
     switch (P.fncw) {
-        case 1: return launch_fused_n<real, 1>(L, P, k, c1, c2, out, vel, s);
-        case 2: return launch_fused_n<real, 2>(L, P, k, c1, c2, out, vel, s);
-        case 3: return launch_fused_n<real, 3>(L, P, k, c1, c2, out, vel, s);
-        case 4: return launch_fused_n<real, 4>(L, P, k, c1, c2, out, vel, s);
+        case 1: return launch_fused_n<real, 1>(L, P, k, k2, out, vel, s);
+        case 2: return launch_fused_n<real, 2>(L, P, k, k2, out, vel, s);
+        case 3: return launch_fused_n<real, 3>(L, P, k, k2, out, vel, s);
+        case 4: return launch_fused_n<real, 4>(L, P, k, k2, out, vel, s);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -1569,7 +1568,7 @@ size_t ws_smem_bytes(int bx, int SI, int SU) {
 }
 
 template <typename real, int NCW, int MOB, int FE>
-cudaError_t launch_ws_k(const Layout &L, const StreamPlan &P, const KC<real> &k, real c1, real c2, real *out,
+cudaError_t launch_ws_k(const Layout &L, const StreamPlan &P, const KC<real> &k, const KC<real> &k2, real *out,
                         const real *vel, cudaStream_t s) {
     using C = WsCfg<real, NCW>;
     const size_t smem = ws_smem_bytes<real>(P.fbox, C::SI, C::SU);
@@ -1604,24 +1603,24 @@ cudaError_t launch_ws_k(const Layout &L, const StreamPlan &P, const KC<real> &k,
         if (B > (R_ + minrows - 1) / minrows) B = (R_ + minrows - 1) / minrows;
     }
     if (B < 1) B = 1;
-    kern<<<(unsigned)B, threads, smem, s>>>(L, k, c1, c2, P.fmapU, out, vel, P.fWo, (int)G);
+    kern<<<(unsigned)B, threads, smem, s>>>(L, k, k2, P.fmapU, out, vel, P.fWo, (int)G);
     return cudaGetLastError();
 }
 
 template <typename real, int NCW>
-cudaError_t launch_ws_n(const Layout &L, const StreamPlan &P, const KC<real> &k, real c1, real c2, real *out,
+cudaError_t launch_ws_n(const Layout &L, const StreamPlan &P, const KC<real> &k, const KC<real> &k2, real *out,
                         const real *vel, cudaStream_t s) {
     if (k.fe == 1) {
         switch (k.mob) {
-            case 0: return launch_ws_k<real, NCW, 0, 1>(L, P, k, c1, c2, out, vel, s);
-            case 1: return launch_ws_k<real, NCW, 1, 1>(L, P, k, c1, c2, out, vel, s);
-            default: return launch_ws_k<real, NCW, 2, 1>(L, P, k, c1, c2, out, vel, s);
+            case 0: return launch_ws_k<real, NCW, 0, 1>(L, P, k, k2, out, vel, s);
+            case 1: return launch_ws_k<real, NCW, 1, 1>(L, P, k, k2, out, vel, s);
+            default: return launch_ws_k<real, NCW, 2, 1>(L, P, k, k2, out, vel, s);
         }
     }
     switch (k.mob) {
-        case 0: return launch_ws_k<real, NCW, 0, 0>(L, P, k, c1, c2, out, vel, s);
-        case 1: return launch_ws_k<real, NCW, 1, 0>(L, P, k, c1, c2, out, vel, s);
-        default: return launch_ws_k<real, NCW, 2, 0>(L, P, k, c1, c2, out, vel, s);
+        case 0: return launch_ws_k<real, NCW, 0, 0>(L, P, k, k2, out, vel, s);
+        case 1: return launch_ws_k<real, NCW, 1, 0>(L, P, k, k2, out, vel, s);
+        default: return launch_ws_k<real, NCW, 2, 0>(L, P, k, k2, out, vel, s);
     }
 }
 
@@ -1751,17 +1750,18 @@ cudaError_t launch_fused(int precision, const Layout &L, const StreamPlan &P, co
     if (!P.fused) return cudaErrorInvalidValue;
     if (P.ws) {
         if (precision == 0) {
-            const KC<double> kd = make_kc<double>(K, 0.5 * dt);
-            return P.fncw == 2 ? launch_ws_n<double, 2>(L, P, kd, 0.5 * dt, dt, (double *)out, (const double *)vel, s)
-                               : launch_ws_n<double, 3>(L, P, kd, 0.5 * dt, dt, (double *)out, (const double *)vel, s);
+            const KC<double> k1 = make_kc<double>(K, 0.5 * dt), k2 = make_kc<double>(K, dt);
+            return P.fncw == 2 ? launch_ws_n<double, 2>(L, P, k1, k2, (double *)out, (const double *)vel, s)
+                               : launch_ws_n<double, 3>(L, P, k1, k2, (double *)out, (const double *)vel, s);
         }
-        const KC<float> kf = make_kc<float>(K, 0.5 * dt);
-        return P.fncw == 2 ? launch_ws_n<float, 2>(L, P, kf, (float)(0.5 * dt), (float)dt, (float *)out, (const float *)vel, s)
-                           : launch_ws_n<float, 3>(L, P, kf, (float)(0.5 * dt), (float)dt, (float *)out, (const float *)vel, s);
+        const KC<float> k1 = make_kc<float>(K, 0.5 * dt), k2 = make_kc<float>(K, dt);
+        return P.fncw == 2 ? launch_ws_n<float, 2>(L, P, k1, k2, (float *)out, (const float *)vel, s)
+                           : launch_ws_n<float, 3>(L, P, k1, k2, (float *)out, (const float *)vel, s);
     }
     if (precision == 0)
-        return launch_fused_t<double>(L, P, make_kc<double>(K, 0.5 * dt), 0.5 * dt, dt, (double *)out, (const double *)vel, s);
-    return launch_fused_t<float>(L, P, make_kc<float>(K, 0.5 * dt), (float)(0.5 * dt), (float)dt, (float *)out,
+        return launch_fused_t<double>(L, P, make_kc<double>(K, 0.5 * dt), make_kc<double>(K, dt), (double *)out,
+                                      (const double *)vel, s);
+    return launch_fused_t<float>(L, P, make_kc<float>(K, 0.5 * dt), make_kc<float>(K, dt), (float *)out,
                                  (const float *)vel, s);
 }
 
