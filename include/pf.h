@@ -95,9 +95,12 @@ typedef struct {
     uint64_t seed;                   /* counter-RNG seed (R-16)                              */
     int32_t device;                  /* CUDA device ordinal                                  */
     int32_t graph_steps;             /* steps per captured CUDA graph (0 = no graphs)        */
-    int32_t kernel_path;             /* stage kernel: 0 auto (pair kernel when nx % 4 == 0 and
-                                        nx >= 16, else tile kernel), 1 tile, 2 one-column streaming
-                                        kernel, 3 pair streaming kernel                         */
+    int32_t kernel_path;             /* stage kernel: 0 auto (single-domain grids of <= 2^19 cells in
+                                        all: the persistent small-grid kernel; else the pair kernel
+                                        when nx % 4 == 0 and nx >= 16, else the tile kernel),
+                                        1 tile, 2 one-column streaming, 3 pair streaming,
+                                        4 fused step (experimental), 5 warp-specialised step
+                                        (experimental), 6 reserved, 7 persistent small-grid     */
     int32_t overlap_halo;            /* slab modes: 1 = update the 2-row boundary bands first and
                                         overlap the halo exchange with the interior update
                                         (needs >= 8 rows per slab), 0 = exchange after the stage */

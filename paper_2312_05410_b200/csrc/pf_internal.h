@@ -84,6 +84,10 @@ cudaError_t launch_stage(int precision, const Layout &L, const StreamPlan &plan,
 // Fused step: out (the other buffer) = u^{n+1} of the state in the buffer P.fmapU describes.
 cudaError_t launch_fused(int precision, const Layout &L, const StreamPlan &P, const Coef &K, void *out, const void *vel,
                          double dt, cudaStream_t s);
+// Small-grid path: nsteps midpoint steps of every member in one cooperative launch (U holds the
+// state before and after; owned cells only, the ghost frame is left stale).
+cudaError_t launch_persistent(int precision, const Layout &L, const Coef &K, void *U, void *Us, const void *vel,
+                              double dt, int64_t nsteps, cudaStream_t s);
 // Rebuild the ghost frame of a buffer from its owned cells (periodic columns; mirror rows and
 // the rho reservoir at global y boundaries).  Slab-interior ghost rows are left to the exchange.
 cudaError_t launch_fill_ghosts(int precision, const Layout &L, double rho_in, void *state, cudaStream_t s);

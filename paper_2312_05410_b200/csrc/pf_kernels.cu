@@ -16,11 +16,14 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
+#include <cooperative_groups.h>
 #include <cudaTypedefs.h>
 #include <utility>
 
 #include "pf_cell.cuh"
 #include "pf_internal.h"
+
+namespace cg = cooperative_groups;
 
 namespace pf {
 
@@ -54,22 +57,28 @@ __device__ __forceinline__ int wrap_x(int gx, int nx) {
     return gx % nx;
 }
 
-template <typename real, int MOB, int FE>
-__global__ void __launch_bounds__(NT) stage_kernel(Layout L, KC<real> k, const real *__restrict__ in,
-                                                   const real *__restrict__ base, real *out,
-                                                   const real *__restrict__ vel) {
-    __shared__ real sc[BY + 4][BX + 4];
-    __shared__ real sp[BY + 4][BX + 4];
-    __shared__ real sr[BY + 2][BX + 2];
-    __shared__ real smc[BY + 2][BX + 2];
-    __shared__ real smp[BY + 2][BX + 2];
-    __shared__ real sM[BY + 2][BX + 2];
-    __shared__ double etab[64];
-    load_exp_table(etab);
+template <typename real>
+struct TileSmem {
+    real sc[BY + 4][BX + 4];
+    real sp[BY + 4][BX + 4];
+    real sr[BY + 2][BX + 2];
+    real smc[BY + 2][BX + 2];
+    real smp[BY + 2][BX + 2];
+    real sM[BY + 2][BX + 2];
+};
 
-    const int m = L.m0 + blockIdx.z;
-    const int tx0 = blockIdx.x * BX;
-    const int ty0 = L.r0 + blockIdx.y * BY;
+// One stage on the tile (member m, columns [tx0, tx0 + 32), rows [ty0, ty0 + 16)): ghost rules
+// applied by index, so the tile reads owned cells only (the ghost frame may be stale).
+template <typename real, int MOB, int FE>
+__device__ __forceinline__ void tile_stage(const Layout &L, const KC<real> &k, const real *__restrict__ in,
+                                           const real *__restrict__ base, real *out, const real *__restrict__ vel,
+                                           const double *etab, TileSmem<real> &ts, int m, int tx0, int ty0) {
+    auto &sc = ts.sc;
+    auto &sp = ts.sp;
+    auto &sr = ts.sr;
+    auto &smc = ts.smc;
+    auto &smp = ts.smp;
+    auto &sM = ts.sM;
     const int nx = L.nx;
     const real *ic = in + m * L.mstride;
     const real *ip = ic + L.fstride;
@@ -107,9 +116,9 @@ __global__ void __launch_bounds__(NT) stage_kernel(Layout L, KC<real> k, const r
         const int sy = t / (BX + 2), sx = t - sy * (BX + 2);
         const int ey = sy + 1, ex = sx + 1;
         real mc, mp, M;
-        constitutive<real, MOB, FE>(k, mo, etab, sc[ey][ex], sp[ey][ex], sc[ey][ex - 1], sc[ey][ex + 1], sc[ey - 1][ex],
-                                 sc[ey + 1][ex], sp[ey][ex - 1], sp[ey][ex + 1], sp[ey - 1][ex], sp[ey + 1][ex], mc,
-                                 mp, M);
+        constitutive<real, MOB, FE>(k, mo, etab, sc[ey][ex], sp[ey][ex], sc[ey][ex - 1], sc[ey][ex + 1],
+                                    sc[ey - 1][ex], sc[ey + 1][ex], sp[ey][ex - 1], sp[ey][ex + 1], sp[ey - 1][ex],
+                                    sp[ey + 1][ex], mc, mp, M);
         smc[sy][sx] = mc;
         smp[sy][sx] = mp;
         sM[sy][sx] = M;
@@ -140,6 +149,47 @@ __global__ void __launch_bounds__(NT) stage_kernel(Layout L, KC<real> k, const r
         out[o] = oc;
         out[o + L.fstride] = op;
         out[o + 2 * L.fstride] = orr;
+    }
+    __syncthreads();   // the tile's shared memory may be refilled next
+}
+
+template <typename real, int MOB, int FE>
+__global__ void __launch_bounds__(NT) stage_kernel(Layout L, KC<real> k, const real *__restrict__ in,
+                                                   const real *__restrict__ base, real *out,
+                                                   const real *__restrict__ vel) {
+    __shared__ TileSmem<real> ts;
+    __shared__ double etab[64];
+    load_exp_table(etab);
+    tile_stage<real, MOB, FE>(L, k, in, base, out, vel, etab, ts, L.m0 + (int)blockIdx.z, (int)blockIdx.x * BX,
+                              L.r0 + (int)blockIdx.y * BY);
+}
+
+// Small-grid path ("B10"): a cooperative persistent kernel that advances every
+// member by nsteps midpoint steps in ONE launch -- both stages of every step over all tiles, with
+// a grid-wide barrier after each stage -- for grids too small to fill the GPU, where the two
+// launches per step (not HBM) are the cost.  Same per-cell arithmetic and tiles as stage_kernel:
+// bitwise identical results.  Writes owned cells only; the host rebuilds the ghost frame after.
+template <typename real, int MOB, int FE>
+__global__ void __launch_bounds__(NT) persistent_kernel(Layout L, KC<real> k1, KC<real> k2, real *U, real *Us,
+                                                        const real *__restrict__ vel, int64_t nsteps) {
+    __shared__ TileSmem<real> ts;
+    __shared__ double etab[64];
+    load_exp_table(etab);
+    cg::grid_group grid = cg::this_grid();
+    const int tx = (L.nx + BX - 1) / BX, ty = (L.ny_loc + BY - 1) / BY;
+    const int ntiles = tx * ty * L.members;
+    for (int64_t s = 0; s < nsteps; ++s) {
+        for (int stage = 1; stage <= 2; ++stage) {
+            const real *in = stage == 1 ? U : Us;
+            real *out = stage == 1 ? Us : U;
+            const KC<real> &kk = stage == 1 ? k1 : k2;
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                const int m = t / (tx * ty), r = t - m * (tx * ty);
+                const int by = r / tx, bxi = r - by * tx;
+                tile_stage<real, MOB, FE>(L, kk, in, U, out, vel, etab, ts, L.m0 + m, bxi * BX, by * BY);
+            }
+            grid.sync();
+        }
     }
 }
 
@@ -1763,6 +1813,48 @@ cudaError_t launch_fused(int precision, const Layout &L, const StreamPlan &P, co
                                       (const double *)vel, s);
     return launch_fused_t<float>(L, P, make_kc<float>(K, 0.5 * dt), make_kc<float>(K, dt), (float *)out,
                                  (const float *)vel, s);
+}
+
+template <typename real, int MOB, int FE>
+cudaError_t launch_persistent_t(const Layout &L, const KC<real> &k1, const KC<real> &k2, real *U, real *Us,
+                                const real *vel, int64_t nsteps, cudaStream_t s) {
+    static int occ = -1, nsm = 0;
+    auto kern = persistent_kernel<real, MOB, FE>;
+    if (occ < 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, 0);
+        if (e != cudaSuccess) return e;
+        if (occ < 1) occ = 1;
+    }
+    const int64_t ntiles = (int64_t)((L.nx + BX - 1) / BX) * ((L.ny_loc + BY - 1) / BY) * L.members;
+    const int64_t maxb = (int64_t)occ * nsm;
+    const int blocks = (int)(ntiles < maxb ? ntiles : maxb);
+    Layout Lc = L;
+    KC<real> a1 = k1, a2 = k2;
+    void *args[] = {&Lc, &a1, &a2, &U, &Us, (void *)&vel, &nsteps};
+    return cudaLaunchCooperativeKernel((const void *)kern, blocks, NT, args, 0, s);
+}
+
+cudaError_t launch_persistent(int precision, const Layout &L, const Coef &K, void *U, void *Us, const void *vel,
+                              double dt, int64_t nsteps, cudaStream_t s) {
+    cudaError_t te = upload_exp_table();
+    if (te != cudaSuccess) return te;
+    if (precision == 0) {
+        const KC<double> k1 = make_kc<double>(K, 0.5 * dt), k2 = make_kc<double>(K, dt);
+        auto f = k1.fe == 1 ? (k1.mob == 0 ? launch_persistent_t<double, 0, 1> : k1.mob == 1 ? launch_persistent_t<double, 1, 1>
+                                                                                        : launch_persistent_t<double, 2, 1>)
+                            : (k1.mob == 0 ? launch_persistent_t<double, 0, 0> : k1.mob == 1 ? launch_persistent_t<double, 1, 0>
+                                                                                        : launch_persistent_t<double, 2, 0>);
+        return f(L, k1, k2, (double *)U, (double *)Us, (const double *)vel, nsteps, s);
+    }
+    const KC<float> k1 = make_kc<float>(K, 0.5 * dt), k2 = make_kc<float>(K, dt);
+    auto f = k1.fe == 1 ? (k1.mob == 0 ? launch_persistent_t<float, 0, 1> : k1.mob == 1 ? launch_persistent_t<float, 1, 1>
+                                                                                   : launch_persistent_t<float, 2, 1>)
+                        : (k1.mob == 0 ? launch_persistent_t<float, 0, 0> : k1.mob == 1 ? launch_persistent_t<float, 1, 0>
+                                                                                   : launch_persistent_t<float, 2, 0>);
+    return f(L, k1, k2, (float *)U, (float *)Us, (const float *)vel, nsteps, s);
 }
 
 void swap_plan_buffers(StreamPlan &P) {

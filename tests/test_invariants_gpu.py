@@ -265,3 +265,17 @@ def test_warp_specialised_step_kernel_bitwise(nx, ny, members, extra):
     b = _run(p.replace(kernel_path=5), 7)
     for m in range(members):
         assert _eq(a[m], b[m]), m
+
+
+@pytest.mark.parametrize("nx,ny,members,extra", [(64, 64, 1, {}), (96, 48, 3, {}), (33, 65, 2, {}),
+                                                  (128, 40, 2, dict(mob_lo=0.5, mob_hi=1.0)),
+                                                  (80, 32, 1, dict(fe_model=1, omega=2.2, temp_rs=0.45, dt=4e-4))])
+def test_persistent_small_grid_kernel_bitwise(nx, ny, members, extra):
+    """The persistent small-grid kernel (kernel_path 7: all steps of a check interval in one
+    cooperative launch) gives the same bits as the stage kernels, across several check intervals,
+    and leaves a valid ghost frame behind (a later pair-kernel run continues bitwise)."""
+    p = _base(nx, ny, n_members=members, rate_lo=0.5, rate_hi=2.0, check_every=9, **extra)
+    a = _run(p.replace(kernel_path=1), 23)
+    b = _run(p.replace(kernel_path=7), 23)
+    for m in range(members):
+        assert _eq(a[m], b[m]), m
