@@ -433,13 +433,17 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// try_wait with a suspend-time hint: a waiting warp is suspended until the phase completes (or the
+// hint elapses) instead of re-issuing the try_wait / branch loop, which took ~40% of the stage
+// kernels' issue slots.
+constexpr uint32_t kSuspendNs = 1000000;
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n"
         "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
         "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-        "r"(parity)
+        "r"(parity), "r"(kSuspendNs)
         : "memory");
 }
 // 3D TMA tile load: box at (x, y, z) of the tensor map -> shared memory, completion on bar.
@@ -450,6 +454,10 @@ __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, i
         "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
         : "memory");
 }
+// Programmatic dependent launch: a stage launch may be scheduled while the previous launch on the
+// stream drains; griddep_wait() returns once that launch has completed and its writes are visible.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap *map) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
@@ -759,6 +767,10 @@ __global__ void __launch_bounds__(32 * NCW + 32, MINB) pair_kernel(
     const int nx = L.nx;
     const Sched sch = make_sched(L, Wo, G);
     const uint32_t box_bytes = (uint32_t)(3 * R * bx * sizeof(real));
+    // set-up above overlaps the previous launch's drain; no global access before this point.  No
+    // explicit trigger: the dependent launch starts as this grid's blocks exit (triggering at block
+    // start measured 20% slower on cfg3 -- waiting dependents crowd the SMs)
+    griddep_wait();
 
     if (warp == NCW) {
         // ------------------------------- producer -------------------------------
@@ -1467,6 +1479,20 @@ cudaError_t launch_ring(const Layout &L, const StreamPlan &P, const KC<real> &k,
     if (B < 1) B = 1;
     const int ri = R == 4 ? 1 : 0;
     const CUtensorMap &mIn = stage == 1 ? P.mapU[ri] : P.mapUs[ri];
+    static const int pdl = env_int("PF_PDL", 1);
+    if (KIND == kPairKind && pdl) {   // programmatic dependent launch (pair_kernel waits in-kernel)
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.gridDim = dim3((unsigned)B);
+        cfg.blockDim = dim3(32 * NCW + 32);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = s;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        return cudaLaunchKernelEx(&cfg, kern, L, k, mIn, P.mapU[ri], out, vel, P.Wo, (int)G);
+    }
     kern<<<(unsigned)B, 32 * NCW + 32, smem, s>>>(L, k, mIn, P.mapU[ri], out, vel, P.Wo, (int)G);
     return cudaGetLastError();
 }
