@@ -52,8 +52,35 @@ def _run(cmd, verbose):
 
 
 def sources():
+    inc = os.path.join(ROOT, "include")
     return sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC)
-                  if f.endswith((".cu", ".cpp", ".h", ".cuh"))) + [os.path.join(ROOT, "include", "pf.h")]
+                  if f.endswith((".cu", ".cpp", ".h", ".cuh"))) + sorted(
+        os.path.join(inc, f) for f in os.listdir(inc) if f.endswith(".h"))
+
+
+def _deps(src, seen=None):
+    """src and the local headers it includes (transitively, quoted includes only)."""
+    seen = set() if seen is None else seen
+    if src in seen or not os.path.exists(src):
+        return seen
+    seen.add(src)
+    for line in open(src):
+        line = line.strip()
+        if line.startswith("#include \""):
+            name = line.split('"')[1]
+            for d in (os.path.dirname(src), CSRC, os.path.join(ROOT, "include")):
+                cand = os.path.join(d, name)
+                if os.path.exists(cand):
+                    _deps(cand, seen)
+                    break
+    return seen
+
+
+def _stale(obj, src):
+    if not os.path.exists(obj):
+        return True
+    t = os.path.getmtime(obj)
+    return any(os.path.getmtime(d) > t for d in _deps(src))
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
@@ -71,16 +98,20 @@ def build(force: bool = False, verbose: bool = False) -> str:
         src = os.path.join(CSRC, f)
         if f.endswith(".cu"):
             obj = os.path.join(BUILD, f[:-3] + ".o")
+            objs.append(obj)
+            if not force and not _stale(obj, src):
+                continue
             _run([os.path.join(CUDA, "bin", "nvcc"), *ARCH, "-O3", "-lineinfo", "-std=c++17",
                   "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr", "-fmad=false",
                   *incs, "-c", src, "-o", obj], verbose)
-            objs.append(obj)
         elif f.endswith(".cpp"):
             obj = os.path.join(BUILD, f[:-4] + ".o")
+            objs.append(obj)
+            if not force and not _stale(obj, src):
+                continue
             # -ffp-contract=off: the initial fields must be bitwise reproducible (R-16)
             _run(["g++", "-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-fno-fast-math",
                   "-Wall", *incs, "-c", src, "-o", obj], verbose)
-            objs.append(obj)
     nccl_so = "libnccl.so.2" if os.path.exists(os.path.join(lib_nccl, "libnccl.so.2")) else "libnccl.so"
     tmp = LIB + ".tmp"
     _run([os.path.join(CUDA, "bin", "nvcc"), *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs,

@@ -1,0 +1,1231 @@
+// unet.cu -- NEXT-4 of SURVEY 8(f): inference of the temporally conditioned U-Net (PAPER.md section
+// 4.3; include/unet.h; readings R-29..R-35 of DESIGN.md 14).
+//
+// Layout: activations NHWC bf16 ([pixel][channel], pixel = (b * H + y) * W + x); conv outputs fp32
+// NHWC; GroupNorm statistics fp64.  Concatenation z (+) d is a channel-offset write into a buffer of
+// 2C channels, so no copy is needed.
+//
+// conv3x3_kernel: implicit GEMM on the 5th-generation tensor cores.
+//   D[pixel, cout] = sum_K A[pixel, K] B[cout, K],  K = (ky * 3 + kx) * cin + ci   (R-29)
+//   One CTA = 128 pixels (UMMA M = 128) x all cout (UMMA N = cout <= 128), fp32 accumulator in TMEM
+//   (cout columns).  K streams through a 2-stage shared-memory ring in blocks of 64: every thread
+//   gathers its pixel's 16-byte channel chunks with cp.async (zero-fill outside the grid = the 'same'
+//   zero padding), the weights likewise; after a proxy fence and a CTA barrier one thread issues
+//   tcgen05.mma (kind::f16, bf16 x bf16 -> fp32, K = 16 per instruction) and tcgen05.commit arrives
+//   on the stage's mbarrier, which gates the reuse of that stage two blocks later.  Operands use the
+//   canonical no-swizzle K-major layout: 8-row x 16-byte core matrices, rows 16 B apart, 8-row groups
+//   128 B apart (SBO), K-chunks of 8 elements LBO apart.  Epilogue: each warp reads its 32 TMEM lanes
+//   (tcgen05.ld 32x32b), one pixel per thread, and stores the fp32 row.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "unet.h"
+
+namespace un {
+namespace {
+
+typedef __nv_bfloat16 bf16;
+
+constexpr int kBM = 128;      // pixels per CTA (UMMA M)
+constexpr int kBK = 64;       // K elements per ring stage (8 chunks of 8 bf16)
+constexpr int kStages = 2;
+constexpr int kBasis = 128;   // time-basis width
+constexpr int kGroups = 4;    // GroupNorm groups (R-30)
+constexpr double kEps = 1e-5; // GroupNorm epsilon (R-30)
+
+// ------------------------------------------------------------------------------------------------
+// PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void *src, bool valid) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+
+template <int COLS>
+__device__ __forceinline__ void tmem_alloc(uint32_t *slot) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(slot)), "n"(COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+}
+template <int COLS>
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(taddr), "n"(COLS) : "memory");
+}
+
+// UMMA shared-memory descriptor, K-major, no swizzle: start >> 4, LBO >> 4 (K direction),
+// SBO >> 4 (M/N direction), version 1 (bits 46-47), layout type 0.
+__device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+    return (uint64_t)((addr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
+           ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);
+}
+// Instruction descriptor, kind::f16: D fp32 (bits 4-5 = 1), A bf16 (bits 7-9 = 1), B bf16
+// (bits 10-12 = 1), both K-major, N >> 3 at bits 17-22, M >> 4 at bits 24-28.
+__host__ __device__ constexpr uint32_t idesc_bf16(int n) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(kBM >> 4) << 24);
+}
+__device__ __forceinline__ void umma(uint32_t tmem, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem),
+        "l"(ad), "l"(bd), "r"(idesc), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint64_t *bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15}, [%16];\n"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+}
+
+// Persistent pipelined implicit GEMM.  One CTA per SM (256 threads) walks the 128-pixel tiles
+// tile = blockIdx.x, blockIdx.x + gridDim.x, ...; every tile's K = 9 cin is cut into blocks of
+// KC = 18 chunks (144 elements; nch = 9 cin / 8 is a multiple of 18 for cin a multiple of 16), and
+// the sequence of (tile, K-block) steps streams through an S-stage shared-memory ring: the loads of
+// step j + S - 1 are in flight while the tensor core runs step j.  The accumulator is double
+// buffered in TMEM (2 x N columns): the epilogue of tile i (tcgen05.ld, fp32 stores, GroupNorm
+// partial sums) runs while the MMAs of tile i + 1 execute.
+constexpr int kKC = 18;
+
+template <int N>
+struct ConvCfg {
+    static constexpr int tcols = 2 * N < 32 ? 32 : 2 * N;           // two accumulators
+    static constexpr uint32_t lbo_a = kBM / 8 * 128;                // K-chunk stride of A (2 KB)
+    static constexpr uint32_t lbo_b = N / 8 * 128;                  // K-chunk stride of B
+    static constexpr uint32_t a_bytes = kKC * lbo_a;
+    static constexpr uint32_t b_bytes = kKC * lbo_b;
+    static constexpr uint32_t stage = a_bytes + b_bytes;
+    static constexpr int S = (110 * 1024) / stage >= 2 ? 2 : ((200 * 1024) / stage > 4 ? 4 : (200 * 1024) / stage);
+    static constexpr size_t smem = 1024 + S * stage + 128;
+    static_assert(S >= 2, "ring too shallow");
+};
+
+__device__ __forceinline__ void cp_async_wait_n(int n) {   // n <= 3
+    switch (n) {
+        case 0: asm volatile("cp.async.wait_group 0;\n" ::: "memory"); break;
+        case 1: asm volatile("cp.async.wait_group 1;\n" ::: "memory"); break;
+        case 2: asm volatile("cp.async.wait_group 2;\n" ::: "memory"); break;
+        default: asm volatile("cp.async.wait_group 3;\n" ::: "memory"); break;
+    }
+}
+
+// Epilogue of one 128-pixel tile t (pixels t*128 .. t*128+127) whose accumulator is TMEM buffer
+// tl & 1: wait for its MMAs, tcgen05.ld (warp w reads lanes 32 (w & 3) .. +31; with N >= 32 the
+// warps w and w + 4 split the columns), fp32 stores, GroupNorm partial sums (see above).
+template <int N, bool HEAD>
+__device__ __forceinline__ void conv_epilogue(uint32_t tacc, uint64_t *bar, uint32_t parity, int64_t t, int64_t npix,
+                                              float *__restrict__ out, double *__restrict__ part, int gran) {
+    constexpr int NG = HEAD ? 1 : kGroups, GC = HEAD ? 1 : N / kGroups;
+    constexpr int ECOLS = N >= 32 ? N / 2 : N;                       // epilogue columns per warp
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    mbar_wait(bar, parity);
+    tc_fence_after();
+    const int lq = warp & 3, hv = warp >> 2;
+    if (N >= 32 || hv == 0) {
+        const int64_t p = t * kBM + 32 * lq + lane;
+        const bool pv = p < npix;
+        const int c0 = N >= 32 ? hv * ECOLS : 0;
+        const uint32_t trow = tacc + ((uint32_t)(32 * lq) << 16);
+        float *o = out + p * N;
+        // groups owned by this warp: all (N = 16) or the half [2 hv, 2 hv + 2) (N >= 32)
+        constexpr int G0N = N >= 32 ? NG / 2 : NG;
+        const int g0 = N >= 32 ? hv * G0N : 0;
+        double gs[G0N], gq[G0N];
+#pragma unroll
+        for (int g = 0; g < G0N; ++g) gs[g] = gq[g] = 0.0;
+#pragma unroll
+        for (int c = 0; c < ECOLS; c += 16) {
+            uint32_t r[16];
+            tmem_ld16(trow + c0 + c, r);
+            if (pv) {
+                float4 *o4 = reinterpret_cast<float4 *>(o + c0 + c);
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    o4[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                        __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    const int lc = c + j;     // column relative to c0 (compile-time after unrolling)
+                    if (HEAD && lc > 0) continue;
+                    const double v = (double)__uint_as_float(r[j]);
+                    gs[lc / GC] += v;
+                    gq[lc / GC] += v * v;
+                }
+            }
+        }
+        if (gran == 1) {
+            if (pv)
+#pragma unroll
+                for (int g = 0; g < G0N; ++g) {
+                    part[(p * NG + g0 + g) * 2] = gs[g];
+                    part[(p * NG + g0 + g) * 2 + 1] = gq[g];
+                }
+        } else {
+#pragma unroll
+            for (int g = 0; g < G0N; ++g)
+                for (int off = 16; off > 0; off >>= 1) {
+                    gs[g] += __shfl_xor_sync(0xffffffffu, gs[g], off);
+                    gq[g] += __shfl_xor_sync(0xffffffffu, gq[g], off);
+                }
+            const int64_t wid = t * 4 + lq;   // global 32-pixel unit
+            if (lane == 0 && wid * 32 < npix)
+#pragma unroll
+                for (int g = 0; g < G0N; ++g) {
+                    part[(wid * NG + g0 + g) * 2] = gs[g];
+                    part[(wid * NG + g0 + g) * 2 + 1] = gq[g];
+                }
+        }
+    }
+    tc_fence_before();
+}
+
+// Epilogue statistics: the sum and the sum of squares (fp64) of each GroupNorm group's channels per
+// unit of `gran` pixels -- a warp's 32 pixels when H W is a multiple of 32 (a warp then never
+// straddles two samples), else each pixel -- written to part[unit][group][2]; HEAD: one group made
+// of channel 0 only.
+template <int N, bool HEAD>
+__global__ void __launch_bounds__(256) conv3x3_kernel(const bf16 *__restrict__ in, const bf16 *__restrict__ w,
+                                                         float *__restrict__ out, double *__restrict__ part,
+                                                         int64_t npix, int H, int W, int cin, int gran) {
+    using C = ConvCfg<N>;
+    constexpr int S = C::S;
+    constexpr int NG = HEAD ? 1 : kGroups, GC = HEAD ? 1 : N / kGroups;
+    constexpr int ECOLS = N >= 32 ? N / 2 : N;                       // epilogue columns per warp
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char *sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    uint64_t *mma_bar = reinterpret_cast<uint64_t *>(sm + S * C::stage);
+    uint64_t *acc_bar = mma_bar + S;
+    uint32_t *tslot = reinterpret_cast<uint32_t *>(acc_bar + 2);
+    const uint32_t sbase = smem_u32(sm);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+    if (tid == 0) {
+        for (int q = 0; q < S; ++q) mbar_init(&mma_bar[q], 1);
+        mbar_init(&acc_bar[0], 1);
+        mbar_init(&acc_bar[1], 1);
+        fence_mbar_init();
+    }
+    if (warp == 0) tmem_alloc<C::tcols>(tslot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tslot;
+
+    const int64_t tiles = (npix + kBM - 1) / kBM;
+    const int ntl = blockIdx.x < tiles ? (int)((tiles - 1 - blockIdx.x) / gridDim.x + 1) : 0;
+    const int HW = H * W, cq = cin >> 3, nkb = 9 * cq / kKC;
+    const int64_t krow = 9 * (int64_t)cin;
+    const int nsteps = ntl * nkb;
+    const int m = tid & 127, half = tid >> 7;
+    const uint32_t arow = (uint32_t)((m >> 3) * 128 + (m & 7) * 16);
+
+    // per-tile gather state of this thread's pixel: center offset, 3x3 validity mask (bit ky*3+kx)
+    int ctl = -1;
+    int64_t pc = 0;
+    uint32_t vmask = 0;
+    const int64_t Wc = (int64_t)W * cin;
+    auto load = [&](int j) {
+        const int tl = j / nkb, kb = j - tl * nkb;
+        if (tl != ctl) {
+            ctl = tl;
+            const int64_t p = ((int64_t)blockIdx.x + (int64_t)tl * gridDim.x) * kBM + m;
+            vmask = 0;
+            pc = 0;
+            if (p < npix) {
+                const int b = (int)(p / HW);
+                const int rem = (int)(p - (int64_t)b * HW);
+                const int y = rem / W, x = rem - y * W;
+                pc = p * cin;
+                const uint32_t rows = (y > 0 ? 1u : 0u) | 2u | (y < H - 1 ? 4u : 0u);
+                const uint32_t cols = (x > 0 ? 1u : 0u) | 2u | (x < W - 1 ? 4u : 0u);
+                for (int ky = 0; ky < 3; ++ky)
+                    if (rows >> ky & 1u) vmask |= cols << (3 * ky);
+            }
+        }
+        const uint32_t a0 = sbase + (j % S) * C::stage, b0 = a0 + C::a_bytes;
+        const int g0 = kb * kKC + half;
+        int tap = g0 / cq, cc = g0 - tap * cq;
+        int ky = tap / 3, kx = tap - 3 * ky;
+        int64_t toff = (ky - 1) * Wc + (kx - 1) * cin;
+#pragma unroll 3
+        for (int q = half; q < kKC; q += 2) {
+            const bool v = (vmask >> (ky * 3 + kx)) & 1u;
+            cp_async16(a0 + q * C::lbo_a + arow, v ? in + pc + toff + cc * 8 : in, v);
+            cc += 2;
+            if (cc >= cq) {
+                cc -= cq;
+                if (++kx == 3) {
+                    kx = 0;
+                    ++ky;
+                    toff += Wc - 2 * cin;
+                } else {
+                    toff += cin;
+                }
+            }
+        }
+        for (int i = tid; i < N * kKC; i += 256) {
+            const int n = i / kKC, q = i - n * kKC;
+            cp_async16(b0 + q * C::lbo_b + (n >> 3) * 128 + (n & 7) * 16, w + n * krow + (int64_t)(kb * kKC + q) * 8, true);
+        }
+    };
+
+    auto epilogue = [&](int tl) {
+        conv_epilogue<N, HEAD>(tmem + (uint32_t)((tl & 1) * N), &acc_bar[tl & 1], (uint32_t)(tl >> 1) & 1u,
+                               (int64_t)blockIdx.x + (int64_t)tl * gridDim.x, npix, out, part, gran);
+    };
+
+    for (int j = 0; j < S - 1; ++j) {
+        if (j < nsteps) load(j);
+        cp_async_commit();
+    }
+    for (int j = 0; j < nsteps; ++j) {
+        const int jn = j + S - 1;
+        if (jn < nsteps) {
+            if (j >= 1) mbar_wait(&mma_bar[(j - 1) % S], (uint32_t)((j - 1) / S) & 1u);   // stage of step j-1 free
+            load(jn);
+        }
+        cp_async_commit();
+        cp_async_wait_n(S - 1);    // step j has landed
+        fence_proxy_async();       // generic-proxy smem writes -> visible to the tensor core
+        __syncthreads();
+        const int tl = j / nkb, kb = j - tl * nkb;
+        if (tid == 0) {
+            tc_fence_after();
+            const uint32_t a0 = sbase + (j % S) * C::stage, b0 = a0 + C::a_bytes;
+            const uint32_t acc = tmem + (uint32_t)((tl & 1) * N);
+#pragma unroll
+            for (int k = 0; k < kKC / 2; ++k)
+                umma(acc, sdesc(a0 + 2 * k * C::lbo_a, C::lbo_a, 128), sdesc(b0 + 2 * k * C::lbo_b, C::lbo_b, 128),
+                     idesc_bf16(N), (kb | k) ? 1u : 0u);
+            umma_commit(&mma_bar[j % S]);
+            if (kb == nkb - 1) umma_commit(&acc_bar[tl & 1]);
+        }
+        if (kb == nkb - 1 && tl >= 1) epilogue(tl - 1);   // overlaps the MMAs of tile tl
+    }
+    if (ntl >= 1) epilogue(ntl - 1);
+    __syncthreads();
+    if (warp == 0) tmem_dealloc<C::tcols>(tmem);
+}
+
+template <int N, bool HEAD>
+cudaError_t launch_conv_n(const bf16 *in, const bf16 *w, float *out, double *part, int64_t npix, int H, int W,
+                          int cin, cudaStream_t st) {
+    using C = ConvCfg<N>;
+    static int nsm = 0, occ = 1;
+    if (nsm == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        cudaError_t e = cudaFuncSetAttribute(conv3x3_kernel<N, HEAD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)C::smem);
+        if (e != cudaSuccess) return e;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, conv3x3_kernel<N, HEAD>, 256, C::smem);
+        if (e != cudaSuccess) return e;
+        occ = occ < 1 ? 1 : (occ > 2 ? 2 : occ);   // TMEM: 2 CTAs x 2N columns <= 512
+    }
+    const int gran = (H * W) % 32 == 0 ? 32 : 1;
+    const int64_t tiles = (npix + kBM - 1) / kBM, slots = (int64_t)nsm * occ;
+    const unsigned grid = (unsigned)(tiles < slots ? tiles : slots);
+    conv3x3_kernel<N, HEAD><<<grid, 256, C::smem, st>>>(in, w, out, part, npix, H, W, cin, gran);
+    return cudaGetLastError();
+}
+
+// Row-tile variant for W a multiple of 128 (the full- and half-resolution levels, where the
+// channel counts are small and the gather above is instruction bound): a tile is 128 consecutive
+// pixels of one image row, and the shared memory holds the three input rows y-1, y, y+1 over the
+// 130 pixels x0-1 .. x0+128, chunk-major (chunk c of pixel i at c * 2080 + i * 16 B), so that the A
+// operand of tap (ky, kx) is the canonical K-major layout starting kx pixels (16 B) into row ky:
+// one descriptor per (tap, 16-channel step), no per-tap gather, each input row read 3x instead of
+// 9x.  The whole weight matrix stays resident in shared memory.
+constexpr int kRowPix = 130;
+constexpr uint32_t kRowLbo = kRowPix * 16;   // chunk-plane stride (2080 B)
+
+template <int N>
+struct RowCfg {
+    static constexpr int nbuf = N <= 64 ? 4 : 2;                   // TMEM accumulators (epilogue lag nbuf-1)
+    static constexpr int tcols = nbuf * N < 32 ? 32 : nbuf * N;
+    static constexpr uint32_t lbo_b = N / 8 * 128;
+};
+
+// Pipeline: loads run S-2 tiles ahead (the refilled stage was consumed two tiles ago, so its MMAs
+// have long finished), the epilogue trails the MMA issue by nbuf-1 tiles (the tcgen05 completion
+// latency stays off the critical path).
+template <int N, bool HEAD>
+__global__ void __launch_bounds__(256) conv3x3_rows_kernel(const bf16 *__restrict__ in, const bf16 *__restrict__ w,
+                                                           float *__restrict__ out, double *__restrict__ part,
+                                                           int64_t npix, int H, int W, int cin, int S, int gran,
+                                                           int dbg) {
+    using C = RowCfg<N>;
+    constexpr int NB = C::nbuf, LAG = NB - 1;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char *sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    const int cq = cin >> 3, PD = S - 2;
+    const uint32_t a_bytes = 3u * cq * kRowLbo, b_bytes = 9u * cq * C::lbo_b;
+    uint64_t *mma_bar = reinterpret_cast<uint64_t *>(sm + S * a_bytes + b_bytes);
+    uint64_t *acc_bar = mma_bar + S;
+    uint32_t *tslot = reinterpret_cast<uint32_t *>(acc_bar + NB);
+    const uint32_t sbase = smem_u32(sm), bbase = sbase + S * a_bytes;
+    const int tid = threadIdx.x, warp = tid >> 5;
+
+    if (tid == 0) {
+        for (int q = 0; q < S; ++q) mbar_init(&mma_bar[q], 1);
+        for (int q = 0; q < NB; ++q) mbar_init(&acc_bar[q], 1);
+        fence_mbar_init();
+    }
+    if (warp == 0) tmem_alloc<C::tcols>(tslot);
+    // resident weights: chunk g = tap * cq + c of row n at g * lbo_b + (n / 8) * 128 + (n % 8) * 16
+    const int nchk = 9 * cq;
+    for (int i = tid; i < N * nchk; i += 256) {
+        const int n = i / nchk, g = i - n * nchk;
+        cp_async16(bbase + g * C::lbo_b + (n >> 3) * 128 + (n & 7) * 16, w + (int64_t)n * 9 * cin + g * 8, true);
+    }
+    cp_async_commit();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tslot;
+
+    const int64_t tiles = npix / kBM;                    // W % 128 == 0: every tile is full
+    const int ntl = blockIdx.x < tiles ? (int)((tiles - 1 - blockIdx.x) / gridDim.x + 1) : 0;
+    const int tpr = W / kBM;                             // tiles per image row
+    const int units = 3 * kRowPix;                       // (row, pixel) pairs per tile
+
+    auto load = [&](int tl) {
+        if (dbg & 1) return;
+        const int64_t t = (int64_t)blockIdx.x + (int64_t)tl * gridDim.x;
+        const int64_t rowid = t / tpr;                   // b * H + y
+        const int x0 = (int)(t - rowid * tpr) * kBM;
+        const int y = (int)(rowid % H);
+        const uint32_t a0 = sbase + (tl % S) * a_bytes;
+        for (int u = tid; u < units; u += 256) {
+            const int r = u / kRowPix, i = u - r * kRowPix;
+            const int yy = y + r - 1, xx = x0 + i - 1;
+            const bool v = yy >= 0 && yy < H && xx >= 0 && xx < W;
+            const bf16 *src = v ? in + ((rowid + r - 1) * W + xx) * cin : in;
+            const uint32_t d = a0 + (uint32_t)(r * cq) * kRowLbo + i * 16;
+            for (int c = 0; c < cq; ++c) cp_async16(d + c * kRowLbo, v ? src + c * 8 : in, v);
+        }
+    };
+
+    auto epilogue = [&](int tl) {
+        if (dbg & 4) {
+            mbar_wait(&acc_bar[tl % NB], (uint32_t)(tl / NB) & 1u);
+            return;
+        }
+        conv_epilogue<N, HEAD>(tmem + (uint32_t)((tl % NB) * N), &acc_bar[tl % NB], (uint32_t)(tl / NB) & 1u,
+                               (int64_t)blockIdx.x + (int64_t)tl * gridDim.x, npix, out, part, gran);
+    };
+
+    for (int j = 0; j < PD; ++j) {
+        if (j < ntl) load(j);
+        cp_async_commit();
+    }
+    for (int j = 0; j < ntl; ++j) {
+        const int jn = j + PD;
+        if (jn < ntl) {
+            if (j >= 2) mbar_wait(&mma_bar[(j - 2) % S], (uint32_t)((j - 2) / S) & 1u);   // stage of tile j-2 free
+            load(jn);
+        }
+        cp_async_commit();
+        cp_async_wait_n(PD);       // weights and tiles <= j have landed
+        fence_proxy_async();
+        __syncthreads();
+        if (tid == 0) {
+            tc_fence_after();
+            const uint32_t a0 = sbase + (j % S) * a_bytes;
+            const uint32_t acc = tmem + (uint32_t)((j % NB) * N);
+            int first = 1;
+            for (int tap = 0; tap < ((dbg & 2) ? 0 : 9); ++tap) {
+                const int ky = tap / 3, kx = tap - 3 * ky;
+                const uint32_t arow = a0 + (uint32_t)(ky * cq) * kRowLbo + kx * 16;
+                for (int c = 0; c < cq; c += 2) {
+                    umma(acc, sdesc(arow + c * kRowLbo, kRowLbo, 128),
+                         sdesc(bbase + (tap * cq + c) * C::lbo_b, C::lbo_b, 128), idesc_bf16(N), first ? 0u : 1u);
+                    first = 0;
+                }
+            }
+            umma_commit(&mma_bar[j % S]);
+            umma_commit(&acc_bar[j % NB]);
+        }
+        if (j >= LAG) epilogue(j - LAG);
+    }
+    for (int t = ntl - LAG > 0 ? ntl - LAG : 0; t < ntl; ++t) epilogue(t);
+    __syncthreads();
+    if (warp == 0) tmem_dealloc<C::tcols>(tmem);
+}
+
+template <int N, bool HEAD>
+cudaError_t launch_conv_rows(const bf16 *in, const bf16 *w, float *out, double *part, int64_t npix, int H, int W,
+                             int cin, cudaStream_t st) {
+    const int cq = cin / 8;
+    const size_t a_bytes = 3 * (size_t)cq * kRowLbo, b_bytes = 9 * (size_t)cq * RowCfg<N>::lbo_b;
+    // stages: as many as fit 2 CTAs per SM (<= 110 KB), 3..5 (prefetch distance S-2 <= 3)
+    int S = (int)((110 * 1024 - 1200 - b_bytes) / a_bytes);
+    S = S > 5 ? 5 : S;
+    if (S < 3) S = (int)((220 * 1024 - 1200 - b_bytes) / a_bytes) >= 3 ? 3 : 0;
+    if (S < 3) return cudaErrorInvalidValue;
+    const size_t smem = 1024 + S * a_bytes + b_bytes + 128;
+    static size_t smem_set = 0;
+    static int nsm = 0;
+    if (nsm == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        cudaError_t e = cudaFuncSetAttribute(conv3x3_rows_kernel<N, HEAD>,
+                                             cudaFuncAttributePreferredSharedMemoryCarveout,
+                                             (int)cudaSharedmemCarveoutMaxShared);
+        if (e != cudaSuccess) return e;
+    }
+    if (smem > smem_set) {
+        cudaError_t e = cudaFuncSetAttribute(conv3x3_rows_kernel<N, HEAD>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        smem_set = smem;
+    }
+    int occ = 1;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, conv3x3_rows_kernel<N, HEAD>, 256, smem);
+    if (e != cudaSuccess) return e;
+    occ = occ < 1 ? 1 : (occ > 512 / RowCfg<N>::tcols ? 512 / RowCfg<N>::tcols : occ);   // TMEM columns
+    const int gran = (H * W) % 32 == 0 ? 32 : 1;
+    const int64_t tiles = npix / kBM, slots = (int64_t)nsm * occ;
+    const unsigned grid = (unsigned)(tiles < slots ? tiles : slots);
+    static const int dbg = getenv("UN_DBG") ? atoi(getenv("UN_DBG")) : 0;
+    conv3x3_rows_kernel<N, HEAD><<<grid, 256, smem, st>>>(in, w, out, part, npix, H, W, cin, S, gran, dbg);
+    return cudaGetLastError();
+}
+
+template <int N, bool HEAD>
+cudaError_t launch_conv_any(const bf16 *in, const bf16 *w, float *out, double *part, int64_t npix, int H, int W,
+                            int cin, cudaStream_t st) {
+    static const int norows = getenv("UN_NO_ROWS") ? atoi(getenv("UN_NO_ROWS")) : 0;
+    if (W % kBM == 0 && cin <= 64 && !norows) return launch_conv_rows<N, HEAD>(in, w, out, part, npix, H, W, cin, st);
+    return launch_conv_n<N, HEAD>(in, w, out, part, npix, H, W, cin, st);
+}
+
+cudaError_t launch_conv(const bf16 *in, const bf16 *w, float *out, double *part, int64_t npix, int H, int W, int cin,
+                        int cout, bool head, cudaStream_t st) {
+    if (head) return cout == 16 ? launch_conv_any<16, true>(in, w, out, part, npix, H, W, cin, st) : cudaErrorInvalidValue;
+    switch (cout) {
+        case 16: return launch_conv_any<16, false>(in, w, out, part, npix, H, W, cin, st);
+        case 32: return launch_conv_any<32, false>(in, w, out, part, npix, H, W, cin, st);
+        case 64: return launch_conv_any<64, false>(in, w, out, part, npix, H, W, cin, st);
+        case 128: return launch_conv_any<128, false>(in, w, out, part, npix, H, W, cin, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+// ------------------------------------------------------------------------------------------------
+// element-wise and reduction kernels
+__device__ __forceinline__ float gelu(float u) {   // P:408-411 (tanh form)
+    return 0.5f * u * (1.0f + tanhf(0.7978845608028654f * (u + 0.044715f * u * u * u)));
+}
+
+// history [B][lb][HW] fp32 -> NHWC bf16 with 16 channels (channels >= lb are zero)
+__global__ void pack_input_kernel(const float *__restrict__ hist, bf16 *__restrict__ dst, int64_t npix, int HW,
+                                  int lb) {
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < npix; p += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = p / HW, q = p - b * HW;
+        __align__(16) bf16 v[16];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) v[c] = __float2bfloat16_rn(c < lb ? hist[(b * lb + c) * HW + q] : 0.0f);
+        uint4 *d = reinterpret_cast<uint4 *>(dst + p * 16);
+        d[0] = reinterpret_cast<uint4 *>(v)[0];
+        d[1] = reinterpret_cast<uint4 *>(v)[1];
+    }
+}
+
+// f(dt) = w2 sin(w1 sin(w0 dt + b0) + b1) + b2; cond[b][k] = (w^{Lp} f)_k for all levels
+__global__ void __launch_bounds__(kBasis) time_mlp_kernel(const double *__restrict__ mlp, const double *__restrict__ wl,
+                                                          const float *__restrict__ dt, float *__restrict__ cond,
+                                                          int ctot) {
+    __shared__ double h0[kBasis], h1[kBasis], f[kBasis];
+    const int i = threadIdx.x, b = blockIdx.x;
+    const double *w0 = mlp, *b0 = w0 + kBasis, *w1 = b0 + kBasis, *b1 = w1 + kBasis * kBasis, *w2 = b1 + kBasis,
+                 *b2 = w2 + kBasis * kBasis;
+    h0[i] = sin(w0[i] * (double)dt[b] + b0[i]);
+    __syncthreads();
+    double s = 0.0;
+    for (int j = 0; j < kBasis; ++j) s += w1[i * kBasis + j] * h0[j];
+    h1[i] = sin(s + b1[i]);
+    __syncthreads();
+    s = 0.0;
+    for (int j = 0; j < kBasis; ++j) s += w2[i * kBasis + j] * h1[j];
+    f[i] = s + b2[i];
+    __syncthreads();
+    for (int k = i; k < ctot; k += kBasis) {
+        double a = 0.0;
+        for (int j = 0; j < kBasis; ++j) a += wl[(int64_t)k * kBasis + j] * f[j];
+        cond[(int64_t)b * ctot + k] = (float)a;
+    }
+}
+
+// GroupNorm statistics: per (sample b, group g) the mean and 1/sqrt(var + eps) over the
+// group's channels and all pixels, from the conv epilogue's per-warp fp64 partial sums, summed in a
+// fixed order (deterministic); var = E[u^2] - mu^2 in fp64.
+__global__ void __launch_bounds__(256) gn_reduce_kernel(const double *__restrict__ part, int HW, int gran, int G,
+                                                        int Cg, double *__restrict__ stats) {
+    const int g = blockIdx.x, b = blockIdx.y, nw = HW / gran;
+    const double *pb = part + ((int64_t)b * nw * G + g) * 2;
+    __shared__ double rs[256], rq[256];
+    double s = 0.0, q = 0.0;
+    for (int i = threadIdx.x; i < nw; i += 256) {
+        s += pb[(int64_t)i * G * 2];
+        q += pb[(int64_t)i * G * 2 + 1];
+    }
+    rs[threadIdx.x] = s;
+    rq[threadIdx.x] = q;
+    __syncthreads();
+    for (int k = 128; k > 0; k >>= 1) {
+        if ((int)threadIdx.x < k) {
+            rs[threadIdx.x] += rs[threadIdx.x + k];
+            rq[threadIdx.x] += rq[threadIdx.x + k];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        const double n = (double)Cg * HW, mean = rs[0] / n, var = rq[0] / n - mean * mean;
+        stats[((int64_t)b * G + g) * 2] = mean;
+        stats[((int64_t)b * G + g) * 2 + 1] = 1.0 / sqrt((var > 0.0 ? var : 0.0) + kEps);
+    }
+}
+
+// y = GELU(gamma (x - mu) / sigma + beta) -> bf16 at dA (channel stride sA, offset oA)
+// and, conditioned by cond[b][coff + k], at dB; 8 channels per thread.
+__global__ void gn_apply_kernel(const float *__restrict__ x, int64_t npix, int HW, int C, int G,
+                                const double *__restrict__ stats, const float *__restrict__ gamma,
+                                const float *__restrict__ beta, const float *__restrict__ cond, int ctot, int coff,
+                                bf16 *dA, int sA, int oA, bf16 *dB, int sB, int oB) {
+    const int nq = C >> 3, Cg = C / G;
+    const int64_t total = npix * nq;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t p = i / nq;
+        const int q = (int)(i - p * nq), c0 = q * 8;
+        const int b = (int)(p / HW);
+        const float4 *src = reinterpret_cast<const float4 *>(x + p * C + c0);
+        const float4 v0 = src[0], v1 = src[1];
+        const float xv[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+        __align__(16) bf16 ya[8], yb[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int k = c0 + j, g = k / Cg;
+            const float mu = (float)stats[((int64_t)b * G + g) * 2], rs = (float)stats[((int64_t)b * G + g) * 2 + 1];
+            const float y = gelu((xv[j] - mu) * rs * gamma[k] + beta[k]);
+            ya[j] = __float2bfloat16_rn(y);
+            if (dB) yb[j] = __float2bfloat16_rn(y * cond[(int64_t)b * ctot + coff + k]);
+        }
+        if (dA) *reinterpret_cast<uint4 *>(dA + p * sA + oA + c0) = *reinterpret_cast<uint4 *>(ya);
+        if (dB) *reinterpret_cast<uint4 *>(dB + p * sB + oB + c0) = *reinterpret_cast<uint4 *>(yb);
+    }
+}
+
+// output head: GN over the single output channel (G = 1, no activation) -> fp32 [B][HW]
+__global__ void head_out_kernel(const float *__restrict__ x, int cstride, int64_t npix, int HW,
+                                const double *__restrict__ stats, const float *__restrict__ gamma,
+                                const float *__restrict__ beta, float *__restrict__ out) {
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < npix; p += (int64_t)gridDim.x * blockDim.x) {
+        const int b = (int)(p / HW);
+        out[p] = (float)(((double)x[p * cstride] - stats[2 * b]) * stats[2 * b + 1]) * gamma[0] + beta[0];
+    }
+}
+
+// 2x2 max pooling, stride 2: [B][H][W][C] -> [B][H/2][W/2][C], 8 channels per thread
+__global__ void maxpool_kernel(const bf16 *__restrict__ src, bf16 *__restrict__ dst, int B, int H, int W, int C) {
+    const int h = H / 2, w = W / 2, nq = C >> 3;
+    const int64_t total = (int64_t)B * h * w * nq;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t po = i / nq;
+        const int q = (int)(i - po * nq);
+        const int b = (int)(po / ((int64_t)h * w)), rem = (int)(po - (int64_t)b * h * w), yo = rem / w, xo = rem - yo * w;
+        __align__(16) bf16 m[8];
+        for (int dy = 0; dy < 2; ++dy)
+            for (int dx = 0; dx < 2; ++dx) {
+                const int64_t pi = ((int64_t)b * H + 2 * yo + dy) * W + 2 * xo + dx;
+                __align__(16) bf16 v[8];
+                *reinterpret_cast<uint4 *>(v) = *reinterpret_cast<const uint4 *>(src + pi * C + q * 8);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) m[j] = (dy | dx) ? __hmax(m[j], v[j]) : v[j];
+            }
+        *reinterpret_cast<uint4 *>(dst + po * C + q * 8) = *reinterpret_cast<uint4 *>(m);
+    }
+}
+
+// up(u)_{k, 2i+m, 2j+n} = u_{k,i,j} w_{m,n} (R-31): [B][h][w][C] -> dst [B][2h][2w] (stride sD, offset oD)
+__global__ void up_kernel(const bf16 *__restrict__ src, int B, int h, int w, int C, const float *__restrict__ wt,
+                          bf16 *__restrict__ dst, int sD, int oD) {
+    const int nq = C >> 3;
+    const int64_t total = (int64_t)B * h * w * nq;
+    const float w00 = wt[0], w01 = wt[1], w10 = wt[2], w11 = wt[3];
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t pi = i / nq;
+        const int q = (int)(i - pi * nq);
+        const int b = (int)(pi / ((int64_t)h * w)), rem = (int)(pi - (int64_t)b * h * w), yi = rem / w, xi = rem - yi * w;
+        __align__(16) bf16 v[8];
+        *reinterpret_cast<uint4 *>(v) = *reinterpret_cast<const uint4 *>(src + pi * C + q * 8);
+        const float ws[4] = {w00, w01, w10, w11};
+#pragma unroll
+        for (int mn = 0; mn < 4; ++mn) {
+            const int m = mn >> 1, n = mn & 1;
+            const int64_t po = ((int64_t)b * 2 * h + 2 * yi + m) * (2 * w) + 2 * xi + n;
+            __align__(16) bf16 o[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) o[j] = __float2bfloat16_rn(__bfloat162float(v[j]) * ws[mn]);
+            *reinterpret_cast<uint4 *>(dst + po * sD + oD + q * 8) = *reinterpret_cast<uint4 *>(o);
+        }
+    }
+}
+
+int grid_for(int64_t n, int bs) {
+    const int64_t g = (n + bs - 1) / bs;
+    return (int)(g > 148 * 64 ? 148 * 64 : (g < 1 ? 1 : g));
+}
+
+std::string g_err;
+
+std::string fmt(const char *f, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, f);
+    vsnprintf(buf, sizeof buf, f, ap);
+    va_end(ap);
+    return buf;
+}
+
+enum Layer { kEnc1, kEnc2, kEnc3, kEnc4, kDec4, kDec3, kDec2, kHead1, kHead2, kLayers };
+
+}  // namespace
+}  // namespace un
+
+using namespace un;
+
+struct un_ctx {
+    un_params p{};
+    cudaStream_t st = nullptr;
+    int cin[kLayers], cout[kLayers], cin_pad[kLayers], cout_pad[kLayers];
+    bf16 *w[kLayers] = {};
+    float *gam[kLayers] = {}, *bet[kLayers] = {};
+    double *mlp = nullptr, *wl = nullptr;
+    float *upw = nullptr;        // 3 x 4
+    int ctot = 0, coff[4] = {0, 0, 0, 0};
+    bool have_w = false;
+    // activations
+    bf16 *in0 = nullptr, *z[3] = {}, *pin[3] = {}, *cat[3] = {}, *z4c = nullptr, *dec[4] = {};
+    float *raw = nullptr, *cond = nullptr, *dout = nullptr, *dhist = nullptr, *ddt = nullptr;
+    double *stats = nullptr, *part = nullptr;   // GN statistics, per-warp partial sums
+    float *h_in = nullptr, *h_out = nullptr;   // pinned staging of un_forward / un_rollout
+    std::string err;
+    int64_t launches = 0;
+    // profiling
+    bool prof = false;
+    std::vector<cudaEvent_t> pool;
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> rec;
+    double flops = 0.0;
+};
+
+namespace {
+
+pf_status fail(un_ctx *c, pf_status s, const std::string &m) {
+    if (c) c->err = m;
+    else g_err = m;
+    return s;
+}
+#define UCK(c, call)                                                                                     \
+    do {                                                                                                 \
+        cudaError_t e_ = (call);                                                                         \
+        if (e_ != cudaSuccess) return fail(c, PF_ERR_CUDA, fmt("%s: %s", #call, cudaGetErrorString(e_))); \
+    } while (0)
+
+cudaEvent_t take_event(un_ctx *c) {
+    if (!c->pool.empty()) {
+        cudaEvent_t e = c->pool.back();
+        c->pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+int level_of(int l) {   // spatial level (0 = full resolution) of conv layer l
+    static const int lv[kLayers] = {0, 1, 2, 3, 3, 2, 1, 0, 0};
+    return lv[l];
+}
+
+pf_status conv_layer(un_ctx *c, int l, const bf16 *in, int B) {
+    const int lv = level_of(l), H = c->p.height >> lv, W = c->p.width >> lv;
+    const int64_t npix = (int64_t)B * H * W;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (c->prof) {
+        e0 = take_event(c);
+        e1 = take_event(c);
+        UCK(c, cudaEventRecord(e0, c->st));
+    }
+    const bool head = l == kHead2;
+    UCK(c, launch_conv(in, c->w[l], c->raw, c->part, npix, H, W, c->cin_pad[l], c->cout_pad[l], head, c->st));
+    if (c->prof) {
+        UCK(c, cudaEventRecord(e1, c->st));
+        c->rec.push_back({0, {e0, e1}});
+    }
+    const int G = head ? 1 : kGroups;
+    const int Cg = head ? 1 : c->cout[l] / kGroups;
+    gn_reduce_kernel<<<dim3(G, B), 256, 0, c->st>>>(c->part, H * W, (H * W) % 32 == 0 ? 32 : 1, G, Cg, c->stats);
+    c->launches += 2;
+    return PF_OK;
+}
+
+pf_status apply_layer(un_ctx *c, int l, int B, int cond_level, bf16 *dA, int sA, int oA, bf16 *dB, int sB, int oB) {
+    const int lv = level_of(l), HW = (c->p.height >> lv) * (c->p.width >> lv);
+    const int64_t npix = (int64_t)B * HW;
+    const int C = c->cout[l];
+    gn_apply_kernel<<<grid_for(npix * (C / 8), 256), 256, 0, c->st>>>(
+        c->raw, npix, HW, C, kGroups, c->stats, c->gam[l], c->bet[l], c->cond, c->ctot,
+        cond_level >= 0 ? c->coff[cond_level] : 0, dA, sA, oA, dB, sB, oB);
+    c->launches += 1;
+    return PF_OK;
+}
+
+pf_status pool_layer(un_ctx *c, const bf16 *src, bf16 *dst, int B, int lv, int C) {
+    const int H = c->p.height >> lv, W = c->p.width >> lv;
+    maxpool_kernel<<<grid_for((int64_t)B * (H / 2) * (W / 2) * (C / 8), 256), 256, 0, c->st>>>(src, dst, B, H, W, C);
+    c->launches += 1;
+    return PF_OK;
+}
+
+pf_status up_layer(un_ctx *c, const bf16 *src, int B, int lv_src, int C, int which, bf16 *dst, int sD, int oD) {
+    const int h = c->p.height >> lv_src, w = c->p.width >> lv_src;
+    up_kernel<<<grid_for((int64_t)B * h * w * (C / 8), 256), 256, 0, c->st>>>(src, B, h, w, C, c->upw + 4 * which, dst,
+                                                                              sD, oD);
+    c->launches += 1;
+    return PF_OK;
+}
+
+// The forward pass on device buffers: c->dhist -> c->dout.
+pf_status forward(un_ctx *c, int B, const float *hist, const float *dt, float *out) {
+    const int C1 = c->p.widths[0], C2 = c->p.widths[1], C3 = c->p.widths[2], C4 = c->p.widths[3];
+    const int64_t HW = (int64_t)c->p.height * c->p.width;
+    cudaEvent_t f0 = nullptr, f1 = nullptr;
+    if (c->prof) {
+        f0 = take_event(c);
+        f1 = take_event(c);
+        UCK(c, cudaEventRecord(f0, c->st));
+    }
+    pack_input_kernel<<<grid_for((int64_t)B * HW, 256), 256, 0, c->st>>>(hist, c->in0, (int64_t)B * HW, (int)HW,
+                                                                         c->p.lb);
+    time_mlp_kernel<<<B, kBasis, 0, c->st>>>(c->mlp, c->wl, dt, c->cond, c->ctot);
+    c->launches += 2;
+    pf_status s;
+    // encoder + conditioning: z_p unconditioned (pooling input), z_p (.) s_p
+    // into the first half of the level's concatenation buffer
+    if ((s = conv_layer(c, kEnc1, c->in0, B)) || (s = apply_layer(c, kEnc1, B, 0, c->z[0], C1, 0, c->cat[0], 2 * C1, 0)))
+        return s;
+    if ((s = pool_layer(c, c->z[0], c->pin[0], B, 0, C1))) return s;
+    if ((s = conv_layer(c, kEnc2, c->pin[0], B)) || (s = apply_layer(c, kEnc2, B, 1, c->z[1], C2, 0, c->cat[1], 2 * C2, 0)))
+        return s;
+    if ((s = pool_layer(c, c->z[1], c->pin[1], B, 1, C2))) return s;
+    if ((s = conv_layer(c, kEnc3, c->pin[1], B)) || (s = apply_layer(c, kEnc3, B, 2, c->z[2], C3, 0, c->cat[2], 2 * C3, 0)))
+        return s;
+    if ((s = pool_layer(c, c->z[2], c->pin[2], B, 2, C3))) return s;
+    if ((s = conv_layer(c, kEnc4, c->pin[2], B)) || (s = apply_layer(c, kEnc4, B, 3, nullptr, 0, 0, c->z4c, C4, 0)))
+        return s;
+    // decoder: d^{L3} = up(conv_block(z4)), d^{Lp} = up(conv_block(z^{Lp+1} (+) d^{Lp+1}))
+    if ((s = conv_layer(c, kDec4, c->z4c, B)) || (s = apply_layer(c, kDec4, B, -1, c->dec[0], C3, 0, nullptr, 0, 0)) ||
+        (s = up_layer(c, c->dec[0], B, 3, C3, 0, c->cat[2], 2 * C3, C3)))
+        return s;
+    if ((s = conv_layer(c, kDec3, c->cat[2], B)) || (s = apply_layer(c, kDec3, B, -1, c->dec[1], C2, 0, nullptr, 0, 0)) ||
+        (s = up_layer(c, c->dec[1], B, 2, C2, 1, c->cat[1], 2 * C2, C2)))
+        return s;
+    if ((s = conv_layer(c, kDec2, c->cat[1], B)) || (s = apply_layer(c, kDec2, B, -1, c->dec[2], C1, 0, nullptr, 0, 0)) ||
+        (s = up_layer(c, c->dec[2], B, 1, C1, 2, c->cat[0], 2 * C1, C1)))
+        return s;
+    // output: GN(conv(conv_block(z^{L1} (+) d^{L1})))
+    if ((s = conv_layer(c, kHead1, c->cat[0], B)) || (s = apply_layer(c, kHead1, B, -1, c->dec[3], C1, 0, nullptr, 0, 0)))
+        return s;
+    if ((s = conv_layer(c, kHead2, c->dec[3], B))) return s;
+    head_out_kernel<<<grid_for((int64_t)B * HW, 256), 256, 0, c->st>>>(c->raw, c->cout_pad[kHead2], (int64_t)B * HW,
+                                                                       (int)HW, c->stats, c->gam[kHead2],
+                                                                       c->bet[kHead2], out);
+    c->launches += 1;
+    UCK(c, cudaGetLastError());
+    if (c->prof) {
+        UCK(c, cudaEventRecord(f1, c->st));
+        c->rec.push_back({1, {f0, f1}});
+    }
+    return PF_OK;
+}
+
+template <typename T>
+pf_status dalloc(un_ctx *c, T **p, size_t n) {
+    if (cudaMalloc((void **)p, n * sizeof(T)) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(c, PF_ERR_NOMEM, fmt("cudaMalloc of %zu bytes failed", n * sizeof(T)));
+    }
+    return PF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+pf_status un_default_params(un_params *o) {
+    if (!o) return PF_ERR_ARG;
+    un_params p{};
+    p.abi_version = UN_ABI_VERSION;
+    p.lb = 3;
+    p.widths[0] = 16;
+    p.widths[1] = 32;
+    p.widths[2] = 64;
+    p.widths[3] = 128;
+    p.height = p.width = 256;
+    p.max_batch = 64;
+    p.device = 0;
+    *o = p;
+    return PF_OK;
+}
+
+int64_t un_blob_size(const un_params *p) {
+    if (!p) return -1;
+    const int c1 = p->widths[0], c2 = p->widths[1], c3 = p->widths[2], c4 = p->widths[3];
+    const int ci[kLayers] = {p->lb, c1, c2, c3, c4, 2 * c3, 2 * c2, 2 * c1, c1};
+    const int co[kLayers] = {c1, c2, c3, c4, c3, c2, c1, c1, 1};
+    int64_t n = 0;
+    for (int l = 0; l < kLayers; ++l) n += (int64_t)co[l] * 9 * ci[l] + 2 * co[l];
+    n += (int64_t)(c1 + c2 + c3 + c4) * kBasis + 12;
+    n += 4 * kBasis + 2 * (int64_t)kBasis * kBasis;
+    return n;
+}
+
+pf_status un_create(const un_params *p, un_ctx **out) {
+    if (!p || !out) return fail(nullptr, PF_ERR_ARG, "NULL argument");
+    *out = nullptr;
+    if (p->abi_version != UN_ABI_VERSION) return fail(nullptr, PF_ERR_ABI, "un_params.abi_version mismatch");
+    if (p->lb < 1 || p->lb > 16) return fail(nullptr, PF_ERR_ARG, "lb must be in 1..16");
+    for (int i = 0; i < 4; ++i)
+        if (p->widths[i] < 16 || p->widths[i] > 128 || p->widths[i] % 16)
+            return fail(nullptr, PF_ERR_ARG, "widths must be multiples of 16 in 16..128");
+    if (p->height < 8 || p->width < 8 || p->height % 8 || p->width % 8)
+        return fail(nullptr, PF_ERR_ARG, "height and width must be positive multiples of 8");
+    if (p->max_batch < 1) return fail(nullptr, PF_ERR_ARG, "max_batch must be >= 1");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return fail(nullptr, PF_ERR_CUDA, "no CUDA device (the U-Net path has no CPU fallback)");
+    }
+    if (p->device < 0 || p->device >= ndev) return fail(nullptr, PF_ERR_ARG, "device out of range");
+    cudaSetDevice(p->device);
+    un_ctx *c = new un_ctx();
+    c->p = *p;
+    const int c1 = p->widths[0], c2 = p->widths[1], c3 = p->widths[2], c4 = p->widths[3];
+    const int ci[kLayers] = {p->lb, c1, c2, c3, c4, 2 * c3, 2 * c2, 2 * c1, c1};
+    const int co[kLayers] = {c1, c2, c3, c4, c3, c2, c1, c1, 1};
+    for (int l = 0; l < kLayers; ++l) {
+        c->cin[l] = ci[l];
+        c->cout[l] = co[l];
+        c->cin_pad[l] = (ci[l] + 15) / 16 * 16;
+        c->cout_pad[l] = co[l] < 16 ? 16 : co[l];
+    }
+    c->ctot = c1 + c2 + c3 + c4;
+    c->coff[0] = 0;
+    c->coff[1] = c1;
+    c->coff[2] = c1 + c2;
+    c->coff[3] = c1 + c2 + c3;
+    auto bad = [&](pf_status s) {
+        g_err = c->err;
+        un_free(c);
+        return s;
+    };
+    if (cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking) != cudaSuccess) {
+        c->err = "cudaStreamCreate failed";
+        return bad(PF_ERR_CUDA);
+    }
+    const int64_t B = p->max_batch, H = p->height, W = p->width;
+    auto hw = [&](int lv) { return (H >> lv) * (W >> lv); };
+    pf_status s = PF_OK;
+    for (int l = 0; l < kLayers && s == PF_OK; ++l) {
+        s = dalloc(c, &c->w[l], (size_t)c->cout_pad[l] * 9 * c->cin_pad[l]);
+        if (s == PF_OK) s = dalloc(c, &c->gam[l], (size_t)c->cout_pad[l]);
+        if (s == PF_OK) s = dalloc(c, &c->bet[l], (size_t)c->cout_pad[l]);
+    }
+    if (s == PF_OK) s = dalloc(c, &c->mlp, (size_t)4 * kBasis + 2 * kBasis * kBasis);
+    if (s == PF_OK) s = dalloc(c, &c->wl, (size_t)c->ctot * kBasis);
+    if (s == PF_OK) s = dalloc(c, &c->upw, 12);
+    if (s == PF_OK) s = dalloc(c, &c->in0, (size_t)(B * hw(0) * 16));
+    const int Cl[4] = {c1, c2, c3, c4};
+    for (int q = 0; q < 3 && s == PF_OK; ++q) {
+        s = dalloc(c, &c->z[q], (size_t)(B * hw(q) * Cl[q]));
+        if (s == PF_OK) s = dalloc(c, &c->pin[q], (size_t)(B * hw(q + 1) * Cl[q]));
+        if (s == PF_OK) s = dalloc(c, &c->cat[q], (size_t)(B * hw(q) * 2 * Cl[q]));
+    }
+    if (s == PF_OK) s = dalloc(c, &c->z4c, (size_t)(B * hw(3) * c4));
+    if (s == PF_OK) s = dalloc(c, &c->dec[0], (size_t)(B * hw(3) * c3));
+    if (s == PF_OK) s = dalloc(c, &c->dec[1], (size_t)(B * hw(2) * c2));
+    if (s == PF_OK) s = dalloc(c, &c->dec[2], (size_t)(B * hw(1) * c1));
+    if (s == PF_OK) s = dalloc(c, &c->dec[3], (size_t)(B * hw(0) * c1));
+    int64_t rawmax = 0;
+    for (int l = 0; l < kLayers; ++l) {
+        const int64_t n = B * hw(level_of(l)) * c->cout_pad[l];
+        rawmax = n > rawmax ? n : rawmax;
+    }
+    if (s == PF_OK) s = dalloc(c, &c->raw, (size_t)rawmax);
+    if (s == PF_OK) s = dalloc(c, &c->cond, (size_t)(B * c->ctot));
+    if (s == PF_OK) s = dalloc(c, &c->stats, (size_t)(B * kGroups * 2));
+    int64_t pmax = 0;   // per-unit partial statistics of the largest layer
+    for (int lv = 0; lv < 4; ++lv) {
+        const int64_t n = B * hw(lv) / (hw(lv) % 32 == 0 ? 32 : 1) * kGroups * 2;
+        pmax = n > pmax ? n : pmax;
+    }
+    if (s == PF_OK) s = dalloc(c, &c->part, (size_t)pmax);
+    if (s == PF_OK) s = dalloc(c, &c->dout, (size_t)(B * hw(0)));
+    if (s == PF_OK) s = dalloc(c, &c->dhist, (size_t)(B * p->lb * hw(0)));
+    if (s == PF_OK) s = dalloc(c, &c->ddt, (size_t)B);
+    if (s != PF_OK) return bad(s);
+    // padded weight rows / channels stay zero
+    for (int l = 0; l < kLayers; ++l) {
+        cudaMemset(c->w[l], 0, (size_t)c->cout_pad[l] * 9 * c->cin_pad[l] * sizeof(bf16));
+        cudaMemset(c->gam[l], 0, c->cout_pad[l] * sizeof(float));
+        cudaMemset(c->bet[l], 0, c->cout_pad[l] * sizeof(float));
+    }
+    // conv FLOPs per sample (algorithmic: unpadded channels, 2 flops per multiply-add)
+    double fl = 0.0;
+    for (int l = 0; l < kLayers; ++l) fl += 2.0 * 9.0 * ci[l] * co[l] * (double)hw(level_of(l));
+    c->flops = fl;
+    if (cudaDeviceSynchronize() != cudaSuccess) {
+        c->err = "device synchronize failed after allocation";
+        return bad(PF_ERR_CUDA);
+    }
+    *out = c;
+    return PF_OK;
+}
+
+pf_status un_set_weights(un_ctx *c, const float *blob, int64_t n) {
+    if (!c || !blob) return fail(c, PF_ERR_ARG, "NULL argument");
+    if (n != un_blob_size(&c->p)) return fail(c, PF_ERR_ARG, fmt("blob has %lld floats, expected %lld", (long long)n,
+                                                                  (long long)un_blob_size(&c->p)));
+    cudaSetDevice(c->p.device);
+    const float *q = blob;
+    for (int l = 0; l < kLayers; ++l) {
+        const int ci = c->cin[l], co = c->cout[l], cip = c->cin_pad[l], cop = c->cout_pad[l];
+        std::vector<bf16> wb((size_t)cop * 9 * cip, __float2bfloat16_rn(0.0f));
+        for (int o = 0; o < co; ++o)
+            for (int t = 0; t < 9; ++t)
+                for (int i = 0; i < ci; ++i) wb[((size_t)o * 9 + t) * cip + i] = __float2bfloat16_rn(q[((size_t)o * 9 + t) * ci + i]);
+        q += (size_t)co * 9 * ci;
+        UCK(c, cudaMemcpy(c->w[l], wb.data(), wb.size() * sizeof(bf16), cudaMemcpyHostToDevice));
+        UCK(c, cudaMemcpy(c->gam[l], q, co * sizeof(float), cudaMemcpyHostToDevice));
+        q += co;
+        UCK(c, cudaMemcpy(c->bet[l], q, co * sizeof(float), cudaMemcpyHostToDevice));
+        q += co;
+    }
+    std::vector<double> wl((size_t)c->ctot * kBasis);
+    for (size_t i = 0; i < wl.size(); ++i) wl[i] = q[i];
+    q += wl.size();
+    UCK(c, cudaMemcpy(c->wl, wl.data(), wl.size() * sizeof(double), cudaMemcpyHostToDevice));
+    UCK(c, cudaMemcpy(c->upw, q, 12 * sizeof(float), cudaMemcpyHostToDevice));
+    q += 12;
+    std::vector<double> mlp((size_t)4 * kBasis + 2 * kBasis * kBasis);
+    for (size_t i = 0; i < mlp.size(); ++i) mlp[i] = q[i];
+    q += mlp.size();
+    UCK(c, cudaMemcpy(c->mlp, mlp.data(), mlp.size() * sizeof(double), cudaMemcpyHostToDevice));
+    c->have_w = true;
+    return PF_OK;
+}
+
+pf_status un_forward_device(un_ctx *c, int32_t batch, const float *hist, const float *dt, float *out) {
+    if (!c || !hist || !dt || !out) return fail(c, PF_ERR_ARG, "NULL argument");
+    if (batch < 1 || batch > c->p.max_batch) return fail(c, PF_ERR_ARG, "batch out of range");
+    if (!c->have_w) return fail(c, PF_ERR_STATE, "no weights: call un_set_weights first");
+    cudaSetDevice(c->p.device);
+    return forward(c, batch, hist, dt, out);
+}
+
+pf_status un_forward(un_ctx *c, int32_t batch, const float *hist, const float *dt, float *out) {
+    if (!c || !hist || !dt || !out) return fail(c, PF_ERR_ARG, "NULL argument");
+    if (batch < 1 || batch > c->p.max_batch) return fail(c, PF_ERR_ARG, "batch out of range");
+    cudaSetDevice(c->p.device);
+    const size_t hw = (size_t)c->p.height * c->p.width;
+    UCK(c, cudaMemcpyAsync(c->dhist, hist, (size_t)batch * c->p.lb * hw * sizeof(float), cudaMemcpyHostToDevice, c->st));
+    UCK(c, cudaMemcpyAsync(c->ddt, dt, (size_t)batch * sizeof(float), cudaMemcpyHostToDevice, c->st));
+    pf_status s = un_forward_device(c, batch, c->dhist, c->ddt, c->dout);
+    if (s != PF_OK) return s;
+    UCK(c, cudaMemcpyAsync(out, c->dout, (size_t)batch * hw * sizeof(float), cudaMemcpyDeviceToHost, c->st));
+    UCK(c, cudaStreamSynchronize(c->st));
+    return PF_OK;
+}
+
+pf_status un_rollout(un_ctx *c, int32_t batch, const float *hist, int32_t lf, int32_t n_leaps, float *out) {
+    if (!c || !hist || !out) return fail(c, PF_ERR_ARG, "NULL argument");
+    if (batch < 1 || batch > c->p.max_batch) return fail(c, PF_ERR_ARG, "batch out of range");
+    if (lf < c->p.lb || n_leaps < 1) return fail(c, PF_ERR_ARG, "need lf >= lb and n_leaps >= 1");
+    if (!c->have_w) return fail(c, PF_ERR_STATE, "no weights: call un_set_weights first");
+    cudaSetDevice(c->p.device);
+    const int lb = c->p.lb;
+    const size_t hw = (size_t)c->p.height * c->p.width;
+    float *win = nullptr, *pred = nullptr, *dts = nullptr;
+    pf_status s = dalloc(c, &win, (size_t)batch * lb * hw);
+    if (s == PF_OK) s = dalloc(c, &pred, (size_t)lf * batch * hw);
+    if (s == PF_OK) s = dalloc(c, &dts, (size_t)lf * batch);
+    if (s == PF_OK) {
+        std::vector<float> hd((size_t)lf * batch);
+        for (int q = 0; q < lf; ++q)
+            for (int b = 0; b < batch; ++b) hd[(size_t)q * batch + b] = (float)(q + 1);
+        if (cudaMemcpyAsync(win, hist, (size_t)batch * lb * hw * sizeof(float), cudaMemcpyHostToDevice, c->st) !=
+                cudaSuccess ||
+            cudaMemcpyAsync(dts, hd.data(), hd.size() * sizeof(float), cudaMemcpyHostToDevice, c->st) != cudaSuccess)
+            s = fail(c, PF_ERR_CUDA, "rollout upload failed");
+        if (s == PF_OK) cudaStreamSynchronize(c->st);
+    }
+    for (int leap = 0; leap < n_leaps && s == PF_OK; ++leap) {
+        for (int q = 0; q < lf && s == PF_OK; ++q)   // dt = q + 1 on the same window
+            s = forward(c, batch, win, dts + (size_t)q * batch, pred + (size_t)q * batch * hw);
+        // outputs [b][leap*lf + q]; next window = predictions lf-lb .. lf-1, channel order oldest first
+        for (int q = 0; q < lf && s == PF_OK; ++q)
+            if (cudaMemcpy2DAsync(out + ((size_t)leap * lf + q) * hw, (size_t)n_leaps * lf * hw * sizeof(float),
+                                  pred + (size_t)q * batch * hw, hw * sizeof(float), hw * sizeof(float), batch,
+                                  cudaMemcpyDeviceToHost, c->st) != cudaSuccess)
+                s = fail(c, PF_ERR_CUDA, "rollout download failed");
+        for (int t = 0; t < lb && s == PF_OK; ++t)
+            if (cudaMemcpy2DAsync(win + (size_t)t * hw, (size_t)lb * hw * sizeof(float),
+                                  pred + (size_t)(lf - lb + t) * batch * hw, hw * sizeof(float), hw * sizeof(float),
+                                  batch, cudaMemcpyDeviceToDevice, c->st) != cudaSuccess)
+                s = fail(c, PF_ERR_CUDA, "rollout window shift failed");
+    }
+    if (cudaStreamSynchronize(c->st) != cudaSuccess && s == PF_OK) s = fail(c, PF_ERR_CUDA, "rollout failed");
+    cudaFree(win);
+    cudaFree(pred);
+    cudaFree(dts);
+    return s;
+}
+
+pf_status un_conv3x3(const uint16_t *in, int32_t batch, int32_t H, int32_t W, int32_t cin, const uint16_t *w,
+                     int32_t cout, float *out, void *stream) {
+    if (!in || !w || !out || batch < 1 || H < 1 || W < 1 || cin < 16 || cin % 16)
+        return fail(nullptr, PF_ERR_ARG, "bad un_conv3x3 arguments (cin must be a multiple of 16)");
+    if (cout != 16 && cout != 32 && cout != 64 && cout != 128) return fail(nullptr, PF_ERR_ARG, "cout must be 16/32/64/128");
+    const int64_t npix = (int64_t)batch * H * W;
+    double *part = nullptr;   // epilogue statistics are not returned here
+    if (cudaMalloc(&part, (size_t)(npix * kGroups * 2) * sizeof(double)) != cudaSuccess)
+        return fail(nullptr, PF_ERR_NOMEM, "cudaMalloc of statistics scratch failed");
+    cudaError_t e = launch_conv(reinterpret_cast<const bf16 *>(in), reinterpret_cast<const bf16 *>(w), out, part,
+                                npix, H, W, cin, cout, false, (cudaStream_t)stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize((cudaStream_t)stream);
+    cudaFree(part);
+    if (e != cudaSuccess) return fail(nullptr, PF_ERR_CUDA, fmt("conv launch: %s", cudaGetErrorString(e)));
+    return PF_OK;
+}
+
+pf_status un_stream(un_ctx *c, void **stream) {
+    if (!c || !stream) return PF_ERR_ARG;
+    *stream = (void *)c->st;
+    return PF_OK;
+}
+
+pf_status un_launch_count(un_ctx *c, int64_t *launches) {
+    if (!c || !launches) return PF_ERR_ARG;
+    *launches = c->launches;
+    return PF_OK;
+}
+
+pf_status un_profile(un_ctx *c, int32_t enable) {
+    if (!c) return PF_ERR_ARG;
+    cudaStreamSynchronize(c->st);
+    for (auto &r : c->rec) {
+        c->pool.push_back(r.second.first);
+        c->pool.push_back(r.second.second);
+    }
+    c->rec.clear();
+    c->prof = enable != 0;
+    return PF_OK;
+}
+
+pf_status un_profile_read(un_ctx *c, double out[4]) {
+    if (!c || !out) return PF_ERR_ARG;
+    UCK(c, cudaStreamSynchronize(c->st));
+    double conv = 0.0, fwd = 0.0, n = 0.0;
+    for (auto &r : c->rec) {
+        float ms = 0.0f;
+        UCK(c, cudaEventElapsedTime(&ms, r.second.first, r.second.second));
+        if (r.first == 0) conv += ms;
+        else {
+            fwd += ms;
+            n += 1.0;
+        }
+    }
+    out[0] = conv;
+    out[1] = fwd;
+    out[2] = n;
+    out[3] = c->flops;
+    return PF_OK;
+}
+
+const char *un_last_error(const un_ctx *c) { return c ? c->err.c_str() : g_err.c_str(); }
+
+void un_free(un_ctx *c) {
+    if (!c) return;
+    if (c->st) cudaStreamSynchronize(c->st);
+    for (int l = 0; l < kLayers; ++l) {
+        cudaFree(c->w[l]);
+        cudaFree(c->gam[l]);
+        cudaFree(c->bet[l]);
+    }
+    cudaFree(c->mlp);
+    cudaFree(c->wl);
+    cudaFree(c->upw);
+    cudaFree(c->in0);
+    for (int q = 0; q < 3; ++q) {
+        cudaFree(c->z[q]);
+        cudaFree(c->pin[q]);
+        cudaFree(c->cat[q]);
+    }
+    cudaFree(c->z4c);
+    for (int q = 0; q < 4; ++q) cudaFree(c->dec[q]);
+    cudaFree(c->raw);
+    cudaFree(c->cond);
+    cudaFree(c->stats);
+    cudaFree(c->part);
+    cudaFree(c->dout);
+    cudaFree(c->dhist);
+    cudaFree(c->ddt);
+    for (auto e : c->pool) cudaEventDestroy(e);
+    for (auto &r : c->rec) {
+        cudaEventDestroy(r.second.first);
+        cudaEventDestroy(r.second.second);
+    }
+    if (c->st) cudaStreamDestroy(c->st);
+    delete c;
+}
+
+}  // extern "C"
