@@ -149,15 +149,13 @@ __device__ __forceinline__ void cp_async_wait_n(int n) {   // n <= 3
 // tl & 1: wait for its MMAs, tcgen05.ld (warp w reads lanes 32 (w & 3) .. +31; with N >= 32 the
 // warps w and w + 4 split the columns), fp32 stores, GroupNorm partial sums (see above).
 template <int N, bool HEAD>
-__device__ __forceinline__ void conv_epilogue(uint32_t tacc, uint64_t *bar, uint32_t parity, int64_t t, int64_t npix,
-                                              float *__restrict__ out, double *__restrict__ part, int gran) {
+__device__ __forceinline__ void conv_tile_out(uint32_t tacc, int64_t t, int64_t npix, float *__restrict__ out,
+                                              double *__restrict__ part, int gran, int sel) {
     constexpr int NG = HEAD ? 1 : kGroups, GC = HEAD ? 1 : N / kGroups;
     constexpr int ECOLS = N >= 32 ? N / 2 : N;                       // epilogue columns per warp
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    mbar_wait(bar, parity);
-    tc_fence_after();
     const int lq = warp & 3, hv = warp >> 2;
-    if (N >= 32 || hv == 0) {
+    if (N >= 32 || hv == sel) {
         const int64_t p = t * kBM + 32 * lq + lane;
         const bool pv = p < npix;
         const int c0 = N >= 32 ? hv * ECOLS : 0;
@@ -166,9 +164,9 @@ __device__ __forceinline__ void conv_epilogue(uint32_t tacc, uint64_t *bar, uint
         // groups owned by this warp: all (N = 16) or the half [2 hv, 2 hv + 2) (N >= 32)
         constexpr int G0N = N >= 32 ? NG / 2 : NG;
         const int g0 = N >= 32 ? hv * G0N : 0;
-        double gs[G0N], gq[G0N];
+        float fs[G0N], fq[G0N];   // per pixel: <= 32 terms, fp32; fp64 across pixels
 #pragma unroll
-        for (int g = 0; g < G0N; ++g) gs[g] = gq[g] = 0.0;
+        for (int g = 0; g < G0N; ++g) fs[g] = fq[g] = 0.0f;
 #pragma unroll
         for (int c = 0; c < ECOLS; c += 16) {
             uint32_t r[16];
@@ -183,11 +181,17 @@ __device__ __forceinline__ void conv_epilogue(uint32_t tacc, uint64_t *bar, uint
                 for (int j = 0; j < 16; ++j) {
                     const int lc = c + j;     // column relative to c0 (compile-time after unrolling)
                     if (HEAD && lc > 0) continue;
-                    const double v = (double)__uint_as_float(r[j]);
-                    gs[lc / GC] += v;
-                    gq[lc / GC] += v * v;
+                    const float v = __uint_as_float(r[j]);
+                    fs[lc / GC] += v;
+                    fq[lc / GC] = fmaf(v, v, fq[lc / GC]);
                 }
             }
+        }
+        double gs[G0N], gq[G0N];
+#pragma unroll
+        for (int g = 0; g < G0N; ++g) {
+            gs[g] = (double)fs[g];
+            gq[g] = (double)fq[g];
         }
         if (gran == 1) {
             if (pv)
@@ -212,7 +216,6 @@ __device__ __forceinline__ void conv_epilogue(uint32_t tacc, uint64_t *bar, uint
                 }
         }
     }
-    tc_fence_before();
 }
 
 // Epilogue statistics: the sum and the sum of squares (fp64) of each GroupNorm group's channels per
@@ -306,8 +309,11 @@ __global__ void __launch_bounds__(256) conv3x3_kernel(const bf16 *__restrict__ i
     };
 
     auto epilogue = [&](int tl) {
-        conv_epilogue<N, HEAD>(tmem + (uint32_t)((tl & 1) * N), &acc_bar[tl & 1], (uint32_t)(tl >> 1) & 1u,
-                               (int64_t)blockIdx.x + (int64_t)tl * gridDim.x, npix, out, part, gran);
+        mbar_wait(&acc_bar[tl & 1], (uint32_t)(tl >> 1) & 1u);
+        tc_fence_after();
+        conv_tile_out<N, HEAD>(tmem + (uint32_t)((tl & 1) * N), (int64_t)blockIdx.x + (int64_t)tl * gridDim.x, npix,
+                               out, part, gran, 0);
+        tc_fence_before();
     };
 
     for (int j = 0; j < S - 1; ++j) {
@@ -378,25 +384,27 @@ constexpr uint32_t kRowLbo = kRowPix * 16;   // chunk-plane stride (2080 B)
 
 template <int N>
 struct RowCfg {
-    static constexpr int nbuf = N <= 64 ? 4 : 2;                   // TMEM accumulators (epilogue lag nbuf-1)
-    static constexpr int tcols = nbuf * N < 32 ? 32 : nbuf * N;
+    static constexpr int T = N >= 64 ? 1 : 64 / N;                  // row tiles per iteration
+    static constexpr int nbuf = T * N * 4 <= 256 ? 4 : 2;          // TMEM accumulator sets (lag nbuf-1)
+    static constexpr int tcols = nbuf * T * N < 32 ? 32 : nbuf * T * N;
     static constexpr uint32_t lbo_b = N / 8 * 128;
 };
 
-// Pipeline: loads run S-2 tiles ahead (the refilled stage was consumed two tiles ago, so its MMAs
-// have long finished), the epilogue trails the MMA issue by nbuf-1 tiles (the tcgen05 completion
-// latency stays off the critical path).
+// Pipeline: each iteration handles T consecutive row tiles (one accumulator set of T x N columns);
+// loads run S-2 iterations ahead (the refilled stage was consumed two iterations ago, so its MMAs
+// have finished), and the epilogue trails the MMA issue by nbuf-1 iterations, so neither the
+// tcgen05 completion latency nor the load latency is on the critical path.
 template <int N, bool HEAD>
 __global__ void __launch_bounds__(256) conv3x3_rows_kernel(const bf16 *__restrict__ in, const bf16 *__restrict__ w,
                                                            float *__restrict__ out, double *__restrict__ part,
-                                                           int64_t npix, int H, int W, int cin, int S, int gran,
-                                                           int dbg) {
+                                                           int64_t npix, int H, int W, int cin, int S, int T,
+                                                           int gran, int dbg) {
     using C = RowCfg<N>;
-    constexpr int NB = C::nbuf, LAG = NB - 1;
+    constexpr int NB = C::nbuf, LAG = NB - 1;   // T <= C::T row tiles per iteration
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char *sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const int cq = cin >> 3, PD = S - 2;
-    const uint32_t a_bytes = 3u * cq * kRowLbo, b_bytes = 9u * cq * C::lbo_b;
+    const uint32_t a_tile = 3u * cq * kRowLbo, a_bytes = T * a_tile, b_bytes = 9u * cq * C::lbo_b;
     uint64_t *mma_bar = reinterpret_cast<uint64_t *>(sm + S * a_bytes + b_bytes);
     uint64_t *acc_bar = mma_bar + S;
     uint32_t *tslot = reinterpret_cast<uint32_t *>(acc_bar + NB);
@@ -422,70 +430,82 @@ __global__ void __launch_bounds__(256) conv3x3_rows_kernel(const bf16 *__restric
     const uint32_t tmem = *tslot;
 
     const int64_t tiles = npix / kBM;                    // W % 128 == 0: every tile is full
-    const int ntl = blockIdx.x < tiles ? (int)((tiles - 1 - blockIdx.x) / gridDim.x + 1) : 0;
+    const int64_t groups = (tiles + T - 1) / T;
+    const int ngl = blockIdx.x < groups ? (int)((groups - 1 - blockIdx.x) / gridDim.x + 1) : 0;
     const int tpr = W / kBM;                             // tiles per image row
-    const int units = 3 * kRowPix;                       // (row, pixel) pairs per tile
+    const int units = T * 3 * kRowPix;                   // (tile, row, pixel) triples per iteration
+    auto tile_of = [&](int k, int i) { return ((int64_t)blockIdx.x + (int64_t)k * gridDim.x) * T + i; };
 
-    auto load = [&](int tl) {
+    auto load = [&](int k) {
         if (dbg & 1) return;
-        const int64_t t = (int64_t)blockIdx.x + (int64_t)tl * gridDim.x;
-        const int64_t rowid = t / tpr;                   // b * H + y
-        const int x0 = (int)(t - rowid * tpr) * kBM;
-        const int y = (int)(rowid % H);
-        const uint32_t a0 = sbase + (tl % S) * a_bytes;
+        const uint32_t a0 = sbase + (k % S) * a_bytes;
         for (int u = tid; u < units; u += 256) {
-            const int r = u / kRowPix, i = u - r * kRowPix;
-            const int yy = y + r - 1, xx = x0 + i - 1;
+            const int i = u / (3 * kRowPix), rr = u - i * 3 * kRowPix, r = rr / kRowPix, px = rr - r * kRowPix;
+            const int64_t t = tile_of(k, i);
+            if (t >= tiles) continue;
+            const int64_t rowid = t / tpr;               // b * H + y
+            const int x0 = (int)(t - rowid * tpr) * kBM;
+            const int y = (int)(rowid % H);
+            const int yy = y + r - 1, xx = x0 + px - 1;
             const bool v = yy >= 0 && yy < H && xx >= 0 && xx < W;
             const bf16 *src = v ? in + ((rowid + r - 1) * W + xx) * cin : in;
-            const uint32_t d = a0 + (uint32_t)(r * cq) * kRowLbo + i * 16;
+            const uint32_t d = a0 + i * a_tile + (uint32_t)(r * cq) * kRowLbo + px * 16;
             for (int c = 0; c < cq; ++c) cp_async16(d + c * kRowLbo, v ? src + c * 8 : in, v);
         }
     };
 
-    auto epilogue = [&](int tl) {
-        if (dbg & 4) {
-            mbar_wait(&acc_bar[tl % NB], (uint32_t)(tl / NB) & 1u);
-            return;
-        }
-        conv_epilogue<N, HEAD>(tmem + (uint32_t)((tl % NB) * N), &acc_bar[tl % NB], (uint32_t)(tl / NB) & 1u,
-                               (int64_t)blockIdx.x + (int64_t)tl * gridDim.x, npix, out, part, gran);
+    auto epilogue = [&](int k) {
+        mbar_wait(&acc_bar[k % NB], (uint32_t)(k / NB) & 1u);
+        tc_fence_after();
+        if (!(dbg & 4))
+            for (int i = 0; i < T; ++i) {
+                const int64_t t = tile_of(k, i);
+                if (t < tiles)
+                    conv_tile_out<N, HEAD>(tmem + (uint32_t)(((k % NB) * C::T + i) * N), t, npix, out, part, gran, i & 1);
+            }
+        tc_fence_before();
     };
 
-    for (int j = 0; j < PD; ++j) {
-        if (j < ntl) load(j);
+    for (int k = 0; k < PD; ++k) {
+        if (k < ngl) load(k);
         cp_async_commit();
     }
-    for (int j = 0; j < ntl; ++j) {
-        const int jn = j + PD;
-        if (jn < ntl) {
-            if (j >= 2) mbar_wait(&mma_bar[(j - 2) % S], (uint32_t)((j - 2) / S) & 1u);   // stage of tile j-2 free
-            load(jn);
+    for (int k = 0; k < ngl; ++k) {
+        const int kn = k + PD;
+        if (kn < ngl) {
+            if (k >= 2) mbar_wait(&mma_bar[(k - 2) % S], (uint32_t)((k - 2) / S) & 1u);   // stage of k-2 free
+            load(kn);
         }
         cp_async_commit();
-        cp_async_wait_n(PD);       // weights and tiles <= j have landed
+        cp_async_wait_n(PD);       // weights and iterations <= k have landed
         fence_proxy_async();
         __syncthreads();
         if (tid == 0) {
             tc_fence_after();
-            const uint32_t a0 = sbase + (j % S) * a_bytes;
-            const uint32_t acc = tmem + (uint32_t)((j % NB) * N);
-            int first = 1;
-            for (int tap = 0; tap < ((dbg & 2) ? 0 : 9); ++tap) {
+            // (tap, channel step) outer, tile inner: consecutive MMAs accumulate into different
+            // TMEM columns, so they do not wait on each other
+            int nt = 0;
+            while (nt < T && tile_of(k, nt) < tiles) ++nt;
+            if (dbg & 2) nt = 0;
+            const uint32_t a0 = sbase + (k % S) * a_bytes;
+            const uint32_t acc0 = tmem + (uint32_t)((k % NB) * C::T * N);
+            for (int tap = 0; tap < 9; ++tap) {
                 const int ky = tap / 3, kx = tap - 3 * ky;
                 const uint32_t arow = a0 + (uint32_t)(ky * cq) * kRowLbo + kx * 16;
                 for (int c = 0; c < cq; c += 2) {
-                    umma(acc, sdesc(arow + c * kRowLbo, kRowLbo, 128),
-                         sdesc(bbase + (tap * cq + c) * C::lbo_b, C::lbo_b, 128), idesc_bf16(N), first ? 0u : 1u);
-                    first = 0;
+                    const uint64_t bd = sdesc(bbase + (tap * cq + c) * C::lbo_b, C::lbo_b, 128);
+                    const uint32_t accf = (tap | c) ? 1u : 0u;
+                    for (int i = 0; i < nt; ++i)
+                        umma(acc0 + (uint32_t)(i * N), sdesc(arow + i * a_tile + c * kRowLbo, kRowLbo, 128), bd,
+                             idesc_bf16(N), accf);
                 }
             }
-            umma_commit(&mma_bar[j % S]);
-            umma_commit(&acc_bar[j % NB]);
+            umma_commit(&mma_bar[k % S]);
+            umma_commit(&acc_bar[k % NB]);
         }
-        if (j >= LAG) epilogue(j - LAG);
+        if (k >= LAG) epilogue(k - LAG);
     }
-    for (int t = ntl - LAG > 0 ? ntl - LAG : 0; t < ntl; ++t) epilogue(t);
+    for (int k = ngl - LAG > 0 ? ngl - LAG : 0; k < ngl; ++k) epilogue(k);
     __syncthreads();
     if (warp == 0) tmem_dealloc<C::tcols>(tmem);
 }
@@ -494,12 +514,18 @@ template <int N, bool HEAD>
 cudaError_t launch_conv_rows(const bf16 *in, const bf16 *w, float *out, double *part, int64_t npix, int H, int W,
                              int cin, cudaStream_t st) {
     const int cq = cin / 8;
-    const size_t a_bytes = 3 * (size_t)cq * kRowLbo, b_bytes = 9 * (size_t)cq * RowCfg<N>::lbo_b;
-    // stages: as many as fit 2 CTAs per SM (<= 110 KB), 3..5 (prefetch distance S-2 <= 3)
-    int S = (int)((110 * 1024 - 1200 - b_bytes) / a_bytes);
+    const size_t a_tile = 3 * (size_t)cq * kRowLbo, b_bytes = 9 * (size_t)cq * RowCfg<N>::lbo_b;
+    // T row tiles per iteration and S stages: prefer 2 CTAs per SM (<= 110 KB) with S >= 3, else one
+    // CTA (<= 220 KB); T as large as fits (<= RowCfg::T), S in 3..5 (prefetch distance S-2 <= 3)
+    int T = RowCfg<N>::T, S = 0;
+    for (; T >= 1 && S < 3; --T) {
+        S = (int)((110 * 1024 - 1200 - b_bytes) / (T * a_tile));
+        if (S < 3) S = (int)((220 * 1024 - 1200 - b_bytes) / (T * a_tile));
+        if (S >= 3) break;
+    }
+    if (T < 1 || S < 3) return cudaErrorInvalidValue;
     S = S > 5 ? 5 : S;
-    if (S < 3) S = (int)((220 * 1024 - 1200 - b_bytes) / a_bytes) >= 3 ? 3 : 0;
-    if (S < 3) return cudaErrorInvalidValue;
+    const size_t a_bytes = T * a_tile;
     const size_t smem = 1024 + S * a_bytes + b_bytes + 128;
     static size_t smem_set = 0;
     static int nsm = 0;
@@ -523,10 +549,10 @@ cudaError_t launch_conv_rows(const bf16 *in, const bf16 *w, float *out, double *
     if (e != cudaSuccess) return e;
     occ = occ < 1 ? 1 : (occ > 512 / RowCfg<N>::tcols ? 512 / RowCfg<N>::tcols : occ);   // TMEM columns
     const int gran = (H * W) % 32 == 0 ? 32 : 1;
-    const int64_t tiles = npix / kBM, slots = (int64_t)nsm * occ;
-    const unsigned grid = (unsigned)(tiles < slots ? tiles : slots);
+    const int64_t groups = (npix / kBM + T - 1) / T, slots = (int64_t)nsm * occ;
+    const unsigned grid = (unsigned)(groups < slots ? groups : slots);
     static const int dbg = getenv("UN_DBG") ? atoi(getenv("UN_DBG")) : 0;
-    conv3x3_rows_kernel<N, HEAD><<<grid, 256, smem, st>>>(in, w, out, part, npix, H, W, cin, S, gran, dbg);
+    conv3x3_rows_kernel<N, HEAD><<<grid, 256, smem, st>>>(in, w, out, part, npix, H, W, cin, S, T, gran, dbg);
     return cudaGetLastError();
 }
 
