@@ -18,6 +18,7 @@
 //   (tcgen05.ld 32x32b), one pixel per thread, and stores the fp32 row.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <cmath>
 #include <cstdarg>
@@ -67,6 +68,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         : "memory");
 }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap *m) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
+}
+__device__ __forceinline__ void tma_load_5d(uint32_t dst, const CUtensorMap *map, int c0, int c1, int c2, int c3, int c4,
+                                            uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, "
+        "%6}], [%7];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(bar))
+        : "memory");
+}
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
 
@@ -148,22 +166,23 @@ __device__ __forceinline__ void cp_async_wait_n(int n) {   // n <= 3
 // Epilogue of one 128-pixel tile t (pixels t*128 .. t*128+127) whose accumulator is TMEM buffer
 // tl & 1: wait for its MMAs, tcgen05.ld (warp w reads lanes 32 (w & 3) .. +31; with N >= 32 the
 // warps w and w + 4 split the columns), fp32 stores, GroupNorm partial sums (see above).
-template <int N, bool HEAD>
+template <int N, bool HEAD, bool SPLIT = true>
 __device__ __forceinline__ void conv_tile_out(uint32_t tacc, int64_t t, int64_t npix, float *__restrict__ out,
                                               double *__restrict__ part, int gran, int sel) {
     constexpr int NG = HEAD ? 1 : kGroups, GC = HEAD ? 1 : N / kGroups;
-    constexpr int ECOLS = N >= 32 ? N / 2 : N;                       // epilogue columns per warp
+    constexpr bool HALF = SPLIT && N >= 32;                          // warps w, w+4 split the columns
+    constexpr int ECOLS = HALF ? N / 2 : N;                          // epilogue columns per warp
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int lq = warp & 3, hv = warp >> 2;
-    if (N >= 32 || hv == sel) {
+    const int lq = warp & 3, hv = (warp >> 2) & 1;
+    if (!SPLIT || N >= 32 || hv == sel) {
         const int64_t p = t * kBM + 32 * lq + lane;
         const bool pv = p < npix;
-        const int c0 = N >= 32 ? hv * ECOLS : 0;
+        const int c0 = HALF ? hv * ECOLS : 0;
         const uint32_t trow = tacc + ((uint32_t)(32 * lq) << 16);
         float *o = out + p * N;
-        // groups owned by this warp: all (N = 16) or the half [2 hv, 2 hv + 2) (N >= 32)
-        constexpr int G0N = N >= 32 ? NG / 2 : NG;
-        const int g0 = N >= 32 ? hv * G0N : 0;
+        // groups owned by this warp: all, or the half [2 hv, 2 hv + 2) when the columns are split
+        constexpr int G0N = HALF ? NG / 2 : NG;
+        const int g0 = HALF ? hv * G0N : 0;
         float fs[G0N], fq[G0N];   // per pixel: <= 32 terms, fp32; fp64 across pixels
 #pragma unroll
         for (int g = 0; g < G0N; ++g) fs[g] = fq[g] = 0.0f;
@@ -381,6 +400,7 @@ cudaError_t launch_conv_n(const bf16 *in, const bf16 *w, float *out, double *par
 // 9x.  The whole weight matrix stays resident in shared memory.
 constexpr int kRowPix = 130;
 constexpr uint32_t kRowLbo = kRowPix * 16;   // chunk-plane stride (2080 B)
+__host__ __device__ constexpr uint32_t row_region(int cq) { return (cq * kRowLbo + 127u) / 128u * 128u; }
 
 template <int N>
 struct RowCfg {
@@ -390,40 +410,56 @@ struct RowCfg {
     static constexpr uint32_t lbo_b = N / 8 * 128;
 };
 
-// Pipeline: each iteration handles T consecutive row tiles (one accumulator set of T x N columns);
-// loads run S-2 iterations ahead (the refilled stage was consumed two iterations ago, so its MMAs
-// have finished), and the epilogue trails the MMA issue by nbuf-1 iterations, so neither the
-// tcgen05 completion latency nor the load latency is on the critical path.
+// Warp-specialised pipeline (no CTA barrier in the loop): warps 0-7 load (each iteration = T
+// consecutive row tiles) with cp.async and signal full[s] through cp.async.mbarrier.arrive.noinc;
+// warp 12 (one lane) waits full[s], issues the MMAs of the iteration into accumulator set k % NB
+// (tiles interleaved) and commits to empty[s] (the stage may be refilled) and accf[b] (the
+// accumulators are ready); warps 8-11 wait accf[b], drain the accumulators (tcgen05.ld, fp32
+// stores, GroupNorm partial sums) and arrive on acce[b] (the set may be overwritten).
+constexpr int kProdWarps = 8;                        // loader warps
+constexpr int kWsThreads = 32 * (kProdWarps + 5);   // + 4 epilogue warps + 1 MMA warp
+
 template <int N, bool HEAD>
-__global__ void __launch_bounds__(256) conv3x3_rows_kernel(const bf16 *__restrict__ in, const bf16 *__restrict__ w,
-                                                           float *__restrict__ out, double *__restrict__ part,
-                                                           int64_t npix, int H, int W, int cin, int S, int T,
-                                                           int gran, int dbg) {
+__global__ void __launch_bounds__(kWsThreads) conv3x3_rows_kernel(const bf16 *__restrict__ in,
+                                                                  const bf16 *__restrict__ w, float *__restrict__ out,
+                                                                  double *__restrict__ part, int64_t npix, int H, int W,
+                                                                  int cin, int S, int T, int gran, int dbg,
+                                                                  const __grid_constant__ CUtensorMap rmap, int use_tma) {
     using C = RowCfg<N>;
-    constexpr int NB = C::nbuf, LAG = NB - 1;   // T <= C::T row tiles per iteration
+    constexpr int NB = C::nbuf;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char *sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-    const int cq = cin >> 3, PD = S - 2;
-    const uint32_t a_tile = 3u * cq * kRowLbo, a_bytes = T * a_tile, b_bytes = 9u * cq * C::lbo_b;
-    uint64_t *mma_bar = reinterpret_cast<uint64_t *>(sm + S * a_bytes + b_bytes);
-    uint64_t *acc_bar = mma_bar + S;
-    uint32_t *tslot = reinterpret_cast<uint32_t *>(acc_bar + NB);
+    const int cq = cin >> 3;
+    const uint32_t rreg = row_region(cq), a_tile = 3u * rreg, a_bytes = T * a_tile, b_bytes = 9u * cq * C::lbo_b;
+    uint64_t *full = reinterpret_cast<uint64_t *>(sm + S * a_bytes + b_bytes);
+    uint64_t *empty = full + S;
+    uint64_t *accf = empty + S;
+    uint64_t *acce = accf + NB;
+    uint32_t *tslot = reinterpret_cast<uint32_t *>(acce + NB);
     const uint32_t sbase = smem_u32(sm), bbase = sbase + S * a_bytes;
-    const int tid = threadIdx.x, warp = tid >> 5;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
     if (tid == 0) {
-        for (int q = 0; q < S; ++q) mbar_init(&mma_bar[q], 1);
-        for (int q = 0; q < NB; ++q) mbar_init(&acc_bar[q], 1);
+        for (int q = 0; q < S; ++q) {
+            mbar_init(&full[q], use_tma ? 1 : kProdWarps * 32);
+            mbar_init(&empty[q], 1);
+        }
+        for (int q = 0; q < NB; ++q) {
+            mbar_init(&accf[q], 1);
+            mbar_init(&acce[q], 4);
+        }
         fence_mbar_init();
     }
-    if (warp == 0) tmem_alloc<C::tcols>(tslot);
+    if (warp == kProdWarps + 4) tmem_alloc<C::tcols>(tslot);
     // resident weights: chunk g = tap * cq + c of row n at g * lbo_b + (n / 8) * 128 + (n % 8) * 16
     const int nchk = 9 * cq;
-    for (int i = tid; i < N * nchk; i += 256) {
+    for (int i = tid; i < N * nchk; i += kWsThreads) {
         const int n = i / nchk, g = i - n * nchk;
         cp_async16(bbase + g * C::lbo_b + (n >> 3) * 128 + (n & 7) * 16, w + (int64_t)n * 9 * cin + g * 8, true);
     }
     cp_async_commit();
+    cp_async_wait_n(0);
+    fence_proxy_async();
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -432,91 +468,147 @@ __global__ void __launch_bounds__(256) conv3x3_rows_kernel(const bf16 *__restric
     const int64_t tiles = npix / kBM;                    // W % 128 == 0: every tile is full
     const int64_t groups = (tiles + T - 1) / T;
     const int ngl = blockIdx.x < groups ? (int)((groups - 1 - blockIdx.x) / gridDim.x + 1) : 0;
-    const int tpr = W / kBM;                             // tiles per image row
-    const int units = T * 3 * kRowPix;                   // (tile, row, pixel) triples per iteration
     auto tile_of = [&](int k, int i) { return ((int64_t)blockIdx.x + (int64_t)k * gridDim.x) * T + i; };
+    const int tpr = W / kBM;                             // tiles per image row
 
-    auto load = [&](int k) {
-        if (dbg & 1) return;
-        const uint32_t a0 = sbase + (k % S) * a_bytes;
-        for (int u = tid; u < units; u += 256) {
-            const int i = u / (3 * kRowPix), rr = u - i * 3 * kRowPix, r = rr / kRowPix, px = rr - r * kRowPix;
-            const int64_t t = tile_of(k, i);
-            if (t >= tiles) continue;
-            const int64_t rowid = t / tpr;               // b * H + y
-            const int x0 = (int)(t - rowid * tpr) * kBM;
-            const int y = (int)(rowid % H);
-            const int yy = y + r - 1, xx = x0 + px - 1;
-            const bool v = yy >= 0 && yy < H && xx >= 0 && xx < W;
-            const bf16 *src = v ? in + ((rowid + r - 1) * W + xx) * cin : in;
-            const uint32_t d = a0 + i * a_tile + (uint32_t)(r * cq) * kRowLbo + px * 16;
-            for (int c = 0; c < cq; ++c) cp_async16(d + c * kRowLbo, v ? src + c * 8 : in, v);
-        }
-    };
-
-    auto epilogue = [&](int k) {
-        mbar_wait(&acc_bar[k % NB], (uint32_t)(k / NB) & 1u);
-        tc_fence_after();
-        if (!(dbg & 4))
-            for (int i = 0; i < T; ++i) {
-                const int64_t t = tile_of(k, i);
-                if (t < tiles)
-                    conv_tile_out<N, HEAD>(tmem + (uint32_t)(((k % NB) * C::T + i) * N), t, npix, out, part, gran, i & 1);
-            }
-        tc_fence_before();
-    };
-
-    for (int k = 0; k < PD; ++k) {
-        if (k < ngl) load(k);
-        cp_async_commit();
-    }
-    for (int k = 0; k < ngl; ++k) {
-        const int kn = k + PD;
-        if (kn < ngl) {
-            if (k >= 2) mbar_wait(&mma_bar[(k - 2) % S], (uint32_t)((k - 2) / S) & 1u);   // stage of k-2 free
-            load(kn);
-        }
-        cp_async_commit();
-        cp_async_wait_n(PD);       // weights and iterations <= k have landed
-        fence_proxy_async();
-        __syncthreads();
-        if (tid == 0) {
-            tc_fence_after();
-            // (tap, channel step) outer, tile inner: consecutive MMAs accumulate into different
-            // TMEM columns, so they do not wait on each other
-            int nt = 0;
-            while (nt < T && tile_of(k, nt) < tiles) ++nt;
-            if (dbg & 2) nt = 0;
-            const uint32_t a0 = sbase + (k % S) * a_bytes;
-            const uint32_t acc0 = tmem + (uint32_t)((k % NB) * C::T * N);
-            for (int tap = 0; tap < 9; ++tap) {
-                const int ky = tap / 3, kx = tap - 3 * ky;
-                const uint32_t arow = a0 + (uint32_t)(ky * cq) * kRowLbo + kx * 16;
-                for (int c = 0; c < cq; c += 2) {
-                    const uint64_t bd = sdesc(bbase + (tap * cq + c) * C::lbo_b, C::lbo_b, 128);
-                    const uint32_t accf = (tap | c) ? 1u : 0u;
-                    for (int i = 0; i < nt; ++i)
-                        umma(acc0 + (uint32_t)(i * N), sdesc(arow + i * a_tile + c * kRowLbo, kRowLbo, 128), bd,
-                             idesc_bf16(N), accf);
+    if (warp < kProdWarps) {
+        // ------------------------------- producers -------------------------------
+        constexpr int NP = kProdWarps * 32;
+        if (use_tma) {   // one thread: a 5D TMA box (16 B x 130 pixels x cq chunks) per (tile, row)
+            if (tid == 0) {
+                prefetch_tmap(&rmap);
+                for (int k = 0; k < ngl; ++k) {
+                    const int s = k % S;
+                    if (k >= S) mbar_wait(&empty[s], (uint32_t)(k / S - 1) & 1u);
+                    const uint32_t a0 = sbase + s * a_bytes;
+                    int nt = 0;
+                    while (nt < T && tile_of(k, nt) < tiles) ++nt;
+                    mbar_expect_tx(&full[s], (uint32_t)nt * 3u * (uint32_t)cq * kRowLbo);
+                    for (int i = 0; i < nt; ++i) {
+                        const int64_t t = tile_of(k, i);
+                        const int64_t rowid = t / tpr;
+                        const int x0 = (int)(t - rowid * tpr) * kBM;
+                        const int b = (int)(rowid / H), y = (int)(rowid - (int64_t)b * H);
+                        for (int r = 0; r < 3; ++r)
+                            tma_load_5d(a0 + i * a_tile + (uint32_t)r * rreg, &rmap, 0, x0 - 1, 0, y + r - 1, b, &full[s]);
+                    }
                 }
             }
-            umma_commit(&mma_bar[k % S]);
-            umma_commit(&acc_bar[k % NB]);
+        } else
+        for (int k = 0; k < ngl; ++k) {
+            const int s = k % S;
+            if (k >= S) mbar_wait(&empty[s], (uint32_t)(k / S - 1) & 1u);
+            const uint32_t a0 = sbase + s * a_bytes;
+            if (!(dbg & 1))
+                for (int i = 0; i < T; ++i) {
+                    const int64_t t = tile_of(k, i);
+                    if (t >= tiles) break;
+                    const int64_t rowid = t / tpr;       // b * H + y (uniform across the producers)
+                    const int x0 = (int)(t - rowid * tpr) * kBM;
+                    const int y = (int)(rowid % H);
+                    for (int r = 0; r < 3; ++r) {
+                        const bool rv = y + r - 1 >= 0 && y + r - 1 < H;
+                        const bf16 *rowp = in + (rowid + r - 1) * W * cin;
+                        const uint32_t d0 = a0 + i * a_tile + (uint32_t)r * rreg;
+                        for (int px = tid; px < kRowPix; px += NP) {
+                            const int xx = x0 + px - 1;
+                            const bool v = rv && xx >= 0 && xx < W;
+                            const bf16 *src = v ? rowp + (int64_t)xx * cin : in;
+                            const uint32_t d = d0 + px * 16;
+                            for (int c = 0; c < cq; ++c) cp_async16(d + c * kRowLbo, v ? src + c * 8 : in, v);
+                        }
+                    }
+                }
+            asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&full[s]))
+                         : "memory");
         }
-        if (k >= LAG) epilogue(k - LAG);
+    } else if (warp == kProdWarps + 4) {
+        // ------------------------------- MMA issuer -------------------------------
+        if (lane == 0) {
+            for (int k = 0; k < ngl; ++k) {
+                const int s = k % S, b = k % NB;
+                mbar_wait(&full[s], (uint32_t)(k / S) & 1u);
+                if (k >= NB) mbar_wait(&acce[b], (uint32_t)(k / NB - 1) & 1u);
+                tc_fence_after();
+                int nt = 0;
+                while (nt < T && tile_of(k, nt) < tiles) ++nt;
+                if (dbg & 2) nt = 0;
+                const uint32_t a0 = sbase + s * a_bytes;
+                const uint32_t acc0 = tmem + (uint32_t)(b * C::T * N);
+                for (int tap = 0; tap < 9; ++tap) {
+                    const int ky = tap / 3, kx = tap - 3 * ky;
+                    const uint32_t arow = a0 + (uint32_t)ky * rreg + kx * 16;
+                    for (int c = 0; c < cq; c += 2) {
+                        const uint64_t bd = sdesc(bbase + (tap * cq + c) * C::lbo_b, C::lbo_b, 128);
+                        const uint32_t accf_ = (tap | c) ? 1u : 0u;
+                        for (int i = 0; i < nt; ++i)
+                            umma(acc0 + (uint32_t)(i * N), sdesc(arow + i * a_tile + c * kRowLbo, kRowLbo, 128), bd,
+                                 idesc_bf16(N), accf_);
+                    }
+                }
+                umma_commit(&empty[s]);
+                umma_commit(&accf[b]);
+            }
+        }
+        __syncwarp();
+    } else {
+        // ------------------------- epilogue warps kProdWarps .. kProdWarps+3 -------------------------
+        for (int k = 0; k < ngl; ++k) {
+            const int b = k % NB;
+            mbar_wait(&accf[b], (uint32_t)(k / NB) & 1u);
+            tc_fence_after();
+            if (!(dbg & 4))
+                for (int i = 0; i < T; ++i) {
+                    const int64_t t = tile_of(k, i);
+                    if (t < tiles)
+                        conv_tile_out<N, HEAD, false>(tmem + (uint32_t)((b * C::T + i) * N), t, npix, out, part, gran, 0);
+                }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&acce[b]);
+        }
     }
-    for (int k = ngl - LAG > 0 ? ngl - LAG : 0; k < ngl; ++k) epilogue(k);
+    tc_fence_before();
     __syncthreads();
-    if (warp == 0) tmem_dealloc<C::tcols>(tmem);
+    if (warp == kProdWarps + 4) tmem_dealloc<C::tcols>(tmem);
+}
+
+// 5D tensor map over the NHWC bf16 activations, ordered (8 channels, pixel x, chunk, row y, sample)
+// so that a box of {8, 130, cq, 1, 1} lands chunk-major in shared memory (chunk plane of 130 x 16 B);
+// out-of-range pixels and rows (the 'same' padding) are zero-filled by the TMA unit.
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void *p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+bool encode_rows_map(CUtensorMap *m, const void *in, int B, int H, int W, int cin) {
+    auto enc = get_encode();
+    if (!enc || (reinterpret_cast<uintptr_t>(in) & 15u)) return false;
+    const int cq = cin / 8;
+    cuuint64_t dims[5] = {8, (cuuint64_t)W, (cuuint64_t)cq, (cuuint64_t)H, (cuuint64_t)B};
+    cuuint64_t strides[4] = {(cuuint64_t)cin * 2, 16, (cuuint64_t)W * cin * 2, (cuuint64_t)H * W * cin * 2};
+    cuuint32_t box[5] = {8, (cuuint32_t)kRowPix, (cuuint32_t)cq, 1, 1};
+    cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void *>(in), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
 }
 
 template <int N, bool HEAD>
 cudaError_t launch_conv_rows(const bf16 *in, const bf16 *w, float *out, double *part, int64_t npix, int H, int W,
                              int cin, cudaStream_t st) {
     const int cq = cin / 8;
-    const size_t a_tile = 3 * (size_t)cq * kRowLbo, b_bytes = 9 * (size_t)cq * RowCfg<N>::lbo_b;
+    const size_t a_tile = 3 * (size_t)row_region(cq), b_bytes = 9 * (size_t)cq * RowCfg<N>::lbo_b;
     // T row tiles per iteration and S stages: prefer 2 CTAs per SM (<= 110 KB) with S >= 3, else one
-    // CTA (<= 220 KB); T as large as fits (<= RowCfg::T), S in 3..5 (prefetch distance S-2 <= 3)
+    // CTA (<= 220 KB); T as large as fits (<= RowCfg::T), S <= 6
     int T = RowCfg<N>::T, S = 0;
     for (; T >= 1 && S < 3; --T) {
         S = (int)((110 * 1024 - 1200 - b_bytes) / (T * a_tile));
@@ -524,7 +616,7 @@ cudaError_t launch_conv_rows(const bf16 *in, const bf16 *w, float *out, double *
         if (S >= 3) break;
     }
     if (T < 1 || S < 3) return cudaErrorInvalidValue;
-    S = S > 5 ? 5 : S;
+    S = S > 6 ? 6 : S;
     const size_t a_bytes = T * a_tile;
     const size_t smem = 1024 + S * a_bytes + b_bytes + 128;
     static size_t smem_set = 0;
@@ -545,14 +637,19 @@ cudaError_t launch_conv_rows(const bf16 *in, const bf16 *w, float *out, double *
         smem_set = smem;
     }
     int occ = 1;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, conv3x3_rows_kernel<N, HEAD>, 256, smem);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, conv3x3_rows_kernel<N, HEAD>, kWsThreads, smem);
     if (e != cudaSuccess) return e;
     occ = occ < 1 ? 1 : (occ > 512 / RowCfg<N>::tcols ? 512 / RowCfg<N>::tcols : occ);   // TMEM columns
     const int gran = (H * W) % 32 == 0 ? 32 : 1;
     const int64_t groups = (npix / kBM + T - 1) / T, slots = (int64_t)nsm * occ;
     const unsigned grid = (unsigned)(groups < slots ? groups : slots);
     static const int dbg = getenv("UN_DBG") ? atoi(getenv("UN_DBG")) : 0;
-    conv3x3_rows_kernel<N, HEAD><<<grid, 256, smem, st>>>(in, w, out, part, npix, H, W, cin, S, T, gran, dbg);
+    static const int notma = getenv("UN_NO_TMA") ? atoi(getenv("UN_NO_TMA")) : 0;
+    CUtensorMap rmap;
+    std::memset(&rmap, 0, sizeof rmap);
+    const int use_tma = !notma && encode_rows_map(&rmap, in, (int)(npix / ((int64_t)H * W)), H, W, cin);
+    conv3x3_rows_kernel<N, HEAD><<<grid, kWsThreads, smem, st>>>(in, w, out, part, npix, H, W, cin, S, T, gran, dbg,
+                                                                   rmap, use_tma);
     return cudaGetLastError();
 }
 
