@@ -675,9 +675,6 @@ cudaError_t launch_conv(const bf16 *in, const bf16 *w, float *out, double *part,
 
 // ------------------------------------------------------------------------------------------------
 // element-wise and reduction kernels
-__device__ __forceinline__ float gelu(float u) {   // P:408-411 (tanh form)
-    return 0.5f * u * (1.0f + tanhf(0.7978845608028654f * (u + 0.044715f * u * u * u)));
-}
 
 // history [B][lb][HW] fp32 -> NHWC bf16 with 16 channels (channels >= lb are zero)
 __global__ void pack_input_kernel(const float *__restrict__ hist, bf16 *__restrict__ dst, int64_t npix, int HW,
@@ -722,7 +719,9 @@ __global__ void __launch_bounds__(kBasis) time_mlp_kernel(const double *__restri
 // group's channels and all pixels, from the conv epilogue's per-warp fp64 partial sums, summed in a
 // fixed order (deterministic); var = E[u^2] - mu^2 in fp64.
 __global__ void __launch_bounds__(256) gn_reduce_kernel(const double *__restrict__ part, int HW, int gran, int G,
-                                                        int Cg, double *__restrict__ stats) {
+                                                        int Cg, double *__restrict__ stats,
+                                                        const float *__restrict__ gamma, const float *__restrict__ beta,
+                                                        int C, float2 *__restrict__ ab) {
     const int g = blockIdx.x, b = blockIdx.y, nw = HW / gran;
     const double *pb = part + ((int64_t)b * nw * G + g) * 2;
     __shared__ double rs[256], rq[256];
@@ -741,20 +740,36 @@ __global__ void __launch_bounds__(256) gn_reduce_kernel(const double *__restrict
         }
         __syncthreads();
     }
+    const double n = (double)Cg * HW, mean = rs[0] / n, var = rq[0] / n - mean * mean;
+    const double rstd = 1.0 / sqrt((var > 0.0 ? var : 0.0) + kEps);
     if (threadIdx.x == 0) {
-        const double n = (double)Cg * HW, mean = rs[0] / n, var = rq[0] / n - mean * mean;
         stats[((int64_t)b * G + g) * 2] = mean;
-        stats[((int64_t)b * G + g) * 2 + 1] = 1.0 / sqrt((var > 0.0 ? var : 0.0) + kEps);
+        stats[((int64_t)b * G + g) * 2 + 1] = rstd;
+    }
+    // GN(u)_k = gamma_k (u - mu) rstd + beta_k = u a_k + c_k
+    for (int j = threadIdx.x; j < Cg; j += 256) {
+        const int k = g * Cg + j;
+        const double a = (double)gamma[k] * rstd;
+        ab[(int64_t)b * C + k] = make_float2((float)a, (float)((double)beta[k] - mean * a));
     }
 }
 
 // y = GELU(gamma (x - mu) / sigma + beta) -> bf16 at dA (channel stride sA, offset oA)
 // and, conditioned by cond[b][coff + k], at dB; 8 channels per thread.
-__global__ void gn_apply_kernel(const float *__restrict__ x, int64_t npix, int HW, int C, int G,
-                                const double *__restrict__ stats, const float *__restrict__ gamma,
-                                const float *__restrict__ beta, const float *__restrict__ cond, int ctot, int coff,
-                                bf16 *dA, int sA, int oA, bf16 *dB, int sB, int oB) {
-    const int nq = C >> 3, Cg = C / G;
+__device__ __forceinline__ float tanh_approx(float x) {
+    float y;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float gelu_fast(float u) {   // P:408-411, hardware tanh (|err| ~ 2^-11)
+    return 0.5f * u * (1.0f + tanh_approx(0.7978845608028654f * (u + 0.044715f * u * u * u)));
+}
+
+__global__ void __launch_bounds__(256) gn_apply_kernel(const float *__restrict__ x, int64_t npix, int HW, int C,
+                                                       const float2 *__restrict__ ab, const float *__restrict__ cond,
+                                                       int ctot, int coff, bf16 *dA, int sA, int oA, bf16 *dB, int sB,
+                                                       int oB) {
+    const int nq = C >> 3;
     const int64_t total = npix * nq;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t p = i / nq;
@@ -763,14 +778,27 @@ __global__ void gn_apply_kernel(const float *__restrict__ x, int64_t npix, int H
         const float4 *src = reinterpret_cast<const float4 *>(x + p * C + c0);
         const float4 v0 = src[0], v1 = src[1];
         const float xv[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+        const float4 *a4 = reinterpret_cast<const float4 *>(ab + (int64_t)b * C + c0);
+        float2 af[8];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const float4 t = a4[j];
+            af[2 * j] = make_float2(t.x, t.y);
+            af[2 * j + 1] = make_float2(t.z, t.w);
+        }
         __align__(16) bf16 ya[8], yb[8];
+        float cv[8];
+        if (dB) {
+            const float4 *c4 = reinterpret_cast<const float4 *>(cond + (int64_t)b * ctot + coff + c0);
+            const float4 t0 = c4[0], t1 = c4[1];
+            cv[0] = t0.x; cv[1] = t0.y; cv[2] = t0.z; cv[3] = t0.w;
+            cv[4] = t1.x; cv[5] = t1.y; cv[6] = t1.z; cv[7] = t1.w;
+        }
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-            const int k = c0 + j, g = k / Cg;
-            const float mu = (float)stats[((int64_t)b * G + g) * 2], rs = (float)stats[((int64_t)b * G + g) * 2 + 1];
-            const float y = gelu((xv[j] - mu) * rs * gamma[k] + beta[k]);
+            const float y = gelu_fast(fmaf(xv[j], af[j].x, af[j].y));
             ya[j] = __float2bfloat16_rn(y);
-            if (dB) yb[j] = __float2bfloat16_rn(y * cond[(int64_t)b * ctot + coff + k]);
+            if (dB) yb[j] = __float2bfloat16_rn(y * cv[j]);
         }
         if (dA) *reinterpret_cast<uint4 *>(dA + p * sA + oA + c0) = *reinterpret_cast<uint4 *>(ya);
         if (dB) *reinterpret_cast<uint4 *>(dB + p * sB + oB + c0) = *reinterpret_cast<uint4 *>(yb);
@@ -870,6 +898,7 @@ struct un_ctx {
     bf16 *in0 = nullptr, *z[3] = {}, *pin[3] = {}, *cat[3] = {}, *z4c = nullptr, *dec[4] = {};
     float *raw = nullptr, *cond = nullptr, *dout = nullptr, *dhist = nullptr, *ddt = nullptr;
     double *stats = nullptr, *part = nullptr;   // GN statistics, per-warp partial sums
+    float2 *ab = nullptr;                       // per (sample, channel) GN affine: y = u a + c
     float *h_in = nullptr, *h_out = nullptr;   // pinned staging of un_forward / un_rollout
     std::string err;
     int64_t launches = 0;
@@ -926,7 +955,8 @@ pf_status conv_layer(un_ctx *c, int l, const bf16 *in, int B) {
     }
     const int G = head ? 1 : kGroups;
     const int Cg = head ? 1 : c->cout[l] / kGroups;
-    gn_reduce_kernel<<<dim3(G, B), 256, 0, c->st>>>(c->part, H * W, (H * W) % 32 == 0 ? 32 : 1, G, Cg, c->stats);
+    gn_reduce_kernel<<<dim3(G, B), 256, 0, c->st>>>(c->part, H * W, (H * W) % 32 == 0 ? 32 : 1, G, Cg, c->stats,
+                                                    c->gam[l], c->bet[l], head ? 1 : c->cout[l], c->ab);
     c->launches += 2;
     return PF_OK;
 }
@@ -936,8 +966,7 @@ pf_status apply_layer(un_ctx *c, int l, int B, int cond_level, bf16 *dA, int sA,
     const int64_t npix = (int64_t)B * HW;
     const int C = c->cout[l];
     gn_apply_kernel<<<grid_for(npix * (C / 8), 256), 256, 0, c->st>>>(
-        c->raw, npix, HW, C, kGroups, c->stats, c->gam[l], c->bet[l], c->cond, c->ctot,
-        cond_level >= 0 ? c->coff[cond_level] : 0, dA, sA, oA, dB, sB, oB);
+        c->raw, npix, HW, C, c->ab, c->cond, c->ctot, cond_level >= 0 ? c->coff[cond_level] : 0, dA, sA, oA, dB, sB, oB);
     c->launches += 1;
     return PF_OK;
 }
@@ -1126,6 +1155,7 @@ pf_status un_create(const un_params *p, un_ctx **out) {
     if (s == PF_OK) s = dalloc(c, &c->raw, (size_t)rawmax);
     if (s == PF_OK) s = dalloc(c, &c->cond, (size_t)(B * c->ctot));
     if (s == PF_OK) s = dalloc(c, &c->stats, (size_t)(B * kGroups * 2));
+    if (s == PF_OK) s = dalloc(c, &c->ab, (size_t)(B * 128));
     int64_t pmax = 0;   // per-unit partial statistics of the largest layer
     for (int lv = 0; lv < 4; ++lv) {
         const int64_t n = B * hw(lv) / (hw(lv) % 32 == 0 ? 32 : 1) * kGroups * 2;
@@ -1338,6 +1368,7 @@ void un_free(un_ctx *c) {
     cudaFree(c->raw);
     cudaFree(c->cond);
     cudaFree(c->stats);
+    cudaFree(c->ab);
     cudaFree(c->part);
     cudaFree(c->dout);
     cudaFree(c->dhist);
