@@ -191,11 +191,15 @@ __device__ __forceinline__ void conv_tile_out(uint32_t tacc, int64_t t, int64_t 
             uint32_t r[16];
             tmem_ld16(trow + c0 + c, r);
             if (pv) {
-                float4 *o4 = reinterpret_cast<float4 *>(o + c0 + c);
+                if (HEAD) {                       // the single real output channel
+                    if (c == 0) out[p] = __uint_as_float(r[0]);
+                } else {
+                    float4 *o4 = reinterpret_cast<float4 *>(o + c0 + c);
 #pragma unroll
-                for (int j = 0; j < 4; ++j)
-                    o4[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
-                                        __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+                    for (int j = 0; j < 4; ++j)
+                        o4[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                            __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+                }
 #pragma unroll
                 for (int j = 0; j < 16; ++j) {
                     const int lc = c + j;     // column relative to c0 (compile-time after unrolling)
@@ -1028,7 +1032,7 @@ pf_status forward(un_ctx *c, int B, const float *hist, const float *dt, float *o
     if ((s = conv_layer(c, kHead1, c->cat[0], B)) || (s = apply_layer(c, kHead1, B, -1, c->dec[3], C1, 0, nullptr, 0, 0)))
         return s;
     if ((s = conv_layer(c, kHead2, c->dec[3], B))) return s;
-    head_out_kernel<<<grid_for((int64_t)B * HW, 256), 256, 0, c->st>>>(c->raw, c->cout_pad[kHead2], (int64_t)B * HW,
+    head_out_kernel<<<grid_for((int64_t)B * HW, 256), 256, 0, c->st>>>(c->raw, 1, (int64_t)B * HW,
                                                                        (int)HW, c->stats, c->gam[kHead2],
                                                                        c->bet[kHead2], out);
     c->launches += 1;
