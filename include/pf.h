@@ -224,6 +224,10 @@ pf_status pf_diagnostics(pf_ctx *ctx, int32_t member, double out[5]);
  * Any pointer may be NULL.  Errors: PF_ERR_ARG. */
 pf_status pf_info(pf_ctx *ctx, int64_t *steps, double *t, int32_t *y0, int32_t *ny_local);
 
+/* Grid and ensemble held by this ctx: global nx, ny and the number of members (host buffers of
+ * pf_get_fields / pf_trajectory are sized from these).  Any pointer may be NULL.  Errors: PF_ERR_ARG. */
+pf_status pf_shape(pf_ctx *ctx, int32_t *nx, int32_t *ny, int32_t *members);
+
 /* Override the step counter and time (used when resuming from saved fields).
  * Errors: PF_ERR_ARG. */
 pf_status pf_set_time(pf_ctx *ctx, int64_t steps, double t);

@@ -73,6 +73,17 @@ pf_status un_forward(un_ctx *ctx, int32_t batch, const float *hist, const float 
  * take the last lb predictions (lb <= lf) as the next window.  Synchronous. */
 pf_status un_rollout(un_ctx *ctx, int32_t batch, const float *hist, int32_t lf, int32_t n_leaps, float *out);
 
+/* Hybrid schedule DNS -> surrogate (section 2.2, the "DNS until t1, then U-Net" runs of
+ * P:240-241): n_dns composite-c snapshots of the DNS ctx `dns` (pf_trajectory, steps_between steps
+ * apart), then the U-Net rollout (un_rollout) from the last lb of them for n_leaps x lf
+ * snapshots.  The DNS ctx must hold a single domain of H x W (= the U-Net grid) with members <=
+ * max_batch; n_dns >= lb; lf >= lb.  out [members][n_dns + n_leaps*lf][H][W] (host, fp32);
+ * seconds[0] = DNS wall time, seconds[1] = surrogate wall time (host clock around each segment,
+ * both synchronised).  The composite (c where phi > 1/2, else 0) is the surrogate's state;
+ * no reconstruction of phi and rho follows the last leap (the paper does not describe one). */
+pf_status un_hybrid(un_ctx *ctx, pf_ctx *dns, int32_t n_dns, int64_t steps_between, int32_t lf, int32_t n_leaps,
+                    float *out, double seconds[2]);
+
 /* One bf16 3x3 'same' convolution on the tensor cores, for parity tests of the GEMM kernel alone:
  * in [npix = batch*H*W][cin] bf16 bits (NHWC), w [cout][9][cin] bf16 bits, out [npix][cout] fp32.
  * cin a multiple of 16, cout in {16, 32, 64, 128}; device pointers; runs on stream (or 0), async. */

@@ -1259,6 +1259,14 @@ pf_status pf_info(pf_ctx *c, int64_t *steps, double *t, int32_t *y0, int32_t *ny
     return PF_OK;
 }
 
+pf_status pf_shape(pf_ctx *c, int32_t *nx, int32_t *ny, int32_t *members) {
+    if (!c) return set_err(nullptr, PF_ERR_ARG, "ctx is NULL");
+    if (nx) *nx = c->p.nx;
+    if (ny) *ny = c->p.ny;
+    if (members) *members = c->p.n_members;
+    return PF_OK;
+}
+
 pf_status pf_set_time(pf_ctx *c, int64_t steps, double t) {
     if (!c) return set_err(nullptr, PF_ERR_ARG, "ctx is NULL");
     if (steps < 0) return set_err(c, PF_ERR_ARG, "steps must be >= 0");

@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdint>
@@ -1285,6 +1286,51 @@ pf_status un_rollout(un_ctx *c, int32_t batch, const float *hist, int32_t lf, in
     cudaFree(pred);
     cudaFree(dts);
     return s;
+}
+
+pf_status un_hybrid(un_ctx *c, pf_ctx *dns, int32_t n_dns, int64_t steps_between, int32_t lf, int32_t n_leaps,
+                    float *out, double seconds[2]) {
+    if (!c || !dns || !out) return fail(c, PF_ERR_ARG, "NULL argument");
+    int32_t nx = 0, ny = 0, members = 0, ny_loc = 0;
+    if (pf_shape(dns, &nx, &ny, &members) != PF_OK || pf_info(dns, nullptr, nullptr, nullptr, &ny_loc) != PF_OK)
+        return fail(c, PF_ERR_ARG, "bad DNS ctx");
+    if (nx != c->p.width || ny != c->p.height || ny_loc != ny)
+        return fail(c, PF_ERR_ARG, "the DNS ctx must be one domain of the U-Net grid (H x W)");
+    if (members < 1 || members > c->p.max_batch) return fail(c, PF_ERR_ARG, "members exceed max_batch");
+    if (n_dns < c->p.lb || lf < c->p.lb || n_leaps < 0 || steps_between < 0)
+        return fail(c, PF_ERR_ARG, "need n_dns >= lb, lf >= lb, n_leaps >= 0");
+    const size_t hw = (size_t)nx * ny;
+    const int lb = c->p.lb, total = n_dns + n_leaps * lf;
+    std::vector<double> traj((size_t)members * n_dns * hw);
+    auto t0 = std::chrono::steady_clock::now();
+    pf_status s = pf_trajectory(dns, n_dns, steps_between, traj.data(), nullptr);
+    auto t1 = std::chrono::steady_clock::now();
+    if (s != PF_OK) return fail(c, s, std::string("DNS segment failed: ") + pf_last_error(dns));
+    std::vector<float> hist((size_t)members * lb * hw);
+    for (int b = 0; b < members; ++b)
+        for (int q = 0; q < n_dns; ++q) {
+            const double *src = traj.data() + ((size_t)b * n_dns + q) * hw;
+            float *dst = out + ((size_t)b * total + q) * hw;
+            for (size_t i = 0; i < hw; ++i) dst[i] = (float)src[i];
+            if (q >= n_dns - lb) std::memcpy(hist.data() + ((size_t)b * lb + (q - (n_dns - lb))) * hw, dst, hw * 4);
+        }
+    double sur = 0.0;
+    if (n_leaps > 0) {
+        std::vector<float> pred((size_t)members * n_leaps * lf * hw);
+        auto t2 = std::chrono::steady_clock::now();
+        s = un_rollout(c, members, hist.data(), lf, n_leaps, pred.data());
+        auto t3 = std::chrono::steady_clock::now();
+        if (s != PF_OK) return s;
+        sur = std::chrono::duration<double>(t3 - t2).count();
+        for (int b = 0; b < members; ++b)
+            std::memcpy(out + ((size_t)b * total + n_dns) * hw, pred.data() + (size_t)b * n_leaps * lf * hw,
+                        (size_t)n_leaps * lf * hw * 4);
+    }
+    if (seconds) {
+        seconds[0] = std::chrono::duration<double>(t1 - t0).count();
+        seconds[1] = sur;
+    }
+    return PF_OK;
 }
 
 pf_status un_conv3x3(const uint16_t *in, int32_t batch, int32_t H, int32_t W, int32_t cin, const uint16_t *w,

@@ -103,6 +103,7 @@ def lib():
             "pf_set_fields": (C.c_int, [_ctx_p, i32, _D, _D, _D]),
             "pf_diagnostics": (C.c_int, [_ctx_p, i32, _D]),
             "pf_info": (C.c_int, [_ctx_p, C.POINTER(i64), _D, C.POINTER(i32), C.POINTER(i32)]),
+            "pf_shape": (C.c_int, [_ctx_p, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32)]),
             "pf_set_time": (C.c_int, [_ctx_p, i64, C.c_double]),
             "pf_launch_count": (C.c_int, [_ctx_p, C.POINTER(i64)]),
             "pf_profile": (C.c_int, [_ctx_p, i32]),
@@ -280,6 +281,13 @@ def pf_info(ctx):
     s, t, y0, ny = C.c_int64(), C.c_double(), C.c_int32(), C.c_int32()
     _check(lib().pf_info(ctx, C.byref(s), C.byref(t), C.byref(y0), C.byref(ny)), ctx)
     return s.value, t.value, y0.value, ny.value
+
+
+def pf_shape(ctx):
+    """(nx, ny, members) of the ctx."""
+    nx, ny, m = C.c_int32(), C.c_int32(), C.c_int32()
+    _check(lib().pf_shape(ctx, C.byref(nx), C.byref(ny), C.byref(m)), ctx)
+    return nx.value, ny.value, m.value
 
 
 def pf_set_time(ctx, steps: int, t: float):

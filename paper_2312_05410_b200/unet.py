@@ -39,6 +39,7 @@ def lib():
             "un_forward": (C.c_int, [vp, i32, _F, _F, _F]),
             "un_rollout": (C.c_int, [vp, i32, _F, i32, i32, _F]),
             "un_conv3x3": (C.c_int, [vp, i32, i32, i32, i32, vp, i32, vp, vp]),
+            "un_hybrid": (C.c_int, [vp, vp, i32, i64, i32, i32, _F, C.POINTER(C.c_double)]),
             "un_stream": (C.c_int, [vp, C.POINTER(vp)]),
             "un_launch_count": (C.c_int, [vp, C.POINTER(i64)]),
             "un_profile": (C.c_int, [vp, i32]),
@@ -117,6 +118,16 @@ class UNet:
         _check(lib().un_rollout(self.ctx, h.shape[0], h.ctypes.data_as(_F), lf, n_leaps,
                                 out.ctypes.data_as(_F)), self.ctx)
         return out
+
+    def hybrid(self, sim, n_dns, steps_between, lf, n_leaps):
+        """DNS (pf ctx of `sim`) for n_dns composite snapshots, then the U-Net rollout; returns
+        (snapshots [members, n_dns + n_leaps*lf, H, W], (dns_seconds, surrogate_seconds))."""
+        nx, ny, mem = pf.pf_shape(sim.ctx)
+        out = np.empty((mem, n_dns + n_leaps * lf, ny, nx), dtype=np.float32)
+        sec = (C.c_double * 2)()
+        _check(lib().un_hybrid(self.ctx, sim.ctx, n_dns, steps_between, lf, n_leaps, out.ctypes.data_as(_F), sec),
+               self.ctx)
+        return out, (sec[0], sec[1])
 
     def stream(self):
         s = C.c_void_p()

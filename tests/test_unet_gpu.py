@@ -136,3 +136,23 @@ def test_full_size_sampled_members():
     assert np.all(np.isfinite(got))
     for b in (0, 37):
         assert _rel(got[b], U.forward(hist[b], dts[b], P)) <= 2e-2, b
+
+
+def test_hybrid_schedule_dns_then_surrogate():
+    """un_hybrid: the DNS part equals pf_trajectory's composite snapshots, the surrogate part equals
+    un_rollout from the last lb of them (bitwise), and both segments are timed."""
+    from paper_2312_05410_b200 import pf
+    p = pf.pf_default_params(2).replace(nx=32, ny=32, n_members=2, ic_height=10.0, check_every=50)
+    n_dns, K, lf, leaps = 4, 5, 3, 2
+    net, _ = _net(32, 32, 2)
+    with net:
+        with pf.Simulation(p) as s:
+            out, (t_dns, t_sur) = net.hybrid(s, n_dns, K, lf, leaps)
+            assert pf.pf_info(s.ctx)[0] == (n_dns - 1) * K
+        with pf.Simulation(p) as s:
+            ref = np.empty((2, n_dns, 32, 32))
+            pf.pf_trajectory(s.ctx, n_dns, K, ref)
+        assert np.array_equal(out[:, :n_dns], ref.astype(np.float32))
+        roll = net.rollout(ref[:, n_dns - 3:].astype(np.float32), lf, leaps)
+    assert np.array_equal(out[:, n_dns:], roll)
+    assert out.shape == (2, n_dns + lf * leaps, 32, 32) and t_dns > 0 and t_sur > 0
