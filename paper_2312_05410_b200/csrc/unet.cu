@@ -141,6 +141,8 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
 // buffered in TMEM (2 x N columns): the epilogue of tile i (tcgen05.ld, fp32 stores, GroupNorm
 // partial sums) runs while the MMAs of tile i + 1 execute.
 constexpr int kKC = 18;
+constexpr int kProdWarps = 8;                        // loader warps of the warp-specialised kernels
+constexpr int kWsThreads = 32 * (kProdWarps + 5);   // + 4 epilogue warps + 1 MMA warp
 
 template <int N>
 struct ConvCfg {
@@ -150,9 +152,6 @@ struct ConvCfg {
     static constexpr uint32_t a_bytes = kKC * lbo_a;
     static constexpr uint32_t b_bytes = kKC * lbo_b;
     static constexpr uint32_t stage = a_bytes + b_bytes;
-    static constexpr int S = (110 * 1024) / stage >= 2 ? 2 : ((200 * 1024) / stage > 4 ? 4 : (200 * 1024) / stage);
-    static constexpr size_t smem = 1024 + S * stage + 128;
-    static_assert(S >= 2, "ring too shallow");
 };
 
 __device__ __forceinline__ void cp_async_wait_n(int n) {   // n <= 3
@@ -246,29 +245,40 @@ __device__ __forceinline__ void conv_tile_out(uint32_t tacc, int64_t t, int64_t 
 // unit of `gran` pixels -- a warp's 32 pixels when H W is a multiple of 32 (a warp then never
 // straddles two samples), else each pixel -- written to part[unit][group][2]; HEAD: one group made
 // of channel 0 only.
+// General-shape kernel (any H, W; here the W = 64 / 32 levels): im2col gather, warp-specialised
+// like the row kernel below.  A step is one (tile, K block of 144) pair; warps 0-7 gather the A block
+// (one pixel row per thread half, cp.async 16-byte channel chunks, zero-fill = the 'same' padding)
+// and the weight block, and signal full[s] (cp.async.mbarrier.arrive.noinc); warp 12 issues the
+// 9 MMAs of the step into the tile's accumulator (2 sets) and commits empty[s] / accf[b];
+// warps 8-11 drain finished tiles.
 template <int N, bool HEAD>
-__global__ void __launch_bounds__(256) conv3x3_kernel(const bf16 *__restrict__ in, const bf16 *__restrict__ w,
-                                                         float *__restrict__ out, double *__restrict__ part,
-                                                         int64_t npix, int H, int W, int cin, int gran) {
+__global__ void __launch_bounds__(kWsThreads) conv3x3_kernel(const bf16 *__restrict__ in, const bf16 *__restrict__ w,
+                                                             float *__restrict__ out, double *__restrict__ part,
+                                                             int64_t npix, int H, int W, int cin, int gran, int S) {
     using C = ConvCfg<N>;
-    constexpr int S = C::S;
-    constexpr int NG = HEAD ? 1 : kGroups, GC = HEAD ? 1 : N / kGroups;
-    constexpr int ECOLS = N >= 32 ? N / 2 : N;                       // epilogue columns per warp
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char *sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-    uint64_t *mma_bar = reinterpret_cast<uint64_t *>(sm + S * C::stage);
-    uint64_t *acc_bar = mma_bar + S;
-    uint32_t *tslot = reinterpret_cast<uint32_t *>(acc_bar + 2);
+    uint64_t *full = reinterpret_cast<uint64_t *>(sm + S * C::stage);
+    uint64_t *empty = full + S;
+    uint64_t *accf = empty + S;
+    uint64_t *acce = accf + 2;
+    uint32_t *tslot = reinterpret_cast<uint32_t *>(acce + 2);
     const uint32_t sbase = smem_u32(sm);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    constexpr int NP = kProdWarps * 32, MMAW = kProdWarps + 4;
 
     if (tid == 0) {
-        for (int q = 0; q < S; ++q) mbar_init(&mma_bar[q], 1);
-        mbar_init(&acc_bar[0], 1);
-        mbar_init(&acc_bar[1], 1);
+        for (int q = 0; q < S; ++q) {
+            mbar_init(&full[q], NP);
+            mbar_init(&empty[q], 1);
+        }
+        for (int q = 0; q < 2; ++q) {
+            mbar_init(&accf[q], 1);
+            mbar_init(&acce[q], 4);
+        }
         fence_mbar_init();
     }
-    if (warp == 0) tmem_alloc<C::tcols>(tslot);
+    if (warp == MMAW) tmem_alloc<C::tcols>(tslot);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -279,120 +289,117 @@ __global__ void __launch_bounds__(256) conv3x3_kernel(const bf16 *__restrict__ i
     const int HW = H * W, cq = cin >> 3, nkb = 9 * cq / kKC;
     const int64_t krow = 9 * (int64_t)cin;
     const int nsteps = ntl * nkb;
-    const int m = tid & 127, half = tid >> 7;
-    const uint32_t arow = (uint32_t)((m >> 3) * 128 + (m & 7) * 16);
 
-    // per-tile gather state of this thread's pixel: center offset, 3x3 validity mask (bit ky*3+kx)
-    int ctl = -1;
-    int64_t pc = 0;
-    uint32_t vmask = 0;
-    const int64_t Wc = (int64_t)W * cin;
-    auto load = [&](int j) {
-        const int tl = j / nkb, kb = j - tl * nkb;
-        if (tl != ctl) {
-            ctl = tl;
-            const int64_t p = ((int64_t)blockIdx.x + (int64_t)tl * gridDim.x) * kBM + m;
-            vmask = 0;
-            pc = 0;
-            if (p < npix) {
-                const int b = (int)(p / HW);
-                const int rem = (int)(p - (int64_t)b * HW);
-                const int y = rem / W, x = rem - y * W;
-                pc = p * cin;
-                const uint32_t rows = (y > 0 ? 1u : 0u) | 2u | (y < H - 1 ? 4u : 0u);
-                const uint32_t cols = (x > 0 ? 1u : 0u) | 2u | (x < W - 1 ? 4u : 0u);
-                for (int ky = 0; ky < 3; ++ky)
-                    if (rows >> ky & 1u) vmask |= cols << (3 * ky);
-            }
-        }
-        const uint32_t a0 = sbase + (j % S) * C::stage, b0 = a0 + C::a_bytes;
-        const int g0 = kb * kKC + half;
-        int tap = g0 / cq, cc = g0 - tap * cq;
-        int ky = tap / 3, kx = tap - 3 * ky;
-        int64_t toff = (ky - 1) * Wc + (kx - 1) * cin;
-#pragma unroll 3
-        for (int q = half; q < kKC; q += 2) {
-            const bool v = (vmask >> (ky * 3 + kx)) & 1u;
-            cp_async16(a0 + q * C::lbo_a + arow, v ? in + pc + toff + cc * 8 : in, v);
-            cc += 2;
-            if (cc >= cq) {
-                cc -= cq;
-                if (++kx == 3) {
-                    kx = 0;
-                    ++ky;
-                    toff += Wc - 2 * cin;
-                } else {
-                    toff += cin;
+    if (warp < kProdWarps) {
+        // ------------------------------- producers -------------------------------
+        const int m = tid & 127, half = tid >> 7;     // pixel row of A, chunk parity
+        const uint32_t arow = (uint32_t)((m >> 3) * 128 + (m & 7) * 16);
+        int ctl = -1;
+        int64_t pc = 0;
+        uint32_t vmask = 0;
+        const int64_t Wc = (int64_t)W * cin;
+        for (int j = 0; j < nsteps; ++j) {
+            const int s = j % S;
+            if (j >= S) mbar_wait(&empty[s], (uint32_t)(j / S - 1) & 1u);
+            const int tl = j / nkb, kb = j - tl * nkb;
+            if (tl != ctl) {
+                ctl = tl;
+                const int64_t p = ((int64_t)blockIdx.x + (int64_t)tl * gridDim.x) * kBM + m;
+                vmask = 0;
+                pc = 0;
+                if (p < npix) {
+                    const int b = (int)(p / HW);
+                    const int rem = (int)(p - (int64_t)b * HW);
+                    const int y = rem / W, x = rem - y * W;
+                    pc = p * cin;
+                    const uint32_t rows = (y > 0 ? 1u : 0u) | 2u | (y < H - 1 ? 4u : 0u);
+                    const uint32_t cols = (x > 0 ? 1u : 0u) | 2u | (x < W - 1 ? 4u : 0u);
+                    for (int ky = 0; ky < 3; ++ky)
+                        if (rows >> ky & 1u) vmask |= cols << (3 * ky);
                 }
             }
+            const uint32_t a0 = sbase + s * C::stage, b0 = a0 + C::a_bytes;
+            const int g0 = kb * kKC + half;
+            int tap = g0 / cq, cc = g0 - tap * cq;
+            int ky = tap / 3, kx = tap - 3 * ky;
+            int64_t toff = (ky - 1) * Wc + (kx - 1) * cin;
+            for (int q = half; q < kKC; q += 2) {
+                const bool v = (vmask >> (ky * 3 + kx)) & 1u;
+                cp_async16(a0 + q * C::lbo_a + arow, v ? in + pc + toff + cc * 8 : in, v);
+                cc += 2;
+                if (cc >= cq) {
+                    cc -= cq;
+                    if (++kx == 3) {
+                        kx = 0;
+                        ++ky;
+                        toff += Wc - 2 * cin;
+                    } else {
+                        toff += cin;
+                    }
+                }
+            }
+            for (int i = tid; i < N * kKC; i += NP) {
+                const int n = i / kKC, q = i - n * kKC;
+                cp_async16(b0 + q * C::lbo_b + (n >> 3) * 128 + (n & 7) * 16, w + n * krow + (int64_t)(kb * kKC + q) * 8,
+                           true);
+            }
+            asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&full[s])) : "memory");
         }
-        for (int i = tid; i < N * kKC; i += 256) {
-            const int n = i / kKC, q = i - n * kKC;
-            cp_async16(b0 + q * C::lbo_b + (n >> 3) * 128 + (n & 7) * 16, w + n * krow + (int64_t)(kb * kKC + q) * 8, true);
-        }
-    };
-
-    auto epilogue = [&](int tl) {
-        mbar_wait(&acc_bar[tl & 1], (uint32_t)(tl >> 1) & 1u);
-        tc_fence_after();
-        conv_tile_out<N, HEAD>(tmem + (uint32_t)((tl & 1) * N), (int64_t)blockIdx.x + (int64_t)tl * gridDim.x, npix,
-                               out, part, gran, 0);
-        tc_fence_before();
-    };
-
-    for (int j = 0; j < S - 1; ++j) {
-        if (j < nsteps) load(j);
-        cp_async_commit();
-    }
-    for (int j = 0; j < nsteps; ++j) {
-        const int jn = j + S - 1;
-        if (jn < nsteps) {
-            if (j >= 1) mbar_wait(&mma_bar[(j - 1) % S], (uint32_t)((j - 1) / S) & 1u);   // stage of step j-1 free
-            load(jn);
-        }
-        cp_async_commit();
-        cp_async_wait_n(S - 1);    // step j has landed
-        fence_proxy_async();       // generic-proxy smem writes -> visible to the tensor core
-        __syncthreads();
-        const int tl = j / nkb, kb = j - tl * nkb;
-        if (tid == 0) {
-            tc_fence_after();
-            const uint32_t a0 = sbase + (j % S) * C::stage, b0 = a0 + C::a_bytes;
-            const uint32_t acc = tmem + (uint32_t)((tl & 1) * N);
+    } else if (warp == MMAW) {
+        // ------------------------------- MMA issuer -------------------------------
+        if (lane == 0)
+            for (int j = 0; j < nsteps; ++j) {
+                const int s = j % S, tl = j / nkb, kb = j - tl * nkb, b = tl & 1;
+                mbar_wait(&full[s], (uint32_t)(j / S) & 1u);
+                if (kb == 0 && tl >= 2) mbar_wait(&acce[b], (uint32_t)(tl / 2 - 1) & 1u);
+                tc_fence_after();
+                const uint32_t a0 = sbase + s * C::stage, b0 = a0 + C::a_bytes;
+                const uint32_t acc = tmem + (uint32_t)(b * N);
 #pragma unroll
-            for (int k = 0; k < kKC / 2; ++k)
-                umma(acc, sdesc(a0 + 2 * k * C::lbo_a, C::lbo_a, 128), sdesc(b0 + 2 * k * C::lbo_b, C::lbo_b, 128),
-                     idesc_bf16(N), (kb | k) ? 1u : 0u);
-            umma_commit(&mma_bar[j % S]);
-            if (kb == nkb - 1) umma_commit(&acc_bar[tl & 1]);
+                for (int k = 0; k < kKC / 2; ++k)
+                    umma(acc, sdesc(a0 + 2 * k * C::lbo_a, C::lbo_a, 128), sdesc(b0 + 2 * k * C::lbo_b, C::lbo_b, 128),
+                         idesc_bf16(N), (kb | k) ? 1u : 0u);
+                umma_commit(&empty[s]);
+                if (kb == nkb - 1) umma_commit(&accf[b]);
+            }
+        __syncwarp();
+    } else {
+        // ------------------------------- epilogue warps -------------------------------
+        for (int tl = 0; tl < ntl; ++tl) {
+            const int b = tl & 1;
+            mbar_wait(&accf[b], (uint32_t)(tl >> 1) & 1u);
+            tc_fence_after();
+            conv_tile_out<N, HEAD, false>(tmem + (uint32_t)(b * N), (int64_t)blockIdx.x + (int64_t)tl * gridDim.x, npix,
+                                          out, part, gran, 0);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&acce[b]);
         }
-        if (kb == nkb - 1 && tl >= 1) epilogue(tl - 1);   // overlaps the MMAs of tile tl
     }
-    if (ntl >= 1) epilogue(ntl - 1);
+    tc_fence_before();
     __syncthreads();
-    if (warp == 0) tmem_dealloc<C::tcols>(tmem);
+    if (warp == MMAW) tmem_dealloc<C::tcols>(tmem);
 }
 
 template <int N, bool HEAD>
 cudaError_t launch_conv_n(const bf16 *in, const bf16 *w, float *out, double *part, int64_t npix, int H, int W,
                           int cin, cudaStream_t st) {
     using C = ConvCfg<N>;
-    static int nsm = 0, occ = 1;
+    const int S = (int)((220 * 1024 - 1200) / C::stage) > 6 ? 6 : (int)((220 * 1024 - 1200) / C::stage);
+    const size_t smem = 1024 + (size_t)S * C::stage + 128;
+    static int nsm = 0;
     if (nsm == 0) {
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
         cudaError_t e = cudaFuncSetAttribute(conv3x3_kernel<N, HEAD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)C::smem);
+                                             (int)smem);
         if (e != cudaSuccess) return e;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, conv3x3_kernel<N, HEAD>, 256, C::smem);
-        if (e != cudaSuccess) return e;
-        occ = occ < 1 ? 1 : (occ > 2 ? 2 : occ);   // TMEM: 2 CTAs x 2N columns <= 512
     }
     const int gran = (H * W) % 32 == 0 ? 32 : 1;
-    const int64_t tiles = (npix + kBM - 1) / kBM, slots = (int64_t)nsm * occ;
-    const unsigned grid = (unsigned)(tiles < slots ? tiles : slots);
-    conv3x3_kernel<N, HEAD><<<grid, 256, C::smem, st>>>(in, w, out, part, npix, H, W, cin, gran);
+    const int64_t tiles = (npix + kBM - 1) / kBM;
+    const unsigned grid = (unsigned)(tiles < nsm ? tiles : nsm);
+    conv3x3_kernel<N, HEAD><<<grid, kWsThreads, smem, st>>>(in, w, out, part, npix, H, W, cin, gran, S);
     return cudaGetLastError();
 }
 
@@ -421,14 +428,12 @@ struct RowCfg {
 // (tiles interleaved) and commits to empty[s] (the stage may be refilled) and accf[b] (the
 // accumulators are ready); warps 8-11 wait accf[b], drain the accumulators (tcgen05.ld, fp32
 // stores, GroupNorm partial sums) and arrive on acce[b] (the set may be overwritten).
-constexpr int kProdWarps = 8;                        // loader warps
-constexpr int kWsThreads = 32 * (kProdWarps + 5);   // + 4 epilogue warps + 1 MMA warp
 
 template <int N, bool HEAD>
 __global__ void __launch_bounds__(kWsThreads) conv3x3_rows_kernel(const bf16 *__restrict__ in,
                                                                   const bf16 *__restrict__ w, float *__restrict__ out,
                                                                   double *__restrict__ part, int64_t npix, int H, int W,
-                                                                  int cin, int S, int T, int gran, int dbg,
+                                                                  int cin, int S, int T, int gran,
                                                                   const __grid_constant__ CUtensorMap rmap, int use_tma) {
     using C = RowCfg<N>;
     constexpr int NB = C::nbuf;
@@ -499,12 +504,11 @@ __global__ void __launch_bounds__(kWsThreads) conv3x3_rows_kernel(const bf16 *__
                     }
                 }
             }
-        } else
-        for (int k = 0; k < ngl; ++k) {
-            const int s = k % S;
-            if (k >= S) mbar_wait(&empty[s], (uint32_t)(k / S - 1) & 1u);
-            const uint32_t a0 = sbase + s * a_bytes;
-            if (!(dbg & 1))
+        } else {         // all producer threads: cp.async 16-byte chunks, zero-fill = the padding
+            for (int k = 0; k < ngl; ++k) {
+                const int s = k % S;
+                if (k >= S) mbar_wait(&empty[s], (uint32_t)(k / S - 1) & 1u);
+                const uint32_t a0 = sbase + s * a_bytes;
                 for (int i = 0; i < T; ++i) {
                     const int64_t t = tile_of(k, i);
                     if (t >= tiles) break;
@@ -524,8 +528,9 @@ __global__ void __launch_bounds__(kWsThreads) conv3x3_rows_kernel(const bf16 *__
                         }
                     }
                 }
-            asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&full[s]))
-                         : "memory");
+                asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&full[s]))
+                             : "memory");
+            }
         }
     } else if (warp == kProdWarps + 4) {
         // ------------------------------- MMA issuer -------------------------------
@@ -537,7 +542,6 @@ __global__ void __launch_bounds__(kWsThreads) conv3x3_rows_kernel(const bf16 *__
                 tc_fence_after();
                 int nt = 0;
                 while (nt < T && tile_of(k, nt) < tiles) ++nt;
-                if (dbg & 2) nt = 0;
                 const uint32_t a0 = sbase + s * a_bytes;
                 const uint32_t acc0 = tmem + (uint32_t)(b * C::T * N);
                 for (int tap = 0; tap < 9; ++tap) {
@@ -562,12 +566,11 @@ __global__ void __launch_bounds__(kWsThreads) conv3x3_rows_kernel(const bf16 *__
             const int b = k % NB;
             mbar_wait(&accf[b], (uint32_t)(k / NB) & 1u);
             tc_fence_after();
-            if (!(dbg & 4))
-                for (int i = 0; i < T; ++i) {
-                    const int64_t t = tile_of(k, i);
-                    if (t < tiles)
-                        conv_tile_out<N, HEAD, false>(tmem + (uint32_t)((b * C::T + i) * N), t, npix, out, part, gran, 0);
-                }
+            for (int i = 0; i < T; ++i) {
+                const int64_t t = tile_of(k, i);
+                if (t < tiles)
+                    conv_tile_out<N, HEAD, false>(tmem + (uint32_t)((b * C::T + i) * N), t, npix, out, part, gran, 0);
+            }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&acce[b]);
@@ -648,12 +651,11 @@ cudaError_t launch_conv_rows(const bf16 *in, const bf16 *w, float *out, double *
     const int gran = (H * W) % 32 == 0 ? 32 : 1;
     const int64_t groups = (npix / kBM + T - 1) / T, slots = (int64_t)nsm * occ;
     const unsigned grid = (unsigned)(groups < slots ? groups : slots);
-    static const int dbg = getenv("UN_DBG") ? atoi(getenv("UN_DBG")) : 0;
     static const int notma = getenv("UN_NO_TMA") ? atoi(getenv("UN_NO_TMA")) : 0;
     CUtensorMap rmap;
     std::memset(&rmap, 0, sizeof rmap);
     const int use_tma = !notma && encode_rows_map(&rmap, in, (int)(npix / ((int64_t)H * W)), H, W, cin);
-    conv3x3_rows_kernel<N, HEAD><<<grid, kWsThreads, smem, st>>>(in, w, out, part, npix, H, W, cin, S, T, gran, dbg,
+    conv3x3_rows_kernel<N, HEAD><<<grid, kWsThreads, smem, st>>>(in, w, out, part, npix, H, W, cin, S, T, gran,
                                                                    rmap, use_tma);
     return cudaGetLastError();
 }
