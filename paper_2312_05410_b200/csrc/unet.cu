@@ -59,7 +59,19 @@ __device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
 __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
+// Waits of the loader and epilogue warps carry a suspend-time hint (the warp sleeps instead of
+// re-issuing try_wait, leaving issue slots to the others); the single MMA-issuing thread spins
+// (mbar_wait_spin), its wake-up latency is on the critical path.
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity), "r"(1000000u)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait_spin(uint64_t *bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n"
         "WAIT_%=:\n\t"
@@ -350,8 +362,8 @@ __global__ void __launch_bounds__(kWsThreads) conv3x3_kernel(const bf16 *__restr
         if (lane == 0)
             for (int j = 0; j < nsteps; ++j) {
                 const int s = j % S, tl = j / nkb, kb = j - tl * nkb, b = tl & 1;
-                mbar_wait(&full[s], (uint32_t)(j / S) & 1u);
-                if (kb == 0 && tl >= 2) mbar_wait(&acce[b], (uint32_t)(tl / 2 - 1) & 1u);
+                mbar_wait_spin(&full[s], (uint32_t)(j / S) & 1u);
+                if (kb == 0 && tl >= 2) mbar_wait_spin(&acce[b], (uint32_t)(tl / 2 - 1) & 1u);
                 tc_fence_after();
                 const uint32_t a0 = sbase + s * C::stage, b0 = a0 + C::a_bytes;
                 const uint32_t acc = tmem + (uint32_t)(b * N);
@@ -537,8 +549,8 @@ __global__ void __launch_bounds__(kWsThreads) conv3x3_rows_kernel(const bf16 *__
         if (lane == 0) {
             for (int k = 0; k < ngl; ++k) {
                 const int s = k % S, b = k % NB;
-                mbar_wait(&full[s], (uint32_t)(k / S) & 1u);
-                if (k >= NB) mbar_wait(&acce[b], (uint32_t)(k / NB - 1) & 1u);
+                mbar_wait_spin(&full[s], (uint32_t)(k / S) & 1u);
+                if (k >= NB) mbar_wait_spin(&acce[b], (uint32_t)(k / NB - 1) & 1u);
                 tc_fence_after();
                 int nt = 0;
                 while (nt < T && tile_of(k, nt) < tiles) ++nt;
