@@ -180,7 +180,8 @@ pf_status pf_step(pf_ctx *ctx, int64_t n);
  * pf_set_fields(ctx, -1, c_in, phi_in, rho_in); pf_step(ctx, n); pf_get_fields(ctx, -1, c_out,
  * phi_out, rho_out) -- bitwise the same result -- but pipelined over `chunks` groups of members
  * (members are independent): the upload of chunk k+1 and the download of chunk k-1 overlap the
- * steps of chunk k on separate streams (pinned host buffers make the copies asynchronous).
+ * steps of chunk k on separate streams (pinned host buffers make the copies asynchronous).  With
+ * chunks >= 3 the first and last chunks hold ~1/8 of the members each (short exposed copies).
  * Buffers: all members stacked, as for member = -1; NULL inputs keep the device state, NULL
  * outputs are skipped.  The blow-up check runs once per chunk at the end of the call (the reported
  * step window is the whole call).  Single-GPU fp64 contexts with chunks >= 2 pipeline; other

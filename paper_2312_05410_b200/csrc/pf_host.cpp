@@ -1022,6 +1022,19 @@ pf_status pf_run_host(pf_ctx *c, int64_t n, const double *ci, const double *pi, 
         c->ev_in.push_back(a);
         c->ev_done.push_back(b);
     }
+    // chunk boundaries: 2 chunks split evenly; with >= 3 the first and last chunks are small
+    // (~1/8 of the members each) so that the exposed upload of the first and download of the last
+    // are short, and the middle chunks (most of the work) run at full size
+    std::vector<int> bnd(K + 1, 0);
+    if (K >= 3) {
+        const int edge = std::max(1, std::min(M / 8, (M - (K - 2)) / 2));
+        bnd[1] = edge;
+        bnd[K - 1] = M - edge;
+        for (int k = 2; k < K - 1; ++k) bnd[k] = edge + (int)((int64_t)(M - 2 * edge) * (k - 1) / (K - 2));
+        bnd[K] = M;
+    } else {
+        for (int k = 0; k <= K; ++k) bnd[k] = (int)((int64_t)M * k / K);
+    }
     const size_t hrow = (size_t)c->p.nx * sizeof(double), hmem = (size_t)S.L.ny_loc * hrow;
     const size_t dpitch = (size_t)S.L.pitch * sizeof(double);
     const double *src[3] = {ci, pi, ri};
@@ -1034,7 +1047,7 @@ pf_status pf_run_host(pf_ctx *c, int64_t n, const double *ci, const double *pi, 
     CK(c, cudaStreamWaitEvent(c->h2d, c->ev_done[0], 0));
     // 1. uploads, chunk by chunk, on the H2D stream
     for (int k = 0; k < K; ++k) {
-        const int m0 = (int)((int64_t)M * k / K), m1 = (int)((int64_t)M * (k + 1) / K);
+        const int m0 = bnd[k], m1 = bnd[k + 1];
         for (int m = m0; m < m1; ++m)
             for (int f = 0; f < 3; ++f)
                 if (src[f])
@@ -1044,7 +1057,7 @@ pf_status pf_run_host(pf_ctx *c, int64_t n, const double *ci, const double *pi, 
     }
     // 2. per chunk on the compute stream: ghost frame, n steps, diagnostics; then its download
     for (int k = 0; k < K; ++k) {
-        const int m0 = (int)((int64_t)M * k / K), m1 = (int)((int64_t)M * (k + 1) / K);
+        const int m0 = bnd[k], m1 = bnd[k + 1];
         pf::Layout L = S.L;
         L.m0 = m0;
         L.members = m1 - m0;
