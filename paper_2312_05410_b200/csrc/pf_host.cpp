@@ -1027,7 +1027,7 @@ pf_status pf_run_host(pf_ctx *c, int64_t n, const double *ci, const double *pi, 
     // are short, and the middle chunks (most of the work) run at full size
     std::vector<int> bnd(K + 1, 0);
     if (K >= 3) {
-        const int edge = std::max(1, std::min(M / 8, (M - (K - 2)) / 2));
+        const int edge = std::max(1, std::min(M / 8, (M - (K - 2)) / 2));   // 1/8: best of 1/4 .. 1/32
         bnd[1] = edge;
         bnd[K - 1] = M - edge;
         for (int k = 2; k < K - 1; ++k) bnd[k] = edge + (int)((int64_t)(M - 2 * edge) * (k - 1) / (K - 2));
