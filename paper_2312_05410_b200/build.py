@@ -101,7 +101,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
             objs.append(obj)
             if not force and not _stale(obj, src):
                 continue
-            _run([os.path.join(CUDA, "bin", "nvcc"), *ARCH, "-O3", "-lineinfo", "-std=c++17",
+            extra = os.environ.get("PF_NVCC_EXTRA", "").split()
+            _run([os.path.join(CUDA, "bin", "nvcc"), *ARCH, "-O3", "-lineinfo", "-std=c++17", *extra,
                   "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr", "-fmad=false",
                   *incs, "-c", src, "-o", obj], verbose)
         elif f.endswith(".cpp"):

@@ -1421,9 +1421,15 @@ constexpr RingVariant kStream1{4, 4, 2}, kStream2{2, 6, 2};
 #define PF_F32_SLOTS 20
 #endif
 constexpr int kF32Slots = PF_F32_SLOTS;
+#ifndef PF_PAIR_R1
+#define PF_PAIR_R1 2
+#endif
+#ifndef PF_PAIR_R2
+#define PF_PAIR_R2 2
+#endif
 template <typename real, int NCW, bool BASE>
 struct PairCfg {
-    static constexpr int R = 2;
+    static constexpr int R = BASE ? PF_PAIR_R2 : PF_PAIR_R1;   // rows per TMA box
     static constexpr int bx_max = kPairCols * NCW + 2 * kPairHalo;
     static constexpr int slot = (3 * R * bx_max * (int)sizeof(real) + 127) / 128 * 128 * (BASE ? 2 : 1);
     // fp64 stage 1 keeps its ring small (>= 3 boxes) to leave L1 to the output stores: measured
