@@ -709,27 +709,32 @@ __global__ void pack_input_kernel(const float *__restrict__ hist, bf16 *__restri
     }
 }
 
-// f(dt) = w2 sin(w1 sin(w0 dt + b0) + b1) + b2; cond[b][k] = (w^{Lp} f)_k for all levels
-__global__ void __launch_bounds__(kBasis) time_mlp_kernel(const double *__restrict__ mlp, const double *__restrict__ wl,
+// f(dt) = w2 sin(w1 sin(w0 dt + b0) + b1) + b2; cond[b][k] = (w^{Lp} f)_k for all levels.
+// The matrices are stored transposed on the device (w1t[j][i] = w1[i][j], wlt[j][k] = wl[k][j]),
+// so that thread i's loads of one column j are coalesced across the block.
+__global__ void __launch_bounds__(kBasis) time_mlp_kernel(const double *__restrict__ mlp, const double *__restrict__ wlt,
                                                           const float *__restrict__ dt, float *__restrict__ cond,
                                                           int ctot) {
     __shared__ double h0[kBasis], h1[kBasis], f[kBasis];
     const int i = threadIdx.x, b = blockIdx.x;
-    const double *w0 = mlp, *b0 = w0 + kBasis, *w1 = b0 + kBasis, *b1 = w1 + kBasis * kBasis, *w2 = b1 + kBasis,
-                 *b2 = w2 + kBasis * kBasis;
+    const double *w0 = mlp, *b0 = w0 + kBasis, *w1t = b0 + kBasis, *b1 = w1t + kBasis * kBasis, *w2t = b1 + kBasis,
+                 *b2 = w2t + kBasis * kBasis;
     h0[i] = sin(w0[i] * (double)dt[b] + b0[i]);
     __syncthreads();
     double s = 0.0;
-    for (int j = 0; j < kBasis; ++j) s += w1[i * kBasis + j] * h0[j];
+#pragma unroll 8
+    for (int j = 0; j < kBasis; ++j) s += w1t[j * kBasis + i] * h0[j];
     h1[i] = sin(s + b1[i]);
     __syncthreads();
     s = 0.0;
-    for (int j = 0; j < kBasis; ++j) s += w2[i * kBasis + j] * h1[j];
+#pragma unroll 8
+    for (int j = 0; j < kBasis; ++j) s += w2t[j * kBasis + i] * h1[j];
     f[i] = s + b2[i];
     __syncthreads();
     for (int k = i; k < ctot; k += kBasis) {
         double a = 0.0;
-        for (int j = 0; j < kBasis; ++j) a += wl[(int64_t)k * kBasis + j] * f[j];
+#pragma unroll 8
+        for (int j = 0; j < kBasis; ++j) a += wlt[(int64_t)j * ctot + k] * f[j];
         cond[(int64_t)b * ctot + k] = (float)a;
     }
 }
@@ -1222,14 +1227,21 @@ pf_status un_set_weights(un_ctx *c, const float *blob, int64_t n) {
         UCK(c, cudaMemcpy(c->bet[l], q, co * sizeof(float), cudaMemcpyHostToDevice));
         q += co;
     }
-    std::vector<double> wl((size_t)c->ctot * kBasis);
-    for (size_t i = 0; i < wl.size(); ++i) wl[i] = q[i];
+    std::vector<double> wl((size_t)c->ctot * kBasis);   // transposed: wl[j][k] = w^{L}[k][j]
+    for (int k = 0; k < c->ctot; ++k)
+        for (int j = 0; j < kBasis; ++j) wl[(size_t)j * c->ctot + k] = q[(size_t)k * kBasis + j];
     q += wl.size();
     UCK(c, cudaMemcpy(c->wl, wl.data(), wl.size() * sizeof(double), cudaMemcpyHostToDevice));
     UCK(c, cudaMemcpy(c->upw, q, 12 * sizeof(float), cudaMemcpyHostToDevice));
     q += 12;
     std::vector<double> mlp((size_t)4 * kBasis + 2 * kBasis * kBasis);
     for (size_t i = 0; i < mlp.size(); ++i) mlp[i] = q[i];
+    for (int m = 0; m < 2; ++m) {   // w1, w2 transposed (w1 at 2*128, w2 at 3*128 + 128^2)
+        double *wm = mlp.data() + (m == 0 ? 2 * kBasis : 3 * kBasis + kBasis * kBasis);
+        const float *src = q + (m == 0 ? 2 * kBasis : 3 * kBasis + kBasis * kBasis);
+        for (int i = 0; i < kBasis; ++i)
+            for (int j = 0; j < kBasis; ++j) wm[(size_t)j * kBasis + i] = src[(size_t)i * kBasis + j];
+    }
     q += mlp.size();
     UCK(c, cudaMemcpy(c->mlp, mlp.data(), mlp.size() * sizeof(double), cudaMemcpyHostToDevice));
     c->have_w = true;
