@@ -25,6 +25,11 @@
 
 namespace cg = cooperative_groups;
 
+#ifndef PF_PAIR_UNROLL
+#define PF_PAIR_UNROLL 1   // unroll of the pair kernel's slot loop (experiment knob)
+#endif
+constexpr int kPairUnroll = PF_PAIR_UNROLL;
+
 namespace pf {
 
 int env_int(const char *name, int dflt) {
@@ -822,6 +827,7 @@ __global__ void __launch_bounds__(32 * NCW + 32, MINB) pair_kernel(
         real P3x = 0, P3y = 0, R3x = 0, R3y = 0;          // phi, rho row k-3
         real Fsx = 0, Fsy = 0;                            // south face fluxes of row k-2
         const real *prev = slots + (sidx == 0 ? S - 1 : sidx - 1) * rg.slot_elems + ci;
+#pragma unroll kPairUnroll
         for (int j = 0; j < nsl; ++j) {
             const real *cur = slots + sidx * rg.slot_elems + ci;
             mbar_wait(&full[sidx], par);
@@ -1421,6 +1427,9 @@ constexpr RingVariant kStream1{4, 4, 2}, kStream2{2, 6, 2};
 #define PF_F32_SLOTS 20
 #endif
 constexpr int kF32Slots = PF_F32_SLOTS;
+#ifndef PF_F64_SLOTS
+#define PF_F64_SLOTS 16
+#endif
 #ifndef PF_PAIR_R1
 #define PF_PAIR_R1 2
 #endif
@@ -1438,7 +1447,7 @@ struct PairCfg {
     static constexpr int ring_raw(int b) { return ((smem_kb * 1024) / b - 2048) / slot; }
     static constexpr int ring(int b) { return (!BASE && sizeof(real) == 8 && ring_raw(b) < 3) ? 3 : ring_raw(b); }
     static constexpr int pick(int b) { return b <= 1 || ring(b) >= 3 ? b : pick(b - 1); }
-    static constexpr int wslots = sizeof(real) == 8 ? 16 : kF32Slots;   // warp slots per SM budget
+    static constexpr int wslots = sizeof(real) == 8 ? PF_F64_SLOTS : kF32Slots;   // warp slots per SM budget
     static constexpr int minb = pick(wslots / (NCW + 1) > 8 ? 8 : wslots / (NCW + 1));
     static constexpr int S = ring(minb) > 8 ? 8 : ring(minb);
     static_assert(S >= 3, "ring too shallow");
