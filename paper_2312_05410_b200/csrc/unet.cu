@@ -931,6 +931,13 @@ struct un_ctx {
     std::vector<cudaEvent_t> pool;
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> rec;
     double flops = 0.0;
+    // CUDA graph of the last forward (batch and buffer pointers as the key): replays skip the
+    // 35 launch latencies; rebuilt when the key changes, bypassed while profiling
+    cudaGraphExec_t gexec = nullptr;
+    int gB = 0;
+    const void *gh = nullptr, *gd = nullptr;
+    void *go = nullptr;
+    int64_t glaunch = 0;
 };
 
 namespace {
@@ -1253,7 +1260,34 @@ pf_status un_forward_device(un_ctx *c, int32_t batch, const float *hist, const f
     if (batch < 1 || batch > c->p.max_batch) return fail(c, PF_ERR_ARG, "batch out of range");
     if (!c->have_w) return fail(c, PF_ERR_STATE, "no weights: call un_set_weights first");
     cudaSetDevice(c->p.device);
-    return forward(c, batch, hist, dt, out);
+    static const bool nograph = getenv("UN_NO_GRAPH") && atoi(getenv("UN_NO_GRAPH"));
+    if (c->prof || nograph) return forward(c, batch, hist, dt, out);
+    if (!c->gexec || c->gB != batch || c->gh != hist || c->gd != dt || c->go != out) {
+        if (c->gexec) cudaGraphExecDestroy(c->gexec);
+        c->gexec = nullptr;
+        cudaGraph_t g = nullptr;
+        UCK(c, cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
+        const int64_t l0 = c->launches;
+        pf_status s = forward(c, batch, hist, dt, out);
+        cudaError_t e = cudaStreamEndCapture(c->st, &g);
+        c->glaunch = c->launches - l0;
+        c->launches = l0;
+        if (s != PF_OK) {
+            if (g) cudaGraphDestroy(g);
+            return s;
+        }
+        if (e != cudaSuccess) return fail(c, PF_ERR_CUDA, fmt("forward capture: %s", cudaGetErrorString(e)));
+        e = cudaGraphInstantiate(&c->gexec, g, 0);
+        cudaGraphDestroy(g);
+        if (e != cudaSuccess) return fail(c, PF_ERR_CUDA, fmt("forward graph: %s", cudaGetErrorString(e)));
+        c->gB = batch;
+        c->gh = hist;
+        c->gd = dt;
+        c->go = out;
+    }
+    UCK(c, cudaGraphLaunch(c->gexec, c->st));
+    c->launches += c->glaunch;
+    return PF_OK;
 }
 
 pf_status un_forward(un_ctx *c, int32_t batch, const float *hist, const float *dt, float *out) {
@@ -1425,6 +1459,7 @@ const char *un_last_error(const un_ctx *c) { return c ? c->err.c_str() : g_err.c
 void un_free(un_ctx *c) {
     if (!c) return;
     if (c->st) cudaStreamSynchronize(c->st);
+    if (c->gexec) cudaGraphExecDestroy(c->gexec);
     for (int l = 0; l < kLayers; ++l) {
         cudaFree(c->w[l]);
         cudaFree(c->gam[l]);
