@@ -1304,7 +1304,19 @@ pf_status un_forward(un_ctx *c, int32_t batch, const float *hist, const float *d
     return PF_OK;
 }
 
+namespace {
+// Rollout writing prediction (leap, q) of member b to out[(b * ostride + ooff + leap * lf + q) * hw].
+pf_status rollout_impl(un_ctx *c, int32_t batch, const float *hist, int32_t lf, int32_t n_leaps, float *out,
+                       int64_t ostride, int64_t ooff);
+}  // namespace
+
 pf_status un_rollout(un_ctx *c, int32_t batch, const float *hist, int32_t lf, int32_t n_leaps, float *out) {
+    return rollout_impl(c, batch, hist, lf, n_leaps, out, (int64_t)n_leaps * lf, 0);
+}
+
+namespace {
+pf_status rollout_impl(un_ctx *c, int32_t batch, const float *hist, int32_t lf, int32_t n_leaps, float *out,
+                       int64_t ostride, int64_t ooff) {
     if (!c || !hist || !out) return fail(c, PF_ERR_ARG, "NULL argument");
     if (batch < 1 || batch > c->p.max_batch) return fail(c, PF_ERR_ARG, "batch out of range");
     if (lf < c->p.lb || n_leaps < 1) return fail(c, PF_ERR_ARG, "need lf >= lb and n_leaps >= 1");
@@ -1331,7 +1343,7 @@ pf_status un_rollout(un_ctx *c, int32_t batch, const float *hist, int32_t lf, in
             s = forward(c, batch, win, dts + (size_t)q * batch, pred + (size_t)q * batch * hw);
         // outputs [b][leap*lf + q]; next window = predictions lf-lb .. lf-1, channel order oldest first
         for (int q = 0; q < lf && s == PF_OK; ++q)
-            if (cudaMemcpy2DAsync(out + ((size_t)leap * lf + q) * hw, (size_t)n_leaps * lf * hw * sizeof(float),
+            if (cudaMemcpy2DAsync(out + ((size_t)ooff + (size_t)leap * lf + q) * hw, (size_t)ostride * hw * sizeof(float),
                                   pred + (size_t)q * batch * hw, hw * sizeof(float), hw * sizeof(float), batch,
                                   cudaMemcpyDeviceToHost, c->st) != cudaSuccess)
                 s = fail(c, PF_ERR_CUDA, "rollout download failed");
@@ -1347,6 +1359,7 @@ pf_status un_rollout(un_ctx *c, int32_t batch, const float *hist, int32_t lf, in
     cudaFree(dts);
     return s;
 }
+}  // namespace
 
 pf_status un_hybrid(un_ctx *c, pf_ctx *dns, int32_t n_dns, int64_t steps_between, int32_t lf, int32_t n_leaps,
                     float *out, double seconds[2]) {
@@ -1375,16 +1388,12 @@ pf_status un_hybrid(un_ctx *c, pf_ctx *dns, int32_t n_dns, int64_t steps_between
             if (q >= n_dns - lb) std::memcpy(hist.data() + ((size_t)b * lb + (q - (n_dns - lb))) * hw, dst, hw * 4);
         }
     double sur = 0.0;
-    if (n_leaps > 0) {
-        std::vector<float> pred((size_t)members * n_leaps * lf * hw);
+    if (n_leaps > 0) {   // predictions land directly in out[:, n_dns:]
         auto t2 = std::chrono::steady_clock::now();
-        s = un_rollout(c, members, hist.data(), lf, n_leaps, pred.data());
+        s = rollout_impl(c, members, hist.data(), lf, n_leaps, out, total, n_dns);
         auto t3 = std::chrono::steady_clock::now();
         if (s != PF_OK) return s;
         sur = std::chrono::duration<double>(t3 - t2).count();
-        for (int b = 0; b < members; ++b)
-            std::memcpy(out + ((size_t)b * total + n_dns) * hw, pred.data() + (size_t)b * n_leaps * lf * hw,
-                        (size_t)n_leaps * lf * hw * 4);
     }
     if (seconds) {
         seconds[0] = std::chrono::duration<double>(t1 - t0).count();

@@ -43,7 +43,7 @@ def main():
         for n_dns in (3, 10):            # the two configurations of P:240-241
             with pf.Simulation(p) as s:
                 s.step(10)
-                net.hybrid(s, 3, 1, 3, 1)                     # warm-up of both paths
+                net.hybrid(s, 3, 1, S - n_dns, 1)             # warm-up of both paths (same shapes)
                 _, (td, tu) = net.hybrid(s, n_dns, K, S - n_dns, 1)
             res[f"hybrid_dns{n_dns}"] = {"dns_s": td, "surrogate_s": tu, "speedup": res["dns_only_s"] / (td + tu)}
     print(json.dumps(res), flush=True)
