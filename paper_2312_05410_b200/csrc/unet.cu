@@ -5,17 +5,21 @@
 // NHWC; GroupNorm statistics fp64.  Concatenation z (+) d is a channel-offset write into a buffer of
 // 2C channels, so no copy is needed.
 //
-// conv3x3_kernel: implicit GEMM on the 5th-generation tensor cores.
+// Convolutions: implicit GEMMs on the 5th-generation tensor cores.
 //   D[pixel, cout] = sum_K A[pixel, K] B[cout, K],  K = (ky * 3 + kx) * cin + ci   (R-29)
-//   One CTA = 128 pixels (UMMA M = 128) x all cout (UMMA N = cout <= 128), fp32 accumulator in TMEM
-//   (cout columns).  K streams through a 2-stage shared-memory ring in blocks of 64: every thread
-//   gathers its pixel's 16-byte channel chunks with cp.async (zero-fill outside the grid = the 'same'
-//   zero padding), the weights likewise; after a proxy fence and a CTA barrier one thread issues
-//   tcgen05.mma (kind::f16, bf16 x bf16 -> fp32, K = 16 per instruction) and tcgen05.commit arrives
-//   on the stage's mbarrier, which gates the reuse of that stage two blocks later.  Operands use the
-//   canonical no-swizzle K-major layout: 8-row x 16-byte core matrices, rows 16 B apart, 8-row groups
-//   128 B apart (SBO), K-chunks of 8 elements LBO apart.  Epilogue: each warp reads its 32 TMEM lanes
-//   (tcgen05.ld 32x32b), one pixel per thread, and stores the fp32 row.
+//   A tile = 128 pixels (UMMA M = 128), N = cout (16..128), fp32 accumulators in TMEM, tcgen05.mma
+//   kind::f16 (bf16 x bf16 -> fp32, K = 16 per instruction) issued by one thread, tcgen05.commit to
+//   mbarriers.  Operands use the canonical no-swizzle K-major layout: 8-row x 16-byte core matrices,
+//   rows 16 B apart, 8-row groups 128 B apart (SBO), 8-element K chunks LBO apart.  Both kernels are
+//   warp specialised (loader warps, one MMA warp, four epilogue warps; mbarrier pipelines, no CTA
+//   barrier in the loop) and persistent:
+//   * conv3x3_rows_kernel (W a multiple of 128): a tile is 128 pixels of one image row; the three
+//     halo rows are loaded once (5D TMA boxes, or cp.async) and the A operand of each tap is a
+//     descriptor shifted by kx pixels into row plane ky; weights resident in shared memory;
+//   * conv3x3_kernel (any shape): im2col gather of 144-element K blocks with cp.async (zero-fill =
+//     the 'same' padding), weights streamed with each block.
+//   Epilogue (conv_tile_out): tcgen05.ld 32x32b (one pixel per thread), fp32 NHWC stores and the
+//   GroupNorm partial sums (sum, sum of squares) per 32-pixel unit, reduced in a fixed order.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
@@ -38,8 +42,6 @@ namespace {
 typedef __nv_bfloat16 bf16;
 
 constexpr int kBM = 128;      // pixels per CTA (UMMA M)
-constexpr int kBK = 64;       // K elements per ring stage (8 chunks of 8 bf16)
-constexpr int kStages = 2;
 constexpr int kBasis = 128;   // time-basis width
 constexpr int kGroups = 4;    // GroupNorm groups (R-30)
 constexpr double kEps = 1e-5; // GroupNorm epsilon (R-30)
