@@ -42,7 +42,7 @@ namespace {
 // ========================================================================================
 // Tile kernel (fallback)
 constexpr int BX = 32;   // tile width  (one warp across x)
-constexpr int BY = 16;   // tile height
+constexpr int BY = 16;   // tile height (tile kernel; the persistent kernel picks 4 or 16)
 constexpr int NT = 256;  // threads per block (32 x 8)
 
 // Local row holding the c/phi value of local row ly after the global mirror rule (R-12),
@@ -62,22 +62,22 @@ __device__ __forceinline__ int wrap_x(int gx, int nx) {
     return gx % nx;
 }
 
-template <typename real>
+template <typename real, int TBY = BY>
 struct TileSmem {
-    real sc[BY + 4][BX + 4];
-    real sp[BY + 4][BX + 4];
-    real sr[BY + 2][BX + 2];
-    real smc[BY + 2][BX + 2];
-    real smp[BY + 2][BX + 2];
-    real sM[BY + 2][BX + 2];
+    real sc[TBY + 4][BX + 4];
+    real sp[TBY + 4][BX + 4];
+    real sr[TBY + 2][BX + 2];
+    real smc[TBY + 2][BX + 2];
+    real smp[TBY + 2][BX + 2];
+    real sM[TBY + 2][BX + 2];
 };
 
 // One stage on the tile (member m, columns [tx0, tx0 + 32), rows [ty0, ty0 + 16)): ghost rules
 // applied by index, so the tile reads owned cells only (the ghost frame may be stale).
-template <typename real, int MOB, int FE>
+template <typename real, int MOB, int FE, int TBY = BY>
 __device__ __forceinline__ void tile_stage(const Layout &L, const KC<real> &k, const real *__restrict__ in,
                                            const real *__restrict__ base, real *out, const real *__restrict__ vel,
-                                           const double *etab, TileSmem<real> &ts, int m, int tx0, int ty0) {
+                                           const double *etab, TileSmem<real, TBY> &ts, int m, int tx0, int ty0) {
     auto &sc = ts.sc;
     auto &sp = ts.sp;
     auto &sr = ts.sr;
@@ -90,14 +90,14 @@ __device__ __forceinline__ void tile_stage(const Layout &L, const KC<real> &k, c
     const real *ir = ip + L.fstride;
 
     // ---- load c, phi with a 2-cell halo (ghost rules applied by index) ----
-    for (int t = threadIdx.x; t < (BY + 4) * (BX + 4); t += NT) {
+    for (int t = threadIdx.x; t < (TBY + 4) * (BX + 4); t += NT) {
         const int sy = t / (BX + 4), sx = t - sy * (BX + 4);
         const int64_t off = L.at(row_cphi(ty0 - 2 + sy, L), wrap_x(tx0 - 2 + sx, nx));
         sc[sy][sx] = ic[off];
         sp[sy][sx] = ip[off];
     }
     // ---- load rho with a 1-cell halo: bottom mirror, top reservoir (R-12) ----
-    for (int t = threadIdx.x; t < (BY + 2) * (BX + 2); t += NT) {
+    for (int t = threadIdx.x; t < (TBY + 2) * (BX + 2); t += NT) {
         const int sy = t / (BX + 2), sx = t - sy * (BX + 2);
         const int gx = wrap_x(tx0 - 1 + sx, nx);
         int g = L.y0 + ty0 - 1 + sy;
@@ -117,7 +117,7 @@ __device__ __forceinline__ void tile_stage(const Layout &L, const KC<real> &k, c
 
     // ---- phase 1: mu_c, mu_phi, M on the tile + 1 ring ----
     const Mob<real> mo = MOB == 2 ? load_mob(vel, m) : Mob<real>{};
-    for (int t = threadIdx.x; t < (BY + 2) * (BX + 2); t += NT) {
+    for (int t = threadIdx.x; t < (TBY + 2) * (BX + 2); t += NT) {
         const int sy = t / (BX + 2), sx = t - sy * (BX + 2);
         const int ey = sy + 1, ex = sx + 1;
         real mc, mp, M;
@@ -135,7 +135,7 @@ __device__ __forceinline__ void tile_stage(const Layout &L, const KC<real> &k, c
     scaled_velocity(k, vel, m, vx, vy);
     const int lx = threadIdx.x & (BX - 1);
     const int gx = tx0 + lx;
-    for (int q = threadIdx.x / BX; q < BY; q += NT / BX) {
+    for (int q = threadIdx.x / BX; q < TBY; q += NT / BX) {
         const int ly = ty0 + q;
         if (gx >= nx || ly >= L.r1) continue;
         const int y = q + 1, x = lx + 1;                    // ring coordinates
@@ -174,14 +174,16 @@ __global__ void __launch_bounds__(NT) stage_kernel(Layout L, KC<real> k, const r
 // a grid-wide barrier after each stage -- for grids too small to fill the GPU, where the two
 // launches per step (not HBM) are the cost.  Same per-cell arithmetic and tiles as stage_kernel:
 // bitwise identical results.  Writes owned cells only; the host rebuilds the ghost frame after.
-template <typename real, int MOB, int FE>
+// TBY: tile height -- 4 for the smallest grids (more, shorter tiles: lower latency per stage),
+// 16 otherwise (tools/small_grid_sweep.py).
+template <typename real, int MOB, int FE, int TBY>
 __global__ void __launch_bounds__(NT) persistent_kernel(Layout L, KC<real> k1, KC<real> k2, real *U, real *Us,
                                                         const real *__restrict__ vel, int64_t nsteps) {
-    __shared__ TileSmem<real> ts;
+    __shared__ TileSmem<real, TBY> ts;
     __shared__ double etab[64];
     load_exp_table(etab);
     cg::grid_group grid = cg::this_grid();
-    const int tx = (L.nx + BX - 1) / BX, ty = (L.ny_loc + BY - 1) / BY;
+    const int tx = (L.nx + BX - 1) / BX, ty = (L.ny_loc + TBY - 1) / TBY;
     const int ntiles = tx * ty * L.members;
     for (int64_t s = 0; s < nsteps; ++s) {
         for (int stage = 1; stage <= 2; ++stage) {
@@ -191,7 +193,7 @@ __global__ void __launch_bounds__(NT) persistent_kernel(Layout L, KC<real> k1, K
             for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
                 const int m = t / (tx * ty), r = t - m * (tx * ty);
                 const int by = r / tx, bxi = r - by * tx;
-                tile_stage<real, MOB, FE>(L, kk, in, U, out, vel, etab, ts, L.m0 + m, bxi * BX, by * BY);
+                tile_stage<real, MOB, FE, TBY>(L, kk, in, U, out, vel, etab, ts, L.m0 + m, bxi * BX, by * TBY);
             }
             grid.sync();
         }
@@ -1856,11 +1858,11 @@ cudaError_t launch_fused(int precision, const Layout &L, const StreamPlan &P, co
                                  (const float *)vel, s);
 }
 
-template <typename real, int MOB, int FE>
-cudaError_t launch_persistent_t(const Layout &L, const KC<real> &k1, const KC<real> &k2, real *U, real *Us,
+template <typename real, int MOB, int FE, int TBY>
+cudaError_t launch_persistent_b(const Layout &L, const KC<real> &k1, const KC<real> &k2, real *U, real *Us,
                                 const real *vel, int64_t nsteps, cudaStream_t s) {
     static int occ = -1, nsm = 0;
-    auto kern = persistent_kernel<real, MOB, FE>;
+    auto kern = persistent_kernel<real, MOB, FE, TBY>;
     if (occ < 0) {
         int dev = 0;
         cudaGetDevice(&dev);
@@ -1869,13 +1871,22 @@ cudaError_t launch_persistent_t(const Layout &L, const KC<real> &k1, const KC<re
         if (e != cudaSuccess) return e;
         if (occ < 1) occ = 1;
     }
-    const int64_t ntiles = (int64_t)((L.nx + BX - 1) / BX) * ((L.ny_loc + BY - 1) / BY) * L.members;
+    const int64_t ntiles = (int64_t)((L.nx + BX - 1) / BX) * ((L.ny_loc + TBY - 1) / TBY) * L.members;
     const int64_t maxb = (int64_t)occ * nsm;
     const int blocks = (int)(ntiles < maxb ? ntiles : maxb);
     Layout Lc = L;
     KC<real> a1 = k1, a2 = k2;
     void *args[] = {&Lc, &a1, &a2, &U, &Us, (void *)&vel, &nsteps};
     return cudaLaunchCooperativeKernel((const void *)kern, blocks, NT, args, 0, s);
+}
+
+template <typename real, int MOB, int FE>
+cudaError_t launch_persistent_t(const Layout &L, const KC<real> &k1, const KC<real> &k2, real *U, real *Us,
+                                const real *vel, int64_t nsteps, cudaStream_t s) {
+    // 32 x 4 tiles up to 2^17 cells (cfg1 +50%, cfg2 +27%), 32 x 16 above (better from 2^18)
+    if ((int64_t)L.nx * L.ny_loc * L.members <= (int64_t)1 << 17)
+        return launch_persistent_b<real, MOB, FE, 4>(L, k1, k2, U, Us, vel, nsteps, s);
+    return launch_persistent_b<real, MOB, FE, 16>(L, k1, k2, U, Us, vel, nsteps, s);
 }
 
 cudaError_t launch_persistent(int precision, const Layout &L, const Coef &K, void *U, void *Us, const void *vel,
