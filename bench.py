@@ -265,7 +265,7 @@ def run_ours(args):
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     oc, op_, orr = (torch.empty_like(hc).pin_memory() for _ in range(3))
-    chunks = min(3, p.n_members)   # tools/e2e_chunks.py: 3 tapered chunks (8/48/8 members) best on configs[2]
+    chunks = min(2, p.n_members)   # tools/e2e_chunks.py: 2 even chunks (34.3 G) ~ 3 tapered (34.5 G), steadier
     e0.record(stream)
     pf.pf_run_host(ctx, e2e_steps, hc, hp, hr, oc, op_, orr, chunks)
     e1.record(stream)
