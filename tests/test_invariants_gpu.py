@@ -269,7 +269,8 @@ def test_warp_specialised_step_kernel_bitwise(nx, ny, members, extra):
 
 @pytest.mark.parametrize("nx,ny,members,extra", [(64, 64, 1, {}), (96, 48, 3, {}), (33, 65, 2, {}),
                                                   (128, 40, 2, dict(mob_lo=0.5, mob_hi=1.0)),
-                                                  (80, 32, 1, dict(fe_model=1, omega=2.2, temp_rs=0.45, dt=4e-4))])
+                                                  (80, 32, 1, dict(fe_model=1, omega=2.2, temp_rs=0.45, dt=4e-4)),
+                                                  (384, 384, 1, {})])   # > 2^17 cells: 32 x 16 tiles
 def test_persistent_small_grid_kernel_bitwise(nx, ny, members, extra):
     """The persistent small-grid kernel (kernel_path 7: all steps of a check interval in one
     cooperative launch) gives the same bits as the stage kernels, across several check intervals,
