@@ -29,6 +29,9 @@ namespace cg = cooperative_groups;
 #define PF_PAIR_UNROLL 1   // unroll of the pair kernel's slot loop (experiment knob)
 #endif
 constexpr int kPairUnroll = PF_PAIR_UNROLL;
+#ifndef PF_TBY_LARGE
+#define PF_TBY_LARGE 16    // persistent-kernel tile height above 2^17 cells (experiment knob)
+#endif
 
 namespace pf {
 
@@ -1886,7 +1889,7 @@ cudaError_t launch_persistent_t(const Layout &L, const KC<real> &k1, const KC<re
     // 32 x 4 tiles up to 2^17 cells (cfg1 +50%, cfg2 +27%), 32 x 16 above (better from 2^18)
     if ((int64_t)L.nx * L.ny_loc * L.members <= (int64_t)1 << 17)
         return launch_persistent_b<real, MOB, FE, 4>(L, k1, k2, U, Us, vel, nsteps, s);
-    return launch_persistent_b<real, MOB, FE, 16>(L, k1, k2, U, Us, vel, nsteps, s);
+    return launch_persistent_b<real, MOB, FE, PF_TBY_LARGE>(L, k1, k2, U, Us, vel, nsteps, s);
 }
 
 cudaError_t launch_persistent(int precision, const Layout &L, const Coef &K, void *U, void *Us, const void *vel,
