@@ -831,6 +831,56 @@ __global__ void __launch_bounds__(256) gn_apply_kernel(const float *__restrict__
     }
 }
 
+// Encoder levels: GN + GELU, the conditioned copy into the concatenation buffer
+// and the 2x2 max pooling of the unconditioned z in one pass over each
+// 2x2 quad; z itself is never stored.  Rounding to bf16 is monotonic, so max(bf16(y)) =
+// bf16(max(y)): the same bits as storing z and pooling it.
+__global__ void __launch_bounds__(256) gn_apply_pool_kernel(const float *__restrict__ x, int B, int H, int W, int C,
+                                                            const float2 *__restrict__ ab,
+                                                            const float *__restrict__ cond, int ctot, int coff,
+                                                            bf16 *dB, int sB, int oB, bf16 *__restrict__ pool) {
+    const int nq = C >> 3, h = H / 2, w = W / 2;
+    const int64_t total = (int64_t)B * h * w * nq;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t po = i / nq;
+        const int q = (int)(i - po * nq), c0 = q * 8;
+        const int b = (int)(po / ((int64_t)h * w)), rem = (int)(po - (int64_t)b * h * w), yo = rem / w, xo = rem - yo * w;
+        const float4 *a4 = reinterpret_cast<const float4 *>(ab + (int64_t)b * C + c0);
+        float2 af[8];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const float4 t = a4[j];
+            af[2 * j] = make_float2(t.x, t.y);
+            af[2 * j + 1] = make_float2(t.z, t.w);
+        }
+        const float4 *c4 = reinterpret_cast<const float4 *>(cond + (int64_t)b * ctot + coff + c0);
+        const float4 t0 = c4[0], t1 = c4[1];
+        const float cv[8] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w};
+        float mx[8];
+#pragma unroll
+        for (int dy = 0; dy < 2; ++dy)
+#pragma unroll
+            for (int dx = 0; dx < 2; ++dx) {
+                const int64_t p = ((int64_t)b * H + 2 * yo + dy) * W + 2 * xo + dx;
+                const float4 *src = reinterpret_cast<const float4 *>(x + p * C + c0);
+                const float4 v0 = src[0], v1 = src[1];
+                const float xv[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+                __align__(16) bf16 yb[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const float y = gelu_fast(fmaf(xv[j], af[j].x, af[j].y));
+                    yb[j] = __float2bfloat16_rn(y * cv[j]);
+                    mx[j] = (dy | dx) ? fmaxf(mx[j], y) : y;
+                }
+                *reinterpret_cast<uint4 *>(dB + p * sB + oB + c0) = *reinterpret_cast<uint4 *>(yb);
+            }
+        __align__(16) bf16 m[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) m[j] = __float2bfloat16_rn(mx[j]);
+        *reinterpret_cast<uint4 *>(pool + po * C + c0) = *reinterpret_cast<uint4 *>(m);
+    }
+}
+
 // output head: GN over the single output channel (G = 1, no activation) -> fp32 [B][HW]
 __global__ void head_out_kernel(const float *__restrict__ x, int cstride, int64_t npix, int HW,
                                 const double *__restrict__ stats, const float *__restrict__ gamma,
@@ -838,27 +888,6 @@ __global__ void head_out_kernel(const float *__restrict__ x, int cstride, int64_
     for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < npix; p += (int64_t)gridDim.x * blockDim.x) {
         const int b = (int)(p / HW);
         out[p] = (float)(((double)x[p * cstride] - stats[2 * b]) * stats[2 * b + 1]) * gamma[0] + beta[0];
-    }
-}
-
-// 2x2 max pooling, stride 2: [B][H][W][C] -> [B][H/2][W/2][C], 8 channels per thread
-__global__ void maxpool_kernel(const bf16 *__restrict__ src, bf16 *__restrict__ dst, int B, int H, int W, int C) {
-    const int h = H / 2, w = W / 2, nq = C >> 3;
-    const int64_t total = (int64_t)B * h * w * nq;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t po = i / nq;
-        const int q = (int)(i - po * nq);
-        const int b = (int)(po / ((int64_t)h * w)), rem = (int)(po - (int64_t)b * h * w), yo = rem / w, xo = rem - yo * w;
-        __align__(16) bf16 m[8];
-        for (int dy = 0; dy < 2; ++dy)
-            for (int dx = 0; dx < 2; ++dx) {
-                const int64_t pi = ((int64_t)b * H + 2 * yo + dy) * W + 2 * xo + dx;
-                __align__(16) bf16 v[8];
-                *reinterpret_cast<uint4 *>(v) = *reinterpret_cast<const uint4 *>(src + pi * C + q * 8);
-#pragma unroll
-                for (int j = 0; j < 8; ++j) m[j] = (dy | dx) ? __hmax(m[j], v[j]) : v[j];
-            }
-        *reinterpret_cast<uint4 *>(dst + po * C + q * 8) = *reinterpret_cast<uint4 *>(m);
     }
 }
 
@@ -921,7 +950,7 @@ struct un_ctx {
     int ctot = 0, coff[4] = {0, 0, 0, 0};
     bool have_w = false;
     // activations
-    bf16 *in0 = nullptr, *z[3] = {}, *pin[3] = {}, *cat[3] = {}, *z4c = nullptr, *dec[4] = {};
+    bf16 *in0 = nullptr, *pin[3] = {}, *cat[3] = {}, *z4c = nullptr, *dec[4] = {};
     float *raw = nullptr, *cond = nullptr, *dout = nullptr, *dhist = nullptr, *ddt = nullptr;
     double *stats = nullptr, *part = nullptr;   // GN statistics, per-warp partial sums
     float2 *ab = nullptr;                       // per (sample, channel) GN affine: y = u a + c
@@ -1004,9 +1033,10 @@ pf_status apply_layer(un_ctx *c, int l, int B, int cond_level, bf16 *dA, int sA,
     return PF_OK;
 }
 
-pf_status pool_layer(un_ctx *c, const bf16 *src, bf16 *dst, int B, int lv, int C) {
-    const int H = c->p.height >> lv, W = c->p.width >> lv;
-    maxpool_kernel<<<grid_for((int64_t)B * (H / 2) * (W / 2) * (C / 8), 256), 256, 0, c->st>>>(src, dst, B, H, W, C);
+pf_status apply_pool_layer(un_ctx *c, int l, int B, int cond_level, bf16 *dB, int sB, int oB, bf16 *pool) {
+    const int lv = level_of(l), H = c->p.height >> lv, W = c->p.width >> lv, C = c->cout[l];
+    gn_apply_pool_kernel<<<grid_for((int64_t)B * (H / 2) * (W / 2) * (C / 8), 256), 256, 0, c->st>>>(
+        c->raw, B, H, W, C, c->ab, c->cond, c->ctot, c->coff[cond_level], dB, sB, oB, pool);
     c->launches += 1;
     return PF_OK;
 }
@@ -1036,15 +1066,12 @@ pf_status forward(un_ctx *c, int B, const float *hist, const float *dt, float *o
     pf_status s;
     // encoder + conditioning: z_p unconditioned (pooling input), z_p (.) s_p
     // into the first half of the level's concatenation buffer
-    if ((s = conv_layer(c, kEnc1, c->in0, B)) || (s = apply_layer(c, kEnc1, B, 0, c->z[0], C1, 0, c->cat[0], 2 * C1, 0)))
+    if ((s = conv_layer(c, kEnc1, c->in0, B)) || (s = apply_pool_layer(c, kEnc1, B, 0, c->cat[0], 2 * C1, 0, c->pin[0])))
         return s;
-    if ((s = pool_layer(c, c->z[0], c->pin[0], B, 0, C1))) return s;
-    if ((s = conv_layer(c, kEnc2, c->pin[0], B)) || (s = apply_layer(c, kEnc2, B, 1, c->z[1], C2, 0, c->cat[1], 2 * C2, 0)))
+    if ((s = conv_layer(c, kEnc2, c->pin[0], B)) || (s = apply_pool_layer(c, kEnc2, B, 1, c->cat[1], 2 * C2, 0, c->pin[1])))
         return s;
-    if ((s = pool_layer(c, c->z[1], c->pin[1], B, 1, C2))) return s;
-    if ((s = conv_layer(c, kEnc3, c->pin[1], B)) || (s = apply_layer(c, kEnc3, B, 2, c->z[2], C3, 0, c->cat[2], 2 * C3, 0)))
+    if ((s = conv_layer(c, kEnc3, c->pin[1], B)) || (s = apply_pool_layer(c, kEnc3, B, 2, c->cat[2], 2 * C3, 0, c->pin[2])))
         return s;
-    if ((s = pool_layer(c, c->z[2], c->pin[2], B, 2, C3))) return s;
     if ((s = conv_layer(c, kEnc4, c->pin[2], B)) || (s = apply_layer(c, kEnc4, B, 3, nullptr, 0, 0, c->z4c, C4, 0)))
         return s;
     // decoder: d^{L3} = up(conv_block(z4)), d^{Lp} = up(conv_block(z^{Lp+1} (+) d^{Lp+1}))
@@ -1171,8 +1198,7 @@ pf_status un_create(const un_params *p, un_ctx **out) {
     if (s == PF_OK) s = dalloc(c, &c->in0, (size_t)(B * hw(0) * 16));
     const int Cl[4] = {c1, c2, c3, c4};
     for (int q = 0; q < 3 && s == PF_OK; ++q) {
-        s = dalloc(c, &c->z[q], (size_t)(B * hw(q) * Cl[q]));
-        if (s == PF_OK) s = dalloc(c, &c->pin[q], (size_t)(B * hw(q + 1) * Cl[q]));
+        s = dalloc(c, &c->pin[q], (size_t)(B * hw(q + 1) * Cl[q]));
         if (s == PF_OK) s = dalloc(c, &c->cat[q], (size_t)(B * hw(q) * 2 * Cl[q]));
     }
     if (s == PF_OK) s = dalloc(c, &c->z4c, (size_t)(B * hw(3) * c4));
@@ -1481,7 +1507,6 @@ void un_free(un_ctx *c) {
     cudaFree(c->upw);
     cudaFree(c->in0);
     for (int q = 0; q < 3; ++q) {
-        cudaFree(c->z[q]);
         cudaFree(c->pin[q]);
         cudaFree(c->cat[q]);
     }
