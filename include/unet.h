@@ -61,7 +61,7 @@ pf_status un_set_weights(un_ctx *ctx, const float *blob, int64_t n);
 
 /* Forward pass, device pointers, asynchronous on the ctx stream (un_stream):
  *   hist [batch][lb][H][W] fp32 (values are rounded to bf16 on entry), dt [batch] fp32,
- *   out [batch][H][W] fp32.  1 <= batch <= max_batch.  The 35 launches are captured into a CUDA
+ *   out [batch][H][W] fp32.  1 <= batch <= max_batch.  The 29 launches are captured into a CUDA
  *   graph on the first call with a given (batch, hist, dt, out) and replayed by later calls with
  *   the same arguments (buffer contents and weights may change in between). */
 pf_status un_forward_device(un_ctx *ctx, int32_t batch, const float *hist, const float *dt, float *out);

@@ -891,27 +891,39 @@ __global__ void head_out_kernel(const float *__restrict__ x, int cstride, int64_
     }
 }
 
-// up(u)_{k, 2i+m, 2j+n} = u_{k,i,j} w_{m,n} (R-31): [B][h][w][C] -> dst [B][2h][2w] (stride sD, offset oD)
-__global__ void up_kernel(const bf16 *__restrict__ src, int B, int h, int w, int C, const float *__restrict__ wt,
-                          bf16 *__restrict__ dst, int sD, int oD) {
+// Decoder levels: GN + GELU of conv_block and the up-sampling of its output (R-31) in
+// one pass: up(d)_{k, 2i+m, 2j+n} = bf16(d_{k,i,j}) w_{m,n}, written straight into the channel
+// half [oD, oD + C) of the next level's concatenation buffer (the same bits as storing d in bf16
+// and up-sampling it).
+__global__ void __launch_bounds__(256) gn_apply_up_kernel(const float *__restrict__ x, int B, int h, int w, int C,
+                                                          const float2 *__restrict__ ab, const float *__restrict__ wt,
+                                                          bf16 *__restrict__ dst, int sD, int oD) {
     const int nq = C >> 3;
     const int64_t total = (int64_t)B * h * w * nq;
-    const float w00 = wt[0], w01 = wt[1], w10 = wt[2], w11 = wt[3];
+    const float ws[4] = {wt[0], wt[1], wt[2], wt[3]};
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t pi = i / nq;
-        const int q = (int)(i - pi * nq);
+        const int q = (int)(i - pi * nq), c0 = q * 8;
         const int b = (int)(pi / ((int64_t)h * w)), rem = (int)(pi - (int64_t)b * h * w), yi = rem / w, xi = rem - yi * w;
-        __align__(16) bf16 v[8];
-        *reinterpret_cast<uint4 *>(v) = *reinterpret_cast<const uint4 *>(src + pi * C + q * 8);
-        const float ws[4] = {w00, w01, w10, w11};
+        const float4 *src = reinterpret_cast<const float4 *>(x + pi * C + c0);
+        const float4 v0 = src[0], v1 = src[1];
+        const float xv[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+        const float4 *a4 = reinterpret_cast<const float4 *>(ab + (int64_t)b * C + c0);
+        float yv[8];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const float4 t = a4[j];
+            yv[2 * j] = __bfloat162float(__float2bfloat16_rn(gelu_fast(fmaf(xv[2 * j], t.x, t.y))));
+            yv[2 * j + 1] = __bfloat162float(__float2bfloat16_rn(gelu_fast(fmaf(xv[2 * j + 1], t.z, t.w))));
+        }
 #pragma unroll
         for (int mn = 0; mn < 4; ++mn) {
             const int m = mn >> 1, n = mn & 1;
             const int64_t po = ((int64_t)b * 2 * h + 2 * yi + m) * (2 * w) + 2 * xi + n;
             __align__(16) bf16 o[8];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) o[j] = __float2bfloat16_rn(__bfloat162float(v[j]) * ws[mn]);
-            *reinterpret_cast<uint4 *>(dst + po * sD + oD + q * 8) = *reinterpret_cast<uint4 *>(o);
+            for (int j = 0; j < 8; ++j) o[j] = __float2bfloat16_rn(yv[j] * ws[mn]);
+            *reinterpret_cast<uint4 *>(dst + po * sD + oD + c0) = *reinterpret_cast<uint4 *>(o);
         }
     }
 }
@@ -1041,10 +1053,10 @@ pf_status apply_pool_layer(un_ctx *c, int l, int B, int cond_level, bf16 *dB, in
     return PF_OK;
 }
 
-pf_status up_layer(un_ctx *c, const bf16 *src, int B, int lv_src, int C, int which, bf16 *dst, int sD, int oD) {
-    const int h = c->p.height >> lv_src, w = c->p.width >> lv_src;
-    up_kernel<<<grid_for((int64_t)B * h * w * (C / 8), 256), 256, 0, c->st>>>(src, B, h, w, C, c->upw + 4 * which, dst,
-                                                                              sD, oD);
+pf_status apply_up_layer(un_ctx *c, int l, int B, int which, bf16 *dst, int sD, int oD) {
+    const int lv = level_of(l), h = c->p.height >> lv, w = c->p.width >> lv, C = c->cout[l];
+    gn_apply_up_kernel<<<grid_for((int64_t)B * h * w * (C / 8), 256), 256, 0, c->st>>>(
+        c->raw, B, h, w, C, c->ab, c->upw + 4 * which, dst, sD, oD);
     c->launches += 1;
     return PF_OK;
 }
@@ -1075,14 +1087,11 @@ pf_status forward(un_ctx *c, int B, const float *hist, const float *dt, float *o
     if ((s = conv_layer(c, kEnc4, c->pin[2], B)) || (s = apply_layer(c, kEnc4, B, 3, nullptr, 0, 0, c->z4c, C4, 0)))
         return s;
     // decoder: d^{L3} = up(conv_block(z4)), d^{Lp} = up(conv_block(z^{Lp+1} (+) d^{Lp+1}))
-    if ((s = conv_layer(c, kDec4, c->z4c, B)) || (s = apply_layer(c, kDec4, B, -1, c->dec[0], C3, 0, nullptr, 0, 0)) ||
-        (s = up_layer(c, c->dec[0], B, 3, C3, 0, c->cat[2], 2 * C3, C3)))
+    if ((s = conv_layer(c, kDec4, c->z4c, B)) || (s = apply_up_layer(c, kDec4, B, 0, c->cat[2], 2 * C3, C3)))
         return s;
-    if ((s = conv_layer(c, kDec3, c->cat[2], B)) || (s = apply_layer(c, kDec3, B, -1, c->dec[1], C2, 0, nullptr, 0, 0)) ||
-        (s = up_layer(c, c->dec[1], B, 2, C2, 1, c->cat[1], 2 * C2, C2)))
+    if ((s = conv_layer(c, kDec3, c->cat[2], B)) || (s = apply_up_layer(c, kDec3, B, 1, c->cat[1], 2 * C2, C2)))
         return s;
-    if ((s = conv_layer(c, kDec2, c->cat[1], B)) || (s = apply_layer(c, kDec2, B, -1, c->dec[2], C1, 0, nullptr, 0, 0)) ||
-        (s = up_layer(c, c->dec[2], B, 1, C1, 2, c->cat[0], 2 * C1, C1)))
+    if ((s = conv_layer(c, kDec2, c->cat[1], B)) || (s = apply_up_layer(c, kDec2, B, 2, c->cat[0], 2 * C1, C1)))
         return s;
     // output: GN(conv(conv_block(z^{L1} (+) d^{L1})))
     if ((s = conv_layer(c, kHead1, c->cat[0], B)) || (s = apply_layer(c, kHead1, B, -1, c->dec[3], C1, 0, nullptr, 0, 0)))
@@ -1202,9 +1211,6 @@ pf_status un_create(const un_params *p, un_ctx **out) {
         if (s == PF_OK) s = dalloc(c, &c->cat[q], (size_t)(B * hw(q) * 2 * Cl[q]));
     }
     if (s == PF_OK) s = dalloc(c, &c->z4c, (size_t)(B * hw(3) * c4));
-    if (s == PF_OK) s = dalloc(c, &c->dec[0], (size_t)(B * hw(3) * c3));
-    if (s == PF_OK) s = dalloc(c, &c->dec[1], (size_t)(B * hw(2) * c2));
-    if (s == PF_OK) s = dalloc(c, &c->dec[2], (size_t)(B * hw(1) * c1));
     if (s == PF_OK) s = dalloc(c, &c->dec[3], (size_t)(B * hw(0) * c1));
     int64_t rawmax = 0;
     for (int l = 0; l < kLayers; ++l) {
