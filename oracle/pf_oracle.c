@@ -60,10 +60,11 @@ static double nb(const double *u, int nx, int ny, int i, int j, int rule, double
  * toprow != NULL. */
 static double nb_row(const double *u, int nx, int ny, int i, int j, int rule, double top, const double *toprow)
 {
-    i = ((i % nx) + nx) % nx;
+    while (i < 0) i += nx;       /* periodic wrap in x */
+    while (i >= nx) i -= nx;
     if (j < 0) j = -1 - j;
     if (j >= ny) {
-        if (rule == ORC_RESERVOIR) return toprow ? toprow[((i % nx) + nx) % nx] : top;
+        if (rule == ORC_RESERVOIR) return toprow ? toprow[i] : top;
         j = 2 * ny - 1 - j;
     }
     return u[(size_t)j * nx + i];
@@ -221,8 +222,10 @@ void orc_source(const orc_model *m, const double *phi, const double *rho, double
 /* Right-hand sides (R-7..R-9):
  *   R_c   = sum over the 4 faces of the face flux  F = 1/2 (M_a + M_b)(mu_b - mu_a)/dx^2,
  *           zero flux through the two y-boundary faces;
- *   R_phi = M_phi L(mu_phi) + S;
- *   R_rho = D_rho L(rho) - v . G(rho) - S.
+ *   R_phi = M_phi L(mu_phi) + S,  S = grad(phi) . (rho v)  (phi in [0,1]: the paper's
+ *           d(phit)/dt source grad(phit).(rho v) divided by d(phit)/d(phi) = 2, R-1);
+ *   R_rho = D_rho L(rho) - v . G(rho) - grad(phit) . (rho v)   with phit = 2 phi - 1
+ *           (P:340 written in the paper's variable phit in [-1,1]; R-9).
  * Any output pointer may be NULL.                                             */
 static void rhs_row(const orc_model *m, const double *c, const double *phi, const double *rho, const double *toprow,
                     double *Rc, double *Rphi, double *Rrho, double *S_out);
@@ -248,6 +251,9 @@ static void rhs_row(const orc_model *m, const double *c, const double *phi, cons
     double *lrho = (double *)malloc(n * sizeof(double));
     double *grx = (double *)malloc(n * sizeof(double));
     double *gry = (double *)malloc(n * sizeof(double));
+    double *phit = (double *)malloc(n * sizeof(double));
+    double *gpx = (double *)malloc(n * sizeof(double));
+    double *gpy = (double *)malloc(n * sizeof(double));
 
     orc_mu(m, c, phi, mu_c, mu_p);
     orc_mobility_field(m, c, phi, M);
@@ -281,13 +287,17 @@ static void rhs_row(const orc_model *m, const double *c, const double *phi, cons
 
     laplacian_row(nx, ny, m->dx, rho, ORC_RESERVOIR, m->rho_in, toprow, lrho);
     gradient_row(nx, ny, m->dx, rho, ORC_RESERVOIR, m->rho_in, toprow, grx, gry);
+    /* vapour sink of P:340 in the paper's order parameter phit = 2 phi - 1 (R-1, R-9) */
+    for (size_t k = 0; k < n; ++k) phit[k] = 2.0 * phi[k] - 1.0;
+    orc_gradient(nx, ny, m->dx, phit, ORC_MIRROR, 0.0, gpx, gpy);
     if (Rrho)
         for (size_t k = 0; k < n; ++k)
-            Rrho[k] = m->D_rho * lrho[k] - (m->v_x * grx[k] + m->v_y * gry[k]) - S[k];
+            Rrho[k] = m->D_rho * lrho[k] - (m->v_x * grx[k] + m->v_y * gry[k])
+                    - rho[k] * (m->v_x * gpx[k] + m->v_y * gpy[k]);
     if (S_out) memcpy(S_out, S, n * sizeof(double));
 
     free(mu_c); free(mu_p); free(M); free(S); free(Fx); free(Fy);
-    free(lmu); free(lrho); free(grx); free(gry);
+    free(lmu); free(lrho); free(grx); free(gry); free(phit); free(gpx); free(gpy);
 }
 
 /* One explicit midpoint step (R-11):

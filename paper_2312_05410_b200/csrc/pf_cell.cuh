@@ -161,7 +161,8 @@ __device__ __forceinline__ real face_flux(real Ma, real Mb, real mua, real mub) 
 //   R_c   = (fe - fw) + (fn - fs), times 1/(2 dx^2)                (conservative)
 //   S     = rho (v_x G_x phi + v_y G_y phi)                        (R-10)
 //   R_phi = M_phi L(mu_phi) + S                                    (R-7)
-//   R_rho = D_rho L(rho) - v . G(rho) - S                          (R-9)
+//   R_rho = D_rho L(rho) - v . G(rho) - 2 S                        (R-9: the paper's sink
+//           grad(phit) . (rho v) with phit = 2 phi - 1 (R-1) is 2 S; S + S is exact)
 //   out   = base + coef R                                          (R-11)
 // vx, vy are the member's velocity divided by 2 dx (folded once per segment, see scaled_velocity).
 template <typename real>
@@ -179,7 +180,7 @@ __device__ __forceinline__ void cell_update(const KC<real> &k, real vx, real vy,
     const real Rp = fma_(lq, k.Mp_dx2, S);
     const real lr = fma_(r0, m4, add_(add_(rl, rr), add_(rd, ru)));          // dx^2 L(rho)
     const real adv = fma_(vx, sub_(rr, rl), mul_(vy, sub_(ru, rd)));
-    const real Rr = sub_(fma_(lr, k.Dr_dx2, -adv), S);
+    const real Rr = sub_(fma_(lr, k.Dr_dx2, -adv), add_(S, S));
     oc = fma_(Rc2, k.coefc, bc);
     op = fma_(Rp, k.coef, bp);
     orr = fma_(Rr, k.coef, br);

@@ -739,6 +739,14 @@ pf_status create_common(const pf_params *p, int mode, int rank, int nranks, cons
             return fail(PF_ERR_NCCL);
         }
     }
+    // The memsets above ran on the non-blocking ctx stream, the uploads below use synchronous
+    // copies on the legacy stream (which does not order against non-blocking streams): fence both
+    // sides explicitly.
+    e = cudaStreamSynchronize(c->stream);
+    if (e != cudaSuccess) {
+        c->err = fmt("create: %s", cudaGetErrorString(e));
+        return fail(PF_ERR_CUDA);
+    }
     // initial conditions, generated on the host per member and slab (row a0)
     for (auto &S : c->slabs) {
         const size_t n = (size_t)S.L.ny_loc * p->nx;
@@ -761,6 +769,11 @@ pf_status create_common(const pf_params *p, int mode, int rank, int nranks, cons
                 }
             }
         }
+    }
+    e = cudaDeviceSynchronize();   // every upload complete before the first kernel on c->stream
+    if (e != cudaSuccess) {
+        c->err = fmt("create: %s", cudaGetErrorString(e));
+        return fail(PF_ERR_CUDA);
     }
     for (auto &S : c->slabs) {   // ghost frames of both buffers (rho reservoir rows in Us too)
         e = pf::launch_fill_ghosts(p->precision, S.L, p->rho_in, S.U, c->stream);

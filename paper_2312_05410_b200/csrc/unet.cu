@@ -1254,6 +1254,9 @@ pf_status un_set_weights(un_ctx *c, const float *blob, int64_t n) {
     if (n != un_blob_size(&c->p)) return fail(c, PF_ERR_ARG, fmt("blob has %lld floats, expected %lld", (long long)n,
                                                                   (long long)un_blob_size(&c->p)));
     cudaSetDevice(c->p.device);
+    // forwards run on the non-blocking c->st, the uploads below on the legacy stream: drain c->st
+    // first (a forward may still read the old weights) and fence the uploads at the end
+    UCK(c, cudaStreamSynchronize(c->st));
     const float *q = blob;
     for (int l = 0; l < kLayers; ++l) {
         const int ci = c->cin[l], co = c->cout[l], cip = c->cin_pad[l], cop = c->cout_pad[l];
@@ -1285,6 +1288,7 @@ pf_status un_set_weights(un_ctx *c, const float *blob, int64_t n) {
     }
     q += mlp.size();
     UCK(c, cudaMemcpy(c->mlp, mlp.data(), mlp.size() * sizeof(double), cudaMemcpyHostToDevice));
+    UCK(c, cudaDeviceSynchronize());
     c->have_w = true;
     return PF_OK;
 }

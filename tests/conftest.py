@@ -18,3 +18,19 @@ def ora():
     from oracle import oracle
     oracle.build()
     return oracle
+
+
+@pytest.hookimpl(trylast=True)
+def pytest_collection_modifyitems(session, config, items):
+    """Start the full-horizon oracle jobs (tests/_horizon.py) in the background when their tests
+    are selected (after -m deselection) and a GPU is present, so they overlap the GPU suite."""
+    if not any("test_zz_full_horizon_gpu" in it.nodeid for it in items):
+        return
+    try:
+        import torch
+        if not torch.cuda.is_available():
+            return
+    except Exception:
+        return
+    from tests import _horizon
+    _horizon.start()

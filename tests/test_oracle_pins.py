@@ -122,7 +122,8 @@ def _face_matrix(nx, ny):
 
 def test_rhs_dense_brute_force_8x8(ora):
     """8x8 brute force: L = -D^T D/dx^2, R_c = -D^T diag(M_f) D mu_c/dx^2 with
-    M_f = (M_a + M_b)/2, R_phi = M_phi L mu_phi + S, R_rho = D_rho L_res rho - v.G rho - S.
+    M_f = (M_a + M_b)/2, R_phi = M_phi L mu_phi + S, R_rho = D_rho L_res rho - v.G rho
+    - rho v.G phit with phit = 2 phi - 1 (P:340 in the paper's variable; R-1, R-9).
     Assembled as dense matrices, independent of the stencil loops."""
     nx = ny = 8
     dx = 0.9
@@ -163,9 +164,11 @@ def test_rhs_dense_brute_force_8x8(ora):
         Mf = 0.5 * (M[ia] + M[ib])
         Rc_bf = -(D.T @ (Mf * (D @ mu_c.ravel()))) / dx**2
         S_bf = rho.ravel() * (m.v_x * (Gx @ phi.ravel()) + m.v_y * (Gy @ phi.ravel()))
+        phit = 2.0 * phi.ravel() - 1.0
         Rp_bf = m.M_phi * (Lmat @ mu_p.ravel()) + S_bf
         Rr_bf = (m.D_rho * (Lres @ rho.ravel() + bres)
-                 - (m.v_x * (Gx @ rho.ravel()) + m.v_y * (Gyres @ rho.ravel() + gres)) - S_bf)
+                 - (m.v_x * (Gx @ rho.ravel()) + m.v_y * (Gyres @ rho.ravel() + gres))
+                 - rho.ravel() * (m.v_x * (Gx @ phit) + m.v_y * (Gy @ phit)))
         Rc, Rp, Rr, S = ora.rhs(m, c, phi, rho)
         for got, want in ((Rc, Rc_bf), (Rp, Rp_bf), (Rr, Rr_bf), (S, S_bf)):
             assert np.max(np.abs(got.ravel() - want)) <= 1e-13 * max(1.0, np.max(np.abs(want)))
@@ -353,6 +356,65 @@ def test_source_closed_form_and_bookkeeping(ora):
     Rc, Rp, Rr, S2 = ora.rhs(m2, c, phi2, rho2)
     assert abs(Rp.sum() - S2.sum()) <= 1e-12 * np.abs(S2).sum()
     assert abs(Rc.sum()) <= 1e-12 * np.abs(Rc).sum()
+
+
+def _vapour_boundary_sum(m, rho):
+    """Sum over cells of D_rho L(rho) - v.G(rho) with the reservoir/mirror rules: everything
+    telescopes except the top reservoir face and the y ends of the central difference."""
+    dx = m.dx
+    top, bot = rho[-1, :], rho[0, :]
+    diff = m.D_rho * (m.rho_in - top) / dx**2
+    adv = m.v_y * (m.rho_in + top - 2.0 * bot) / (2.0 * dx)
+    return float(np.sum(diff - adv))
+
+
+def test_vapour_sink_equals_paper_source_in_phit(ora):
+    """P:331-340 in the paper's variable phit = 2 phi - 1 in [-1, 1]: the phit equation
+    gains grad(phit).(rho v) and the rho equation loses exactly the same field.  With phi stored in
+    [0, 1] (R-1) d(phit)/dt = 2 d(phi)/dt, so cell by cell
+        2 (R_phi - M_phi L mu_phi) == -(R_rho - D_rho L rho + v.G rho) == rho v.G(phit).
+    A sink of -S (half the paper's) fails this by a factor of 2."""
+    nx = ny = 8
+    for seed in range(3):
+        g = np.random.default_rng(300 + seed)
+        c = g.random((ny, nx)); phi = g.random((ny, nx)); rho = g.random((ny, nx))
+        m = _model(ora, dx=0.7, M_phi=1.3, D_rho=0.6, rho_in=0.9, v_x=0.31, v_y=-0.57)
+        Rc, Rp, Rr, S = ora.rhs(m, c, phi, rho)
+        _, mu_p = ora.mu(m, c, phi)
+        ch = m.M_phi * ora.laplacian(mu_p, m.dx)
+        # the paper's phit source, written out with explicit neighbours (mirror rule in y, R-12)
+        pt = 2.0 * phi - 1.0
+        ptp = np.vstack([pt, pt[-1:]]); ptm = np.vstack([pt[:1], pt])
+        gx = (np.roll(pt, -1, 1) - np.roll(pt, 1, 1)) / (2 * m.dx)
+        gy = (ptp[1:] - ptm[:-1]) / (2 * m.dx)
+        src_phit = rho * (m.v_x * gx + m.v_y * gy)
+        rp = np.vstack([rho, np.full((1, nx), m.rho_in)]); rm = np.vstack([rho[:1], rho])
+        lrho = (np.roll(rho, -1, 1) + np.roll(rho, 1, 1) + rp[1:] + rm[:-1] - 4 * rho) / m.dx**2
+        vgr = m.v_x * (np.roll(rho, -1, 1) - np.roll(rho, 1, 1)) / (2 * m.dx) \
+            + m.v_y * (rp[1:] - rm[:-1]) / (2 * m.dx)
+        tol = 1e-13 * np.max(np.abs(src_phit))
+        np.testing.assert_allclose(2.0 * (Rp - ch), src_phit, atol=tol, rtol=0)
+        np.testing.assert_allclose(-(Rr - m.D_rho * lrho + vgr), src_phit, atol=tol, rtol=0)
+
+
+def test_vapour_plus_solid_bookkeeping(ora):
+    """P:331 + P:340: d/dt (phit + rho) is a pure divergence, so sum(rho + phit) = sum(rho + 2 phi)
+    changes only through the boundary faces: per RHS, sum(R_rho + 2 R_phi) = B(rho) with B the top
+    reservoir diffusion face and the y ends of the central advection; per midpoint step,
+    sum(rho + 2 phi)^{n+1} - sum(rho + 2 phi)^n = dt B(rho*)."""
+    c, phi, rho = inputs.random_state(16, 24, 17, phi_kind="smooth")
+    m = _model(ora, nx=16, ny=24, D_rho=0.8, rho_in=0.9, v_x=0.2, v_y=-0.6)
+    Rc, Rp, Rr, S = ora.rhs(m, c, phi, rho)
+    B = _vapour_boundary_sum(m, rho)
+    scale = np.abs(Rr).sum() + 2 * np.abs(Rp).sum()
+    assert abs((Rr + 2 * Rp).sum() - B) <= 1e-13 * scale
+    # a literal -S sink would leave sum(S) behind
+    assert abs(S.sum()) > 1e-3 * scale
+    # one step: u* from the RHS at u^n (P:348 midpoint), boundary sum at u*
+    rs = rho + 0.5 * m.dt * Rr
+    c1, p1, r1 = ora.step(m, c, phi, rho, 1)
+    lhs = (r1 + 2 * p1).sum() - (rho + 2 * phi).sum()
+    assert abs(lhs - m.dt * _vapour_boundary_sum(m, rs)) <= 1e-12 * m.dt * scale
 
 
 def test_mass_conservation_with_and_without_source(ora):

@@ -154,27 +154,31 @@ def test_cfg5_recipe_1024_full_grid_fp32(ora):
     assert e <= 1e-4, e
 
 
-@pytest.mark.skipif(os.environ.get("PF_NIGHTLY") != "1", reason="full horizons take ~10 min of oracle time; PF_NIGHTLY=1")
-def test_nightly_full_horizons(ora):
-    """SURVEY 8(c.4) full horizons: configs[1] 10,000 steps and configs[2] members 0, 21, 42, 63
-    after 5,000 steps, <= 1e-8 normwise."""
-    p2 = pf.pf_default_params(2)
-    m2, ic2 = oracle_member(ora, p2, 0)
-    f2 = _POOL.submit(lambda: ora.step(m2, *ora.initial_fields(ic2, 256, 256, 0), 10000))
-    p3 = pf.pf_default_params(3)
-
-    def long(k):
-        m, ic = oracle_member(ora, p3, k)
-        return k, ora.step(m, *ora.initial_fields(ic, 512, 512, k), 5000)
-
-    f3 = [_POOL.submit(long, k) for k in (0, 21, 42, 63)]
-    with pf.Simulation(p2) as s:
-        s.step(10000)
-        g2 = s.fields(0)
-    with pf.Simulation(p3) as s:
-        s.step(5000)
-        g3 = {k: s.fields(k) for k in (0, 21, 42, 63)}
-    assert normwise(g2, f2.result()) <= 1e-8
-    for f in f3:
-        k, ref = f.result()
-        assert normwise(g3[k], ref) <= 1e-8, k
+@pytest.mark.parametrize("nslabs", [4, 8])
+def test_cfg4_loopback_slabs_vs_oracle(ora, nslabs):
+    """configs[3] (4096^2 fp64) in P = 4 / 8 y-slabs (loopback transport: the per-stage 2-row halo
+    exchange and the overlap schedule of the multi-GPU path, in one process) against the oracle
+    directly: the full grid after 1 step (<= 1e-12, diagnostics within 1e-12) and light-cone
+    windows after 100 steps (<= 1e-8) straddling the slab boundaries y = 512 and y = 1024 (P = 8)
+    / y = 1024 (P = 4) with the film interface at y = 512."""
+    p = pf.pf_default_params(4)
+    nx, ny = p.nx, p.ny
+    m, ic = oracle_member(ora, p, 0)
+    wins = [(500, 0, 1024, 1536), (2500, 600, 1024, 1024)]
+    futs = [_POOL.submit(_window, ora, m, ic, 0, nx, ny, i0, j0, W, H, 100) for i0, j0, W, H in wins]
+    f1 = _POOL.submit(lambda: ora.step(m, *ora.initial_fields(ic, nx, ny, 0), 1))
+    with pf.Simulation(p, ("loopback", nslabs)) as s:
+        s.step(1)
+        g1 = s.fields(0)
+        d1 = s.diagnostics(0)
+        s.step(99)
+        g100 = s.fields(0)
+    ref1 = f1.result()
+    assert normwise(g1, ref1) <= 1e-12
+    dref = ora.diagnostics(m, *ref1)
+    for q in range(4):
+        assert abs(d1[q] - dref[q]) <= 1e-12 * abs(dref[q]), (q, d1[q], dref[q])
+    for (i0, j0, W, H), f in zip(wins, futs):
+        ref, valid, cols = f.result()
+        e = _window_err(g100, j0, H, cols, ref, valid)
+        assert e <= 1e-8, ((i0, j0), e)
