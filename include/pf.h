@@ -98,9 +98,10 @@ typedef struct {
     int32_t kernel_path;             /* stage kernel: 0 auto (single-domain grids of <= 2^19 cells in
                                         all: the persistent small-grid kernel; else the pair kernel
                                         when nx % 4 == 0 and nx >= 16, else the tile kernel),
-                                        1 tile, 2 one-column streaming, 3 pair streaming,
-                                        4 fused step (experimental), 5 warp-specialised step
-                                        (experimental), 6 reserved, 7 persistent small-grid     */
+                                        1 tile, 3 pair streaming, 5 warp-specialised step
+                                        (experimental), 7 persistent small-grid; 2 and 4 (the
+                                        round-1 one-column and fused-step kernels) are retired
+                                        and rejected with PF_ERR_ARG, 6 is reserved            */
     int32_t overlap_halo;            /* slab modes: 1 = update the 2-row boundary bands first and
                                         overlap the halo exchange with the interior update
                                         (needs >= 8 rows per slab), 0 = exchange after the stage */

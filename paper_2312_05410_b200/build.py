@@ -19,6 +19,7 @@ BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libpf.so")
 CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+PARTS = {"pf_kernels.cu": 6}   # compilation parts of a .cu file (-DPF_PART=0..n-1)
 
 
 def _nccl_dirs():
@@ -83,7 +84,11 @@ def _stale(obj, src):
     return any(os.path.getmtime(d) > t for d in _deps(src))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, lib: str = None, build_dir: str = None) -> str:
+    """Build LIB (or `lib` from objects in `build_dir`: variant builds with other PF_NVCC_EXTRA knobs)."""
+    global BUILD, LIB
+    if lib:
+        LIB, BUILD = lib, build_dir or lib + ".build"
     srcs = sources()
     if not force and os.path.exists(LIB):
         t = os.path.getmtime(LIB)
@@ -93,26 +98,34 @@ def build(force: bool = False, verbose: bool = False) -> str:
     inc_nccl, lib_nccl = _nccl_dirs()
     incs = ["-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", os.path.join(CUDA, "include"),
             "-I", inc_nccl]
-    objs = []
+    extra = os.environ.get("PF_NVCC_EXTRA", "").split()
+    jobs, objs = [], []
     for f in sorted(os.listdir(CSRC)):
         src = os.path.join(CSRC, f)
         if f.endswith(".cu"):
-            obj = os.path.join(BUILD, f[:-3] + ".o")
-            objs.append(obj)
-            if not force and not _stale(obj, src):
-                continue
-            extra = os.environ.get("PF_NVCC_EXTRA", "").split()
-            _run([os.path.join(CUDA, "bin", "nvcc"), *ARCH, "-O3", "-lineinfo", "-std=c++17", *extra,
-                  "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr", "-fmad=false",
-                  *incs, "-c", src, "-o", obj], verbose)
+            # pf_kernels.cu is compiled once per part (PF_PART, see the file's header): the pair
+            # kernel instantiations of each precision / stage build in parallel
+            parts = [None] if f not in PARTS else list(range(PARTS[f]))
+            for part in parts:
+                obj = os.path.join(BUILD, f[:-3] + ("" if part is None else f"_p{part}") + ".o")
+                objs.append(obj)
+                if not force and not _stale(obj, src):
+                    continue
+                dpart = [] if part is None else [f"-DPF_PART={part}"]
+                jobs.append([os.path.join(CUDA, "bin", "nvcc"), *ARCH, "-O3", "-lineinfo", "-std=c++17", *extra,
+                             *dpart, "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr",
+                             "-fmad=false", *incs, "-c", src, "-o", obj])
         elif f.endswith(".cpp"):
             obj = os.path.join(BUILD, f[:-4] + ".o")
             objs.append(obj)
             if not force and not _stale(obj, src):
                 continue
             # -ffp-contract=off: the initial fields must be bitwise reproducible (R-16)
-            _run(["g++", "-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-fno-fast-math",
-                  "-Wall", *incs, "-c", src, "-o", obj], verbose)
+            jobs.append(["g++", "-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-fno-fast-math",
+                         "-Wall", *incs, "-c", src, "-o", obj])
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as ex:
+        list(ex.map(lambda cmd: _run(cmd, verbose), jobs))
     nccl_so = "libnccl.so.2" if os.path.exists(os.path.join(lib_nccl, "libnccl.so.2")) else "libnccl.so"
     tmp = LIB + ".tmp"
     _run([os.path.join(CUDA, "bin", "nvcc"), *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs,
@@ -123,5 +136,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="--verbose" in sys.argv)
+    out = None
+    for a in sys.argv[1:]:
+        if a.startswith("--out="):
+            out = a[len("--out="):]
+    build(force="--force" in sys.argv, verbose="--verbose" in sys.argv, lib=out)
     print(LIB)

@@ -239,7 +239,7 @@ struct pf_ctx {
     cudaStream_t comm_stream = nullptr;   // halo exchange, overlapped with interior compute
     cudaEvent_t ev_band = nullptr, ev_xchg = nullptr;
     bool overlap = false;                 // band / exchange / interior schedule in use
-    bool fused = false;                   // fused-step kernel in use (kernel_path 4)
+    bool fused = false;                   // one-pass step kernel in use (kernel_path 5)
     bool persistent = false;              // small-grid cooperative kernel (kernel_path 7 / auto)
     ncclComm_t comm = nullptr;
     void *vel = nullptr;   // [members][2] in the storage precision
@@ -315,6 +315,7 @@ pf_status validate(const pf_params *p, std::string &why) {
     if (!(p->mob_lo > 0) || !(p->mob_hi >= p->mob_lo)) { why = "need 0 < mob_lo <= mob_hi"; return PF_ERR_ARG; }
     if (p->overlap_halo != 0 && p->overlap_halo != 1) { why = "overlap_halo must be 0 or 1"; return PF_ERR_ARG; }
     if (p->kernel_path < 0 || p->kernel_path > 7) { why = "kernel_path must be 0 .. 7"; return PF_ERR_ARG; }
+    if (p->kernel_path == 2 || p->kernel_path == 4 || p->kernel_path == 6) { why = "kernel_path 2, 4 (retired) and 6 (reserved) are not available"; return PF_ERR_ARG; }
     if (p->kernel_path >= 2 && p->kernel_path <= 6 && !(p->nx % 4 == 0 && p->nx >= 16)) { why = "streaming kernels need nx % 4 == 0 and nx >= 16"; return PF_ERR_ARG; }
     if (p->ic < PF_IC_FILM || p->ic > PF_IC_NONE) { why = "unknown ic"; return PF_ERR_ARG; }
     if ((p->ic == PF_IC_ROUGH_SUBSTRATE || p->ic == PF_IC_COLUMNS) && !(p->W_phi > 0)) { why = "tanh recipes need W_phi > 0"; return PF_ERR_ARG; }
@@ -470,7 +471,7 @@ pf_status one_step(pf_ctx *c, bool capture, int64_t step) {
                                     step, s.U, s.Us, c->stream));
             if (!capture) c->launches += 1;
         }
-    if (c->fused) {   // one fused pass per step (kernel_path 4, single domain): U -> Us, then swap
+    if (c->fused) {   // one fused pass per step (kernel_path 5, single domain): U -> Us, then swap
         Slab &S = c->slabs[0];
         cudaEvent_t e0 = nullptr, e1 = nullptr;
         if (prof) {
@@ -689,7 +690,7 @@ pf_status create_common(const pf_params *p, int mode, int rank, int nranks, cons
     }
     // overlap schedule: slab modes, bands of 2 rows leave an interior of >= 4 rows
     c->overlap = mode != kSingle && rows >= 8 && p->overlap_halo != 0;
-    c->fused = mode == kSingle && (p->kernel_path == 4 || p->kernel_path == 5) && c->slabs[0].plan.fused;
+    c->fused = mode == kSingle && p->kernel_path == 5 && c->slabs[0].plan.fused;
     {   // small grids: one cooperative launch per check interval instead of two launches per step
         const int64_t cells = (int64_t)p->n_members * p->nx * p->ny;
         c->persistent = mode == kSingle && !(p->noise_rho > 0.0) &&

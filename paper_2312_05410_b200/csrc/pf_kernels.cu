@@ -1,14 +1,16 @@
 // pf_kernels.cu -- sm_100a kernels of the PVD phase-field midpoint step.
 //
-// stream_kernel (performance path): one fused pass per explicit-midpoint stage (P:348 section
-//   4.2).  Persistent blocks walk x-strips of the grid in y.  A producer warp streams boxes of
-//   R rows x 3 fields (c, phi, rho) of a strip -- plus the stage-2 base rows -- into a shared-
-//   memory ring with 3D TMA tensor copies (cp.async.bulk.tensor, mbarrier completion); compute
-//   warps evaluate mu / M once per cell (row a2) and the flux divergence, source, vapour and
-//   Euler-form update (rows a3-a5), exchanging x-neighbours by warp shuffles, and write the
-//   result together with its ghost-frame copies (row a1).
-// stage_kernel (fallback path, any nx): 2D shared-memory tiles with a 2-cell halo, ghost rules
-//   applied by index.
+// pair_kernel (performance path): one fused pass per explicit-midpoint stage (section 4.2).
+//   Persistent blocks walk x-strips of the grid in y.  A producer warp streams boxes of R rows x
+//   3 fields (c, phi, rho) of a strip -- plus the stage-2 base rows -- into a shared-memory ring
+//   with 3D TMA tensor copies (cp.async.bulk.tensor, mbarrier completion); compute warps (two
+//   columns per lane) evaluate mu / M once per cell (row a2) and the flux divergence, source,
+//   vapour and Euler-form update (rows a3-a5), exchanging x-neighbours by warp shuffles, and write
+//   the result together with its ghost-frame copies (row a1).
+// ws_kernel (experimental, kernel_path 5): one pass per midpoint step, stage-1 warps hand u* to
+//   stage-2 warps through shared memory.
+// stage_kernel (fallback path, any nx) and persistent_kernel (small grids): 2D shared-memory
+//   tiles with a 2-cell halo, ghost rules applied by index.
 // diag_kernel: fp64 sums, free energy E_h and non-finite counts with fixed-order reductions.
 //
 // Every cell's value comes from the same arithmetic (pf_cell.cuh) on every path, so results are
@@ -25,6 +27,14 @@
 
 namespace cg = cooperative_groups;
 
+// Compilation parts (build.py compiles this file once per part, in parallel): 0 = host plumbing,
+// tile / persistent / diagnostics / ghost / pack kernels; 1-4 = pair kernel fp64 stage 1, fp64
+// stage 2, fp32 stage 1, fp32 stage 2; 5 = warp-specialised step kernel.  Undefined = all.
+#ifndef PF_PART
+#define PF_PART -1
+#endif
+#define PF_IN(k) (PF_PART < 0 || PF_PART == (k))
+
 #ifndef PF_PAIR_UNROLL
 #define PF_PAIR_UNROLL 1   // unroll of the pair kernel's slot loop (experiment knob)
 #endif
@@ -35,10 +45,14 @@ constexpr int kPairUnroll = PF_PAIR_UNROLL;
 
 namespace pf {
 
+#if PF_IN(0)
 int env_int(const char *name, int dflt) {
     const char *v = getenv(name);
     return v ? atoi(v) : dflt;
 }
+#else
+int env_int(const char *name, int dflt);
+#endif
 
 namespace {
 
@@ -545,7 +559,7 @@ template <typename real>
 size_t stream_smem_bytes(int bx, int R, int S, bool base) {
     Ring<real> rg(bx, R, base);
     return 128 + (size_t)S * rg.slot_elems * sizeof(real) + 64 * sizeof(real) /* read slack */ +
-           (size_t)S * 16 + 64 * 8;
+           (size_t)S * 16 + 64 * 8;   // full, empty barriers; exp table
 }
 
 // Store one output value (field f, local row r, column x) and its ghost-frame copies: periodic
@@ -563,158 +577,6 @@ __device__ __forceinline__ void store_with_ghosts(const Layout &L, real *b, int 
     store_row_ghosts(L, b, r, x, v);
     if (g <= 1) store_row_ghosts(L, b, -1 - r, x, v);                                // y0 == 0 here
     else if (g >= L.ny - 2 && f != 2) store_row_ghosts(L, b, 2 * L.ny_loc - 1 - r, x, v);   // top slab
-}
-
-template <typename real, int NCW, int R, int S, bool BASE, int MOB, int FE, int MINB>
-__global__ void __launch_bounds__(32 * NCW + 32, MINB) stream_kernel(
-    Layout L, KC<real> k, const __grid_constant__ CUtensorMap mapIn, const __grid_constant__ CUtensorMap mapBase,
-    real *out, const real *__restrict__ vel, int Wo, int G) {
-    // Warp roles.  Warps [0, NCW): compute.  Warp NCW: producer -- lane 0 issues one TMA box per
-    // ring slot (R rows x 3 fields of the strip with 16 B halo columns on each side, plus the base
-    // box in stage 2), gated per slot by an "empty" mbarrier that every compute warp arrives on
-    // once it no longer reads the slot.  Compute warps never synchronise with each other: warp w
-    // owns output columns x0 + 30w + [0, 30); lane l evaluates mu / M at column x0 + 30w - 1 + l
-    // and passes them to lanes l -+ 1 by warp shuffles.  Rows are consumed R per slot (unrolled),
-    // computing unconditionally (only stores are predicated) so the per-lane sliding windows
-    // rotate by register renaming.
-    constexpr int HL = 16 / (int)sizeof(real);
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    const int bx = Wo + 2 * HL;
-    const Ring<real> rg(bx, R, BASE);
-    // 128 B-aligned ring base, derived from smem_raw by an offset so that the compiler keeps the
-    // shared address space (LDS, not generic LD) for every ring access.
-    real *slots = reinterpret_cast<real *>(smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u));
-    uint64_t *full = reinterpret_cast<uint64_t *>(slots + S * rg.slot_elems + 64);
-    uint64_t *empty = full + S;
-    double *etab = reinterpret_cast<double *>(empty + S);
-    load_exp_table(etab);
-
-    const int t = threadIdx.x;
-    const int warp = t >> 5, lane = t & 31;
-    if (t == 0) {
-        for (int q = 0; q < S; ++q) {
-            mbar_init(&full[q], 1);
-            mbar_init(&empty[q], NCW);
-        }
-        fence_mbar_init();
-    }
-    __syncthreads();
-
-    const int nx = L.nx;
-    const Sched sch = make_sched(L, Wo, G);
-    const uint32_t box_bytes = (uint32_t)(3 * R * bx * sizeof(real));
-
-    if (warp == NCW) {
-        // ------------------------------- producer -------------------------------
-        if (lane != 0) return;
-        prefetch_tmap(&mapIn);
-        if (BASE) prefetch_tmap(&mapBase);
-        uint32_t g = 0;
-        int64_t pos = sch.lo;
-        Seg sg;
-        while (next_seg(L, Wo, sch, pos, sg)) {
-            const int n = sg.yb - sg.ya + 4, nsl = (n + R - 1) / R;
-            for (int j = 0; j < nsl; ++j, ++g) {
-                const int slot = g % S;
-                if (g >= (uint32_t)S) mbar_wait(&empty[slot], ((g / S) - 1) & 1u);
-                real *sl = slots + slot * rg.slot_elems;
-                const int k0 = sg.ya - 2 + j * R;                 // first row of the box
-                mbar_expect_tx(&full[slot], BASE ? 2 * box_bytes : box_bytes);
-                // x: storage column of x0 - HL is x0 - HL + gx; y: storage row of k0 is k0 + 2
-                tma_load_3d(sl, &mapIn, sg.x0 - HL + L.gx, k0 + 2, 3 * sg.m, &full[slot]);
-                if (BASE) tma_load_3d(sl + rg.in_elems, &mapBase, sg.x0 - HL + L.gx, k0, 3 * sg.m, &full[slot]);
-            }
-        }
-        return;
-    }
-
-    // --------------------------- compute warps ---------------------------------
-    const int cx = 30 * warp - 1 + lane;    // strip-relative column of this lane's mu / M
-    const int ci = HL + cx;                 // its column in a box row
-    const int plane = R * bx;               // elements per field plane of a box
-    int sidx = 0;                           // ring slot of the current box
-    uint32_t par = 0;                       // its full-barrier phase parity
-    int64_t pos = sch.lo;
-    Seg sg;
-    while (next_seg(L, Wo, sch, pos, sg)) {
-        const int n = sg.yb - sg.ya + 4, nsl = (n + R - 1) / R;
-        const int x = sg.x0 + cx;           // global column of this lane
-        const bool store = lane >= 1 && lane <= 30 && cx < sg.Wp;
-        real *ob = out + sg.m * L.mstride;
-        real vx, vy;
-        scaled_velocity(k, vel, sg.m, vx, vy);
-        const Mob<real> mo = MOB == 2 ? load_mob(vel, sg.m) : Mob<real>{};
-
-        real c_m2 = 0, c_m1 = 0, c_0 = 0;                 // c rows k-2, k-1, k (own column)
-        real p_m3 = 0, p_m2 = 0, p_m1 = 0, p_0 = 0;       // phi rows k-3 .. k
-        real r_m3 = 0, r_m2 = 0, r_m1 = 0;                // rho rows k-3 .. k-1
-        real a_m2 = 0, a_m1 = 0;                          // mu_c rows k-2, k-1
-        real b_m3 = 0, b_m2 = 0, b_m1 = 0;                // mu_phi rows k-3 .. k-1
-        real M_m2 = 0, M_m1 = 0;                          // M rows k-2, k-1
-        real fn_m = 0;                                    // north face flux of row k-3
-        const real *prev = slots + (sidx == 0 ? S - 1 : sidx - 1) * rg.slot_elems + ci;
-        for (int j = 0; j < nsl; ++j) {
-            const real *cur = slots + sidx * rg.slot_elems + ci;
-            mbar_wait(&full[sidx], par);
-#pragma unroll
-            for (int u = 0; u < R; ++u) {
-                const int i = j * R + u;                  // row k = ya - 2 + i
-                const real *rk = cur + u * bx;                                             // row k
-                const real *rk1 = u >= 1 ? cur + (u - 1) * bx : prev + (R - 1) * bx;       // row k-1
-                const real *rk2 = u >= 2 ? cur + (u - 2) * bx : prev + (R - 2 + u) * bx;   // row k-2
-                c_m2 = c_m1; c_m1 = c_0; c_0 = rk[0];
-                p_m3 = p_m2; p_m2 = p_m1; p_m1 = p_0; p_0 = rk[plane];
-                r_m3 = r_m2; r_m2 = r_m1; r_m1 = rk1[2 * plane];
-                a_m2 = a_m1;
-                b_m3 = b_m2; b_m2 = b_m1;
-                M_m2 = M_m1;
-                // mu / M of row k-1 at this lane's column
-                constitutive<real, MOB, FE>(k, mo, etab, c_m1, p_m1, rk1[-1], rk1[1], c_m2, c_0, rk1[plane - 1],
-                                         rk1[plane + 1], p_m2, p_0, a_m1, b_m1, M_m1);
-                // update of row k-2.  East face flux from this lane's mu / M and lane+1's; the west
-                // flux is lane-1's east flux; the south flux is last row's north flux.
-                const real ar = __shfl_down_sync(0xffffffffu, a_m2, 1);
-                const real Mr = __shfl_down_sync(0xffffffffu, M_m2, 1);
-                const real bl = __shfl_up_sync(0xffffffffu, b_m2, 1), br_ = __shfl_down_sync(0xffffffffu, b_m2, 1);
-                const real fe = face_flux<real>(M_m2, Mr, a_m2, ar);
-                const real fw = __shfl_up_sync(0xffffffffu, fe, 1);
-                const real fn = face_flux<real>(M_m2, M_m1, a_m2, a_m1);
-                const real fs = fn_m;
-                fn_m = fn;
-                real bc = c_m2, bp = p_m2, bq = r_m2;   // stage 1: base = input
-                if (BASE) {                               // stage 2: base row k-2 = row u of the base box
-                    const real *bs = cur + rg.in_elems + u * bx;
-                    bc = bs[0]; bp = bs[plane]; bq = bs[2 * plane];
-                }
-                real oc, op, orr;
-                cell_update<real>(k, vx, vy, fe, fw, fn, fs, b_m2, bl, br_, b_m3, b_m1,
-                                  rk2[plane - 1], rk2[plane + 1], p_m3, p_m1,
-                                  r_m2, rk2[2 * plane - 1], rk2[2 * plane + 1], r_m3, r_m1,
-                                  bc, bp, bq, oc, op, orr);
-                if (store && i >= 4 && i < n) {
-                    const int r = sg.ya - 4 + i;          // local row k-2
-                    const bool edge = (x < L.gx) | (x >= nx - L.gx) | (L.y0 + r <= 1) | (L.y0 + r >= L.ny - 2);
-                    if (!edge) {
-                        const int64_t o = L.at(r, x);
-                        ob[o] = oc;
-                        ob[o + L.fstride] = op;
-                        ob[o + 2 * L.fstride] = orr;
-                    } else {
-                        store_with_ghosts<real>(L, ob, 0, r, x, oc);
-                        store_with_ghosts<real>(L, ob + L.fstride, 1, r, x, op);
-                        store_with_ghosts<real>(L, ob + 2 * L.fstride, 2, r, x, orr);
-                    }
-                }
-            }
-            // the previous box is no longer read (its last row was row k-2 of iteration jR+1)
-            __syncwarp();
-            if (j >= 1 && lane == 0) mbar_arrive(&empty[sidx == 0 ? S - 1 : sidx - 1]);
-            prev = cur;
-            if (++sidx == S) { sidx = 0; par ^= 1u; }
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[sidx == 0 ? S - 1 : sidx - 1]);   // the segment's last box
-    }
 }
 
 // ----------------------------------------------------------------------------------------
@@ -748,6 +610,11 @@ constexpr int kPairHalo = 4;    // box columns left of the strip (and right of i
 #endif
 constexpr bool kSinglesShfl = PF_SINGLES_SHFL;
 
+// A dedicated producer warp issues the TMA boxes and waits on per-slot "empty" mbarriers.  (Measured
+// alternative, round 2: no producer warp -- the last compute warp to release a slot refills it,
+// elected by a shared-memory counter, with 15-16 compute warps per SM instead of 12-16: 5-8%
+// slower on configs[2] stage 1 even with the schedule tabulated; the refill work sits on a compute
+// warp's critical path.  DESIGN.md 7.)
 template <typename real, int NCW, int R, int S, bool BASE, int MOB, int FE, int MINB>
 __global__ void __launch_bounds__(32 * NCW + 32, MINB) pair_kernel(
     Layout L, KC<real> k, const __grid_constant__ CUtensorMap mapIn, const __grid_constant__ CUtensorMap mapBase,
@@ -911,228 +778,14 @@ __global__ void __launch_bounds__(32 * NCW + 32, MINB) pair_kernel(
                     }
                 }
             }
+            // the previous box is no longer read (its last row was row k-2 of iteration jR+1)
             __syncwarp();
             if (j >= 1 && lane == 0) mbar_arrive(&empty[sidx == 0 ? S - 1 : sidx - 1]);
             prev = cur;
             if (++sidx == S) { sidx = 0; par ^= 1u; }
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[sidx == 0 ? S - 1 : sidx - 1]);
-    }
-}
-
-// ----------------------------------------------------------------------------------------
-// Fused-step kernel (SURVEY 7 "B9"): one pass per explicit-midpoint STEP instead of per stage.
-// Reads u^n once (3 fields) and writes u^{n+1} once (48 B per fp64 cell-step instead of 120 B);
-// the midpoint state u* never leaves the SM.  Rows stream through a TMA ring of 1-row boxes; per
-// input row k a compute lane (two columns, as in the pair kernel) evaluates
-//   stage 1: mu, M of u^n at row k-1 and u* at row k-2;
-//   stage 2 (lag 3): mu, M of u* at row k-3 and u^{n+1} at row k-4.
-// u* stays in registers (rows k-2 .. k-5), x-neighbours by warp shuffles.  A warp covers 64
-// columns; its u* is valid on 62, its stage-2 mu on 60, its outputs on the middle 56 (lanes
-// 2..29), so warps overlap by 8 columns (the halo is recomputed, 14%).  The midpoint ghost rows
-// of u* at the global y boundaries are replaced by the identities the two-pass kernels get from
-// the mirrored rows (zero boundary flux, mu_phi(-1) = mu_phi(0), phi*(-1) = phi*(0),
-// rho*(-1) = rho*(0), rho* above the top = the reservoir row), so every cell gets the same bits as
-// with the stage kernels.  Single-domain contexts only (a y-slab would need a 4-row u^n halo).
-constexpr int kFusedCols = 56;   // output columns per compute warp
-constexpr int kFusedHalo = 4;    // box columns left of the strip (and right of it)
-
-template <typename real, int NCW, int S, int MOB, int FE, int MINB>
-__global__ void __launch_bounds__(32 * NCW + 32, MINB) fused_kernel(
-    Layout L, KC<real> k, KC<real> k2, const __grid_constant__ CUtensorMap mapIn, real *out,
-    const real *__restrict__ vel, int Wo, int G) {
-    static_assert(S >= 8, "rows k .. k-4 are read from the ring, plus prefetch");
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    const int bx = Wo + 2 * kFusedHalo;
-    const Ring<real> rg(bx, 1, false);
-    unsigned char *base_sm = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
-    real *slots = reinterpret_cast<real *>(base_sm);
-    uint64_t *full = reinterpret_cast<uint64_t *>(base_sm + (size_t)S * rg.slot_elems * sizeof(real));
-    uint64_t *empty = full + S;
-    double *etab = reinterpret_cast<double *>(empty + S);
-    load_exp_table(etab);
-
-    const int t = threadIdx.x;
-    const int warp = t >> 5, lane = t & 31;
-    if (t == 0) {
-        for (int q = 0; q < S; ++q) {
-            mbar_init(&full[q], 1);
-            mbar_init(&empty[q], NCW);
-        }
-        fence_mbar_init();
-    }
-    __syncthreads();
-
-    const int nx = L.nx;
-    const Sched sch = make_sched(L, Wo, G);
-    const uint32_t box_bytes = (uint32_t)(3 * bx * sizeof(real));
-    constexpr int LEAD = 4, TRAIL = 4;   // input rows before / after the segment's output rows
-
-    if (warp == NCW) {
-        // ------------------------------- producer -------------------------------
-        if (lane != 0) return;
-        prefetch_tmap(&mapIn);
-        uint32_t g = 0;
-        int64_t pos = sch.lo;
-        Seg sg;
-        while (next_seg(L, Wo, sch, pos, sg)) {
-            const int n = sg.yb - sg.ya + LEAD + TRAIL;
-            const int bxs = sg.x0 - kFusedHalo + L.gx;
-            for (int j = 0; j < n; ++j, ++g) {
-                const int slot = g % S;
-                if (g >= (uint32_t)S) mbar_wait(&empty[slot], ((g / S) - 1) & 1u);
-                mbar_expect_tx(&full[slot], box_bytes);
-                // input row sg.ya - LEAD + j (storage row + 2); rows past the frame are zero-filled
-                tma_load_3d(slots + slot * rg.slot_elems, &mapIn, bxs, sg.ya - LEAD + j + 2, 3 * sg.m, &full[slot]);
-            }
-        }
-        return;
-    }
-
-    // --------------------------- compute warps ---------------------------------
-    // lane l of warp w owns strip columns cx, cx + 1, cx = 56 w + 2 l - 4; lanes 2..29 store
-    const int cx = kFusedCols * warp + 2 * lane - 4;
-    const int ci = kFusedHalo + cx;          // its (even) column in a box row
-    const int plane = bx;                    // fields of a 1-row box are bx apart
-    const unsigned FULL = 0xffffffffu;
-    int sidx = 0;
-    uint32_t par = 0;
-    int64_t pos = sch.lo;
-    Seg sg;
-    while (next_seg(L, Wo, sch, pos, sg)) {
-        const int n = sg.yb - sg.ya + LEAD + TRAIL;
-        const int x = sg.x0 + cx;
-        const bool store = lane >= 2 && lane <= 29 && cx < sg.Wp;
-        const bool xedge = (x < L.gx) | (x + 1 >= nx - L.gx);
-        real *ob = out + sg.m * L.mstride;
-        real vx, vy;
-        scaled_velocity(k, vel, sg.m, vx, vy);
-        const Mob<real> mo = MOB == 2 ? load_mob(vel, sg.m) : Mob<real>{};
-        // stage 1 windows (rows of u^n's mu / M): as in the pair kernel
-        real A1x = 0, A1y = 0, A2x = 0, A2y = 0, M1x = 0, M1y = 0, M2x = 0, M2y = 0;
-        real B1x = 0, B1y = 0, B2x = 0, B2y = 0, B3x = 0, B3y = 0, P3x = 0, P3y = 0, R3x = 0, R3y = 0;
-        real Fsx = 0, Fsy = 0;
-        // u* rows (pairs): c* k-2..k-4, phi* and rho* k-2..k-5
-        real Cs2x = 0, Cs2y = 0, Cs3x = 0, Cs3y = 0, Cs4x = 0, Cs4y = 0;
-        real Ps2x = 0, Ps2y = 0, Ps3x = 0, Ps3y = 0, Ps4x = 0, Ps4y = 0, Ps5x = 0, Ps5y = 0;
-        real Rs2x = 0, Rs2y = 0, Rs3x = 0, Rs3y = 0, Rs4x = 0, Rs4y = 0, Rs5x = 0, Rs5y = 0;
-        // stage 2 windows (rows of u*'s mu / M): A, M rows k-3, k-4; B rows k-3 .. k-5
-        real D1x = 0, D1y = 0, D2x = 0, D2y = 0, N1x = 0, N1y = 0, N2x = 0, N2y = 0;
-        real E1x = 0, E1y = 0, E2x = 0, E2y = 0, E3x = 0, E3y = 0, Gsx = 0, Gsy = 0;
-        // ring rows k-1 .. k-4 (slot pointers at this lane's column)
-        const real *r1 = nullptr, *r2 = nullptr, *r3 = nullptr, *r4 = nullptr;
-        for (int i = 0; i < n; ++i) {
-            const real *r0 = slots + sidx * rg.slot_elems + ci;     // row k = ya - 4 + i
-            mbar_wait(&full[sidx], par);
-            const int kk = sg.ya - LEAD + i;                          // local row k
-            // ---------------- stage 1: mu1 at k-1, u* at k-2 ----------------
-            if (i >= 2) {
-                const auto c0 = ld2(r0), c1 = ld2(r1), c2 = ld2(r2);
-                const auto p0 = ld2(r0 + plane), p1 = ld2(r1 + plane), p2 = ld2(r2 + plane);
-                const auto q1 = ld2(r1 + 2 * plane), q2 = ld2(r2 + 2 * plane);
-                const real cw1 = __shfl_up_sync(FULL, c1.y, 1), ce1 = __shfl_down_sync(FULL, c1.x, 1);
-                const real pw1 = __shfl_up_sync(FULL, p1.y, 1), pe1 = __shfl_down_sync(FULL, p1.x, 1);
-                const real pw2 = __shfl_up_sync(FULL, p2.y, 1), pe2 = __shfl_down_sync(FULL, p2.x, 1);
-                const real rw2 = __shfl_up_sync(FULL, q2.y, 1), re2 = __shfl_down_sync(FULL, q2.x, 1);
-                A2x = A1x; A2y = A1y; M2x = M1x; M2y = M1y;
-                B3x = B2x; B3y = B2y; B2x = B1x; B2y = B1y;
-                constitutive<real, MOB, FE>(k, mo, etab, c1.x, p1.x, cw1, c1.y, c2.x, c0.x, pw1, p1.y, p2.x, p0.x,
-                                            A1x, B1x, M1x);
-                constitutive<real, MOB, FE>(k, mo, etab, c1.y, p1.y, c1.x, ce1, c2.y, c0.y, p1.x, pe1, p2.y, p0.y,
-                                            A1y, B1y, M1y);
-                const real An = __shfl_down_sync(FULL, A2x, 1), Mn = __shfl_down_sync(FULL, M2x, 1);
-                const real Bn = __shfl_down_sync(FULL, B2x, 1), Bp = __shfl_up_sync(FULL, B2y, 1);
-                const real fex = face_flux<real>(M2x, M2y, A2x, A2y);
-                const real fey = face_flux<real>(M2y, Mn, A2y, An);
-                const real fwx = __shfl_up_sync(FULL, fey, 1);
-                const real fnx = face_flux<real>(M2x, M1x, A2x, A1x);
-                const real fny = face_flux<real>(M2y, M1y, A2y, A1y);
-                // rotate the u* window, then u*(k-2) = u^n(k-2) + dt/2 R(u^n)
-                Cs4x = Cs3x; Cs4y = Cs3y; Cs3x = Cs2x; Cs3y = Cs2y;
-                Ps5x = Ps4x; Ps5y = Ps4y; Ps4x = Ps3x; Ps4y = Ps3y; Ps3x = Ps2x; Ps3y = Ps2y;
-                Rs5x = Rs4x; Rs5y = Rs4y; Rs4x = Rs3x; Rs4y = Rs3y; Rs3x = Rs2x; Rs3y = Rs2y;
-                cell_update<real>(k, vx, vy, fex, fwx, fnx, Fsx, B2x, Bp, B2y, B3x, B1x, pw2, p2.y, P3x, p1.x, q2.x,
-                                  rw2, q2.y, R3x, q1.x, c2.x, p2.x, q2.x, Cs2x, Ps2x, Rs2x);
-                cell_update<real>(k, vx, vy, fey, fex, fny, Fsy, B2y, B2x, Bn, B3y, B1y, p2.x, pe2, P3y, p1.y, q2.y,
-                                  q2.x, re2, R3y, q1.y, c2.y, p2.y, q2.y, Cs2y, Ps2y, Rs2y);
-                Fsx = fnx; Fsy = fny;
-                P3x = p2.x; P3y = p2.y; R3x = q2.x; R3y = q2.y;
-            }
-            // ---------------- stage 2: mu2 at k-3, u^{n+1} at k-4 ----------------
-            if (i >= 5) {
-                const int gq = L.y0 + kk - 3, gu = L.y0 + kk - 4;      // global rows
-                // mu2 of u* at row k-3: the ghost neighbours at the y boundaries are mirrors
-                const bool qbot = gq == 0, qtop = gq == L.ny - 1;
-                const real cdx = qbot ? Cs3x : Cs4x, cdy = qbot ? Cs3y : Cs4y;
-                const real cux = qtop ? Cs3x : Cs2x, cuy = qtop ? Cs3y : Cs2y;
-                const real pdx = qbot ? Ps3x : Ps4x, pdy = qbot ? Ps3y : Ps4y;
-                const real pux = qtop ? Ps3x : Ps2x, puy = qtop ? Ps3y : Ps2y;
-                const real cw = __shfl_up_sync(FULL, Cs3y, 1), ce = __shfl_down_sync(FULL, Cs3x, 1);
-                const real pw = __shfl_up_sync(FULL, Ps3y, 1), pe = __shfl_down_sync(FULL, Ps3x, 1);
-                D2x = D1x; D2y = D1y; N2x = N1x; N2y = N1y;
-                E3x = E2x; E3y = E2y; E2x = E1x; E2y = E1y;
-                constitutive<real, MOB, FE>(k, mo, etab, Cs3x, Ps3x, cw, Cs3y, cdx, cux, pw, Ps3y, pdx, pux, D1x, E1x,
-                                            N1x);
-                constitutive<real, MOB, FE>(k, mo, etab, Cs3y, Ps3y, Cs3x, ce, cdy, cuy, Ps3x, pe, pdy, puy, D1y, E1y,
-                                            N1y);
-                // update of row k-4 (u* row k-4 is Cs4/Ps4/Rs4; mu2 rows k-5, k-4, k-3 = E3, E2, E1)
-                const bool ubot = gu == 0, utop = gu == L.ny - 1;
-                const real An = __shfl_down_sync(FULL, D2x, 1), Mn = __shfl_down_sync(FULL, N2x, 1);
-                const real Bn = __shfl_down_sync(FULL, E2x, 1), Bp = __shfl_up_sync(FULL, E2y, 1);
-                const real fex = face_flux<real>(N2x, N2y, D2x, D2y);
-                const real fey = face_flux<real>(N2y, Mn, D2y, An);
-                const real fwx = __shfl_up_sync(FULL, fey, 1);
-                real fnx = face_flux<real>(N2x, N1x, D2x, D1x), fny = face_flux<real>(N2y, N1y, D2y, D1y);
-                if (utop) { fnx = real(0); fny = real(0); }
-                const real fsx = ubot ? real(0) : Gsx, fsy = ubot ? real(0) : Gsy;
-                Gsx = fnx; Gsy = fny;
-                const real qdx = ubot ? E2x : E3x, qdy = ubot ? E2y : E3y;
-                const real qux = utop ? E2x : E1x, quy = utop ? E2y : E1y;
-                const real phdx = ubot ? Ps4x : Ps5x, phdy = ubot ? Ps4y : Ps5y;
-                const real phux = utop ? Ps4x : Ps3x, phuy = utop ? Ps4y : Ps3y;
-                const auto rt = ld2(r3 + 2 * plane);                    // rho ghost row (reservoir) if utop
-                const real rdx = ubot ? Rs4x : Rs5x, rdy = ubot ? Rs4y : Rs5y;
-                const real rux = utop ? rt.x : Rs3x, ruy = utop ? rt.y : Rs3y;
-                const real pw4 = __shfl_up_sync(FULL, Ps4y, 1), pe4 = __shfl_down_sync(FULL, Ps4x, 1);
-                const real rw4 = __shfl_up_sync(FULL, Rs4y, 1), re4 = __shfl_down_sync(FULL, Rs4x, 1);
-                const auto b0 = ld2(r4), b1 = ld2(r4 + plane), b2 = ld2(r4 + 2 * plane);   // u^n row k-4
-                real ocx, opx, orx, ocy, opy, ory;
-                cell_update<real>(k2, vx, vy, fex, fwx, fnx, fsx, E2x, Bp, E2y, qdx, qux, pw4, Ps4y, phdx, phux, Rs4x,
-                                  rw4, Rs4y, rdx, rux, b0.x, b1.x, b2.x, ocx, opx, orx);
-                cell_update<real>(k2, vx, vy, fey, fex, fny, fsy, E2y, E2x, Bn, qdy, quy, Ps4x, pe4, phdy, phuy, Rs4y,
-                                  Rs4x, re4, rdy, ruy, b0.y, b1.y, b2.y, ocy, opy, ory);
-                if (store && i >= LEAD + 4 && kk - 4 < sg.yb) {
-                    const int r = kk - 4;
-                    const bool edge = xedge | (L.y0 + r <= 1) | (L.y0 + r >= L.ny - 2);
-                    if (!edge) {
-                        real *o = ob + L.at(r, x);
-                        st2(o, ocx, ocy);
-                        st2(o + L.fstride, opx, opy);
-                        st2(o + 2 * L.fstride, orx, ory);
-                    } else {
-                        store_with_ghosts<real>(L, ob, 0, r, x, ocx);
-                        store_with_ghosts<real>(L, ob + L.fstride, 1, r, x, opx);
-                        store_with_ghosts<real>(L, ob + 2 * L.fstride, 2, r, x, orx);
-                        store_with_ghosts<real>(L, ob, 0, r, x + 1, ocy);
-                        store_with_ghosts<real>(L, ob + L.fstride, 1, r, x + 1, opy);
-                        store_with_ghosts<real>(L, ob + 2 * L.fstride, 2, r, x + 1, ory);
-                    }
-                }
-            }
-            // the slot of row k-4 is no longer read
-            __syncwarp();
-            if (i >= 4 && lane == 0) {
-                const int s4 = sidx >= 4 ? sidx - 4 : sidx - 4 + S;
-                mbar_arrive(&empty[s4]);
-            }
-            r4 = r3; r3 = r2; r2 = r1; r1 = r0;
-            if (++sidx == S) { sidx = 0; par ^= 1u; }
-        }
-        // release the segment's last 4 rows
-        __syncwarp();
-        if (lane == 0)
-            for (int d = 1; d <= 4 && d <= n; ++d) mbar_arrive(&empty[sidx >= d ? sidx - d : sidx - d + S]);
+        if (lane == 0) mbar_arrive(&empty[sidx == 0 ? S - 1 : sidx - 1]);   // the segment's last box
     }
 }
 
@@ -1418,16 +1071,11 @@ KC<real> make_kc(const Coef &K, double coef) {
     return k;
 }
 
-// Ring geometry (rows per TMA box R, ring depth S, resident blocks per SM MINB) per kernel kind
-// and stage.  Stage 1 streams 3 fields per row, stage 2 six (input + base), so stage 2 gets the
-// shallower ring.
-struct RingVariant {
-    int R, S, minb;
-};
-constexpr RingVariant kStream1{4, 4, 2}, kStream2{2, 6, 2};
-// Pair kernel: about 128 registers per thread, so MINB = 16 / (NCW + 1) blocks of NCW + 1 warps
-// fill the register file with 12-16 compute warps per SM; rings of 2-row boxes as deep as the
-// shared memory left to each of the MINB blocks allows (at most 8 boxes).
+// Pair kernel ring geometry per precision, stage and producer mode: about 128 registers per
+// thread, so MINB = wslots / (warps per block) blocks fill the register file with 15-16 compute
+// warps per SM (12-16 with the producer warp); rings of 2-row boxes as deep as the shared memory
+// left to each of the MINB blocks allows (at most 8 boxes, at least 3: the box being read, the
+// previous one, and one in flight).
 #ifndef PF_F32_SLOTS
 #define PF_F32_SLOTS 20
 #endif
@@ -1441,33 +1089,37 @@ constexpr int kF32Slots = PF_F32_SLOTS;
 #ifndef PF_PAIR_R2
 #define PF_PAIR_R2 2
 #endif
+#ifndef PF_S1_SMEM_KB
+#define PF_S1_SMEM_KB 150   // fp64 stage-1 shared-memory budget per SM
+#endif
 template <typename real, int NCW, bool BASE>
 struct PairCfg {
     static constexpr int R = BASE ? PF_PAIR_R2 : PF_PAIR_R1;   // rows per TMA box
     static constexpr int bx_max = kPairCols * NCW + 2 * kPairHalo;
     static constexpr int slot = (3 * R * bx_max * (int)sizeof(real) + 127) / 128 * 128 * (BASE ? 2 : 1);
     // fp64 stage 1 keeps its ring small (>= 3 boxes) to leave L1 to the output stores: measured
-    // 4-5% faster than filling the shared memory (profiles/r1_kbench.log)
-    static constexpr int smem_kb = (sizeof(real) == 8 && !BASE) ? 150 : 227;
+    // 4-5% faster than filling the shared memory (r1)
+    static constexpr int smem_kb = (sizeof(real) == 8 && !BASE) ? PF_S1_SMEM_KB : 227;
     static constexpr int ring_raw(int b) { return ((smem_kb * 1024) / b - 2048) / slot; }
     static constexpr int ring(int b) { return (!BASE && sizeof(real) == 8 && ring_raw(b) < 3) ? 3 : ring_raw(b); }
     static constexpr int pick(int b) { return b <= 1 || ring(b) >= 3 ? b : pick(b - 1); }
     static constexpr int wslots = sizeof(real) == 8 ? PF_F64_SLOTS : kF32Slots;   // warp slots per SM budget
-    static constexpr int minb = pick(wslots / (NCW + 1) > 8 ? 8 : wslots / (NCW + 1));
+    static constexpr int wpb = NCW + 1;                                            // warps per block (+ producer)
+    static constexpr int minb = pick(wslots / wpb > 8 ? 8 : wslots / wpb);
     static constexpr int S = ring(minb) > 8 ? 8 : ring(minb);
     static_assert(S >= 3, "ring too shallow");
 };
 
-enum Kind { kStreamKind = 1, kPairKind = 2 };
-
-template <int KIND, typename real, int NCW, int R, int S, bool BASE, int MOB, int FE, int MINB>
-cudaError_t launch_ring(const Layout &L, const StreamPlan &P, const KC<real> &k, int stage, real *out,
-                        const real *vel, cudaStream_t s) {
+template <typename real, int NCW, bool BASE, int MOB, int FE>
+cudaError_t launch_pair_k(const Layout &L, const StreamPlan &P, const KC<real> &k, int stage, real *out,
+                          const real *vel, cudaStream_t s) {
+    using C = PairCfg<real, NCW, BASE>;
+    constexpr int R = C::R, S = C::S, MINB = C::minb;
     const size_t smem = stream_smem_bytes<real>(P.box_x, R, S, BASE);
+    const int threads = 32 * C::wpb;
     static int occ = -1, nsm = 0;
     static size_t smem_set = 0;
-    auto kern = KIND == kPairKind ? pair_kernel<real, NCW, R, S, BASE, MOB, FE, MINB>
-                                  : stream_kernel<real, NCW, R, S, BASE, MOB, FE, MINB>;
+    auto kern = pair_kernel<real, NCW, R, S, BASE, MOB, FE, MINB>;
     if (smem > smem_set) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
@@ -1478,7 +1130,7 @@ cudaError_t launch_ring(const Layout &L, const StreamPlan &P, const KC<real> &k,
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * NCW + 32, smem);
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
         if (e != cudaSuccess) return e;
         if (occ < 1) occ = 1;
     }
@@ -1500,152 +1152,50 @@ cudaError_t launch_ring(const Layout &L, const StreamPlan &P, const KC<real> &k,
     const int ri = R == 4 ? 1 : 0;
     const CUtensorMap &mIn = stage == 1 ? P.mapU[ri] : P.mapUs[ri];
     static const int pdl = env_int("PF_PDL", 1);
-    if (KIND == kPairKind && pdl) {   // programmatic dependent launch (pair_kernel waits in-kernel)
+    if (pdl) {   // programmatic dependent launch (pair_kernel waits in-kernel)
         cudaLaunchConfig_t cfg = {};
         cudaLaunchAttribute at[1];
         at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         at[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.gridDim = dim3((unsigned)B);
-        cfg.blockDim = dim3(32 * NCW + 32);
+        cfg.blockDim = dim3(threads);
         cfg.dynamicSmemBytes = smem;
         cfg.stream = s;
         cfg.attrs = at;
         cfg.numAttrs = 1;
         return cudaLaunchKernelEx(&cfg, kern, L, k, mIn, P.mapU[ri], out, vel, P.Wo, (int)G);
     }
-    kern<<<(unsigned)B, 32 * NCW + 32, smem, s>>>(L, k, mIn, P.mapU[ri], out, vel, P.Wo, (int)G);
+    kern<<<(unsigned)B, threads, smem, s>>>(L, k, mIn, P.mapU[ri], out, vel, P.Wo, (int)G);
     return cudaGetLastError();
 }
 
-template <int KIND, typename real, int NCW, bool BASE, int R, int S, int MINB>
-cudaError_t launch_ring_h(const Layout &L, const StreamPlan &P, const KC<real> &k, int stage, real *out,
+template <typename real, int NCW, bool BASE>
+cudaError_t launch_pair_h(const Layout &L, const StreamPlan &P, const KC<real> &k, int stage, real *out,
                           const real *vel, cudaStream_t s) {
     if (k.fe == 1) {
         switch (k.mob) {
-            case 0: return launch_ring<KIND, real, NCW, R, S, BASE, 0, 1, MINB>(L, P, k, stage, out, vel, s);
-            case 1: return launch_ring<KIND, real, NCW, R, S, BASE, 1, 1, MINB>(L, P, k, stage, out, vel, s);
-            default: return launch_ring<KIND, real, NCW, R, S, BASE, 2, 1, MINB>(L, P, k, stage, out, vel, s);
+            case 0: return launch_pair_k<real, NCW, BASE, 0, 1>(L, P, k, stage, out, vel, s);
+            case 1: return launch_pair_k<real, NCW, BASE, 1, 1>(L, P, k, stage, out, vel, s);
+            default: return launch_pair_k<real, NCW, BASE, 2, 1>(L, P, k, stage, out, vel, s);
         }
     }
     switch (k.mob) {
-        case 0: return launch_ring<KIND, real, NCW, R, S, BASE, 0, 0, MINB>(L, P, k, stage, out, vel, s);
-        case 1: return launch_ring<KIND, real, NCW, R, S, BASE, 1, 0, MINB>(L, P, k, stage, out, vel, s);
-        default: return launch_ring<KIND, real, NCW, R, S, BASE, 2, 0, MINB>(L, P, k, stage, out, vel, s);
+        case 0: return launch_pair_k<real, NCW, BASE, 0, 0>(L, P, k, stage, out, vel, s);
+        case 1: return launch_pair_k<real, NCW, BASE, 1, 0>(L, P, k, stage, out, vel, s);
+        default: return launch_pair_k<real, NCW, BASE, 2, 0>(L, P, k, stage, out, vel, s);
     }
 }
 
-template <typename real, int NCW>
-cudaError_t launch_stream_n(const Layout &L, const StreamPlan &P, const KC<real> &k, int stage, real *out,
-                            const real *vel, cudaStream_t s) {
-    if (stage == 1)
-        return launch_ring_h<kStreamKind, real, NCW, false, kStream1.R, kStream1.S, kStream1.minb>(L, P, k, stage,
-                                                                                                    out, vel, s);
-    return launch_ring_h<kStreamKind, real, NCW, true, kStream2.R, kStream2.S, kStream2.minb>(L, P, k, stage, out,
-                                                                                              vel, s);
-}
-
-template <typename real, int NCW>
-cudaError_t launch_pair_n(const Layout &L, const StreamPlan &P, const KC<real> &k, int stage, real *out,
-                          const real *vel, cudaStream_t s) {
-    using C1 = PairCfg<real, NCW, false>;
-    using C2 = PairCfg<real, NCW, true>;
-    if (stage == 1) return launch_ring_h<kPairKind, real, NCW, false, C1::R, C1::S, C1::minb>(L, P, k, stage, out, vel, s);
-    return launch_ring_h<kPairKind, real, NCW, true, C2::R, C2::S, C2::minb>(L, P, k, stage, out, vel, s);
-}
-
-template <typename real>
-cudaError_t launch_stream(const Layout &L, const StreamPlan &P, const KC<real> &k, int stage, real *out,
-                          const real *vel, cudaStream_t s) {
-    if (P.kind == kPairKind) {
-        switch (P.ncw) {
-            case 1: return launch_pair_n<real, 1>(L, P, k, stage, out, vel, s);
-            case 2: return launch_pair_n<real, 2>(L, P, k, stage, out, vel, s);
-            case 3: return launch_pair_n<real, 3>(L, P, k, stage, out, vel, s);
-            case 4: return launch_pair_n<real, 4>(L, P, k, stage, out, vel, s);
-            default: return cudaErrorInvalidValue;
-        }
-    }
+// One stage of the pair kernel (both precisions, both stages: a separate compilation part each,
+// see build.py).
+template <typename real, bool BASE>
+cudaError_t launch_pair(const Layout &L, const StreamPlan &P, const KC<real> &k, int stage, real *out,
+                        const real *vel, cudaStream_t s) {
     switch (P.ncw) {
-        case 2: return launch_stream_n<real, 2>(L, P, k, stage, out, vel, s);
-        case 4: return launch_stream_n<real, 4>(L, P, k, stage, out, vel, s);
-        case 6: return launch_stream_n<real, 6>(L, P, k, stage, out, vel, s);
-        case 8: return launch_stream_n<real, 8>(L, P, k, stage, out, vel, s);
-        default: return cudaErrorInvalidValue;
-    }
-}
-
-// Fused-step kernel configuration: ~2 blocks of NCW + 1 warps per SM (its two sets of stage windows
-// need ~2x the registers of the pair kernel); 1-row ring slots, 12 deep (rows k .. k-4 held).
-template <typename real, int NCW>
-struct FusedCfg {
-    static constexpr int minb = 2;
-    static constexpr int S = 12;
-};
-
-template <typename real, int NCW, int MOB, int FE>
-cudaError_t launch_fused_k(const Layout &L, const StreamPlan &P, const KC<real> &k, const KC<real> &k2, real *out,
-                           const real *vel, cudaStream_t s) {
-    using C = FusedCfg<real, NCW>;
-    const size_t smem = stream_smem_bytes<real>(P.fbox, 1, C::S, false);
-    static int occ = -1, nsm = 0;
-    static size_t smem_set = 0;
-    auto kern = fused_kernel<real, NCW, C::S, MOB, FE, C::minb>;
-    if (smem > smem_set) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        smem_set = smem;
-        occ = -1;
-    }
-    if (occ < 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * NCW + 32, smem);
-        if (e != cudaSuccess) return e;
-        if (occ < 1) occ = 1;
-    }
-    const int64_t T = (int64_t)L.members * (L.r1 - L.r0);
-    const int64_t minrows = 24;
-    int64_t B = (int64_t)occ * nsm;
-    int64_t G = B / P.fstrips;
-    if (G > (T + minrows - 1) / minrows) G = (T + minrows - 1) / minrows;
-    if (G >= 4) {
-        B = G * P.fstrips;
-    } else {
-        G = 0;
-        const int64_t R_ = (int64_t)L.members * P.fstrips * (L.r1 - L.r0);
-        if (B > (R_ + minrows - 1) / minrows) B = (R_ + minrows - 1) / minrows;
-    }
-    if (B < 1) B = 1;
-    kern<<<(unsigned)B, 32 * NCW + 32, smem, s>>>(L, k, k2, P.fmapU, out, vel, P.fWo, (int)G);
-    return cudaGetLastError();
-}
-
-template <typename real, int NCW>
-cudaError_t launch_fused_n(const Layout &L, const StreamPlan &P, const KC<real> &k, const KC<real> &k2, real *out,
-                           const real *vel, cudaStream_t s) {
-    if (k.fe == 1) {
-        switch (k.mob) {
-            case 0: return launch_fused_k<real, NCW, 0, 1>(L, P, k, k2, out, vel, s);
-            case 1: return launch_fused_k<real, NCW, 1, 1>(L, P, k, k2, out, vel, s);
-            default: return launch_fused_k<real, NCW, 2, 1>(L, P, k, k2, out, vel, s);
-        }
-    }
-    switch (k.mob) {
-        case 0: return launch_fused_k<real, NCW, 0, 0>(L, P, k, k2, out, vel, s);
-        case 1: return launch_fused_k<real, NCW, 1, 0>(L, P, k, k2, out, vel, s);
-        default: return launch_fused_k<real, NCW, 2, 0>(L, P, k, k2, out, vel, s);
-    }
-}
-
-template <typename real>
-cudaError_t launch_fused_t(const Layout &L, const StreamPlan &P, const KC<real> &k, const KC<real> &k2, real *out,
-                           const real *vel, cudaStream_t s) {
-    switch (P.fncw) {
-        case 1: return launch_fused_n<real, 1>(L, P, k, k2, out, vel, s);
-        case 2: return launch_fused_n<real, 2>(L, P, k, k2, out, vel, s);
-        case 3: return launch_fused_n<real, 3>(L, P, k, k2, out, vel, s);
-        case 4: return launch_fused_n<real, 4>(L, P, k, k2, out, vel, s);
+        case 1: return launch_pair_h<real, 1, BASE>(L, P, k, stage, out, vel, s);
+        case 2: return launch_pair_h<real, 2, BASE>(L, P, k, stage, out, vel, s);
+        case 3: return launch_pair_h<real, 3, BASE>(L, P, k, stage, out, vel, s);
+        case 4: return launch_pair_h<real, 4, BASE>(L, P, k, stage, out, vel, s);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -1758,41 +1308,23 @@ bool encode_map(CUtensorMap *m, int precision, const Layout &L, void *buf, int b
 
 }  // namespace
 
+#if PF_IN(0)
 bool stream_eligible(const Layout &L) { return L.nx >= 16 && L.nx % 4 == 0 && L.ny_loc >= 2; }
 
 cudaError_t make_stream_plan(int precision, const Layout &L, void *U, void *Us, StreamPlan &P) {
     P = StreamPlan();
     if (L.path == 1 || !stream_eligible(L)) return cudaSuccess;
-    const int HL = precision == 0 ? 2 : 4;       // stream-kernel box halo: 16 B of columns
-    if (L.path == 3 || L.path == 0 || L.path == 4 || L.path == 5) {
-        // pair kernel: strips of Wo <= 240 columns (box Wo + 8 <= 256 elements), Wo a multiple of
-        // 4 (16 B rows for fp32 too), split nx evenly; 60 output columns per compute warp
-        int strips = (L.nx + 239) / 240;
-        int Wo = (L.nx + strips - 1) / strips;
-        Wo = (Wo + 3) / 4 * 4;
-        strips = (L.nx + Wo - 1) / Wo;
-        P.kind = 2;
-        P.ncw = (Wo + kPairCols - 1) / kPairCols;
-        P.Wo = Wo;
-        P.strips = strips;
-        P.box_x = Wo + 2 * kPairHalo;
-    } else {
-        // stream kernel: strip width at most 256 - 2 HL - 12 columns (box <= 256 elements), split
-        // nx evenly, a multiple of HL so boxes and rows stay 16 B aligned; NCW warps of 30 columns
-        const int maxw = 256 - 2 * HL - 12;
-        int strips = (L.nx + maxw - 1) / maxw;
-        int Wo = (L.nx + strips - 1) / strips;
-        Wo = (Wo + HL - 1) / HL * HL;
-        strips = (L.nx + Wo - 1) / Wo;
-        const int need = (Wo + 29) / 30;
-        int ncw = need <= 2 ? 2 : (need <= 4 ? 4 : (need <= 6 ? 6 : 8));
-        if (30 * ncw < Wo) return cudaErrorInvalidValue;
-        P.kind = 1;
-        P.ncw = ncw;
-        P.Wo = Wo;
-        P.strips = strips;
-        P.box_x = Wo + 2 * HL;
-    }
+    // pair kernel: strips of Wo <= 240 columns (box Wo + 8 <= 256 elements), Wo a multiple of 4
+    // (16 B rows for fp32 too), split nx evenly; 60 output columns per compute warp
+    int strips = (L.nx + 239) / 240;
+    int Wo = (L.nx + strips - 1) / strips;
+    Wo = (Wo + 3) / 4 * 4;
+    strips = (L.nx + Wo - 1) / Wo;
+    P.kind = 2;
+    P.ncw = (Wo + kPairCols - 1) / kPairCols;
+    P.Wo = Wo;
+    P.strips = strips;
+    P.box_x = Wo + 2 * kPairHalo;
     for (int ri = 0; ri < 2; ++ri)
         if (!encode_map(&P.mapU[ri], precision, L, U, P.box_x, ri ? 4 : 2) ||
             !encode_map(&P.mapUs[ri], precision, L, Us, P.box_x, ri ? 4 : 2))
@@ -1819,48 +1351,53 @@ cudaError_t make_stream_plan(int precision, const Layout &L, void *U, void *Us, 
         P.fused = true;
         P.ws = true;
     }
-    if (L.path == 4) {
-        // fused kernel: strips of 56 NCW columns, NCW for the least idle columns (ties: wider)
-        int best = 1, waste = 1 << 30;
-        for (int ncw = 1; ncw <= 4; ++ncw) {
-            const int w = kFusedCols * ncw, st = (L.nx + w - 1) / w, idle = st * w - L.nx;
-            if (idle <= waste + L.nx / 50) { if (idle < waste) waste = idle; best = ncw; }
-        }
-        static const int force = env_int("PF_FUSED_NCW", 0);
-        if (force >= 1 && force <= 4) best = force;
-        P.fncw = best;
-        P.fWo = kFusedCols * best;
-        P.fstrips = (L.nx + P.fWo - 1) / P.fWo;
-        P.fbox = P.fWo + 2 * kFusedHalo;
-        if (!encode_map(&P.fmapU, precision, L, U, P.fbox, 1) || !encode_map(&P.fmapUs, precision, L, Us, P.fbox, 1))
-            return cudaErrorInvalidValue;
-        P.fused = true;
-    }
     return cudaSuccess;
 }
+#endif
 
+#if PF_IN(5)
 cudaError_t launch_fused(int precision, const Layout &L, const StreamPlan &P, const Coef &K, void *out, const void *vel,
                          double dt, cudaStream_t s) {
     cudaError_t te = upload_exp_table();
     if (te != cudaSuccess) return te;
-    if (!P.fused) return cudaErrorInvalidValue;
-    if (P.ws) {
-        if (precision == 0) {
-            const KC<double> k1 = make_kc<double>(K, 0.5 * dt), k2 = make_kc<double>(K, dt);
-            return P.fncw == 2 ? launch_ws_n<double, 2>(L, P, k1, k2, (double *)out, (const double *)vel, s)
-                               : launch_ws_n<double, 3>(L, P, k1, k2, (double *)out, (const double *)vel, s);
-        }
-        const KC<float> k1 = make_kc<float>(K, 0.5 * dt), k2 = make_kc<float>(K, dt);
-        return P.fncw == 2 ? launch_ws_n<float, 2>(L, P, k1, k2, (float *)out, (const float *)vel, s)
-                           : launch_ws_n<float, 3>(L, P, k1, k2, (float *)out, (const float *)vel, s);
+    if (!P.fused || !P.ws) return cudaErrorInvalidValue;
+    if (precision == 0) {
+        const KC<double> k1 = make_kc<double>(K, 0.5 * dt), k2 = make_kc<double>(K, dt);
+        return P.fncw == 2 ? launch_ws_n<double, 2>(L, P, k1, k2, (double *)out, (const double *)vel, s)
+                           : launch_ws_n<double, 3>(L, P, k1, k2, (double *)out, (const double *)vel, s);
     }
-    if (precision == 0)
-        return launch_fused_t<double>(L, P, make_kc<double>(K, 0.5 * dt), make_kc<double>(K, dt), (double *)out,
-                                      (const double *)vel, s);
-    return launch_fused_t<float>(L, P, make_kc<float>(K, 0.5 * dt), make_kc<float>(K, dt), (float *)out,
-                                 (const float *)vel, s);
+    const KC<float> k1 = make_kc<float>(K, 0.5 * dt), k2 = make_kc<float>(K, dt);
+    return P.fncw == 2 ? launch_ws_n<float, 2>(L, P, k1, k2, (float *)out, (const float *)vel, s)
+                       : launch_ws_n<float, 3>(L, P, k1, k2, (float *)out, (const float *)vel, s);
 }
+#endif
 
+// The pair-kernel stage launch of one precision and stage (compilation parts 1-4).
+#define PF_PAIR_ENTRY(NAME, REAL, BASE)                                                                          \
+    cudaError_t NAME(const Layout &L, const StreamPlan &P, const Coef &K, int stage, void *out, const void *vel,   \
+                     double coef, cudaStream_t s) {                                                              \
+        cudaError_t te = upload_exp_table();                                                                     \
+        if (te != cudaSuccess) return te;                                                                        \
+        return launch_pair<REAL, BASE>(L, P, make_kc<REAL>(K, coef), stage, (REAL *)out, (const REAL *)vel, s);  \
+    }
+cudaError_t pair_stage1_f64(const Layout &, const StreamPlan &, const Coef &, int, void *, const void *, double, cudaStream_t);
+cudaError_t pair_stage2_f64(const Layout &, const StreamPlan &, const Coef &, int, void *, const void *, double, cudaStream_t);
+cudaError_t pair_stage1_f32(const Layout &, const StreamPlan &, const Coef &, int, void *, const void *, double, cudaStream_t);
+cudaError_t pair_stage2_f32(const Layout &, const StreamPlan &, const Coef &, int, void *, const void *, double, cudaStream_t);
+#if PF_IN(1)
+PF_PAIR_ENTRY(pair_stage1_f64, double, false)
+#endif
+#if PF_IN(2)
+PF_PAIR_ENTRY(pair_stage2_f64, double, true)
+#endif
+#if PF_IN(3)
+PF_PAIR_ENTRY(pair_stage1_f32, float, false)
+#endif
+#if PF_IN(4)
+PF_PAIR_ENTRY(pair_stage2_f32, float, true)
+#endif
+
+#if PF_IN(0)
 template <typename real, int MOB, int FE, int TBY>
 cudaError_t launch_persistent_b(const Layout &L, const KC<real> &k1, const KC<real> &k2, real *U, real *Us,
                                 const real *vel, int64_t nsteps, cudaStream_t s) {
@@ -1924,8 +1461,10 @@ cudaError_t launch_stage(int precision, const Layout &L, const StreamPlan &P, co
     if (te != cudaSuccess) return te;
     if (P.ok) {
         if (precision == 0)
-            return launch_stream<double>(L, P, make_kc<double>(K, coef), stage, (double *)out, (const double *)vel, s);
-        return launch_stream<float>(L, P, make_kc<float>(K, coef), stage, (float *)out, (const float *)vel, s);
+            return stage == 1 ? pair_stage1_f64(L, P, K, stage, out, vel, coef, s)
+                              : pair_stage2_f64(L, P, K, stage, out, vel, coef, s);
+        return stage == 1 ? pair_stage1_f32(L, P, K, stage, out, vel, coef, s)
+                          : pair_stage2_f32(L, P, K, stage, out, vel, coef, s);
     }
     dim3 grid((L.nx + BX - 1) / BX, (L.r1 - L.r0 + BY - 1) / BY, L.members);
     if (precision == 0) {
@@ -2023,5 +1562,7 @@ cudaError_t launch_unpack_f64(int precision, const Layout &L, int field, int mem
         unpack_kernel<float><<<nb, 256, 0, s>>>(L, field, member0, nmem, src, (float *)state);
     return cudaGetLastError();
 }
+
+#endif  // PF_IN(0)
 
 }  // namespace pf

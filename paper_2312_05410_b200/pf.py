@@ -13,7 +13,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpf.so")
+# PF_LIB: an alternative in-tree build of the same library (A/B experiments of compile-time knobs)
+LIB_PATH = os.environ.get("PF_LIB") or os.path.join(_HERE, "libpf.so")
 HEADER = os.path.join(os.path.dirname(_HERE), "include", "pf.h")
 
 PF_ABI_VERSION = 6

@@ -40,15 +40,13 @@ def _eq(a, b):
 @pytest.mark.parametrize("nx,ny,members", [(64, 64, 1), (96, 48, 2), (260, 40, 1), (512, 72, 2), (16, 20, 1),
                                             (1000, 24, 1), (4096, 12, 1)])
 def test_tile_stream_pair_paths_bitwise(nx, ny, members):
-    """The three stage kernels (tile; one-column streaming; pair streaming) give identical bits:
-    same per-cell arithmetic, so any difference is an indexing or ghost-frame bug.  Covers one to
-    four compute warps per strip, several strips with a ragged last strip and minimal grids."""
+    """The stage kernels (tile; pair streaming) give identical bits: same per-cell arithmetic, so
+    any difference is an indexing, ring-refill or ghost-frame bug.  Covers one to four compute warps
+    per strip, several strips with a ragged last strip and minimal grids."""
     p = _base(nx, ny, n_members=members, rate_lo=0.5, rate_hi=2.0)
     a = _run(p.replace(kernel_path=1), 20)
-    b = _run(p.replace(kernel_path=2), 20)
     c = _run(p.replace(kernel_path=3), 20)
     for m in range(members):
-        assert _eq(a[m], b[m]), m
         assert _eq(a[m], c[m]), m
 
 
@@ -97,7 +95,7 @@ def test_resume_equals_straight_run():
 
 
 @pytest.mark.parametrize("nslabs,path,overlap,graph", [(2, 0, 1, 0), (4, 0, 1, 0), (4, 1, 1, 0), (8, 0, 1, 0),
-                                                        (4, 2, 1, 0), (4, 0, 0, 0), (2, 0, 1, 8), (16, 0, 1, 0)])
+                                                        (4, 3, 1, 0), (4, 0, 0, 0), (2, 0, 1, 8), (16, 0, 1, 0)])
 def test_loopback_slabs_equal_single_domain(nslabs, path, overlap, graph):
     """The y-slab decomposition (2-row halo exchanged after every stage) is bitwise invisible, with
     and without the overlap schedule (boundary bands first, exchange on the comm stream while the
@@ -229,28 +227,12 @@ def test_stochastic_inflow_invariants():
 
 
 def test_regular_solution_paths_bitwise():
-    """The regular-solution variant gives identical bits on the tile, stream and pair kernels."""
+    """The regular-solution variant gives identical bits on the tile and pair kernels."""
     p = _base(128, 40, n_members=2, fe_model=1, omega=2.2, temp_rs=0.45, rate_lo=0.5, rate_hi=2.0, dt=4e-4)
     a = _run(p.replace(kernel_path=1), 12)
-    b = _run(p.replace(kernel_path=2), 12)
     c = _run(p.replace(kernel_path=3), 12)
     for m in range(2):
-        assert _eq(a[m], b[m]) and _eq(a[m], c[m])
-
-
-@pytest.mark.parametrize("nx,ny,members,extra", [(128, 40, 2, {}), (512, 72, 2, {}), (96, 64, 3, dict(noise_rho=0.2)),
-                                                  (1000, 24, 1, {}), (200, 48, 2, dict(fe_model=1, omega=2.2,
-                                                                                     temp_rs=0.45, dt=4e-4))])
-def test_fused_step_kernel_bitwise(nx, ny, members, extra):
-    """The experimental fused-step kernel (kernel_path 4: one pass per midpoint step, u* kept on
-    chip, buffers swapped each step) gives the same bits as the two-stage pair kernel, including the
-    y-boundary identities it substitutes for u*'s ghost rows, stochastic inflow and the
-    regular-solution energy."""
-    p = _base(nx, ny, n_members=members, rate_lo=0.5, rate_hi=2.0, **extra)
-    a = _run(p.replace(kernel_path=3), 7)
-    b = _run(p.replace(kernel_path=4), 7)
-    for m in range(members):
-        assert _eq(a[m], b[m]), m
+        assert _eq(a[m], c[m])
 
 
 @pytest.mark.parametrize("nx,ny,members,extra", [(128, 40, 2, {}), (512, 72, 2, {}), (96, 64, 3, dict(noise_rho=0.2)),
