@@ -96,12 +96,15 @@ typedef struct {
     int32_t device;                  /* CUDA device ordinal                                  */
     int32_t graph_steps;             /* steps per captured CUDA graph (0 = no graphs)        */
     int32_t kernel_path;             /* stage kernel: 0 auto (single-domain grids of <= 2^19 cells in
-                                        all: the persistent small-grid kernel; else the pair kernel
-                                        when nx % 4 == 0 and nx >= 16, else the tile kernel),
-                                        1 tile, 3 pair streaming, 5 warp-specialised step
-                                        (experimental), 7 persistent small-grid; 2 and 4 (the
-                                        round-1 one-column and fused-step kernels) are retired
-                                        and rejected with PF_ERR_ARG, 6 is reserved            */
+                                        all: the band small-grid kernel where its bands fit, else
+                                        the persistent small-grid kernel; larger grids: the pair
+                                        kernel when nx % 4 == 0 and nx >= 16, else the tile
+                                        kernel), 1 tile, 3 pair streaming, 5 warp-specialised step
+                                        (experimental), 6 band small-grid (state resident in shared
+                                        memory, neighbour flags; PF_ERR_ARG where it does not fit),
+                                        7 persistent small-grid (grid barriers); 2 and 4 (the
+                                        round-1 one-column and fused-step kernels) are retired and
+                                        rejected with PF_ERR_ARG                                */
     int32_t overlap_halo;            /* slab modes: 1 = update the 2-row boundary bands first and
                                         overlap the halo exchange with the interior update
                                         (needs >= 8 rows per slab), 0 = exchange after the stage */

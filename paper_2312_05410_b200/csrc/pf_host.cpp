@@ -240,7 +240,9 @@ struct pf_ctx {
     cudaEvent_t ev_band = nullptr, ev_xchg = nullptr;
     bool overlap = false;                 // band / exchange / interior schedule in use
     bool fused = false;                   // one-pass step kernel in use (kernel_path 5)
-    bool persistent = false;              // small-grid cooperative kernel (kernel_path 7 / auto)
+    bool persistent = false;              // small-grid cooperative tile kernel (kernel_path 7)
+    bool band = false;                    // small-grid band kernel (kernel_path 6 / auto, pf_band.cu)
+    pf::BandPlan bplan;
     ncclComm_t comm = nullptr;
     void *vel = nullptr;   // [members][2] in the storage precision
     double *h_diag = nullptr;
@@ -315,8 +317,8 @@ pf_status validate(const pf_params *p, std::string &why) {
     if (!(p->mob_lo > 0) || !(p->mob_hi >= p->mob_lo)) { why = "need 0 < mob_lo <= mob_hi"; return PF_ERR_ARG; }
     if (p->overlap_halo != 0 && p->overlap_halo != 1) { why = "overlap_halo must be 0 or 1"; return PF_ERR_ARG; }
     if (p->kernel_path < 0 || p->kernel_path > 7) { why = "kernel_path must be 0 .. 7"; return PF_ERR_ARG; }
-    if (p->kernel_path == 2 || p->kernel_path == 4 || p->kernel_path == 6) { why = "kernel_path 2, 4 (retired) and 6 (reserved) are not available"; return PF_ERR_ARG; }
-    if (p->kernel_path >= 2 && p->kernel_path <= 6 && !(p->nx % 4 == 0 && p->nx >= 16)) { why = "streaming kernels need nx % 4 == 0 and nx >= 16"; return PF_ERR_ARG; }
+    if (p->kernel_path == 2 || p->kernel_path == 4) { why = "kernel_path 2 and 4 (retired) are not available"; return PF_ERR_ARG; }
+    if ((p->kernel_path == 3 || p->kernel_path == 5) && !(p->nx % 4 == 0 && p->nx >= 16)) { why = "streaming kernels need nx % 4 == 0 and nx >= 16"; return PF_ERR_ARG; }
     if (p->ic < PF_IC_FILM || p->ic > PF_IC_NONE) { why = "unknown ic"; return PF_ERR_ARG; }
     if ((p->ic == PF_IC_ROUGH_SUBSTRATE || p->ic == PF_IC_COLUMNS) && !(p->W_phi > 0)) { why = "tanh recipes need W_phi > 0"; return PF_ERR_ARG; }
     if (p->ic == PF_IC_ROUGH_SUBSTRATE && !(p->ic_wavelength != 0)) { why = "ic_wavelength must be != 0"; return PF_ERR_ARG; }
@@ -691,9 +693,19 @@ pf_status create_common(const pf_params *p, int mode, int rank, int nranks, cons
     // overlap schedule: slab modes, bands of 2 rows leave an interior of >= 4 rows
     c->overlap = mode != kSingle && rows >= 8 && p->overlap_halo != 0;
     c->fused = mode == kSingle && p->kernel_path == 5 && c->slabs[0].plan.fused;
-    {   // small grids: one cooperative launch per check interval instead of two launches per step
+    {   // small grids: one cooperative launch per check interval instead of two launches per step --
+        // the band kernel (state in shared memory, neighbour flags) where its bands fit, else the
+        // persistent tile kernel (grid barriers)
         const int64_t cells = (int64_t)p->n_members * p->nx * p->ny;
-        c->persistent = mode == kSingle && !(p->noise_rho > 0.0) &&
+        const bool small = mode == kSingle && !(p->noise_rho > 0.0);
+        if (small && (p->kernel_path == 6 || (p->kernel_path == 0 && cells <= kPersistentCells)))
+            c->band = pf::make_band_plan(p->precision, c->slabs[0].L, c->bplan);
+        if (p->kernel_path == 6 && !c->band) {
+            c->err = "kernel_path 6: the band kernel needs a single-domain ctx without inflow noise, ny >= 2 and a band "
+                     "(ny / min(16, ny / 2) rows) that fits one block's shared memory and 2048 cells";
+            return fail(PF_ERR_ARG);
+        }
+        c->persistent = small && !c->band &&
                         (p->kernel_path == 7 || (p->kernel_path == 0 && cells <= kPersistentCells));
     }
     c->ny_host = mode == kNccl ? rows : p->ny;
@@ -975,7 +987,14 @@ pf_status pf_step(pf_ctx *c, int64_t n) {
         if (chunk > left) chunk = left;
         int64_t done = 0;
         const bool use_graph = c->p.graph_steps > 0 && !c->prof && c->mode != kNccl && !(c->p.noise_rho > 0.0) &&
-                               !c->fused && !c->persistent;   // fused swaps buffers on the host each step
+                               !c->fused && !c->persistent && !c->band;   // fused swaps buffers on the host each step
+        if (c->band && !c->prof && chunk > 0) {
+            Slab &S = c->slabs[0];
+            CK(c, pf::launch_band(c->p.precision, S.L, c->bplan, c->K, S.U, c->vel, c->p.dt, chunk, c->stream));
+            CK(c, pf::launch_fill_ghosts(c->p.precision, S.L, c->p.rho_in, S.U, c->stream));
+            c->launches += 1 + pf::kFillLaunches;
+            done = chunk;
+        }
         if (c->persistent && !c->prof && chunk > 0) {
             Slab &S = c->slabs[0];
             CK(c, pf::launch_persistent(c->p.precision, S.L, c->K, S.U, S.Us, c->vel, c->p.dt, chunk, c->stream));

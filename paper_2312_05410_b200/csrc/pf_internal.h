@@ -88,6 +88,19 @@ cudaError_t launch_fused(int precision, const Layout &L, const StreamPlan &P, co
 // state before and after; owned cells only, the ghost frame is left stale).
 cudaError_t launch_persistent(int precision, const Layout &L, const Coef &K, void *U, void *Us, const void *vel,
                               double dt, int64_t nsteps, cudaStream_t s);
+// Small-grid band path (pf_band.cu): every member is one thread-block cluster of <= 16 blocks,
+// each block a band of >= 2 full-width rows held in shared memory for a whole launch; halo rows are
+// pushed into the neighbours' shared memory (DSMEM) between two cluster barriers per stage.
+struct BandPlan {
+    bool ok = false;
+    int bands_per_member = 0, blocks = 0, hmax = 0;
+    size_t smem = 0;            // dynamic shared memory per block
+};
+bool make_band_plan(int precision, const Layout &L, BandPlan &B);
+// nsteps midpoint steps of every member (U holds the state before and after; owned cells only).
+cudaError_t launch_band(int precision, const Layout &L, const BandPlan &B, const Coef &K, void *U, const void *vel,
+                        double dt, int64_t nsteps, cudaStream_t s);
+
 // Rebuild the ghost frame of a buffer from its owned cells (periodic columns; mirror rows and
 // the rho reservoir at global y boundaries).  Slab-interior ghost rows are left to the exchange.
 cudaError_t launch_fill_ghosts(int precision, const Layout &L, double rho_in, void *state, cudaStream_t s);

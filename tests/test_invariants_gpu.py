@@ -249,6 +249,44 @@ def test_warp_specialised_step_kernel_bitwise(nx, ny, members, extra):
         assert _eq(a[m], b[m]), m
 
 
+@pytest.mark.parametrize("nx,ny,members,extra", [(64, 64, 1, {}), (128, 128, 1, {}), (96, 48, 3, {}), (33, 65, 2, {}),
+                                                  (128, 40, 2, dict(mob_lo=0.5, mob_hi=1.0)),
+                                                  (80, 32, 1, dict(fe_model=1, omega=2.2, temp_rs=0.45, dt=4e-4)),
+                                                  (500, 24, 1, {}), (16, 8, 5, {}), (8, 8, 1, {})])
+def test_band_small_grid_kernel_bitwise(nx, ny, members, extra):
+    """The band small-grid kernel (kernel_path 6: each member one thread-block cluster of <= 16
+    bands of >= 2 rows held in shared memory, halo rows pushed into the neighbours' shared memory,
+    all steps of a check interval in one launch) gives the same bits as the tile kernel: uneven
+    bands, bands of exactly 2 rows, several members (clusters), per-member mobilities, the
+    regular-solution energy, and several launches."""
+    p = _base(nx, ny, n_members=members, rate_lo=0.5, rate_hi=2.0, check_every=9, **extra)
+    a = _run(p.replace(kernel_path=1), 23)
+    b = _run(p.replace(kernel_path=6), 23)
+    for m in range(members):
+        assert _eq(a[m], b[m]), m
+
+
+def test_band_kernel_is_the_small_grid_default_and_resumes():
+    """The default small-grid paths (configs[0]: band kernel; configs[1]: persistent tile kernel)
+    equal the pair kernel bitwise; a band run continues bitwise on the pair kernel (valid ghost
+    frame)."""
+    for cfg in (1, 2):
+        p = pf.pf_default_params(cfg)
+        a = _run(p.replace(kernel_path=0, check_every=50), 120)
+        b = _run(p.replace(kernel_path=3, graph_steps=0), 120)
+        assert _eq(a[0], b[0]), cfg
+    p = _base(96, 40, check_every=10)
+    with pf.Simulation(p.replace(kernel_path=6)) as s:
+        s.step(15)
+        u = s.fields(0)
+    with pf.Simulation(p.replace(kernel_path=3, ic=pf.PF_IC_NONE)) as s:
+        s.set_fields(0, *u)
+        s.step(10)
+        x = s.fields(0)
+    y = _run(p.replace(kernel_path=1), 25)[0]
+    assert _eq(x, y)
+
+
 @pytest.mark.parametrize("nx,ny,members,extra", [(64, 64, 1, {}), (96, 48, 3, {}), (33, 65, 2, {}),
                                                   (128, 40, 2, dict(mob_lo=0.5, mob_hi=1.0)),
                                                   (80, 32, 1, dict(fe_model=1, omega=2.2, temp_rs=0.45, dt=4e-4)),

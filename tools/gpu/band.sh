@@ -1,0 +1,6 @@
+cd $GRAFT_REPO_ROOT
+out=gpurun_out/${TAG:-band}
+mkdir -p $out
+timeout 600 python -m pytest tests/test_invariants_gpu.py -x -q -k "band or persistent" > $out/tests.log 2>&1
+timeout 300 python tools/small_grid_sweep.py > $out/sweep.jsonl 2>&1
+timeout 600 python -m pytest tests/test_parity_gpu.py -x -q > $out/parity.log 2>&1
