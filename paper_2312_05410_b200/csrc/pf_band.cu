@@ -110,15 +110,31 @@ __global__ void __launch_bounds__(kBT, 1) band_kernel(Layout L, KC<real> k1, KC<
     real base[3][MAXC];
     real outv[3][MAXC];
     const int nown = h * nx;
+    // the cells of this thread, fixed for the whole launch (no index division in the step loop):
+    // phase A cells q = t + i kBT (i < kAC) of the (h+2) x (nx+2) ring, phase B cells of the band
+    constexpr int kAC = 4;
+    const int nA = (h + 2) * (nx + 2);
+    int arr[kAC], ax[kAC], by[MAXC], bx[MAXC];
+#pragma unroll
+    for (int i = 0; i < kAC; ++i) {
+        const int q = t + i * kBT;
+        arr[i] = q / (nx + 2) - 1;
+        ax[i] = q - (arr[i] + 1) * (nx + 2) - 1;
+    }
+#pragma unroll
+    for (int i = 0; i < MAXC; ++i) {
+        const int q = t + i * kBT;
+        by[i] = q / nx;
+        bx[i] = q - by[i] * nx;
+    }
     cluster.sync();   // every block has started (DSMEM targets exist) and loaded its band
     int par = 0;      // halo parity read by this stage
 
     for (int64_t s = 0; s < nsteps; ++s) {
         for (int stage = 1; stage <= 2; ++stage) {
-            const KC<real> &k = stage == 1 ? k1 : k2;
+            const KC<real> k = stage == 1 ? k1 : k2;
             // A: mu_c, mu_phi, M on rows -1 .. h, columns -1 .. nx (row a2)
-            for (int q = t; q < (h + 2) * (nx + 2); q += kBT) {
-                const int rr = q / (nx + 2) - 1, x = q - (q / (nx + 2)) * (nx + 2) - 1;
+            auto cell_a = [&](int rr, int x) {
                 const int o0 = gg.u(BandGeo::srow(rr, h, par), x);
                 const int od = gg.u(BandGeo::srow(rr - 1, h, par), x), ou = gg.u(BandGeo::srow(rr + 1, h, par), x);
                 real mc, mp, M;
@@ -127,14 +143,18 @@ __global__ void __launch_bounds__(kBT, 1) band_kernel(Layout L, KC<real> k1, KC<
                 smc[gg.w(rr, x)] = mc;
                 smp[gg.w(rr, x)] = mp;
                 sM[gg.w(rr, x)] = M;
-            }
+            };
+#pragma unroll
+            for (int i = 0; i < kAC; ++i)
+                if (t + i * kBT < nA) cell_a(arr[i], ax[i]);
+            for (int q = t + kAC * kBT; q < nA; q += kBT) cell_a(q / (nx + 2) - 1, q - (q / (nx + 2)) * (nx + 2) - 1);
             __syncthreads();
             // B: fluxes, source, vapour, update of the owned cells (rows a3-a5), into registers
 #pragma unroll
             for (int i = 0; i < MAXC; ++i) {
                 const int q = t + i * kBT;
                 if (q < nown) {
-                    const int y = q / nx, x = q - y * nx;
+                    const int y = by[i], x = bx[i];
                     const int c0 = gg.u(y + 4, x), w0 = gg.w(y, x), Q = gg.Q;
                     const int cd = gg.u(BandGeo::srow(y - 1, h, par), x), cu = gg.u(BandGeo::srow(y + 1, h, par), x);
                     if (stage == 1) {
@@ -160,7 +180,7 @@ __global__ void __launch_bounds__(kBT, 1) band_kernel(Layout L, KC<real> k1, KC<
             for (int i = 0; i < MAXC; ++i) {
                 const int q = t + i * kBT;
                 if (q < nown) {
-                    const int y = q / nx, x = q - y * nx;
+                    const int y = by[i], x = bx[i];
 #pragma unroll
                     for (int f = 0; f < 3; ++f) {
                         const real v = outv[f][i];
