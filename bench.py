@@ -104,20 +104,76 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
-def _cpu_baseline(seconds=12.0):
-    """The oracle as it stands, single thread, on a bounded sample of configs[2]: member 0
-    (512 x 512 fp64), as many explicit-midpoint steps as fit in ~`seconds`."""
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def _oracle_member_worker(cfg, member, warmup, steps, seconds, out):
+    """One oracle process (single thread): `warmup` untimed steps of member `member` of configs[cfg -
+    1] (a 512 x 512 tile for the single-grid configs), then `steps` timed steps (or as many as fit
+    in `seconds` when steps is 0).  Puts (cells, steps, seconds) on `out`."""
+    sys.path.insert(0, ROOT)
     from oracle import oracle as ora
-    pr = ora.preset(3)
-    m = ora.member_model(pr, 0)
-    u = ora.initial_fields(pr["ic"], 512, 512, 0)
-    steps, t0 = 0, time.perf_counter()
-    while time.perf_counter() - t0 < seconds:
-        u = ora.step(m, *u, 5)
-        steps += 5
-    el = time.perf_counter() - t0
-    return {"value": 512 * 512 * steps / el, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"configs[2] member 0 (512x512 fp64), {steps} midpoint steps, single thread, {el:.1f} s"}
+    pr = ora.preset(cfg)
+    m = ora.member_model(pr, member if cfg == 3 else 0)
+    nx = PRESETS[cfg][0]
+    tx = min(512, nx)
+    if cfg == 3:
+        u = ora.initial_fields(pr["ic"], nx, PRESETS[cfg][1], member)
+    else:
+        c, phi, rho = ora.initial_fields_rows(pr["ic"], nx, 0, 0, min(512, PRESETS[cfg][1]))
+        u = (c[:, :tx].copy(), phi[:, :tx].copy(), rho[:, :tx].copy())
+    cells = u[0].size
+    if warmup:
+        u = ora.step(m, *u, warmup)
+    done, t0 = 0, time.perf_counter()
+    if steps > 0:
+        u = ora.step(m, *u, steps)
+        done = steps
+    else:
+        while time.perf_counter() - t0 < seconds:
+            u = ora.step(m, *u, 1)
+            done += 1
+    out.put((cells, done, time.perf_counter() - t0))
+
+
+def _oracle_ensemble(cfg, procs, warmup, steps, seconds=0.0):
+    """The oracle as it stands on `procs` concurrent single-threaded processes (one ensemble member,
+    or one 512 x 512 tile, each; SURVEY 8(d) "min(nproc, members) concurrent oracle processes").
+    Returns (cells per step over all processes, steps, wall seconds of the slowest process)."""
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")            # the parent may hold a CUDA context: never fork it
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_oracle_member_worker, args=(cfg, k, warmup, steps, seconds, q)) for k in range(procs)]
+    for p in ps:
+        p.start()
+    res = [q.get() for _ in ps]
+    for p in ps:
+        p.join()
+    cells = sum(r[0] for r in res)
+    nsteps = min(r[1] for r in res)
+    wall = max(r[2] for r in res)
+    return cells, nsteps, wall, res
+
+
+def _cpu_baseline(seconds=12.0):
+    """The oracle as it stands on min(nproc, 64) concurrent single-threaded processes, one member of
+    configs[2] (512 x 512 fp64) each, for ~`seconds`: aggregate cell-updates/s of the host."""
+    procs = min(os.cpu_count() or 1, PRESETS[3][2])
+    cells, nsteps, wall, res = _oracle_ensemble(3, procs, 0, 0, seconds)
+    value = sum(r[0] * r[1] / r[2] for r in res)
+    return {"value": value, "unit": UNIT, "cores": procs, "kind": "oracle", "cpu_model": _cpu_model(),
+            "nproc": os.cpu_count(),
+            "sample": f"configs[2] members 0..{procs - 1} (512x512 fp64), one single-threaded oracle process per "
+                      f"member on {procs} cores concurrently, {min(r[1] for r in res)}-{max(r[1] for r in res)} "
+                      f"midpoint steps each in {wall:.1f} s; value = sum of the per-process rates"}
 
 
 # (nx, ny, members, storage) of BASELINE.json configs[0..4] (R-13, R-14)
@@ -145,41 +201,93 @@ def workload_config(cfg, ws):
 
 
 def run_reference(args):
-    """--impl reference: the oracle (the reference arm of this tier) as it stands, one thread on
-    the host cores; each step advances a bounded 512 x 512 sample of the workload (configs[2]:
-    member 0; configs[3..4]: the bottom 512 x 512 tile) by one explicit-midpoint step."""
+    """--impl reference: the oracle (the reference arm of this tier) as it stands, on the host cores:
+    min(nproc, members) concurrent single-threaded processes, each advancing one ensemble member
+    (configs[2]) or one 512 x 512 tile (the single-grid configs) through W warm-up and K timed
+    explicit-midpoint steps.  A "step" of this arm is therefore one step of that bounded sample;
+    ms_per_step is its measured wall time per step (not extrapolated)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     ws = int(os.environ.get("WORLD_SIZE", "1"))
-    from oracle import oracle as ora
     cfg = args.config
-    pr = ora.preset(cfg)
-    m = ora.member_model(pr, 0)
-    nx, ny, mem, dt = PRESETS[cfg]
-    tx, ty = min(512, nx), min(512, ny)
-    c, phi, rho = ora.initial_fields_rows(pr["ic"], nx, 0, 0, ty)
-    u = (c[:, :tx].copy(), phi[:, :tx].copy(), rho[:, :tx].copy())
-    for _ in range(args.warmup):
-        u = ora.step(m, *u, 1)
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        u = ora.step(m, *u, 1)
-    el = time.perf_counter() - t0
-    v = tx * ty * args.steps / el
+    members = PRESETS[cfg][2] * (ws if cfg == 3 else 1)
+    procs = max(1, min(os.cpu_count() or 1, members if cfg == 3 else 1))
+    cells, nsteps, wall, res = _oracle_ensemble(cfg, procs, args.warmup, args.steps)
+    v = cells * nsteps / wall
     cfgd = workload_config(cfg, ws)
-    cells = cfgd["members_per_gpu"] * nx * PRESETS[cfg][1] * ws
-    sample = (f"{tx}x{ty} fp64 tile of configs[{cfg - 1}] ({'member 0' if cfg == 3 else 'bottom tile'}), "
-              f"{args.steps} midpoint steps, single thread, {el:.2f} s; ms_per_step extrapolated to the "
-              f"{cells} cells of the {ws}-GPU workload")
+    sample = (f"{procs} concurrent single-threaded oracle processes ({_cpu_model()}, nproc {os.cpu_count()}), each "
+              f"{'one member (512x512 fp64) of' if cfg == 3 else 'a 512x512 fp64 tile of'} configs[{cfg - 1}]: "
+              f"{args.warmup} warm-up + {nsteps} timed midpoint steps in {wall:.2f} s (slowest process)")
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * cells / v,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded BASELINE.json configs recipe, DESIGN.md 5)", "config": cfgd,
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "steps": nsteps, "warmup": args.warmup, "ms_per_step": 1e3 * wall / nsteps,
+            "higher_is_better": True, "scaling": "strong" if cfg == 5 else "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (seeded BASELINE.json configs recipe, DESIGN.md 5)", "config": cfgd,
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": procs, "kind": "oracle", "cpu_model": _cpu_model(),
+                             "sample": sample},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def _timed_steps(sim, stream, steps, dist, dev):
+    """Device time (ms, max over ranks) of one pf_step(steps) call, CUDA events on the ctx stream,
+    barrier + synchronize on both sides."""
+    import torch
+    from paper_2312_05410_b200 import dist as D
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    sim.step(steps)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ms = e0.elapsed_time(e1)
+    return D.max_over_ranks(dist, ms, dev) if dist is not None else ms
+
+
+def _slab_leg(args, ws, rank, local, dist, dev):
+    """The y-slab path of configs[3] at the same N: weak-scaled 4096 x (4096 N) fp64,
+    4096 rows per GPU, the 2-row halo exchanged per stage over NCCL (pf_create_slab) and overlapped
+    with the interior update; timed like the main line (K steps after W warm-up, max over ranks).
+    At N > 1 rank 0 also times the single-GPU 4096^2 domain (the other ranks wait), so the weak-
+    scaling efficiency T(1)/T(N) of this run is reported next to the per-GPU rate."""
+    import torch
+    from paper_2312_05410_b200 import dist as D
+    from paper_2312_05410_b200 import pf
+    p = pf.pf_default_params(4).replace(device=local)
+    p = p.replace(ny=p.ny * ws)
+    mode = ("slab", rank, ws, D.nccl_uid(dist, dev)) if ws > 1 else "single"
+    with pf.Simulation(p, mode) as sim:
+        stream = torch.cuda.ExternalStream(pf.pf_stream(sim.ctx), device=dev)
+        sim.step(args.warmup)
+        ms = _timed_steps(sim, stream, args.steps, dist, dev)
+        cells_local = p.nx * sim.ny_local
+    ms1 = ms
+    if ws > 1:
+        if rank == 0:
+            p1 = pf.pf_default_params(4).replace(device=local)
+            with pf.Simulation(p1) as s1:
+                st1 = torch.cuda.ExternalStream(pf.pf_stream(s1.ctx), device=dev)
+                s1.step(args.warmup)
+                ms1 = _timed_steps(s1, st1, args.steps, None, dev)
+        if dist is not None:
+            dist.barrier()
+    if rank != 0:
+        return None
+    value = cells_local * ws * args.steps / (ms * 1e-3)
+    return {"workload": f"configs[3] weak: {p.nx} x {p.ny} fp64 in {ws} y-slab(s) of {cells_local // p.nx} rows, "
+                        + ("2-row halo per stage over NCCL (ncclSend/Recv on a comm stream) overlapped with the "
+                           "interior update" if ws > 1 else "single domain (no exchange at N = 1)"),
+            "value": value, "unit": UNIT, "per_gpu": value / ws, "ms_per_step": ms / args.steps,
+            "ms_per_step_1gpu": ms1 / args.steps, "weak_efficiency": ms1 / ms, "steps": args.steps,
+            "halo_bytes_per_stage_per_neighbour": 2 * 3 * (p.nx + 8) * 8 if ws > 1 else 0}
 
 
 def run_ours(args):
@@ -189,6 +297,9 @@ def run_ours(args):
 
     from paper_2312_05410_b200 import dist as D
     ws, rank, local = D.world()
+    if ws > 1:   # NCCL init lines (rank counts of every communicator) go to stderr for the driver
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     if args.gpus != ws and ws > 1:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={ws}")
     torch.cuda.set_device(local)
@@ -291,13 +402,16 @@ def run_ours(args):
                    "streams); copies amortised over the steps of one call; one warm-up call, median of 3 timed calls",
            "runs_ms": runs}
 
+    slab = _slab_leg(args, ws, rank, local, dist, dev) if (cfg == 3 and not args.no_slab) else None
+
     line = None
     if rank == 0:
         alg_per_cell_step = esz * (VALUES_STAGE1 + VALUES_STAGE2)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64" if p.precision == pf.PF_F64 else "f32",
+            "scaling": "strong" if cfg == 5 else "weak", "vs_baseline": None,
+            "dtype": "f64" if p.precision == pf.PF_F64 else "f32",
             "data": "synthetic (seeded BASELINE.json configs recipe, DESIGN.md 5)",
             "config": workload_config(cfg, ws),
             "hbm_gbs_effective": value * alg_per_cell_step / ws / 1e9,
@@ -312,7 +426,9 @@ def run_ours(args):
             "gpu_launches": launches,
             "clocks": clk.summary(),
         }
-        if not args.no_cpu_baseline:
+        if slab is not None:
+            line["slab"] = slab
+        if not args.no_cpu_baseline and ws == 1:
             line["cpu_baseline"] = _cpu_baseline()
         print(json.dumps(line), flush=True)
     sim.close()
@@ -330,6 +446,7 @@ def main():
     ap.add_argument("--config", type=int, default=3, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-slab", action="store_true", help="skip the configs[3] y-slab leg of the default run")
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")
