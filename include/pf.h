@@ -275,6 +275,14 @@ pf_status pf_s2_rel_l2(const double *comp_true, const double *comp_pred, int32_t
 /* Last error message of ctx (ctx == NULL: the calling thread's last create error). */
 const char *pf_last_error(const pf_ctx *ctx);
 
+/* Debug: the guard zones around every state buffer of a checked build (-DPF_GUARD_BYTES=N, built by
+ * __graft_entry__.build() as paper_2312_05410_b200/_variants/libpf_checked.so, with device-side
+ * bounds checks that trap).  *guard_bytes = N (0 in the production build, where *corrupted = 0);
+ * *corrupted = guard bytes that no longer hold their fill pattern, i.e. evidence of an out-of-bounds
+ * global write.  Synchronises the ctx stream.  Errors: PF_ERR_ARG (NULL), PF_ERR_CUDA.  (Stands in
+ * for compute-sanitizer memcheck, which the GPU pool does not allow.) */
+pf_status pf_debug_guards(pf_ctx *ctx, int64_t *guard_bytes, int64_t *corrupted);
+
 /* Release everything the ctx owns.  NULL-safe.  Slab mode: collective (NCCL teardown). */
 void pf_free(pf_ctx *ctx);
 

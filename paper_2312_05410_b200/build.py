@@ -122,7 +122,7 @@ def build(force: bool = False, verbose: bool = False, lib: str = None, build_dir
                 continue
             # -ffp-contract=off: the initial fields must be bitwise reproducible (R-16)
             jobs.append(["g++", "-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-fno-fast-math",
-                         "-Wall", *incs, "-c", src, "-o", obj])
+                         "-Wall", *os.environ.get("PF_CXX_EXTRA", "").split(), *incs, "-c", src, "-o", obj])
     from concurrent.futures import ThreadPoolExecutor
     with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as ex:
         list(ex.map(lambda cmd: _run(cmd, verbose), jobs))
@@ -133,6 +133,29 @@ def build(force: bool = False, verbose: bool = False, lib: str = None, build_dir
           "-L", os.path.join(CUDA, "lib64"), "-lcufft", "-Xlinker", f"-rpath,{os.path.join(CUDA, 'lib64')}"], verbose)
     os.replace(tmp, LIB)
     return LIB
+
+
+CHECKED_LIB = os.path.join(HERE, "_variants", "libpf_checked.so")
+
+
+def build_checked(force: bool = False, verbose: bool = False) -> str:
+    """The checked build: device-side bounds checks that trap (PF_DEVICE_CHECKS) and 64 KiB guard zones
+    around every state buffer (PF_GUARD_BYTES, read back by pf_debug_guards).  A stand-in for
+    compute-sanitizer memcheck, which the GPU pool does not allow."""
+    global BUILD, LIB
+    saved = (BUILD, LIB, os.environ.get("PF_NVCC_EXTRA"))
+    os.makedirs(os.path.dirname(CHECKED_LIB), exist_ok=True)
+    try:
+        os.environ["PF_NVCC_EXTRA"] = "-DPF_DEVICE_CHECKS -DPF_GUARD_BYTES=65536"
+        os.environ["PF_CXX_EXTRA"] = "-DPF_GUARD_BYTES=65536"
+        return build(force=force, verbose=verbose, lib=CHECKED_LIB)
+    finally:
+        BUILD, LIB = saved[0], saved[1]
+        if saved[2] is None:
+            os.environ.pop("PF_NVCC_EXTRA", None)
+        else:
+            os.environ["PF_NVCC_EXTRA"] = saved[2]
+        os.environ.pop("PF_CXX_EXTRA", None)
 
 
 if __name__ == "__main__":

@@ -63,6 +63,7 @@ struct BandGeo {
 // Store value v of field plane `pl` at (storage row sr, column x) with its periodic ghost copy.
 template <typename real>
 __device__ __forceinline__ void put(real *pl, const BandGeo &gg, int sr, int x, real v) {
+    PF_DCHECK(sr >= 0 && sr < gg.hmax + 8 && x >= 0 && x < gg.nx);
     pl[gg.u(sr, x)] = v;
     if (x < 2) pl[gg.u(sr, x + gg.nx)] = v;
     if (x >= gg.nx - 2) pl[gg.u(sr, x - gg.nx)] = v;
@@ -205,6 +206,7 @@ __global__ void __launch_bounds__(kBT, 1) band_kernel(Layout L, KC<real> k1, KC<
     for (int q = t; q < nown; q += kBT) {
         const int y = q / nx, x = q - y * nx;
         const int64_t o = L.at(y0 + y, x);
+        PF_DCHECK(y0 + y >= 0 && y0 + y < L.ny_loc && x >= 0 && x < nx && m < L.m0 + L.members);
         oc[o] = sc[gg.u(y + 4, x)];
         oc[L.fstride + o] = sp[gg.u(y + 4, x)];
         oc[2 * L.fstride + o] = sr[gg.u(y + 4, x)];

@@ -221,10 +221,21 @@ pf::Coef make_coef(const pf_params &p) {
     return K;
 }
 
+// Guard zones around every state buffer (checked builds, -DPF_GUARD_BYTES=N; 0 otherwise): filled
+// with kGuardByte at creation and compared by pf_debug_guards, they catch any out-of-bounds global
+// write of the stage kernels (compute-sanitizer is not available on the GPU pool).
+#ifndef PF_GUARD_BYTES
+#define PF_GUARD_BYTES 0
+#endif
+constexpr size_t kGuardBytes = PF_GUARD_BYTES;
+constexpr unsigned char kGuardByte = 0x5A;
+
 struct Slab {
     pf::Layout L{};
     void *U = nullptr;    // state u^n (also receives u^{n+1}: stage 2 updates in place)
     void *Us = nullptr;   // midpoint stage state u*
+    void *alloc[2] = {nullptr, nullptr};   // the two allocations (guard zone + buffer + guard zone)
+    size_t bytes = 0;                      // buffer bytes (without guards)
     double *partials = nullptr;
     double *diag = nullptr;   // members * kDiag
     pf::StreamPlan plan;      // streaming-kernel geometry and TMA tensor maps (plan.ok: in use)
@@ -346,8 +357,8 @@ void destroy(pf_ctx *c) {
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->gexec) cudaGraphExecDestroy(c->gexec);
     for (auto &s : c->slabs) {
-        cudaFree(s.U);
-        cudaFree(s.Us);
+        cudaFree(s.alloc[0]);
+        cudaFree(s.alloc[1]);
         cudaFree(s.partials);
         cudaFree(s.diag);
     }
@@ -683,10 +694,17 @@ pf_status create_common(const pf_params *p, int mode, int rank, int nranks, cons
         const size_t bytes = (size_t)sl.L.mstride * p->n_members * c->esz;
         c->slabs.push_back(sl);
         Slab &S = c->slabs.back();
-        if (cudaMalloc(&S.U, bytes) != cudaSuccess || cudaMalloc(&S.Us, bytes) != cudaSuccess) {
+        S.bytes = bytes;
+        if (cudaMalloc(&S.alloc[0], bytes + 2 * kGuardBytes) != cudaSuccess ||
+            cudaMalloc(&S.alloc[1], bytes + 2 * kGuardBytes) != cudaSuccess) {
             cudaGetLastError();
             c->err = fmt("cudaMalloc of 2 x %zu bytes failed", bytes);
             return fail(PF_ERR_NOMEM);
+        }
+        S.U = (char *)S.alloc[0] + kGuardBytes;
+        S.Us = (char *)S.alloc[1] + kGuardBytes;
+        for (int b = 0; b < 2; ++b) {
+            if (kGuardBytes) cudaMemsetAsync(S.alloc[b], kGuardByte, bytes + 2 * kGuardBytes, c->stream);
         }
         cudaMemsetAsync(S.U, 0, bytes, c->stream);
         cudaMemsetAsync(S.Us, 0, bytes, c->stream);
@@ -1376,6 +1394,24 @@ pf_status pf_stream(pf_ctx *c, void **stream) {
 }
 
 const char *pf_last_error(const pf_ctx *c) { return c ? c->err.c_str() : g_create_error.c_str(); }
+
+pf_status pf_debug_guards(pf_ctx *c, int64_t *guard_bytes, int64_t *corrupted) {
+    if (!c || !guard_bytes || !corrupted) return set_err(c, PF_ERR_ARG, "NULL argument");
+    cudaSetDevice(c->p.device);
+    CK(c, cudaStreamSynchronize(c->stream));
+    *guard_bytes = (int64_t)kGuardBytes;
+    *corrupted = 0;
+    if (kGuardBytes == 0) return PF_OK;
+    std::vector<unsigned char> h(kGuardBytes);
+    for (auto &S : c->slabs)
+        for (int b = 0; b < 2; ++b)
+            for (int side = 0; side < 2; ++side) {
+                const char *g = (const char *)S.alloc[b] + (side ? kGuardBytes + S.bytes : 0);
+                CK(c, cudaMemcpy(h.data(), g, kGuardBytes, cudaMemcpyDeviceToHost));
+                for (unsigned char v : h) *corrupted += v != kGuardByte;
+            }
+    return PF_OK;
+}
 
 void pf_free(pf_ctx *c) { destroy(c); }
 

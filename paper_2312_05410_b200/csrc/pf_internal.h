@@ -5,6 +5,24 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+// Device-side bounds checks of the checked build (-DPF_DEVICE_CHECKS, see pf_debug_guards in
+// include/pf.h): a failed check prints its location and traps (the launch fails loudly).
+#ifdef PF_DEVICE_CHECKS
+#include <cstdio>
+#define PF_DCHECK(cond)                                                                         \
+    do {                                                                                        \
+        if (!(cond)) {                                                                          \
+            printf("PF_DCHECK failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #cond, \
+                   (int)blockIdx.x, (int)threadIdx.x);                                          \
+            __trap();                                                                           \
+        }                                                                                       \
+    } while (0)
+#else
+#define PF_DCHECK(cond) \
+    do {                \
+    } while (0)
+#endif
+
 namespace pf {
 
 // Device layout of one state buffer:

@@ -168,6 +168,7 @@ __device__ __forceinline__ void tile_stage(const Layout &L, const KC<real> &k, c
                           sp[cy][cx - 1], sp[cy][cx + 1], sp[cy - 1][cx], sp[cy + 1][cx],
                           sr[y][x], sr[y][x - 1], sr[y][x + 1], sr[y - 1][x], sr[y + 1][x],
                           base[o], base[o + L.fstride], base[o + 2 * L.fstride], oc, op, orr);
+        PF_DCHECK(ly >= 0 && ly < L.ny_loc && gx >= 0 && gx < nx && m >= 0);
         out[o] = oc;
         out[o + L.fstride] = op;
         out[o + 2 * L.fstride] = orr;
@@ -567,6 +568,7 @@ size_t stream_smem_bytes(int bx, int R, int S, bool base) {
 // bottom; rho's top ghost rows hold the reservoir value and are never overwritten).
 template <typename real>
 __device__ __forceinline__ void store_row_ghosts(const Layout &L, real *b, int r, int x, real v) {
+    PF_DCHECK(r >= -2 && r < L.ny_loc + 2 && x >= 0 && x < L.nx);
     b[L.at(r, x)] = v;
     if (x < L.gx) b[L.at(r, x + L.nx)] = v;
     if (x >= L.nx - L.gx) b[L.at(r, x - L.nx)] = v;
@@ -702,6 +704,7 @@ __global__ void __launch_bounds__(32 * NCW + 32, MINB) pair_kernel(
 #pragma unroll kPairUnroll
         for (int j = 0; j < nsl; ++j) {
             const real *cur = slots + sidx * rg.slot_elems + ci;
+            PF_DCHECK(sidx >= 0 && sidx < S && ci >= 1 && (R - 1) * bx + 2 * plane + ci + 2 < rg.in_elems + 64);
             mbar_wait(&full[sidx], par);
 #pragma unroll
             for (int u = 0; u < R; ++u) {
@@ -763,6 +766,7 @@ __global__ void __launch_bounds__(32 * NCW + 32, MINB) pair_kernel(
                 if (store && i >= 4 && i < n) {
                     const int r = sg.ya - 4 + i;          // local row k-2
                     const bool edge = xedge | (L.y0 + r <= 1) | (L.y0 + r >= L.ny - 2);
+                    PF_DCHECK(sg.m >= L.m0 && sg.m < L.m0 + L.members && r >= L.r0 && r < L.r1 && x >= 0 && x + 1 < nx);
                     if (!edge) {
                         real *o = ob + L.at(r, x);
                         st2(o, ocx, ocy);
@@ -1016,6 +1020,7 @@ __global__ void __launch_bounds__(32 * (2 * NCW + 1), MINB) ws_kernel(
                 const int r = q - 2;
                 if (store && r >= sg.ya && r < sg.yb) {
                     const bool edge = xedge | (L.y0 + r <= 1) | (L.y0 + r >= L.ny - 2);
+                    PF_DCHECK(sg.m >= L.m0 && sg.m < L.m0 + L.members && r >= L.r0 && r < L.r1 && x >= 0 && x + 1 < nx);
                     if (!edge) {
                         real *o = ob + L.at(r, x);
                         st2(o, ocx, ocy);

@@ -110,6 +110,7 @@ def lib():
             "pf_profile": (C.c_int, [_ctx_p, i32]),
             "pf_profile_read": (C.c_int, [_ctx_p, _D]),
             "pf_stream": (C.c_int, [_ctx_p, C.POINTER(C.c_void_p)]),
+            "pf_debug_guards": (C.c_int, [_ctx_p, C.POINTER(i64), C.POINTER(i64)]),
             "pf_last_error": (C.c_char_p, [_ctx_p]),
             "pf_free": (None, [_ctx_p]),
         }
@@ -316,6 +317,13 @@ def pf_stream(ctx) -> int:
     s = C.c_void_p()
     _check(lib().pf_stream(ctx, C.byref(s)), ctx)
     return s.value or 0
+
+
+def pf_debug_guards(ctx):
+    """(guard bytes per zone, corrupted guard bytes) of a checked build (0, 0 in production)."""
+    g, bad = C.c_int64(), C.c_int64()
+    _check(lib().pf_debug_guards(ctx, C.byref(g), C.byref(bad)), ctx)
+    return g.value, bad.value
 
 
 def pf_free(ctx):

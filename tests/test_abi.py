@@ -143,3 +143,20 @@ def test_inflow_row_bitwise(L, ora):
         want = [ora.inflow(8, m, st, 40, i, 0.9, 0.2) for i in range(40)]
         assert row.tolist() == want
     assert np.all(pf.pf_inflow_row(p.replace(noise_rho=0.0), 1, 1) == 0.9)
+
+
+def test_checked_build_has_device_checks():
+    """The checked build (build.build_checked, run by __graft_entry__.build) carries the device-side
+    bounds checks: many more trap instructions than the production library (SASS via cuobjdump)."""
+    import os
+    import shutil
+    import subprocess
+    from paper_2312_05410_b200 import build
+    if not os.path.exists(build.CHECKED_LIB) or shutil.which("cuobjdump") is None:
+        pytest.skip("checked build not built here (run __graft_entry__.build())")
+
+    def traps(path):
+        out = subprocess.run(["cuobjdump", "-sass", path], capture_output=True, text=True).stdout
+        return out.count("BPT.TRAP")
+
+    assert traps(build.CHECKED_LIB) > 10 * max(1, traps(build.LIB))

@@ -1,6 +1,8 @@
-"""Small runs of each kernel path for compute-sanitizer (memcheck / racecheck / synccheck):
+"""Small runs of each kernel path, for the checked build (PF_LIB=paper_2312_05410_b200/_variants/
+libpf_checked.so: device bounds checks that trap + guard zones around the state buffers, checked
+here through pf_debug_guards) or for compute-sanitizer where a pool allows it:
 
-    compute-sanitizer --tool racecheck python tools/sanitize_case.py pair
+    PF_LIB=$PWD/paper_2312_05410_b200/_variants/libpf_checked.so python tools/sanitize_case.py pair
 
 cases: band (configs[0] 64^2, the band cluster kernel), persistent (64^2, cooperative tile kernel),
 pair (512 x 72, 2 members: the TMA-ring stage kernels), loopback (512 x 72 in 2 y-slabs with the
@@ -34,8 +36,10 @@ def main(case):
         s.step(n)
         u = s.fields(0)
         d = s.diagnostics(0)
+        guard, bad = pf.pf_debug_guards(s.ctx)
     assert all(np.all(np.isfinite(f)) for f in u) and d[4] == 0
-    print(f"{case}: ok ({n} steps)")
+    assert bad == 0, f"{bad} guard bytes overwritten"
+    print(f"{case}: ok ({n} steps, guard zones of {guard} B intact)")
 
 
 if __name__ == "__main__":
