@@ -205,6 +205,24 @@ pf_status pf_run_host(pf_ctx *ctx, int64_t n, const double *c_in, const double *
  * Errors: PF_ERR_ARG, PF_ERR_NOMEM, PF_ERR_STATE, and pf_step's errors. */
 pf_status pf_trajectory(pf_ctx *ctx, int32_t n_snapshots, int64_t steps_between, double *out, double *times);
 
+/* The same trajectory streamed to a FILE (SURVEY 8(f) NEXT-1 "adds I/O and a trajectory file";
+ * P:354-355 dataset of trajectories x (50, 256, 256)): snapshot s of every member is copied to a
+ * pinned host buffer while the next steps run and a writer thread appends it to `path`.
+ * Layout (little-endian):
+ *   header, 96 bytes: char magic[8] = "PFTRAJ01"; uint32 header_bytes (= 96 + 64 members),
+ *     uint32 version = 1; int32 nx, ny_global, y0, ny_rows, members, member_offset, n_snapshots,
+ *     dtype (0 = float64, 1 = float32); int64 steps_between, step0 (pf_info steps before
+ *     snapshot 0); float64 dt, t0, dx, rho_in;
+ *   members records of 8 float64: global member id, v_x, v_y, M_A^bulk, M_B^bulk, M_A^surf,
+ *     M_B^surf, 0 (R-10, R-15, R-21, R-23);
+ *   data: [n_snapshots][members][ny_rows][nx] of dtype, the composite composition c[phi > 1/2]
+ *     (identical to pf_trajectory's values; float32 = rounded);
+ *   footer: float64 t of every snapshot.
+ * Synchronous.  Errors: PF_ERR_ARG (bad arguments, I/O failure: message names the path),
+ * PF_ERR_NOMEM, PF_ERR_STATE and pf_step's errors (the file is then incomplete). */
+pf_status pf_trajectory_file(pf_ctx *ctx, const char *path, int32_t n_snapshots, int64_t steps_between,
+                             int32_t dtype);
+
 /* Copy member `member` (0..n_members-1, or -1 = all members, stacked) to host buffers of
  * ny_local*nx doubles each (times n_members for -1).  fp32 fields are widened to double.
  * Errors: PF_ERR_ARG, PF_ERR_CUDA. */

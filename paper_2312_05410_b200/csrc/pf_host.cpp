@@ -16,6 +16,9 @@
 #include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
+#include <condition_variable>
+#include <mutex>
+#include <thread>
 #include <utility>
 #include <cmath>
 #include <cstdarg>
@@ -1244,6 +1247,166 @@ pf_status pf_trajectory(pf_ctx *c, int32_t n_snapshots, int64_t steps_between, d
     }
     CK(c, cudaStreamSynchronize(c->d2h));
     return PF_OK;
+}
+
+// Trajectory file (NEXT-1 I/O; layout in include/pf.h): snapshot s of every member goes device ->
+// pinned host buffer (d2h stream) while the next steps run; a writer thread appends it to the file
+// while the GPU keeps stepping (pf_step blocks the calling thread).  Two host buffers.
+pf_status pf_trajectory_file(pf_ctx *c, const char *path, int32_t n_snapshots, int64_t steps_between,
+                             int32_t dtype) {
+    if (!c) return set_err(nullptr, PF_ERR_ARG, "ctx is NULL");
+    if (!path || n_snapshots < 1 || steps_between < 0 || (dtype != 0 && dtype != 1))
+        return set_err(c, PF_ERR_ARG, "bad trajectory-file arguments");
+    if (c->blown) return set_err(c, PF_ERR_STATE, "state blew up; call pf_set_fields first");
+    Nvtx nv("pf trajectory file");
+    cudaSetDevice(c->p.device);
+    const int M = c->p.n_members;
+    const size_t per = (size_t)c->ny_host * c->p.nx, n = per * M;
+    FILE *f = std::fopen(path, "wb");
+    if (!f) return set_err(c, PF_ERR_ARG, fmt("cannot open %s for writing", path));
+    // header (little-endian, 96 bytes) + per-member records
+    struct Header {
+        char magic[8];
+        uint32_t header_bytes, version;
+        int32_t nx, ny_global, y0, ny_rows, members, member_offset, n_snapshots, dtype;
+        int64_t steps_between, step0;
+        double dt, t0, dx, rho_in;
+    } h{};
+    static_assert(sizeof(Header) == 96, "trajectory header layout");
+    std::memcpy(h.magic, "PFTRAJ01", 8);
+    h.header_bytes = (uint32_t)(sizeof(Header) + (size_t)M * 8 * sizeof(double));
+    h.version = 1;
+    h.nx = c->p.nx;
+    h.ny_global = c->p.ny;
+    h.y0 = c->y_host0;
+    h.ny_rows = c->ny_host;
+    h.members = M;
+    h.member_offset = c->p.member_offset;
+    h.n_snapshots = n_snapshots;
+    h.dtype = dtype;
+    h.steps_between = steps_between;
+    h.step0 = c->steps;
+    h.dt = c->p.dt;
+    h.t0 = c->t;
+    h.dx = c->p.dx;
+    h.rho_in = c->p.rho_in;
+    bool ok = std::fwrite(&h, sizeof h, 1, f) == 1;
+    for (int m = 0; m < M && ok; ++m) {   // global id, v_x, v_y, M_A^b, M_B^b, M_A^s, M_B^s, 0
+        double r[8] = {0};
+        const int64_t gm = (int64_t)c->p.member_offset + m;
+        r[0] = (double)gm;
+        member_velocity(c->p, gm, r[1], r[2]);
+        member_mobility(c->p, gm, r + 3);
+        ok = std::fwrite(r, sizeof r, 1, f) == 1;
+    }
+    if (!ok) {
+        std::fclose(f);
+        return set_err(c, PF_ERR_ARG, fmt("write to %s failed", path));
+    }
+    // device snapshot buffers (shared with pf_trajectory), pinned host buffers, events
+    if (c->snap_n < n) {
+        for (int b = 0; b < 2; ++b) {
+            cudaFree(c->snap[b]);
+            c->snap[b] = nullptr;
+        }
+        c->snap_n = 0;
+        for (int b = 0; b < 2; ++b)
+            if (cudaMalloc((void **)&c->snap[b], n * sizeof(double)) != cudaSuccess) {
+                cudaGetLastError();
+                std::fclose(f);
+                return set_err(c, PF_ERR_NOMEM, "cudaMalloc of snapshot buffers failed");
+            }
+        c->snap_n = n;
+    }
+    if (!c->d2h) {
+        CK(c, cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking));
+        CK(c, cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking));
+    }
+    for (int b = 0; b < 2; ++b)
+        if (!c->ev_snap[b]) {
+            CK(c, cudaEventCreateWithFlags(&c->ev_snap[b], cudaEventDisableTiming));
+            CK(c, cudaEventCreateWithFlags(&c->ev_copied[b], cudaEventDisableTiming));
+        }
+    double *hb[2] = {nullptr, nullptr};
+    for (int b = 0; b < 2; ++b)
+        if (cudaMallocHost((void **)&hb[b], n * sizeof(double)) != cudaSuccess) {
+            cudaGetLastError();
+            cudaFreeHost(hb[0]);
+            std::fclose(f);
+            return set_err(c, PF_ERR_NOMEM, "cudaMallocHost of the trajectory buffers failed");
+        }
+    // writer thread: snapshot s in host buffer s & 1, written once its copy event completed
+    std::mutex mu;
+    std::condition_variable cv;
+    int queued = 0, written = 0;
+    bool werr = false;
+    std::vector<float> tmp(dtype == 1 ? n : 0);
+    std::thread writer([&] {
+        for (int s = 0; s < n_snapshots; ++s) {
+            {
+                std::unique_lock<std::mutex> lk(mu);
+                cv.wait(lk, [&] { return queued > s || werr; });
+                if (werr) return;
+            }
+            const int b = s & 1;
+            bool good = cudaEventSynchronize(c->ev_copied[b]) == cudaSuccess;
+            if (good && dtype == 0) {
+                good = std::fwrite(hb[b], sizeof(double), n, f) == n;
+            } else if (good) {
+                for (size_t i = 0; i < n; ++i) tmp[i] = (float)hb[b][i];
+                good = std::fwrite(tmp.data(), sizeof(float), n, f) == n;
+            }
+            std::lock_guard<std::mutex> lk(mu);
+            if (!good) werr = true;
+            written = s + 1;
+            cv.notify_all();
+            if (werr) return;
+        }
+    });
+    std::vector<double> times((size_t)n_snapshots);
+    pf_status st = PF_OK;
+    for (int s = 0; s < n_snapshots && st == PF_OK; ++s) {
+        if (s > 0 && (st = pf_step(c, steps_between)) != PF_OK) break;
+        const int b = s & 1;
+        {   // host buffer b is free once snapshot s - 2 is on disk
+            std::unique_lock<std::mutex> lk(mu);
+            cv.wait(lk, [&] { return written >= s - 1 || werr; });
+            if (werr) { st = set_err(c, PF_ERR_ARG, fmt("write to %s failed", path)); break; }
+        }
+        if (s >= 2) {
+            cudaError_t e = cudaStreamWaitEvent(c->stream, c->ev_copied[b], 0);
+            if (e != cudaSuccess) { st = set_err(c, PF_ERR_CUDA, cudaGetErrorString(e)); break; }
+        }
+        for (auto &S : c->slabs) {
+            cudaError_t e = pf::launch_composite(c->p.precision, S.L, S.U, c->snap[b], (int64_t)per,
+                                                 S.L.y0 - c->y_host0, c->stream);
+            if (e != cudaSuccess) { st = set_err(c, PF_ERR_CUDA, cudaGetErrorString(e)); break; }
+            c->launches += 1;
+        }
+        if (st != PF_OK) break;
+        cudaEventRecord(c->ev_snap[b], c->stream);
+        cudaStreamWaitEvent(c->d2h, c->ev_snap[b], 0);
+        cudaMemcpyAsync(hb[b], c->snap[b], n * sizeof(double), cudaMemcpyDeviceToHost, c->d2h);
+        cudaEventRecord(c->ev_copied[b], c->d2h);
+        times[(size_t)s] = c->t;
+        std::lock_guard<std::mutex> lk(mu);
+        queued = s + 1;
+        cv.notify_all();
+    }
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        if (st != PF_OK) werr = true;
+        cv.notify_all();
+    }
+    writer.join();
+    if (st == PF_OK && werr) st = set_err(c, PF_ERR_ARG, fmt("write to %s failed", path));
+    if (st == PF_OK && std::fwrite(times.data(), sizeof(double), times.size(), f) != times.size())
+        st = set_err(c, PF_ERR_ARG, fmt("write to %s failed", path));
+    cudaStreamSynchronize(c->d2h);
+    cudaFreeHost(hb[0]);
+    cudaFreeHost(hb[1]);
+    if (std::fclose(f) != 0 && st == PF_OK) st = set_err(c, PF_ERR_ARG, fmt("closing %s failed", path));
+    return st;
 }
 
 pf_status pf_get_fields(pf_ctx *c, int32_t member, double *fc, double *fp, double *fr) {

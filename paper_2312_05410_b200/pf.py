@@ -96,6 +96,7 @@ def lib():
             "pf_halo_plan": (C.c_int, [i32, i32, i32, C.POINTER(i32)]),
             "pf_run_host": (C.c_int, [_ctx_p, i64, _D, _D, _D, _D, _D, _D, i32]),
             "pf_trajectory": (C.c_int, [_ctx_p, i32, i64, _D, _D]),
+            "pf_trajectory_file": (C.c_int, [_ctx_p, C.c_char_p, i32, i64, i32]),
             "pf_s2_nbins": (i32, [i32, i32]),
             "pf_s2": (C.c_int, [_D, i32, i32, i32, C.c_double, _D, _D, i32]),
             "pf_s2_rel_l2": (C.c_int, [_D, _D, i32, i32, i32, C.c_double, _D]),
@@ -243,6 +244,38 @@ def pf_run_host(ctx, n, c_in, phi_in, rho_in, c_out, phi_out, rho_out, chunks: i
 def pf_trajectory(ctx, n_snapshots: int, steps_between: int, out, times=None):
     """out: [members][n_snapshots][ny_local][nx] fp64 (numpy or pinned torch); times: [n_snapshots]."""
     _check(lib().pf_trajectory(ctx, int(n_snapshots), int(steps_between), _hptr(out), _hptr(times)), ctx)
+
+
+def pf_trajectory_file(ctx, path: str, n_snapshots: int, steps_between: int, dtype: str = "float64"):
+    """Stream a trajectory to `path` (layout: include/pf.h pf_trajectory_file; read it back with
+    read_trajectory)."""
+    code = {"float64": 0, "float32": 1}[dtype]
+    _check(lib().pf_trajectory_file(ctx, os.fsencode(path), n_snapshots, steps_between, code), ctx)
+
+
+_TRAJ_HEADER = np.dtype([("magic", "S8"), ("header_bytes", "<u4"), ("version", "<u4"), ("nx", "<i4"),
+                         ("ny_global", "<i4"), ("y0", "<i4"), ("ny_rows", "<i4"), ("members", "<i4"),
+                         ("member_offset", "<i4"), ("n_snapshots", "<i4"), ("dtype", "<i4"),
+                         ("steps_between", "<i8"), ("step0", "<i8"), ("dt", "<f8"), ("t0", "<f8"),
+                         ("dx", "<f8"), ("rho_in", "<f8")])
+
+
+def read_trajectory(path: str):
+    """(header dict, member records [members, 8], snapshots as a read-only memmap [n_snapshots,
+    members, ny_rows, nx], times [n_snapshots]) of a pf_trajectory_file file.  A dataset view
+    [member][snapshot] is ``snaps.transpose(1, 0, 2, 3)``."""
+    hdr = np.fromfile(path, dtype=_TRAJ_HEADER, count=1)[0]
+    if hdr["magic"] != b"PFTRAJ01" or hdr["version"] != 1:
+        raise ValueError(f"{path}: not a PFTRAJ01 v1 file")
+    h = {k: (hdr[k].item() if k != "magic" else hdr[k].decode()) for k in _TRAJ_HEADER.names}
+    M, S, ny, nx = h["members"], h["n_snapshots"], h["ny_rows"], h["nx"]
+    recs = np.fromfile(path, dtype="<f8", count=8 * M, offset=_TRAJ_HEADER.itemsize).reshape(M, 8)
+    dt = np.dtype("<f8") if h["dtype"] == 0 else np.dtype("<f4")
+    snaps = np.memmap(path, dtype=dt, mode="r", offset=h["header_bytes"], shape=(S, M, ny, nx))
+    times = np.fromfile(path, dtype="<f8", count=S, offset=h["header_bytes"] + S * M * ny * nx * dt.itemsize)
+    if times.size != S:
+        raise ValueError(f"{path}: truncated (no time footer)")
+    return h, recs, snaps, times
 
 
 def pf_s2(comp, threshold: float = 0.5, maps: bool = True, radial: bool = True):

@@ -160,3 +160,26 @@ def test_checked_build_has_device_checks():
         return out.count("BPT.TRAP")
 
     assert traps(build.CHECKED_LIB) > 10 * max(1, traps(build.LIB))
+
+
+def test_read_trajectory_parses_the_documented_layout(tmp_path):
+    """read_trajectory against a file assembled here from include/pf.h's layout description."""
+    M, S, ny, nx = 3, 4, 5, 8
+    hdr = np.zeros(1, dtype=pf._TRAJ_HEADER)
+    hdr["magic"] = b"PFTRAJ01"
+    hdr["header_bytes"] = 96 + 64 * M
+    hdr["version"] = 1
+    hdr["nx"], hdr["ny_global"], hdr["y0"], hdr["ny_rows"] = nx, ny, 0, ny
+    hdr["members"], hdr["member_offset"], hdr["n_snapshots"], hdr["dtype"] = M, 7, S, 1
+    hdr["steps_between"], hdr["step0"], hdr["dt"], hdr["t0"] = 10, 20, 1e-3, 0.02
+    assert hdr.itemsize == 96
+    recs = np.arange(8 * M, dtype="<f8").reshape(M, 8)
+    data = np.random.default_rng(1).random((S, M, ny, nx)).astype("<f4")
+    times = 0.02 + 0.01 * np.arange(S)
+    path = tmp_path / "t.pftraj"
+    with open(path, "wb") as f:
+        f.write(hdr.tobytes()); f.write(recs.tobytes()); f.write(data.tobytes()); f.write(times.tobytes())
+    h, r, snaps, t = pf.read_trajectory(str(path))
+    assert h["members"] == M and h["member_offset"] == 7 and h["dtype"] == 1 and h["magic"] == "PFTRAJ01"
+    assert np.array_equal(r, recs) and np.array_equal(np.asarray(snaps), data) and np.array_equal(t, times)
+    assert snaps.transpose(1, 0, 2, 3).shape == (M, S, ny, nx)

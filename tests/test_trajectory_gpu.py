@@ -87,3 +87,34 @@ def test_trajectory_single_snapshot_takes_no_steps():
         assert s.info()[0] == 0
         c, phi, _ = s.fields(-1)
         assert np.array_equal(out[:, 0], _composite(c, phi))
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_trajectory_file_equals_trajectory(tmp_path, dtype):
+    """pf_trajectory_file (the streamed trajectory file of NEXT-1) holds exactly pf_trajectory's
+    snapshots (float32: the rounded values), the member records, the snapshot times, and leaves the
+    ctx at the same step."""
+    p = _params()
+    S, K = 7, 5
+    with pf.Simulation(p) as s:
+        s.step(2)
+        ref = np.empty((p.n_members, S, p.ny, p.nx))
+        tref = np.zeros(S)
+        pf.pf_trajectory(s.ctx, S, K, ref, tref)
+    path = str(tmp_path / f"traj_{dtype}.pftraj")
+    with pf.Simulation(p) as s:
+        s.step(2)
+        pf.pf_trajectory_file(s.ctx, path, S, K, dtype)
+        assert s.info()[0] == 2 + (S - 1) * K
+    h, recs, snaps, times = pf.read_trajectory(path)
+    assert (h["members"], h["n_snapshots"], h["ny_rows"], h["nx"], h["step0"], h["steps_between"]) == \
+        (p.n_members, S, p.ny, p.nx, 2, K)
+    want = ref.transpose(1, 0, 2, 3)
+    if dtype == "float64":
+        assert np.array_equal(np.asarray(snaps), want)
+    else:
+        assert np.array_equal(np.asarray(snaps), want.astype(np.float32))
+    assert np.array_equal(times, tref)
+    for m in range(p.n_members):
+        assert recs[m, 0] == m
+        assert (recs[m, 1], recs[m, 2]) == pf.pf_member_velocity(p, m)

@@ -42,6 +42,17 @@ def main():
         t0 = time.perf_counter()
         pf.pf_trajectory(s.ctx, a.snapshots, a.every, out)
         ms_traj = 1e3 * (time.perf_counter() - t0)
+        # the same trajectory streamed to a file (float32, the dataset's storage), writer thread
+        # overlapping the stepping
+        import tempfile
+        path = os.path.join(tempfile.mkdtemp(), "dataset.pftraj")
+        t0 = time.perf_counter()
+        pf.pf_trajectory_file(s.ctx, path, a.snapshots, a.every, "float32")
+        ms_file = 1e3 * (time.perf_counter() - t0)
+        file_bytes = os.path.getsize(path)
+        os.remove(path)
+    res.update({"ms_trajectory_file_f32": ms_file, "file_bytes": file_bytes,
+                "trajectories_per_s_file": p.n_members / (ms_file * 1e-3)})
     res.update({"ms_plain": ms_plain, "ms_trajectory": ms_traj,
                 "cell_updates_per_s_plain": cells * steps / (ms_plain * 1e-3),
                 "cell_updates_per_s_trajectory": cells * steps / (ms_traj * 1e-3),
