@@ -223,32 +223,6 @@ cudaError_t upload_exp_table_band() {
     return e;
 }
 
-template <typename real>
-KC<real> make_kc_band(const Coef &K, double coef) {
-    KC<real> k;
-    k.half_inv_dx2 = (real)K.half_inv_dx2;
-    k.inv_2dx = (real)K.inv_2dx;
-    k.m_kc_dx2 = (real)(-K.kc_dx2);
-    k.m_kp_dx2 = (real)(-K.kp_dx2);
-    k.W_c = (real)K.W_c;
-    k.W2c = (real)K.W2c;
-    k.W2p = (real)K.W2p;
-    k.two_inv_sigma = (real)(2.0 * K.inv_sigma);
-    k.MBb = (real)K.MBb;
-    k.dMb = (real)K.dMb;
-    k.MBs = (real)K.MBs;
-    k.dMs = (real)K.dMs;
-    k.mob = K.mob;
-    k.fe = K.fe;
-    k.omega = (real)K.omega;
-    k.temp = (real)K.temp;
-    k.Mp_dx2 = (real)K.Mp_dx2;
-    k.Dr_dx2 = (real)K.Dr_dx2;
-    k.rho_in = (real)K.rho_in;
-    k.coef = (real)coef;
-    k.coefc = (real)(coef * K.half_inv_dx2);
-    return k;
-}
 
 template <typename real, int MOB, int FE, int MAXC>
 cudaError_t launch_band_c(const Layout &L, const BandPlan &B, const KC<real> &k1, const KC<real> &k2, void *U,
@@ -279,7 +253,7 @@ cudaError_t launch_band_c(const Layout &L, const BandPlan &B, const KC<real> &k1
 template <typename real, int MOB, int FE>
 cudaError_t launch_band_t(const Layout &L, const BandPlan &B, const Coef &K, void *U, const void *vel, double dt,
                           int64_t nsteps, cudaStream_t s) {
-    const KC<real> k1 = make_kc_band<real>(K, 0.5 * dt), k2 = make_kc_band<real>(K, dt);
+    const KC<real> k1 = make_kc<real>(K, 0.5 * dt), k2 = make_kc<real>(K, dt);
     const int64_t cells = (int64_t)B.hmax * L.nx;
     if (cells <= kBT) return launch_band_c<real, MOB, FE, 1>(L, B, k1, k2, U, vel, nsteps, s);
     if (cells <= 2 * kBT) return launch_band_c<real, MOB, FE, 2>(L, B, k1, k2, U, vel, nsteps, s);

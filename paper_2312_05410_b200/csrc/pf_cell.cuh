@@ -20,6 +20,10 @@ struct KC {                    // coefficients folded into the compute precision
     int fe;                    // 0 polynomial composition well (R-2), 1 regular solution (R-28)
     int mob;                   // 0: shared, M_A = M_B (h(c) drops out); 1: shared, M_A != M_B;
                                // 2: per member (record array, R-23)
+    // exp_neg's constants as launch parameters rather than immediates: the compiler keeps them in
+    // uniform registers (fp64 operands of DFMA / DADD) instead of re-materialising each 64-bit
+    // immediate with two integer moves per use in the hot loop
+    double ex_l2e64, ex_magic, ex_ln2hi, ex_ln2lo, ex_c6, ex_c24, ex_c120, ex_min;
 };
 
 // Per-member record (device array, storage precision, kMembStride values per member, pf_internal.h):
@@ -51,26 +55,64 @@ __device__ __forceinline__ float fma_(float a, float b, float c) { return __fmaf
 // 1e-307 are irrelevant to M_c).  Max error ~2 ulp.
 __constant__ double kExp2Tab[64];                        // 2^(j/64), filled by the host
 
-__device__ __forceinline__ double exp_neg(double x, const double *tab) {
-    const double kMagic = 6755399441055744.0;                 // 1.5 * 2^52
-    const double k64Log2e = 92.332482616893656;              // 64 / ln 2
-    const double kLn2Hi64 = 6.93147180369123816490e-01 / 64.0, kLn2Lo64 = 1.90821492927058770002e-10 / 64.0;
-    x = x > -708.0 ? x : -708.0;
-    const double kd = fma_(x, k64Log2e, kMagic);            // m = round(64 x / ln 2) in the low word
+// Constants (host side, set_exp_constants): kMagic = 1.5 * 2^52, 64 / ln 2, ln2 hi / 64 and lo / 64
+// (negated), 1/6, 1/24, 1/120 and the clamp -708.
+template <typename K>
+__device__ __forceinline__ double exp_neg(double x, const double *tab, const K &k) {
+    x = x > k.ex_min ? x : k.ex_min;
+    const double kd = fma_(x, k.ex_l2e64, k.ex_magic);      // m = round(64 x / ln 2) in the low word
     const int m = __double2loint(kd);
-    const double nd = sub_(kd, kMagic);
-    double r = fma_(nd, -kLn2Hi64, x);
-    r = fma_(nd, -kLn2Lo64, r);
+    const double nd = sub_(kd, k.ex_magic);
+    double r = fma_(nd, k.ex_ln2hi, x);
+    r = fma_(nd, k.ex_ln2lo, r);
     // P(r) = (1 + r) + r^2 ((1/2 + r/6) + r^2 (1/24 + r/120))
     const double r2 = mul_(r, r);
     const double a = add_(r, 1.0);
-    const double b = fma_(r, 1.0 / 6.0, 0.5);
-    const double c = fma_(r, 1.0 / 120.0, 1.0 / 24.0);
+    const double b = fma_(r, k.ex_c6, 0.5);
+    const double c = fma_(r, k.ex_c120, k.ex_c24);
     double p = fma_(r2, fma_(r2, c, b), a);
     p = mul_(p, tab[m & 63]);
     return __hiloint2double(__double2hiint(p) + ((m >> 6) << 20), __double2loint(p));
 }
-__device__ __forceinline__ float exp_neg(float x, const double *) { return expf(x); }
+template <typename K>
+__device__ __forceinline__ float exp_neg(float x, const double *, const K &) { return expf(x); }
+
+// The per-launch coefficient struct of a stage with factor coef (dt/2 or dt), from the ctx's
+// coefficients (host side, shared by every kernel translation unit).
+template <typename real>
+inline KC<real> make_kc(const Coef &K, double coef) {
+    KC<real> k;
+    k.half_inv_dx2 = (real)K.half_inv_dx2;
+    k.inv_2dx = (real)K.inv_2dx;
+    k.m_kc_dx2 = (real)(-K.kc_dx2);
+    k.m_kp_dx2 = (real)(-K.kp_dx2);
+    k.W_c = (real)K.W_c;
+    k.W2c = (real)K.W2c;
+    k.W2p = (real)K.W2p;
+    k.two_inv_sigma = (real)(2.0 * K.inv_sigma);
+    k.MBb = (real)K.MBb;
+    k.dMb = (real)K.dMb;
+    k.MBs = (real)K.MBs;
+    k.dMs = (real)K.dMs;
+    k.mob = K.mob;
+    k.fe = K.fe;
+    k.omega = (real)K.omega;
+    k.temp = (real)K.temp;
+    k.Mp_dx2 = (real)K.Mp_dx2;
+    k.Dr_dx2 = (real)K.Dr_dx2;
+    k.rho_in = (real)K.rho_in;
+    k.coef = (real)coef;
+    k.coefc = (real)(coef * K.half_inv_dx2);
+    k.ex_l2e64 = 92.332482616893656;                            // 64 / ln 2
+    k.ex_magic = 6755399441055744.0;                            // 1.5 * 2^52
+    k.ex_ln2hi = -(6.93147180369123816490e-01 / 64.0);          // ln 2 split as in fdlibm
+    k.ex_ln2lo = -(1.90821492927058770002e-10 / 64.0);
+    k.ex_c6 = 1.0 / 6.0;
+    k.ex_c24 = 1.0 / 24.0;
+    k.ex_c120 = 1.0 / 120.0;
+    k.ex_min = -708.0;
+    return k;
+}
 
 // Block-wide copy of the exp table into shared memory (call before the first exp_neg).
 __device__ __forceinline__ void load_exp_table(double *tab) {
@@ -125,7 +167,7 @@ __device__ __forceinline__ void constitutive(const KC<real> &k, const Mob<real> 
     // M_c = M_bulk + e (M_surf_mix - M_bulk)                         (R-5, R-6)
     const real pp = mul_(mul_(p, p), fma_(p, m2, real(3)));           // 1/4 (2 - phit)(1 + phit)^2
     const real q = mul_(sub_(p, real(0.5)), k.two_inv_sigma);          // phit / sigma_surf
-    const real e = exp_neg(mul_(-q, q), etab);
+    const real e = exp_neg(mul_(-q, q), etab, k);
     real mb, ms;
     if (MOB != 0) {
         const real ch = clamp01(c);                                   // clamp(c, 0, 1)

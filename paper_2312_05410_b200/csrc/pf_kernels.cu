@@ -617,6 +617,9 @@ constexpr bool kSinglesShfl = PF_SINGLES_SHFL;
 // elected by a shared-memory counter, with 15-16 compute warps per SM instead of 12-16: 5-8%
 // slower on configs[2] stage 1 even with the schedule tabulated; the refill work sits on a compute
 // warp's critical path.  DESIGN.md 7.)
+// (Measured alternative, round 2: stage-1 rows staged in shared memory and written by cp.async.bulk
+// per field -- 35% slower than the STG.128 stores below; the stores were not the bottleneck, the
+// compute warps' dependency latency is.)
 template <typename real, int NCW, int R, int S, bool BASE, int MOB, int FE, int MINB>
 __global__ void __launch_bounds__(32 * NCW + 32, MINB) pair_kernel(
     Layout L, KC<real> k, const __grid_constant__ CUtensorMap mapIn, const __grid_constant__ CUtensorMap mapBase,
@@ -1049,32 +1052,6 @@ __global__ void __launch_bounds__(32 * (2 * NCW + 1), MINB) ws_kernel(
     }
 }
 
-template <typename real>
-KC<real> make_kc(const Coef &K, double coef) {
-    KC<real> k;
-    k.half_inv_dx2 = (real)K.half_inv_dx2;
-    k.inv_2dx = (real)K.inv_2dx;
-    k.m_kc_dx2 = (real)(-K.kc_dx2);
-    k.m_kp_dx2 = (real)(-K.kp_dx2);
-    k.W_c = (real)K.W_c;
-    k.W2c = (real)K.W2c;
-    k.W2p = (real)K.W2p;
-    k.two_inv_sigma = (real)(2.0 * K.inv_sigma);
-    k.MBb = (real)K.MBb;
-    k.dMb = (real)K.dMb;
-    k.MBs = (real)K.MBs;
-    k.dMs = (real)K.dMs;
-    k.mob = K.mob;
-    k.fe = K.fe;
-    k.omega = (real)K.omega;
-    k.temp = (real)K.temp;
-    k.Mp_dx2 = (real)K.Mp_dx2;
-    k.Dr_dx2 = (real)K.Dr_dx2;
-    k.rho_in = (real)K.rho_in;
-    k.coef = (real)coef;
-    k.coefc = (real)(coef * K.half_inv_dx2);
-    return k;
-}
 
 // Pair kernel ring geometry per precision, stage and producer mode: about 128 registers per
 // thread, so MINB = wslots / (warps per block) blocks fill the register file with 15-16 compute
