@@ -9,7 +9,7 @@ Every function follows the paper's definition in its order and notation (P = PAP
   conv        P:383-387  conv(u)_{k',i,j} = sum_k sum_m sum_n u_{k,i+m,j+n} w_{k,k',m,n}
               read as a 3x3 'same' cross-correlation with one zero cell of padding (R-29)
   group_norm  P:389-405  mu_g, sigma_g^2 over (C/G channels x W x H), (u - mu)/sqrt(sigma^2 + eps),
-              then gamma_k u_hat + beta_k (R-30: G = 4 groups, eps = 1e-5)
+              then gamma_k u_hat + beta_k (R-30: G = min(8, C) = 8 groups, eps = 1e-5)
   gelu        P:408-411  0.5 u (1 + tanh(sqrt(2/pi) (u + 0.044715 u^3)))
   conv_block  P:412-415  GELU(GN(conv(u)))
   down        P:417-422  2x2 max pooling, stride 2
@@ -25,7 +25,7 @@ from __future__ import annotations
 
 import numpy as np
 
-GROUPS = 4       # R-30
+GROUPS = 8       # R-30: G = min(8, C) (SPEC), 8 for every width used (16 .. 128)
 EPS = 1e-5       # R-30
 
 
@@ -82,8 +82,10 @@ def time_basis(dt, P):
 
 
 def groups_of(c):
-    """Group count of a C-channel GroupNorm: GROUPS, or 1 for the 1-channel output (R-30)."""
-    return GROUPS if c % GROUPS == 0 else 1
+    """Group count of a C-channel GroupNorm (R-30, SPEC): G = min(8, C), or G = C when C is not a
+    multiple of it (the 1-channel output: G = 1)."""
+    g = min(GROUPS, c)
+    return g if c % g == 0 else c
 
 
 def encode(hist, P):

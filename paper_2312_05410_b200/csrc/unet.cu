@@ -43,7 +43,7 @@ typedef __nv_bfloat16 bf16;
 
 constexpr int kBM = 128;      // pixels per CTA (UMMA M)
 constexpr int kBasis = 128;   // time-basis width
-constexpr int kGroups = 4;    // GroupNorm groups (R-30)
+constexpr int kGroups = 8;    // GroupNorm groups: min(8, C) = 8 for every width 16..128 (R-30, SPEC)
 constexpr double kEps = 1e-5; // GroupNorm epsilon (R-30)
 
 // ------------------------------------------------------------------------------------------------

@@ -139,10 +139,15 @@ def _dptr(a):
     return a.ctypes.data_as(_D)
 
 
-def _hptr(a):
-    """Host pointer of a numpy array or of a pinned CPU torch tensor (float64, contiguous)."""
+def _hptr(a, need: int = 0):
+    """Host pointer of a numpy array or of a pinned CPU torch tensor (float64, contiguous) holding at
+    least `need` elements (the library writes / reads that many: a smaller buffer would be
+    accessed out of bounds, so it is rejected here)."""
     if a is None:
         return None
+    n = a.size if isinstance(a, np.ndarray) else (a.numel() if hasattr(a, "numel") else None)
+    if need and n is not None and n < need:
+        raise ValueError(f"host buffer holds {n} elements, the call needs {need}")
     if isinstance(a, np.ndarray):
         return _dptr(a)
     # torch tensor (pinned host memory for the e2e bench)
@@ -228,22 +233,34 @@ def pf_step(ctx, n: int):
     _check(lib().pf_step(ctx, int(n)), ctx)
 
 
+def _field_elems(ctx, member):
+    """Elements of one field buffer of pf_get/set_fields: local rows x nx (x members for -1)."""
+    nx, _, mem = pf_shape(ctx)
+    rows = pf_info(ctx)[3]
+    return rows * nx * (mem if member == -1 else 1)
+
+
 def pf_get_fields(ctx, member, c, phi, rho):
-    _check(lib().pf_get_fields(ctx, member, _hptr(c), _hptr(phi), _hptr(rho)), ctx)
+    n = _field_elems(ctx, member)
+    _check(lib().pf_get_fields(ctx, member, _hptr(c, n), _hptr(phi, n), _hptr(rho, n)), ctx)
 
 
 def pf_set_fields(ctx, member, c, phi, rho):
-    _check(lib().pf_set_fields(ctx, member, _hptr(c), _hptr(phi), _hptr(rho)), ctx)
+    n = _field_elems(ctx, member)
+    _check(lib().pf_set_fields(ctx, member, _hptr(c, n), _hptr(phi, n), _hptr(rho, n)), ctx)
 
 
 def pf_run_host(ctx, n, c_in, phi_in, rho_in, c_out, phi_out, rho_out, chunks: int = 4):
-    _check(lib().pf_run_host(ctx, int(n), _hptr(c_in), _hptr(phi_in), _hptr(rho_in), _hptr(c_out), _hptr(phi_out),
-                             _hptr(rho_out), int(chunks)), ctx)
+    k = _field_elems(ctx, -1)
+    _check(lib().pf_run_host(ctx, int(n), _hptr(c_in, k), _hptr(phi_in, k), _hptr(rho_in, k), _hptr(c_out, k),
+                             _hptr(phi_out, k), _hptr(rho_out, k), int(chunks)), ctx)
 
 
 def pf_trajectory(ctx, n_snapshots: int, steps_between: int, out, times=None):
     """out: [members][n_snapshots][ny_local][nx] fp64 (numpy or pinned torch); times: [n_snapshots]."""
-    _check(lib().pf_trajectory(ctx, int(n_snapshots), int(steps_between), _hptr(out), _hptr(times)), ctx)
+    k = _field_elems(ctx, -1) * int(n_snapshots)
+    _check(lib().pf_trajectory(ctx, int(n_snapshots), int(steps_between), _hptr(out, k),
+                               _hptr(times, int(n_snapshots))), ctx)
 
 
 def pf_trajectory_file(ctx, path: str, n_snapshots: int, steps_between: int, dtype: str = "float64"):

@@ -100,8 +100,20 @@ class UNet:
         b = _f32(blob)
         _check(lib().un_set_weights(self.ctx, b.ctypes.data_as(_F), b.size), self.ctx)
 
+    def _check_hist(self, hist):
+        """The library copies B * lb * H * W floats from the pointer: a wrongly shaped array would be
+        read out of bounds, so the shape is checked here."""
+        want = (self.p.lb, self.p.height, self.p.width)
+        if np.ndim(hist) != 4 or tuple(np.shape(hist)[1:]) != want:
+            raise ValueError(f"hist must have shape (B, {want[0]}, {want[1]}, {want[2]}), got {np.shape(hist)}")
+        if not 1 <= np.shape(hist)[0] <= self.p.max_batch:
+            raise ValueError(f"batch {np.shape(hist)[0]} outside [1, max_batch = {self.p.max_batch}]")
+
     def forward(self, hist, dt):
-        """hist [B, lb, H, W], dt [B] (host) -> [B, H, W] float32 (host)."""
+        """hist [B, lb, H, W], dt [B] or scalar (host) -> [B, H, W] float32 (host)."""
+        self._check_hist(hist)
+        if np.ndim(dt) not in (0, 1) or (np.ndim(dt) == 1 and np.shape(dt)[0] != np.shape(hist)[0]):
+            raise ValueError(f"dt must be a scalar or have shape ({np.shape(hist)[0]},), got {np.shape(dt)}")
         h, d = _f32(hist), _f32(np.broadcast_to(dt, (hist.shape[0],)))
         out = np.empty((h.shape[0], self.p.height, self.p.width), dtype=np.float32)
         _check(lib().un_forward(self.ctx, h.shape[0], h.ctypes.data_as(_F), d.ctypes.data_as(_F),
@@ -113,6 +125,7 @@ class UNet:
                                        C.c_void_p(out_ptr)), self.ctx)
 
     def rollout(self, hist, lf, n_leaps):
+        self._check_hist(hist)
         h = _f32(hist)
         out = np.empty((h.shape[0], n_leaps * lf, self.p.height, self.p.width), dtype=np.float32)
         _check(lib().un_rollout(self.ctx, h.shape[0], h.ctypes.data_as(_F), lf, n_leaps,

@@ -118,7 +118,7 @@ def _torch_forward(hist, dt, P):
     F = torch.nn.functional
     T = {k: torch.from_numpy(np.ascontiguousarray(v)) for k, v in P.items()}
 
-    def cb(x, name, groups=4, act=True):
+    def cb(x, name, groups=8, act=True):   # R-30: min(8, C) = 8 for these widths
         w = T["w_" + name].permute(0, 3, 1, 2)          # [co, ci, 3, 3]
         y = F.group_norm(F.conv2d(x, w, padding=1), groups, T["g_" + name], T["b_" + name], eps=1e-5)
         return F.gelu(y, approximate="tanh") if act else y
