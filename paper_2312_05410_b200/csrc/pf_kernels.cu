@@ -440,177 +440,7 @@ __global__ void inflow_kernel(Layout L, double rho_in, double sigma, uint64_t se
     }
 }
 
-// ========================================================================================
-// Streaming kernel
-__device__ __forceinline__ uint32_t smem_u32(const void *p) {
-    return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void fence_mbar_init() {
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-// try_wait with a suspend-time hint: a waiting warp is suspended until the phase completes (or the
-// hint elapses) instead of re-issuing the try_wait / branch loop, which took ~40% of the stage
-// kernels' issue slots.
-constexpr uint32_t kSuspendNs = 1000000;
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
-        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-        "r"(parity), "r"(kSuspendNs)
-        : "memory");
-}
-// 3D TMA tile load: box at (x, y, z) of the tensor map -> shared memory, completion on bar.
-__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, int x, int y, int z, uint64_t *bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
-        "[%5];" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
-        : "memory");
-}
-// Programmatic dependent launch: a stage launch may be scheduled while the previous launch on the
-// stream drains; griddep_wait() returns once that launch has completed and its writes are visible.
-__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-
-__device__ __forceinline__ void prefetch_tmap(const CUtensorMap *map) {
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
-}
-
-// Work schedule shared by the producer and the compute warps.  Grouped mode (G > 0): blocks come
-// in groups of `strips`; block b works on strip b % strips of the row range [T g/G, T (g+1)/G) of
-// the concatenated (member, row) space (T = members * ny_loc rows, g = b / strips), so the blocks
-// of a group stream the same rows at the same time.  Ungrouped mode (G == 0): block b owns the
-// row range [R b/B, R (b+1)/B) of the concatenated (member, strip, row) space.
-struct Seg {
-    int m, x0, Wp, ya, yb;
-};
-struct Sched {
-    int64_t lo, hi;
-    int strip;        // grouped: fixed strip of this block; -1 ungrouped
-};
-__device__ __forceinline__ Sched make_sched(const Layout &L, int Wo, int G) {
-    const int strips = (L.nx + Wo - 1) / Wo;
-    const int nyl = L.r1 - L.r0;        // rows of this launch's row window
-    Sched sc;
-    if (G > 0) {
-        const int g = blockIdx.x / strips;
-        sc.strip = blockIdx.x - g * strips;
-        const int64_t T = (int64_t)L.members * nyl;
-        sc.lo = T * g / G;
-        sc.hi = T * (g + 1) / G;
-    } else {
-        const int64_t R = (int64_t)L.members * strips * nyl;
-        sc.strip = -1;
-        sc.lo = R * blockIdx.x / gridDim.x;
-        sc.hi = R * (blockIdx.x + 1) / gridDim.x;
-    }
-    return sc;
-}
-__device__ __forceinline__ bool next_seg(const Layout &L, int Wo, const Sched &sc, int64_t &pos, Seg &sg) {
-    if (pos >= sc.hi) return false;
-    const int nyl = L.r1 - L.r0, strips = (L.nx + Wo - 1) / Wo;
-    const int64_t col = pos / nyl;      // grouped: member; ungrouped: member * strips + strip
-    const int la = (int)(pos - col * nyl);
-    const int lb = (int)min((int64_t)nyl, (int64_t)la + (sc.hi - pos));
-    pos += lb - la;
-    sg.ya = L.r0 + la;
-    sg.yb = L.r0 + lb;
-    int sidx;
-    if (sc.strip >= 0) {
-        sg.m = (int)col;
-        sidx = sc.strip;
-    } else {
-        sg.m = (int)(col / strips);
-        sidx = (int)(col - (int64_t)sg.m * strips);
-    }
-    sg.m += L.m0;                       // buffer index of the member
-    sg.x0 = sidx * Wo;
-    sg.Wp = min(Wo, L.nx - sg.x0);
-    return true;
-}
-
-// Shared-memory geometry of the ring (runtime box width bx).
-template <typename real>
-struct Ring {
-    int bx;            // box width in elements (Wo + 2 HL)
-    int in_elems;      // one input box: 3 fields x R rows x bx (rounded to 128 B)
-    int slot_elems;    // input box (+ base box for stage 2)
-    __host__ __device__ static int round128(int elems) {
-        const int b = elems * (int)sizeof(real);
-        return ((b + 127) / 128 * 128) / (int)sizeof(real);
-    }
-    __host__ __device__ Ring(int bx_, int R, bool base) : bx(bx_) {
-        in_elems = round128(3 * R * bx);
-        slot_elems = in_elems * (base ? 2 : 1);
-    }
-};
-
-template <typename real>
-size_t stream_smem_bytes(int bx, int R, int S, bool base) {
-    Ring<real> rg(bx, R, base);
-    return 128 + (size_t)S * rg.slot_elems * sizeof(real) + 64 * sizeof(real) /* read slack */ +
-           (size_t)S * 16 + 64 * 8;   // full, empty barriers; exp table
-}
-
-// Store one output value (field f, local row r, column x) and its ghost-frame copies: periodic
-// x ghost columns and, at the global y boundaries, the mirror ghost rows (c, phi; rho at the
-// bottom; rho's top ghost rows hold the reservoir value and are never overwritten).
-template <typename real>
-__device__ __forceinline__ void store_row_ghosts(const Layout &L, real *b, int r, int x, real v) {
-    PF_DCHECK(r >= -2 && r < L.ny_loc + 2 && x >= 0 && x < L.nx);
-    b[L.at(r, x)] = v;
-    if (x < L.gx) b[L.at(r, x + L.nx)] = v;
-    if (x >= L.nx - L.gx) b[L.at(r, x - L.nx)] = v;
-}
-template <typename real>
-__device__ __forceinline__ void store_with_ghosts(const Layout &L, real *b, int f, int r, int x, real v) {
-    const int g = L.y0 + r;
-    store_row_ghosts(L, b, r, x, v);
-    if (g <= 1) store_row_ghosts(L, b, -1 - r, x, v);                                // y0 == 0 here
-    else if (g >= L.ny - 2 && f != 2) store_row_ghosts(L, b, 2 * L.ny_loc - 1 - r, x, v);   // top slab
-}
-
-// ----------------------------------------------------------------------------------------
-// Pair kernel (default performance path).  Same producer / ring / schedule as stream_kernel, but
-// every compute lane owns TWO adjacent columns, so a warp covers 64 columns (60 outputs plus one
-// halo column on each side).  Per row and pair of cells a lane issues 128-bit shared loads, 10
-// shuffles and 128-bit global stores -- half the per-cell shuffle, load, barrier, loop and store
-// instructions of the one-column layout -- and the two columns give the scheduler independent
-// fp64 chains.  The per-cell arithmetic is the same pf_cell.cuh code, so results are bitwise
-// identical to the tile and stream kernels.
-template <typename real> struct Vec2;
-template <> struct Vec2<double> { using T = double2; };
-template <> struct Vec2<float> { using T = float2; };
-
-template <typename real>
-__device__ __forceinline__ typename Vec2<real>::T ld2(const real *p) {
-    return *reinterpret_cast<const typename Vec2<real>::T *>(p);
-}
-template <typename real>
-__device__ __forceinline__ void st2(real *p, real x, real y) {
-    typename Vec2<real>::T v;
-    v.x = x;
-    v.y = y;
-    *reinterpret_cast<typename Vec2<real>::T *>(p) = v;
-}
-
-constexpr int kPairCols = 60;   // output columns per compute warp
-constexpr int kPairHalo = 4;    // box columns left of the strip (and right of it)
-#ifndef PF_SINGLES_SHFL
-#define PF_SINGLES_SHFL 1
-#endif
-constexpr bool kSinglesShfl = PF_SINGLES_SHFL;
+#include "pf_stream.cuh"
 
 // A dedicated producer warp issues the TMA boxes and waits on per-slot "empty" mbarriers.  (Measured
 // alternative, round 2: no producer warp -- the last compute warp to release a slot refills it,
@@ -1295,7 +1125,7 @@ bool stream_eligible(const Layout &L) { return L.nx >= 16 && L.nx % 4 == 0 && L.
 
 cudaError_t make_stream_plan(int precision, const Layout &L, void *U, void *Us, StreamPlan &P) {
     P = StreamPlan();
-    if (L.path == 1 || !stream_eligible(L)) return cudaSuccess;
+    if (L.path == 1 || !stream_eligible(L)) return cudaSuccess;   // paths 0, 3, 5: the pair plan
     // pair kernel: strips of Wo <= 240 columns (box Wo + 8 <= 256 elements), Wo a multiple of 4
     // (16 B rows for fp32 too), split nx evenly; 60 output columns per compute warp
     int strips = (L.nx + 239) / 240;
