@@ -954,6 +954,8 @@ using namespace un;
 struct un_ctx {
     un_params p{};
     cudaStream_t st = nullptr;
+    cudaStream_t st2 = nullptr;                 // side stream: the time MLP overlaps the input pack and enc1
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int cin[kLayers], cout[kLayers], cin_pad[kLayers], cout_pad[kLayers];
     bf16 *w[kLayers] = {};
     float *gam[kLayers] = {}, *bet[kLayers] = {};
@@ -1071,15 +1073,21 @@ pf_status forward(un_ctx *c, int B, const float *hist, const float *dt, float *o
         f1 = take_event(c);
         UCK(c, cudaEventRecord(f0, c->st));
     }
+    // the time MLP (depends on dt only) runs on the side stream, overlapping the input pack and the
+    // first convolution; the first conditioned layer (enc1's GN apply) joins it
+    UCK(c, cudaEventRecord(c->ev_fork, c->st));
+    UCK(c, cudaStreamWaitEvent(c->st2, c->ev_fork, 0));
+    time_mlp_kernel<<<B, kBasis, 0, c->st2>>>(c->mlp, c->wl, dt, c->cond, c->ctot);
+    UCK(c, cudaEventRecord(c->ev_join, c->st2));
     pack_input_kernel<<<grid_for((int64_t)B * HW, 256), 256, 0, c->st>>>(hist, c->in0, (int64_t)B * HW, (int)HW,
                                                                          c->p.lb);
-    time_mlp_kernel<<<B, kBasis, 0, c->st>>>(c->mlp, c->wl, dt, c->cond, c->ctot);
     c->launches += 2;
     pf_status s;
     // encoder + conditioning: z_p unconditioned (pooling input), z_p (.) s_p
     // into the first half of the level's concatenation buffer
-    if ((s = conv_layer(c, kEnc1, c->in0, B)) || (s = apply_pool_layer(c, kEnc1, B, 0, c->cat[0], 2 * C1, 0, c->pin[0])))
-        return s;
+    if ((s = conv_layer(c, kEnc1, c->in0, B))) return s;
+    UCK(c, cudaStreamWaitEvent(c->st, c->ev_join, 0));
+    if ((s = apply_pool_layer(c, kEnc1, B, 0, c->cat[0], 2 * C1, 0, c->pin[0]))) return s;
     if ((s = conv_layer(c, kEnc2, c->pin[0], B)) || (s = apply_pool_layer(c, kEnc2, B, 1, c->cat[1], 2 * C2, 0, c->pin[1])))
         return s;
     if ((s = conv_layer(c, kEnc3, c->pin[1], B)) || (s = apply_pool_layer(c, kEnc3, B, 2, c->cat[2], 2 * C3, 0, c->pin[2])))
@@ -1189,8 +1197,11 @@ pf_status un_create(const un_params *p, un_ctx **out) {
         un_free(c);
         return s;
     };
-    if (cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking) != cudaSuccess) {
-        c->err = "cudaStreamCreate failed";
+    if (cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+        c->err = "cudaStreamCreate / cudaEventCreate failed";
         return bad(PF_ERR_CUDA);
     }
     const int64_t B = p->max_batch, H = p->height, W = p->width;
@@ -1412,15 +1423,25 @@ pf_status un_hybrid(un_ctx *c, pf_ctx *dns, int32_t n_dns, int64_t steps_between
         return fail(c, PF_ERR_ARG, "need n_dns >= lb, lf >= lb, n_leaps >= 0");
     const size_t hw = (size_t)nx * ny;
     const int lb = c->p.lb, total = n_dns + n_leaps * lf;
-    std::vector<double> traj((size_t)members * n_dns * hw);
+    // the DNS snapshots land in pinned memory (asynchronous copies overlapping the steps; pageable
+    // copies made the DNS segment's time vary by 2x between runs)
+    double *traj = nullptr;
+    if (cudaMallocHost((void **)&traj, (size_t)members * n_dns * hw * sizeof(double)) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(c, PF_ERR_NOMEM, "cudaMallocHost of the DNS snapshots failed");
+    }
+    struct FreeHost {
+        double *p;
+        ~FreeHost() { cudaFreeHost(p); }
+    } traj_guard{traj};
     auto t0 = std::chrono::steady_clock::now();
-    pf_status s = pf_trajectory(dns, n_dns, steps_between, traj.data(), nullptr);
+    pf_status s = pf_trajectory(dns, n_dns, steps_between, traj, nullptr);
     auto t1 = std::chrono::steady_clock::now();
     if (s != PF_OK) return fail(c, s, std::string("DNS segment failed: ") + pf_last_error(dns));
     std::vector<float> hist((size_t)members * lb * hw);
     for (int b = 0; b < members; ++b)
         for (int q = 0; q < n_dns; ++q) {
-            const double *src = traj.data() + ((size_t)b * n_dns + q) * hw;
+            const double *src = traj + ((size_t)b * n_dns + q) * hw;
             float *dst = out + ((size_t)b * total + q) * hw;
             for (size_t i = 0; i < hw; ++i) dst[i] = (float)src[i];
             if (q >= n_dns - lb) std::memcpy(hist.data() + ((size_t)b * lb + (q - (n_dns - lb))) * hw, dst, hw * 4);
@@ -1536,6 +1557,9 @@ void un_free(un_ctx *c) {
         cudaEventDestroy(r.second.second);
     }
     if (c->st) cudaStreamDestroy(c->st);
+    if (c->st2) cudaStreamDestroy(c->st2);
+    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    if (c->ev_join) cudaEventDestroy(c->ev_join);
     delete c;
 }
 

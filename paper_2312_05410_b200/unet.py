@@ -136,7 +136,13 @@ class UNet:
         """DNS (pf ctx of `sim`) for n_dns composite snapshots, then the U-Net rollout; returns
         (snapshots [members, n_dns + n_leaps*lf, H, W], (dns_seconds, surrogate_seconds))."""
         nx, ny, mem = pf.pf_shape(sim.ctx)
-        out = np.zeros((mem, n_dns + n_leaps * lf, ny, nx), dtype=np.float32)   # pre-faulted pages
+        shape = (mem, n_dns + n_leaps * lf, ny, nx)
+        try:   # pinned host memory: the predictions are copied asynchronously at full PCIe rate
+            import torch
+            self._pinned = torch.empty(shape, dtype=torch.float32, pin_memory=True)
+            out = self._pinned.numpy()
+        except Exception:
+            out = np.zeros(shape, dtype=np.float32)   # pre-faulted pageable pages
         sec = (C.c_double * 2)()
         _check(lib().un_hybrid(self.ctx, sim.ctx, n_dns, steps_between, lf, n_leaps, out.ctypes.data_as(_F), sec),
                self.ctx)
