@@ -50,6 +50,19 @@ def test_tile_stream_pair_paths_bitwise(nx, ny, members):
         assert _eq(a[m], c[m]), m
 
 
+@pytest.mark.parametrize("nx,ny,members,extra", [(64, 64, 1, {}), (512, 72, 2, {}), (1000, 24, 1, {}),
+                                                  (260, 40, 2, dict(mob_lo=0.5, mob_hi=1.0)),
+                                                  (128, 40, 2, dict(fe_model=1, omega=2.2, temp_rs=0.45, dt=4e-4))])
+def test_fp32_pair_kernel_bitwise(nx, ny, members, extra):
+    """fp32 storage (configs[4]'s precision): the pair kernel computes a lane's two cells as one
+    packed pair (FADD2 / FMUL2 / FFMA2) and must still give the scalar tile kernel's bits."""
+    p = _base(nx, ny, n_members=members, rate_lo=0.5, rate_hi=2.0, precision=pf.PF_F32, **extra)
+    a = _run(p.replace(kernel_path=1), 20)
+    c = _run(p.replace(kernel_path=3), 20)
+    for m in range(members):
+        assert _eq(a[m], c[m]), m
+
+
 @pytest.mark.parametrize("shift", [64, 5, 1])
 def test_x_translation_equivariance(shift):
     nx, ny = 256, 40
