@@ -238,19 +238,41 @@ __device__ __forceinline__ void conv_tile_out(uint32_t tacc, int64_t t, int64_t 
                     part[(p * NG + g0 + g) * 2 + 1] = gq[g];
                 }
         } else {
+            // warp sums of the 2 G0N values by a reduce-scatter butterfly: at each of the first
+            // log2(NV) steps a lane keeps half of its values (chosen by its lane bit) and adds the
+            // partner's copy of that half, so a step costs NV / 2 shuffles instead of NV; then full
+            // xor steps.  Lane l ends with the sum of value (l >> (5 - m)) & (NV - 1), fixed order
+            // (deterministic).  5x fewer fp64 shuffles than one xor-reduction per value at G = 8.
+            constexpr int NV = 2 * G0N;
+            constexpr int M = NV >= 32 ? 5 : (NV >= 16 ? 4 : (NV >= 8 ? 3 : (NV >= 4 ? 2 : (NV >= 2 ? 1 : 0))));
+            double v[NV];
 #pragma unroll
-            for (int g = 0; g < G0N; ++g)
-                for (int off = 16; off > 0; off >>= 1) {
-                    gs[g] += __shfl_xor_sync(0xffffffffu, gs[g], off);
-                    gq[g] += __shfl_xor_sync(0xffffffffu, gq[g], off);
+            for (int g = 0; g < G0N; ++g) {
+                v[2 * g] = gs[g];
+                v[2 * g + 1] = gq[g];
+            }
+#pragma unroll
+            for (int st = 0; st < 5; ++st) {
+                const int o = 16 >> st;
+                if (st < M) {
+                    const int half = NV >> (st + 1);
+                    const bool upper = (lane & o) != 0;
+#pragma unroll
+                    for (int j = 0; j < half; ++j) {
+                        const double send = upper ? v[j] : v[j + half];
+                        const double keep = upper ? v[j + half] : v[j];
+                        v[j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+                    }
+                } else {
+                    v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
                 }
+            }
             const int64_t wid = t * 4 + lq;   // global 32-pixel unit
-            if (lane == 0 && wid * 32 < npix)
-#pragma unroll
-                for (int g = 0; g < G0N; ++g) {
-                    part[(wid * NG + g0 + g) * 2] = gs[g];
-                    part[(wid * NG + g0 + g) * 2 + 1] = gq[g];
-                }
+            constexpr int SH = 5 - M;
+            if ((lane & ((1 << SH) - 1)) == 0 && wid * 32 < npix) {
+                const int idx = (lane >> SH) & (NV - 1);   // = 2 g + (0: sum, 1: sum of squares)
+                part[(wid * NG + g0 + (idx >> 1)) * 2 + (idx & 1)] = v[0];
+            }
         }
     }
 }
@@ -369,9 +391,12 @@ __global__ void __launch_bounds__(kWsThreads) conv3x3_kernel(const bf16 *__restr
                 tc_fence_after();
                 const uint32_t a0 = sbase + s * C::stage, b0 = a0 + C::a_bytes;
                 const uint32_t acc = tmem + (uint32_t)(b * N);
+                // descriptors advanced by adding (byte offset >> 4) to the start-address field
+                // (every address stays below 2^18, so the 14-bit field never carries)
+                const uint64_t da = sdesc(a0, C::lbo_a, 128), db = sdesc(b0, C::lbo_b, 128);
 #pragma unroll
                 for (int k = 0; k < kKC / 2; ++k)
-                    umma(acc, sdesc(a0 + 2 * k * C::lbo_a, C::lbo_a, 128), sdesc(b0 + 2 * k * C::lbo_b, C::lbo_b, 128),
+                    umma(acc, da + (uint64_t)((2 * k * C::lbo_a) >> 4), db + (uint64_t)((2 * k * C::lbo_b) >> 4),
                          idesc_bf16(N), (kb | k) ? 1u : 0u);
                 umma_commit(&empty[s]);
                 if (kb == nkb - 1) umma_commit(&accf[b]);
@@ -558,15 +583,22 @@ __global__ void __launch_bounds__(kWsThreads) conv3x3_rows_kernel(const bf16 *__
                 while (nt < T && tile_of(k, nt) < tiles) ++nt;
                 const uint32_t a0 = sbase + s * a_bytes;
                 const uint32_t acc0 = tmem + (uint32_t)(b * C::T * N);
+                // the single issuing thread was the bottleneck of the N = 16 layers (a descriptor
+                // built from scratch per MMA): descriptors are now advanced by adding (byte offset
+                // >> 4) to the 14-bit start-address field (addresses stay below 2^18: no carry)
+                const uint64_t dA0 = sdesc(a0, kRowLbo, 128), dB0 = sdesc(bbase, C::lbo_b, 128);
+                const uint64_t stepB = (uint64_t)((2 * C::lbo_b) >> 4), stepA = (uint64_t)((2 * kRowLbo) >> 4);
+                const uint64_t tileA = (uint64_t)(a_tile >> 4);
+                uint64_t bd = dB0;
+#pragma unroll
                 for (int tap = 0; tap < 9; ++tap) {
                     const int ky = tap / 3, kx = tap - 3 * ky;
-                    const uint32_t arow = a0 + (uint32_t)ky * rreg + kx * 16;
-                    for (int c = 0; c < cq; c += 2) {
-                        const uint64_t bd = sdesc(bbase + (tap * cq + c) * C::lbo_b, C::lbo_b, 128);
+                    uint64_t ad = dA0 + (uint64_t)((ky * rreg + kx * 16) >> 4);
+                    for (int c = 0; c < cq; c += 2, ad += stepA, bd += stepB) {
                         const uint32_t accf_ = (tap | c) ? 1u : 0u;
-                        for (int i = 0; i < nt; ++i)
-                            umma(acc0 + (uint32_t)(i * N), sdesc(arow + i * a_tile + c * kRowLbo, kRowLbo, 128), bd,
-                                 idesc_bf16(N), accf_);
+                        uint64_t adi = ad;
+                        for (int i = 0; i < nt; ++i, adi += tileA)
+                            umma(acc0 + (uint32_t)(i * N), adi, bd, idesc_bf16(N), accf_);
                     }
                 }
                 umma_commit(&empty[s]);
