@@ -25,8 +25,21 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
 // try_wait with a suspend-time hint: a waiting warp is suspended until the phase completes (or the
 // hint elapses) instead of re-issuing the try_wait / branch loop, which took ~40% of the stage
 // kernels' issue slots.
-constexpr uint32_t kSuspendNs = 1000000;
+#ifndef PF_SUSPEND_NS
+#define PF_SUSPEND_NS 1000000
+#endif
+constexpr uint32_t kSuspendNs = PF_SUSPEND_NS;
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    if (kSuspendNs == 0) {   // plain try_wait loop (A/B knob)
+        asm volatile(
+            "{\n\t.reg .pred p;\n"
+            "WAIT_%=:\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+            "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+            "r"(parity)
+            : "memory");
+        return;
+    }
     asm volatile(
         "{\n\t.reg .pred p;\n"
         "WAIT_%=:\n\t"
