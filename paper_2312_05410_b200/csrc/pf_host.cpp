@@ -248,6 +248,10 @@ enum Mode { kSingle = 0, kLoopback = 1, kNccl = 2 };
 
 // Grids up to this many cells (all members) use the persistent small-grid kernel by default.
 constexpr int64_t kPersistentCells = 1 << 19;   // crossover ~2^20 (tools/small_grid_sweep.py)
+// ... and up to this many the band kernel (one cluster per member) where its bands fit: it wins at
+// 64^2 (1.00 vs 0.82 G), the one-barrier-per-step persistent kernel from 128^2 (3.15 vs 2.03 G;
+// profiles/r2/small_grid_sweep_r2zf.jsonl)
+constexpr int64_t kBandCells = 1 << 13;
 
 }  // namespace
 
@@ -732,7 +736,7 @@ pf_status create_common(const pf_params *p, int mode, int rank, int nranks, cons
         // persistent tile kernel (grid barriers)
         const int64_t cells = (int64_t)p->n_members * p->nx * p->ny;
         const bool small = mode == kSingle && !(p->noise_rho > 0.0);
-        if (small && (p->kernel_path == 6 || (p->kernel_path == 0 && cells <= kPersistentCells)))
+        if (small && (p->kernel_path == 6 || (p->kernel_path == 0 && cells <= kBandCells)))
             c->band = pf::make_band_plan(p->precision, c->slabs[0].L, c->bplan);
         if (p->kernel_path == 6 && !c->band) {
             c->err = "kernel_path 6: the band kernel needs a single-domain ctx without inflow noise, ny >= 2 and a band "

@@ -176,6 +176,144 @@ __device__ __forceinline__ void tile_stage(const Layout &L, const KC<real> &k, c
     __syncthreads();   // the tile's shared memory may be refilled next
 }
 
+// Both midpoint stages of one step on a tile, for the small-grid persistent kernel (one grid
+// barrier per STEP instead of per stage): the tile loads u^n with a 4-cell halo (ghost rules by
+// index), computes u* on the tile plus a 2-cell halo (the halo redundantly, bit for bit what the
+// neighbouring tiles compute), fills u*'s out-of-domain halo rows with the ghost rules of u*'s own
+// ghost frame (mirror rows; rho: bottom mirror, top reservoir -- computing them would flip the
+// sign of the source, which is odd under the mirror), then stage 2 on the tile with base u^n.
+// Same per-cell arithmetic and argument order as tile_stage: bitwise the two-launch result.
+template <typename real, int TBY>
+struct TileStepSmem {
+    real c0[TBY + 8][BX + 8], p0[TBY + 8][BX + 8];                       // u^n c, phi: rows -4 .. TBY+3
+    real r0[TBY + 6][BX + 6];                                            // u^n rho: rows -3 .. TBY+2
+    real m1c[TBY + 6][BX + 6], m1p[TBY + 6][BX + 6], M1[TBY + 6][BX + 6]; // stage-1 mu / M: rows -3 .. TBY+2
+    real cs[TBY + 4][BX + 4], ps[TBY + 4][BX + 4], rs[TBY + 4][BX + 4];   // u*: rows -2 .. TBY+1
+    real m2c[TBY + 2][BX + 2], m2p[TBY + 2][BX + 2], M2[TBY + 2][BX + 2]; // stage-2 mu / M: rows -1 .. TBY
+};
+
+template <typename real, int MOB, int FE, int TBY>
+__device__ __forceinline__ void tile_step(const Layout &L, const KC<real> &k1, const KC<real> &k2,
+                                          const real *__restrict__ in, real *out, const real *__restrict__ vel,
+                                          const double *etab, TileStepSmem<real, TBY> &ts, int m, int tx0, int ty0) {
+    const int nx = L.nx;
+    const real *ic = in + m * L.mstride;
+    const real *ip = ic + L.fstride;
+    const real *ir = ip + L.fstride;
+    const Mob<real> mo = MOB == 2 ? load_mob(vel, m) : Mob<real>{};
+    real vx, vy;
+    scaled_velocity(k1, vel, m, vx, vy);
+    // ---- u^n: c, phi with a 4-cell halo, rho with a 3-cell halo (ghost rules by index) ----
+    for (int t = threadIdx.x; t < (TBY + 8) * (BX + 8); t += NT) {
+        const int sy = t / (BX + 8), sx = t - sy * (BX + 8);
+        const int64_t off = L.at(row_cphi(ty0 - 4 + sy, L), wrap_x(tx0 - 4 + sx, nx));
+        ts.c0[sy][sx] = ic[off];
+        ts.p0[sy][sx] = ip[off];
+    }
+    for (int t = threadIdx.x; t < (TBY + 6) * (BX + 6); t += NT) {
+        const int sy = t / (BX + 6), sx = t - sy * (BX + 6);
+        int g = L.y0 + ty0 - 3 + sy;
+        real v;
+        if (g >= L.ny) {
+            v = k1.rho_in;
+        } else {
+            if (g < 0) g = -1 - g;
+            int r = g - L.y0;
+            r = r < -2 ? -2 : r;
+            r = r > L.ny_loc + 1 ? L.ny_loc + 1 : r;
+            v = ir[L.at(r, wrap_x(tx0 - 3 + sx, nx))];
+        }
+        ts.r0[sy][sx] = v;
+    }
+    __syncthreads();
+    // ---- stage 1, a2: mu / M of u^n on rows -3 .. TBY+2, columns -3 .. 34 ----
+    for (int t = threadIdx.x; t < (TBY + 6) * (BX + 6); t += NT) {
+        const int sy = t / (BX + 6), sx = t - sy * (BX + 6);
+        const int ey = sy + 1, ex = sx + 1;
+        real mc, mp, M;
+        constitutive<real, MOB, FE>(k1, mo, etab, ts.c0[ey][ex], ts.p0[ey][ex], ts.c0[ey][ex - 1], ts.c0[ey][ex + 1],
+                                    ts.c0[ey - 1][ex], ts.c0[ey + 1][ex], ts.p0[ey][ex - 1], ts.p0[ey][ex + 1],
+                                    ts.p0[ey - 1][ex], ts.p0[ey + 1][ex], mc, mp, M);
+        ts.m1c[sy][sx] = mc;
+        ts.m1p[sy][sx] = mp;
+        ts.M1[sy][sx] = M;
+    }
+    __syncthreads();
+    // ---- stage 1, a3-a5: u* on rows -2 .. TBY+1, columns -2 .. 33 (in-domain rows only) ----
+    for (int t = threadIdx.x; t < (TBY + 4) * (BX + 4); t += NT) {
+        const int sy = t / (BX + 4), sx = t - sy * (BX + 4);
+        const int g = L.y0 + ty0 - 2 + sy;
+        if (g < 0 || g >= L.ny) continue;
+        const int y = sy + 1, x = sx + 1;          // mu / M and rho^n coordinates
+        const int cy = sy + 2, cx = sx + 2;        // u^n c / phi coordinates
+        real oc, op, orr;
+        const real fe = face_flux<real>(ts.M1[y][x], ts.M1[y][x + 1], ts.m1c[y][x], ts.m1c[y][x + 1]);
+        const real fw = face_flux<real>(ts.M1[y][x - 1], ts.M1[y][x], ts.m1c[y][x - 1], ts.m1c[y][x]);
+        const real fn = face_flux<real>(ts.M1[y][x], ts.M1[y + 1][x], ts.m1c[y][x], ts.m1c[y + 1][x]);
+        const real fs = face_flux<real>(ts.M1[y - 1][x], ts.M1[y][x], ts.m1c[y - 1][x], ts.m1c[y][x]);
+        cell_update<real>(k1, vx, vy, fe, fw, fn, fs, ts.m1p[y][x], ts.m1p[y][x - 1], ts.m1p[y][x + 1],
+                          ts.m1p[y - 1][x], ts.m1p[y + 1][x], ts.p0[cy][cx - 1], ts.p0[cy][cx + 1], ts.p0[cy - 1][cx],
+                          ts.p0[cy + 1][cx], ts.r0[y][x], ts.r0[y][x - 1], ts.r0[y][x + 1], ts.r0[y - 1][x],
+                          ts.r0[y + 1][x], ts.c0[cy][cx], ts.p0[cy][cx], ts.r0[y][x], oc, op, orr);
+        ts.cs[sy][sx] = oc;
+        ts.ps[sy][sx] = op;
+        ts.rs[sy][sx] = orr;
+    }
+    __syncthreads();
+    // ---- u*'s out-of-domain rows: its ghost rules (c, phi mirror; rho bottom mirror, top rho_in) ----
+    if (L.y0 + ty0 - 2 < 0 || L.y0 + ty0 + TBY + 1 >= L.ny) {
+        for (int t = threadIdx.x; t < (TBY + 4) * (BX + 4); t += NT) {
+            const int sy = t / (BX + 4), sx = t - sy * (BX + 4);
+            const int g = L.y0 + ty0 - 2 + sy;
+            if ((g >= 0 && g < L.ny) || g > L.ny + 1) continue;   // rows beyond ny+1 feed no output
+            const int gm = g < 0 ? -1 - g : 2 * L.ny - 1 - g;   // mirrored in-domain row
+            const int my = gm - (L.y0 + ty0 - 2);
+            ts.cs[sy][sx] = ts.cs[my][sx];
+            ts.ps[sy][sx] = ts.ps[my][sx];
+            ts.rs[sy][sx] = g < 0 ? ts.rs[my][sx] : k1.rho_in;
+        }
+        __syncthreads();
+    }
+    // ---- stage 2, a2: mu / M of u* on rows -1 .. TBY, columns -1 .. 32 ----
+    for (int t = threadIdx.x; t < (TBY + 2) * (BX + 2); t += NT) {
+        const int sy = t / (BX + 2), sx = t - sy * (BX + 2);
+        const int ey = sy + 1, ex = sx + 1;
+        real mc, mp, M;
+        constitutive<real, MOB, FE>(k2, mo, etab, ts.cs[ey][ex], ts.ps[ey][ex], ts.cs[ey][ex - 1], ts.cs[ey][ex + 1],
+                                    ts.cs[ey - 1][ex], ts.cs[ey + 1][ex], ts.ps[ey][ex - 1], ts.ps[ey][ex + 1],
+                                    ts.ps[ey - 1][ex], ts.ps[ey + 1][ex], mc, mp, M);
+        ts.m2c[sy][sx] = mc;
+        ts.m2p[sy][sx] = mp;
+        ts.M2[sy][sx] = M;
+    }
+    __syncthreads();
+    // ---- stage 2, a3-a5: u^{n+1} of the tile, base u^n ----
+    const int lx = threadIdx.x & (BX - 1);
+    const int gx = tx0 + lx;
+    for (int q = threadIdx.x / BX; q < TBY; q += NT / BX) {
+        const int ly = ty0 + q;
+        if (gx >= nx || ly >= L.ny_loc) continue;
+        const int y = q + 1, x = lx + 1;          // stage-2 mu / M coordinates
+        const int sy = q + 2, sx = lx + 2;        // u* coordinates
+        const int64_t o = m * L.mstride + L.at(ly, gx);
+        real oc, op, orr;
+        const real fe = face_flux<real>(ts.M2[y][x], ts.M2[y][x + 1], ts.m2c[y][x], ts.m2c[y][x + 1]);
+        const real fw = face_flux<real>(ts.M2[y][x - 1], ts.M2[y][x], ts.m2c[y][x - 1], ts.m2c[y][x]);
+        const real fn = face_flux<real>(ts.M2[y][x], ts.M2[y + 1][x], ts.m2c[y][x], ts.m2c[y + 1][x]);
+        const real fs = face_flux<real>(ts.M2[y - 1][x], ts.M2[y][x], ts.m2c[y - 1][x], ts.m2c[y][x]);
+        cell_update<real>(k2, vx, vy, fe, fw, fn, fs, ts.m2p[y][x], ts.m2p[y][x - 1], ts.m2p[y][x + 1],
+                          ts.m2p[y - 1][x], ts.m2p[y + 1][x], ts.ps[sy][sx - 1], ts.ps[sy][sx + 1], ts.ps[sy - 1][sx],
+                          ts.ps[sy + 1][sx], ts.rs[sy][sx], ts.rs[sy][sx - 1], ts.rs[sy][sx + 1], ts.rs[sy - 1][sx],
+                          ts.rs[sy + 1][sx], ts.c0[q + 4][lx + 4], ts.p0[q + 4][lx + 4], ts.r0[q + 3][lx + 3], oc, op,
+                          orr);
+        PF_DCHECK(ly >= 0 && ly < L.ny_loc && gx >= 0 && gx < nx);
+        out[o] = oc;
+        out[o + L.fstride] = op;
+        out[o + 2 * L.fstride] = orr;
+    }
+    __syncthreads();   // the tile's shared memory may be refilled next
+}
+
 template <typename real, int MOB, int FE>
 __global__ void __launch_bounds__(NT) stage_kernel(Layout L, KC<real> k, const real *__restrict__ in,
                                                    const real *__restrict__ base, real *out,
@@ -214,6 +352,41 @@ __global__ void __launch_bounds__(NT) persistent_kernel(Layout L, KC<real> k1, K
                 tile_stage<real, MOB, FE, TBY>(L, kk, in, U, out, vel, etab, ts, L.m0 + m, bxi * BX, by * TBY);
             }
             grid.sync();
+        }
+    }
+}
+
+// Small-grid path, one grid barrier per STEP: tile_step (both stages on a tile with a 4-cell u^n
+// halo) ping-pongs between U and Us; after an odd number of steps the result is copied back to U.
+template <typename real, int MOB, int FE, int TBY>
+__global__ void __launch_bounds__(NT) persistent_step_kernel(Layout L, KC<real> k1, KC<real> k2, real *U, real *Us,
+                                                             const real *__restrict__ vel, int64_t nsteps) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    TileStepSmem<real, TBY> &ts = *reinterpret_cast<TileStepSmem<real, TBY> *>(smem_raw);
+    __shared__ double etab[64];
+    load_exp_table(etab);
+    cg::grid_group grid = cg::this_grid();
+    const int tx = (L.nx + BX - 1) / BX, ty = (L.ny_loc + TBY - 1) / TBY;
+    const int ntiles = tx * ty * L.members;
+    for (int64_t s = 0; s < nsteps; ++s) {
+        const real *in = (s & 1) ? Us : U;
+        real *out = (s & 1) ? U : Us;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            const int m = t / (tx * ty), r = t - m * (tx * ty);
+            const int by = r / tx, bxi = r - by * tx;
+            tile_step<real, MOB, FE, TBY>(L, k1, k2, in, out, vel, etab, ts, L.m0 + m, bxi * BX, by * TBY);
+        }
+        grid.sync();
+    }
+    if (nsteps & 1) {   // the last step wrote Us: owned cells back to U
+        const int64_t per = (int64_t)L.ny_loc * L.nx, total = per * L.members;
+        for (int64_t q = (int64_t)blockIdx.x * NT + threadIdx.x; q < total; q += (int64_t)gridDim.x * NT) {
+            const int64_t m = q / per, rem = q - m * per;
+            const int r = (int)(rem / L.nx), x = (int)(rem - (int64_t)r * L.nx);
+            const int64_t o = (L.m0 + m) * L.mstride + L.at(r, x);
+            U[o] = Us[o];
+            U[o + L.fstride] = Us[o + L.fstride];
+            U[o + 2 * L.fstride] = Us[o + 2 * L.fstride];
         }
     }
 }
@@ -1211,6 +1384,31 @@ PF_PAIR_ENTRY(pair_stage2_f32, float, true)
 
 #if PF_IN(0)
 template <typename real, int MOB, int FE, int TBY>
+cudaError_t launch_persistent_step(const Layout &L, const KC<real> &k1, const KC<real> &k2, real *U, real *Us,
+                                   const real *vel, int64_t nsteps, cudaStream_t s) {
+    static int occ = -1, nsm = 0;
+    auto kern = persistent_step_kernel<real, MOB, FE, TBY>;
+    const size_t smem = sizeof(TileStepSmem<real, TBY>);
+    if (occ < 0) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, smem);
+        if (e != cudaSuccess) return e;
+        if (occ < 1) occ = 1;
+    }
+    const int64_t ntiles = (int64_t)((L.nx + BX - 1) / BX) * ((L.ny_loc + TBY - 1) / TBY) * L.members;
+    const int64_t maxb = (int64_t)occ * nsm;
+    const int blocks = (int)(ntiles < maxb ? ntiles : maxb);
+    Layout Lc = L;
+    KC<real> a1 = k1, a2 = k2;
+    void *args[] = {&Lc, &a1, &a2, &U, &Us, (void *)&vel, &nsteps};
+    return cudaLaunchCooperativeKernel((const void *)kern, blocks, NT, args, smem, s);
+}
+
+template <typename real, int MOB, int FE, int TBY>
 cudaError_t launch_persistent_b(const Layout &L, const KC<real> &k1, const KC<real> &k2, real *U, real *Us,
                                 const real *vel, int64_t nsteps, cudaStream_t s) {
     static int occ = -1, nsm = 0;
@@ -1235,9 +1433,14 @@ cudaError_t launch_persistent_b(const Layout &L, const KC<real> &k1, const KC<re
 template <typename real, int MOB, int FE>
 cudaError_t launch_persistent_t(const Layout &L, const KC<real> &k1, const KC<real> &k2, real *U, real *Us,
                                 const real *vel, int64_t nsteps, cudaStream_t s) {
-    // 32 x 4 tiles up to 2^17 cells (cfg1 +50%, cfg2 +27%), 32 x 16 above (better from 2^18)
-    if ((int64_t)L.nx * L.ny_loc * L.members <= (int64_t)1 << 17)
-        return launch_persistent_b<real, MOB, FE, 4>(L, k1, k2, U, Us, vel, nsteps, s);
+    const int64_t cells = (int64_t)L.nx * L.ny_loc * L.members;
+    static const int step = env_int("PF_PERSIST_STEP", 1);
+    if (step) {   // one grid barrier per step (tile_step): 32 x 4 tiles up to 2^14 cells, 32 x 8 above
+        if (cells <= (int64_t)1 << 14) return launch_persistent_step<real, MOB, FE, 4>(L, k1, k2, U, Us, vel, nsteps, s);
+        return launch_persistent_step<real, MOB, FE, 8>(L, k1, k2, U, Us, vel, nsteps, s);
+    }
+    // one grid barrier per stage (round 1): 32 x 4 tiles up to 2^17 cells, 32 x 16 above
+    if (cells <= (int64_t)1 << 17) return launch_persistent_b<real, MOB, FE, 4>(L, k1, k2, U, Us, vel, nsteps, s);
     return launch_persistent_b<real, MOB, FE, PF_TBY_LARGE>(L, k1, k2, U, Us, vel, nsteps, s);
 }
 
