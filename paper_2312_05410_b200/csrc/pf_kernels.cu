@@ -192,7 +192,7 @@ struct TileStepSmem {
     real m2c[TBY + 2][BX + 2], m2p[TBY + 2][BX + 2], M2[TBY + 2][BX + 2]; // stage-2 mu / M: rows -1 .. TBY
 };
 
-template <typename real, int MOB, int FE, int TBY>
+template <typename real, int MOB, int FE, int TBY, int NTH>
 __device__ __forceinline__ void tile_step(const Layout &L, const KC<real> &k1, const KC<real> &k2,
                                           const real *__restrict__ in, real *out, const real *__restrict__ vel,
                                           const double *etab, TileStepSmem<real, TBY> &ts, int m, int tx0, int ty0) {
@@ -204,13 +204,13 @@ __device__ __forceinline__ void tile_step(const Layout &L, const KC<real> &k1, c
     real vx, vy;
     scaled_velocity(k1, vel, m, vx, vy);
     // ---- u^n: c, phi with a 4-cell halo, rho with a 3-cell halo (ghost rules by index) ----
-    for (int t = threadIdx.x; t < (TBY + 8) * (BX + 8); t += NT) {
+    for (int t = threadIdx.x; t < (TBY + 8) * (BX + 8); t += NTH) {
         const int sy = t / (BX + 8), sx = t - sy * (BX + 8);
         const int64_t off = L.at(row_cphi(ty0 - 4 + sy, L), wrap_x(tx0 - 4 + sx, nx));
         ts.c0[sy][sx] = ic[off];
         ts.p0[sy][sx] = ip[off];
     }
-    for (int t = threadIdx.x; t < (TBY + 6) * (BX + 6); t += NT) {
+    for (int t = threadIdx.x; t < (TBY + 6) * (BX + 6); t += NTH) {
         const int sy = t / (BX + 6), sx = t - sy * (BX + 6);
         int g = L.y0 + ty0 - 3 + sy;
         real v;
@@ -227,7 +227,7 @@ __device__ __forceinline__ void tile_step(const Layout &L, const KC<real> &k1, c
     }
     __syncthreads();
     // ---- stage 1, a2: mu / M of u^n on rows -3 .. TBY+2, columns -3 .. 34 ----
-    for (int t = threadIdx.x; t < (TBY + 6) * (BX + 6); t += NT) {
+    for (int t = threadIdx.x; t < (TBY + 6) * (BX + 6); t += NTH) {
         const int sy = t / (BX + 6), sx = t - sy * (BX + 6);
         const int ey = sy + 1, ex = sx + 1;
         real mc, mp, M;
@@ -240,7 +240,7 @@ __device__ __forceinline__ void tile_step(const Layout &L, const KC<real> &k1, c
     }
     __syncthreads();
     // ---- stage 1, a3-a5: u* on rows -2 .. TBY+1, columns -2 .. 33 (in-domain rows only) ----
-    for (int t = threadIdx.x; t < (TBY + 4) * (BX + 4); t += NT) {
+    for (int t = threadIdx.x; t < (TBY + 4) * (BX + 4); t += NTH) {
         const int sy = t / (BX + 4), sx = t - sy * (BX + 4);
         const int g = L.y0 + ty0 - 2 + sy;
         if (g < 0 || g >= L.ny) continue;
@@ -262,7 +262,7 @@ __device__ __forceinline__ void tile_step(const Layout &L, const KC<real> &k1, c
     __syncthreads();
     // ---- u*'s out-of-domain rows: its ghost rules (c, phi mirror; rho bottom mirror, top rho_in) ----
     if (L.y0 + ty0 - 2 < 0 || L.y0 + ty0 + TBY + 1 >= L.ny) {
-        for (int t = threadIdx.x; t < (TBY + 4) * (BX + 4); t += NT) {
+        for (int t = threadIdx.x; t < (TBY + 4) * (BX + 4); t += NTH) {
             const int sy = t / (BX + 4), sx = t - sy * (BX + 4);
             const int g = L.y0 + ty0 - 2 + sy;
             if ((g >= 0 && g < L.ny) || g > L.ny + 1) continue;   // rows beyond ny+1 feed no output
@@ -275,7 +275,7 @@ __device__ __forceinline__ void tile_step(const Layout &L, const KC<real> &k1, c
         __syncthreads();
     }
     // ---- stage 2, a2: mu / M of u* on rows -1 .. TBY, columns -1 .. 32 ----
-    for (int t = threadIdx.x; t < (TBY + 2) * (BX + 2); t += NT) {
+    for (int t = threadIdx.x; t < (TBY + 2) * (BX + 2); t += NTH) {
         const int sy = t / (BX + 2), sx = t - sy * (BX + 2);
         const int ey = sy + 1, ex = sx + 1;
         real mc, mp, M;
@@ -290,7 +290,7 @@ __device__ __forceinline__ void tile_step(const Layout &L, const KC<real> &k1, c
     // ---- stage 2, a3-a5: u^{n+1} of the tile, base u^n ----
     const int lx = threadIdx.x & (BX - 1);
     const int gx = tx0 + lx;
-    for (int q = threadIdx.x / BX; q < TBY; q += NT / BX) {
+    for (int q = threadIdx.x / BX; q < TBY; q += NTH / BX) {
         const int ly = ty0 + q;
         if (gx >= nx || ly >= L.ny_loc) continue;
         const int y = q + 1, x = lx + 1;          // stage-2 mu / M coordinates
@@ -358,9 +358,10 @@ __global__ void __launch_bounds__(NT) persistent_kernel(Layout L, KC<real> k1, K
 
 // Small-grid path, one grid barrier per STEP: tile_step (both stages on a tile with a 4-cell u^n
 // halo) ping-pongs between U and Us; after an odd number of steps the result is copied back to U.
-template <typename real, int MOB, int FE, int TBY>
-__global__ void __launch_bounds__(NT) persistent_step_kernel(Layout L, KC<real> k1, KC<real> k2, real *U, real *Us,
-                                                             const real *__restrict__ vel, int64_t nsteps) {
+template <typename real, int MOB, int FE, int TBY, int kStepNT>
+__global__ void __launch_bounds__(kStepNT) persistent_step_kernel(Layout L, KC<real> k1, KC<real> k2, real *U,
+                                                                  real *Us, const real *__restrict__ vel,
+                                                                  int64_t nsteps) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     TileStepSmem<real, TBY> &ts = *reinterpret_cast<TileStepSmem<real, TBY> *>(smem_raw);
     __shared__ double etab[64];
@@ -374,13 +375,13 @@ __global__ void __launch_bounds__(NT) persistent_step_kernel(Layout L, KC<real> 
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
             const int m = t / (tx * ty), r = t - m * (tx * ty);
             const int by = r / tx, bxi = r - by * tx;
-            tile_step<real, MOB, FE, TBY>(L, k1, k2, in, out, vel, etab, ts, L.m0 + m, bxi * BX, by * TBY);
+            tile_step<real, MOB, FE, TBY, kStepNT>(L, k1, k2, in, out, vel, etab, ts, L.m0 + m, bxi * BX, by * TBY);
         }
         grid.sync();
     }
     if (nsteps & 1) {   // the last step wrote Us: owned cells back to U
         const int64_t per = (int64_t)L.ny_loc * L.nx, total = per * L.members;
-        for (int64_t q = (int64_t)blockIdx.x * NT + threadIdx.x; q < total; q += (int64_t)gridDim.x * NT) {
+        for (int64_t q = (int64_t)blockIdx.x * kStepNT + threadIdx.x; q < total; q += (int64_t)gridDim.x * kStepNT) {
             const int64_t m = q / per, rem = q - m * per;
             const int r = (int)(rem / L.nx), x = (int)(rem - (int64_t)r * L.nx);
             const int64_t o = (L.m0 + m) * L.mstride + L.at(r, x);
@@ -1383,11 +1384,11 @@ PF_PAIR_ENTRY(pair_stage2_f32, float, true)
 #endif
 
 #if PF_IN(0)
-template <typename real, int MOB, int FE, int TBY>
+template <typename real, int MOB, int FE, int TBY, int kStepNT>
 cudaError_t launch_persistent_step(const Layout &L, const KC<real> &k1, const KC<real> &k2, real *U, real *Us,
                                    const real *vel, int64_t nsteps, cudaStream_t s) {
     static int occ = -1, nsm = 0;
-    auto kern = persistent_step_kernel<real, MOB, FE, TBY>;
+    auto kern = persistent_step_kernel<real, MOB, FE, TBY, kStepNT>;
     const size_t smem = sizeof(TileStepSmem<real, TBY>);
     if (occ < 0) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1395,7 +1396,7 @@ cudaError_t launch_persistent_step(const Layout &L, const KC<real> &k1, const KC
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, smem);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kStepNT, smem);
         if (e != cudaSuccess) return e;
         if (occ < 1) occ = 1;
     }
@@ -1405,7 +1406,7 @@ cudaError_t launch_persistent_step(const Layout &L, const KC<real> &k1, const KC
     Layout Lc = L;
     KC<real> a1 = k1, a2 = k2;
     void *args[] = {&Lc, &a1, &a2, &U, &Us, (void *)&vel, &nsteps};
-    return cudaLaunchCooperativeKernel((const void *)kern, blocks, NT, args, smem, s);
+    return cudaLaunchCooperativeKernel((const void *)kern, blocks, kStepNT, args, smem, s);
 }
 
 template <typename real, int MOB, int FE, int TBY>
@@ -1435,9 +1436,11 @@ cudaError_t launch_persistent_t(const Layout &L, const KC<real> &k1, const KC<re
                                 const real *vel, int64_t nsteps, cudaStream_t s) {
     const int64_t cells = (int64_t)L.nx * L.ny_loc * L.members;
     static const int step = env_int("PF_PERSIST_STEP", 1);
-    if (step) {   // one grid barrier per step (tile_step): 32 x 4 tiles up to 2^14 cells, 32 x 8 above
-        if (cells <= (int64_t)1 << 14) return launch_persistent_step<real, MOB, FE, 4>(L, k1, k2, U, Us, vel, nsteps, s);
-        return launch_persistent_step<real, MOB, FE, 8>(L, k1, k2, U, Us, vel, nsteps, s);
+    if (step) {   // one grid barrier per step (tile_step): 32 x 4 tiles up to 2^14 cells, 32 x 8 above;
+                  // 512 threads per block up to 2^16 cells (shorter per-phase loops), 256 above
+        if (cells <= (int64_t)1 << 14) return launch_persistent_step<real, MOB, FE, 4, 512>(L, k1, k2, U, Us, vel, nsteps, s);
+        if (cells <= (int64_t)1 << 16) return launch_persistent_step<real, MOB, FE, 8, 512>(L, k1, k2, U, Us, vel, nsteps, s);
+        return launch_persistent_step<real, MOB, FE, 8, 256>(L, k1, k2, U, Us, vel, nsteps, s);
     }
     // one grid barrier per stage (round 1): 32 x 4 tiles up to 2^17 cells, 32 x 16 above
     if (cells <= (int64_t)1 << 17) return launch_persistent_b<real, MOB, FE, 4>(L, k1, k2, U, Us, vel, nsteps, s);
