@@ -39,6 +39,9 @@ namespace cg = cooperative_groups;
 #define PF_PAIR_UNROLL 1   // unroll of the pair kernel's slot loop (experiment knob)
 #endif
 constexpr int kPairUnroll = PF_PAIR_UNROLL;
+#ifndef PF_STEP_TBY4_LOG2
+#define PF_STEP_TBY4_LOG2 14   // step persistent kernel: 32 x 4 tiles up to 2^this cells, 32 x 8 above
+#endif
 #ifndef PF_TBY_LARGE
 #define PF_TBY_LARGE 16    // persistent-kernel tile height above 2^17 cells (experiment knob)
 #endif
@@ -1438,7 +1441,7 @@ cudaError_t launch_persistent_t(const Layout &L, const KC<real> &k1, const KC<re
     static const int step = env_int("PF_PERSIST_STEP", 1);
     if (step) {   // one grid barrier per step (tile_step): 32 x 4 tiles up to 2^14 cells, 32 x 8 above;
                   // 512 threads per block up to 2^16 cells (shorter per-phase loops), 256 above
-        if (cells <= (int64_t)1 << 14) return launch_persistent_step<real, MOB, FE, 4, 512>(L, k1, k2, U, Us, vel, nsteps, s);
+        if (cells <= (int64_t)1 << PF_STEP_TBY4_LOG2) return launch_persistent_step<real, MOB, FE, 4, 512>(L, k1, k2, U, Us, vel, nsteps, s);
         if (cells <= (int64_t)1 << 16) return launch_persistent_step<real, MOB, FE, 8, 512>(L, k1, k2, U, Us, vel, nsteps, s);
         return launch_persistent_step<real, MOB, FE, 8, 256>(L, k1, k2, U, Us, vel, nsteps, s);
     }
