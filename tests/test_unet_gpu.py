@@ -73,6 +73,10 @@ def test_forward_matches_oracle(H, W, batch):
     for b in range(batch):
         ref = U.forward(hist[b], dts[b], P)
         assert _rel(got[b], ref) <= 2e-2, (b, _rel(got[b], ref))
+        # elementwise: every output within 6e-2 of the output's scale (R-36: nine bf16 roundings
+        # of re-normalised activations, u = 2^-9 each, ~1.8% worst case; x3 margin for the final
+        # GroupNorm's division by a sample standard deviation)
+        assert np.max(np.abs(got[b] - ref)) <= 6e-2 * np.max(np.abs(ref)), (b, np.max(np.abs(got[b] - ref)))
 
 
 def test_forward_other_widths_and_lookback():
@@ -135,7 +139,9 @@ def test_full_size_sampled_members():
         got = net.forward(hist, dts)
     assert np.all(np.isfinite(got))
     for b in (0, 37):
-        assert _rel(got[b], U.forward(hist[b], dts[b], P)) <= 2e-2, b
+        ref = U.forward(hist[b], dts[b], P)
+        assert _rel(got[b], ref) <= 2e-2, b
+        assert np.max(np.abs(got[b] - ref)) <= 6e-2 * np.max(np.abs(ref)), b
 
 
 def test_hybrid_schedule_dns_then_surrogate():
