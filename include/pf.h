@@ -301,6 +301,18 @@ const char *pf_last_error(const pf_ctx *ctx);
  * for compute-sanitizer memcheck, which the GPU pool does not allow.) */
 pf_status pf_debug_guards(pf_ctx *ctx, int64_t *guard_bytes, int64_t *corrupted);
 
+/* Diagnostics of a PF_TRACE build (PF_NVCC_EXTRA=-DPF_TRACE=1 python -m
+ * paper_2312_05410_b200.build --out=...; tools/trace_stage1.py); zeros
+ * in a normal build.  They read the fp64 stage-1 pair kernel's timeline of its last launch:
+ *   pf_debug_trace:       out[5][512][2] int64 -- per warp (compute warps 0-3, producer = 4) and box:
+ *                         full-barrier wait start / end (producer: empty wait start / TMA issue), ns of
+ *                         the global timer, block 37 only;
+ *   pf_debug_block_spans: out[1024][3] int64 -- per block: start (after the dependent-launch wait),
+ *                         SM id, end of compute warp 0.
+ * out: host memory the caller owns.  Returns a cudaError_t value (0 = success). */
+int pf_debug_trace(long long *out);
+int pf_debug_block_spans(long long *out);
+
 /* Release everything the ctx owns.  NULL-safe.  Slab mode: collective (NCCL teardown). */
 void pf_free(pf_ctx *ctx);
 

@@ -619,6 +619,21 @@ __global__ void inflow_kernel(Layout L, double rho_in, double sigma, uint64_t se
 
 #include "pf_stream.cuh"
 
+// Timeline trace of one block (diagnostic build, -DPF_TRACE=1; read with pf_debug_trace): per box
+// g < kTraceBoxes the producer's wait start / issue time and each compute warp's full-barrier wait
+// start / end, from the global nanosecond timer.
+#ifndef PF_TRACE
+#define PF_TRACE 0
+#endif
+constexpr int kTraceBoxes = 512, kTraceBlock = 37;
+__device__ long long g_ptrace[5][kTraceBoxes][2];
+__device__ long long g_bspan[1024][3];   // per block: griddep_wait return, SM id, compute warp 0's end
+__device__ __forceinline__ long long gtimer() {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 // A dedicated producer warp issues the TMA boxes and waits on per-slot "empty" mbarriers.  (Measured
 // alternative, round 2: no producer warp -- the last compute warp to release a slot refills it,
 // elected by a shared-memory counter, with 15-16 compute warps per SM instead of 12-16: 5-8%
@@ -660,6 +675,7 @@ __global__ void __launch_bounds__(32 * NCW + 32, MINB) pair_kernel(
     // explicit trigger: the dependent launch starts as this grid's blocks exit (triggering at block
     // start measured 20% slower on cfg3 -- waiting dependents crowd the SMs)
     griddep_wait();
+    if (PF_TRACE && t == 0 && blockIdx.x < 1024) g_bspan[blockIdx.x][0] = gtimer();
 
     if (warp == NCW) {
         // ------------------------------- producer -------------------------------
@@ -674,12 +690,17 @@ __global__ void __launch_bounds__(32 * NCW + 32, MINB) pair_kernel(
             const int bxs = sg.x0 - kPairHalo + L.gx;           // storage column of the box origin
             for (int j = 0; j < nsl; ++j, ++g) {
                 const int slot = g % S;
+                const long long tw = PF_TRACE ? gtimer() : 0;
                 if (g >= (uint32_t)S) mbar_wait(&empty[slot], ((g / S) - 1) & 1u);
                 real *sl = slots + slot * rg.slot_elems;
                 const int k0 = sg.ya - 2 + j * R;                 // first row of the box
                 mbar_expect_tx(&full[slot], BASE ? 2 * box_bytes : box_bytes);
                 tma_load_3d(sl, &mapIn, bxs, k0 + 2, 3 * sg.m, &full[slot]);
                 if (BASE) tma_load_3d(sl + rg.in_elems, &mapBase, bxs, k0, 3 * sg.m, &full[slot]);
+                if (PF_TRACE && blockIdx.x == kTraceBlock && g < (uint32_t)kTraceBoxes) {
+                    g_ptrace[4][g][0] = tw;
+                    g_ptrace[4][g][1] = gtimer();
+                }
             }
         }
         return;
@@ -693,6 +714,7 @@ __global__ void __launch_bounds__(32 * NCW + 32, MINB) pair_kernel(
     const int plane = R * bx;
     int sidx = 0;
     uint32_t par = 0;
+    uint32_t gtr = 0;                       // PF_TRACE: box counter of this warp
     int64_t pos = sch.lo;
     Seg sg;
     while (next_seg(L, Wo, sch, pos, sg)) {
@@ -715,7 +737,13 @@ __global__ void __launch_bounds__(32 * NCW + 32, MINB) pair_kernel(
         for (int j = 0; j < nsl; ++j) {
             const real *cur = slots + sidx * rg.slot_elems + ci;
             PF_DCHECK(sidx >= 0 && sidx < S && ci >= 1 && (R - 1) * bx + 2 * plane + ci + 2 < rg.in_elems + 64);
+            const long long tw0 = PF_TRACE ? gtimer() : 0;
             mbar_wait(&full[sidx], par);
+            if (PF_TRACE && blockIdx.x == kTraceBlock && lane == 0 && warp < 4 && gtr < (uint32_t)kTraceBoxes) {
+                g_ptrace[warp][gtr][0] = tw0;
+                g_ptrace[warp][gtr][1] = gtimer();
+            }
+            ++gtr;
 #pragma unroll
             for (int u = 0; u < R; ++u) {
                 const int i = j * R + u;                  // row k = ya - 2 + i
@@ -775,21 +803,8 @@ __global__ void __launch_bounds__(32 * NCW + 32, MINB) pair_kernel(
                 P3x = p2.x; P3y = p2.y; R3x = r2.x; R3y = r2.y;
                 if (store && i >= 4 && i < n) {
                     const int r = sg.ya - 4 + i;          // local row k-2
-                    const bool edge = xedge | (L.y0 + r <= 1) | (L.y0 + r >= L.ny - 2);
                     PF_DCHECK(sg.m >= L.m0 && sg.m < L.m0 + L.members && r >= L.r0 && r < L.r1 && x >= 0 && x + 1 < nx);
-                    if (!edge) {
-                        real *o = ob + L.at(r, x);
-                        st2(o, ocx, ocy);
-                        st2(o + L.fstride, opx, opy);
-                        st2(o + 2 * L.fstride, orx, ory);
-                    } else {      // the value and its ghost-frame copies
-                        store_with_ghosts<real>(L, ob, 0, r, x, ocx);
-                        store_with_ghosts<real>(L, ob + L.fstride, 1, r, x, opx);
-                        store_with_ghosts<real>(L, ob + 2 * L.fstride, 2, r, x, orx);
-                        store_with_ghosts<real>(L, ob, 0, r, x + 1, ocy);
-                        store_with_ghosts<real>(L, ob + L.fstride, 1, r, x + 1, opy);
-                        store_with_ghosts<real>(L, ob + 2 * L.fstride, 2, r, x + 1, ory);
-                    }
+                    store_pair_ghosts<real>(L, ob, r, x, xedge, ocx, ocy, opx, opy, orx, ory);
                 }
             }
             // the previous box is no longer read (its last row was row k-2 of iteration jR+1)
@@ -800,6 +815,12 @@ __global__ void __launch_bounds__(32 * NCW + 32, MINB) pair_kernel(
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[sidx == 0 ? S - 1 : sidx - 1]);   // the segment's last box
+    }
+    if (PF_TRACE && warp == 0 && lane == 0 && blockIdx.x < 1024) {
+        unsigned sm;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+        g_bspan[blockIdx.x][2] = gtimer();
+        g_bspan[blockIdx.x][1] = (long long)sm;
     }
 }
 
@@ -1029,21 +1050,8 @@ __global__ void __launch_bounds__(32 * (2 * NCW + 1), MINB) ws_kernel(
                 P3x = p2.x; P3y = p2.y; R3x = q2.x; R3y = q2.y;
                 const int r = q - 2;
                 if (store && r >= sg.ya && r < sg.yb) {
-                    const bool edge = xedge | (L.y0 + r <= 1) | (L.y0 + r >= L.ny - 2);
                     PF_DCHECK(sg.m >= L.m0 && sg.m < L.m0 + L.members && r >= L.r0 && r < L.r1 && x >= 0 && x + 1 < nx);
-                    if (!edge) {
-                        real *o = ob + L.at(r, x);
-                        st2(o, ocx, ocy);
-                        st2(o + L.fstride, opx, opy);
-                        st2(o + 2 * L.fstride, orx, ory);
-                    } else {
-                        store_with_ghosts<real>(L, ob, 0, r, x, ocx);
-                        store_with_ghosts<real>(L, ob + L.fstride, 1, r, x, opx);
-                        store_with_ghosts<real>(L, ob + 2 * L.fstride, 2, r, x, orx);
-                        store_with_ghosts<real>(L, ob, 0, r, x + 1, ocy);
-                        store_with_ghosts<real>(L, ob + L.fstride, 1, r, x + 1, opy);
-                        store_with_ghosts<real>(L, ob + 2 * L.fstride, 2, r, x + 1, ory);
-                    }
+                    store_pair_ghosts<real>(L, ob, r, x, xedge, ocx, ocy, opx, opy, orx, ory);
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&us_empty[uidx >= 2 ? uidx - 2 : uidx - 2 + SU]);   // row q-2 done
@@ -1375,6 +1383,17 @@ cudaError_t pair_stage1_f32(const Layout &, const StreamPlan &, const Coef &, in
 cudaError_t pair_stage2_f32(const Layout &, const StreamPlan &, const Coef &, int, void *, const void *, double, cudaStream_t);
 #if PF_IN(1)
 PF_PAIR_ENTRY(pair_stage1_f64, double, false)
+}  // namespace pf
+// Diagnostic: the timeline trace of the fp64 stage-1 pair kernel's block kTraceBlock (PF_TRACE
+// builds; zeros otherwise): [5 warps (4 compute, producer)][512 boxes][wait start, wait end / issue].
+extern "C" int pf_debug_trace(long long *out) {
+    return (int)cudaMemcpyFromSymbol(out, pf::g_ptrace, sizeof(pf::g_ptrace));
+}
+// [1024 blocks][griddep_wait return, SM id, compute warp 0's end] (PF_TRACE builds; zeros otherwise)
+extern "C" int pf_debug_block_spans(long long *out) {
+    return (int)cudaMemcpyFromSymbol(out, pf::g_bspan, sizeof(pf::g_bspan));
+}
+namespace pf {
 #endif
 #if PF_IN(2)
 PF_PAIR_ENTRY(pair_stage2_f64, double, true)

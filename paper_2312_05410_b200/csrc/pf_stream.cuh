@@ -3,6 +3,10 @@
 // persistent blocks, the ring geometry, the ghost-frame stores and 128-bit pair loads / stores.
 // Internal; included inside namespace pf { namespace { ... } } of each translation unit.
 #pragma once
+#include <climits>
+#ifndef PF_STORE_HINT
+#define PF_STORE_HINT 0   // output pair stores: 0 default, 1 streaming (.cs), 2 write-through (.wt)
+#endif
 
 // ========================================================================================
 // Streaming kernel
@@ -179,7 +183,40 @@ __device__ __forceinline__ void st2(real *p, real x, real y) {
     typename Vec2<real>::T v;
     v.x = x;
     v.y = y;
+#if PF_STORE_HINT == 1
+    __stcs(reinterpret_cast<typename Vec2<real>::T *>(p), v);   // streaming (evict-first) store
+#elif PF_STORE_HINT == 2
+    __stwt(reinterpret_cast<typename Vec2<real>::T *>(p), v);   // write-through
+#else
     *reinterpret_cast<typename Vec2<real>::T *>(p) = v;
+#endif
+}
+
+// A lane's two adjacent outputs (columns x, x + 1 of local row r; fields c, phi, rho) and their
+// ghost-frame copies (row a1), without divergent scalar paths: the main pairs are stored by every
+// lane; the mirror rows at the global y boundaries are a whole-row (warp-uniform) extra store; only
+// the lanes whose pair lies in the periodic ghost band (x < gx or x >= nx - gx: both columns,
+// gx even) add their ghost-column pair.  Round 1 sent such lanes through per-value scalar
+// store_with_ghosts calls, a divergent path every warp of the first and last strip executed on
+// every row: those blocks ran ~40% longer than the middle strips (block timeline trace, DESIGN 7).
+template <typename real>
+__device__ __forceinline__ void store_pair_ghosts(const Layout &L, real *ob, int r, int x, bool xedge, real ocx,
+                                                  real ocy, real opx, real opy, real orx, real ory) {
+    auto put = [&](int rr, int xc, bool rho) {
+        real *q = ob + L.at(rr, xc);
+        st2(q, ocx, ocy);
+        st2(q + L.fstride, opx, opy);
+        if (rho) st2(q + 2 * L.fstride, orx, ory);
+    };
+    const int g = L.y0 + r;
+    const int rm = g <= 1 ? -1 - r : (g >= L.ny - 2 ? 2 * L.ny_loc - 1 - r : INT_MIN);   // mirror row
+    put(r, x, true);
+    if (rm != INT_MIN) put(rm, x, g <= 1);       // rho: bottom mirror; its top ghost rows keep rho_in
+    if (xedge) {
+        const int xg = x < L.gx ? x + L.nx : x - L.nx;
+        put(r, xg, true);
+        if (rm != INT_MIN) put(rm, xg, g <= 1);
+    }
 }
 
 constexpr int kPairCols = 60;   // output columns per compute warp
