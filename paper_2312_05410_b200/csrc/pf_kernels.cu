@@ -642,24 +642,58 @@ __device__ __forceinline__ long long gtimer() {
 // (Measured alternative, round 2: stage-1 rows staged in shared memory and written by cp.async.bulk
 // per field -- 35% slower than the STG.128 stores below; the stores were not the bottleneck, the
 // compute warps' dependency latency is.)
-template <typename real, int NCW, int R, int S, bool BASE, int MOB, int FE, int MINB>
-__global__ void __launch_bounds__(32 * NCW + 32, MINB) pair_kernel(
+//
+// Packed variant (V > 1, PF_PAIR_WG builds): V of these blocks share one CTA -- warpgroup 0 holds
+// their V producer warps (setmaxnreg.dec to 24 registers), warpgroups 1.. their V * NCW = 12 or
+// 16 compute warps (setmaxnreg.inc: the registers the producers gave up, 160 per thread for 12
+// compute warps instead of the 128 the 4-blocks-per-SM layout allows).  Same rings, schedule and
+// arithmetic per virtual block, so results are bitwise identical.
+// Registers per compute thread of a packed block: the CTA's allocation (launch-bound cap x threads)
+// minus the producer warpgroup's 24 per thread.  setmaxnreg.inc waits until the CTA's pool holds
+// that many, so the launch checks the compiled register count against it (launch_pair_k).
+__host__ __device__ constexpr int pair_packed_cap(int V, int NCW) {
+    return (65536 / (128 + 32 * V * NCW)) / 8 * 8;
+}
+__host__ __device__ constexpr int pair_packed_regs(int V, int NCW) {
+    return ((pair_packed_cap(V, NCW) * (128 + 32 * V * NCW) - 24 * 128) / (32 * V * NCW)) / 8 * 8 > 248
+               ? 248
+               : ((pair_packed_cap(V, NCW) * (128 + 32 * V * NCW) - 24 * 128) / (32 * V * NCW)) / 8 * 8;
+}
+
+template <typename real, int NCW, int R, int S, bool BASE, int MOB, int FE, int MINB, int V>
+__global__ void __launch_bounds__(V == 1 ? 32 * NCW + 32 : 128 + 32 * V * NCW, V == 1 ? MINB : 1) pair_kernel(
     Layout L, KC<real> k, const __grid_constant__ CUtensorMap mapIn, const __grid_constant__ CUtensorMap mapBase,
-    real *out, const real *__restrict__ vel, int Wo, int G) {
+    real *out, const real *__restrict__ vel, int Wo, int G, int NB) {
     static_assert(R >= 2, "rows k-1, k-2 must lie in the current or the previous box");
+    static_assert(V == 1 || (V <= 4 && (V * NCW) % 4 == 0), "packed blocks fill whole warpgroups");
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int bx = Wo + 2 * kPairHalo;
     const Ring<real> rg(bx, R, BASE);
     unsigned char *base_sm = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
-    real *slots = reinterpret_cast<real *>(base_sm);
-    uint64_t *full = reinterpret_cast<uint64_t *>(base_sm + (size_t)S * rg.slot_elems * sizeof(real));
-    uint64_t *empty = full + S;
-    double *etab = reinterpret_cast<double *>(empty + S);
-    load_exp_table(etab);
 
     const int t = threadIdx.x;
     const int warp = t >> 5, lane = t & 31;
-    if (t == 0) {
+    const bool producer = V == 1 ? warp == NCW : warp < 4;
+    const int v = V == 1 ? 0 : (producer ? warp : (warp - 4) / NCW);   // virtual block of this warp
+    const int cw = V == 1 ? warp : (warp - 4) - v * NCW;                // compute warp within it
+    real *slots;
+    uint64_t *full, *empty;
+    double *etab;
+    if (V == 1) {
+        slots = reinterpret_cast<real *>(base_sm);
+        full = reinterpret_cast<uint64_t *>(base_sm + (size_t)S * rg.slot_elems * sizeof(real));
+        empty = full + S;
+        etab = reinterpret_cast<double *>(empty + S);
+    } else {
+        const size_t vbytes = ((size_t)S * rg.slot_elems * sizeof(real) + (size_t)S * 16 + 127) / 128 * 128;
+        etab = reinterpret_cast<double *>(base_sm);
+        unsigned char *reg = base_sm + 64 * 8 + (size_t)(v < V ? v : 0) * vbytes;
+        slots = reinterpret_cast<real *>(reg);
+        full = reinterpret_cast<uint64_t *>(reg + (size_t)S * rg.slot_elems * sizeof(real));
+        empty = full + S;
+    }
+    load_exp_table(etab);
+    if (V == 1 ? t == 0 : (producer && warp < V && lane == 0)) {   // each virtual block's barriers
         for (int q = 0; q < S; ++q) {
             mbar_init(&full[q], 1);
             mbar_init(&empty[q], NCW);
@@ -667,19 +701,21 @@ __global__ void __launch_bounds__(32 * NCW + 32, MINB) pair_kernel(
         fence_mbar_init();
     }
     __syncthreads();
-
+    const int vb = V == 1 ? (int)blockIdx.x : (int)blockIdx.x * V + v;
     const int nx = L.nx;
-    const Sched sch = make_sched(L, Wo, G);
-    const uint32_t box_bytes = (uint32_t)(3 * R * bx * sizeof(real));
-    // set-up above overlaps the previous launch's drain; no global access before this point.  No
+    // set-up above overlaps the previous launch's drain; no global access before griddep_wait.  No
     // explicit trigger: the dependent launch starts as this grid's blocks exit (triggering at block
-    // start measured 20% slower on cfg3 -- waiting dependents crowd the SMs)
-    griddep_wait();
-    if (PF_TRACE && t == 0 && blockIdx.x < 1024) g_bspan[blockIdx.x][0] = gtimer();
+    // start measured 20% slower on cfg3 -- waiting dependents crowd the SMs).  (Each role runs its
+    // own copy of the prologue below: ptxas allocates registers per setmaxnreg region, so the two
+    // regions must not merge again.)
 
-    if (warp == NCW) {
+    if (producer) {
         // ------------------------------- producer -------------------------------
-        if (lane != 0) return;
+        if (V > 1) asm volatile("setmaxnreg.dec.sync.aligned.u32 24;" ::: "memory");
+        if (lane != 0 || v >= V) return;
+        const Sched sch = make_sched(L, Wo, G, vb, NB);
+        const uint32_t box_bytes = (uint32_t)(3 * R * bx * sizeof(real));
+        griddep_wait();
         prefetch_tmap(&mapIn);
         if (BASE) prefetch_tmap(&mapBase);
         uint32_t g = 0;
@@ -697,7 +733,7 @@ __global__ void __launch_bounds__(32 * NCW + 32, MINB) pair_kernel(
                 mbar_expect_tx(&full[slot], BASE ? 2 * box_bytes : box_bytes);
                 tma_load_3d(sl, &mapIn, bxs, k0 + 2, 3 * sg.m, &full[slot]);
                 if (BASE) tma_load_3d(sl + rg.in_elems, &mapBase, bxs, k0, 3 * sg.m, &full[slot]);
-                if (PF_TRACE && blockIdx.x == kTraceBlock && g < (uint32_t)kTraceBoxes) {
+                if (PF_TRACE && vb == kTraceBlock && g < (uint32_t)kTraceBoxes) {
                     g_ptrace[4][g][0] = tw;
                     g_ptrace[4][g][1] = gtimer();
                 }
@@ -707,9 +743,13 @@ __global__ void __launch_bounds__(32 * NCW + 32, MINB) pair_kernel(
     }
 
     // --------------------------- compute warps ---------------------------------
+    if (V > 1) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(pair_packed_regs(V, NCW)) : "memory");
+    const Sched sch = make_sched(L, Wo, G, vb, NB);
+    griddep_wait();
+    if (PF_TRACE && cw == 0 && lane == 0 && vb < 1024) g_bspan[vb][0] = gtimer();
     // Lane l of warp w owns strip-relative columns cx, cx + 1 with cx = 60 w + 2 l - 2: lanes 1..30
     // write them, lane 0's right column and lane 31's left column are the flux halo.
-    const int cx = kPairCols * warp + 2 * lane - 2;
+    const int cx = kPairCols * cw + 2 * lane - 2;
     const int ci = kPairHalo + cx;          // its (even) column in a box row
     const int plane = R * bx;
     int sidx = 0;
@@ -739,9 +779,9 @@ __global__ void __launch_bounds__(32 * NCW + 32, MINB) pair_kernel(
             PF_DCHECK(sidx >= 0 && sidx < S && ci >= 1 && (R - 1) * bx + 2 * plane + ci + 2 < rg.in_elems + 64);
             const long long tw0 = PF_TRACE ? gtimer() : 0;
             mbar_wait(&full[sidx], par);
-            if (PF_TRACE && blockIdx.x == kTraceBlock && lane == 0 && warp < 4 && gtr < (uint32_t)kTraceBoxes) {
-                g_ptrace[warp][gtr][0] = tw0;
-                g_ptrace[warp][gtr][1] = gtimer();
+            if (PF_TRACE && vb == kTraceBlock && lane == 0 && cw < 4 && gtr < (uint32_t)kTraceBoxes) {
+                g_ptrace[cw][gtr][0] = tw0;
+                g_ptrace[cw][gtr][1] = gtimer();
             }
             ++gtr;
 #pragma unroll
@@ -816,11 +856,11 @@ __global__ void __launch_bounds__(32 * NCW + 32, MINB) pair_kernel(
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[sidx == 0 ? S - 1 : sidx - 1]);   // the segment's last box
     }
-    if (PF_TRACE && warp == 0 && lane == 0 && blockIdx.x < 1024) {
+    if (PF_TRACE && cw == 0 && lane == 0 && vb < 1024) {
         unsigned sm;
         asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
-        g_bspan[blockIdx.x][2] = gtimer();
-        g_bspan[blockIdx.x][1] = (long long)sm;
+        g_bspan[vb][2] = gtimer();
+        g_bspan[vb][1] = (long long)sm;
     }
 }
 
@@ -1086,6 +1126,9 @@ constexpr int kF32Slots = PF_F32_SLOTS;
 #ifndef PF_PAIR_R2
 #define PF_PAIR_R2 2
 #endif
+#ifndef PF_PAIR_WG
+#define PF_PAIR_WG 2        // packed pair blocks (setmaxnreg): 0 off, 1 fp64, 2 fp64 + fp32 stage 1
+#endif
 #ifndef PF_S1_SMEM_KB
 #define PF_S1_SMEM_KB 150   // fp64 stage-1 shared-memory budget per SM
 #endif
@@ -1105,18 +1148,25 @@ struct PairCfg {
     static constexpr int minb = pick(wslots / wpb > 8 ? 8 : wslots / wpb);
     static constexpr int S = ring(minb) > 8 ? 8 : ring(minb);
     static_assert(S >= 3, "ring too shallow");
+    // packed blocks (pair_kernel V > 1): the minb blocks of an SM as one CTA when their compute
+    // warps fill whole warpgroups.  Measured (one B200, tools/kbench.py, gpurun_out r2wg2): fp64
+    // stage 1 -8% (cfg3) / -10.5% (cfg4), stage 2 -1%; fp32 (16 compute warps, 112 instead of 96
+    // registers) stage 1 -6%, stage 2 +1% -- so fp32 packs stage 1 only.
+    static constexpr bool pack = sizeof(real) == 8 ? PF_PAIR_WG >= 1 : (PF_PAIR_WG >= 2 && !BASE);
+    static constexpr int V = (pack && minb > 1 && minb <= 4 && (minb * NCW) % 4 == 0) ? minb : 1;
 };
 
 template <typename real, int NCW, bool BASE, int MOB, int FE>
 cudaError_t launch_pair_k(const Layout &L, const StreamPlan &P, const KC<real> &k, int stage, real *out,
                           const real *vel, cudaStream_t s) {
     using C = PairCfg<real, NCW, BASE>;
-    constexpr int R = C::R, S = C::S, MINB = C::minb;
-    const size_t smem = stream_smem_bytes<real>(P.box_x, R, S, BASE);
-    const int threads = 32 * C::wpb;
+    constexpr int R = C::R, S = C::S, MINB = C::minb, V = C::V;
+    const size_t smem = V == 1 ? stream_smem_bytes<real>(P.box_x, R, S, BASE)
+                               : pair_packed_smem_bytes<real>(P.box_x, R, S, BASE, V);
+    const int threads = V == 1 ? 32 * C::wpb : 128 + 32 * V * NCW;
     static int occ = -1, nsm = 0;
     static size_t smem_set = 0;
-    auto kern = pair_kernel<real, NCW, R, S, BASE, MOB, FE, MINB>;
+    auto kern = pair_kernel<real, NCW, R, S, BASE, MOB, FE, MINB, V>;
     if (smem > smem_set) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
@@ -1127,13 +1177,19 @@ cudaError_t launch_pair_k(const Layout &L, const StreamPlan &P, const KC<real> &
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        if (V > 1) {   // the compute warps' setmaxnreg.inc must be satisfiable from the CTA's pool
+            cudaFuncAttributes fa;
+            cudaError_t e = cudaFuncGetAttributes(&fa, kern);
+            if (e != cudaSuccess) return e;
+            if (fa.numRegs * threads - 24 * 128 < pair_packed_regs(V, NCW) * 32 * V * NCW) return cudaErrorInvalidConfiguration;
+        }
         cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
         if (e != cudaSuccess) return e;
         if (occ < 1) occ = 1;
     }
     const int64_t R_ = (int64_t)L.members * P.strips * (L.r1 - L.r0);
     const int64_t minrows = 16;
-    int64_t B = (int64_t)occ * nsm;
+    int64_t B = (int64_t)occ * nsm * V;   // (virtual) blocks
     static const int nogroup = env_int("PF_STREAM_NOGROUP", 0);
     // grouped schedule when at least 4 groups of `strips` blocks fit in one resident wave
     int64_t G = B / P.strips;
@@ -1146,6 +1202,8 @@ cudaError_t launch_pair_k(const Layout &L, const StreamPlan &P, const KC<real> &
         if (B > (R_ + minrows - 1) / minrows) B = (R_ + minrows - 1) / minrows;
     }
     if (B < 1) B = 1;
+    const int NB = (int)B;
+    B = (B + V - 1) / V;                   // CTAs
     const int ri = R == 4 ? 1 : 0;
     const CUtensorMap &mIn = stage == 1 ? P.mapU[ri] : P.mapUs[ri];
     static const int pdl = env_int("PF_PDL", 1);
@@ -1160,9 +1218,9 @@ cudaError_t launch_pair_k(const Layout &L, const StreamPlan &P, const KC<real> &
         cfg.stream = s;
         cfg.attrs = at;
         cfg.numAttrs = 1;
-        return cudaLaunchKernelEx(&cfg, kern, L, k, mIn, P.mapU[ri], out, vel, P.Wo, (int)G);
+        return cudaLaunchKernelEx(&cfg, kern, L, k, mIn, P.mapU[ri], out, vel, P.Wo, (int)G, NB);
     }
-    kern<<<(unsigned)B, threads, smem, s>>>(L, k, mIn, P.mapU[ri], out, vel, P.Wo, (int)G);
+    kern<<<(unsigned)B, threads, smem, s>>>(L, k, mIn, P.mapU[ri], out, vel, P.Wo, (int)G, NB);
     return cudaGetLastError();
 }
 

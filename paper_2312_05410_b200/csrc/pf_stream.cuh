@@ -80,23 +80,30 @@ struct Sched {
     int64_t lo, hi;
     int strip;        // grouped: fixed strip of this block; -1 ungrouped
 };
-__device__ __forceinline__ Sched make_sched(const Layout &L, int Wo, int G) {
+// b / nb: the (virtual) block index and count; blocks b >= nb get an empty range.
+__device__ __forceinline__ Sched make_sched(const Layout &L, int Wo, int G, int b, int nb) {
     const int strips = (L.nx + Wo - 1) / Wo;
     const int nyl = L.r1 - L.r0;        // rows of this launch's row window
     Sched sc;
-    if (G > 0) {
-        const int g = blockIdx.x / strips;
-        sc.strip = blockIdx.x - g * strips;
+    if (b >= nb) {
+        sc.strip = 0;
+        sc.lo = sc.hi = 0;
+    } else if (G > 0) {
+        const int g = b / strips;
+        sc.strip = b - g * strips;
         const int64_t T = (int64_t)L.members * nyl;
         sc.lo = T * g / G;
         sc.hi = T * (g + 1) / G;
     } else {
         const int64_t R = (int64_t)L.members * strips * nyl;
         sc.strip = -1;
-        sc.lo = R * blockIdx.x / gridDim.x;
-        sc.hi = R * (blockIdx.x + 1) / gridDim.x;
+        sc.lo = R * b / nb;
+        sc.hi = R * (b + 1) / nb;
     }
     return sc;
+}
+__device__ __forceinline__ Sched make_sched(const Layout &L, int Wo, int G) {
+    return make_sched(L, Wo, G, (int)blockIdx.x, (int)gridDim.x);
 }
 __device__ __forceinline__ bool next_seg(const Layout &L, int Wo, const Sched &sc, int64_t &pos, Seg &sg) {
     if (pos >= sc.hi) return false;
@@ -136,6 +143,18 @@ struct Ring {
         slot_elems = in_elems * (base ? 2 : 1);
     }
 };
+
+// Warpgroup-packed pair blocks (V > 1): V virtual blocks per CTA, each with its own ring and
+// barriers; the exp table once.
+template <typename real>
+size_t pair_region_bytes(int bx, int R, int S, bool base) {
+    Ring<real> rg(bx, R, base);
+    return ((size_t)S * rg.slot_elems * sizeof(real) + (size_t)S * 16 + 127) / 128 * 128;
+}
+template <typename real>
+size_t pair_packed_smem_bytes(int bx, int R, int S, bool base, int V) {
+    return 128 + 64 * 8 + (size_t)V * pair_region_bytes<real>(bx, R, S, base) + 64 * sizeof(real);
+}
 
 template <typename real>
 size_t stream_smem_bytes(int bx, int R, int S, bool base) {

@@ -5,11 +5,11 @@ out=gpurun_out/${TAG:-ab}
 mkdir -p $out
 for rep in 1 2; do
 for cfg in ${CFGS:-3 4}; do
-  timeout 120 python tools/kbench.py --config $cfg --steps 100 >> $out/kb_c${cfg}_default.json 2>&1
+  timeout 60 python tools/kbench.py --config $cfg --steps 100 >> $out/kb_c${cfg}_default.json 2>&1
   for f in paper_2312_05410_b200/_variants/libpf_*.so; do
     n=$(basename $f .so)
     [ "$n" = "libpf_checked" ] && continue
-    PF_LIB=$PWD/$f timeout 120 python tools/kbench.py --config $cfg --steps 100 >> $out/kb_c${cfg}_$n.json 2>&1
+    PF_LIB=$PWD/$f timeout 60 python tools/kbench.py --config $cfg --steps 100 >> $out/kb_c${cfg}_$n.json 2>&1
   done
 done
 done
