@@ -39,6 +39,16 @@ namespace cg = cooperative_groups;
 #define PF_PAIR_UNROLL 1   // unroll of the pair kernel's slot loop (experiment knob)
 #endif
 constexpr int kPairUnroll = PF_PAIR_UNROLL;
+#ifndef PF_STEP_UNROLL
+#define PF_STEP_UNROLL 0   // unroll of tile_step's per-phase cell loops (0: the compiler's choice)
+#endif
+#define PF_PRAGMA(x) _Pragma(#x)
+#define PF_UNROLL_N(n) PF_PRAGMA(unroll n)
+#if PF_STEP_UNROLL > 0
+#define PF_STEP_LOOP_HINT PF_UNROLL_N(PF_STEP_UNROLL)
+#else
+#define PF_STEP_LOOP_HINT
+#endif
 #ifndef PF_STEP_TBY4_LOG2
 #define PF_STEP_TBY4_LOG2 14   // step persistent kernel: 32 x 4 tiles up to 2^this cells, 32 x 8 above
 #endif
@@ -207,12 +217,14 @@ __device__ __forceinline__ void tile_step(const Layout &L, const KC<real> &k1, c
     real vx, vy;
     scaled_velocity(k1, vel, m, vx, vy);
     // ---- u^n: c, phi with a 4-cell halo, rho with a 3-cell halo (ghost rules by index) ----
+    PF_STEP_LOOP_HINT
     for (int t = threadIdx.x; t < (TBY + 8) * (BX + 8); t += NTH) {
         const int sy = t / (BX + 8), sx = t - sy * (BX + 8);
         const int64_t off = L.at(row_cphi(ty0 - 4 + sy, L), wrap_x(tx0 - 4 + sx, nx));
         ts.c0[sy][sx] = ic[off];
         ts.p0[sy][sx] = ip[off];
     }
+    PF_STEP_LOOP_HINT
     for (int t = threadIdx.x; t < (TBY + 6) * (BX + 6); t += NTH) {
         const int sy = t / (BX + 6), sx = t - sy * (BX + 6);
         int g = L.y0 + ty0 - 3 + sy;
@@ -230,6 +242,7 @@ __device__ __forceinline__ void tile_step(const Layout &L, const KC<real> &k1, c
     }
     __syncthreads();
     // ---- stage 1, a2: mu / M of u^n on rows -3 .. TBY+2, columns -3 .. 34 ----
+    PF_STEP_LOOP_HINT
     for (int t = threadIdx.x; t < (TBY + 6) * (BX + 6); t += NTH) {
         const int sy = t / (BX + 6), sx = t - sy * (BX + 6);
         const int ey = sy + 1, ex = sx + 1;
@@ -243,6 +256,7 @@ __device__ __forceinline__ void tile_step(const Layout &L, const KC<real> &k1, c
     }
     __syncthreads();
     // ---- stage 1, a3-a5: u* on rows -2 .. TBY+1, columns -2 .. 33 (in-domain rows only) ----
+    PF_STEP_LOOP_HINT
     for (int t = threadIdx.x; t < (TBY + 4) * (BX + 4); t += NTH) {
         const int sy = t / (BX + 4), sx = t - sy * (BX + 4);
         const int g = L.y0 + ty0 - 2 + sy;
@@ -278,6 +292,7 @@ __device__ __forceinline__ void tile_step(const Layout &L, const KC<real> &k1, c
         __syncthreads();
     }
     // ---- stage 2, a2: mu / M of u* on rows -1 .. TBY, columns -1 .. 32 ----
+    PF_STEP_LOOP_HINT
     for (int t = threadIdx.x; t < (TBY + 2) * (BX + 2); t += NTH) {
         const int sy = t / (BX + 2), sx = t - sy * (BX + 2);
         const int ey = sy + 1, ex = sx + 1;
@@ -1518,6 +1533,12 @@ cudaError_t launch_persistent_t(const Layout &L, const KC<real> &k1, const KC<re
     static const int step = env_int("PF_PERSIST_STEP", 1);
     if (step) {   // one grid barrier per step (tile_step): 32 x 4 tiles up to 2^14 cells, 32 x 8 above;
                   // 512 threads per block up to 2^16 cells (shorter per-phase loops), 256 above
+#ifdef PF_STEP_TBY6
+        static const int tby = env_int("PF_STEP_TBY", 0);   // experiment: force 4 / 6 / 8-row tiles
+        if (tby == 4) return launch_persistent_step<real, MOB, FE, 4, 512>(L, k1, k2, U, Us, vel, nsteps, s);
+        if (tby == 6) return launch_persistent_step<real, MOB, FE, 6, 512>(L, k1, k2, U, Us, vel, nsteps, s);
+        if (tby == 8) return launch_persistent_step<real, MOB, FE, 8, 512>(L, k1, k2, U, Us, vel, nsteps, s);
+#endif
         if (cells <= (int64_t)1 << PF_STEP_TBY4_LOG2) return launch_persistent_step<real, MOB, FE, 4, 512>(L, k1, k2, U, Us, vel, nsteps, s);
         if (cells <= (int64_t)1 << 16) return launch_persistent_step<real, MOB, FE, 8, 512>(L, k1, k2, U, Us, vel, nsteps, s);
         return launch_persistent_step<real, MOB, FE, 8, 256>(L, k1, k2, U, Us, vel, nsteps, s);
