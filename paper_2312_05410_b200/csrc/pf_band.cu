@@ -57,8 +57,53 @@ struct BandGeo {
     }
     __host__ __device__ int u(int srw, int x) const { return srw * P + (x + 2); }
     __host__ __device__ int w(int r, int x) const { return (r + 1) * Q + (x + 1); }
-    __host__ __device__ size_t bytes(size_t esz) const { return (size_t)(3 * uplane + 3 * wplane) * esz + 64 * 8; }
+    // + exp table + the two halo mbarriers (PF_BAND_P2P)
+    __host__ __device__ size_t bytes(size_t esz) const { return (size_t)(3 * uplane + 3 * wplane) * esz + 64 * 8 + 16; }
 };
+
+#ifndef PF_BAND_P2P
+#define PF_BAND_P2P 1   // halo rows by st.async + per-parity mbarriers instead of a cluster barrier per stage
+#endif
+__device__ __forceinline__ uint32_t smem_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+// shared::cluster address of the same location in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa_rank(uint32_t a, int rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+    return r;
+}
+// asynchronous store into another CTA's shared memory, completing `bytes` on its mbarrier
+__device__ __forceinline__ void st_async(uint32_t ra, double v, uint32_t rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(ra),
+                 "l"(__double_as_longlong(v)), "r"(rbar)
+                 : "memory");
+}
+__device__ __forceinline__ void st_async(uint32_t ra, float v, uint32_t rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(ra),
+                 "r"(__float_as_uint(v)), "r"(rbar)
+                 : "memory");
+}
+__device__ __forceinline__ void hbar_init(uint64_t *b) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(b)) : "memory");
+}
+__device__ __forceinline__ void hbar_expect(uint64_t *b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void hbar_wait(uint64_t *b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "HW_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra HW_%=;\n}" ::"r"(smem_addr(b)),
+        "r"(parity)
+        : "memory");
+}
+// put() into the neighbour's plane (shared::cluster address rpl) with its periodic ghost copy
+template <typename real>
+__device__ __forceinline__ void push(uint32_t rpl, uint32_t rbar, const BandGeo &gg, int sr, int x, real v) {
+    st_async(rpl + (uint32_t)gg.u(sr, x) * (uint32_t)sizeof(real), v, rbar);
+    if (x < 2) st_async(rpl + (uint32_t)gg.u(sr, x + gg.nx) * (uint32_t)sizeof(real), v, rbar);
+    if (x >= gg.nx - 2) st_async(rpl + (uint32_t)gg.u(sr, x - gg.nx) * (uint32_t)sizeof(real), v, rbar);
+}
 
 // Store value v of field plane `pl` at (storage row sr, column x) with its periodic ghost copy.
 template <typename real>
@@ -84,6 +129,7 @@ __global__ void __launch_bounds__(kBT, 1) band_kernel(Layout L, KC<real> k1, KC<
     real *sc = su, *sp = su + gg.uplane, *sr = su + 2 * gg.uplane;
     real *smc = su + 3 * gg.uplane, *smp = smc + gg.wplane, *sM = smp + gg.wplane;
     double *etab = reinterpret_cast<double *>(sM + gg.wplane);
+    uint64_t *hbar = reinterpret_cast<uint64_t *>(etab + 64);   // halo rows of parity 0 / 1 arrived
     load_exp_table(etab);
     // the neighbours' shared memory (DSMEM): below = rank bi-1 (its rows h'-2, h'-1 are our rows
     // -2, -1), above = rank bi+1 (its rows 0, 1 are our rows h, h+1)
@@ -128,12 +174,33 @@ __global__ void __launch_bounds__(kBT, 1) band_kernel(Layout L, KC<real> k1, KC<
         by[i] = q / nx;
         bx[i] = q - by[i] * nx;
     }
+    if (PF_BAND_P2P && t == 0) {
+        hbar_init(&hbar[0]);
+        hbar_init(&hbar[1]);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
     cluster.sync();   // every block has started (DSMEM targets exist) and loaded its band
     int par = 0;      // halo parity read by this stage
+    // PF_BAND_P2P: the neighbours push their border rows with st.async, each completing its bytes
+    // on this block's mbarrier of that halo parity: 2 rows x (nx + 4 ghost-column copies) x 3
+    // fields per neighbour and stage.  A block waits for exactly the rows it reads, so no
+    // cluster-wide barrier is needed per stage: the parity double-buffering makes a push of
+    // stage g + 2 (same buffer as stage g) impossible before the neighbour finished reading it,
+    // because that push needs the neighbour's stage-(g + 1) rows, sent after its reads.
+    const uint32_t rx_bytes = (uint32_t)(((bottom ? 0 : 1) + (top ? 0 : 1)) * 2 * (nx + 4) * 3 * (int)sizeof(real));
+    const uint32_t su_a = smem_addr(su), hb_a = smem_addr(hbar);
+    const uint32_t rsu_dn = bottom ? 0u : mapa_rank(su_a, bi - 1), rhb_dn = bottom ? 0u : mapa_rank(hb_a, bi - 1);
+    const uint32_t rsu_up = top ? 0u : mapa_rank(su_a, bi + 1), rhb_up = top ? 0u : mapa_rank(hb_a, bi + 1);
+    const int64_t nstages = 2 * nsteps;
 
     for (int64_t s = 0; s < nsteps; ++s) {
         for (int stage = 1; stage <= 2; ++stage) {
             const KC<real> k = stage == 1 ? k1 : k2;
+            const int64_t g = 2 * s + stage - 1;   // stage index; reads halo parity par = g & 1
+            if (PF_BAND_P2P && g > 0) {           // the neighbours' rows of stage g - 1
+                if (t == 0) hbar_expect(&hbar[par], rx_bytes);
+                hbar_wait(&hbar[par], (uint32_t)(((g - 1) >> 1) & 1));
+            }
             // A: mu_c, mu_phi, M on rows -1 .. h, columns -1 .. nx (row a2)
             auto cell_a = [&](int rr, int x) {
                 const int o0 = gg.u(BandGeo::srow(rr, h, par), x);
@@ -177,6 +244,7 @@ __global__ void __launch_bounds__(kBT, 1) band_kernel(Layout L, KC<real> k1, KC<
             // C: own rows (+ ghost columns, + mirror rows at the global boundaries) and the pushes
             // of the border rows into the neighbours' halos, all into halo parity np
             const int np = par ^ 1;
+            const bool last = g == nstages - 1;   // P2P: no pushes nobody reads
 #pragma unroll
             for (int i = 0; i < MAXC; ++i) {
                 const int q = t + i * kBT;
@@ -187,20 +255,34 @@ __global__ void __launch_bounds__(kBT, 1) band_kernel(Layout L, KC<real> k1, KC<
                         const real v = outv[f][i];
                         put(su + f * gg.uplane, gg, y + 4, x, v);
                         if (y < 2) {
-                            if (!bottom) put(su_dn + f * gg.uplane, gg, BandGeo::srow(h_dn + y, h_dn, np), x, v);
-                            else put(su + f * gg.uplane, gg, BandGeo::srow(-1 - y, h, np), x, v);   // mirror (rho too)
+                            if (!bottom) {
+                                if (!PF_BAND_P2P) put(su_dn + f * gg.uplane, gg, BandGeo::srow(h_dn + y, h_dn, np), x, v);
+                                else if (!last)
+                                    push(rsu_dn + (uint32_t)(f * gg.uplane * (int)sizeof(real)), rhb_dn + 8u * np, gg,
+                                         BandGeo::srow(h_dn + y, h_dn, np), x, v);
+                            } else {
+                                put(su + f * gg.uplane, gg, BandGeo::srow(-1 - y, h, np), x, v);   // mirror (rho too)
+                            }
                         }
                         if (y >= h - 2) {
-                            if (!top) put(su_up + f * gg.uplane, gg, BandGeo::srow(y - h, 2, np), x, v);
-                            else if (f != 2) put(su + f * gg.uplane, gg, BandGeo::srow(2 * h - 1 - y, h, np), x, v);
+                            if (!top) {
+                                if (!PF_BAND_P2P) put(su_up + f * gg.uplane, gg, BandGeo::srow(y - h, 2, np), x, v);
+                                else if (!last)
+                                    push(rsu_up + (uint32_t)(f * gg.uplane * (int)sizeof(real)), rhb_up + 8u * np, gg,
+                                         BandGeo::srow(y - h, 2, np), x, v);
+                            } else if (f != 2) {
+                                put(su + f * gg.uplane, gg, BandGeo::srow(2 * h - 1 - y, h, np), x, v);
+                            }
                         }
                     }
                 }
             }
-            cluster.sync();   // every halo row of parity np is in place; every block left phase B
+            if (PF_BAND_P2P) __syncthreads();   // own rows and mirror rows in place
+            else cluster.sync();   // every halo row of parity np is in place; every block left phase B
             par = np;
         }
     }
+    if (PF_BAND_P2P) cluster.sync();   // no block leaves while a neighbour may still address it
     // owned cells back to the state buffer (ghost frame rebuilt by the host)
     real *oc = U + (int64_t)m * L.mstride;
     for (int q = t; q < nown; q += kBT) {

@@ -894,27 +894,43 @@ __global__ void __launch_bounds__(V == 1 ? 32 * NCW + 32 : 128 + 32 * V * NCW, V
 // get from u*'s mirrored ghost rows (zero boundary flux, mu_phi(-1) = mu_phi(0), phi*(-1) = phi*(0),
 // rho*(-1) = rho*(0), rho* above the top = the reservoir row), so results are bitwise those of
 // the stage kernels.  Single-domain contexts only.
-template <typename real, int NCW, int SI, int SU, int MOB, int FE, int MINB>
-__global__ void __launch_bounds__(32 * (2 * NCW + 1), MINB) ws_kernel(
+__host__ __device__ constexpr int ws_packed_cap(int V, int NCW) { return (65536 / (128 + 64 * V * NCW)) / 8 * 8; }
+__host__ __device__ constexpr int ws_packed_regs(int V, int NCW) {
+    return ((ws_packed_cap(V, NCW) * (128 + 64 * V * NCW) - 24 * 128) / (64 * V * NCW)) / 8 * 8 > 248
+               ? 248
+               : ((ws_packed_cap(V, NCW) * (128 + 64 * V * NCW) - 24 * 128) / (64 * V * NCW)) / 8 * 8;
+}
+
+// Packed variant (V > 1): as pair_kernel's -- V blocks per CTA, their producers in warpgroup 0
+// (setmaxnreg.dec), their 2 NCW compute warps each in the other warpgroups (setmaxnreg.inc).
+template <typename real, int NCW, int SI, int SU, int MOB, int FE, int MINB, int V>
+__global__ void __launch_bounds__(V == 1 ? 32 * (2 * NCW + 1) : 128 + 64 * V * NCW, V == 1 ? MINB : 1) ws_kernel(
     Layout L, KC<real> k, KC<real> k2, const __grid_constant__ CUtensorMap mapIn, real *out,
-    const real *__restrict__ vel, int Wo, int G) {
+    const real *__restrict__ vel, int Wo, int G, int NB) {
+    static_assert(V == 1 || (V <= 4 && (2 * V * NCW) % 4 == 0), "packed blocks fill whole warpgroups");
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int bx = Wo + 2 * kPairHalo;
     const int in_el = ((3 * bx * (int)sizeof(real) + 127) / 128 * 128) / (int)sizeof(real);
     const int us_el = ((6 * bx * (int)sizeof(real) + 127) / 128 * 128) / (int)sizeof(real);
     unsigned char *base_sm = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
-    real *ring = reinterpret_cast<real *>(base_sm);
+    const int t = threadIdx.x;
+    const int warp = t >> 5, lane = t & 31;
+    const bool producer = V == 1 ? warp == 2 * NCW : warp < 4;
+    const int v = V == 1 ? 0 : (producer ? warp : (warp - 4) / (2 * NCW));
+    const int cw = V == 1 ? warp : (warp - 4) - v * 2 * NCW;   // < NCW: stage-1 warp, else stage 2
+    const size_t vbytes = ((size_t)SI * in_el * sizeof(real) + (size_t)SU * us_el * sizeof(real) + 64 * sizeof(real) +
+                           (size_t)(2 * SI + 2 * SU) * 8 + 127) / 128 * 128;
+    unsigned char *reg = V == 1 ? base_sm : base_sm + 64 * 8 + (size_t)(v < V ? v : 0) * vbytes;
+    real *ring = reinterpret_cast<real *>(reg);
     real *usr = ring + (size_t)SI * in_el;
     uint64_t *full_in = reinterpret_cast<uint64_t *>(usr + (size_t)SU * us_el + 64);
     uint64_t *empty_in = full_in + SI;
     uint64_t *us_full = empty_in + SI;
     uint64_t *us_empty = us_full + SU;
-    double *etab = reinterpret_cast<double *>(us_empty + SU);
+    double *etab = V == 1 ? reinterpret_cast<double *>(us_empty + SU) : reinterpret_cast<double *>(base_sm);
     load_exp_table(etab);
 
-    const int t = threadIdx.x;
-    const int warp = t >> 5, lane = t & 31;
-    if (t == 0) {
+    if (V == 1 ? t == 0 : (producer && warp < V && lane == 0)) {
         for (int q = 0; q < SI; ++q) {
             mbar_init(&full_in[q], 1);
             mbar_init(&empty_in[q], NCW);
@@ -928,14 +944,16 @@ __global__ void __launch_bounds__(32 * (2 * NCW + 1), MINB) ws_kernel(
     __syncthreads();
 
     const int nx = L.nx;
-    const Sched sch = make_sched(L, Wo, G);
+    const int vb = V == 1 ? (int)blockIdx.x : (int)blockIdx.x * V + v;
     const uint32_t box_bytes = (uint32_t)(3 * bx * sizeof(real));
     constexpr int LEAD = 4, TRAIL = 4;
     const unsigned FULL = 0xffffffffu;
 
-    if (warp == 2 * NCW) {
+    if (producer) {
         // ------------------------------- producer -------------------------------
-        if (lane != 0) return;
+        if (V > 1) asm volatile("setmaxnreg.dec.sync.aligned.u32 24;" ::: "memory");
+        if (lane != 0 || v >= V) return;
+        const Sched sch = make_sched(L, Wo, G, vb, NB);
         prefetch_tmap(&mapIn);
         uint32_t g = 0;
         int64_t pos = sch.lo;
@@ -953,9 +971,11 @@ __global__ void __launch_bounds__(32 * (2 * NCW + 1), MINB) ws_kernel(
         return;
     }
 
-    if (warp < NCW) {
+    if (V > 1) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(ws_packed_regs(V, NCW)) : "memory");
+    const Sched sch = make_sched(L, Wo, G, vb, NB);
+    if (cw < NCW) {
         // --------------------------- stage-1 warps ------------------------------
-        const int cx = kPairCols * warp + 2 * lane - 4;       // strip column of the lane's left column
+        const int cx = kPairCols * cw + 2 * lane - 4;         // strip column of the lane's left column
         const int ci = kPairHalo + cx;
         const bool wr = lane >= 1 && lane <= 30;               // writes u* columns [60 w - 2, 60 w + 58)
         int sidx = 0, uidx = 0;
@@ -1035,7 +1055,7 @@ __global__ void __launch_bounds__(32 * (2 * NCW + 1), MINB) ws_kernel(
     }
 
     // --------------------------- stage-2 warps ---------------------------------
-    const int w2 = warp - NCW;
+    const int w2 = cw - NCW;
     const int cx = kPairCols * w2 + 2 * lane - 2;
     const int ci = kPairHalo + cx;
     int uidx = 0;
@@ -1271,15 +1291,22 @@ cudaError_t launch_pair(const Layout &L, const StreamPlan &P, const KC<real> &k,
 }
 
 // Warp-specialised step kernel: NCW stage-1 + NCW stage-2 warps + 1 producer per block.
+#ifndef PF_WS_WG
+#define PF_WS_WG 1          // packed ws blocks (setmaxnreg), fp64
+#endif
 template <typename real, int NCW>
 struct WsCfg {
     static constexpr int minb = NCW <= 2 ? 3 : 2;
     static constexpr int SI = 8, SU = 6;
+    static constexpr int V = (PF_WS_WG && sizeof(real) == 8 && (2 * minb * NCW) % 4 == 0) ? minb : 1;
 };
 
 template <typename real>
-size_t ws_smem_bytes(int bx, int SI, int SU) {
+size_t ws_smem_bytes(int bx, int SI, int SU, int V) {
     const size_t in_b = (3 * bx * sizeof(real) + 127) / 128 * 128, us_b = (6 * bx * sizeof(real) + 127) / 128 * 128;
+    if (V > 1)
+        return 128 + 64 * 8 +
+               (size_t)V * ((SI * in_b + SU * us_b + 64 * sizeof(real) + (size_t)(2 * SI + 2 * SU) * 8 + 127) / 128 * 128);
     return 128 + SI * in_b + SU * us_b + 64 * sizeof(real) + (size_t)(2 * SI + 2 * SU) * 8 + 64 * 8;
 }
 
@@ -1287,11 +1314,12 @@ template <typename real, int NCW, int MOB, int FE>
 cudaError_t launch_ws_k(const Layout &L, const StreamPlan &P, const KC<real> &k, const KC<real> &k2, real *out,
                         const real *vel, cudaStream_t s) {
     using C = WsCfg<real, NCW>;
-    const size_t smem = ws_smem_bytes<real>(P.fbox, C::SI, C::SU);
+    constexpr int V = C::V;
+    const size_t smem = ws_smem_bytes<real>(P.fbox, C::SI, C::SU, V);
     static int occ = -1, nsm = 0;
     static size_t smem_set = 0;
-    auto kern = ws_kernel<real, NCW, C::SI, C::SU, MOB, FE, C::minb>;
-    const int threads = 32 * (2 * NCW + 1);
+    auto kern = ws_kernel<real, NCW, C::SI, C::SU, MOB, FE, C::minb, V>;
+    const int threads = V == 1 ? 32 * (2 * NCW + 1) : 128 + 64 * V * NCW;
     if (smem > smem_set) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
@@ -1302,13 +1330,19 @@ cudaError_t launch_ws_k(const Layout &L, const StreamPlan &P, const KC<real> &k,
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        if (V > 1) {   // the compute warps' setmaxnreg.inc must be satisfiable from the CTA's pool
+            cudaFuncAttributes fa;
+            cudaError_t e = cudaFuncGetAttributes(&fa, kern);
+            if (e != cudaSuccess) return e;
+            if (fa.numRegs * threads - 24 * 128 < ws_packed_regs(V, NCW) * 64 * V * NCW) return cudaErrorInvalidConfiguration;
+        }
         cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
         if (e != cudaSuccess) return e;
         if (occ < 1) occ = 1;
     }
     const int64_t T = (int64_t)L.members * (L.r1 - L.r0);
     const int64_t minrows = 24;
-    int64_t B = (int64_t)occ * nsm;
+    int64_t B = (int64_t)occ * nsm * V;   // (virtual) blocks
     int64_t G = B / P.fstrips;
     if (G > (T + minrows - 1) / minrows) G = (T + minrows - 1) / minrows;
     if (G >= 4) {
@@ -1319,7 +1353,9 @@ cudaError_t launch_ws_k(const Layout &L, const StreamPlan &P, const KC<real> &k,
         if (B > (R_ + minrows - 1) / minrows) B = (R_ + minrows - 1) / minrows;
     }
     if (B < 1) B = 1;
-    kern<<<(unsigned)B, threads, smem, s>>>(L, k, k2, P.fmapU, out, vel, P.fWo, (int)G);
+    const int NB = (int)B;
+    B = (B + V - 1) / V;
+    kern<<<(unsigned)B, threads, smem, s>>>(L, k, k2, P.fmapU, out, vel, P.fWo, (int)G, NB);
     return cudaGetLastError();
 }
 
@@ -1531,16 +1567,21 @@ cudaError_t launch_persistent_t(const Layout &L, const KC<real> &k1, const KC<re
                                 const real *vel, int64_t nsteps, cudaStream_t s) {
     const int64_t cells = (int64_t)L.nx * L.ny_loc * L.members;
     static const int step = env_int("PF_PERSIST_STEP", 1);
-    if (step) {   // one grid barrier per step (tile_step): 32 x 4 tiles up to 2^14 cells, 32 x 8 above;
-                  // 512 threads per block up to 2^16 cells (shorter per-phase loops), 256 above
+    if (step) {   // one grid barrier per step (tile_step): 32 x 4 tiles / 512 threads up to 2^14 cells,
+                  // 32 x 16 / 1024 up to 2^16, 32 x 8 / 256 above
 #ifdef PF_STEP_TBY6
-        static const int tby = env_int("PF_STEP_TBY", 0);   // experiment: force 4 / 6 / 8-row tiles
+        static const int tby = env_int("PF_STEP_TBY", 0);   // experiment: force a tile shape
         if (tby == 4) return launch_persistent_step<real, MOB, FE, 4, 512>(L, k1, k2, U, Us, vel, nsteps, s);
         if (tby == 6) return launch_persistent_step<real, MOB, FE, 6, 512>(L, k1, k2, U, Us, vel, nsteps, s);
         if (tby == 8) return launch_persistent_step<real, MOB, FE, 8, 512>(L, k1, k2, U, Us, vel, nsteps, s);
+        if (tby == 9) return launch_persistent_step<real, MOB, FE, 8, 544>(L, k1, k2, U, Us, vel, nsteps, s);
+        if (tby == 16) return launch_persistent_step<real, MOB, FE, 16, 1024>(L, k1, k2, U, Us, vel, nsteps, s);
+        if (tby == 12) return launch_persistent_step<real, MOB, FE, 12, 704>(L, k1, k2, U, Us, vel, nsteps, s);
 #endif
         if (cells <= (int64_t)1 << PF_STEP_TBY4_LOG2) return launch_persistent_step<real, MOB, FE, 4, 512>(L, k1, k2, U, Us, vel, nsteps, s);
-        if (cells <= (int64_t)1 << 16) return launch_persistent_step<real, MOB, FE, 8, 512>(L, k1, k2, U, Us, vel, nsteps, s);
+        // 2^14 .. 2^16 cells (configs[1]): 32 x 16 tiles with 1024 threads, so that every phase of
+        // tile_step is one pass over its cells (32 x 8 / 512: 9.2 G on configs[1], 16 / 1024: 10.5 G)
+        if (cells <= (int64_t)1 << 16) return launch_persistent_step<real, MOB, FE, 16, 1024>(L, k1, k2, U, Us, vel, nsteps, s);
         return launch_persistent_step<real, MOB, FE, 8, 256>(L, k1, k2, U, Us, vel, nsteps, s);
     }
     // one grid barrier per stage (round 1): 32 x 4 tiles up to 2^17 cells, 32 x 16 above
