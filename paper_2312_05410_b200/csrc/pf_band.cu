@@ -62,7 +62,7 @@ struct BandGeo {
 };
 
 #ifndef PF_BAND_P2P
-#define PF_BAND_P2P 1   // halo rows by st.async + per-parity mbarriers instead of a cluster barrier per stage
+#define PF_BAND_P2P 0   // 1: halo rows by st.async + per-parity mbarriers instead of a cluster barrier per stage (measured slower)
 #endif
 __device__ __forceinline__ uint32_t smem_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 // shared::cluster address of the same location in CTA `rank` of the cluster
