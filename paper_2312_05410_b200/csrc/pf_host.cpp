@@ -269,6 +269,8 @@ struct pf_ctx {
     bool overlap = false;                 // band / exchange / interior schedule in use
     bool fused = false;                   // one-pass step kernel in use (kernel_path 5)
     bool persistent = false;              // small-grid cooperative tile kernel (kernel_path 7)
+    unsigned *pflags = nullptr;           // persistent step kernel: per-tile step flags (neighbour sync)
+    uint32_t pepoch = 0;                  // ... steps its flags have counted so far
     bool band = false;                    // small-grid band kernel (kernel_path 6 / auto, pf_band.cu)
     pf::BandPlan bplan;
     ncclComm_t comm = nullptr;
@@ -370,6 +372,7 @@ void destroy(pf_ctx *c) {
         cudaFree(s.diag);
     }
     cudaFree(c->vel);
+    cudaFree(c->pflags);
     cudaFree(c->staging);
     if (c->h_diag) cudaFreeHost(c->h_diag);
     for (auto e : c->ev_pool) cudaEventDestroy(e);
@@ -745,6 +748,15 @@ pf_status create_common(const pf_params *p, int mode, int rank, int nranks, cons
         }
         c->persistent = small && !c->band &&
                         (p->kernel_path == 7 || (p->kernel_path == 0 && cells <= kPersistentCells));
+        if (c->persistent) {   // one flag per tile of the finest tiling (32 x 4)
+            const size_t nflags = (size_t)((p->nx + 31) / 32) * ((p->ny + 3) / 4) * p->n_members;
+            if (cudaMalloc((void **)&c->pflags, nflags * sizeof(unsigned)) != cudaSuccess ||
+                cudaMemsetAsync(c->pflags, 0, nflags * sizeof(unsigned), c->stream) != cudaSuccess) {
+                cudaGetLastError();
+                c->err = "cudaMalloc of the persistent kernel's tile flags failed";
+                return fail(PF_ERR_NOMEM);
+            }
+        }
     }
     c->ny_host = mode == kNccl ? rows : p->ny;
     c->y_host0 = mode == kNccl ? rank * rows : 0;
@@ -1038,7 +1050,9 @@ pf_status pf_step(pf_ctx *c, int64_t n) {
         if (c->persistent && !c->prof && chunk > 0) {
             Nvtx nv("pf persistent kernel (small grid)");
             Slab &S = c->slabs[0];
-            CK(c, pf::launch_persistent(c->p.precision, S.L, c->K, S.U, S.Us, c->vel, c->p.dt, chunk, c->stream));
+            CK(c, pf::launch_persistent(c->p.precision, S.L, c->K, S.U, S.Us, c->vel, c->p.dt, chunk, c->pflags,
+                                        c->pepoch, c->stream));
+            c->pepoch += (uint32_t)chunk;
             CK(c, pf::launch_fill_ghosts(c->p.precision, S.L, c->p.rho_in, S.U, c->stream));
             c->launches += 1 + pf::kFillLaunches;
             done = chunk;

@@ -104,8 +104,10 @@ cudaError_t launch_fused(int precision, const Layout &L, const StreamPlan &P, co
                          double dt, cudaStream_t s);
 // Small-grid path: nsteps midpoint steps of every member in one cooperative launch (U holds the
 // state before and after; owned cells only, the ghost frame is left stale).
+// flags: one unsigned per tile (zeroed once; nullptr = a grid barrier per step), epoch: the steps
+// counted on them by earlier launches of this ctx.
 cudaError_t launch_persistent(int precision, const Layout &L, const Coef &K, void *U, void *Us, const void *vel,
-                              double dt, int64_t nsteps, cudaStream_t s);
+                              double dt, int64_t nsteps, unsigned *flags, uint32_t epoch, cudaStream_t s);
 // Small-grid band path (pf_band.cu): every member is one thread-block cluster of <= 16 blocks,
 // each block a band of >= 2 full-width rows held in shared memory for a whole launch; halo rows are
 // pushed into the neighbours' shared memory (DSMEM) between two cluster barriers per stage.

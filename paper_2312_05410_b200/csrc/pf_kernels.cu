@@ -376,10 +376,26 @@ __global__ void __launch_bounds__(NT) persistent_kernel(Layout L, KC<real> k1, K
 
 // Small-grid path, one grid barrier per STEP: tile_step (both stages on a tile with a 4-cell u^n
 // halo) ping-pongs between U and Us; after an odd number of steps the result is copied back to U.
+//
+// Step ordering (flags != nullptr, PF_STEP_FLAGS): instead of a grid barrier per step, a tile of
+// step s waits only for the (up to) 8 tiles its 4-cell u^n halo reaches to have finished step s-1
+// -- flags[tile] counts the steps a tile has completed (release store after the tile's outputs;
+// acquire polls, one thread per neighbour).  That also orders the buffer reuse: a tile writes into
+// the buffer its neighbours read in step s-1 only after they finished that step.  (Grid barrier:
+// ~1.2 us per step, 22% of the configs[1] kernel's stall samples.)
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned *p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 template <typename real, int MOB, int FE, int TBY, int kStepNT>
 __global__ void __launch_bounds__(kStepNT) persistent_step_kernel(Layout L, KC<real> k1, KC<real> k2, real *U,
                                                                   real *Us, const real *__restrict__ vel,
-                                                                  int64_t nsteps) {
+                                                                  int64_t nsteps, unsigned *flags, uint32_t epoch) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     TileStepSmem<real, TBY> &ts = *reinterpret_cast<TileStepSmem<real, TBY> *>(smem_raw);
     __shared__ double etab[64];
@@ -393,10 +409,26 @@ __global__ void __launch_bounds__(kStepNT) persistent_step_kernel(Layout L, KC<r
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
             const int m = t / (tx * ty), r = t - m * (tx * ty);
             const int by = r / tx, bxi = r - by * tx;
+            if (flags && s > 0) {   // the neighbours' step s-1 (the previous launch: stream order)
+                if (threadIdx.x < 9 && threadIdx.x != 4) {
+                    const int dy = (int)threadIdx.x / 3 - 1, dx = (int)threadIdx.x % 3 - 1;
+                    const int ny_ = by + dy, nx_ = (bxi + dx + tx) % tx;
+                    if (ny_ >= 0 && ny_ < ty) {
+                        const unsigned *f = flags + (m * ty + ny_) * tx + nx_;
+                        const unsigned want = epoch + (unsigned)s;
+                        while ((int)(ld_acquire_u32(f) - want) < 0) {
+                        }
+                    }
+                }
+                __syncthreads();
+            }
             tile_step<real, MOB, FE, TBY, kStepNT>(L, k1, k2, in, out, vel, etab, ts, L.m0 + m, bxi * BX, by * TBY);
+            // tile_step ended with a CTA barrier, so the release (cumulative) covers the whole tile
+            if (flags && threadIdx.x == 0) st_release_u32(flags + t, epoch + (unsigned)s + 1u);
         }
-        grid.sync();
+        if (!flags) grid.sync();
     }
+    if (flags) grid.sync();   // the copy-back below reads every tile
     if (nsteps & 1) {   // the last step wrote Us: owned cells back to U
         const int64_t per = (int64_t)L.ny_loc * L.nx, total = per * L.members;
         for (int64_t q = (int64_t)blockIdx.x * kStepNT + threadIdx.x; q < total; q += (int64_t)gridDim.x * kStepNT) {
@@ -1517,7 +1549,7 @@ PF_PAIR_ENTRY(pair_stage2_f32, float, true)
 #if PF_IN(0)
 template <typename real, int MOB, int FE, int TBY, int kStepNT>
 cudaError_t launch_persistent_step(const Layout &L, const KC<real> &k1, const KC<real> &k2, real *U, real *Us,
-                                   const real *vel, int64_t nsteps, cudaStream_t s) {
+                                   const real *vel, int64_t nsteps, unsigned *flags, uint32_t epoch, cudaStream_t s) {
     static int occ = -1, nsm = 0;
     auto kern = persistent_step_kernel<real, MOB, FE, TBY, kStepNT>;
     const size_t smem = sizeof(TileStepSmem<real, TBY>);
@@ -1536,7 +1568,9 @@ cudaError_t launch_persistent_step(const Layout &L, const KC<real> &k1, const KC
     const int blocks = (int)(ntiles < maxb ? ntiles : maxb);
     Layout Lc = L;
     KC<real> a1 = k1, a2 = k2;
-    void *args[] = {&Lc, &a1, &a2, &U, &Us, (void *)&vel, &nsteps};
+    static const int use_flags = env_int("PF_STEP_FLAGS", 0);   // measured: +0-6% at 256^2, -3% at 128^2 / 512^2
+    unsigned *fl = use_flags ? flags : nullptr;
+    void *args[] = {&Lc, &a1, &a2, &U, &Us, (void *)&vel, &nsteps, &fl, &epoch};
     return cudaLaunchCooperativeKernel((const void *)kern, blocks, kStepNT, args, smem, s);
 }
 
@@ -1564,25 +1598,25 @@ cudaError_t launch_persistent_b(const Layout &L, const KC<real> &k1, const KC<re
 
 template <typename real, int MOB, int FE>
 cudaError_t launch_persistent_t(const Layout &L, const KC<real> &k1, const KC<real> &k2, real *U, real *Us,
-                                const real *vel, int64_t nsteps, cudaStream_t s) {
+                                const real *vel, int64_t nsteps, unsigned *flags, uint32_t epoch, cudaStream_t s) {
     const int64_t cells = (int64_t)L.nx * L.ny_loc * L.members;
     static const int step = env_int("PF_PERSIST_STEP", 1);
     if (step) {   // one grid barrier per step (tile_step): 32 x 4 tiles / 512 threads up to 2^14 cells,
                   // 32 x 16 / 1024 up to 2^16, 32 x 8 / 256 above
 #ifdef PF_STEP_TBY6
         static const int tby = env_int("PF_STEP_TBY", 0);   // experiment: force a tile shape
-        if (tby == 4) return launch_persistent_step<real, MOB, FE, 4, 512>(L, k1, k2, U, Us, vel, nsteps, s);
-        if (tby == 6) return launch_persistent_step<real, MOB, FE, 6, 512>(L, k1, k2, U, Us, vel, nsteps, s);
-        if (tby == 8) return launch_persistent_step<real, MOB, FE, 8, 512>(L, k1, k2, U, Us, vel, nsteps, s);
-        if (tby == 9) return launch_persistent_step<real, MOB, FE, 8, 544>(L, k1, k2, U, Us, vel, nsteps, s);
-        if (tby == 16) return launch_persistent_step<real, MOB, FE, 16, 1024>(L, k1, k2, U, Us, vel, nsteps, s);
-        if (tby == 12) return launch_persistent_step<real, MOB, FE, 12, 704>(L, k1, k2, U, Us, vel, nsteps, s);
+        if (tby == 4) return launch_persistent_step<real, MOB, FE, 4, 512>(L, k1, k2, U, Us, vel, nsteps, flags, epoch, s);
+        if (tby == 6) return launch_persistent_step<real, MOB, FE, 6, 512>(L, k1, k2, U, Us, vel, nsteps, flags, epoch, s);
+        if (tby == 8) return launch_persistent_step<real, MOB, FE, 8, 512>(L, k1, k2, U, Us, vel, nsteps, flags, epoch, s);
+        if (tby == 9) return launch_persistent_step<real, MOB, FE, 8, 544>(L, k1, k2, U, Us, vel, nsteps, flags, epoch, s);
+        if (tby == 16) return launch_persistent_step<real, MOB, FE, 16, 1024>(L, k1, k2, U, Us, vel, nsteps, flags, epoch, s);
+        if (tby == 12) return launch_persistent_step<real, MOB, FE, 12, 704>(L, k1, k2, U, Us, vel, nsteps, flags, epoch, s);
 #endif
-        if (cells <= (int64_t)1 << PF_STEP_TBY4_LOG2) return launch_persistent_step<real, MOB, FE, 4, 512>(L, k1, k2, U, Us, vel, nsteps, s);
+        if (cells <= (int64_t)1 << PF_STEP_TBY4_LOG2) return launch_persistent_step<real, MOB, FE, 4, 512>(L, k1, k2, U, Us, vel, nsteps, flags, epoch, s);
         // 2^14 .. 2^16 cells (configs[1]): 32 x 16 tiles with 1024 threads, so that every phase of
         // tile_step is one pass over its cells (32 x 8 / 512: 9.2 G on configs[1], 16 / 1024: 10.5 G)
-        if (cells <= (int64_t)1 << 16) return launch_persistent_step<real, MOB, FE, 16, 1024>(L, k1, k2, U, Us, vel, nsteps, s);
-        return launch_persistent_step<real, MOB, FE, 8, 256>(L, k1, k2, U, Us, vel, nsteps, s);
+        if (cells <= (int64_t)1 << 16) return launch_persistent_step<real, MOB, FE, 16, 1024>(L, k1, k2, U, Us, vel, nsteps, flags, epoch, s);
+        return launch_persistent_step<real, MOB, FE, 8, 256>(L, k1, k2, U, Us, vel, nsteps, flags, epoch, s);
     }
     // one grid barrier per stage (round 1): 32 x 4 tiles up to 2^17 cells, 32 x 16 above
     if (cells <= (int64_t)1 << 17) return launch_persistent_b<real, MOB, FE, 4>(L, k1, k2, U, Us, vel, nsteps, s);
@@ -1590,7 +1624,7 @@ cudaError_t launch_persistent_t(const Layout &L, const KC<real> &k1, const KC<re
 }
 
 cudaError_t launch_persistent(int precision, const Layout &L, const Coef &K, void *U, void *Us, const void *vel,
-                              double dt, int64_t nsteps, cudaStream_t s) {
+                              double dt, int64_t nsteps, unsigned *flags, uint32_t epoch, cudaStream_t s) {
     cudaError_t te = upload_exp_table();
     if (te != cudaSuccess) return te;
     if (precision == 0) {
@@ -1599,14 +1633,14 @@ cudaError_t launch_persistent(int precision, const Layout &L, const Coef &K, voi
                                                                                         : launch_persistent_t<double, 2, 1>)
                             : (k1.mob == 0 ? launch_persistent_t<double, 0, 0> : k1.mob == 1 ? launch_persistent_t<double, 1, 0>
                                                                                         : launch_persistent_t<double, 2, 0>);
-        return f(L, k1, k2, (double *)U, (double *)Us, (const double *)vel, nsteps, s);
+        return f(L, k1, k2, (double *)U, (double *)Us, (const double *)vel, nsteps, flags, epoch, s);
     }
     const KC<float> k1 = make_kc<float>(K, 0.5 * dt), k2 = make_kc<float>(K, dt);
     auto f = k1.fe == 1 ? (k1.mob == 0 ? launch_persistent_t<float, 0, 1> : k1.mob == 1 ? launch_persistent_t<float, 1, 1>
                                                                                    : launch_persistent_t<float, 2, 1>)
                         : (k1.mob == 0 ? launch_persistent_t<float, 0, 0> : k1.mob == 1 ? launch_persistent_t<float, 1, 0>
                                                                                    : launch_persistent_t<float, 2, 0>);
-    return f(L, k1, k2, (float *)U, (float *)Us, (const float *)vel, nsteps, s);
+    return f(L, k1, k2, (float *)U, (float *)Us, (const float *)vel, nsteps, flags, epoch, s);
 }
 
 void swap_plan_buffers(StreamPlan &P) {
