@@ -362,7 +362,15 @@ def run_ours(args):
     stage_ms = prof[0] + prof[2]
     nslab_launch = max(1.0, (n1 + n2))
     alg_bytes = cells_local * esz * (VALUES_STAGE1 * n1 + VALUES_STAGE2 * n2)
-    achieved = alg_bytes / (stage_ms * 1e-3) / 1e9 if stage_ms > 0 else None
+    achieved_bracketed = alg_bytes / (stage_ms * 1e-3) / 1e9 if stage_ms > 0 else None
+    # the stage kernels' average launch duration IN the timed region: the timed region holds the
+    # 2K stage launches (back to back, programmatic dependent launch) and the diagnostics launches
+    # of the blow-up checks; the latter's event time comes from the bracketed pass.  (Bracketing
+    # every stage launch with events breaks the dependent-launch overlap, which makes the
+    # bracketed launches 3-7% slower than in the timed step: reported beside, as achieved_bracketed.)
+    diag_ms = prof[4] if prof[5] > 0 else 0.0
+    stage_ms_live = ms - diag_ms
+    achieved = alg_bytes / (stage_ms_live * 1e-3) / 1e9 if stage_ms_live > 0 else achieved_bracketed
     peak, peak_src = _peaks()
     key = f"cfg{cfg}_n{ws}"
     tr = _traffic(key)
@@ -420,8 +428,14 @@ def run_ours(args):
                          "frac": (achieved / peak) if achieved else None, "traffic": tr,
                          "kernel": "pair_kernel (both midpoint stages; stage 1 and stage 2 launches)",
                          "algorithmic_bytes_per_launch": alg_bytes / nslab_launch,
+                         "avg_launch_ms": stage_ms_live / nslab_launch,
+                         "timing": "stage kernels' share of the timed region: (timed ms - diagnostics ms) / "
+                                   "stage launches, CUDA events on the ctx stream",
+                         "achieved_bracketed": achieved_bracketed,
+                         "avg_launch_ms_bracketed": stage_ms / nslab_launch,
+                         "diag_ms": diag_ms, "stage_launches": nslab_launch,
                          "step_share": (stage_ms / args.steps) / (ms_max / args.steps) if ms_max > 0 else None,
-                         "avg_launch_ms": stage_ms / nslab_launch, "peak_source": peak_src},
+                         "peak_source": peak_src},
             "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clk.summary(),

@@ -312,6 +312,11 @@ pf_status pf_debug_guards(pf_ctx *ctx, int64_t *guard_bytes, int64_t *corrupted)
  * out: host memory the caller owns.  Returns a cudaError_t value (0 = success). */
 int pf_debug_trace(long long *out);
 int pf_debug_block_spans(long long *out);
+/* Diagnostic of a PF_TRACE build: the small-grid step kernel's (kernel_path 7) phase timeline of
+ * its last launch, out[160 blocks][64 steps][8] int64 global-timer ns: [0] tile start, [1] u^n
+ * loaded, [2] stage-1 mu/M, [3] u*, [4] stage-2 mu/M, [5] tile written, [6] grid barrier passed.
+ * Zeros in a normal build.  out: host memory the caller owns.  Returns a cudaError_t value. */
+int pf_debug_step_trace(long long *out);
 
 /* Release everything the ctx owns.  NULL-safe.  Slab mode: collective (NCCL teardown). */
 void pf_free(pf_ctx *ctx);

@@ -205,11 +205,32 @@ struct TileStepSmem {
     real m2c[TBY + 2][BX + 2], m2p[TBY + 2][BX + 2], M2[TBY + 2][BX + 2]; // stage-2 mu / M: rows -1 .. TBY
 };
 
+// Phase timeline of the step kernel (diagnostic build, -DPF_TRACE=1; read with
+// pf_debug_step_trace): per block and step s < kStepTraceSteps, thread 0's global-timer stamps at
+// [0] tile start, [1] u^n loaded, [2] stage-1 a2, [3] u*, [4] stage-2 a2, [5] tile done, [6] grid
+// barrier passed -- each after the phase's CTA barrier.
+#ifndef PF_TRACE
+#define PF_TRACE 0
+#endif
+constexpr int kStepTraceBlocks = 160, kStepTraceSteps = 64;
+static __device__ long long g_strace[kStepTraceBlocks][kStepTraceSteps][8];
+__device__ __forceinline__ long long step_gtimer() {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define PF_STEP_STAMP(trs, k)                                                                    \
+    do {                                                                                          \
+        if (PF_TRACE && (trs) >= 0 && threadIdx.x == 0) g_strace[blockIdx.x][(trs)][(k)] = step_gtimer(); \
+    } while (0)
+
 template <typename real, int MOB, int FE, int TBY, int NTH>
 __device__ __forceinline__ void tile_step(const Layout &L, const KC<real> &k1, const KC<real> &k2,
                                           const real *__restrict__ in, real *out, const real *__restrict__ vel,
-                                          const double *etab, TileStepSmem<real, TBY> &ts, int m, int tx0, int ty0) {
+                                          const double *etab, TileStepSmem<real, TBY> &ts, int m, int tx0, int ty0,
+                                          int trs = -1) {
     const int nx = L.nx;
+    PF_STEP_STAMP(trs, 0);
     const real *ic = in + m * L.mstride;
     const real *ip = ic + L.fstride;
     const real *ir = ip + L.fstride;
@@ -241,6 +262,7 @@ __device__ __forceinline__ void tile_step(const Layout &L, const KC<real> &k1, c
         ts.r0[sy][sx] = v;
     }
     __syncthreads();
+    PF_STEP_STAMP(trs, 1);
     // ---- stage 1, a2: mu / M of u^n on rows -3 .. TBY+2, columns -3 .. 34 ----
     PF_STEP_LOOP_HINT
     for (int t = threadIdx.x; t < (TBY + 6) * (BX + 6); t += NTH) {
@@ -255,6 +277,7 @@ __device__ __forceinline__ void tile_step(const Layout &L, const KC<real> &k1, c
         ts.M1[sy][sx] = M;
     }
     __syncthreads();
+    PF_STEP_STAMP(trs, 2);
     // ---- stage 1, a3-a5: u* on rows -2 .. TBY+1, columns -2 .. 33 (in-domain rows only) ----
     PF_STEP_LOOP_HINT
     for (int t = threadIdx.x; t < (TBY + 4) * (BX + 4); t += NTH) {
@@ -277,6 +300,7 @@ __device__ __forceinline__ void tile_step(const Layout &L, const KC<real> &k1, c
         ts.rs[sy][sx] = orr;
     }
     __syncthreads();
+    PF_STEP_STAMP(trs, 3);
     // ---- u*'s out-of-domain rows: its ghost rules (c, phi mirror; rho bottom mirror, top rho_in) ----
     if (L.y0 + ty0 - 2 < 0 || L.y0 + ty0 + TBY + 1 >= L.ny) {
         for (int t = threadIdx.x; t < (TBY + 4) * (BX + 4); t += NTH) {
@@ -305,6 +329,7 @@ __device__ __forceinline__ void tile_step(const Layout &L, const KC<real> &k1, c
         ts.M2[sy][sx] = M;
     }
     __syncthreads();
+    PF_STEP_STAMP(trs, 4);
     // ---- stage 2, a3-a5: u^{n+1} of the tile, base u^n ----
     const int lx = threadIdx.x & (BX - 1);
     const int gx = tx0 + lx;
@@ -330,6 +355,7 @@ __device__ __forceinline__ void tile_step(const Layout &L, const KC<real> &k1, c
         out[o + 2 * L.fstride] = orr;
     }
     __syncthreads();   // the tile's shared memory may be refilled next
+    PF_STEP_STAMP(trs, 5);
 }
 
 template <typename real, int MOB, int FE>
@@ -422,11 +448,16 @@ __global__ void __launch_bounds__(kStepNT) persistent_step_kernel(Layout L, KC<r
                 }
                 __syncthreads();
             }
-            tile_step<real, MOB, FE, TBY, kStepNT>(L, k1, k2, in, out, vel, etab, ts, L.m0 + m, bxi * BX, by * TBY);
+            const int trs = PF_TRACE && t == (int)blockIdx.x && blockIdx.x < kStepTraceBlocks && s < kStepTraceSteps
+                                ? (int)s : -1;
+            tile_step<real, MOB, FE, TBY, kStepNT>(L, k1, k2, in, out, vel, etab, ts, L.m0 + m, bxi * BX, by * TBY,
+                                                   trs);
             // tile_step ended with a CTA barrier, so the release (cumulative) covers the whole tile
             if (flags && threadIdx.x == 0) st_release_u32(flags + t, epoch + (unsigned)s + 1u);
         }
         if (!flags) grid.sync();
+        if (PF_TRACE && threadIdx.x == 0 && blockIdx.x < kStepTraceBlocks && s < kStepTraceSteps)
+            g_strace[blockIdx.x][s][6] = step_gtimer();
     }
     if (flags) grid.sync();   // the copy-back below reads every tile
     if (nsteps & 1) {   // the last step wrote Us: owned cells back to U
@@ -441,6 +472,18 @@ __global__ void __launch_bounds__(kStepNT) persistent_step_kernel(Layout L, KC<r
         }
     }
 }
+
+#if PF_IN(0)
+}  // namespace
+}  // namespace pf
+// Diagnostic: the step kernel's phase timeline of its last launch (PF_TRACE builds; zeros
+// otherwise): out[160 blocks][64 steps][8] int64 global-timer ns, see PF_STEP_STAMP.
+extern "C" int pf_debug_step_trace(long long *out) {
+    return (int)cudaMemcpyFromSymbol(out, pf::g_strace, sizeof(pf::g_strace));
+}
+namespace pf {
+namespace {
+#endif
 
 // ========================================================================================
 // Ghost frame (row a1 in memory)
