@@ -88,9 +88,17 @@ pf_status un_hybrid(un_ctx *ctx, pf_ctx *dns, int32_t n_dns, int64_t steps_betwe
 
 /* One bf16 3x3 'same' convolution on the tensor cores, for parity tests of the GEMM kernel alone:
  * in [npix = batch*H*W][cin] bf16 bits (NHWC), w [cout][9][cin] bf16 bits, out [npix][cout] fp32.
- * cin a multiple of 16, cout in {16, 32, 64, 128}; device pointers; runs on stream (or 0), async. */
+ * cin a multiple of 16, cout in {16, 32, 64, 128}; device pointers; runs on stream (or 0) and
+ * synchronises it.  The input is repacked on the device into the kernels' row-chunk activation
+ * layout ([b][y][chunk][x][8], unet.cu) before the convolution. */
 pf_status un_conv3x3(const uint16_t *in, int32_t batch, int32_t H, int32_t W, int32_t cin, const uint16_t *w,
                      int32_t cout, float *out, void *stream);
+
+/* Diagnostic of a UN_TRACE build (PF_NVCC_EXTRA=-DUN_TRACE=1): per CTA (160 slots) cycle sums of the
+ * row-tile convolution's roles since the last reset, out[160][8] = {MMA warp: full wait, acce wait,
+ * issue; producer: empty wait, copy issue; epilogue warp 0: accf wait, drain; iterations}.  Zeros
+ * in a normal build.  reset != 0 zeroes the record after reading.  Returns a cudaError_t value. */
+int un_debug_trace(unsigned long long *out, int reset);
 
 pf_status un_stream(un_ctx *ctx, void **stream);
 /* Kernel launches issued by this ctx so far. */

@@ -1,8 +1,12 @@
 // unet.cu -- NEXT-4 of SURVEY 8(f): inference of the temporally conditioned U-Net (PAPER.md section
 // 4.3; include/unet.h; readings R-29..R-35 of DESIGN.md 14).
 //
-// Layout: activations NHWC bf16 ([pixel][channel], pixel = (b * H + y) * W + x); conv outputs fp32
-// NHWC; GroupNorm statistics fp64.  Concatenation z (+) d is a channel-offset write into a buffer of
+// Layout: activations bf16 in ROW-CHUNK order [b][y][chunk][x][8]: the 8-channel chunk q of pixel
+// (b, y, x) of a C-channel buffer at ((((b * H + y) * (C / 8) + q) * W + x) * 8 (rc_off), so that one
+// chunk of one image row is W * 16 contiguous bytes -- the convolutions load their halo rows as
+// contiguous 2 KB bulk copies instead of 16-byte TMA box rows (round 2: the NHWC 5D TMA boxes
+// moved ~16 B per cycle per SM and bounded the 16-channel layers).  Conv outputs fp32 NHWC;
+// GroupNorm statistics fp64.  Concatenation z (+) d is a channel-offset write into a buffer of
 // 2C channels, so no copy is needed.
 //
 // Convolutions: implicit GEMMs on the 5th-generation tensor cores.
@@ -14,8 +18,9 @@
 //   warp specialised (loader warps, one MMA warp, four epilogue warps; mbarrier pipelines, no CTA
 //   barrier in the loop) and persistent:
 //   * conv3x3_rows_kernel (W a multiple of 128): a tile is 128 pixels of one image row; the three
-//     halo rows are loaded once (5D TMA boxes, or cp.async) and the A operand of each tap is a
-//     descriptor shifted by kx pixels into row plane ky; weights resident in shared memory;
+//     halo rows are loaded once (one 2 KB bulk copy per row and channel chunk) and the A operand of
+//     each tap is a descriptor shifted by kx pixels into row plane ky; weights resident in shared
+//     memory;
 //   * conv3x3_kernel (any shape): im2col gather of 144-element K blocks with cp.async (zero-fill =
 //     the 'same' padding), weights streamed with each block.
 //   Epilogue (conv_tile_out): tcgen05.ld 32x32b (one pixel per thread), fp32 NHWC stores and the
@@ -64,7 +69,31 @@ __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier
 // Waits of the loader and epilogue warps carry a suspend-time hint (the warp sleeps instead of
 // re-issuing try_wait, leaving issue slots to the others); the single MMA-issuing thread spins
 // (mbar_wait_spin), its wake-up latency is on the critical path.
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+#ifndef UN_WATCHDOG
+#define UN_WATCHDOG 0   // debug builds: bounded mbarrier waits that report (block, warp, tag) and trap
+#endif
+__device__ __forceinline__ bool mbar_try(uint64_t *bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __noinline__ void mbar_watchdog(uint64_t *bar, uint32_t parity, int tag) {
+    for (long long it = 0; !mbar_try(bar, parity); ++it)
+        if (it == (1ll << 26)) {
+            printf("UN_WATCHDOG block %d warp %d lane %d tag %d parity %u\n", (int)blockIdx.x, (int)(threadIdx.x >> 5),
+                   (int)(threadIdx.x & 31), tag, parity);
+            __trap();
+        }
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity, int tag = 0) {
+    if (UN_WATCHDOG) {
+        mbar_watchdog(bar, parity, tag);
+        return;
+    }
     asm volatile(
         "{\n\t.reg .pred p;\n"
         "WAIT_%=:\n\t"
@@ -73,7 +102,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         "r"(parity), "r"(1000000u)
         : "memory");
 }
-__device__ __forceinline__ void mbar_wait_spin(uint64_t *bar, uint32_t parity) {
+__device__ __forceinline__ void mbar_wait_spin(uint64_t *bar, uint32_t parity, int tag = 0) {
+    if (UN_WATCHDOG) {
+        mbar_watchdog(bar, parity, tag);
+        return;
+    }
     asm volatile(
         "{\n\t.reg .pred p;\n"
         "WAIT_%=:\n\t"
@@ -89,17 +122,37 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
 __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
-__device__ __forceinline__ void prefetch_tmap(const CUtensorMap *m) {
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
+// element offset of chunk q of pixel (row = b * H + y, x) in a row-chunk buffer of cqt chunks
+__host__ __device__ __forceinline__ int64_t rc_off(int64_t row, int x, int W, int cqt, int q) {
+    return ((row * cqt + q) * W + x) * 8;
 }
-__device__ __forceinline__ void tma_load_5d(uint32_t dst, const CUtensorMap *map, int c0, int c1, int c2, int c3, int c4,
-                                            uint64_t *bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, "
-        "%6}], [%7];" ::"r"(dst),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(bar))
-        : "memory");
+
+#ifndef UN_TRACE
+#define UN_TRACE 0   // diagnostic builds: per-CTA cycle sums of the row kernel's roles (un_debug_trace)
+#endif
+__device__ unsigned long long g_untrace[160][8];
+__device__ __forceinline__ long long un_clock() { return UN_TRACE ? clock64() : 0; }
+#define UN_TR_ADD(slot, v)                                                                  \
+    do {                                                                                    \
+        if (UN_TRACE && blockIdx.x < 160) atomicAdd(&g_untrace[blockIdx.x][(slot)], (unsigned long long)(v)); \
+    } while (0)
+
+__device__ __forceinline__ bool elect_one() {   // true in exactly one lane of the (converged) warp
+    uint32_t e;
+    asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\tselp.u32 %0, 1, 0, e;\n}" : "=r"(e));
+    return e != 0;
 }
+
+// 1D bulk copy global -> shared (cp.async.bulk, async proxy), completing `bytes` on mbarrier bar;
+// addresses 16-byte aligned, bytes a multiple of 16
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, int64_t src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+// 16-byte zeros for the bulk copies of out-of-image rows / pixels (one row plane of 130 pixels x
+// 8 chunks)
+__device__ __align__(128) uint4 g_zero16[130 * 8];
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
 
@@ -125,17 +178,24 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t 
 __host__ __device__ constexpr uint32_t idesc_bf16(int n) {
     return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(kBM >> 4) << 24);
 }
-__device__ __forceinline__ void umma(uint32_t tmem, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc) {
+// Warp-uniform forms: the whole warp executes them (descriptors computed warp-uniformly, so they
+// live in uniform registers) and one lane chosen by elect.sync issues the instruction.  A loop of
+// MMAs run by a single lane instead needs a register-to-uniform move and an election loop per MMA:
+// measured 60-250 cycles per M128 x N16 MMA against 39 this way (tools/mma_bench.cu).
+__device__ __forceinline__ void umma_e(uint32_t tmem, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc) {
     asm volatile(
-        "{\n\t.reg .pred p;\n\t"
+        "{\n\t.reg .pred p, e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
         "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem),
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem),
         "l"(ad), "l"(bd), "r"(idesc), "r"(acc)
         : "memory");
 }
-__device__ __forceinline__ void umma_commit(uint64_t *bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
-                 : "memory");
+__device__ __forceinline__ void umma_commit_e(uint64_t *bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(smem_u32(bar))
+        : "memory");
 }
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
     asm volatile(
@@ -157,6 +217,9 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
 constexpr int kKC = 18;
 constexpr int kProdWarps = 8;                        // loader warps of the warp-specialised kernels
 constexpr int kWsThreads = 32 * (kProdWarps + 5);   // + 4 epilogue warps + 1 MMA warp
+// row kernel: 3 groups of 4 epilogue warps (0-11), producer warp 12, MMA warp 13
+constexpr int kRowEpiGroups = 3, kRowProdWarp = 4 * kRowEpiGroups, kRowMmaWarp = kRowProdWarp + 1;
+constexpr int kRowThreads = 32 * (kRowMmaWarp + 1);
 
 template <int N>
 struct ConvCfg {
@@ -333,7 +396,8 @@ __global__ void __launch_bounds__(kWsThreads) conv3x3_kernel(const bf16 *__restr
         int ctl = -1;
         int64_t pc = 0;
         uint32_t vmask = 0;
-        const int64_t Wc = (int64_t)W * cin;
+        // row-chunk layout: tap (ky, kx), chunk cc of pixel (row, x) at pc + (ky - 1) Wc + (kx - 1) 8 + cc W 8
+        const int64_t Wc = (int64_t)W * cin, Wq = (int64_t)W * 8;
         for (int j = 0; j < nsteps; ++j) {
             const int s = j % S;
             if (j >= S) mbar_wait(&empty[s], (uint32_t)(j / S - 1) & 1u);
@@ -347,7 +411,7 @@ __global__ void __launch_bounds__(kWsThreads) conv3x3_kernel(const bf16 *__restr
                     const int b = (int)(p / HW);
                     const int rem = (int)(p - (int64_t)b * HW);
                     const int y = rem / W, x = rem - y * W;
-                    pc = p * cin;
+                    pc = rc_off((int64_t)b * H + y, x, W, cq, 0);
                     const uint32_t rows = (y > 0 ? 1u : 0u) | 2u | (y < H - 1 ? 4u : 0u);
                     const uint32_t cols = (x > 0 ? 1u : 0u) | 2u | (x < W - 1 ? 4u : 0u);
                     for (int ky = 0; ky < 3; ++ky)
@@ -358,19 +422,19 @@ __global__ void __launch_bounds__(kWsThreads) conv3x3_kernel(const bf16 *__restr
             const int g0 = kb * kKC + half;
             int tap = g0 / cq, cc = g0 - tap * cq;
             int ky = tap / 3, kx = tap - 3 * ky;
-            int64_t toff = (ky - 1) * Wc + (kx - 1) * cin;
+            int64_t toff = (ky - 1) * Wc + (kx - 1) * 8;
             for (int q = half; q < kKC; q += 2) {
                 const bool v = (vmask >> (ky * 3 + kx)) & 1u;
-                cp_async16(a0 + q * C::lbo_a + arow, v ? in + pc + toff + cc * 8 : in, v);
+                cp_async16(a0 + q * C::lbo_a + arow, v ? in + pc + toff + cc * Wq : in, v);
                 cc += 2;
                 if (cc >= cq) {
                     cc -= cq;
                     if (++kx == 3) {
                         kx = 0;
                         ++ky;
-                        toff += Wc - 2 * cin;
+                        toff += Wc - 16;
                     } else {
-                        toff += cin;
+                        toff += 8;
                     }
                 }
             }
@@ -383,24 +447,24 @@ __global__ void __launch_bounds__(kWsThreads) conv3x3_kernel(const bf16 *__restr
         }
     } else if (warp == MMAW) {
         // ------------------------------- MMA issuer -------------------------------
-        if (lane == 0)
-            for (int j = 0; j < nsteps; ++j) {
-                const int s = j % S, tl = j / nkb, kb = j - tl * nkb, b = tl & 1;
-                mbar_wait_spin(&full[s], (uint32_t)(j / S) & 1u);
-                if (kb == 0 && tl >= 2) mbar_wait_spin(&acce[b], (uint32_t)(tl / 2 - 1) & 1u);
-                tc_fence_after();
-                const uint32_t a0 = sbase + s * C::stage, b0 = a0 + C::a_bytes;
-                const uint32_t acc = tmem + (uint32_t)(b * N);
-                // descriptors advanced by adding (byte offset >> 4) to the start-address field
-                // (every address stays below 2^18, so the 14-bit field never carries)
-                const uint64_t da = sdesc(a0, C::lbo_a, 128), db = sdesc(b0, C::lbo_b, 128);
+        // the whole warp runs the loop; one elected lane issues (umma_e)
+        for (int j = 0; j < nsteps; ++j) {
+            const int s = j % S, tl = j / nkb, kb = j - tl * nkb, b = tl & 1;
+            mbar_wait_spin(&full[s], (uint32_t)(j / S) & 1u);
+            if (kb == 0 && tl >= 2) mbar_wait_spin(&acce[b], (uint32_t)(tl / 2 - 1) & 1u);
+            tc_fence_after();
+            const uint32_t a0 = sbase + s * C::stage, b0 = a0 + C::a_bytes;
+            const uint32_t acc = tmem + (uint32_t)(b * N);
+            // descriptors advanced by adding (byte offset >> 4) to the start-address field
+            // (every address stays below 2^18, so the 14-bit field never carries)
+            const uint64_t da = sdesc(a0, C::lbo_a, 128), db = sdesc(b0, C::lbo_b, 128);
 #pragma unroll
-                for (int k = 0; k < kKC / 2; ++k)
-                    umma(acc, da + (uint64_t)((2 * k * C::lbo_a) >> 4), db + (uint64_t)((2 * k * C::lbo_b) >> 4),
-                         idesc_bf16(N), (kb | k) ? 1u : 0u);
-                umma_commit(&empty[s]);
-                if (kb == nkb - 1) umma_commit(&accf[b]);
-            }
+            for (int k = 0; k < kKC / 2; ++k)
+                umma_e(acc, da + (uint64_t)((2 * k * C::lbo_a) >> 4), db + (uint64_t)((2 * k * C::lbo_b) >> 4),
+                       idesc_bf16(N), (kb | k) ? 1u : 0u);
+            umma_commit_e(&empty[s]);
+            if (kb == nkb - 1) umma_commit_e(&accf[b]);
+        }
         __syncwarp();
     } else {
         // ------------------------------- epilogue warps -------------------------------
@@ -461,25 +525,25 @@ struct RowCfg {
     static constexpr uint32_t lbo_b = N / 8 * 128;
 };
 
-// Warp-specialised pipeline (no CTA barrier in the loop): warps 0-7 load (each iteration = T
-// consecutive row tiles) with cp.async and signal full[s] through cp.async.mbarrier.arrive.noinc;
+// Warp-specialised pipeline (no CTA barrier in the loop): warp 0 loads (each iteration = T
+// consecutive row tiles) with bulk copies completing on full[s] (warps 1-7 idle);
 // warp 12 (one lane) waits full[s], issues the MMAs of the iteration into accumulator set k % NB
 // (tiles interleaved) and commits to empty[s] (the stage may be refilled) and accf[b] (the
 // accumulators are ready); warps 8-11 wait accf[b], drain the accumulators (tcgen05.ld, fp32
 // stores, GroupNorm partial sums) and arrive on acce[b] (the set may be overwritten).
 
-template <int N, bool HEAD>
-__global__ void __launch_bounds__(kWsThreads) conv3x3_rows_kernel(const bf16 *__restrict__ in,
+template <int N, bool HEAD, int CQ>
+__global__ void __launch_bounds__(kRowThreads) conv3x3_rows_kernel(const bf16 *__restrict__ in,
                                                                   const bf16 *__restrict__ w, float *__restrict__ out,
                                                                   double *__restrict__ part, int64_t npix, int H, int W,
-                                                                  int cin, int S, int T, int gran,
-                                                                  const __grid_constant__ CUtensorMap rmap, int use_tma) {
+                                                                  int cin, int S, int T, int gran) {
     using C = RowCfg<N>;
     constexpr int NB = C::nbuf;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char *sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-    const int cq = cin >> 3;
-    const uint32_t rreg = row_region(cq), a_tile = 3u * rreg, a_bytes = T * a_tile, b_bytes = 9u * cq * C::lbo_b;
+    constexpr int cq = CQ;   // 8-channel chunks of the input (cin = 8 CQ)
+    constexpr uint32_t rreg = row_region(CQ), a_tile = 3u * rreg, b_bytes = 9u * CQ * C::lbo_b;
+    const uint32_t a_bytes = T * a_tile;
     uint64_t *full = reinterpret_cast<uint64_t *>(sm + S * a_bytes + b_bytes);
     uint64_t *empty = full + S;
     uint64_t *accf = empty + S;
@@ -490,19 +554,19 @@ __global__ void __launch_bounds__(kWsThreads) conv3x3_rows_kernel(const bf16 *__
 
     if (tid == 0) {
         for (int q = 0; q < S; ++q) {
-            mbar_init(&full[q], use_tma ? 1 : kProdWarps * 32);
+            mbar_init(&full[q], 1);
             mbar_init(&empty[q], 1);
         }
         for (int q = 0; q < NB; ++q) {
             mbar_init(&accf[q], 1);
-            mbar_init(&acce[q], 4);
+            mbar_init(&acce[q], 4 * kRowEpiGroups);
         }
         fence_mbar_init();
     }
-    if (warp == kProdWarps + 4) tmem_alloc<C::tcols>(tslot);
+    if (warp == kRowMmaWarp) tmem_alloc<C::tcols>(tslot);
     // resident weights: chunk g = tap * cq + c of row n at g * lbo_b + (n / 8) * 128 + (n % 8) * 16
     const int nchk = 9 * cq;
-    for (int i = tid; i < N * nchk; i += kWsThreads) {
+    for (int i = tid; i < N * nchk; i += kRowThreads) {
         const int n = i / nchk, g = i - n * nchk;
         cp_async16(bbase + g * C::lbo_b + (n >> 3) * 128 + (n & 7) * 16, w + (int64_t)n * 9 * cin + g * 8, true);
     }
@@ -520,146 +584,147 @@ __global__ void __launch_bounds__(kWsThreads) conv3x3_rows_kernel(const bf16 *__
     auto tile_of = [&](int k, int i) { return ((int64_t)blockIdx.x + (int64_t)k * gridDim.x) * T + i; };
     const int tpr = W / kBM;                             // tiles per image row
 
-    if (warp < kProdWarps) {
-        // ------------------------------- producers -------------------------------
-        constexpr int NP = kProdWarps * 32;
-        if (use_tma) {   // one thread: a 5D TMA box (16 B x 130 pixels x cq chunks) per (tile, row)
-            if (tid == 0) {
-                prefetch_tmap(&rmap);
-                for (int k = 0; k < ngl; ++k) {
-                    const int s = k % S;
-                    if (k >= S) mbar_wait(&empty[s], (uint32_t)(k / S - 1) & 1u);
-                    const uint32_t a0 = sbase + s * a_bytes;
-                    int nt = 0;
-                    while (nt < T && tile_of(k, nt) < tiles) ++nt;
-                    mbar_expect_tx(&full[s], (uint32_t)nt * 3u * (uint32_t)cq * kRowLbo);
-                    for (int i = 0; i < nt; ++i) {
-                        const int64_t t = tile_of(k, i);
-                        const int64_t rowid = t / tpr;
-                        const int x0 = (int)(t - rowid * tpr) * kBM;
-                        const int b = (int)(rowid / H), y = (int)(rowid - (int64_t)b * H);
-                        for (int r = 0; r < 3; ++r)
-                            tma_load_5d(a0 + i * a_tile + (uint32_t)r * rreg, &rmap, 0, x0 - 1, 0, y + r - 1, b, &full[s]);
+    if (warp == kRowProdWarp) {
+        // ------------------------------- producer -------------------------------
+        // one warp: per iteration, lane 0 posts the stage's byte count, then the lanes issue one
+        // bulk copy per (tile, halo row, chunk): the 130 pixels x0-1 .. x0+128 of one chunk of one
+        // input row are 2080 contiguous bytes of the row-chunk layout.  Rows outside the image
+        // and the pixels -1 / W at the image edges (the 'same' padding) come from a zero buffer.
+        const int64_t zsrc = (int64_t)reinterpret_cast<uintptr_t>(g_zero16);
+        long long tw = 0, ti = 0;
+        for (int k = 0; k < ngl; ++k) {
+            const int s = k % S;
+            const long long c0 = un_clock();
+            if (k >= S) mbar_wait(&empty[s], (uint32_t)(k / S - 1) & 1u, 1);
+            const long long c1 = un_clock();
+            tw += c1 - c0;
+            const uint32_t a0 = sbase + s * a_bytes;
+            int nt = 0;
+            while (nt < T && tile_of(k, nt) < tiles) ++nt;
+            // warp-uniform loops; one elected lane issues each copy (operands in uniform registers)
+            if (elect_one()) mbar_expect_tx(&full[s], (uint32_t)nt * 3u * (uint32_t)CQ * kRowLbo);
+            for (int i = 0; i < nt; ++i) {
+                const int64_t t = tile_of(k, i);
+                const int64_t rowid = t / tpr;
+                const int x0 = (int)(t - rowid * tpr) * kBM;
+                const int y = (int)(rowid % H);
+                const int lo = x0 > 0 ? x0 - 1 : 0, hi = x0 + kBM < W ? x0 + kBM : W - 1;
+                const uint32_t dlo = (uint32_t)(lo - (x0 - 1)) * 16u, nbytes = (uint32_t)(hi - lo + 1) * 16u;
+#pragma unroll
+                for (int r = 0; r < 3; ++r) {
+                    const int yy = y + r - 1;
+                    const uint32_t d = a0 + i * a_tile + (uint32_t)r * rreg;
+                    if (yy < 0 || yy >= H) {
+                        if (elect_one()) bulk_g2s(d, zsrc, CQ * kRowLbo, &full[s]);   // CQ <= 8: within g_zero16
+                    } else {
+                        const int64_t src = (int64_t)reinterpret_cast<uintptr_t>(in + rc_off(rowid + r - 1, lo, W, CQ, 0));
+#pragma unroll
+                        for (int c = 0; c < CQ; ++c)
+                            if (elect_one())
+                                bulk_g2s(d + (uint32_t)c * kRowLbo + dlo, src + (int64_t)c * W * 16, nbytes, &full[s]);
+                        if (x0 == 0)
+#pragma unroll
+                            for (int c = 0; c < CQ; ++c)
+                                if (elect_one()) bulk_g2s(d + (uint32_t)c * kRowLbo, zsrc, 16u, &full[s]);
+                        if (x0 + kBM == W)
+#pragma unroll
+                            for (int c = 0; c < CQ; ++c)
+                                if (elect_one())
+                                    bulk_g2s(d + (uint32_t)c * kRowLbo + (uint32_t)(kRowPix - 1) * 16u, zsrc, 16u, &full[s]);
                     }
                 }
             }
-        } else {         // all producer threads: cp.async 16-byte chunks, zero-fill = the padding
-            for (int k = 0; k < ngl; ++k) {
-                const int s = k % S;
-                if (k >= S) mbar_wait(&empty[s], (uint32_t)(k / S - 1) & 1u);
-                const uint32_t a0 = sbase + s * a_bytes;
-                for (int i = 0; i < T; ++i) {
-                    const int64_t t = tile_of(k, i);
-                    if (t >= tiles) break;
-                    const int64_t rowid = t / tpr;       // b * H + y (uniform across the producers)
-                    const int x0 = (int)(t - rowid * tpr) * kBM;
-                    const int y = (int)(rowid % H);
-                    for (int r = 0; r < 3; ++r) {
-                        const bool rv = y + r - 1 >= 0 && y + r - 1 < H;
-                        const bf16 *rowp = in + (rowid + r - 1) * W * cin;
-                        const uint32_t d0 = a0 + i * a_tile + (uint32_t)r * rreg;
-                        for (int px = tid; px < kRowPix; px += NP) {
-                            const int xx = x0 + px - 1;
-                            const bool v = rv && xx >= 0 && xx < W;
-                            const bf16 *src = v ? rowp + (int64_t)xx * cin : in;
-                            const uint32_t d = d0 + px * 16;
-                            for (int c = 0; c < cq; ++c) cp_async16(d + c * kRowLbo, v ? src + c * 8 : in, v);
-                        }
-                    }
-                }
-                asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&full[s]))
-                             : "memory");
-            }
+            ti += un_clock() - c1;
         }
-    } else if (warp == kProdWarps + 4) {
-        // ------------------------------- MMA issuer -------------------------------
         if (lane == 0) {
-            for (int k = 0; k < ngl; ++k) {
-                const int s = k % S, b = k % NB;
-                mbar_wait_spin(&full[s], (uint32_t)(k / S) & 1u);
-                if (k >= NB) mbar_wait_spin(&acce[b], (uint32_t)(k / NB - 1) & 1u);
-                tc_fence_after();
-                int nt = 0;
-                while (nt < T && tile_of(k, nt) < tiles) ++nt;
-                const uint32_t a0 = sbase + s * a_bytes;
-                const uint32_t acc0 = tmem + (uint32_t)(b * C::T * N);
-                // the single issuing thread was the bottleneck of the N = 16 layers (a descriptor
-                // built from scratch per MMA): descriptors are now advanced by adding (byte offset
-                // >> 4) to the 14-bit start-address field (addresses stay below 2^18: no carry)
-                const uint64_t dA0 = sdesc(a0, kRowLbo, 128), dB0 = sdesc(bbase, C::lbo_b, 128);
-                const uint64_t stepB = (uint64_t)((2 * C::lbo_b) >> 4), stepA = (uint64_t)((2 * kRowLbo) >> 4);
-                const uint64_t tileA = (uint64_t)(a_tile >> 4);
-                uint64_t bd = dB0;
+            UN_TR_ADD(3, tw);
+            UN_TR_ADD(4, ti);
+        }
+    } else if (warp == kRowMmaWarp) {
+        // ------------------------------- MMA issuer -------------------------------
+        // the whole warp runs the loop with warp-uniform descriptors; one elected lane issues
+        // (umma_e).  Descriptors advance by adding (byte offset >> 4) to the 14-bit start-address
+        // field (addresses stay below 2^18: no carry).
+        long long tf = 0, ta = 0, tm = 0;
+        for (int k = 0; k < ngl; ++k) {
+            const int s = k % S, b = k % NB;
+            const long long c0 = un_clock();
+            mbar_wait_spin(&full[s], (uint32_t)(k / S) & 1u, 2);
+            const long long c1 = un_clock();
+            if (k >= NB) mbar_wait_spin(&acce[b], (uint32_t)(k / NB - 1) & 1u, 3);
+            const long long c2 = un_clock();
+            tf += c1 - c0;
+            ta += c2 - c1;
+            tc_fence_after();
+            int nt = 0;
+            while (nt < T && tile_of(k, nt) < tiles) ++nt;
+            const uint32_t a0 = sbase + s * a_bytes;
+            const uint32_t acc0 = tmem + (uint32_t)(b * C::T * N);
+            // tile-outer, (tap, chunk pair) inner with compile-time descriptor offsets: each MMA is a
+            // uniform add of an immediate to the tile's start field (the accumulation order within a
+            // tile is (tap, chunk), as before)
+            const uint64_t dA0 = sdesc(a0, kRowLbo, 128), dB0 = sdesc(bbase, C::lbo_b, 128);
+            for (int i = 0; i < nt; ++i) {
+                const uint64_t dAi = dA0 + (uint64_t)((i * a_tile) >> 4);
+                const uint32_t acc = acc0 + (uint32_t)(i * N);
 #pragma unroll
                 for (int tap = 0; tap < 9; ++tap) {
-                    const int ky = tap / 3, kx = tap - 3 * ky;
-                    uint64_t ad = dA0 + (uint64_t)((ky * rreg + kx * 16) >> 4);
-                    for (int c = 0; c < cq; c += 2, ad += stepA, bd += stepB) {
-                        const uint32_t accf_ = (tap | c) ? 1u : 0u;
-                        uint64_t adi = ad;
-                        for (int i = 0; i < nt; ++i, adi += tileA)
-                            umma(acc0 + (uint32_t)(i * N), adi, bd, idesc_bf16(N), accf_);
+#pragma unroll
+                    for (int c = 0; c < CQ; c += 2) {
+                        const uint32_t aoff = ((tap / 3) * rreg + (tap % 3) * 16 + (c / 2) * 2 * kRowLbo) >> 4;
+                        const uint32_t boff = ((tap * CQ + c) * C::lbo_b) >> 4;
+                        umma_e(acc, dAi + aoff, dB0 + boff, idesc_bf16(N), (tap | c) ? 1u : 0u);
                     }
                 }
-                umma_commit(&empty[s]);
-                umma_commit(&accf[b]);
             }
+            umma_commit_e(&empty[s]);
+            umma_commit_e(&accf[b]);
+            tm += un_clock() - c2;
+        }
+        if (lane == 0) {
+            UN_TR_ADD(0, tf);
+            UN_TR_ADD(1, ta);
+            UN_TR_ADD(2, tm);
         }
         __syncwarp();
     } else {
-        // ------------------------- epilogue warps kProdWarps .. kProdWarps+3 -------------------------
+        // ------------------------- epilogue warps 0 .. 11 -------------------------
+        // group g = warp / 4 drains the tiles u = k T + i with u % kRowEpiGroups == g (a group of
+        // four warps covers the 128 TMEM lanes); every group arrives on acce[b] once per iteration
+        const int grp = warp >> 2;
+        long long te = 0, tp = 0;
         for (int k = 0; k < ngl; ++k) {
             const int b = k % NB;
-            mbar_wait(&accf[b], (uint32_t)(k / NB) & 1u);
+            const long long c0 = un_clock();
+            mbar_wait(&accf[b], (uint32_t)(k / NB) & 1u, 4);
+            const long long c1 = un_clock();
+            te += c1 - c0;
             tc_fence_after();
             for (int i = 0; i < T; ++i) {
                 const int64_t t = tile_of(k, i);
-                if (t < tiles)
+                if (t < tiles && (k * T + i) % kRowEpiGroups == grp)
                     conv_tile_out<N, HEAD, false>(tmem + (uint32_t)((b * C::T + i) * N), t, npix, out, part, gran, 0);
             }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&acce[b]);
+            tp += un_clock() - c1;
+        }
+        if (lane == 0 && warp == 0) {
+            UN_TR_ADD(5, te);
+            UN_TR_ADD(6, tp);
         }
     }
+    if (UN_TRACE && tid == 0) UN_TR_ADD(7, ngl);
     tc_fence_before();
     __syncthreads();
-    if (warp == kProdWarps + 4) tmem_dealloc<C::tcols>(tmem);
+    if (warp == kRowMmaWarp) tmem_dealloc<C::tcols>(tmem);
 }
 
-// 5D tensor map over the NHWC bf16 activations, ordered (8 channels, pixel x, chunk, row y, sample)
-// so that a box of {8, 130, cq, 1, 1} lands chunk-major in shared memory (chunk plane of 130 x 16 B);
-// out-of-range pixels and rows (the 'same' padding) are zero-filled by the TMA unit.
-PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
-    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-    if (!fn) {
-        cudaDriverEntryPointQueryResult q;
-        void *p = nullptr;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-    }
-    return fn;
-}
-
-bool encode_rows_map(CUtensorMap *m, const void *in, int B, int H, int W, int cin) {
-    auto enc = get_encode();
-    if (!enc || (reinterpret_cast<uintptr_t>(in) & 15u)) return false;
-    const int cq = cin / 8;
-    cuuint64_t dims[5] = {8, (cuuint64_t)W, (cuuint64_t)cq, (cuuint64_t)H, (cuuint64_t)B};
-    cuuint64_t strides[4] = {(cuuint64_t)cin * 2, 16, (cuuint64_t)W * cin * 2, (cuuint64_t)H * W * cin * 2};
-    cuuint32_t box[5] = {8, (cuuint32_t)kRowPix, (cuuint32_t)cq, 1, 1};
-    cuuint32_t estr[5] = {1, 1, 1, 1, 1};
-    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void *>(in), dims, strides, box, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    return r == CUDA_SUCCESS;
-}
-
-template <int N, bool HEAD>
-cudaError_t launch_conv_rows(const bf16 *in, const bf16 *w, float *out, double *part, int64_t npix, int H, int W,
-                             int cin, cudaStream_t st) {
-    const int cq = cin / 8;
+template <int N, bool HEAD, int CQ>
+cudaError_t launch_conv_rows_c(const bf16 *in, const bf16 *w, float *out, double *part, int64_t npix, int H, int W,
+                               int cin, cudaStream_t st) {
+    const int cq = CQ;
     const size_t a_tile = 3 * (size_t)row_region(cq), b_bytes = 9 * (size_t)cq * RowCfg<N>::lbo_b;
     // T row tiles per iteration and S stages: prefer 2 CTAs per SM (<= 110 KB) with S >= 3, else one
     // CTA (<= 220 KB); T as large as fits (<= RowCfg::T), S <= 6
@@ -679,31 +744,38 @@ cudaError_t launch_conv_rows(const bf16 *in, const bf16 *w, float *out, double *
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        cudaError_t e = cudaFuncSetAttribute(conv3x3_rows_kernel<N, HEAD>,
+        cudaError_t e = cudaFuncSetAttribute(conv3x3_rows_kernel<N, HEAD, CQ>,
                                              cudaFuncAttributePreferredSharedMemoryCarveout,
                                              (int)cudaSharedmemCarveoutMaxShared);
         if (e != cudaSuccess) return e;
     }
     if (smem > smem_set) {
-        cudaError_t e = cudaFuncSetAttribute(conv3x3_rows_kernel<N, HEAD>,
+        cudaError_t e = cudaFuncSetAttribute(conv3x3_rows_kernel<N, HEAD, CQ>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         smem_set = smem;
     }
     int occ = 1;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, conv3x3_rows_kernel<N, HEAD>, kWsThreads, smem);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, conv3x3_rows_kernel<N, HEAD, CQ>, kRowThreads, smem);
     if (e != cudaSuccess) return e;
     occ = occ < 1 ? 1 : (occ > 512 / RowCfg<N>::tcols ? 512 / RowCfg<N>::tcols : occ);   // TMEM columns
     const int gran = (H * W) % 32 == 0 ? 32 : 1;
     const int64_t groups = (npix / kBM + T - 1) / T, slots = (int64_t)nsm * occ;
     const unsigned grid = (unsigned)(groups < slots ? groups : slots);
-    static const int notma = getenv("UN_NO_TMA") ? atoi(getenv("UN_NO_TMA")) : 0;
-    CUtensorMap rmap;
-    std::memset(&rmap, 0, sizeof rmap);
-    const int use_tma = !notma && encode_rows_map(&rmap, in, (int)(npix / ((int64_t)H * W)), H, W, cin);
-    conv3x3_rows_kernel<N, HEAD><<<grid, kWsThreads, smem, st>>>(in, w, out, part, npix, H, W, cin, S, T, gran,
-                                                                   rmap, use_tma);
+    conv3x3_rows_kernel<N, HEAD, CQ><<<grid, kRowThreads, smem, st>>>(in, w, out, part, npix, H, W, cin, S, T, gran);
     return cudaGetLastError();
+}
+
+template <int N, bool HEAD>
+cudaError_t launch_conv_rows(const bf16 *in, const bf16 *w, float *out, double *part, int64_t npix, int H, int W,
+                             int cin, cudaStream_t st) {
+    switch (cin / 8) {   // cin a multiple of 16, <= 64
+        case 2: return launch_conv_rows_c<N, HEAD, 2>(in, w, out, part, npix, H, W, cin, st);
+        case 4: return launch_conv_rows_c<N, HEAD, 4>(in, w, out, part, npix, H, W, cin, st);
+        case 6: return launch_conv_rows_c<N, HEAD, 6>(in, w, out, part, npix, H, W, cin, st);
+        case 8: return launch_conv_rows_c<N, HEAD, 8>(in, w, out, part, npix, H, W, cin, st);
+        default: return cudaErrorInvalidValue;
+    }
 }
 
 template <int N, bool HEAD>
@@ -729,17 +801,27 @@ cudaError_t launch_conv(const bf16 *in, const bf16 *w, float *out, double *part,
 // ------------------------------------------------------------------------------------------------
 // element-wise and reduction kernels
 
-// history [B][lb][HW] fp32 -> NHWC bf16 with 16 channels (channels >= lb are zero)
+// history [B][lb][HW] fp32 -> row-chunk bf16 with 16 channels (channels >= lb are zero)
 __global__ void pack_input_kernel(const float *__restrict__ hist, bf16 *__restrict__ dst, int64_t npix, int HW,
-                                  int lb) {
+                                  int W, int lb) {
     for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < npix; p += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t b = p / HW, q = p - b * HW;
+        const int64_t b = p / HW, q = p - b * HW, row = p / W;
+        const int x = (int)(p - row * W);
         __align__(16) bf16 v[16];
 #pragma unroll
         for (int c = 0; c < 16; ++c) v[c] = __float2bfloat16_rn(c < lb ? hist[(b * lb + c) * HW + q] : 0.0f);
-        uint4 *d = reinterpret_cast<uint4 *>(dst + p * 16);
-        d[0] = reinterpret_cast<uint4 *>(v)[0];
-        d[1] = reinterpret_cast<uint4 *>(v)[1];
+        *reinterpret_cast<uint4 *>(dst + rc_off(row, x, W, 2, 0)) = reinterpret_cast<uint4 *>(v)[0];
+        *reinterpret_cast<uint4 *>(dst + rc_off(row, x, W, 2, 1)) = reinterpret_cast<uint4 *>(v)[1];
+    }
+}
+
+// NHWC bf16 -> row-chunk bf16 (un_conv3x3's input, which the ABI takes NHWC)
+__global__ void nhwc_to_rc_kernel(const bf16 *__restrict__ src, bf16 *__restrict__ dst, int64_t npix, int W, int cq) {
+    const int64_t total = npix * cq;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t p = i / cq, row = p / W;
+        const int q = (int)(i - p * cq), x = (int)(p - row * W);
+        *reinterpret_cast<uint4 *>(dst + rc_off(row, x, W, cq, q)) = *reinterpret_cast<const uint4 *>(src + i * 8);
     }
 }
 
@@ -823,7 +905,7 @@ __device__ __forceinline__ float gelu_fast(float u) {   // P:408-411, hardware t
     return 0.5f * u * (1.0f + tanh_approx(0.7978845608028654f * (u + 0.044715f * u * u * u)));
 }
 
-__global__ void __launch_bounds__(256) gn_apply_kernel(const float *__restrict__ x, int64_t npix, int HW, int C,
+__global__ void __launch_bounds__(256) gn_apply_kernel(const float *__restrict__ x, int64_t npix, int HW, int W, int C,
                                                        const float2 *__restrict__ ab, const float *__restrict__ cond,
                                                        int ctot, int coff, bf16 *dA, int sA, int oA, bf16 *dB, int sB,
                                                        int oB) {
@@ -858,8 +940,10 @@ __global__ void __launch_bounds__(256) gn_apply_kernel(const float *__restrict__
             ya[j] = __float2bfloat16_rn(y);
             if (dB) yb[j] = __float2bfloat16_rn(y * cv[j]);
         }
-        if (dA) *reinterpret_cast<uint4 *>(dA + p * sA + oA + c0) = *reinterpret_cast<uint4 *>(ya);
-        if (dB) *reinterpret_cast<uint4 *>(dB + p * sB + oB + c0) = *reinterpret_cast<uint4 *>(yb);
+        const int64_t row = p / W;
+        const int xx = (int)(p - row * W);
+        if (dA) *reinterpret_cast<uint4 *>(dA + rc_off(row, xx, W, sA >> 3, (oA >> 3) + q)) = *reinterpret_cast<uint4 *>(ya);
+        if (dB) *reinterpret_cast<uint4 *>(dB + rc_off(row, xx, W, sB >> 3, (oB >> 3) + q)) = *reinterpret_cast<uint4 *>(yb);
     }
 }
 
@@ -904,12 +988,13 @@ __global__ void __launch_bounds__(256) gn_apply_pool_kernel(const float *__restr
                     yb[j] = __float2bfloat16_rn(y * cv[j]);
                     mx[j] = (dy | dx) ? fmaxf(mx[j], y) : y;
                 }
-                *reinterpret_cast<uint4 *>(dB + p * sB + oB + c0) = *reinterpret_cast<uint4 *>(yb);
+                *reinterpret_cast<uint4 *>(dB + rc_off((int64_t)b * H + 2 * yo + dy, 2 * xo + dx, W, sB >> 3, (oB >> 3) + q)) =
+                    *reinterpret_cast<uint4 *>(yb);
             }
         __align__(16) bf16 m[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) m[j] = __float2bfloat16_rn(mx[j]);
-        *reinterpret_cast<uint4 *>(pool + po * C + c0) = *reinterpret_cast<uint4 *>(m);
+        *reinterpret_cast<uint4 *>(pool + rc_off((int64_t)b * h + yo, xo, w, nq, q)) = *reinterpret_cast<uint4 *>(m);
     }
 }
 
@@ -951,11 +1036,11 @@ __global__ void __launch_bounds__(256) gn_apply_up_kernel(const float *__restric
 #pragma unroll
         for (int mn = 0; mn < 4; ++mn) {
             const int m = mn >> 1, n = mn & 1;
-            const int64_t po = ((int64_t)b * 2 * h + 2 * yi + m) * (2 * w) + 2 * xi + n;
             __align__(16) bf16 o[8];
 #pragma unroll
             for (int j = 0; j < 8; ++j) o[j] = __float2bfloat16_rn(yv[j] * ws[mn]);
-            *reinterpret_cast<uint4 *>(dst + po * sD + oD + c0) = *reinterpret_cast<uint4 *>(o);
+            *reinterpret_cast<uint4 *>(dst + rc_off((int64_t)b * 2 * h + 2 * yi + m, 2 * xi + n, 2 * w, sD >> 3, (oD >> 3) + q)) =
+                *reinterpret_cast<uint4 *>(o);
         }
     }
 }
@@ -1074,7 +1159,7 @@ pf_status apply_layer(un_ctx *c, int l, int B, int cond_level, bf16 *dA, int sA,
     const int64_t npix = (int64_t)B * HW;
     const int C = c->cout[l];
     gn_apply_kernel<<<grid_for(npix * (C / 8), 256), 256, 0, c->st>>>(
-        c->raw, npix, HW, C, c->ab, c->cond, c->ctot, cond_level >= 0 ? c->coff[cond_level] : 0, dA, sA, oA, dB, sB, oB);
+        c->raw, npix, HW, c->p.width >> lv, C, c->ab, c->cond, c->ctot, cond_level >= 0 ? c->coff[cond_level] : 0, dA, sA, oA, dB, sB, oB);
     c->launches += 1;
     return PF_OK;
 }
@@ -1112,7 +1197,7 @@ pf_status forward(un_ctx *c, int B, const float *hist, const float *dt, float *o
     time_mlp_kernel<<<B, kBasis, 0, c->st2>>>(c->mlp, c->wl, dt, c->cond, c->ctot);
     UCK(c, cudaEventRecord(c->ev_join, c->st2));
     pack_input_kernel<<<grid_for((int64_t)B * HW, 256), 256, 0, c->st>>>(hist, c->in0, (int64_t)B * HW, (int)HW,
-                                                                         c->p.lb);
+                                                                         c->p.width, c->p.lb);
     c->launches += 2;
     pf_status s;
     // encoder + conditioning: z_p unconditioned (pooling input), z_p (.) s_p
@@ -1500,14 +1585,33 @@ pf_status un_conv3x3(const uint16_t *in, int32_t batch, int32_t H, int32_t W, in
     if (cout != 16 && cout != 32 && cout != 64 && cout != 128) return fail(nullptr, PF_ERR_ARG, "cout must be 16/32/64/128");
     const int64_t npix = (int64_t)batch * H * W;
     double *part = nullptr;   // epilogue statistics are not returned here
-    if (cudaMalloc(&part, (size_t)(npix * kGroups * 2) * sizeof(double)) != cudaSuccess)
-        return fail(nullptr, PF_ERR_NOMEM, "cudaMalloc of statistics scratch failed");
-    cudaError_t e = launch_conv(reinterpret_cast<const bf16 *>(in), reinterpret_cast<const bf16 *>(w), out, part,
-                                npix, H, W, cin, cout, false, (cudaStream_t)stream);
+    bf16 *rc = nullptr;       // the input in the kernels' row-chunk layout
+    if (cudaMalloc(&part, (size_t)(npix * kGroups * 2) * sizeof(double)) != cudaSuccess ||
+        cudaMalloc(&rc, (size_t)npix * cin * sizeof(bf16)) != cudaSuccess) {
+        cudaFree(part);
+        cudaGetLastError();
+        return fail(nullptr, PF_ERR_NOMEM, "cudaMalloc of conv scratch failed");
+    }
+    nhwc_to_rc_kernel<<<grid_for(npix * (cin / 8), 256), 256, 0, (cudaStream_t)stream>>>(
+        reinterpret_cast<const bf16 *>(in), rc, npix, W, cin / 8);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess)
+        e = launch_conv(rc, reinterpret_cast<const bf16 *>(w), out, part, npix, H, W, cin, cout, false,
+                        (cudaStream_t)stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize((cudaStream_t)stream);
     cudaFree(part);
+    cudaFree(rc);
     if (e != cudaSuccess) return fail(nullptr, PF_ERR_CUDA, fmt("conv launch: %s", cudaGetErrorString(e)));
     return PF_OK;
+}
+
+int un_debug_trace(unsigned long long *out, int reset) {
+    cudaError_t e = cudaMemcpyFromSymbol(out, g_untrace, sizeof(g_untrace));
+    if (e == cudaSuccess && reset) {
+        static unsigned long long zero[160][8];
+        e = cudaMemcpyToSymbol(g_untrace, zero, sizeof(zero));
+    }
+    return (int)e;
 }
 
 pf_status un_stream(un_ctx *c, void **stream) {
