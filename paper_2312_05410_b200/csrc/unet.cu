@@ -81,6 +81,7 @@ __device__ __forceinline__ bool mbar_try(uint64_t *bar, uint32_t parity) {
         : "memory");
     return ok != 0;
 }
+#if UN_WATCHDOG
 __device__ __noinline__ void mbar_watchdog(uint64_t *bar, uint32_t parity, int tag) {
     for (long long it = 0; !mbar_try(bar, parity); ++it)
         if (it == (1ll << 26)) {
@@ -89,6 +90,9 @@ __device__ __noinline__ void mbar_watchdog(uint64_t *bar, uint32_t parity, int t
             __trap();
         }
 }
+#else
+__device__ __forceinline__ void mbar_watchdog(uint64_t *, uint32_t, int) {}
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity, int tag = 0) {
     if (UN_WATCHDOG) {
         mbar_watchdog(bar, parity, tag);
