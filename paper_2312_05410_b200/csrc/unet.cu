@@ -72,6 +72,7 @@ __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier
 #ifndef UN_WATCHDOG
 #define UN_WATCHDOG 0   // debug builds: bounded mbarrier waits that report (block, warp, tag) and trap
 #endif
+#if UN_WATCHDOG
 __device__ __forceinline__ bool mbar_try(uint64_t *bar, uint32_t parity) {
     uint32_t ok;
     asm volatile(
@@ -81,7 +82,6 @@ __device__ __forceinline__ bool mbar_try(uint64_t *bar, uint32_t parity) {
         : "memory");
     return ok != 0;
 }
-#if UN_WATCHDOG
 __device__ __noinline__ void mbar_watchdog(uint64_t *bar, uint32_t parity, int tag) {
     for (long long it = 0; !mbar_try(bar, parity); ++it)
         if (it == (1ll << 26)) {
@@ -221,8 +221,9 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
 constexpr int kKC = 18;
 constexpr int kProdWarps = 8;                        // loader warps of the warp-specialised kernels
 constexpr int kWsThreads = 32 * (kProdWarps + 5);   // + 4 epilogue warps + 1 MMA warp
-// row kernel: 3 groups of 4 epilogue warps (0-11), producer warp 12, MMA warp 13
-constexpr int kRowEpiGroups = 3, kRowProdWarp = 4 * kRowEpiGroups, kRowMmaWarp = kRowProdWarp + 1;
+// row kernel: 2 groups of 4 epilogue warps (0-7), 4 producer warps (8-11), MMA warp 12
+constexpr int kRowEpiGroups = 2, kRowProdWarp = 4 * kRowEpiGroups, kRowProdWarps = 4;
+constexpr int kRowMmaWarp = kRowProdWarp + kRowProdWarps;
 constexpr int kRowThreads = 32 * (kRowMmaWarp + 1);
 
 template <int N>
@@ -511,68 +512,89 @@ cudaError_t launch_conv_n(const bf16 *in, const bf16 *w, float *out, double *par
 }
 
 // Row-tile variant for W a multiple of 128 (the full- and half-resolution levels, where the
-// channel counts are small and the gather above is instruction bound): a tile is 128 consecutive
-// pixels of one image row, and the shared memory holds the three input rows y-1, y, y+1 over the
-// 130 pixels x0-1 .. x0+128, chunk-major (chunk c of pixel i at c * 2080 + i * 16 B), so that the A
-// operand of tap (ky, kx) is the canonical K-major layout starting kx pixels (16 B) into row ky:
-// one descriptor per (tap, 16-channel step), no per-tap gather, each input row read 3x instead of
-// 9x.  The whole weight matrix stays resident in shared memory.
+// channel counts are small and the gather below is instruction bound): a tile is 128 consecutive
+// output pixels of one image row.  Shared memory holds a ring of INPUT rows, each over the 130
+// pixels x0-1 .. x0+128 of its tile column, chunk-major (chunk c of pixel i at c * 2080 + i * 16 B),
+// so that the A operand of tap (ky, kx) is the canonical K-major layout starting kx pixels (16 B)
+// into the ring slot of input row y + ky - 1: one descriptor per (tap, 16-channel step), no per-tap
+// gather.  A CTA walks segments of R consecutive output rows of one tile column (sliding window):
+// every input row is loaded ONCE per segment (R + 2 rows for R outputs) and serves three outputs.
+// The whole weight matrix stays resident in shared memory.
 constexpr int kRowPix = 130;
 constexpr uint32_t kRowLbo = kRowPix * 16;   // chunk-plane stride (2080 B)
 __host__ __device__ constexpr uint32_t row_region(int cq) { return (cq * kRowLbo + 127u) / 128u * 128u; }
 
 template <int N>
 struct RowCfg {
-    static constexpr int T = N >= 64 ? 1 : 64 / N;                  // row tiles per iteration
-    static constexpr int nbuf = T * N * 4 <= 256 ? 4 : 2;          // TMEM accumulator sets (lag nbuf-1)
-    static constexpr int tcols = nbuf * T * N < 32 ? 32 : nbuf * T * N;
+    // TMEM accumulator sets, a multiple of the epilogue groups (set b is always drained by group
+    // b % kRowEpiGroups): 6 x N columns for N <= 32, 4 x N above
+    static constexpr int nbuf = N <= 32 ? 6 : 4;
+    static_assert(nbuf % kRowEpiGroups == 0, "accumulator sets per epilogue group");
+    static constexpr int tneed = nbuf * N;
+    static constexpr int tcols = tneed <= 32 ? 32 : tneed <= 64 ? 64 : tneed <= 128 ? 128 : tneed <= 256 ? 256 : 512;
     static constexpr uint32_t lbo_b = N / 8 * 128;
 };
 
-// Warp-specialised pipeline (no CTA barrier in the loop): warp 0 loads (each iteration = T
-// consecutive row tiles) with bulk copies completing on full[s] (warps 1-7 idle);
-// warp 12 (one lane) waits full[s], issues the MMAs of the iteration into accumulator set k % NB
-// (tiles interleaved) and commits to empty[s] (the stage may be refilled) and accf[b] (the
-// accumulators are ready); warps 8-11 wait accf[b], drain the accumulators (tcgen05.ld, fp32
-// stores, GroupNorm partial sums) and arrive on acce[b] (the set may be overwritten).
+// Segments: seg = (b * nyb + yb) * tpr + xc covers output rows [yb R, min(H, yb R + R)) of tile
+// column xc of image b; CTA c takes seg = c, c + grid, ...  Every role walks the same sequence.
+struct RowSeg {
+    int64_t row0;   // b * H + y0 (first output row)
+    int y0, nr, x0;
+};
+__device__ __forceinline__ RowSeg row_seg(int64_t seg, int H, int R, int nyb, int tpr) {
+    RowSeg g;
+    const int xc = (int)(seg % tpr);
+    const int64_t rest = seg / tpr;
+    const int yb = (int)(rest % nyb);
+    const int64_t b = rest / nyb;
+    g.y0 = yb * R;
+    g.nr = H - g.y0 < R ? H - g.y0 : R;
+    g.row0 = b * H + g.y0;
+    g.x0 = xc * kBM;
+    return g;
+}
 
+// Warp-specialised pipeline (no CTA barrier in the loop): warps 8-11 load input rows into the ring
+// (cp.async completing on full[slot]); warp 12 issues, per output row, the MMAs of its 9 taps into
+// accumulator set o % NB and commits empty[slot] of the input row no later output needs and
+// accf[b]; epilogue group o % 2 (warps 4g .. 4g+3) drains set b (tcgen05.ld, fp32 stores, GroupNorm
+// partial sums) and arrives on acce[b].
 template <int N, bool HEAD, int CQ>
 __global__ void __launch_bounds__(kRowThreads) conv3x3_rows_kernel(const bf16 *__restrict__ in,
-                                                                  const bf16 *__restrict__ w, float *__restrict__ out,
-                                                                  double *__restrict__ part, int64_t npix, int H, int W,
-                                                                  int cin, int S, int T, int gran) {
+                                                                   const bf16 *__restrict__ w, float *__restrict__ out,
+                                                                   double *__restrict__ part, int64_t npix, int H,
+                                                                   int W, int S, int R, int gran) {
     using C = RowCfg<N>;
     constexpr int NB = C::nbuf;
+    static_assert(CQ >= 2 && CQ <= 8 && CQ % 2 == 0, "cin = 16 .. 64");
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char *sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-    constexpr int cq = CQ;   // 8-channel chunks of the input (cin = 8 CQ)
-    constexpr uint32_t rreg = row_region(CQ), a_tile = 3u * rreg, b_bytes = 9u * CQ * C::lbo_b;
-    const uint32_t a_bytes = T * a_tile;
-    uint64_t *full = reinterpret_cast<uint64_t *>(sm + S * a_bytes + b_bytes);
+    constexpr uint32_t rreg = row_region(CQ), b_bytes = 9u * CQ * C::lbo_b;
+    uint64_t *full = reinterpret_cast<uint64_t *>(sm + S * rreg + b_bytes);
     uint64_t *empty = full + S;
     uint64_t *accf = empty + S;
     uint64_t *acce = accf + NB;
     uint32_t *tslot = reinterpret_cast<uint32_t *>(acce + NB);
-    const uint32_t sbase = smem_u32(sm), bbase = sbase + S * a_bytes;
+    const uint32_t sbase = smem_u32(sm), bbase = sbase + S * rreg;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
     if (tid == 0) {
         for (int q = 0; q < S; ++q) {
-            mbar_init(&full[q], 1);
+            mbar_init(&full[q], 32 * kRowProdWarps);   // the producer lanes (cp.async.mbarrier.arrive.noinc)
             mbar_init(&empty[q], 1);
         }
         for (int q = 0; q < NB; ++q) {
             mbar_init(&accf[q], 1);
-            mbar_init(&acce[q], 4 * kRowEpiGroups);
+            mbar_init(&acce[q], 4);
         }
         fence_mbar_init();
     }
     if (warp == kRowMmaWarp) tmem_alloc<C::tcols>(tslot);
-    // resident weights: chunk g = tap * cq + c of row n at g * lbo_b + (n / 8) * 128 + (n % 8) * 16
-    const int nchk = 9 * cq;
+    // resident weights: chunk g = tap * CQ + c of row n at g * lbo_b + (n / 8) * 128 + (n % 8) * 16
+    constexpr int nchk = 9 * CQ;
     for (int i = tid; i < N * nchk; i += kRowThreads) {
         const int n = i / nchk, g = i - n * nchk;
-        cp_async16(bbase + g * C::lbo_b + (n >> 3) * 128 + (n & 7) * 16, w + (int64_t)n * 9 * cin + g * 8, true);
+        cp_async16(bbase + g * C::lbo_b + (n >> 3) * 128 + (n & 7) * 16, w + (int64_t)n * 9 * 8 * CQ + g * 8, true);
     }
     cp_async_commit();
     cp_async_wait_n(0);
@@ -582,65 +604,48 @@ __global__ void __launch_bounds__(kRowThreads) conv3x3_rows_kernel(const bf16 *_
     tc_fence_after();
     const uint32_t tmem = *tslot;
 
-    const int64_t tiles = npix / kBM;                    // W % 128 == 0: every tile is full
-    const int64_t groups = (tiles + T - 1) / T;
-    const int ngl = blockIdx.x < groups ? (int)((groups - 1 - blockIdx.x) / gridDim.x + 1) : 0;
-    auto tile_of = [&](int k, int i) { return ((int64_t)blockIdx.x + (int64_t)k * gridDim.x) * T + i; };
-    const int tpr = W / kBM;                             // tiles per image row
+    const int tpr = W / kBM, nyb = (H + R - 1) / R;
+    const int64_t nseg = npix / ((int64_t)H * W) * nyb * tpr;
 
-    if (warp == kRowProdWarp) {
-        // ------------------------------- producer -------------------------------
-        // one warp: per iteration, lane 0 posts the stage's byte count, then the lanes issue one
-        // bulk copy per (tile, halo row, chunk): the 130 pixels x0-1 .. x0+128 of one chunk of one
-        // input row are 2080 contiguous bytes of the row-chunk layout.  Rows outside the image
-        // and the pixels -1 / W at the image edges (the 'same' padding) come from a zero buffer.
-        const int64_t zsrc = (int64_t)reinterpret_cast<uintptr_t>(g_zero16);
+    if (warp >= kRowProdWarp && warp < kRowProdWarp + kRowProdWarps) {
+        // ------------------------------- producers -------------------------------
+        // per input row: the 130 pixels x0-1 .. x0+128 of every channel chunk (2080 contiguous bytes
+        // of the row-chunk layout per chunk) by 16-byte cp.async (LSU path; a warp instruction moves
+        // 512 contiguous bytes), zero-filled outside the image (the 'same' padding); each lane's
+        // copies complete on full[slot] (cp.async.mbarrier.arrive.noinc, 32 arrivals per fill).
+        // (Round 2: one 2080-byte cp.async.bulk per chunk instead cost ~170-250 issue cycles per
+        // copy, which bounded the 16-channel layers.)
         long long tw = 0, ti = 0;
-        for (int k = 0; k < ngl; ++k) {
-            const int s = k % S;
-            const long long c0 = un_clock();
-            if (k >= S) mbar_wait(&empty[s], (uint32_t)(k / S - 1) & 1u, 1);
-            const long long c1 = un_clock();
-            tw += c1 - c0;
-            const uint32_t a0 = sbase + s * a_bytes;
-            int nt = 0;
-            while (nt < T && tile_of(k, nt) < tiles) ++nt;
-            // warp-uniform loops; one elected lane issues each copy (operands in uniform registers)
-            if (elect_one()) mbar_expect_tx(&full[s], (uint32_t)nt * 3u * (uint32_t)CQ * kRowLbo);
-            for (int i = 0; i < nt; ++i) {
-                const int64_t t = tile_of(k, i);
-                const int64_t rowid = t / tpr;
-                const int x0 = (int)(t - rowid * tpr) * kBM;
-                const int y = (int)(rowid % H);
-                const int lo = x0 > 0 ? x0 - 1 : 0, hi = x0 + kBM < W ? x0 + kBM : W - 1;
-                const uint32_t dlo = (uint32_t)(lo - (x0 - 1)) * 16u, nbytes = (uint32_t)(hi - lo + 1) * 16u;
+        uint32_t q = 0;   // input rows loaded by this CTA
+        for (int64_t sg = blockIdx.x; sg < nseg; sg += gridDim.x) {
+            const RowSeg g = row_seg(sg, H, R, nyb, tpr);
+            for (int jr = 0; jr < g.nr + 2; ++jr, ++q) {
+                const uint32_t slot = q % (uint32_t)S;
+                const long long c0 = un_clock();
+                if (q >= (uint32_t)S) mbar_wait(&empty[slot], (q / (uint32_t)S - 1u) & 1u, 1);
+                const long long c1 = un_clock();
+                tw += c1 - c0;
+                const uint32_t d = sbase + slot * rreg;
+                const int yy = g.y0 - 1 + jr;
+                const bool rv = yy >= 0 && yy < H;
+                const bf16 *rowp = in + rc_off(rv ? g.row0 - 1 + jr : 0, 0, W, CQ, 0);
+                // the CQ x 130 16-byte chunks split over the producer lanes
+                const int pl = tid - 32 * kRowProdWarp;
 #pragma unroll
-                for (int r = 0; r < 3; ++r) {
-                    const int yy = y + r - 1;
-                    const uint32_t d = a0 + i * a_tile + (uint32_t)r * rreg;
-                    if (yy < 0 || yy >= H) {
-                        if (elect_one()) bulk_g2s(d, zsrc, CQ * kRowLbo, &full[s]);   // CQ <= 8: within g_zero16
-                    } else {
-                        const int64_t src = (int64_t)reinterpret_cast<uintptr_t>(in + rc_off(rowid + r - 1, lo, W, CQ, 0));
-#pragma unroll
-                        for (int c = 0; c < CQ; ++c)
-                            if (elect_one())
-                                bulk_g2s(d + (uint32_t)c * kRowLbo + dlo, src + (int64_t)c * W * 16, nbytes, &full[s]);
-                        if (x0 == 0)
-#pragma unroll
-                            for (int c = 0; c < CQ; ++c)
-                                if (elect_one()) bulk_g2s(d + (uint32_t)c * kRowLbo, zsrc, 16u, &full[s]);
-                        if (x0 + kBM == W)
-#pragma unroll
-                            for (int c = 0; c < CQ; ++c)
-                                if (elect_one())
-                                    bulk_g2s(d + (uint32_t)c * kRowLbo + (uint32_t)(kRowPix - 1) * 16u, zsrc, 16u, &full[s]);
+                for (int jj = 0; jj < (CQ * kRowPix + 32 * kRowProdWarps - 1) / (32 * kRowProdWarps); ++jj) {
+                    const int job = pl + jj * 32 * kRowProdWarps;
+                    if (job < CQ * kRowPix) {
+                        const int c = job / kRowPix, px = job - c * kRowPix;
+                        const int xx = g.x0 - 1 + px;
+                        const bool v = rv && xx >= 0 && xx < W;
+                        cp_async16(d + (uint32_t)c * kRowLbo + (uint32_t)px * 16u, v ? rowp + ((int64_t)c * W + xx) * 8 : in, v);
                     }
                 }
+                asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&full[slot])) : "memory");
+                ti += un_clock() - c1;
             }
-            ti += un_clock() - c1;
         }
-        if (lane == 0) {
+        if (tid == 32 * kRowProdWarp) {
             UN_TR_ADD(3, tw);
             UN_TR_ADD(4, ti);
         }
@@ -650,76 +655,85 @@ __global__ void __launch_bounds__(kRowThreads) conv3x3_rows_kernel(const bf16 *_
         // (umma_e).  Descriptors advance by adding (byte offset >> 4) to the 14-bit start-address
         // field (addresses stay below 2^18: no carry).
         long long tf = 0, ta = 0, tm = 0;
-        for (int k = 0; k < ngl; ++k) {
-            const int s = k % S, b = k % NB;
-            const long long c0 = un_clock();
-            mbar_wait_spin(&full[s], (uint32_t)(k / S) & 1u, 2);
-            const long long c1 = un_clock();
-            if (k >= NB) mbar_wait_spin(&acce[b], (uint32_t)(k / NB - 1) & 1u, 3);
-            const long long c2 = un_clock();
-            tf += c1 - c0;
-            ta += c2 - c1;
-            tc_fence_after();
-            int nt = 0;
-            while (nt < T && tile_of(k, nt) < tiles) ++nt;
-            const uint32_t a0 = sbase + s * a_bytes;
-            const uint32_t acc0 = tmem + (uint32_t)(b * C::T * N);
-            // tile-outer, (tap, chunk pair) inner with compile-time descriptor offsets: each MMA is a
-            // uniform add of an immediate to the tile's start field (the accumulation order within a
-            // tile is (tap, chunk), as before)
-            const uint64_t dA0 = sdesc(a0, kRowLbo, 128), dB0 = sdesc(bbase, C::lbo_b, 128);
-            for (int i = 0; i < nt; ++i) {
-                const uint64_t dAi = dA0 + (uint64_t)((i * a_tile) >> 4);
-                const uint32_t acc = acc0 + (uint32_t)(i * N);
+        uint32_t q = 0, o = 0;   // input rows, output rows of this CTA
+        const uint64_t dB0 = sdesc(bbase, C::lbo_b, 128);
+        for (int64_t sg = blockIdx.x; sg < nseg; sg += gridDim.x) {
+            const RowSeg g = row_seg(sg, H, R, nyb, tpr);
+            for (int j = 0; j < g.nr; ++j, ++o) {
+                const uint32_t b = o % NB;
+                const long long c0 = un_clock();
+                for (uint32_t r = (j == 0 ? 0u : 2u); r < 3u; ++r) {   // input rows q+j .. q+j+2
+                    const uint32_t qq = q + (uint32_t)j + r;
+                    mbar_wait_spin(&full[qq % (uint32_t)S], (qq / (uint32_t)S) & 1u, 2);
+                }
+                const long long c1 = un_clock();
+                if (o >= (uint32_t)NB) mbar_wait_spin(&acce[b], (o / NB - 1u) & 1u, 3);
+                const long long c2 = un_clock();
+                tf += c1 - c0;
+                ta += c2 - c1;
+                tc_fence_after();
+                const uint32_t acc = tmem + b * (uint32_t)N;
+                uint64_t dA[3];
+#pragma unroll
+                for (int ky = 0; ky < 3; ++ky)
+                    dA[ky] = sdesc(sbase + ((q + (uint32_t)(j + ky)) % (uint32_t)S) * rreg, kRowLbo, 128);
 #pragma unroll
                 for (int tap = 0; tap < 9; ++tap) {
 #pragma unroll
                     for (int c = 0; c < CQ; c += 2) {
-                        const uint32_t aoff = ((tap / 3) * rreg + (tap % 3) * 16 + (c / 2) * 2 * kRowLbo) >> 4;
+                        const uint32_t aoff = ((tap % 3) * 16 + (c / 2) * 2 * kRowLbo) >> 4;
                         const uint32_t boff = ((tap * CQ + c) * C::lbo_b) >> 4;
-                        umma_e(acc, dAi + aoff, dB0 + boff, idesc_bf16(N), (tap | c) ? 1u : 0u);
+                        umma_e(acc, dA[tap / 3] + aoff, dB0 + boff, idesc_bf16(N), (tap | c) ? 1u : 0u);
                     }
                 }
+                // input row q+j is not read by later outputs; at the segment's end neither are the last two
+                umma_commit_e(&empty[(q + (uint32_t)j) % (uint32_t)S]);
+                if (j == g.nr - 1) {
+                    umma_commit_e(&empty[(q + (uint32_t)j + 1u) % (uint32_t)S]);
+                    umma_commit_e(&empty[(q + (uint32_t)j + 2u) % (uint32_t)S]);
+                }
+                umma_commit_e(&accf[b]);
+                tm += un_clock() - c2;
             }
-            umma_commit_e(&empty[s]);
-            umma_commit_e(&accf[b]);
-            tm += un_clock() - c2;
+            q += (uint32_t)g.nr + 2u;
         }
         if (lane == 0) {
             UN_TR_ADD(0, tf);
             UN_TR_ADD(1, ta);
             UN_TR_ADD(2, tm);
+            UN_TR_ADD(7, o);
         }
         __syncwarp();
-    } else {
-        // ------------------------- epilogue warps 0 .. 11 -------------------------
-        // group g = warp / 4 drains the tiles u = k T + i with u % kRowEpiGroups == g (a group of
-        // four warps covers the 128 TMEM lanes); every group arrives on acce[b] once per iteration
-        const int grp = warp >> 2;
+    } else if (warp < 4 * kRowEpiGroups) {
+        // ------------------------- epilogue warps 0 .. 7 -------------------------
+        // group grp = warp / 4 drains the outputs o with o % 2 == grp (accumulator sets b = o % NB,
+        // NB a multiple of 2); a group of four warps covers the 128 TMEM lanes
+        const uint32_t grp = (uint32_t)(warp >> 2);
         long long te = 0, tp = 0;
-        for (int k = 0; k < ngl; ++k) {
-            const int b = k % NB;
-            const long long c0 = un_clock();
-            mbar_wait(&accf[b], (uint32_t)(k / NB) & 1u, 4);
-            const long long c1 = un_clock();
-            te += c1 - c0;
-            tc_fence_after();
-            for (int i = 0; i < T; ++i) {
-                const int64_t t = tile_of(k, i);
-                if (t < tiles && (k * T + i) % kRowEpiGroups == grp)
-                    conv_tile_out<N, HEAD, false>(tmem + (uint32_t)((b * C::T + i) * N), t, npix, out, part, gran, 0);
+        uint32_t o = 0;
+        for (int64_t sg = blockIdx.x; sg < nseg; sg += gridDim.x) {
+            const RowSeg g = row_seg(sg, H, R, nyb, tpr);
+            for (int j = 0; j < g.nr; ++j, ++o) {
+                if (o % (uint32_t)kRowEpiGroups != grp) continue;
+                const uint32_t b = o % NB;
+                const long long c0 = un_clock();
+                mbar_wait(&accf[b], (o / NB) & 1u, 4);
+                const long long c1 = un_clock();
+                te += c1 - c0;
+                tc_fence_after();
+                const int64_t t = (g.row0 + j) * tpr + g.x0 / kBM;   // 128-pixel tile index
+                conv_tile_out<N, HEAD, false>(tmem + b * (uint32_t)N, t, npix, out, part, gran, 0);
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&acce[b]);
+                tp += un_clock() - c1;
             }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&acce[b]);
-            tp += un_clock() - c1;
         }
         if (lane == 0 && warp == 0) {
             UN_TR_ADD(5, te);
             UN_TR_ADD(6, tp);
         }
     }
-    if (UN_TRACE && tid == 0) UN_TR_ADD(7, ngl);
     tc_fence_before();
     __syncthreads();
     if (warp == kRowMmaWarp) tmem_dealloc<C::tcols>(tmem);
@@ -728,20 +742,16 @@ __global__ void __launch_bounds__(kRowThreads) conv3x3_rows_kernel(const bf16 *_
 template <int N, bool HEAD, int CQ>
 cudaError_t launch_conv_rows_c(const bf16 *in, const bf16 *w, float *out, double *part, int64_t npix, int H, int W,
                                int cin, cudaStream_t st) {
-    const int cq = CQ;
-    const size_t a_tile = 3 * (size_t)row_region(cq), b_bytes = 9 * (size_t)cq * RowCfg<N>::lbo_b;
-    // T row tiles per iteration and S stages: prefer 2 CTAs per SM (<= 110 KB) with S >= 3, else one
-    // CTA (<= 220 KB); T as large as fits (<= RowCfg::T), S <= 6
-    int T = RowCfg<N>::T, S = 0;
-    for (; T >= 1 && S < 3; --T) {
-        S = (int)((110 * 1024 - 1200 - b_bytes) / (T * a_tile));
-        if (S < 3) S = (int)((220 * 1024 - 1200 - b_bytes) / (T * a_tile));
-        if (S >= 3) break;
-    }
-    if (T < 1 || S < 3) return cudaErrorInvalidValue;
-    S = S > 6 ? 6 : S;
-    const size_t a_bytes = T * a_tile;
-    const size_t smem = 1024 + S * a_bytes + b_bytes + 128;
+    (void)cin;
+    const size_t rreg = row_region(CQ), b_bytes = 9 * (size_t)CQ * RowCfg<N>::lbo_b;
+    const size_t fixed = 1024 + b_bytes + 512;
+    // ring slots: as many input rows as one CTA's shared memory holds, up to 16 (the loads of a
+    // row are issued when the MMAs that read the row it replaces have COMPLETED; a deep ring keeps
+    // that refill ahead of the tensor core; 8 slots left the MMA warp waiting ~400 cycles per output)
+    int S = (int)((220 * 1024 - fixed) / rreg);
+    S = S > 16 ? 16 : S;
+    if (S < 4) return cudaErrorInvalidValue;
+    const size_t smem = fixed + S * rreg;
     static size_t smem_set = 0;
     static int nsm = 0;
     if (nsm == 0) {
@@ -764,9 +774,28 @@ cudaError_t launch_conv_rows_c(const bf16 *in, const bf16 *w, float *out, double
     if (e != cudaSuccess) return e;
     occ = occ < 1 ? 1 : (occ > 512 / RowCfg<N>::tcols ? 512 / RowCfg<N>::tcols : occ);   // TMEM columns
     const int gran = (H * W) % 32 == 0 ? 32 : 1;
-    const int64_t groups = (npix / kBM + T - 1) / T, slots = (int64_t)nsm * occ;
-    const unsigned grid = (unsigned)(groups < slots ? groups : slots);
-    conv3x3_rows_kernel<N, HEAD, CQ><<<grid, kRowThreads, smem, st>>>(in, w, out, part, npix, H, W, cin, S, T, gran);
+    // segment height R: the smallest cost max-segments-per-CTA x (R + 2) input rows over R in 4..64
+    const int64_t B = npix / ((int64_t)H * W), cols = B * (W / kBM);
+    const int64_t slots = (int64_t)nsm * occ;
+    int R = 4;
+    int64_t best = -1;
+    for (int r = 4; r <= 64; ++r) {
+        const int64_t nseg = cols * ((H + r - 1) / r);
+        const int64_t g = nseg < slots ? nseg : slots;
+        const int64_t cost = (nseg + g - 1) / g * (int64_t)(r + 2);
+        if (best < 0 || cost < best) {
+            best = cost;
+            R = r;
+        }
+    }
+    if (R > H) R = H;
+    const int64_t nseg = cols * ((H + R - 1) / R);
+    const unsigned grid = (unsigned)(nseg < slots ? nseg : slots);
+    static const bool dbg = getenv("UN_DEBUG_LAUNCH") && atoi(getenv("UN_DEBUG_LAUNCH"));
+    if (dbg)
+        fprintf(stderr, "conv_rows N=%d CQ=%d H=%d W=%d S=%d R=%d occ=%d grid=%u smem=%zu\n", N, CQ, H, W, S, R, occ, grid,
+                smem);
+    conv3x3_rows_kernel<N, HEAD, CQ><<<grid, kRowThreads, smem, st>>>(in, w, out, part, npix, H, W, S, R, gran);
     return cudaGetLastError();
 }
 

@@ -2,7 +2,8 @@
 cd $GRAFT_REPO_ROOT
 out=gpurun_out/${TAG:-unet3}
 mkdir -p $out
-timeout 60 python tools/unet_probe.py conv 8 80 128 64 16 > $out/probe.log 2>&1 || exit 1
+UN_DEBUG_LAUNCH=1 timeout 60 python tools/unet_probe.py conv 8 80 128 64 16 > $out/probe.log 2>&1 || exit 1
+UN_DEBUG_LAUNCH=1 UN_NO_GRAPH=1 timeout 60 python tools/unet_probe.py fwd 64 256 256 >> $out/probe.log 2>&1
 timeout 400 python -m pytest tests/test_unet_gpu.py -x -q > $out/tests.log 2>&1
 echo "rc=$?" >> $out/tests.log
 timeout 120 python tools/unet_bench.py --no-cpu > $out/unet_bench.json 2> $out/unet_bench.err
