@@ -147,16 +147,6 @@ __device__ __forceinline__ bool elect_one() {   // true in exactly one lane of t
     return e != 0;
 }
 
-// 1D bulk copy global -> shared (cp.async.bulk, async proxy), completing `bytes` on mbarrier bar;
-// addresses 16-byte aligned, bytes a multiple of 16
-__device__ __forceinline__ void bulk_g2s(uint32_t dst, int64_t src, uint32_t bytes, uint64_t *bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
-}
-// 16-byte zeros for the bulk copies of out-of-image rows / pixels (one row plane of 130 pixels x
-// 8 chunks)
-__device__ __align__(128) uint4 g_zero16[130 * 8];
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
 
@@ -200,6 +190,16 @@ __device__ __forceinline__ void umma_commit_e(uint64_t *bar) {
         "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
         "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(smem_u32(bar))
         : "memory");
+}
+// zero 16 fp32 columns of the calling warp's 32 TMEM lanes (tcgen05.st 32x32b.x16) and wait
+__device__ __forceinline__ void tmem_zero16(uint32_t taddr) {
+    const uint32_t z = 0u;
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, "
+        "%1};\n" ::"r"(taddr),
+        "r"(z)
+        : "memory");
+    asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
 }
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
     asm volatile(
@@ -245,20 +245,20 @@ __device__ __forceinline__ void cp_async_wait_n(int n) {   // n <= 3
     }
 }
 
-// Epilogue of one 128-pixel tile t (pixels t*128 .. t*128+127) whose accumulator is TMEM buffer
-// tl & 1: wait for its MMAs, tcgen05.ld (warp w reads lanes 32 (w & 3) .. +31; with N >= 32 the
-// warps w and w + 4 split the columns), fp32 stores, GroupNorm partial sums (see above).
+// Epilogue of one tile of up to 128 pixels (TMEM lane m = pixel pbase + m, m < nvalid) from the
+// accumulator at tacc: tcgen05.ld (warp w reads lanes 32 (w & 3) .. +31; with N >= 32 the warps w
+// and w + 4 split the columns), fp32 stores, GroupNorm partial sums (see above).
 template <int N, bool HEAD, bool SPLIT = true>
-__device__ __forceinline__ void conv_tile_out(uint32_t tacc, int64_t t, int64_t npix, float *__restrict__ out,
-                                              double *__restrict__ part, int gran, int sel) {
+__device__ __forceinline__ void conv_tile_out(uint32_t tacc, int64_t pbase, int nvalid, int64_t npix,
+                                              float *__restrict__ out, double *__restrict__ part, int gran, int sel) {
     constexpr int NG = HEAD ? 1 : kGroups, GC = HEAD ? 1 : N / kGroups;
     constexpr bool HALF = SPLIT && N >= 32;                          // warps w, w+4 split the columns
     constexpr int ECOLS = HALF ? N / 2 : N;                          // epilogue columns per warp
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int lq = warp & 3, hv = (warp >> 2) & 1;
     if (!SPLIT || N >= 32 || hv == sel) {
-        const int64_t p = t * kBM + 32 * lq + lane;
-        const bool pv = p < npix;
+        const int64_t p = pbase + 32 * lq + lane;   // TMEM lane m = 32 lq + lane is pixel pbase + m
+        const bool pv = 32 * lq + lane < nvalid && p < npix;
         const int c0 = HALF ? hv * ECOLS : 0;
         const uint32_t trow = tacc + ((uint32_t)(32 * lq) << 16);
         float *o = out + p * N;
@@ -335,9 +335,9 @@ __device__ __forceinline__ void conv_tile_out(uint32_t tacc, int64_t t, int64_t 
                     v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
                 }
             }
-            const int64_t wid = t * 4 + lq;   // global 32-pixel unit
+            const int64_t wid = pbase / 32 + lq;   // global 32-pixel unit (pbase a multiple of 32)
             constexpr int SH = 5 - M;
-            if ((lane & ((1 << SH) - 1)) == 0 && wid * 32 < npix) {
+            if ((lane & ((1 << SH) - 1)) == 0 && 32 * lq < nvalid && wid * 32 < npix) {
                 const int idx = (lane >> SH) & (NV - 1);   // = 2 g + (0: sum, 1: sum of squares)
                 part[(wid * NG + g0 + (idx >> 1)) * 2 + (idx & 1)] = v[0];
             }
@@ -477,7 +477,7 @@ __global__ void __launch_bounds__(kWsThreads) conv3x3_kernel(const bf16 *__restr
             const int b = tl & 1;
             mbar_wait(&accf[b], (uint32_t)(tl >> 1) & 1u);
             tc_fence_after();
-            conv_tile_out<N, HEAD, false>(tmem + (uint32_t)(b * N), (int64_t)blockIdx.x + (int64_t)tl * gridDim.x, npix,
+            conv_tile_out<N, HEAD, false>(tmem + (uint32_t)(b * N), ((int64_t)blockIdx.x + (int64_t)tl * gridDim.x) * kBM, kBM, npix,
                                           out, part, gran, 0);
             tc_fence_before();
             __syncwarp();
@@ -533,6 +533,8 @@ struct RowCfg {
     static constexpr int tneed = nbuf * N;
     static constexpr int tcols = tneed <= 32 ? 32 : tneed <= 64 ? 64 : tneed <= 128 ? 128 : tneed <= 256 ? 256 : 512;
     static constexpr uint32_t lbo_b = N / 8 * 128;
+    // the B operand holds, per K chunk (kx, 8 channels), the 3 N rows [W(ky=2); W(ky=1); W(ky=0)]
+    static constexpr uint32_t lbo_b3 = 3 * lbo_b;
 };
 
 // Segments: seg = (b * nyb + yb) * tpr + xc covers output rows [yb R, min(H, yb R + R)) of tile
@@ -566,7 +568,7 @@ __global__ void __launch_bounds__(kRowThreads) conv3x3_rows_kernel(const bf16 *_
                                                                    int W, int S, int R, int gran) {
     using C = RowCfg<N>;
     constexpr int NB = C::nbuf;
-    static_assert(CQ >= 2 && CQ <= 8 && CQ % 2 == 0, "cin = 16 .. 64");
+    static_assert(CQ >= 2 && CQ <= 16 && CQ % 2 == 0, "cin = 16 .. 128");
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char *sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     constexpr uint32_t rreg = row_region(CQ), b_bytes = 9u * CQ * C::lbo_b;
@@ -590,11 +592,15 @@ __global__ void __launch_bounds__(kRowThreads) conv3x3_rows_kernel(const bf16 *_
         fence_mbar_init();
     }
     if (warp == kRowMmaWarp) tmem_alloc<C::tcols>(tslot);
-    // resident weights: chunk g = tap * CQ + c of row n at g * lbo_b + (n / 8) * 128 + (n % 8) * 16
+    // resident weights: for K chunk gk = kx * CQ + c (8 channels) the 3 N rows n' = (2 - ky) N + n
+    // at gk * lbo_b3 + (n' / 8) * 128 + (n' % 8) * 16, so that one MMA of an input row serves the
+    // outputs it feeds through ky = 2, 1, 0 (the rows before, at and after it)
     constexpr int nchk = 9 * CQ;
     for (int i = tid; i < N * nchk; i += kRowThreads) {
-        const int n = i / nchk, g = i - n * nchk;
-        cp_async16(bbase + g * C::lbo_b + (n >> 3) * 128 + (n & 7) * 16, w + (int64_t)n * 9 * 8 * CQ + g * 8, true);
+        const int n = i / nchk, g = i - n * nchk;   // g = tap * CQ + c in the global [n][tap][cin] order
+        const int tap = g / CQ, c = g - tap * CQ, ky = tap / 3, kx = tap - 3 * ky;
+        const int np = (2 - ky) * N + n, gk = kx * CQ + c;
+        cp_async16(bbase + gk * C::lbo_b3 + (np >> 3) * 128 + (np & 7) * 16, w + (int64_t)n * 9 * 8 * CQ + g * 8, true);
     }
     cp_async_commit();
     cp_async_wait_n(0);
@@ -603,8 +609,15 @@ __global__ void __launch_bounds__(kRowThreads) conv3x3_rows_kernel(const bf16 *_
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tslot;
+    // every accumulator set starts at zero (the MMAs always accumulate; the epilogue re-zeroes a
+    // set after draining it)
+    if (warp < 4 * kRowEpiGroups && (warp >> 2) == 0)
+        for (int cc = 0; cc < NB * N; cc += 16) tmem_zero16(tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)cc);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
 
-    const int tpr = W / kBM, nyb = (H + R - 1) / R;
+    const int tpr = (W + kBM - 1) / kBM, nyb = (H + R - 1) / R;   // W a multiple of 128, or W < 128
     const int64_t nseg = npix / ((int64_t)H * W) * nyb * tpr;
 
     if (warp >= kRowProdWarp && warp < kRowProdWarp + kRowProdWarps) {
@@ -655,47 +668,68 @@ __global__ void __launch_bounds__(kRowThreads) conv3x3_rows_kernel(const bf16 *_
         // (umma_e).  Descriptors advance by adding (byte offset >> 4) to the 14-bit start-address
         // field (addresses stay below 2^18: no carry).
         long long tf = 0, ta = 0, tm = 0;
+        // Per INPUT row i of a segment (0 .. nr+1, image row y0 - 1 + i), the MMAs of its 3 kx
+        // shifts x CQ/2 channel steps, each with N' = (outputs fed) x N: input row i feeds
+        // outputs i - 2 (ky = 2), i - 1 (ky = 1) and i (ky = 0), whose accumulator sets are
+        // adjacent in TMEM unless the ring wraps (then two MMAs).  Output i - 2 is complete after
+        // row i; row i is released right after its own MMAs.  The accumulation order within an
+        // output is still (ky, kx, channel step).
         uint32_t q = 0, o = 0;   // input rows, output rows of this CTA
-        const uint64_t dB0 = sdesc(bbase, C::lbo_b, 128);
+        const uint64_t dB0 = sdesc(bbase, C::lbo_b3, 128);
         for (int64_t sg = blockIdx.x; sg < nseg; sg += gridDim.x) {
             const RowSeg g = row_seg(sg, H, R, nyb, tpr);
-            for (int j = 0; j < g.nr; ++j, ++o) {
-                const uint32_t b = o % NB;
+            for (int i = 0; i < g.nr + 2; ++i) {
+                const uint32_t qq = q + (uint32_t)i;
                 const long long c0 = un_clock();
-                for (uint32_t r = (j == 0 ? 0u : 2u); r < 3u; ++r) {   // input rows q+j .. q+j+2
-                    const uint32_t qq = q + (uint32_t)j + r;
-                    mbar_wait_spin(&full[qq % (uint32_t)S], (qq / (uint32_t)S) & 1u, 2);
-                }
+                mbar_wait_spin(&full[qq % (uint32_t)S], (qq / (uint32_t)S) & 1u, 2);
                 const long long c1 = un_clock();
-                if (o >= (uint32_t)NB) mbar_wait_spin(&acce[b], (o / NB - 1u) & 1u, 3);
+                const int jlo = i - 2 > 0 ? i - 2 : 0, jhi = i < g.nr - 1 ? i : g.nr - 1;
+                if (i < g.nr && o + (uint32_t)i >= (uint32_t)NB)   // output i's set is first touched here
+                    mbar_wait_spin(&acce[(o + (uint32_t)i) % NB], ((o + (uint32_t)i) / NB - 1u) & 1u, 3);
                 const long long c2 = un_clock();
                 tf += c1 - c0;
                 ta += c2 - c1;
                 tc_fence_after();
-                const uint32_t acc = tmem + b * (uint32_t)N;
-                uint64_t dA[3];
+                const uint64_t dA = sdesc(sbase + (qq % (uint32_t)S) * rreg, kRowLbo, 128);
+                // runs of outputs with adjacent accumulator sets, <= 256 columns per MMA; the common
+                // case (3 outputs, no wrap) with a compile-time instruction descriptor
+                const uint32_t sl = (o + (uint32_t)jlo) % NB;
+                if (3 * N <= 256 && jhi - jlo == 2 && sl + 2u < (uint32_t)NB) {
+                    const uint32_t acc = tmem + sl * (uint32_t)N;
 #pragma unroll
-                for (int ky = 0; ky < 3; ++ky)
-                    dA[ky] = sdesc(sbase + ((q + (uint32_t)(j + ky)) % (uint32_t)S) * rreg, kRowLbo, 128);
+                    for (int kx = 0; kx < 3; ++kx) {
 #pragma unroll
-                for (int tap = 0; tap < 9; ++tap) {
-#pragma unroll
-                    for (int c = 0; c < CQ; c += 2) {
-                        const uint32_t aoff = ((tap % 3) * 16 + (c / 2) * 2 * kRowLbo) >> 4;
-                        const uint32_t boff = ((tap * CQ + c) * C::lbo_b) >> 4;
-                        umma_e(acc, dA[tap / 3] + aoff, dB0 + boff, idesc_bf16(N), (tap | c) ? 1u : 0u);
+                        for (int c = 0; c < CQ; c += 2) {
+                            const uint32_t aoff = (kx * 16 + (c / 2) * 2 * kRowLbo) >> 4;
+                            const uint32_t boff = ((kx * CQ + c) * C::lbo_b3) >> 4;
+                            umma_e(acc, dA + aoff, dB0 + boff, idesc_bf16(3 * N), 1u);
+                        }
                     }
+                } else
+                for (int j0 = jlo; j0 <= jhi;) {
+                    const uint32_t s0 = (o + (uint32_t)j0) % NB;
+                    int len = 1;
+                    while (j0 + len <= jhi && s0 + (uint32_t)len < (uint32_t)NB && (len + 1) * N <= 256) ++len;
+                    const uint32_t acc = tmem + s0 * (uint32_t)N;
+                    const uint32_t prow = (uint32_t)(j0 - (i - 2)) * (uint32_t)N;   // first B row: part (2 - ky)
+                    const uint32_t id = idesc_bf16(len * N);
+#pragma unroll
+                    for (int kx = 0; kx < 3; ++kx) {
+#pragma unroll
+                        for (int c = 0; c < CQ; c += 2) {
+                            const uint32_t aoff = (kx * 16 + (c / 2) * 2 * kRowLbo) >> 4;
+                            const uint32_t boff = ((kx * CQ + c) * C::lbo_b3 + prow / 8 * 128) >> 4;
+                            umma_e(acc, dA + aoff, dB0 + boff, id, 1u);
+                        }
+                    }
+                    j0 += len;
                 }
-                // input row q+j is not read by later outputs; at the segment's end neither are the last two
-                umma_commit_e(&empty[(q + (uint32_t)j) % (uint32_t)S]);
-                if (j == g.nr - 1) {
-                    umma_commit_e(&empty[(q + (uint32_t)j + 1u) % (uint32_t)S]);
-                    umma_commit_e(&empty[(q + (uint32_t)j + 2u) % (uint32_t)S]);
-                }
-                umma_commit_e(&accf[b]);
+                umma_commit_e(&empty[qq % (uint32_t)S]);              // row i is not read again
+                if (i >= 2) umma_commit_e(&accf[(o + (uint32_t)(i - 2)) % NB]);   // output i - 2 complete
                 tm += un_clock() - c2;
             }
             q += (uint32_t)g.nr + 2u;
+            o += (uint32_t)g.nr;
         }
         if (lane == 0) {
             UN_TR_ADD(0, tf);
@@ -721,8 +755,12 @@ __global__ void __launch_bounds__(kRowThreads) conv3x3_rows_kernel(const bf16 *_
                 const long long c1 = un_clock();
                 te += c1 - c0;
                 tc_fence_after();
-                const int64_t t = (g.row0 + j) * tpr + g.x0 / kBM;   // 128-pixel tile index
-                conv_tile_out<N, HEAD, false>(tmem + b * (uint32_t)N, t, npix, out, part, gran, 0);
+                const int nvalid = W - g.x0 < kBM ? W - g.x0 : kBM;   // W < 128: one row of W pixels
+                conv_tile_out<N, HEAD, false>(tmem + b * (uint32_t)N, (g.row0 + j) * W + g.x0, nvalid, npix, out,
+                                              part, gran, 0);
+                // the set starts the next output at zero
+                for (int cc = 0; cc < N; cc += 16)
+                    tmem_zero16(tmem + ((uint32_t)(32 * (warp & 3)) << 16) + b * (uint32_t)N + (uint32_t)cc);
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&acce[b]);
@@ -748,9 +786,13 @@ cudaError_t launch_conv_rows_c(const bf16 *in, const bf16 *w, float *out, double
     // ring slots: as many input rows as one CTA's shared memory holds, up to 16 (the loads of a
     // row are issued when the MMAs that read the row it replaces have COMPLETED; a deep ring keeps
     // that refill ahead of the tensor core; 8 slots left the MMA warp waiting ~400 cycles per output)
-    int S = (int)((220 * 1024 - fixed) / rreg);
+    // Two CTAs per SM (each one's waits overlap the other's MMAs) when 8+ slots fit in half the
+    // shared memory and the TMEM sets allow it; else one CTA with up to 16 slots.
+    int S = (int)((110 * 1024 - fixed) / rreg);
+    const bool two = S >= 8 && RowCfg<N>::tcols <= 256;
+    if (!two) S = (int)((220 * 1024 - fixed) / rreg);
     S = S > 16 ? 16 : S;
-    if (S < 4) return cudaErrorInvalidValue;
+    if (S < 4) return cudaErrorNotSupported;   // weights + 4 row slots do not fit: the gather kernel
     const size_t smem = fixed + S * rreg;
     static size_t smem_set = 0;
     static int nsm = 0;
@@ -769,13 +811,12 @@ cudaError_t launch_conv_rows_c(const bf16 *in, const bf16 *w, float *out, double
         if (e != cudaSuccess) return e;
         smem_set = smem;
     }
-    int occ = 1;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, conv3x3_rows_kernel<N, HEAD, CQ>, kRowThreads, smem);
-    if (e != cudaSuccess) return e;
-    occ = occ < 1 ? 1 : (occ > 512 / RowCfg<N>::tcols ? 512 / RowCfg<N>::tcols : occ);   // TMEM columns
+    // CTAs per SM from the shared-memory split above (CTAs are independent: an over-estimate only
+    // queues CTAs, it cannot deadlock)
+    const int occ = two ? 2 : 1;
     const int gran = (H * W) % 32 == 0 ? 32 : 1;
     // segment height R: the smallest cost max-segments-per-CTA x (R + 2) input rows over R in 4..64
-    const int64_t B = npix / ((int64_t)H * W), cols = B * (W / kBM);
+    const int64_t B = npix / ((int64_t)H * W), cols = B * ((W + kBM - 1) / kBM);
     const int64_t slots = (int64_t)nsm * occ;
     int R = 4;
     int64_t best = -1;
@@ -802,20 +843,27 @@ cudaError_t launch_conv_rows_c(const bf16 *in, const bf16 *w, float *out, double
 template <int N, bool HEAD>
 cudaError_t launch_conv_rows(const bf16 *in, const bf16 *w, float *out, double *part, int64_t npix, int H, int W,
                              int cin, cudaStream_t st) {
-    switch (cin / 8) {   // cin a multiple of 16, <= 64
+    switch (cin / 8) {   // cin a multiple of 16
         case 2: return launch_conv_rows_c<N, HEAD, 2>(in, w, out, part, npix, H, W, cin, st);
         case 4: return launch_conv_rows_c<N, HEAD, 4>(in, w, out, part, npix, H, W, cin, st);
         case 6: return launch_conv_rows_c<N, HEAD, 6>(in, w, out, part, npix, H, W, cin, st);
         case 8: return launch_conv_rows_c<N, HEAD, 8>(in, w, out, part, npix, H, W, cin, st);
-        default: return cudaErrorInvalidValue;
+        case 16: return launch_conv_rows_c<N, HEAD, 16>(in, w, out, part, npix, H, W, cin, st);
+        default: return cudaErrorNotSupported;
     }
 }
 
 template <int N, bool HEAD>
 cudaError_t launch_conv_any(const bf16 *in, const bf16 *w, float *out, double *part, int64_t npix, int H, int W,
                             int cin, cudaStream_t st) {
+    // the row kernel for rows of a multiple of 128 pixels or of 32 / 64 / 96 pixels (one row per
+    // 128-lane tile, the rest of the tile idle) when its weights and a 4-row ring fit in shared
+    // memory; else the im2col gather kernel
     static const int norows = getenv("UN_NO_ROWS") ? atoi(getenv("UN_NO_ROWS")) : 0;
-    if (W % kBM == 0 && cin <= 64 && !norows) return launch_conv_rows<N, HEAD>(in, w, out, part, npix, H, W, cin, st);
+    if (!norows && (W % kBM == 0 || (W < kBM && W % 32 == 0))) {
+        const cudaError_t e = launch_conv_rows<N, HEAD>(in, w, out, part, npix, H, W, cin, st);
+        if (e != cudaErrorNotSupported) return e;
+    }
     return launch_conv_n<N, HEAD>(in, w, out, part, npix, H, W, cin, st);
 }
 

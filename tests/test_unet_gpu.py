@@ -37,7 +37,11 @@ def _rel(a, b):
                                             (1, 5, 256, 16, 64), (2, 1, 128, 48, 128),
                                             # enough row tiles that every CTA's shared-memory ring
                                             # wraps (more iterations than stages)
-                                            (8, 80, 128, 64, 16), (8, 160, 256, 16, 16)])
+                                            (8, 80, 128, 64, 16), (8, 160, 256, 16, 16),
+                                            # rows of 32 / 64 pixels through the row kernel (one row
+                                            # per 128-lane tile), cin up to 128
+                                            (2, 20, 64, 128, 32), (3, 12, 32, 64, 128), (2, 16, 64, 32, 64),
+                                            (9, 40, 64, 128, 16)])
 def test_conv3x3_tensor_core_kernel(B, H, W, cin, cout):
     import torch
     g = np.random.default_rng(B * 1000 + cin + cout)
