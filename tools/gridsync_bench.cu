@@ -35,6 +35,21 @@ __global__ void k_hier(int iters, unsigned *count) {
     }
 }
 
+// (c) a flat barrier: CTA barrier, one release-add per CTA on a global counter, thread 0 polls with
+// acquire loads until every CTA of this round arrived, CTA barrier.
+__global__ void k_flat(int iters, unsigned *count) {
+    for (int i = 0; i < iters; ++i) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(count) : "memory");
+            const unsigned target = gridDim.x * (unsigned)(i + 1);
+            while (ld_acquire(count) < target) {
+            }
+        }
+        __syncthreads();
+    }
+}
+
 int main() {
     int nsm = 0;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
@@ -42,8 +57,8 @@ int main() {
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    for (int blocks : {64, 128, 256, 444}) {
-        for (int threads : {256, 512}) {
+    for (int blocks : {64, 128, 148, 256}) {
+        for (int threads : {256, 512, 1024}) {
             void *args[] = {(void *)&iters};
             cudaLaunchCooperativeKernel((void *)k_grid, blocks, threads, args, 0, 0);   // warm-up
             cudaEventRecord(e0);
@@ -59,6 +74,24 @@ int main() {
     }
     unsigned *count;
     cudaMalloc(&count, 4);
+    for (int blocks : {128, 148}) {
+        for (int threads : {512, 1024}) {
+            for (int rep = 0; rep < 2; ++rep) {
+                cudaMemset(count, 0, 4);
+                void *args[] = {(void *)&iters, (void *)&count};
+                cudaEventRecord(e0);
+                cudaLaunchCooperativeKernel((void *)k_flat, blocks, threads, args, 0, 0);
+                cudaEventRecord(e1);
+                cudaEventSynchronize(e1);
+                float ms = 0;
+                cudaEventElapsedTime(&ms, e0, e1);
+                cudaError_t e = cudaGetLastError();
+                if (rep)
+                    printf("{\"kind\": \"flat\", \"blocks\": %d, \"threads\": %d, \"us_per_sync\": %.3f, \"err\": \"%s\"}\n",
+                           blocks, threads, 1e3 * ms / iters, cudaGetErrorString(e));
+            }
+        }
+    }
     for (int cs : {8, 16}) {
         cudaFuncSetAttribute(k_hier, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         for (int blocks : {128, 256}) {
