@@ -317,6 +317,11 @@ int pf_debug_block_spans(long long *out);
  * loaded, [2] stage-1 mu/M, [3] u*, [4] stage-2 mu/M, [5] tile written, [6] grid barrier passed.
  * Zeros in a normal build.  out: host memory the caller owns.  Returns a cudaError_t value. */
 int pf_debug_step_trace(long long *out);
+/* Diagnostic of a PF_TRACE build: the band kernel's (kernel_path 6) phase timeline of its last
+ * launch, out[16 blocks][128 stages][4] int64 clock64 cycles of thread 0 of the first cluster's
+ * blocks: [0] after phase A (mu/M), [1] after phase B (update), [2] after the stage's cluster
+ * barrier, [3] stage start.  Zeros in a normal build.  Returns a cudaError_t value. */
+int pf_debug_band_trace(long long *out);
 
 /* Release everything the ctx owns.  NULL-safe.  Slab mode: collective (NCCL teardown). */
 void pf_free(pf_ctx *ctx);

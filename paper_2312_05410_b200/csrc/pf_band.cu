@@ -13,11 +13,14 @@
 //      registers (stage 1 also keeps u^n there as the stage-2 base);
 //   C  the new values go to the block's own rows (with their periodic ghost columns and, at the
 //      global y boundaries, the mirror rows, R-12), and the two bottom / two top rows are pushed
-//      straight into the neighbouring blocks' halo rows (DSMEM stores);
-//   -- one cluster barrier: every halo is complete --
+//      straight into the neighbouring blocks' halo rows with st.async stores that complete on the
+//      receiving block's mbarrier of that halo parity;
+//   -- a block waits for exactly its two neighbours' rows (no cluster-wide barrier per stage) --
 // The halo rows are double-buffered by stage parity (a push of stage s+1 cannot overwrite rows a
-// neighbour still reads in stage s), so one cluster barrier (~0.2 us) per stage suffices and no
-// stage touches L2.  (Measured alternative: halo rows through a global buffer with per-band epoch
+// neighbour still reads in stage s), and no stage touches L2.  (Round 2: with the per-stage
+// coefficient struct passed by reference -- selecting it at run time had copied it through local
+// memory every stage, a third of the stage -- the st.async pushes beat one cluster barrier per
+// stage, 1.34 vs 1.21 G cell-updates/s on configs[0]; build with -DPF_BAND_P2P=0 for the barrier.)  (Measured alternative: halo rows through a global buffer with per-band epoch
 // flags, one block per SM over the whole GPU: 2-3x SLOWER than the persistent tile kernel -- every
 // stage paid several L2 round trips.)
 // The per-cell arithmetic is pf_cell.cuh with the argument order of the tile kernel, so results
@@ -25,6 +28,7 @@
 // are written back to the state buffer at the end of the launch; the host rebuilds the ghost frame.
 #include <cooperative_groups.h>
 #include <cstdint>
+#include <cstdlib>
 
 #include "pf_cell.cuh"
 #include "pf_internal.h"
@@ -61,8 +65,20 @@ struct BandGeo {
     __host__ __device__ size_t bytes(size_t esz) const { return (size_t)(3 * uplane + 3 * wplane) * esz + 64 * 8 + 16; }
 };
 
+// Phase timeline (diagnostic build, -DPF_TRACE=1; pf_debug_band_trace): per block of the first
+// cluster and stage g < 128, thread 0's clock64 after phase A's CTA barrier, after phase B's, and
+// after the stage's cluster barrier; [3] the stage start.
+#ifndef PF_TRACE
+#define PF_TRACE 0
+#endif
+__device__ long long g_btrace[16][128][4];
+#define PF_BAND_STAMP(g, k)                                                                          \
+    do {                                                                                             \
+        if (PF_TRACE && threadIdx.x == 0 && blockIdx.x < 16 && (g) < 128) g_btrace[blockIdx.x][(g)][(k)] = clock64(); \
+    } while (0)
+
 #ifndef PF_BAND_P2P
-#define PF_BAND_P2P 0   // 1: halo rows by st.async + per-parity mbarriers instead of a cluster barrier per stage (measured slower)
+#define PF_BAND_P2P 1   // halo rows by st.async + per-parity mbarriers (0: a cluster barrier per stage, 10% slower)
 #endif
 __device__ __forceinline__ uint32_t smem_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 // shared::cluster address of the same location in CTA `rank` of the cluster
@@ -193,14 +209,16 @@ __global__ void __launch_bounds__(kBT, 1) band_kernel(Layout L, KC<real> k1, KC<
     const uint32_t rsu_up = top ? 0u : mapa_rank(su_a, bi + 1), rhb_up = top ? 0u : mapa_rank(hb_a, bi + 1);
     const int64_t nstages = 2 * nsteps;
 
-    for (int64_t s = 0; s < nsteps; ++s) {
-        for (int stage = 1; stage <= 2; ++stage) {
-            const KC<real> k = stage == 1 ? k1 : k2;
+    // One midpoint stage; called with the stage's coefficient struct by reference (a struct selected
+    // at run time, `KC k = stage == 1 ? k1 : k2`, was copied through local memory every stage:
+    // ~1600 of ~4800 cycles per stage on configs[0], tools/trace_band.py)
+    auto run_stage = [&](const KC<real> &k, const int stage, const int64_t s) {
             const int64_t g = 2 * s + stage - 1;   // stage index; reads halo parity par = g & 1
             if (PF_BAND_P2P && g > 0) {           // the neighbours' rows of stage g - 1
                 if (t == 0) hbar_expect(&hbar[par], rx_bytes);
                 hbar_wait(&hbar[par], (uint32_t)(((g - 1) >> 1) & 1));
             }
+            PF_BAND_STAMP(g, 3);
             // A: mu_c, mu_phi, M on rows -1 .. h, columns -1 .. nx (row a2)
             auto cell_a = [&](int rr, int x) {
                 const int o0 = gg.u(BandGeo::srow(rr, h, par), x);
@@ -217,6 +235,7 @@ __global__ void __launch_bounds__(kBT, 1) band_kernel(Layout L, KC<real> k1, KC<
                 if (t + i * kBT < nA) cell_a(arr[i], ax[i]);
             for (int q = t + kAC * kBT; q < nA; q += kBT) cell_a(q / (nx + 2) - 1, q - (q / (nx + 2)) * (nx + 2) - 1);
             __syncthreads();
+            PF_BAND_STAMP(g, 0);
             // B: fluxes, source, vapour, update of the owned cells (rows a3-a5), into registers
 #pragma unroll
             for (int i = 0; i < MAXC; ++i) {
@@ -241,6 +260,7 @@ __global__ void __launch_bounds__(kBT, 1) band_kernel(Layout L, KC<real> k1, KC<
                 }
             }
             __syncthreads();   // the block is done reading its own rows
+            PF_BAND_STAMP(g, 1);
             // C: own rows (+ ghost columns, + mirror rows at the global boundaries) and the pushes
             // of the border rows into the neighbours' halos, all into halo parity np
             const int np = par ^ 1;
@@ -279,8 +299,12 @@ __global__ void __launch_bounds__(kBT, 1) band_kernel(Layout L, KC<real> k1, KC<
             }
             if (PF_BAND_P2P) __syncthreads();   // own rows and mirror rows in place
             else cluster.sync();   // every halo row of parity np is in place; every block left phase B
+            PF_BAND_STAMP(g, 2);
             par = np;
-        }
+    };
+    for (int64_t s = 0; s < nsteps; ++s) {
+        run_stage(k1, 1, s);
+        run_stage(k2, 2, s);
     }
     if (PF_BAND_P2P) cluster.sync();   // no block leaves while a neighbour may still address it
     // owned cells back to the state buffer (ghost frame rebuilt by the host)
@@ -344,6 +368,14 @@ cudaError_t launch_band_t(const Layout &L, const BandPlan &B, const Coef &K, voi
 
 }  // namespace
 
+}  // namespace pf
+// Diagnostic: the band kernel's phase timeline of its last launch (PF_TRACE builds; zeros
+// otherwise): out[16 blocks][128 stages][4] clock64 cycles (see PF_BAND_STAMP).
+extern "C" int pf_debug_band_trace(long long *out) {
+    return (int)cudaMemcpyFromSymbol(out, pf::g_btrace, sizeof(pf::g_btrace));
+}
+namespace pf {
+
 bool make_band_plan(int precision, const Layout &L, BandPlan &B) {
     B = BandPlan();
     const size_t esz = precision == 0 ? 8 : 4;
@@ -351,7 +383,9 @@ bool make_band_plan(int precision, const Layout &L, BandPlan &B) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     // one cluster per member, bands of >= 2 rows, at most 16 blocks (non-portable cluster size)
-    const int bpm = L.ny_loc / 2 < kMaxCluster ? L.ny_loc / 2 : kMaxCluster;
+    static const int maxc = getenv("PF_BAND_CLUSTER") ? atoi(getenv("PF_BAND_CLUSTER")) : kMaxCluster;   // A/B knob
+    const int cmax = maxc >= 1 && maxc <= kMaxCluster ? maxc : kMaxCluster;
+    const int bpm = L.ny_loc / 2 < cmax ? L.ny_loc / 2 : cmax;
     if (bpm < 1) return false;
     const int hmax = (L.ny_loc + bpm - 1) / bpm;
     if ((int64_t)hmax * L.nx > kMaxCells) return false;
