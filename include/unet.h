@@ -97,7 +97,9 @@ pf_status un_conv3x3(const uint16_t *in, int32_t batch, int32_t H, int32_t W, in
 /* Diagnostic of a UN_TRACE build (PF_NVCC_EXTRA=-DUN_TRACE=1): per CTA (160 slots) cycle sums of the
  * row-tile convolution's roles since the last reset, out[160][8] = {MMA warp: full wait, acce wait,
  * issue; producer: empty wait, copy issue; epilogue warp 0: accf wait, drain; iterations}.  Zeros
- * in a normal build.  reset != 0 zeroes the record after reading.  Returns a cudaError_t value. */
+ * in a normal build; then out[160 * 8 + 4 c + k] = CTA c's clock64 at entry, MMA loop start, MMA loop
+ * end and exit of the last launch (out holds 160 * 12 values).  reset != 0 zeroes the sums after
+ * reading.  Returns a cudaError_t value. */
 int un_debug_trace(unsigned long long *out, int reset);
 
 pf_status un_stream(un_ctx *ctx, void **stream);

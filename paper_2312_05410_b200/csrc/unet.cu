@@ -135,6 +135,11 @@ __host__ __device__ __forceinline__ int64_t rc_off(int64_t row, int x, int W, in
 #define UN_TRACE 0   // diagnostic builds: per-CTA cycle sums of the row kernel's roles (un_debug_trace)
 #endif
 __device__ unsigned long long g_untrace[160][8];
+__device__ long long g_untrace_span[160][4];   // per CTA: entry, MMA loop start, MMA loop end, exit (clock64)
+#define UN_SPAN(k)                                                                                  \
+    do {                                                                                            \
+        if (UN_TRACE && blockIdx.x < 160) g_untrace_span[blockIdx.x][(k)] = clock64();              \
+    } while (0)
 __device__ __forceinline__ long long un_clock() { return UN_TRACE ? clock64() : 0; }
 #define UN_TR_ADD(slot, v)                                                                  \
     do {                                                                                    \
@@ -561,12 +566,18 @@ __device__ __forceinline__ RowSeg row_seg(int64_t seg, int H, int R, int nyb, in
 // accumulator set o % NB and commits empty[slot] of the input row no later output needs and
 // accf[b]; epilogue group o % 2 (warps 4g .. 4g+3) drains set b (tcgen05.ld, fp32 stores, GroupNorm
 // partial sums) and arrives on acce[b].
+// two CTAs per SM for the narrow layers (their ring fits in half the shared memory): registers
+// capped at 72 per thread so two 416-thread CTAs fit the register file
+template <int N, int CQ>
+constexpr int row_min_blocks() { return CQ <= 4 && N <= 64 ? 2 : 1; }
+
 template <int N, bool HEAD, int CQ>
-__global__ void __launch_bounds__(kRowThreads) conv3x3_rows_kernel(const bf16 *__restrict__ in,
+__global__ void __launch_bounds__(kRowThreads, row_min_blocks<N, CQ>()) conv3x3_rows_kernel(const bf16 *__restrict__ in,
                                                                    const bf16 *__restrict__ w, float *__restrict__ out,
                                                                    double *__restrict__ part, int64_t npix, int H,
                                                                    int W, int S, int R, int gran) {
     using C = RowCfg<N>;
+    if (threadIdx.x == 32 * kRowMmaWarp) UN_SPAN(0);
     constexpr int NB = C::nbuf;
     static_assert(CQ >= 2 && CQ <= 16 && CQ % 2 == 0, "cin = 16 .. 128");
     extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -668,6 +679,7 @@ __global__ void __launch_bounds__(kRowThreads) conv3x3_rows_kernel(const bf16 *_
         // (umma_e).  Descriptors advance by adding (byte offset >> 4) to the 14-bit start-address
         // field (addresses stay below 2^18: no carry).
         long long tf = 0, ta = 0, tm = 0;
+        if (lane == 0) UN_SPAN(1);
         // Per INPUT row i of a segment (0 .. nr+1, image row y0 - 1 + i), the MMAs of its 3 kx
         // shifts x CQ/2 channel steps, each with N' = (outputs fed) x N: input row i feeds
         // outputs i - 2 (ky = 2), i - 1 (ky = 1) and i (ky = 0), whose accumulator sets are
@@ -732,6 +744,7 @@ __global__ void __launch_bounds__(kRowThreads) conv3x3_rows_kernel(const bf16 *_
             o += (uint32_t)g.nr;
         }
         if (lane == 0) {
+            UN_SPAN(2);
             UN_TR_ADD(0, tf);
             UN_TR_ADD(1, ta);
             UN_TR_ADD(2, tm);
@@ -775,6 +788,7 @@ __global__ void __launch_bounds__(kRowThreads) conv3x3_rows_kernel(const bf16 *_
     tc_fence_before();
     __syncthreads();
     if (warp == kRowMmaWarp) tmem_dealloc<C::tcols>(tmem);
+    if (threadIdx.x == 32 * kRowMmaWarp) UN_SPAN(3);
 }
 
 template <int N, bool HEAD, int CQ>
@@ -788,8 +802,8 @@ cudaError_t launch_conv_rows_c(const bf16 *in, const bf16 *w, float *out, double
     // that refill ahead of the tensor core; 8 slots left the MMA warp waiting ~400 cycles per output)
     // Two CTAs per SM (each one's waits overlap the other's MMAs) when 8+ slots fit in half the
     // shared memory and the TMEM sets allow it; else one CTA with up to 16 slots.
-    int S = (int)((110 * 1024 - fixed) / rreg);
-    const bool two = S >= 8 && RowCfg<N>::tcols <= 256;
+    int S = (int)((104 * 1024 - fixed) / rreg);
+    const bool two = S >= 8 && RowCfg<N>::tcols <= 256 && row_min_blocks<N, CQ>() == 2;
     if (!two) S = (int)((220 * 1024 - fixed) / rreg);
     S = S > 16 ? 16 : S;
     if (S < 4) return cudaErrorNotSupported;   // weights + 4 row slots do not fit: the gather kernel
@@ -833,9 +847,17 @@ cudaError_t launch_conv_rows_c(const bf16 *in, const bf16 *w, float *out, double
     const int64_t nseg = cols * ((H + R - 1) / R);
     const unsigned grid = (unsigned)(nseg < slots ? nseg : slots);
     static const bool dbg = getenv("UN_DEBUG_LAUNCH") && atoi(getenv("UN_DEBUG_LAUNCH"));
-    if (dbg)
-        fprintf(stderr, "conv_rows N=%d CQ=%d H=%d W=%d S=%d R=%d occ=%d grid=%u smem=%zu\n", N, CQ, H, W, S, R, occ, grid,
-                smem);
+    if (dbg) {
+        cudaFuncAttributes fa{};
+        cudaFuncGetAttributes(&fa, conv3x3_rows_kernel<N, HEAD, CQ>);
+        int occ_api = -1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_api, conv3x3_rows_kernel<N, HEAD, CQ>, kRowThreads, smem);
+        fprintf(stderr,
+                "conv_rows N=%d CQ=%d H=%d W=%d S=%d R=%d occ=%d grid=%u smem=%zu | regs=%d static_smem=%zu local=%zu "
+                "maxdyn=%d occ_api=%d\n",
+                N, CQ, H, W, S, R, occ, grid, smem, fa.numRegs, fa.sharedSizeBytes, fa.localSizeBytes,
+                fa.maxDynamicSharedSizeBytes, occ_api);
+    }
     conv3x3_rows_kernel<N, HEAD, CQ><<<grid, kRowThreads, smem, st>>>(in, w, out, part, npix, H, W, S, R, gran);
     return cudaGetLastError();
 }
@@ -1688,6 +1710,8 @@ pf_status un_conv3x3(const uint16_t *in, int32_t batch, int32_t H, int32_t W, in
 
 int un_debug_trace(unsigned long long *out, int reset) {
     cudaError_t e = cudaMemcpyFromSymbol(out, g_untrace, sizeof(g_untrace));
+    if (e == cudaSuccess)   // the per-CTA spans follow the sums: out[160 * 8 .. + 160 * 4)
+        e = cudaMemcpyFromSymbol(out + 160 * 8, g_untrace_span, sizeof(g_untrace_span));
     if (e == cudaSuccess && reset) {
         static unsigned long long zero[160][8];
         e = cudaMemcpyToSymbol(g_untrace, zero, sizeof(zero));

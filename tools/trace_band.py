@@ -24,9 +24,11 @@ def main():
     bb = b[:, :, 1] - b[:, :, 0]
     cc = b[:, :, 2] - b[:, :, 1]
     tot = b[:, 1:, 3] - b[:, :-1, 3]
+    wait = b[:, 1:, 3] - b[:, :-1, 2]   # P2P builds: the halo wait (stage end to next stage start)
     print(json.dumps({"phase_A_cyc": float(np.median(a)), "phase_B_cyc": float(np.median(bb)),
                       "phase_C_cyc": float(np.median(cc)), "stage_cyc": float(np.median(tot)),
-                      "phase_C_max_over_blocks_cyc": float(np.median(cc.max(axis=0)))}))
+                      "phase_C_max_over_blocks_cyc": float(np.median(cc.max(axis=0))),
+                      "halo_wait_cyc": float(np.median(wait))}))
 
 
 if __name__ == "__main__":
