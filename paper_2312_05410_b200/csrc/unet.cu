@@ -532,8 +532,8 @@ __host__ __device__ constexpr uint32_t row_region(int cq) { return (cq * kRowLbo
 template <int N>
 struct RowCfg {
     // TMEM accumulator sets, a multiple of the epilogue groups (set b is always drained by group
-    // b % kRowEpiGroups): 6 x N columns for N <= 32, 4 x N above
-    static constexpr int nbuf = N <= 32 ? 6 : 4;
+    // b % kRowEpiGroups): 8 x N columns for N <= 32, 4 x N above
+    static constexpr int nbuf = N <= 32 ? 8 : 4;
     static_assert(nbuf % kRowEpiGroups == 0, "accumulator sets per epilogue group");
     static constexpr int tneed = nbuf * N;
     static constexpr int tcols = tneed <= 32 ? 32 : tneed <= 64 ? 64 : tneed <= 128 ? 128 : tneed <= 256 ? 256 : 512;
