@@ -1654,6 +1654,7 @@ cudaError_t launch_persistent_t(const Layout &L, const KC<real> &k1, const KC<re
         if (tby == 9) return launch_persistent_step<real, MOB, FE, 8, 544>(L, k1, k2, U, Us, vel, nsteps, flags, epoch, s);
         if (tby == 16) return launch_persistent_step<real, MOB, FE, 16, 1024>(L, k1, k2, U, Us, vel, nsteps, flags, epoch, s);
         if (tby == 12) return launch_persistent_step<real, MOB, FE, 12, 704>(L, k1, k2, U, Us, vel, nsteps, flags, epoch, s);
+        if (tby == 15) return launch_persistent_step<real, MOB, FE, 15, 1024>(L, k1, k2, U, Us, vel, nsteps, flags, epoch, s);
 #endif
         if (cells <= (int64_t)1 << PF_STEP_TBY4_LOG2) return launch_persistent_step<real, MOB, FE, 4, 512>(L, k1, k2, U, Us, vel, nsteps, flags, epoch, s);
         // 2^14 .. 2^16 cells (configs[1]): 32 x 16 tiles with 1024 threads, so that every phase of
