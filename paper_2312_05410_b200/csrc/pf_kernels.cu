@@ -433,6 +433,8 @@ __global__ void __launch_bounds__(kStepNT) persistent_step_kernel(Layout L, KC<r
         const real *in = (s & 1) ? Us : U;
         real *out = (s & 1) ? U : Us;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            if (PF_TRACE && threadIdx.x == 0 && t == (int)blockIdx.x && blockIdx.x < kStepTraceBlocks && s < kStepTraceSteps)
+                g_strace[blockIdx.x][s][7] = step_gtimer();
             const int m = t / (tx * ty), r = t - m * (tx * ty);
             const int by = r / tx, bxi = r - by * tx;
             if (flags && s > 0) {   // the neighbours' step s-1 (the previous launch: stream order)

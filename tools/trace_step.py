@@ -44,6 +44,7 @@ def main():
     step = b[:, 1:, 6].min(axis=0) - b[:, :-1, 6].min(axis=0)
     out["step_ns"] = float(np.median(step))
     out["start_after_release_ns"] = float(np.median(b[:, 1:, 0] - b[:, :-1, 6]))
+    out["loop_top_after_release_ns"] = float(np.median(b[:, 1:, 7] - b[:, :-1, 6]))
     print(json.dumps(out), flush=True)
 
 
