@@ -410,7 +410,12 @@ def run_ours(args):
                    "streams); copies amortised over the steps of one call; one warm-up call, median of 3 timed calls",
            "runs_ms": runs}
 
-    slab = _slab_leg(args, ws, rank, local, dist, dev) if (cfg == 3 and not args.no_slab) else None
+    slab = None
+    if cfg == 3 and not args.no_slab:
+        try:   # a failure of the slab leg (its own NCCL communicator) must not cost the main line
+            slab = _slab_leg(args, ws, rank, local, dist, dev)
+        except Exception as exc:   # noqa: BLE001 -- reported in the line, not swallowed
+            slab = {"error": f"{type(exc).__name__}: {exc}"[:300]} if rank == 0 else None
 
     line = None
     if rank == 0:
