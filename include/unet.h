@@ -63,10 +63,15 @@ pf_status un_set_weights(un_ctx *ctx, const float *blob, int64_t n);
  *   hist [batch][lb][H][W] fp32 (values are rounded to bf16 on entry), dt [batch] fp32,
  *   out [batch][H][W] fp32.  1 <= batch <= max_batch.  The 29 launches are captured into a CUDA
  *   graph on the first call with a given (batch, hist, dt, out) and replayed by later calls with
- *   the same arguments (buffer contents and weights may change in between). */
+ *   the same arguments (buffer contents and weights may change in between; up to 8 such graphs
+ *   are kept, least recently used replaced). */
 pf_status un_forward_device(un_ctx *ctx, int32_t batch, const float *hist, const float *dt, float *out);
 
-/* Same with host buffers: H2D copy, forward, D2H copy; returns after the result is on the host. */
+/* Same with host buffers: H2D copy, forward, D2H copy; returns after the result is on the host.
+ * Batches of >= 16 samples are pipelined over 4 sample chunks (the H2D copy of chunk k+1 and the D2H
+ * copy of chunk k-1 overlap the forward of chunk k; one cached CUDA graph per chunk); the copies
+ * overlap only when hist / dt / out are page-locked host memory.  Same results as one forward of
+ * the whole batch (samples are independent). */
 pf_status un_forward(un_ctx *ctx, int32_t batch, const float *hist, const float *dt, float *out);
 
 /* Autoregressive rollout (SPEC-style window bookkeeping, "roll out the remaining part"):

@@ -1196,13 +1196,22 @@ struct un_ctx {
     std::vector<cudaEvent_t> pool;
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> rec;
     double flops = 0.0;
-    // CUDA graph of the last forward (batch and buffer pointers as the key): replays skip the
-    // 35 launch latencies; rebuilt when the key changes, bypassed while profiling
-    cudaGraphExec_t gexec = nullptr;
-    int gB = 0;
-    const void *gh = nullptr, *gd = nullptr;
-    void *go = nullptr;
-    int64_t glaunch = 0;
+    // CUDA graphs of recent forwards (batch and buffer pointers as the key; un_forward's chunks
+    // use one entry each): replays skip the 29 launch latencies; bypassed while profiling
+    struct GraphEntry {
+        cudaGraphExec_t exec = nullptr;
+        int B = 0;
+        const void *h = nullptr, *d = nullptr;
+        void *o = nullptr;
+        int64_t launches = 0, used = 0;
+    };
+    static constexpr int kGraphs = 8;
+    GraphEntry graphs[kGraphs];
+    int64_t graph_clock = 0;
+    // un_forward's copy pipeline: H2D and D2H streams, per-chunk events
+    static constexpr int kChunks = 4;
+    cudaStream_t cs_in = nullptr, cs_out = nullptr;
+    cudaEvent_t ev_in[kChunks] = {}, ev_fwd[kChunks] = {};
 };
 
 namespace {
@@ -1417,8 +1426,14 @@ pf_status un_create(const un_params *p, un_ctx **out) {
         un_free(c);
         return s;
     };
-    if (cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking) != cudaSuccess ||
+    bool ev_ok = true;
+    for (int k = 0; k < un_ctx::kChunks; ++k)
+        ev_ok = ev_ok && cudaEventCreateWithFlags(&c->ev_in[k], cudaEventDisableTiming) == cudaSuccess &&
+                cudaEventCreateWithFlags(&c->ev_fwd[k], cudaEventDisableTiming) == cudaSuccess;
+    if (!ev_ok || cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking) != cudaSuccess ||
         cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&c->cs_in, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&c->cs_out, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess) {
         c->err = "cudaStreamCreate / cudaEventCreate failed";
@@ -1531,31 +1546,38 @@ pf_status un_forward_device(un_ctx *c, int32_t batch, const float *hist, const f
     cudaSetDevice(c->p.device);
     static const bool nograph = getenv("UN_NO_GRAPH") && atoi(getenv("UN_NO_GRAPH"));
     if (c->prof || nograph) return forward(c, batch, hist, dt, out);
-    if (!c->gexec || c->gB != batch || c->gh != hist || c->gd != dt || c->go != out) {
-        if (c->gexec) cudaGraphExecDestroy(c->gexec);
-        c->gexec = nullptr;
+    un_ctx::GraphEntry *ge = nullptr;
+    for (auto &x : c->graphs)
+        if (x.exec && x.B == batch && x.h == hist && x.d == dt && x.o == out) ge = &x;
+    if (!ge) {   // capture into the least recently used entry
+        ge = &c->graphs[0];
+        for (auto &x : c->graphs)
+            if (!x.exec || x.used < ge->used) ge = &x;
+        if (ge->exec) cudaGraphExecDestroy(ge->exec);
+        ge->exec = nullptr;
         cudaGraph_t g = nullptr;
         UCK(c, cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
         const int64_t l0 = c->launches;
         pf_status s = forward(c, batch, hist, dt, out);
         cudaError_t e = cudaStreamEndCapture(c->st, &g);
-        c->glaunch = c->launches - l0;
+        ge->launches = c->launches - l0;
         c->launches = l0;
         if (s != PF_OK) {
             if (g) cudaGraphDestroy(g);
             return s;
         }
         if (e != cudaSuccess) return fail(c, PF_ERR_CUDA, fmt("forward capture: %s", cudaGetErrorString(e)));
-        e = cudaGraphInstantiate(&c->gexec, g, 0);
+        e = cudaGraphInstantiate(&ge->exec, g, 0);
         cudaGraphDestroy(g);
         if (e != cudaSuccess) return fail(c, PF_ERR_CUDA, fmt("forward graph: %s", cudaGetErrorString(e)));
-        c->gB = batch;
-        c->gh = hist;
-        c->gd = dt;
-        c->go = out;
+        ge->B = batch;
+        ge->h = hist;
+        ge->d = dt;
+        ge->o = out;
     }
-    UCK(c, cudaGraphLaunch(c->gexec, c->st));
-    c->launches += c->glaunch;
+    ge->used = ++c->graph_clock;
+    UCK(c, cudaGraphLaunch(ge->exec, c->st));
+    c->launches += ge->launches;
     return PF_OK;
 }
 
@@ -1563,12 +1585,35 @@ pf_status un_forward(un_ctx *c, int32_t batch, const float *hist, const float *d
     if (!c || !hist || !dt || !out) return fail(c, PF_ERR_ARG, "NULL argument");
     if (batch < 1 || batch > c->p.max_batch) return fail(c, PF_ERR_ARG, "batch out of range");
     cudaSetDevice(c->p.device);
-    const size_t hw = (size_t)c->p.height * c->p.width;
-    UCK(c, cudaMemcpyAsync(c->dhist, hist, (size_t)batch * c->p.lb * hw * sizeof(float), cudaMemcpyHostToDevice, c->st));
-    UCK(c, cudaMemcpyAsync(c->ddt, dt, (size_t)batch * sizeof(float), cudaMemcpyHostToDevice, c->st));
-    pf_status s = un_forward_device(c, batch, c->dhist, c->ddt, c->dout);
-    if (s != PF_OK) return s;
-    UCK(c, cudaMemcpyAsync(out, c->dout, (size_t)batch * hw * sizeof(float), cudaMemcpyDeviceToHost, c->st));
+    const size_t hw = (size_t)c->p.height * c->p.width, lb = (size_t)c->p.lb;
+    // Pipelined over up to kChunks sample chunks: the H2D copy of chunk k+1 (stream cs_in) and the
+    // D2H copy of chunk k-1 (cs_out) overlap the forward of chunk k (c->st; the chunks' forwards
+    // share the activation buffers and run in order).  The copies are asynchronous only from
+    // page-locked host memory; from pageable memory the driver stages them and they serialise.
+    const int nch = batch >= 4 * un_ctx::kChunks ? un_ctx::kChunks : 1;
+    const int per = (batch + nch - 1) / nch;
+    UCK(c, cudaEventRecord(c->ev_fwd[0], c->st));   // order after earlier work on c->st
+    UCK(c, cudaStreamWaitEvent(c->cs_in, c->ev_fwd[0], 0));
+    for (int k = 0; k < nch; ++k) {
+        const int b0 = k * per, nb = b0 + per <= batch ? per : batch - b0;
+        if (nb <= 0) break;
+        UCK(c, cudaMemcpyAsync(c->dhist + b0 * lb * hw, hist + b0 * lb * hw, (size_t)nb * lb * hw * sizeof(float),
+                               cudaMemcpyHostToDevice, c->cs_in));
+        UCK(c, cudaMemcpyAsync(c->ddt + b0, dt + b0, (size_t)nb * sizeof(float), cudaMemcpyHostToDevice, c->cs_in));
+        UCK(c, cudaEventRecord(c->ev_in[k], c->cs_in));
+    }
+    for (int k = 0; k < nch; ++k) {
+        const int b0 = k * per, nb = b0 + per <= batch ? per : batch - b0;
+        if (nb <= 0) break;
+        UCK(c, cudaStreamWaitEvent(c->st, c->ev_in[k], 0));
+        pf_status s = un_forward_device(c, nb, c->dhist + b0 * lb * hw, c->ddt + b0, c->dout + b0 * hw);
+        if (s != PF_OK) return s;
+        UCK(c, cudaEventRecord(c->ev_fwd[k], c->st));
+        UCK(c, cudaStreamWaitEvent(c->cs_out, c->ev_fwd[k], 0));
+        UCK(c, cudaMemcpyAsync(out + b0 * hw, c->dout + b0 * hw, (size_t)nb * hw * sizeof(float),
+                               cudaMemcpyDeviceToHost, c->cs_out));
+    }
+    UCK(c, cudaStreamSynchronize(c->cs_out));
     UCK(c, cudaStreamSynchronize(c->st));
     return PF_OK;
 }
@@ -1768,7 +1813,14 @@ const char *un_last_error(const un_ctx *c) { return c ? c->err.c_str() : g_err.c
 void un_free(un_ctx *c) {
     if (!c) return;
     if (c->st) cudaStreamSynchronize(c->st);
-    if (c->gexec) cudaGraphExecDestroy(c->gexec);
+    for (auto &x : c->graphs)
+        if (x.exec) cudaGraphExecDestroy(x.exec);
+    for (int k = 0; k < un_ctx::kChunks; ++k) {
+        if (c->ev_in[k]) cudaEventDestroy(c->ev_in[k]);
+        if (c->ev_fwd[k]) cudaEventDestroy(c->ev_fwd[k]);
+    }
+    if (c->cs_in) cudaStreamDestroy(c->cs_in);
+    if (c->cs_out) cudaStreamDestroy(c->cs_out);
     for (int l = 0; l < kLayers; ++l) {
         cudaFree(c->w[l]);
         cudaFree(c->gam[l]);

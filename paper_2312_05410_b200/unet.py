@@ -109,13 +109,18 @@ class UNet:
         if not 1 <= np.shape(hist)[0] <= self.p.max_batch:
             raise ValueError(f"batch {np.shape(hist)[0]} outside [1, max_batch = {self.p.max_batch}]")
 
-    def forward(self, hist, dt):
-        """hist [B, lb, H, W], dt [B] or scalar (host) -> [B, H, W] float32 (host)."""
+    def forward(self, hist, dt, out=None):
+        """hist [B, lb, H, W], dt [B] or scalar (host) -> [B, H, W] float32 (host; written into `out`
+        when given, e.g. a page-locked array, which lets un_forward overlap its copies)."""
         self._check_hist(hist)
         if np.ndim(dt) not in (0, 1) or (np.ndim(dt) == 1 and np.shape(dt)[0] != np.shape(hist)[0]):
             raise ValueError(f"dt must be a scalar or have shape ({np.shape(hist)[0]},), got {np.shape(dt)}")
         h, d = _f32(hist), _f32(np.broadcast_to(dt, (hist.shape[0],)))
-        out = np.empty((h.shape[0], self.p.height, self.p.width), dtype=np.float32)
+        shape = (h.shape[0], self.p.height, self.p.width)
+        if out is None:
+            out = np.empty(shape, dtype=np.float32)
+        elif out.shape != shape or out.dtype != np.float32 or not out.flags["C_CONTIGUOUS"]:
+            raise ValueError(f"out must be a C-contiguous float32 array of shape {shape}")
         _check(lib().un_forward(self.ctx, h.shape[0], h.ctypes.data_as(_F), d.ctypes.data_as(_F),
                                 out.ctypes.data_as(_F)), self.ctx)
         return out

@@ -74,13 +74,18 @@ def main():
               (2 * c1, c1, 0), (c1, 1, 0)]
     conv_bytes = sum((HW >> lv) * (HW >> lv) * (2 * ci + 4 * co) for ci, co, lv in layers)
     achieved = conv_bytes * B / (conv_ms * 1e-3) / 1e9
-    # end to end: host buffers through un_forward (H2D of the histories, D2H of the predictions)
-    net.forward(hist, dts)
+    # end to end: page-locked host buffers through un_forward (H2D of the histories and dt, D2H of
+    # the predictions, pipelined over sample chunks inside the call)
+    hist_p = torch.from_numpy(hist).pin_memory().numpy()
+    dts_p = torch.from_numpy(dts).pin_memory().numpy()
+    out_p = torch.empty((B, HW, HW), dtype=torch.float32).pin_memory().numpy()
+    net.forward(hist_p, dts_p, out_p)
     t0 = time.perf_counter()
     n_e2e = max(3, a.iters // 4)
     for _ in range(n_e2e):
-        out = net.forward(hist, dts)
+        net.forward(hist_p, dts_p, out_p)
     e2e = B * n_e2e / (time.perf_counter() - t0)
+    out = out_p
     # sampled parity
     from oracle import unet_oracle as U
     P = synth.unpack(blob)
@@ -101,7 +106,10 @@ def main():
                      "bytes_per_sample": conv_bytes, "flops_per_sample": flops,
                      "tensor_tflops": tflops, "tensor_frac": tflops / peak_tf},
         "e2e": {"value": e2e, "unit": "samples/s", "h2d_bytes_per_step": hist.nbytes + dts.nbytes,
-                "d2h_bytes_per_step": B * HW * HW * 4},
+                "d2h_bytes_per_step": B * HW * HW * 4,
+                "note": "un_forward with page-locked host buffers (histories, dt, predictions); copies "
+                        "pipelined against the forward over 4 sample chunks inside the call; wall clock "
+                        "over the calls"},
         "gpu_launches": launches,
         "parity_rel_l2": errs,
         "clocks": clk.summary(),
