@@ -96,6 +96,29 @@ def test_forward_other_widths_and_lookback():
         assert _rel(got[b], U.forward(hist[b], dt, P)) <= 2e-2
 
 
+def test_host_forward_chunk_pipeline_equals_one_device_forward():
+    """un_forward pipelines batches of >= 16 over 4 sample chunks (copies overlapped, one graph per
+    chunk); the result equals one un_forward_device of the whole batch bitwise, also for a batch
+    that does not split evenly, and with page-locked buffers."""
+    import torch
+    for B in (18, 20):
+        net, _ = _net(32, 32, B, seed=23)
+        hist = synth.histories(B, 3, 32, 32, seed=9).astype(np.float32)
+        dts = (1.0 + np.arange(B) % 5).astype(np.float32)
+        with net:
+            host = net.forward(hist, dts)
+            pinned = torch.empty((B, 32, 32), dtype=torch.float32).pin_memory().numpy()
+            net.forward(torch.from_numpy(hist).pin_memory().numpy(), torch.from_numpy(dts).pin_memory().numpy(), pinned)
+            dh, dd = torch.from_numpy(hist).cuda(), torch.from_numpy(dts).cuda()
+            do = torch.empty((B, 32, 32), dtype=torch.float32, device="cuda")
+            torch.cuda.synchronize()   # the ctx stream does not order against torch's stream
+            net.forward_device(B, dh.data_ptr(), dd.data_ptr(), do.data_ptr())
+            torch.cuda.synchronize()
+            dev = do.cpu().numpy()
+        assert np.array_equal(host, dev), B
+        assert np.array_equal(pinned, dev), B
+
+
 def test_batch_members_are_independent_and_deterministic():
     net, _ = _net(32, 32, 4)
     hist = synth.histories(4, 3, 32, 32, seed=8)
