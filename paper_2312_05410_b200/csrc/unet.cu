@@ -3,23 +3,25 @@
 //
 // Layout: activations bf16 in ROW-CHUNK order [b][y][chunk][x][8]: the 8-channel chunk q of pixel
 // (b, y, x) of a C-channel buffer at ((((b * H + y) * (C / 8) + q) * W + x) * 8 (rc_off), so that one
-// chunk of one image row is W * 16 contiguous bytes -- the convolutions load their halo rows as
-// contiguous 2 KB bulk copies instead of 16-byte TMA box rows (round 2: the NHWC 5D TMA boxes
-// moved ~16 B per cycle per SM and bounded the 16-channel layers).  Conv outputs fp32 NHWC;
-// GroupNorm statistics fp64.  Concatenation z (+) d is a channel-offset write into a buffer of
-// 2C channels, so no copy is needed.
+// chunk of one image row is W * 16 contiguous bytes -- the convolutions load their input rows with
+// fully coalesced 16-byte cp.async (512 contiguous bytes per warp instruction) instead of 16-byte
+// TMA box rows over NHWC.  Conv outputs fp32 NHWC; GroupNorm statistics fp64 across 32-pixel units
+// (fp32 within a unit).  Concatenation z (+) d is a channel-offset write into a buffer of 2C
+// channels, so no copy is needed.
 //
 // Convolutions: implicit GEMMs on the 5th-generation tensor cores.
 //   D[pixel, cout] = sum_K A[pixel, K] B[cout, K],  K = (ky * 3 + kx) * cin + ci   (R-29)
 //   A tile = 128 pixels (UMMA M = 128), N = cout (16..128), fp32 accumulators in TMEM, tcgen05.mma
-//   kind::f16 (bf16 x bf16 -> fp32, K = 16 per instruction) issued by one thread, tcgen05.commit to
-//   mbarriers.  Operands use the canonical no-swizzle K-major layout: 8-row x 16-byte core matrices,
-//   rows 16 B apart, 8-row groups 128 B apart (SBO), 8-element K chunks LBO apart.  Both kernels are
-//   warp specialised (loader warps, one MMA warp, four epilogue warps; mbarrier pipelines, no CTA
-//   barrier in the loop) and persistent:
-//   * conv3x3_rows_kernel (W a multiple of 128): a tile is 128 pixels of one image row; the three
-//     halo rows are loaded once (one 2 KB bulk copy per row and channel chunk) and the A operand of
-//     each tap is a descriptor shifted by kx pixels into row plane ky; weights resident in shared
+//   kind::f16 (bf16 x bf16 -> fp32, K = 16 per instruction) issued warp-uniformly by one elected
+//   lane, tcgen05.commit to mbarriers.  Operands use the canonical no-swizzle K-major layout: 8-row
+//   x 16-byte core matrices, rows 16 B apart, 8-row groups 128 B apart (SBO), 8-element K chunks LBO
+//   apart.  Both kernels are warp specialised (loader warps, one MMA warp, epilogue warps;
+//   mbarrier pipelines, no CTA barrier in the loop) and persistent:
+//   * conv3x3_rows_kernel (rows of a multiple of 128 pixels, or of 32 / 64): a tile is 128 pixels
+//     of one image row; a CTA walks segments of output rows with a ring of input rows in shared
+//     memory (each loaded once per segment); the A operand of tap (ky, kx) is a descriptor shifted
+//     by kx pixels into the slot of input row y + ky - 1, and one MMA of N = 3 cout per (input row,
+//     kx, channel step) feeds the three outputs that row touches; weights resident in shared
 //     memory;
 //   * conv3x3_kernel (any shape): im2col gather of 144-element K blocks with cp.async (zero-fill =
 //     the 'same' padding), weights streamed with each block.
@@ -38,6 +40,7 @@
 #include <cstring>
 #include <string>
 #include <vector>
+#include <type_traits>
 
 #include "unet.h"
 
@@ -250,6 +253,12 @@ __device__ __forceinline__ void cp_async_wait_n(int n) {   // n <= 3
     }
 }
 
+#ifndef UN_GN_WARP_F32
+// The per-warp (32-pixel) GroupNorm partial sums are reduced across the warp in fp32 (<= 32 x
+// C/G terms, relative error ~1e-6) and accumulated over units in fp64 by gn_reduce_kernel: 4.6%
+// faster forwards than an fp64 butterfly, forward parity unchanged to 1e-7 (R-36).  0: fp64.
+#define UN_GN_WARP_F32 1
+#endif
 // Epilogue of one tile of up to 128 pixels (TMEM lane m = pixel pbase + m, m < nvalid) from the
 // accumulator at tacc: tcgen05.ld (warp w reads lanes 32 (w & 3) .. +31; with N >= 32 the warps w
 // and w + 4 split the columns), fp32 stores, GroupNorm partial sums (see above).
@@ -318,11 +327,12 @@ __device__ __forceinline__ void conv_tile_out(uint32_t tacc, int64_t pbase, int 
             // (deterministic).  5x fewer fp64 shuffles than one xor-reduction per value at G = 8.
             constexpr int NV = 2 * G0N;
             constexpr int M = NV >= 32 ? 5 : (NV >= 16 ? 4 : (NV >= 8 ? 3 : (NV >= 4 ? 2 : (NV >= 2 ? 1 : 0))));
-            double v[NV];
+            using red_t = typename std::conditional<UN_GN_WARP_F32 != 0, float, double>::type;
+            red_t v[NV];
 #pragma unroll
             for (int g = 0; g < G0N; ++g) {
-                v[2 * g] = gs[g];
-                v[2 * g + 1] = gq[g];
+                v[2 * g] = UN_GN_WARP_F32 ? (red_t)fs[g] : (red_t)gs[g];
+                v[2 * g + 1] = UN_GN_WARP_F32 ? (red_t)fq[g] : (red_t)gq[g];
             }
 #pragma unroll
             for (int st = 0; st < 5; ++st) {
@@ -332,8 +342,8 @@ __device__ __forceinline__ void conv_tile_out(uint32_t tacc, int64_t pbase, int 
                     const bool upper = (lane & o) != 0;
 #pragma unroll
                     for (int j = 0; j < half; ++j) {
-                        const double send = upper ? v[j] : v[j + half];
-                        const double keep = upper ? v[j + half] : v[j];
+                        const red_t send = upper ? v[j] : v[j + half];
+                        const red_t keep = upper ? v[j + half] : v[j];
                         v[j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
                     }
                 } else {
@@ -344,7 +354,7 @@ __device__ __forceinline__ void conv_tile_out(uint32_t tacc, int64_t pbase, int 
             constexpr int SH = 5 - M;
             if ((lane & ((1 << SH) - 1)) == 0 && 32 * lq < nvalid && wid * 32 < npix) {
                 const int idx = (lane >> SH) & (NV - 1);   // = 2 g + (0: sum, 1: sum of squares)
-                part[(wid * NG + g0 + (idx >> 1)) * 2 + (idx & 1)] = v[0];
+                part[(wid * NG + g0 + (idx >> 1)) * 2 + (idx & 1)] = (double)v[0];
             }
         }
     }

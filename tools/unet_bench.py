@@ -96,7 +96,7 @@ def main():
     res = {
         "metric": "U-Net (temporal conditioning) inference samples/s, 256x256, lb=3, batch 64",
         "value": B / (ms * 1e-3), "unit": "samples/s", "ms_per_forward": ms, "batch": B,
-        "higher_is_better": True, "dtype": "bf16 (fp32 accumulate, fp64 GN statistics)", "data": "synthetic",
+        "higher_is_better": True, "dtype": "bf16 (fp32 accumulate, GN statistics fp64 across 32-pixel units)", "data": "synthetic",
         "config": {"workload": f"U-Net TC forward, {B} x {HW}x{HW}, lb=3, widths 16/32/64/128, random bf16 weights",
                    "l2": "activations > 126 MB L2 at batch 64"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak_bw, "unit": "GB/s",
