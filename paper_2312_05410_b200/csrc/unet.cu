@@ -585,7 +585,7 @@ template <int N, bool HEAD, int CQ>
 __global__ void __launch_bounds__(kRowThreads, row_min_blocks<N, CQ>()) conv3x3_rows_kernel(const bf16 *__restrict__ in,
                                                                    const bf16 *__restrict__ w, float *__restrict__ out,
                                                                    double *__restrict__ part, int64_t npix, int H,
-                                                                   int W, int S, int R, int gran) {
+                                                                   int W, int S, int R, int gran, int creal) {
     using C = RowCfg<N>;
     if (threadIdx.x == 32 * kRowMmaWarp) UN_SPAN(0);
     constexpr int NB = C::nbuf;
@@ -671,7 +671,8 @@ __global__ void __launch_bounds__(kRowThreads, row_min_blocks<N, CQ>()) conv3x3_
                     if (job < CQ * kRowPix) {
                         const int c = job / kRowPix, px = job - c * kRowPix;
                         const int xx = g.x0 - 1 + px;
-                        const bool v = rv && xx >= 0 && xx < W;
+                        // chunks >= creal are known zeros (the padded input channels): zero-filled, not read
+                        const bool v = rv && xx >= 0 && xx < W && c < creal;
                         cp_async16(d + (uint32_t)c * kRowLbo + (uint32_t)px * 16u, v ? rowp + ((int64_t)c * W + xx) * 8 : in, v);
                     }
                 }
@@ -803,7 +804,7 @@ __global__ void __launch_bounds__(kRowThreads, row_min_blocks<N, CQ>()) conv3x3_
 
 template <int N, bool HEAD, int CQ>
 cudaError_t launch_conv_rows_c(const bf16 *in, const bf16 *w, float *out, double *part, int64_t npix, int H, int W,
-                               int cin, cudaStream_t st) {
+                               int cin, int creal, cudaStream_t st) {
     (void)cin;
     const size_t rreg = row_region(CQ), b_bytes = 9 * (size_t)CQ * RowCfg<N>::lbo_b;
     const size_t fixed = 1024 + b_bytes + 512;
@@ -868,45 +869,48 @@ cudaError_t launch_conv_rows_c(const bf16 *in, const bf16 *w, float *out, double
                 N, CQ, H, W, S, R, occ, grid, smem, fa.numRegs, fa.sharedSizeBytes, fa.localSizeBytes,
                 fa.maxDynamicSharedSizeBytes, occ_api);
     }
-    conv3x3_rows_kernel<N, HEAD, CQ><<<grid, kRowThreads, smem, st>>>(in, w, out, part, npix, H, W, S, R, gran);
+    conv3x3_rows_kernel<N, HEAD, CQ><<<grid, kRowThreads, smem, st>>>(in, w, out, part, npix, H, W, S, R, gran,
+                                                                      creal > 0 && creal < CQ ? creal : CQ);
     return cudaGetLastError();
 }
 
 template <int N, bool HEAD>
 cudaError_t launch_conv_rows(const bf16 *in, const bf16 *w, float *out, double *part, int64_t npix, int H, int W,
-                             int cin, cudaStream_t st) {
+                             int cin, int creal, cudaStream_t st) {
     switch (cin / 8) {   // cin a multiple of 16
-        case 2: return launch_conv_rows_c<N, HEAD, 2>(in, w, out, part, npix, H, W, cin, st);
-        case 4: return launch_conv_rows_c<N, HEAD, 4>(in, w, out, part, npix, H, W, cin, st);
-        case 6: return launch_conv_rows_c<N, HEAD, 6>(in, w, out, part, npix, H, W, cin, st);
-        case 8: return launch_conv_rows_c<N, HEAD, 8>(in, w, out, part, npix, H, W, cin, st);
-        case 16: return launch_conv_rows_c<N, HEAD, 16>(in, w, out, part, npix, H, W, cin, st);
+        case 2: return launch_conv_rows_c<N, HEAD, 2>(in, w, out, part, npix, H, W, cin, creal, st);
+        case 4: return launch_conv_rows_c<N, HEAD, 4>(in, w, out, part, npix, H, W, cin, creal, st);
+        case 6: return launch_conv_rows_c<N, HEAD, 6>(in, w, out, part, npix, H, W, cin, creal, st);
+        case 8: return launch_conv_rows_c<N, HEAD, 8>(in, w, out, part, npix, H, W, cin, creal, st);
+        case 16: return launch_conv_rows_c<N, HEAD, 16>(in, w, out, part, npix, H, W, cin, creal, st);
         default: return cudaErrorNotSupported;
     }
 }
 
 template <int N, bool HEAD>
 cudaError_t launch_conv_any(const bf16 *in, const bf16 *w, float *out, double *part, int64_t npix, int H, int W,
-                            int cin, cudaStream_t st) {
+                            int cin, int creal, cudaStream_t st) {
     // the row kernel for rows of a multiple of 128 pixels or of 32 / 64 / 96 pixels (one row per
     // 128-lane tile, the rest of the tile idle) when its weights and a 4-row ring fit in shared
     // memory; else the im2col gather kernel
     static const int norows = getenv("UN_NO_ROWS") ? atoi(getenv("UN_NO_ROWS")) : 0;
     if (!norows && (W % kBM == 0 || (W < kBM && W % 32 == 0))) {
-        const cudaError_t e = launch_conv_rows<N, HEAD>(in, w, out, part, npix, H, W, cin, st);
+        const cudaError_t e = launch_conv_rows<N, HEAD>(in, w, out, part, npix, H, W, cin, creal, st);
         if (e != cudaErrorNotSupported) return e;
     }
     return launch_conv_n<N, HEAD>(in, w, out, part, npix, H, W, cin, st);
 }
 
+// creal: the input's leading channel chunks that can be non-zero (0: all); the row kernel
+// zero-fills the rest without reading them (the gather kernel reads them: they must be zero)
 cudaError_t launch_conv(const bf16 *in, const bf16 *w, float *out, double *part, int64_t npix, int H, int W, int cin,
-                        int cout, bool head, cudaStream_t st) {
-    if (head) return cout == 16 ? launch_conv_any<16, true>(in, w, out, part, npix, H, W, cin, st) : cudaErrorInvalidValue;
+                        int cout, bool head, cudaStream_t st, int creal = 0) {
+    if (head) return cout == 16 ? launch_conv_any<16, true>(in, w, out, part, npix, H, W, cin, creal, st) : cudaErrorInvalidValue;
     switch (cout) {
-        case 16: return launch_conv_any<16, false>(in, w, out, part, npix, H, W, cin, st);
-        case 32: return launch_conv_any<32, false>(in, w, out, part, npix, H, W, cin, st);
-        case 64: return launch_conv_any<64, false>(in, w, out, part, npix, H, W, cin, st);
-        case 128: return launch_conv_any<128, false>(in, w, out, part, npix, H, W, cin, st);
+        case 16: return launch_conv_any<16, false>(in, w, out, part, npix, H, W, cin, creal, st);
+        case 32: return launch_conv_any<32, false>(in, w, out, part, npix, H, W, cin, creal, st);
+        case 64: return launch_conv_any<64, false>(in, w, out, part, npix, H, W, cin, creal, st);
+        case 128: return launch_conv_any<128, false>(in, w, out, part, npix, H, W, cin, creal, st);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -924,7 +928,8 @@ __global__ void pack_input_kernel(const float *__restrict__ hist, bf16 *__restri
 #pragma unroll
         for (int c = 0; c < 16; ++c) v[c] = __float2bfloat16_rn(c < lb ? hist[(b * lb + c) * HW + q] : 0.0f);
         *reinterpret_cast<uint4 *>(dst + rc_off(row, x, W, 2, 0)) = reinterpret_cast<uint4 *>(v)[0];
-        *reinterpret_cast<uint4 *>(dst + rc_off(row, x, W, 2, 1)) = reinterpret_cast<uint4 *>(v)[1];
+        // channels 8 .. 15 are zero for lb <= 8: that chunk plane stays as zeroed at un_create
+        if (lb > 8) *reinterpret_cast<uint4 *>(dst + rc_off(row, x, W, 2, 1)) = reinterpret_cast<uint4 *>(v)[1];
     }
 }
 
@@ -1263,7 +1268,8 @@ pf_status conv_layer(un_ctx *c, int l, const bf16 *in, int B) {
         UCK(c, cudaEventRecord(e0, c->st));
     }
     const bool head = l == kHead2;
-    UCK(c, launch_conv(in, c->w[l], c->raw, c->part, npix, H, W, c->cin_pad[l], c->cout_pad[l], head, c->st));
+    const int creal = l == kEnc1 ? (c->p.lb + 7) / 8 : 0;   // enc1: the lb history channels, padded to 16
+    UCK(c, launch_conv(in, c->w[l], c->raw, c->part, npix, H, W, c->cin_pad[l], c->cout_pad[l], head, c->st, creal));
     if (c->prof) {
         UCK(c, cudaEventRecord(e1, c->st));
         c->rec.push_back({0, {e0, e1}});
@@ -1461,6 +1467,7 @@ pf_status un_create(const un_params *p, un_ctx **out) {
     if (s == PF_OK) s = dalloc(c, &c->wl, (size_t)c->ctot * kBasis);
     if (s == PF_OK) s = dalloc(c, &c->upw, 12);
     if (s == PF_OK) s = dalloc(c, &c->in0, (size_t)(B * hw(0) * 16));
+    if (s == PF_OK) cudaMemset(c->in0, 0, (size_t)(B * hw(0) * 16) * sizeof(bf16));   // chunk 1 stays zero for lb <= 8
     const int Cl[4] = {c1, c2, c3, c4};
     for (int q = 0; q < 3 && s == PF_OK; ++q) {
         s = dalloc(c, &c->pin[q], (size_t)(B * hw(q + 1) * Cl[q]));
