@@ -262,7 +262,7 @@ def _slab_leg(args, ws, rank, local, dist, dev):
     from paper_2312_05410_b200 import dist as D
     from paper_2312_05410_b200 import pf
     p = pf.pf_default_params(4).replace(device=local)
-    p = p.replace(ny=p.ny * ws)
+    p = p.replace(ny=p.ny * ws, halo_transport=1 if args.slab_transport == "peer" else 0)
     mode = ("slab", rank, ws, D.nccl_uid(dist, dev)) if ws > 1 else "single"
     with pf.Simulation(p, mode) as sim:
         stream = torch.cuda.ExternalStream(pf.pf_stream(sim.ctx), device=dev)
@@ -283,8 +283,11 @@ def _slab_leg(args, ws, rank, local, dist, dev):
         return None
     value = cells_local * ws * args.steps / (ms * 1e-3)
     return {"workload": f"configs[3] weak: {p.nx} x {p.ny} fp64 in {ws} y-slab(s) of {cells_local // p.nx} rows, "
-                        + ("2-row halo per stage over NCCL (ncclSend/Recv on a comm stream) overlapped with the "
-                           "interior update" if ws > 1 else "single domain (no exchange at N = 1)"),
+                        + (("2-row halo per stage over NCCL (ncclSend/Recv on a comm stream)"
+                            if args.slab_transport == "nccl" else
+                            "2-row halo per stage as peer stores into the neighbours' ghost rows (B11: CUDA-IPC "
+                            "mappings, push kernel + arrival counters)") + " overlapped with the interior update"
+                           if ws > 1 else "single domain (no exchange at N = 1)"),
             "value": value, "unit": UNIT, "per_gpu": value / ws, "ms_per_step": ms / args.steps,
             "ms_per_step_1gpu": ms1 / args.steps, "weak_efficiency": ms1 / ms, "steps": args.steps,
             "halo_bytes_per_stage_per_neighbour": 2 * 3 * (p.nx + 8) * 8 if ws > 1 else 0}
@@ -466,6 +469,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-slab", action="store_true", help="skip the configs[3] y-slab leg of the default run")
+    ap.add_argument("--slab-transport", choices=["nccl", "peer"], default="nccl",
+                    help="halo transport of the slab leg at N > 1: NCCL send/recv (default) or the B11 peer stores")
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")

@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define PF_ABI_VERSION 6u
+#define PF_ABI_VERSION 7u
 
 typedef struct pf_ctx pf_ctx; /* opaque */
 
@@ -108,6 +108,18 @@ typedef struct {
     int32_t overlap_halo;            /* slab modes: 1 = update the 2-row boundary bands first and
                                         overlap the halo exchange with the interior update
                                         (needs >= 8 rows per slab), 0 = exchange after the stage */
+    int32_t halo_transport;          /* slab modes, how the 2 boundary rows reach the neighbours
+                                        after every stage:
+                                        0 = NCCL send/recv (pf_create_slab) or device-to-device
+                                            copies (pf_create_loopback);
+                                        1 = peer stores: one kernel per slab and stage writes the
+                                            rows straight into the neighbours' ghost rows (CUDA-IPC
+                                            mappings over NVLink in pf_create_slab, exchanged once
+                                            over the NCCL communicator at create; device pointers in
+                                            loopback) and increments an arrival counter in the
+                                            receiver's memory, which the receiver's stream awaits
+                                            with cuStreamWaitValue32.  Results are bitwise those of
+                                            transport 0.  Disables CUDA graphs for the ctx.       */
 } pf_params;
 
 /* Fill *out with the preset of BASELINE.json configs[cfg-1] (cfg = 1..5; R-13, R-14).

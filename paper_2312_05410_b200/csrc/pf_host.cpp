@@ -242,6 +242,12 @@ struct Slab {
     double *partials = nullptr;
     double *diag = nullptr;   // members * kDiag
     pf::StreamPlan plan;      // streaming-kernel geometry and TMA tensor maps (plan.ok: in use)
+    // halo_transport = 1 (B11, pf_halo.cu): the neighbours' buffers ([0] below, [1] above; IPC
+    // mappings in the multi-process slab mode), their arrival counters this slab bumps, and this
+    // slab's own counters ([0] arrivals from below, [1] from above)
+    void *nbU[2] = {nullptr, nullptr}, *nbUs[2] = {nullptr, nullptr};
+    unsigned *nbflag[2] = {nullptr, nullptr};
+    unsigned *myflag = nullptr;
 };
 
 enum Mode { kSingle = 0, kLoopback = 1, kNccl = 2 };
@@ -274,6 +280,13 @@ struct pf_ctx {
     bool band = false;                    // small-grid band kernel (kernel_path 6 / auto, pf_band.cu)
     pf::BandPlan bplan;
     ncclComm_t comm = nullptr;
+    // halo_transport = 1 (B11): arrival counters (2 per slab), exchanges issued so far, blocks per
+    // push (= counter increments per exchange and direction), IPC mappings to close
+    bool peer = false;
+    unsigned *xflags = nullptr;
+    uint32_t xepoch = 0;
+    int xblocks = 0;
+    std::vector<void *> ipc_open;
     void *vel = nullptr;   // [members][2] in the storage precision
     double *h_diag = nullptr;
     double *staging = nullptr;
@@ -346,6 +359,7 @@ pf_status validate(const pf_params *p, std::string &why) {
     if (!(p->noise_rho >= 0) || !std::isfinite(p->noise_rho)) { why = "noise_rho must be finite and >= 0"; return PF_ERR_ARG; }
     if (!(p->mob_lo > 0) || !(p->mob_hi >= p->mob_lo)) { why = "need 0 < mob_lo <= mob_hi"; return PF_ERR_ARG; }
     if (p->overlap_halo != 0 && p->overlap_halo != 1) { why = "overlap_halo must be 0 or 1"; return PF_ERR_ARG; }
+    if (p->halo_transport != 0 && p->halo_transport != 1) { why = "halo_transport must be 0 or 1"; return PF_ERR_ARG; }
     if (p->kernel_path < 0 || p->kernel_path > 7) { why = "kernel_path must be 0 .. 7"; return PF_ERR_ARG; }
     if (p->kernel_path == 2 || p->kernel_path == 4) { why = "kernel_path 2 and 4 (retired) are not available"; return PF_ERR_ARG; }
     if ((p->kernel_path == 3 || p->kernel_path == 5) && !(p->nx % 4 == 0 && p->nx >= 16)) { why = "streaming kernels need nx % 4 == 0 and nx >= 16"; return PF_ERR_ARG; }
@@ -380,6 +394,8 @@ void destroy(pf_ctx *c) {
         cudaEventDestroy(r.second.first);
         cudaEventDestroy(r.second.second);
     }
+    for (void *q : c->ipc_open) cudaIpcCloseMemHandle(q);
+    cudaFree(c->xflags);
     if (c->comm) ncclCommDestroy(c->comm);
     if (c->ev_band) cudaEventDestroy(c->ev_band);
     if (c->ev_xchg) cudaEventDestroy(c->ev_xchg);
@@ -421,6 +437,24 @@ pf_status exchange(pf_ctx *c, int which, cudaStream_t st) {
     Nvtx nv("pf halo exchange");
     if (c->mode == kSingle) return PF_OK;
     const size_t rowb = (size_t)c->slabs[0].L.pitch * c->esz;   // full padded rows (ghost columns too)
+    if (c->peer) {   // B11: one push kernel per slab (pf_halo.cu); finish_exchange awaits the arrivals
+        for (auto &s : c->slabs) {
+            pf::HaloPush h{};
+            h.src = (const char *)buf_of(s, which);
+            for (int d = 0; d < 2; ++d) {
+                h.dst[d] = (char *)(which == 0 ? s.nbU[d] : s.nbUs[d]);
+                h.flag[d] = s.nbflag[d];
+            }
+            h.rowb = (int64_t)rowb;
+            h.fstride_b = s.L.fstride * (int64_t)c->esz;
+            h.rows = s.L.ny_loc;
+            h.nchunks = 3 * s.L.members;
+            CK(c, pf::launch_halo_push(h, st));
+            if (h.dst[0] || h.dst[1]) c->launches += 1;
+        }
+        ++c->xepoch;
+        return PF_OK;
+    }
     if (c->mode == kLoopback) {
         const int P = (int)c->slabs.size();
         for (int s = 0; s < P; ++s) {
@@ -465,6 +499,35 @@ pf_status exchange(pf_ctx *c, int which, cudaStream_t st) {
             }
         }
     NK(c, ncclGroupEnd());
+    return PF_OK;
+}
+
+// B11: `st` waits until every neighbour's push of the latest exchange has arrived (the arrival
+// counters reach xepoch * xblocks; cyclic GEQ compare, so the 32-bit counters may wrap).
+using WaitValueFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+WaitValueFn wait_value_fn() {
+    static WaitValueFn fn = nullptr;
+    if (!fn) {
+        void *q = nullptr;
+        cudaDriverEntryPointQueryResult r;
+        if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &q, cudaEnableDefault, &r) == cudaSuccess &&
+            r == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<WaitValueFn>(q);
+    }
+    return fn;
+}
+
+pf_status finish_exchange(pf_ctx *c, cudaStream_t st) {
+    if (!c->peer) return PF_OK;
+    WaitValueFn wv = wait_value_fn();
+    if (!wv) return set_err(c, PF_ERR_CUDA, "cuStreamWaitValue32 is not available");
+    const uint32_t want = c->xepoch * (uint32_t)c->xblocks;
+    for (auto &s : c->slabs)
+        for (int d = 0; d < 2; ++d)
+            if (s.nbU[d]) {
+                CUresult r = wv((CUstream)st, (CUdeviceptr)(s.myflag + d), want, CU_STREAM_WAIT_VALUE_GEQ);
+                if (r != CUDA_SUCCESS) return set_err(c, PF_ERR_CUDA, fmt("cuStreamWaitValue32 failed (%d)", (int)r));
+            }
     return PF_OK;
 }
 
@@ -538,6 +601,7 @@ pf_status one_step(pf_ctx *c, bool capture, int64_t step) {
                 if ((st = launch_rows(c, s, stage, 0, s.L.ny_loc, capture)) != PF_OK) return st;
             if (prof) CK(c, cudaEventRecord(e1, c->stream));
             if ((st = exchange(c, which, c->stream)) != PF_OK) return st;
+            if ((st = finish_exchange(c, c->stream)) != PF_OK) return st;
         } else {
             for (auto &s : c->slabs) {
                 if ((st = launch_rows(c, s, stage, 0, 2, capture)) != PF_OK) return st;
@@ -551,6 +615,7 @@ pf_status one_step(pf_ctx *c, bool capture, int64_t step) {
                 if ((st = launch_rows(c, s, stage, 2, s.L.ny_loc - 2, capture)) != PF_OK) return st;
             if (prof) CK(c, cudaEventRecord(e1, c->stream));
             CK(c, cudaStreamWaitEvent(c->stream, c->ev_xchg, 0));
+            if ((st = finish_exchange(c, c->stream)) != PF_OK) return st;
         }
         if (prof) c->ev_rec.push_back({stage, {e0, e1}});
     }
@@ -558,7 +623,7 @@ pf_status one_step(pf_ctx *c, bool capture, int64_t step) {
 }
 
 pf_status ensure_graph(pf_ctx *c) {
-    if (c->gexec || c->p.graph_steps <= 0 || c->mode == kNccl) return PF_OK;
+    if (c->gexec || c->p.graph_steps <= 0 || c->mode == kNccl || c->peer) return PF_OK;
     cudaGraph_t g = nullptr;
     CK(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
     pf_status st = PF_OK;
@@ -645,6 +710,106 @@ pf_status check_blowup(pf_ctx *c, int64_t from, int64_t to) {
                        fmt("blow-up: non-finite %s in steps (%lld, %lld], first member %d", fields.c_str(),
                            (long long)from, (long long)to, worst + c->p.member_offset));
     }
+    return PF_OK;
+}
+
+// B11 (halo_transport = 1): arrival counters, and the neighbours' buffers and counters -- device
+// pointers of the other slabs in loopback, CUDA-IPC mappings of the neighbouring ranks' allocations
+// (handles all-gathered over the NCCL communicator) in the multi-process slab mode.  Called after
+// the initial fields and ghost frames are complete: the all-gather is also the barrier that keeps
+// a neighbour's first push behind this rank's fill_ghosts.
+pf_status setup_peer(pf_ctx *c) {
+    const int nsl = (int)c->slabs.size();
+    const size_t nflag = 2 * (size_t)nsl + 2;   // 2 per slab + the barrier word of peer_barrier
+    CK(c, cudaMalloc((void **)&c->xflags, nflag * sizeof(unsigned)));
+    CK(c, cudaMemsetAsync(c->xflags, 0, nflag * sizeof(unsigned), c->stream));
+    c->xblocks = pf::halo_push_blocks(c->p.n_members, (int64_t)c->slabs[0].L.pitch * (int64_t)c->esz);
+    for (int s = 0; s < nsl; ++s) c->slabs[s].myflag = c->xflags + 2 * s;
+    if (c->mode == kLoopback) {
+        for (int s = 0; s < nsl; ++s) {
+            Slab &S = c->slabs[s];
+            if (s > 0) {
+                S.nbU[0] = c->slabs[s - 1].U;
+                S.nbUs[0] = c->slabs[s - 1].Us;
+                S.nbflag[0] = c->slabs[s - 1].myflag + 1;
+            }
+            if (s < nsl - 1) {
+                S.nbU[1] = c->slabs[s + 1].U;
+                S.nbUs[1] = c->slabs[s + 1].Us;
+                S.nbflag[1] = c->slabs[s + 1].myflag + 0;
+            }
+        }
+        return PF_OK;
+    }
+    // Every rank takes part in both collectives below even when one of its own steps failed, and
+    // the all-reduce of the ok bits makes the ranks agree: a rank whose mapping failed must not
+    // leave its neighbours waiting forever for pushes that never come.
+    struct Rec {
+        cudaIpcMemHandle_t h[3];   // U allocation, Us allocation, counters
+        int32_t ok;
+        int32_t pad[15];
+    };
+    Slab &S = c->slabs[0];
+    Rec mine{};
+    std::string why;
+    mine.ok = cudaIpcGetMemHandle(&mine.h[0], S.alloc[0]) == cudaSuccess &&
+              cudaIpcGetMemHandle(&mine.h[1], S.alloc[1]) == cudaSuccess &&
+              cudaIpcGetMemHandle(&mine.h[2], c->xflags) == cudaSuccess;
+    if (!mine.ok) why = fmt("cudaIpcGetMemHandle: %s", cudaGetErrorString(cudaGetLastError()));
+    const int P = c->nranks;
+    std::vector<Rec> all(P);
+    Rec *d = nullptr;
+    int32_t *okw = nullptr;
+    CK(c, cudaMalloc((void **)&d, (size_t)(P + 1) * sizeof(Rec)));
+    CK(c, cudaMalloc((void **)&okw, sizeof(int32_t)));
+    auto collective = [&](ncclResult_t r) {
+        if (r != ncclSuccess) why = fmt("NCCL (peer setup): %s", ncclGetErrorString(r));
+        return r == ncclSuccess;
+    };
+    bool good = cudaMemcpyAsync(d + P, &mine, sizeof(Rec), cudaMemcpyHostToDevice, c->stream) == cudaSuccess &&
+                collective(ncclAllGather(d + P, d, sizeof(Rec), ncclUint8, c->comm, c->stream)) &&
+                cudaMemcpyAsync(all.data(), d, (size_t)P * sizeof(Rec), cudaMemcpyDeviceToHost, c->stream) ==
+                    cudaSuccess &&
+                cudaStreamSynchronize(c->stream) == cudaSuccess;
+    for (int dd = 0; good && dd < 2; ++dd) {
+        const int nb = dd == 0 ? c->rank - 1 : c->rank + 1;
+        if (nb < 0 || nb >= P || !all[nb].ok) continue;
+        void *q[3] = {nullptr, nullptr, nullptr};
+        for (int k = 0; k < 3 && good; ++k) {
+            cudaError_t e = cudaIpcOpenMemHandle(&q[k], all[nb].h[k], cudaIpcMemLazyEnablePeerAccess);
+            if (e != cudaSuccess) {
+                why = fmt("cudaIpcOpenMemHandle (rank %d): %s", nb, cudaGetErrorString(e));
+                good = false;
+            } else {
+                c->ipc_open.push_back(q[k]);
+            }
+        }
+        if (!good) break;
+        S.nbU[dd] = (char *)q[0] + kGuardBytes;
+        S.nbUs[dd] = (char *)q[1] + kGuardBytes;
+        S.nbflag[dd] = (unsigned *)q[2] + (dd == 0 ? 1 : 0);
+    }
+    int32_t ok = good && mine.ok ? 1 : 0, all_ok = 0;
+    bool agreed = cudaMemcpyAsync(okw, &ok, sizeof ok, cudaMemcpyHostToDevice, c->stream) == cudaSuccess &&
+                  collective(ncclAllReduce(okw, okw, 1, ncclInt32, ncclMin, c->comm, c->stream)) &&
+                  cudaMemcpyAsync(&all_ok, okw, sizeof all_ok, cudaMemcpyDeviceToHost, c->stream) == cudaSuccess &&
+                  cudaStreamSynchronize(c->stream) == cudaSuccess;
+    cudaFree(d);
+    cudaFree(okw);
+    if (!agreed || !all_ok) {
+        cudaGetLastError();
+        return set_err(c, PF_ERR_CUDA, "peer halo transport setup failed" +
+                                           (why.empty() ? std::string(" on another rank") : ": " + why));
+    }
+    return PF_OK;
+}
+
+// Multi-process peer transport: a device-side barrier on c->stream (a one-word all-reduce) that
+// keeps the next push behind every rank's host writes and fill_ghosts (pf_set_fields).
+pf_status peer_barrier(pf_ctx *c) {
+    if (!c->peer || c->mode != kNccl) return PF_OK;
+    unsigned *w = c->xflags + 2 * c->slabs.size();
+    NK(c, ncclAllReduce(w, w, 1, ncclUint32, ncclSum, c->comm, c->stream));
     return PF_OK;
 }
 
@@ -847,7 +1012,10 @@ pf_status create_common(const pf_params *p, int mode, int rank, int nranks, cons
         }
         c->launches += 2 * pf::kFillLaunches;
     }
+    c->peer = mode != kSingle && p->halo_transport == 1;
+    if (c->peer && (st = setup_peer(c)) != PF_OK) return fail(st);
     st = exchange(c, 0, c->stream);
+    if (st == PF_OK) st = finish_exchange(c, c->stream);
     if (st != PF_OK) return fail(st);
     e = cudaStreamSynchronize(c->stream);
     if (e != cudaSuccess) {
@@ -1038,7 +1206,8 @@ pf_status pf_step(pf_ctx *c, int64_t n) {
         if (chunk > left) chunk = left;
         int64_t done = 0;
         const bool use_graph = c->p.graph_steps > 0 && !c->prof && c->mode != kNccl && !(c->p.noise_rho > 0.0) &&
-                               !c->fused && !c->persistent && !c->band;   // fused swaps buffers on the host each step
+                               !c->fused && !c->persistent && !c->band &&
+                               !c->peer;   // fused swaps buffers on the host each step; peer waits on epochs
         if (c->band && !c->prof && chunk > 0) {
             Nvtx nv("pf band kernel (small grid)");
             Slab &S = c->slabs[0];
@@ -1492,7 +1661,9 @@ pf_status pf_set_fields(pf_ctx *c, int32_t member, const double *fc, const doubl
         CK(c, pf::launch_fill_ghosts(c->p.precision, S.L, c->p.rho_in, S.U, c->stream));
         c->launches += pf::kFillLaunches;
     }
+    if ((st = peer_barrier(c)) != PF_OK) return st;
     st = exchange(c, 0, c->stream);
+    if (st == PF_OK) st = finish_exchange(c, c->stream);
     if (st != PF_OK) return st;
     CK(c, cudaStreamSynchronize(c->stream));
     c->blown = false;

@@ -144,6 +144,21 @@ cudaError_t launch_pack_f64(int precision, const Layout &L, int field, int membe
                             const void *state, double *dst, cudaStream_t s);
 cudaError_t launch_unpack_f64(int precision, const Layout &L, int field, int member0, int nmem,
                               const double *src, void *state, cudaStream_t s);
+// B11 halo push (pf_halo.cu; halo_transport = 1): the two boundary rows of every (member, field)
+// of `src` stored straight into the neighbours' ghost rows, then one system-scope increment of
+// the receiver's arrival counter per block and direction (halo_push_blocks(...) per exchange).
+struct HaloPush {
+    const char *src;      // this slab's state buffer written by the stage
+    char *dst[2];         // [0] the slab below's same buffer, [1] the slab above's (nullptr: none)
+    unsigned *flag[2];    // [0] the slab below's "from above" counter, [1] the slab above's "from below"
+    int64_t rowb;         // bytes per storage row (pitch * element size)
+    int64_t fstride_b;    // bytes per field (members are 3 fields apart)
+    int rows;             // owned rows per slab (the same on every slab)
+    int nchunks;          // members * 3
+};
+int halo_push_blocks(int members, int64_t rowb);
+cudaError_t launch_halo_push(const HaloPush &h, cudaStream_t s);
+
 // Number of kernel launches made by one launch_stage / launch_diag call.
 constexpr int kStageLaunches = 1;
 constexpr int kDiagLaunches = 2;

@@ -1311,7 +1311,13 @@ cudaError_t launch_pair_k(const Layout &L, const StreamPlan &P, const KC<real> &
         B = G * P.strips;
     } else {
         G = 0;
-        if (B > (R_ + minrows - 1) / minrows) B = (R_ + minrows - 1) / minrows;
+        // >= 16 rows per block, but never fewer blocks than (member, strip) windows: a 2-row
+        // boundary band of the slab overlap schedule (4096 wide: 18 strips) otherwise ran on 3
+        // blocks, 6 strips each back to back (~28 us per band launch, gpurun_out r2s3b)
+        int64_t cap = (R_ + minrows - 1) / minrows;
+        const int64_t windows = (int64_t)L.members * P.strips;
+        if (cap < windows) cap = windows;
+        if (B > cap) B = cap;
     }
     if (B < 1) B = 1;
     const int NB = (int)B;

@@ -17,7 +17,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("PF_LIB") or os.path.join(_HERE, "libpf.so")
 HEADER = os.path.join(os.path.dirname(_HERE), "include", "pf.h")
 
-PF_ABI_VERSION = 6
+PF_ABI_VERSION = 7
 PF_OK, PF_ERR_ARG, PF_ERR_UNSTABLE_DT, PF_ERR_NOMEM, PF_ERR_CUDA, PF_ERR_NCCL, PF_ERR_BLOWUP, \
     PF_ERR_STATE, PF_ERR_ABI = range(9)
 STATUS_NAMES = ["PF_OK", "PF_ERR_ARG", "PF_ERR_UNSTABLE_DT", "PF_ERR_NOMEM", "PF_ERR_CUDA",
@@ -45,6 +45,7 @@ class pf_params(C.Structure):
         ("noise_c_gaussian", C.c_int32), ("check_every", C.c_int32),
         ("seed", C.c_uint64), ("device", C.c_int32), ("graph_steps", C.c_int32),
         ("kernel_path", C.c_int32), ("overlap_halo", C.c_int32),
+        ("halo_transport", C.c_int32),
     ]
 
     def as_dict(self):

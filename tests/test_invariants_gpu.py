@@ -127,6 +127,44 @@ def test_loopback_slabs_equal_single_domain(nslabs, path, overlap, graph):
     np.testing.assert_allclose(d, d1, rtol=1e-12, atol=0)
 
 
+@pytest.mark.parametrize("nslabs,path,overlap,prec", [(2, 0, 1, 0), (4, 0, 1, 0), (8, 3, 1, 0), (4, 0, 0, 0),
+                                                       (16, 0, 1, 0), (4, 3, 1, 1), (3, 1, 1, 0)])
+def test_loopback_peer_transport_equals_single_domain(nslabs, path, overlap, prec):
+    """B11 (halo_transport = 1): the push kernel stores each slab's 2 boundary rows straight into
+    the neighbours' ghost rows and bumps their arrival counters, the receiving stream waits on the
+    counters (cuStreamWaitValue32) -- bitwise the single-domain run (fp64 and fp32, with and
+    without the overlap schedule, 4-row slabs), diagnostics too, and a pf_set_fields resume
+    (which re-exchanges the halo through the same path) continues bitwise."""
+    p = _base(128, 48 * nslabs if nslabs == 3 else 64, n_members=2, kernel_path=path, overlap_halo=overlap,
+              graph_steps=8, precision=prec)
+    a = _run(p, 25)
+    q = p.replace(halo_transport=1)
+    b = _run(q, 25, mode=("loopback", nslabs))
+    for m in range(2):
+        assert _eq(a[m], b[m]), m
+    with pf.Simulation(q, ("loopback", nslabs)) as s:
+        s.step(11)
+        u = s.fields(1)
+        d = s.diagnostics(1)
+    with pf.Simulation(p) as s:
+        s.step(11)
+        d1 = s.diagnostics(1)
+    np.testing.assert_allclose(d, d1, rtol=1e-12 if prec == 0 else 1e-6, atol=0)
+    with pf.Simulation(q.replace(ic=pf.PF_IC_NONE), ("loopback", nslabs)) as s:
+        s.set_fields(1, *u)
+        s.step(14)
+        assert _eq(s.fields(1), a[1])
+
+
+def test_loopback_peer_transport_large_grid_cfg4_physics():
+    """configs[3] physics on 1024 x 512 in 8 slabs of 64 rows, peer transport: bitwise the
+    single domain after 30 steps (interface on a slab boundary)."""
+    p = pf.pf_default_params(4).replace(nx=1024, ny=512, ic_height=128.0)
+    a = _run(p, 30)
+    b = _run(p.replace(halo_transport=1), 30, mode=("loopback", 8))
+    assert _eq(a[0], b[0])
+
+
 def test_loopback_overlap_large_grid_cfg4_physics():
     """A 1024 x 512 grid of configs[3] physics in 4 slabs of 128 rows (interface on a slab
     boundary): overlap schedule bitwise equal to the single domain after 30 steps."""

@@ -31,10 +31,13 @@ def _rank_main(rank, nranks, uid, pdict, steps, q):
 
 
 @pytest.mark.skipif(_n_gpus() < 2, reason="needs 2 GPUs (one NCCL rank each)")
-@pytest.mark.parametrize("overlap", [1, 0])
-def test_two_rank_nccl_slabs_equal_single_domain(overlap):
+@pytest.mark.parametrize("overlap,transport", [(1, 0), (0, 0), (1, 1), (0, 1)])
+def test_two_rank_nccl_slabs_equal_single_domain(overlap, transport):
+    """transport 0: NCCL send/recv per stage; 1: B11 peer stores into the neighbour's ghost rows
+    through CUDA-IPC mappings (handles exchanged over the NCCL communicator) + arrival counters."""
     from paper_2312_05410_b200 import pf
-    pdict = dict(nx=512, ny=256, ic_height=64.0, overlap_halo=overlap, graph_steps=0, check_every=10)
+    pdict = dict(nx=512, ny=256, ic_height=64.0, overlap_halo=overlap, graph_steps=0, check_every=10,
+                 halo_transport=transport)
     p = pf.pf_default_params(4)
     for k, v in pdict.items():
         setattr(p, k, v)
