@@ -38,6 +38,8 @@ def main():
         print(json.dumps({"config": cfg, "nx": p.nx, "steps": steps, "band_G": _try(p.replace(kernel_path=6), steps),
                           "persistent_G": _try(p.replace(kernel_path=7), steps),
                           "pair_graph_G": _try(p.replace(kernel_path=3, graph_steps=50), steps)}), flush=True)
+    if "--only-configs" in sys.argv:   # configs[0] / configs[1] only (A/B runs)
+        return
     for (n, m) in ((64, 1), (128, 1), (256, 1), (256, 4), (512, 1), (512, 4), (1024, 1)):
         p = pf.pf_default_params(2).replace(nx=n, ny=n, n_members=m, ic_height=n / 8, graph_steps=50, check_every=100)
         steps = 400 if n * n * m <= 1 << 18 else 200
