@@ -542,12 +542,15 @@ cudaEvent_t take_event(pf_ctx *c) {
     return e;
 }
 
-pf_status launch_rows(pf_ctx *c, Slab &s, int stage, int r0, int r1, bool capture) {
+// Rows [r0, r1) minus [g0, g1) (a gap only on the pair path, see Layout::g0).
+pf_status launch_rows(pf_ctx *c, Slab &s, int stage, int r0, int r1, bool capture, int g0 = 0, int g1 = 0) {
     if (r1 <= r0) return PF_OK;
     Nvtx nv(stage == 1 ? "pf stage 1 (u* = u + dt/2 R(u))" : "pf stage 2 (u = u + dt R(u*))");
     pf::Layout L = s.L;
     L.r0 = r0;
     L.r1 = r1;
+    L.g0 = g0;
+    L.g1 = g1;
     const void *in = stage == 1 ? s.U : s.Us;
     void *out = stage == 1 ? s.Us : s.U;
     const double coef = stage == 1 ? 0.5 * c->p.dt : c->p.dt;
@@ -604,6 +607,10 @@ pf_status one_step(pf_ctx *c, bool capture, int64_t step) {
             if ((st = finish_exchange(c, c->stream)) != PF_OK) return st;
         } else {
             for (auto &s : c->slabs) {
+                if (s.plan.ok) {   // pair kernel: both bands in one launch (rows [2, ny_loc-2) skipped)
+                    if ((st = launch_rows(c, s, stage, 0, s.L.ny_loc, capture, 2, s.L.ny_loc - 2)) != PF_OK) return st;
+                    continue;
+                }
                 if ((st = launch_rows(c, s, stage, 0, 2, capture)) != PF_OK) return st;
                 if ((st = launch_rows(c, s, stage, s.L.ny_loc - 2, s.L.ny_loc, capture)) != PF_OK) return st;
             }

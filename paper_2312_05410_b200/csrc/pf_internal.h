@@ -42,8 +42,12 @@ struct Layout {
     int64_t fstride;             // elements per field  = (ny_loc + 4) * pitch
     int64_t mstride;             // elements per member = 3 * fstride
     int r0, r1;                  // row window [r0, r1) a stage launch updates (default [0, ny_loc))
+    int g0, g1;                  // rows [g0, g1) inside the window that the launch skips (g0 == g1:
+                                 // none; pair kernel only: both 2-row boundary bands of the slab
+                                 // overlap schedule in ONE launch)
     int m0;                      // first member of a stage launch (members = its count; default 0)
     __host__ __device__ int64_t at(int r, int x) const { return (int64_t)(r + 2) * pitch + (x + gx); }
+    __host__ __device__ int rows() const { return r1 - r0 - (g1 - g0); }   // rows a launch updates
 };
 
 // Coefficients of the discrete model, folded on the host once per ctx.

@@ -1299,13 +1299,13 @@ cudaError_t launch_pair_k(const Layout &L, const StreamPlan &P, const KC<real> &
         if (e != cudaSuccess) return e;
         if (occ < 1) occ = 1;
     }
-    const int64_t R_ = (int64_t)L.members * P.strips * (L.r1 - L.r0);
+    const int64_t R_ = (int64_t)L.members * P.strips * L.rows();
     const int64_t minrows = 16;
     int64_t B = (int64_t)occ * nsm * V;   // (virtual) blocks
     static const int nogroup = env_int("PF_STREAM_NOGROUP", 0);
     // grouped schedule when at least 4 groups of `strips` blocks fit in one resident wave
     int64_t G = B / P.strips;
-    const int64_t T = (int64_t)L.members * (L.r1 - L.r0);
+    const int64_t T = (int64_t)L.members * L.rows();
     if (G > (T + minrows - 1) / minrows) G = (T + minrows - 1) / minrows;
     if (G >= 4 && !nogroup) {
         B = G * P.strips;
@@ -1315,7 +1315,8 @@ cudaError_t launch_pair_k(const Layout &L, const StreamPlan &P, const KC<real> &
         // boundary band of the slab overlap schedule (4096 wide: 18 strips) otherwise ran on 3
         // blocks, 6 strips each back to back (~28 us per band launch, gpurun_out r2s3b)
         int64_t cap = (R_ + minrows - 1) / minrows;
-        const int64_t windows = (int64_t)L.members * P.strips;
+        // (both bands in one launch, Layout::g0: a block per band and strip)
+        const int64_t windows = (int64_t)L.members * P.strips * (L.g1 > L.g0 ? 2 : 1);
         if (cap < windows) cap = windows;
         if (B > cap) B = cap;
     }

@@ -83,7 +83,7 @@ struct Sched {
 // b / nb: the (virtual) block index and count; blocks b >= nb get an empty range.
 __device__ __forceinline__ Sched make_sched(const Layout &L, int Wo, int G, int b, int nb) {
     const int strips = (L.nx + Wo - 1) / Wo;
-    const int nyl = L.r1 - L.r0;        // rows of this launch's row window
+    const int nyl = L.rows();           // rows of this launch's row window (minus its gap)
     Sched sc;
     if (b >= nb) {
         sc.strip = 0;
@@ -107,13 +107,16 @@ __device__ __forceinline__ Sched make_sched(const Layout &L, int Wo, int G) {
 }
 __device__ __forceinline__ bool next_seg(const Layout &L, int Wo, const Sched &sc, int64_t &pos, Seg &sg) {
     if (pos >= sc.hi) return false;
-    const int nyl = L.r1 - L.r0, strips = (L.nx + Wo - 1) / Wo;
+    const int nyl = L.rows(), strips = (L.nx + Wo - 1) / Wo;
     const int64_t col = pos / nyl;      // grouped: member; ungrouped: member * strips + strip
     const int la = (int)(pos - col * nyl);
-    const int lb = (int)min((int64_t)nyl, (int64_t)la + (sc.hi - pos));
+    int lb = (int)min((int64_t)nyl, (int64_t)la + (sc.hi - pos));
+    const int gv = L.g0 - L.r0;         // window rows before the gap: a segment never spans it
+    if (la < gv && lb > gv) lb = gv;
     pos += lb - la;
-    sg.ya = L.r0 + la;
-    sg.yb = L.r0 + lb;
+    const int sh = la < gv ? 0 : L.g1 - L.g0;
+    sg.ya = L.r0 + la + sh;
+    sg.yb = L.r0 + lb + sh;
     int sidx;
     if (sc.strip >= 0) {
         sg.m = (int)col;
