@@ -119,7 +119,15 @@ typedef struct {
                                             loopback) and increments an arrival counter in the
                                             receiver's memory, which the receiver's stream awaits
                                             with cuStreamWaitValue32.  Results are bitwise those of
-                                            transport 0.  Disables CUDA graphs for the ctx.       */
+                                            transport 0.  Disables CUDA graphs for the ctx.
+                                        2 = NCCL send / receive to SELF (pf_create with n_slabs > 1
+                                            only; pf_create_slab rejects it): the slabs of a one-GPU
+                                            context exchange through a 1-rank communicator, each
+                                            transfer a ncclSend matched by a ncclRecv in one group,
+                                            issued by the code transport 0 runs across ranks, and
+                                            the diagnostics through ncclAllGather -- the one-GPU
+                                            stand-in that executes the NCCL path.  Bitwise those of
+                                            transport 0; no CUDA graphs.                           */
 } pf_params;
 
 /* Fill *out with the preset of BASELINE.json configs[cfg-1] (cfg = 1..5; R-13, R-14).

@@ -283,6 +283,7 @@ struct pf_ctx {
     // halo_transport = 1 (B11): arrival counters (2 per slab), exchanges issued so far, blocks per
     // push (= counter increments per exchange and direction), IPC mappings to close
     bool peer = false;
+    bool nccl_self = false;   // halo_transport = 2: loopback slabs exchanging through ncclSend / ncclRecv to self
     unsigned *xflags = nullptr;
     uint32_t xepoch = 0;
     int xblocks = 0;
@@ -359,7 +360,7 @@ pf_status validate(const pf_params *p, std::string &why) {
     if (!(p->noise_rho >= 0) || !std::isfinite(p->noise_rho)) { why = "noise_rho must be finite and >= 0"; return PF_ERR_ARG; }
     if (!(p->mob_lo > 0) || !(p->mob_hi >= p->mob_lo)) { why = "need 0 < mob_lo <= mob_hi"; return PF_ERR_ARG; }
     if (p->overlap_halo != 0 && p->overlap_halo != 1) { why = "overlap_halo must be 0 or 1"; return PF_ERR_ARG; }
-    if (p->halo_transport != 0 && p->halo_transport != 1) { why = "halo_transport must be 0 or 1"; return PF_ERR_ARG; }
+    if (p->halo_transport < 0 || p->halo_transport > 2) { why = "halo_transport must be 0, 1 or 2"; return PF_ERR_ARG; }
     if (p->kernel_path < 0 || p->kernel_path > 7) { why = "kernel_path must be 0 .. 7"; return PF_ERR_ARG; }
     if (p->kernel_path == 2 || p->kernel_path == 4) { why = "kernel_path 2 and 4 (retired) are not available"; return PF_ERR_ARG; }
     if ((p->kernel_path == 3 || p->kernel_path == 5) && !(p->nx % 4 == 0 && p->nx >= 16)) { why = "streaming kernels need nx % 4 == 0 and nx >= 16"; return PF_ERR_ARG; }
@@ -433,6 +434,23 @@ bool halo_plan(int ny, int nranks, int rank, int out[8]) {
     return true;
 }
 
+// One neighbour relation over NCCL (inside the caller's group): rows [srow, srow + 2) of every
+// field of every member of `from` go to `peer`, rows [rrow, rrow + 2) of `to` come from it -- full
+// padded rows (ghost columns too), one send / receive pair per (member, field) in that order.
+pf_status nccl_rows(pf_ctx *c, Slab &from, int srow, Slab &to, int rrow, int peer, int which, cudaStream_t st) {
+    const ncclDataType_t dt = c->p.precision == PF_F64 ? ncclFloat64 : ncclFloat32;
+    const size_t rowb = (size_t)from.L.pitch * c->esz, cnt = 2 * (size_t)from.L.pitch;
+    const char *sb = (const char *)buf_of(from, which);
+    char *rb = (char *)buf_of(to, which);
+    for (int m = 0; m < from.L.members; ++m)
+        for (int f = 0; f < 3; ++f) {
+            const size_t off = ((size_t)m * from.L.mstride + (size_t)f * from.L.fstride) * c->esz;
+            NK(c, ncclSend(sb + off + (size_t)(srow + 2) * rowb, cnt, dt, peer, c->comm, st));
+            NK(c, ncclRecv(rb + off + (size_t)(rrow + 2) * rowb, cnt, dt, peer, c->comm, st));
+        }
+    return PF_OK;
+}
+
 pf_status exchange(pf_ctx *c, int which, cudaStream_t st) {
     Nvtx nv("pf halo exchange");
     if (c->mode == kSingle) return PF_OK;
@@ -453,6 +471,23 @@ pf_status exchange(pf_ctx *c, int which, cudaStream_t st) {
             if (h.dst[0] || h.dst[1]) c->launches += 1;
         }
         ++c->xepoch;
+        return PF_OK;
+    }
+    pf_status stx = PF_OK;
+    if (c->mode == kLoopback && c->nccl_self) {
+        // halo_transport = 2: the slabs of this one-GPU context exchange through a 1-rank NCCL
+        // communicator, every transfer a ncclSend to self followed by its ncclRecv from self (NCCL
+        // matches the k-th send to a peer with the k-th receive from it), in one group -- the issue
+        // code (nccl_rows: counts, types, row addressing, stream) is the one the multi-rank
+        // transport runs, so it is exercised on a one-GPU box.
+        const int P = (int)c->slabs.size();
+        NK(c, ncclGroupStart());
+        for (int s = 0; s + 1 < P; ++s) {
+            Slab &lo = c->slabs[s], &hi = c->slabs[s + 1];
+            if ((stx = nccl_rows(c, lo, lo.L.ny_loc - 2, hi, -2, 0, which, st)) != PF_OK) return stx;
+            if ((stx = nccl_rows(c, hi, 0, lo, lo.L.ny_loc, 0, which, st)) != PF_OK) return stx;
+        }
+        NK(c, ncclGroupEnd());
         return PF_OK;
     }
     if (c->mode == kLoopback) {
@@ -482,22 +517,9 @@ pf_status exchange(pf_ctx *c, int which, cudaStream_t st) {
     Slab &me = c->slabs[0];
     int plan[8];
     halo_plan(c->p.ny, c->nranks, c->rank, plan);
-    const ncclDataType_t dt = c->p.precision == PF_F64 ? ncclFloat64 : ncclFloat32;
-    const size_t cnt = 2 * (size_t)me.L.pitch;
-    char *base = (char *)buf_of(me, which);
     NK(c, ncclGroupStart());
-    for (int m = 0; m < me.L.members; ++m)
-        for (int f = 0; f < 3; ++f) {
-            char *fb = base + ((size_t)m * me.L.mstride + (size_t)f * me.L.fstride) * c->esz;
-            if (plan[2] >= 0) {
-                NK(c, ncclSend(fb + (size_t)(plan[4] + 2) * rowb, cnt, dt, plan[2], c->comm, st));
-                NK(c, ncclRecv(fb + (size_t)(plan[6] + 2) * rowb, cnt, dt, plan[2], c->comm, st));
-            }
-            if (plan[3] >= 0) {
-                NK(c, ncclSend(fb + (size_t)(plan[5] + 2) * rowb, cnt, dt, plan[3], c->comm, st));
-                NK(c, ncclRecv(fb + (size_t)(plan[7] + 2) * rowb, cnt, dt, plan[3], c->comm, st));
-            }
-        }
+    if (plan[2] >= 0 && (stx = nccl_rows(c, me, plan[4], me, plan[6], plan[2], which, st)) != PF_OK) return stx;
+    if (plan[3] >= 0 && (stx = nccl_rows(c, me, plan[5], me, plan[7], plan[3], which, st)) != PF_OK) return stx;
     NK(c, ncclGroupEnd());
     return PF_OK;
 }
@@ -630,7 +652,7 @@ pf_status one_step(pf_ctx *c, bool capture, int64_t step) {
 }
 
 pf_status ensure_graph(pf_ctx *c) {
-    if (c->gexec || c->p.graph_steps <= 0 || c->mode == kNccl || c->peer) return PF_OK;
+    if (c->gexec || c->p.graph_steps <= 0 || c->mode == kNccl || c->peer || c->nccl_self) return PF_OK;
     cudaGraph_t g = nullptr;
     CK(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
     pf_status st = PF_OK;
@@ -685,6 +707,19 @@ pf_status gather_diag(pf_ctx *c, std::vector<double> &out) {
         CK(c, cudaStreamSynchronize(c->stream));
         for (int r = 0; r < c->nranks; ++r)
             for (size_t k = 0; k < n; ++k) out[k] += h[r * n + k];
+        return PF_OK;
+    }
+    if (c->nccl_self) {   // every slab's record through the 1-rank communicator's all-gather
+        const size_t P = c->slabs.size();
+        double *dall = nullptr;
+        CK(c, cudaMallocAsync((void **)&dall, n * P * sizeof(double), c->stream));
+        for (size_t s = 0; s < P; ++s)
+            NK(c, ncclAllGather(c->slabs[s].diag, dall + s * n, n, ncclFloat64, c->comm, c->stream));
+        CK(c, cudaMemcpyAsync(c->h_diag, dall, n * P * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        CK(c, cudaFreeAsync(dall, c->stream));
+        CK(c, cudaStreamSynchronize(c->stream));
+        for (size_t s = 0; s < P; ++s)
+            for (size_t k = 0; k < n; ++k) out[k] += c->h_diag[s * n + k];
         return PF_OK;
     }
     for (size_t s = 0; s < c->slabs.size(); ++s)
@@ -965,6 +1000,20 @@ pf_status create_common(const pf_params *p, int mode, int rank, int nranks, cons
             return fail(PF_ERR_CUDA);
         }
     }
+    if (mode == kNccl && p->halo_transport == 2) {
+        c->err = "halo_transport 2 (NCCL send to self) is the one-GPU loopback stand-in: pf_create with n_slabs > 1";
+        return fail(PF_ERR_ARG);
+    }
+    c->nccl_self = mode == kLoopback && p->halo_transport == 2;
+    if (c->nccl_self) {   // a communicator of this one rank
+        ncclUniqueId id;
+        ncclResult_t r = ncclGetUniqueId(&id);
+        if (r == ncclSuccess) r = ncclCommInitRank(&c->comm, 1, id, 0);
+        if (r != ncclSuccess) {
+            c->err = fmt("ncclCommInitRank (1 rank): %s", ncclGetErrorString(r));
+            return fail(PF_ERR_NCCL);
+        }
+    }
     if (mode == kNccl) {
         ncclUniqueId id;
         std::memcpy(&id, uid, sizeof id);
@@ -1214,7 +1263,7 @@ pf_status pf_step(pf_ctx *c, int64_t n) {
         int64_t done = 0;
         const bool use_graph = c->p.graph_steps > 0 && !c->prof && c->mode != kNccl && !(c->p.noise_rho > 0.0) &&
                                !c->fused && !c->persistent && !c->band &&
-                               !c->peer;   // fused swaps buffers on the host each step; peer waits on epochs
+                               !c->peer && !c->nccl_self;   // fused swaps buffers on the host each step; peer waits on epochs
         if (c->band && !c->prof && chunk > 0) {
             Nvtx nv("pf band kernel (small grid)");
             Slab &S = c->slabs[0];

@@ -156,6 +156,43 @@ def test_loopback_peer_transport_equals_single_domain(nslabs, path, overlap, pre
         assert _eq(s.fields(1), a[1])
 
 
+@pytest.mark.parametrize("nslabs,path,overlap,prec", [(2, 0, 1, 0), (4, 0, 1, 0), (8, 3, 0, 0), (4, 1, 1, 1),
+                                                       (16, 0, 1, 0)])
+def test_loopback_nccl_self_transport_equals_single_domain(nslabs, path, overlap, prec):
+    """halo_transport = 2: the slabs of a one-GPU context exchange their boundary rows through a
+    1-rank NCCL communicator (ncclSend to self matched with ncclRecv from self, one group per
+    exchange), i.e. through the issue code of the multi-rank NCCL transport (nccl_rows), and the
+    diagnostics go through ncclAllGather -- bitwise the single-domain run (fp64 and fp32, with and
+    without the overlap schedule, 4-row slabs), and a pf_set_fields resume continues bitwise."""
+    p = _base(128, 64, n_members=2, kernel_path=path, overlap_halo=overlap, precision=prec)
+    a = _run(p, 25)
+    q = p.replace(halo_transport=2)
+    b = _run(q, 25, mode=("loopback", nslabs))
+    for m in range(2):
+        assert _eq(a[m], b[m]), m
+    with pf.Simulation(q, ("loopback", nslabs)) as s:
+        s.step(11)
+        u = s.fields(1)
+        d = s.diagnostics(1)
+    with pf.Simulation(p) as s:
+        s.step(11)
+        d1 = s.diagnostics(1)
+    np.testing.assert_allclose(d, d1, rtol=1e-12 if prec == 0 else 1e-6, atol=0)
+    with pf.Simulation(q.replace(ic=pf.PF_IC_NONE), ("loopback", nslabs)) as s:
+        s.set_fields(1, *u)
+        s.step(14)
+        assert _eq(s.fields(1), a[1])
+
+
+def test_nccl_self_transport_is_loopback_only():
+    """pf_create_slab (one slab per rank) rejects transport 2; a single domain ignores it."""
+    p = _base(64, 64, halo_transport=2)
+    with pf.Simulation(p) as s:
+        s.step(2)
+    with pytest.raises(Exception, match="halo_transport 2"):
+        pf.Simulation(p, ("slab", 0, 2, pf.pf_nccl_unique_id()))
+
+
 def test_loopback_peer_transport_large_grid_cfg4_physics():
     """configs[3] physics on 1024 x 512 in 8 slabs of 64 rows, peer transport: bitwise the
     single domain after 30 steps (interface on a slab boundary)."""

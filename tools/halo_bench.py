@@ -29,7 +29,7 @@ def main():
     base = pf.pf_default_params(args.config).replace(graph_steps=0, check_every=1000000)
     cells = base.nx * base.ny * base.n_members
     for P in [int(x) for x in args.slabs.split(",")]:
-        for transport in ((0,) if P == 1 else (0, 1)):
+        for transport in ((0,) if P == 1 else (0, 1, 2)):
             for overlap in ((1,) if P == 1 else (1, 0)):
                 p = base.replace(halo_transport=transport, overlap_halo=overlap)
                 mode = "single" if P == 1 else ("loopback", P)
