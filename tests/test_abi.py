@@ -120,7 +120,7 @@ def test_create_validation_errors(L):
         pf.pf_create_loopback(p.replace(ny=64), 5)
     assert e.value.status == pf.PF_ERR_ARG
     with pytest.raises(pf.PfError) as e:   # halo transport: 0 (NCCL / copies) or 1 (peer stores)
-        pf.pf_create_loopback(p.replace(ny=64, halo_transport=2), 4)
+        pf.pf_create_loopback(p.replace(ny=64, halo_transport=3), 4)
     assert e.value.status == pf.PF_ERR_ARG and "halo_transport" in str(e.value)
     with pytest.raises(pf.PfError):
         pf.pf_default_params(9)
