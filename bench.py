@@ -281,7 +281,37 @@ def _slab_leg(args, ws, rank, local, dist, dev):
             dist.barrier()
     if rank != 0:
         return None
+    loop = None
+    if ws == 1:
+        # One GPU has no neighbour: time the slab SCHEDULE instead -- the same 4096^2 domain as 2
+        # loopback y-slabs on this GPU whose 2-row halos go through NCCL (sends to self on a 1-rank
+        # communicator, halo_transport 2: the multi-rank transport's issue code) overlapped with
+        # the interior update.  Same cells per step as the single domain above.
+        q = pf.pf_default_params(4).replace(device=local, halo_transport=2, overlap_halo=1, graph_steps=0)
+        with pf.Simulation(q, ("loopback", 2)) as s2:
+            st2 = torch.cuda.ExternalStream(pf.pf_stream(s2.ctx), device=dev)
+            s2.step(args.warmup)
+            l0 = pf.pf_launch_count(s2.ctx)
+            runs2 = [_timed_steps(s2, st2, args.steps, None, dev) for _ in range(3)]
+            ms2 = sorted(runs2)[1]
+            l1 = l0 + (pf.pf_launch_count(s2.ctx) - l0) // 3
+        loop = {"workload": "the same 4096 x 4096 domain as 2 loopback y-slabs of 2048 rows on this GPU, 2-row halo "
+                            "per stage over NCCL (ncclSend/ncclRecv to self, 1-rank communicator) overlapped with "
+                            "the interior update",
+                "value": q.nx * q.ny * args.steps / (ms2 * 1e-3), "unit": UNIT, "ms_per_step": ms2 / args.steps,
+                "schedule_efficiency": ms / ms2, "launches": l1 - l0,
+                "runs_ms_per_step": [r / args.steps for r in runs2],
+                "timing": "median of 3 timed calls of K steps (a call now and then takes 2-8x longer on the "
+                          "host side of NCCL's group launches; profiles/r2/nccl_self_bench_r2t3.jsonl)",
+                "halo_bytes_per_stage_per_neighbour": 2 * 3 * (q.nx + 8) * 8}
     value = cells_local * ws * args.steps / (ms * 1e-3)
+    out = _slab_line(args, p, ws, cells_local, value, ms, ms1)
+    if loop is not None:
+        out["loopback_nccl"] = loop
+    return out
+
+
+def _slab_line(args, p, ws, cells_local, value, ms, ms1):
     return {"workload": f"configs[3] weak: {p.nx} x {p.ny} fp64 in {ws} y-slab(s) of {cells_local // p.nx} rows, "
                         + (("2-row halo per stage over NCCL (ncclSend/Recv on a comm stream)"
                             if args.slab_transport == "nccl" else
@@ -293,6 +323,9 @@ def _slab_leg(args, ws, rank, local, dist, dev):
             "halo_bytes_per_stage_per_neighbour": 2 * 3 * (p.nx + 8) * 8 if ws > 1 else 0}
 
 
+_JSON_OUT = sys.stdout
+
+
 def run_ours(args):
     import numpy as np
     import torch
@@ -300,6 +333,13 @@ def run_ours(args):
 
     from paper_2312_05410_b200 import dist as D
     ws, rank, local = D.world()
+    # NCCL (and any other library) may print to stdout -- at NCCL_DEBUG=VERSION its version line goes
+    # there whatever NCCL_DEBUG_FILE says, and the N = 1 run creates a communicator too (loopback slab
+    # leg): keep the process's fd 1 for the one JSON line and point everything else at stderr.
+    global _JSON_OUT
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     if ws > 1:   # NCCL init lines (rank counts of every communicator) go to stderr for the driver
         os.environ.setdefault("NCCL_DEBUG", "INFO")
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
@@ -452,7 +492,7 @@ def run_ours(args):
             line["slab"] = slab
         if not args.no_cpu_baseline and ws == 1:
             line["cpu_baseline"] = _cpu_baseline()
-        print(json.dumps(line), flush=True)
+        print(json.dumps(line), file=_JSON_OUT, flush=True)
     sim.close()
     if dist is not None:
         dist.barrier()

@@ -651,8 +651,16 @@ pf_status one_step(pf_ctx *c, bool capture, int64_t step) {
     return PF_OK;
 }
 
+// PF_NCCL_SELF_GRAPH=1: the send-to-self exchanges of transport 2 captured into the step graphs
+// (experiment knob; off, a transport-2 ctx launches directly like the multi-rank NCCL mode).
+bool nccl_self_graph() {
+    static const bool on = [] { const char *v = getenv("PF_NCCL_SELF_GRAPH"); return v && atoi(v) != 0; }();
+    return on;
+}
+
 pf_status ensure_graph(pf_ctx *c) {
-    if (c->gexec || c->p.graph_steps <= 0 || c->mode == kNccl || c->peer || c->nccl_self) return PF_OK;
+    const bool self_graph = nccl_self_graph();
+    if (c->gexec || c->p.graph_steps <= 0 || c->mode == kNccl || c->peer || (c->nccl_self && !self_graph)) return PF_OK;
     cudaGraph_t g = nullptr;
     CK(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
     pf_status st = PF_OK;
@@ -1263,7 +1271,7 @@ pf_status pf_step(pf_ctx *c, int64_t n) {
         int64_t done = 0;
         const bool use_graph = c->p.graph_steps > 0 && !c->prof && c->mode != kNccl && !(c->p.noise_rho > 0.0) &&
                                !c->fused && !c->persistent && !c->band &&
-                               !c->peer && !c->nccl_self;   // fused swaps buffers on the host each step; peer waits on epochs
+                               !c->peer && (!c->nccl_self || nccl_self_graph());   // fused swaps buffers on the host each step; peer waits on epochs
         if (c->band && !c->prof && chunk > 0) {
             Nvtx nv("pf band kernel (small grid)");
             Slab &S = c->slabs[0];

@@ -154,31 +154,45 @@ def test_cfg5_recipe_1024_full_grid_fp32(ora):
     assert e <= 1e-4, e
 
 
-@pytest.mark.parametrize("nslabs", [4, 8])
-def test_cfg4_loopback_slabs_vs_oracle(ora, nslabs):
-    """configs[3] (4096^2 fp64) in P = 4 / 8 y-slabs (loopback transport: the per-stage 2-row halo
-    exchange and the overlap schedule of the multi-GPU path, in one process) against the oracle
-    directly: the full grid after 1 step (<= 1e-12, diagnostics within 1e-12) and light-cone
-    windows after 100 steps (<= 1e-8) straddling the slab boundaries y = 512 and y = 1024 (P = 8)
-    / y = 1024 (P = 4) with the film interface at y = 512."""
+_CFG4_REF = {}
+
+
+def _cfg4_refs(ora, p, wins):
+    """The oracle's side of test_cfg4_loopback_slabs_vs_oracle, computed once for its cases."""
+    if not _CFG4_REF:
+        nx, ny = p.nx, p.ny
+        m, ic = oracle_member(ora, p, 0)
+        _CFG4_REF["m"] = m
+        _CFG4_REF["wins"] = [_POOL.submit(_window, ora, m, ic, 0, nx, ny, i0, j0, W, H, 100)
+                             for i0, j0, W, H in wins]
+        _CFG4_REF["one"] = _POOL.submit(lambda: ora.step(m, *ora.initial_fields(ic, nx, ny, 0), 1))
+    return _CFG4_REF
+
+
+@pytest.mark.parametrize("nslabs,transport", [(4, 0), (8, 0), (8, 2), (4, 1)])
+def test_cfg4_loopback_slabs_vs_oracle(ora, nslabs, transport):
+    """configs[3] (4096^2 fp64) in P = 4 / 8 y-slabs (the per-stage 2-row halo exchange and the
+    overlap schedule of the multi-GPU path, in one process; transport 0 device copies, 1 peer
+    stores, 2 NCCL sends to self) against the oracle directly: the full grid after 1 step
+    (<= 1e-12, diagnostics within 1e-12) and light-cone windows after 100 steps (<= 1e-8)
+    straddling the slab boundaries y = 512 and y = 1024 (P = 8) / y = 1024 (P = 4) with the film
+    interface at y = 512."""
     p = pf.pf_default_params(4)
-    nx, ny = p.nx, p.ny
-    m, ic = oracle_member(ora, p, 0)
     wins = [(500, 0, 1024, 1536), (2500, 600, 1024, 1024)]
-    futs = [_POOL.submit(_window, ora, m, ic, 0, nx, ny, i0, j0, W, H, 100) for i0, j0, W, H in wins]
-    f1 = _POOL.submit(lambda: ora.step(m, *ora.initial_fields(ic, nx, ny, 0), 1))
-    with pf.Simulation(p, ("loopback", nslabs)) as s:
+    R = _cfg4_refs(ora, p, wins)
+    m = R["m"]
+    with pf.Simulation(p.replace(halo_transport=transport), ("loopback", nslabs)) as s:
         s.step(1)
         g1 = s.fields(0)
         d1 = s.diagnostics(0)
         s.step(99)
         g100 = s.fields(0)
-    ref1 = f1.result()
+    ref1 = R["one"].result()
     assert normwise(g1, ref1) <= 1e-12
     dref = ora.diagnostics(m, *ref1)
     for q in range(4):
         assert abs(d1[q] - dref[q]) <= 1e-12 * abs(dref[q]), (q, d1[q], dref[q])
-    for (i0, j0, W, H), f in zip(wins, futs):
+    for (i0, j0, W, H), f in zip(wins, R["wins"]):
         ref, valid, cols = f.result()
         e = _window_err(g100, j0, H, cols, ref, valid)
         assert e <= 1e-8, ((i0, j0), e)
