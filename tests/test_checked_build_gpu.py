@@ -19,7 +19,7 @@ def checked_lib():
     return build.build_checked()
 
 
-@pytest.mark.parametrize("case", ["band", "persistent", "pair", "loopback", "ws", "tile"])
+@pytest.mark.parametrize("case", ["band", "persistent", "pair", "loopback", "peer", "nccl_self", "ws", "tile"])
 def test_checked_build_case(checked_lib, case):
     env = dict(os.environ, PF_LIB=checked_lib)
     r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "sanitize_case.py"), case], env=env,

@@ -6,7 +6,7 @@ here through pf_debug_guards) or for compute-sanitizer where a pool allows it:
 
 cases: band (configs[0] 64^2, the band cluster kernel), persistent (64^2, cooperative tile kernel),
 pair (512 x 72, 2 members: the TMA-ring stage kernels), loopback (512 x 72 in 2 y-slabs with the
-overlap schedule), ws (warp-specialised step kernel), tile (fallback kernel), diag (diagnostics)."""
+overlap schedule; peer / nccl_self: the same with halo transport 1 / 2), ws (warp-specialised step kernel), tile (fallback kernel), diag (diagnostics)."""
 import os
 import sys
 
@@ -26,6 +26,10 @@ def main(case):
         p, mode, n = small.replace(kernel_path=3), "single", 3
     elif case == "loopback":
         p, mode, n = small.replace(kernel_path=3, overlap_halo=1, ny=64), ("loopback", 2), 3
+    elif case == "peer":       # loopback slabs, B11 peer-store transport
+        p, mode, n = small.replace(kernel_path=3, overlap_halo=1, ny=64, halo_transport=1), ("loopback", 2), 3
+    elif case == "nccl_self":  # loopback slabs exchanging through NCCL sends to self (transport 2)
+        p, mode, n = small.replace(kernel_path=3, overlap_halo=1, ny=64, halo_transport=2), ("loopback", 2), 3
     elif case == "ws":
         p, mode, n = small.replace(kernel_path=5), "single", 3
     elif case == "tile":
