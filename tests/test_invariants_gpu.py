@@ -184,6 +184,30 @@ def test_loopback_nccl_self_transport_equals_single_domain(nslabs, path, overlap
         assert _eq(s.fields(1), a[1])
 
 
+def test_nccl_self_transport_inside_cuda_graphs_bitwise():
+    """PF_NCCL_SELF_GRAPH=1 (read once per process, hence the subprocess): the NCCL groups of
+    transport 2 captured into the step graphs give the bits of the direct launches."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import numpy as np\n"
+        "from paper_2312_05410_b200 import pf\n"
+        "p = pf.pf_default_params(2).replace(nx=128, ny=64, ic_height=16.0, n_members=2, seed=21, halo_transport=2,\n"
+        "                                    overlap_halo=1)\n"
+        "out = []\n"
+        "for g in (0, 8):\n"
+        "    with pf.Simulation(p.replace(graph_steps=g), ('loopback', 4)) as s:\n"
+        "        s.step(25)\n"
+        "        out.append([s.fields(m) for m in range(2)])\n"
+        "assert all(np.array_equal(x, y) for a, b in zip(*out) for x, y in zip(a, b))\n"
+        "print('graph == direct')\n")
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, PF_NCCL_SELF_GRAPH="1"), cwd=root,
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "graph == direct" in r.stdout, (r.stdout[-1000:], r.stderr[-3000:])
+
+
 def test_nccl_self_transport_is_loopback_only():
     """pf_create_slab (one slab per rank) rejects transport 2; a single domain ignores it."""
     p = _base(64, 64, halo_transport=2)
