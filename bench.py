@@ -292,16 +292,16 @@ def _slab_leg(args, ws, rank, local, dist, dev):
             st2 = torch.cuda.ExternalStream(pf.pf_stream(s2.ctx), device=dev)
             s2.step(args.warmup)
             l0 = pf.pf_launch_count(s2.ctx)
-            runs2 = [_timed_steps(s2, st2, args.steps, None, dev) for _ in range(3)]
-            ms2 = sorted(runs2)[1]
-            l1 = l0 + (pf.pf_launch_count(s2.ctx) - l0) // 3
+            runs2 = [_timed_steps(s2, st2, args.steps, None, dev) for _ in range(5)]
+            ms2 = sorted(runs2)[2]
+            l1 = l0 + (pf.pf_launch_count(s2.ctx) - l0) // 5
         loop = {"workload": "the same 4096 x 4096 domain as 2 loopback y-slabs of 2048 rows on this GPU, 2-row halo "
                             "per stage over NCCL (ncclSend/ncclRecv to self, 1-rank communicator) overlapped with "
                             "the interior update",
                 "value": q.nx * q.ny * args.steps / (ms2 * 1e-3), "unit": UNIT, "ms_per_step": ms2 / args.steps,
                 "schedule_efficiency": ms / ms2, "launches": l1 - l0,
                 "runs_ms_per_step": [r / args.steps for r in runs2],
-                "timing": "median of 3 timed calls of K steps (a call now and then takes 2-8x longer on the "
+                "timing": "median of 5 timed calls of K steps (a call now and then takes 2-8x longer on the "
                           "host side of NCCL's group launches; profiles/r2/nccl_self_bench_r2t3.jsonl)",
                 "halo_bytes_per_stage_per_neighbour": 2 * 3 * (q.nx + 8) * 8}
     value = cells_local * ws * args.steps / (ms * 1e-3)
